@@ -1,0 +1,255 @@
+"""DGSEM spatial operators R^(1)_h and R^(2)_h on periodic Cartesian meshes.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+Layout L: a field is a flat fp64 vector indexed
+[elem][var][j][i] (i fastest), elem = ey*nx + ex.  Internally it is viewed
+as (ny, nx, nv, p, p) in 2D and (nx, nv, p) in 1D.
+
+R^(1)_h follows eq:DGSEM_wt on affine Cartesian elements, where
+J_geo = dx dy/4 and s-hat = dy/2 (xi_1 faces), dx/2 (xi_2 faces), so
+    R1_ij = -[ (2/dx) ( sum_l Dhat_il Fx_lj + f*_E,j lhat_i(1) - f*_W,j lhat_i(-1) )
+             + (2/dy) ( sum_m Dhat_jm Fy_im + f*_N,i lhat_j(1) - f*_S,i lhat_j(-1) ) ].
+f*_E/W/N/S are the canonical (normal +e_d) face fluxes; the outward normal
+of the element's W and S faces is -e_d, hence the minus signs.  Traces are
+the solution polynomial evaluated at xi = +-1: w(+-1) = sum_i l_i(+-1) w_i.
+
+R^(2)_h(W, sigma) is *defined* by differentiating the discrete equations in
+time with w_t = sigma (P:211-213 and eq:DGSEM_wtt; NS: P:869-905), i.e. the
+directional derivative of R^(1)_h at W in direction sigma.  It is computed
+with forward-mode AD (oracle.ad), which reproduces the volume term
+(dF/dw) sigma and the linearised face flux f~* of P:226-228 (including the
+derivative of the LLF wave speed, reading R3).
+
+Navier-Stokes (C5): BR1 lifting (reading R19; the paper uses BR2,
+P:834): d = lifted gradient of w_grad = (u, v, T) from the weak form
+eq:Lifting with the central surface value 1/2(g_L + g_R);
+face gradients d^L, d^R are the traces of the lifted polynomial.  The
+viscous surface flux is 1/2(F^v_L + F^v_R).n.
+"""
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import ad, physics
+from .basis import Basis
+
+
+@dataclass(frozen=True)
+class Mesh:
+    dim: int
+    nx: int
+    ny: int = 1
+    xmin: float = 0.0
+    xmax: float = 1.0
+    ymin: float = 0.0
+    ymax: float = 1.0
+
+    @property
+    def dx(self):
+        return (self.xmax - self.xmin) / self.nx
+
+    @property
+    def dy(self):
+        return (self.ymax - self.ymin) / self.ny
+
+    @property
+    def n_elem(self):
+        return self.nx * (self.ny if self.dim == 2 else 1)
+
+
+@dataclass
+class Disc:
+    basis: Basis
+    mesh: Mesh
+    eq: physics.Equation
+
+    @property
+    def p(self):
+        return self.basis.p
+
+    @property
+    def nv(self):
+        return self.eq.nv
+
+    @property
+    def m(self):
+        return self.nv * self.p ** self.mesh.dim
+
+    @property
+    def n(self):
+        return self.mesh.n_elem * self.m
+
+    def field_shape(self):
+        p, nv, me = self.p, self.nv, self.mesh
+        return (me.ny, me.nx, nv, p, p) if me.dim == 2 else (me.nx, nv, p)
+
+    def to_field(self, x):
+        return ad.apply_linear(lambda c: np.reshape(c, self.field_shape()), x)
+
+    def to_flat(self, F):
+        return ad.apply_linear(lambda c: np.reshape(c, -1), F)
+
+    def node_coords(self):
+        """Physical node coordinates, each of field shape without the var
+        axis broadcast: x(ex, i) = xmin + ex dx + (xi_i + 1) dx/2."""
+        me, xi = self.mesh, self.basis.xi
+        xs = me.xmin + np.arange(me.nx)[:, None] * me.dx + (xi[None, :] + 1.0) * me.dx / 2
+        if me.dim == 1:
+            return (xs,)                                  # (nx, p)
+        ys = me.ymin + np.arange(me.ny)[:, None] * me.dy + (xi[None, :] + 1.0) * me.dy / 2
+        X = np.broadcast_to(xs[None, :, None, :], (me.ny, me.nx, self.p, self.p))
+        Y = np.broadcast_to(ys[:, None, :, None], (me.ny, me.nx, self.p, self.p))
+        return (X, Y)                                     # (ny, nx, p(j), p(i))
+
+
+# ---------------------------------------------------------------------------
+# field helpers (2D axes: 0 ey, 1 ex, 2 var, 3 j, 4 i;  1D: 0 ex, 1 var, 2 i)
+
+def _split(F, var_axis):
+    n = F.shape[var_axis]
+    idx = [slice(None)] * (var_axis + 1)
+    out = []
+    for v in range(n):
+        idx[var_axis] = v
+        out.append(F[tuple(idx)])
+    return tuple(out)
+
+
+def _lin(f, x):
+    return ad.apply_linear(f, x)
+
+
+def _roll(x, shift, axis):
+    return _lin(lambda c: np.roll(c, shift, axis=axis), x)
+
+
+class _Ops:
+    """Tensor-product derivative/trace operators of one discretization."""
+
+    def __init__(self, disc: Disc):
+        b = disc.basis
+        self.disc = disc
+        self.Dh, self.lp, self.lm = b.Dhat, b.l_plus, b.l_minus
+        self.lhp, self.lhm = b.lhat_plus, b.lhat_minus
+        self.dim = disc.mesh.dim
+
+    # traces: polynomial evaluated at the element end
+    def trace(self, F, d, side):
+        l = self.lp if side > 0 else self.lm
+        if self.dim == 1:
+            return _lin(lambda c: np.einsum("...i,i->...", c, l), F)
+        if d == 0:
+            return _lin(lambda c: np.einsum("...ji,i->...j", c, l), F)
+        return _lin(lambda c: np.einsum("...ji,j->...i", c, l), F)
+
+    def volume(self, F, d):
+        """sum_l Dhat_il F_lj (d = 0) or sum_m Dhat_jm F_im (d = 1)."""
+        Dh = self.Dh
+        if self.dim == 1:
+            return _lin(lambda c: np.einsum("il,...l->...i", Dh, c), F)
+        if d == 0:
+            return _lin(lambda c: np.einsum("il,...jl->...ji", Dh, c), F)
+        return _lin(lambda c: np.einsum("jm,...mi->...ji", Dh, c), F)
+
+    def surface(self, fplus, fminus, d):
+        """f+ lhat(1) - f- lhat(-1) spread onto the element nodes; f+/f- are
+        canonical (normal +e_d) fluxes on the element's +/- face."""
+        hp, hm = self.lhp, self.lhm
+        if self.dim == 1:
+            return _lin(lambda c: c[..., None] * hp, fplus) - _lin(lambda c: c[..., None] * hm, fminus)
+        if d == 0:
+            return (_lin(lambda c: c[..., :, None] * hp[None, :], fplus)
+                    - _lin(lambda c: c[..., :, None] * hm[None, :], fminus))
+        return (_lin(lambda c: c[..., None, :] * hp[:, None], fplus)
+                - _lin(lambda c: c[..., None, :] * hm[:, None], fminus))
+
+    def elem_axis(self, d):
+        """Array axis along which elements neighbour in direction d."""
+        if self.dim == 1:
+            return 0
+        return 1 if d == 0 else 0
+
+    def faces(self, F, d):
+        """Own traces on the +/- faces and the matching neighbour traces:
+        returns (own_plus, nbr_plus, nbr_minus, own_minus), where nbr_plus is
+        the neighbour across the + face (its - trace) and nbr_minus the
+        neighbour across the - face (its + trace)."""
+        ax = self.elem_axis(d)
+        tp, tm = self.trace(F, d, +1), self.trace(F, d, -1)
+        return tp, _roll(tm, -1, ax), _roll(tp, +1, ax), tm
+
+
+def _scale(d, me):
+    return 2.0 / (me.dx if d == 0 else me.dy)
+
+
+def lifting(disc: Disc, Wf, ops=None):
+    """BR1 lifted gradients of w_grad (eq:Lifting, central surface
+    value P:861):  d^d = (2/h_d) [ sum Dhat g + g*_+ lhat(1) - g*_- lhat(-1) ].
+    Returns (gx, gy), each a tuple (u_d, v_d, T_d) of field-shaped arrays."""
+    ops = ops or _Ops(disc)
+    eq, me = disc.eq, disc.mesh
+    g = physics.grad_vars(eq, _split(Wf, 2))
+    G = ad.stack(list(g), axis=2)                       # (ny, nx, 3, p, p)
+    out = []
+    for d in range(2):
+        own_p, nbr_p, nbr_m, own_m = ops.faces(G, d)
+        gstar_p = 0.5 * (own_p + nbr_p)                 # canonical L = own, R = nbr
+        gstar_m = 0.5 * (nbr_m + own_m)                 # canonical L = nbr, R = own
+        D = _scale(d, me) * (ops.volume(G, d) + ops.surface(gstar_p, gstar_m, d))
+        out.append(_split(D, 2))
+    return out[0], out[1]
+
+
+def rhs1_field(disc: Disc, Wf):
+    """R^(1)_h on a field-shaped array (values, duals or hyper-duals)."""
+    ops = _Ops(disc)
+    eq, me = disc.eq, disc.mesh
+    dim = me.dim
+    va = 2 if dim == 2 else 1
+    w = _split(Wf, va)
+    if eq.viscous:
+        gx, gy = lifting(disc, Wf, ops)
+        Gx, Gy = ad.stack(list(gx), axis=2), ad.stack(list(gy), axis=2)
+    total = 0.0
+    for d in range(dim):
+        # volume flux at the nodes
+        F = list(physics.flux(eq, w, d))
+        if eq.viscous:
+            Fv = physics.viscous_flux(eq, w, gx, gy, d)
+            F = [f - fv for f, fv in zip(F, Fv)]
+        Fa = ad.stack(F, axis=va)
+        # traces of the state (and of the lifted gradients for NS)
+        wp, wnp, wnm, wm = [_split(t, va) for t in ops.faces(Wf, d)]
+        fp = list(physics.llf(eq, wp, wnp, d))           # + face: L = own, R = nbr
+        fm = list(physics.llf(eq, wnm, wm, d))           # - face: L = nbr, R = own
+        if eq.viscous:
+            gxp, gxnp, gxnm, gxm = [_split(t, 2) for t in ops.faces(Gx, d)]
+            gyp, gynp, gynm, gym = [_split(t, 2) for t in ops.faces(Gy, d)]
+            fvL = physics.viscous_flux(eq, wp, gxp, gyp, d)
+            fvR = physics.viscous_flux(eq, wnp, gxnp, gynp, d)
+            fp = [f - 0.5 * (a + b) for f, a, b in zip(fp, fvL, fvR)]
+            fvL = physics.viscous_flux(eq, wnm, gxnm, gynm, d)
+            fvR = physics.viscous_flux(eq, wm, gxm, gym, d)
+            fm = [f - 0.5 * (a + b) for f, a, b in zip(fm, fvL, fvR)]
+        fpa = ad.stack(fp, axis=va)
+        fma = ad.stack(fm, axis=va)
+        total = total + _scale(d, me) * (ops.volume(Fa, d) + ops.surface(fpa, fma, d))
+    return -total
+
+
+def rhs1(disc: Disc, W):
+    """R^(1)_h(W) for a flat layout-L vector (or Jet of flat vectors)."""
+    return disc.to_flat(rhs1_field(disc, disc.to_field(W)))
+
+
+def rhs2(disc: Disc, W, sigma):
+    """R^(2)_h(W, sigma): dual part of R^(1)_h(W + e1 sigma)."""
+    return rhs1(disc, ad.Jet(np.asarray(W, float), np.asarray(sigma, float))).d1
+
+
+def rhs12(disc: Disc, W, sigma):
+    """(R^(1)_h(W), R^(2)_h(W, sigma)) from one dual evaluation."""
+    r = rhs1(disc, ad.Jet(np.asarray(W, float), np.asarray(sigma, float)))
+    return r.v, r.d1

@@ -1,0 +1,82 @@
+"""Alg. 1 HBPC(q, k_max): implicit predictor, k_max correction sweeps, FSAL
+update, with the stage equations in the generalized form
+eq:Newton_Residual.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+Readings: R5 -- the corrector right-hand side includes I_l
+(eq:corrector is normative; P:152 omits it); R6 -- after each converged
+stage solve R1_l := R1(w_l) and R2_l := R2(w_l, R1_l) are recomputed (the
+Remark at P:89-91), stage 1 reuses the FSAL cache; R12 -- the BJ_ext blocks
+are built at w^n once per (alpha1, alpha2) pair per step.
+"""
+import numpy as np
+
+from . import implicit
+from .dgsem import rhs1, rhs12
+from .tableau import tableau
+
+
+class HBPC:
+    def __init__(self, disc, q, kmax, opts: implicit.NewtonOpts):
+        self.disc, self.q, self.kmax, self.opts = disc, q, kmax, opts
+        self.c, self.B1, self.B2 = tableau(q)
+        self.s = len(self.c)
+        self.cache = None            # (R1(w^n), R2(w^n)) -- FSAL
+
+    def _ops(self, w):
+        r1 = rhs1(self.disc, w)
+        _, r2 = rhs12(self.disc, w, r1)
+        return r1, r2
+
+    def step(self, Wn, dt, stats=None):
+        """Advance W^n -> W^{n+1}.  Returns W^{n+1}."""
+        if stats is None:
+            stats = dict(stage_solves=0, newton_its=0, gmres_its=0, precond_builds=0)
+        disc, s, opts = self.disc, self.s, self.opts
+        if self.cache is None:
+            self.cache = self._ops(Wn)
+        R1n, R2n = self.cache
+        c, B1, B2 = self.c, self.B1, self.B2
+
+        pcs = {}
+
+        def precond(a1, a2):
+            if opts.precond != "bjext" or opts.precond_policy != "per_step_per_alpha":
+                return None
+            key = (a1, a2)
+            if key not in pcs:
+                pcs[key] = implicit.BJExt(disc, Wn, a1, a2, dt)
+                stats["precond_builds"] += 1
+            return pcs[key]
+
+        # ---- predictor eq:predictor / eq:nonlinear_predictor
+        w = [Wn] + [None] * (s - 1)
+        R1 = [R1n] + [None] * (s - 1)
+        R2 = [R2n] + [None] * (s - 1)
+        for l in range(1, s):
+            dc = c[l] - c[l - 1]
+            a1, a2 = dc / 2.0, dc * dc / 6.0
+            c2 = a2 * dt * dt / 2.0
+            b = w[l - 1] + a1 * dt * R1[l - 1] + c2 * R2[l - 1]
+            w[l], _ = implicit.newton_solve(disc, a1, a2, dt, b, w[l - 1], opts,
+                                            precond(a1, a2), stats)
+            stats["stage_solves"] += 1
+            R1[l], R2[l] = self._ops(w[l])
+
+        # ---- corrector eq:corrector / eq:nonlinear_corrector
+        for k in range(self.kmax):
+            wn, R1n_, R2n_ = [Wn] + [None] * (s - 1), [R1n] + [None] * (s - 1), [R2n] + [None] * (s - 1)
+            for l in range(1, s):
+                I_l = dt * sum(B1[l, j] * R1[j] for j in range(s)) \
+                    + dt * dt * sum(B2[l, j] * R2[j] for j in range(s))
+                b = Wn - dt * R1[l] + (dt * dt / 2.0) * R2[l] + I_l
+                wn[l], _ = implicit.newton_solve(disc, 1.0, 1.0, dt, b, w[l], opts,
+                                                 precond(1.0, 1.0), stats)
+                stats["stage_solves"] += 1
+                R1n_[l], R2n_[l] = self._ops(wn[l])
+            w, R1, R2 = wn, R1n_, R2n_
+
+        # ---- update / FSAL
+        self.cache = (R1[s - 1], R2[s - 1])
+        return w[s - 1]

@@ -1,0 +1,116 @@
+"""Point-wise physics: fluxes, numerical flux, viscous flux, gradient variables.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+States are tuples of per-variable components (numpy arrays or ad.Jet), so
+every function here is evaluated unchanged on plain values, duals and
+hyper-duals.
+
+  advection     F = a w                                   (C1/C2)
+  euler         F_x = (rho u, rho u^2 + p, rho u v, u (E + p))      (eq:Euler,
+                p = (gamma-1)(E - rho |v|^2 / 2)                     P:388-394)
+                with reference Mach number eps = 1 (reading R18)
+  navier_stokes F - F^v, F^v = (0, tau, tau.v + q), tau = mu(grad v +
+                grad v^T - 2/3 div v I), q = lambda_T grad T, lambda_T = c_p mu/Pr,
+                c_p = R gamma/(gamma-1), R = 1/gamma, T = p/(rho R)
+
+Numerical flux (reading R3): the paper's
+eq:Riemann is a global Lax-Friedrichs flux with a constant lambda; the
+BASELINE configs name LLF/Rusanov, so the configs use
+    f*(wL, wR; e_d) = 1/2 (F_d(wL) + F_d(wR)) + 1/2 lambda_f (wL - wR),
+    lambda_f = max(|v_L.e_d| + c_L, |v_R.e_d| + c_R),
+evaluated in the canonical orientation of a face (L = the element on the
+-e_d side, normal +e_d); ties take L, sign(0) = +1.  For advection
+lambda_f = |a_d| and f* is the exact upwind flux.
+"""
+from dataclasses import dataclass
+
+from . import ad
+
+
+@dataclass(frozen=True)
+class Equation:
+    kind: str                  # "advection" | "euler" | "navier_stokes"
+    a: tuple = (1.0, 1.0)      # advection velocity
+    gamma: float = 1.4
+    mu: float = 0.0
+    prandtl: float = 0.72
+
+    @property
+    def nv(self):
+        return 1 if self.kind == "advection" else 4
+
+    @property
+    def viscous(self):
+        return self.kind == "navier_stokes"
+
+
+def pressure(eq, w):
+    rho, mx, my, E = w
+    return (eq.gamma - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho)
+
+
+def flux(eq, w, d):
+    """Inviscid physical flux F_d(w) in direction d (0 = x, 1 = y)."""
+    if eq.kind == "advection":
+        return (eq.a[d] * w[0],)
+    rho, mx, my, E = w
+    p = pressure(eq, w)
+    vn = (mx if d == 0 else my) / rho
+    return (rho * vn,
+            mx * vn + (p if d == 0 else 0.0),
+            my * vn + (p if d == 1 else 0.0),
+            vn * (E + p))
+
+
+def wave_speed(eq, w, d):
+    """|v.e_d| + c (Euler/NS), |a_d| (advection)."""
+    if eq.kind == "advection":
+        return abs(eq.a[d]) + 0.0 * w[0]
+    rho, mx, my, E = w
+    p = pressure(eq, w)
+    vn = (mx if d == 0 else my) / rho
+    return ad.absval(vn) + ad.sqrt(eq.gamma * p / rho)
+
+
+def llf(eq, wL, wR, d):
+    """Canonical-orientation LLF flux across a face with normal +e_d."""
+    FL, FR = flux(eq, wL, d), flux(eq, wR, d)
+    lam = ad.maxval(wave_speed(eq, wL, d), wave_speed(eq, wR, d))
+    return tuple(0.5 * (fl + fr) + 0.5 * lam * (l - r)
+                 for fl, fr, l, r in zip(FL, FR, wL, wR))
+
+
+# ---- Navier-Stokes --------------------------------------------------------
+
+def gas_constants(eq):
+    R = 1.0 / eq.gamma                      # R = 1/(gamma eps^2), eps = 1
+    cp = R * eq.gamma / (eq.gamma - 1.0)
+    lam_T = cp * eq.mu / eq.prandtl
+    return R, cp, lam_T
+
+
+def grad_vars(eq, w):
+    """w_grad = (v1, v2, T) (eq:LiftingEq), T from p = rho R T."""
+    rho, mx, my, E = w
+    R, _, _ = gas_constants(eq)
+    p = pressure(eq, w)
+    return (mx / rho, my / rho, p / (rho * R))
+
+
+def viscous_flux(eq, w, gx, gy, d):
+    """F^v_d(w, grad) with gx = (u_x, v_x, T_x), gy = (u_y, v_y, T_y)."""
+    rho, mx, my, E = w
+    u, v = mx / rho, my / rho
+    _, _, lam_T = gas_constants(eq)
+    ux, vx, Tx = gx
+    uy, vy, Ty = gy
+    div = ux + vy
+    mu = eq.mu
+    if d == 0:
+        txx = mu * (2.0 * ux - (2.0 / 3.0) * div)
+        txy = mu * (uy + vx)
+        return (0.0 * rho, txx, txy, txx * u + txy * v + lam_T * Tx)
+    tyx = mu * (uy + vx)
+    tyy = mu * (2.0 * vy - (2.0 / 3.0) * div)
+    return (0.0 * rho, tyx, tyy, tyx * u + tyy * v + lam_T * Ty)

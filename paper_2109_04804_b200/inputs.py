@@ -1,0 +1,90 @@
+"""Seeded synthetic inputs shared by the CUDA path and the CPU oracle.
+
+This module holds NO arithmetic of the method (no basis, no operator, no
+solver): it evaluates the analytic initial conditions of BASELINE.json's
+configs at node coordinates handed in by the caller, adds the seeded noise,
+and draws random perturbations for parity tests.  Node coordinates come
+from the library (``hbpdc_node_coords``) in the product path and from the
+oracle in tests; tests check that the two agree.
+
+Recipes: DESIGN.md section "Inputs".  Seeds: master 2109_04804; config k
+(0-based, C1 = 0) noise stream ``default_rng(2109_04804 + k)``; operator
+test inputs ``default_rng(2109_04804 + 100*k + test_id)``.
+"""
+import math
+
+import numpy as np
+
+MASTER_SEED = 2109_04804
+GAMMA = 1.4
+
+
+def conserved(rho, u, v, p, gamma=GAMMA):
+    """(rho, rho u, rho v, E) with E = p/(gamma-1) + rho |v|^2 / 2."""
+    return (rho, rho * u, rho * v, p / (gamma - 1.0) + 0.5 * rho * (u * u + v * v))
+
+
+def ic_primitive(case, X, Y=None, gamma=GAMMA):
+    """Analytic initial condition of a config at coordinates X (and Y).
+    Returns a tuple of variables (1 for advection, 4 conserved for Euler/NS)."""
+    if case == "C1":                                       # 1D advection
+        return (np.sin(2 * math.pi * X),)
+    if case == "C2":                                       # 2D advection
+        return (np.sin(2 * math.pi * X) * np.sin(2 * math.pi * Y),)
+    if case == "C3":                                       # isentropic vortex
+        beta = 5.0
+        r2 = X * X + Y * Y
+        T = 1.0 - (gamma - 1.0) * beta * beta * np.exp(1.0 - r2) / (8.0 * gamma * math.pi ** 2)
+        rho = T ** (1.0 / (gamma - 1.0))
+        p = rho ** gamma
+        f = beta / (2 * math.pi) * np.exp(0.5 * (1.0 - r2))
+        return conserved(rho, 1.0 - f * Y, 1.0 + f * X, p, gamma)
+    if case == "C4":                                       # density wave
+        rho = 1.0 + 0.2 * np.sin(2 * math.pi * (X + Y))
+        one = np.ones_like(X)
+        return conserved(rho, one, one, one, gamma)
+    if case == "C5":                                       # TGV-type, Mach 0.1
+        M = 0.1
+        rho = np.ones_like(X)
+        u = np.sin(X) * np.cos(Y)
+        v = -np.cos(X) * np.sin(Y)
+        p = 1.0 / (gamma * M * M) + 0.25 * (np.cos(2 * X) + np.cos(2 * Y))
+        return conserved(rho, u, v, p, gamma)
+    raise ValueError(case)
+
+
+def layout(vars_, dim):
+    """Stack per-variable node arrays into layout L ([elem][var][j][i]).
+    2D inputs have shape (ny, nx, p, p) [j, i]; 1D inputs (nx, p)."""
+    ax = 2 if dim == 2 else 1
+    return np.ascontiguousarray(np.stack(vars_, axis=ax)).reshape(-1)
+
+
+CASE_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
+
+
+def initial_state(case, coords, noise=None, gamma=GAMMA):
+    """Nodal interpolation of the IC in layout L, plus the seeded
+    uniform noise of amplitude `noise` on every conserved variable (C3:
+    1e-6), drawn in layout order from default_rng(MASTER_SEED + k)."""
+    dim = len(coords)
+    W = layout(ic_primitive(case, *coords, gamma=gamma), dim)
+    if noise:
+        rng = np.random.default_rng(MASTER_SEED + CASE_INDEX[case])
+        W = W + rng.uniform(-noise, noise, size=W.shape)
+    return W
+
+
+def perturbed_state(W_ic, seed, rel=1e-2):
+    """W = IC + U[-rel, rel) |IC| in layout order (parity inputs)."""
+    rng = np.random.default_rng(seed)
+    return W_ic + rng.uniform(-rel, rel, size=W_ic.shape) * np.abs(W_ic)
+
+
+def random_field(n, seed, scale=1.0, unit_norm=False):
+    """N(0, 1) * scale, optionally normalised to unit 2-norm (Krylov-like)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(n) * scale
+    if unit_norm:
+        x = x / np.linalg.norm(x)
+    return x

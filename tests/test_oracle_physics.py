@@ -1,0 +1,133 @@
+"""Pins for oracle.physics and oracle.ad.  CPU only."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ad, physics
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+EU = physics.Equation("euler")
+NS = physics.Equation("navier_stokes", mu=1e-3)
+
+
+def test_euler_flux_example():
+    g = GOLD["euler_flux_eps1"]
+    w = tuple(np.array(x) for x in g["w"])
+    assert float(physics.pressure(EU, w)) == pytest.approx(g["p"], abs=1e-15)
+    np.testing.assert_allclose([float(f) for f in physics.flux(EU, w, 0)], g["Fx"], atol=1e-15)
+
+
+def test_pressure_example():
+    g = GOLD["pressure"]
+    # S:140 uses the momentum components as given (rho v = 0.3)
+    w = tuple(np.array(x) for x in g["w"])
+    assert float(physics.pressure(EU, w)) == pytest.approx(g["p"], abs=1e-12)
+
+
+def test_advection_flux_and_upwind():
+    g = GOLD["advection_flux"]
+    eq = physics.Equation("advection", a=tuple(g["a"]))
+    assert physics.flux(eq, (np.array(g["w"]),), 0)[0] == pytest.approx(g["Fx"])
+    assert physics.flux(eq, (np.array(g["w"]),), 1)[0] == pytest.approx(g["Fy"])
+    u = GOLD["llf_upwind"]
+    f = physics.llf(eq, (np.array(u["wL"]),), (np.array(u["wR"]),), 0)[0]
+    assert float(f) == pytest.approx(u["fstar_llf"], abs=1e-15)
+    # the exact upwind flux: a>0 takes the left state
+    assert float(f) == pytest.approx(0.3 * u["wL"], abs=1e-15)
+
+
+def _rand_states(rng, n=50):
+    rho = rng.uniform(0.5, 2.0, n)
+    u, v = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    p = rng.uniform(0.5, 2.0, n)
+    return (rho, rho * u, rho * v, p / 0.4 + 0.5 * rho * (u * u + v * v))
+
+
+def test_llf_consistency_and_conservation():
+    rng = np.random.default_rng(1)
+    wL, wR = _rand_states(rng), _rand_states(rng)
+    for d in range(2):
+        F = physics.flux(EU, wL, d)
+        fc = physics.llf(EU, wL, wL, d)
+        for a, b in zip(F, fc):
+            np.testing.assert_allclose(a, b, rtol=1e-15, atol=1e-15)
+        # f*(L, R; +e) and the flux the right element sees with its outward
+        # normal are exact negatives (canonical orientation) -- and the flux
+        # is symmetric under L<->R swap with normal flip:
+        #   f*(wL, wR, n) = -f*(wR, wL, -n): with -n the physical flux and the
+        # velocity flip sign, so mirror the states' normal momentum.
+        fl = physics.llf(EU, wL, wR, d)
+        mir = lambda w: tuple(-x if k == 1 + d else x for k, x in enumerate(w))
+        fr = physics.llf(EU, mir(wR), mir(wL), d)
+        for k in range(4):
+            sgn = 1.0 if k == 1 + d else -1.0
+            np.testing.assert_allclose(fl[k], sgn * fr[k], rtol=1e-13, atol=1e-13)
+
+
+def test_dual_derivatives_match_central_fd():
+    """(dF/dw) sigma from the dual part equals central differences of the
+    plain flux; the d12 part equals FD of the d1 part."""
+    rng = np.random.default_rng(2)
+    w, s, t = _rand_states(rng), _rand_states(rng), _rand_states(rng)
+    h = 1e-6
+    for d in range(2):
+        J = physics.llf(EU, tuple(ad.Jet(a, b, c) for a, b, c in zip(w, s, t)),
+                        tuple(ad.Jet(a + 0.1, b, c) for a, b, c in zip(w, s, t)), d)
+        fp = physics.llf(EU, tuple(a + h * b for a, b in zip(w, s)),
+                         tuple(a + 0.1 + h * b for a, b in zip(w, s)), d)
+        fm = physics.llf(EU, tuple(a - h * b for a, b in zip(w, s)),
+                         tuple(a + 0.1 - h * b for a, b in zip(w, s)), d)
+        for k in range(4):
+            fd = (fp[k] - fm[k]) / (2 * h)
+            np.testing.assert_allclose(J[k].d1, fd, rtol=1e-7, atol=1e-7)
+        # mixed second derivative: FD of the e1 part along direction t
+        Jp = physics.llf(EU, tuple(ad.Jet(a + h * c, b) for a, b, c in zip(w, s, t)),
+                         tuple(ad.Jet(a + 0.1 + h * c, b) for a, b, c in zip(w, s, t)), d)
+        Jm = physics.llf(EU, tuple(ad.Jet(a - h * c, b) for a, b, c in zip(w, s, t)),
+                         tuple(ad.Jet(a + 0.1 - h * c, b) for a, b, c in zip(w, s, t)), d)
+        for k in range(4):
+            fd = (Jp[k].d1 - Jm[k].d1) / (2 * h)
+            np.testing.assert_allclose(J[k].d12, fd, rtol=1e-6, atol=1e-6)
+
+
+def test_jet_rules():
+    x = ad.Jet(np.array([2.0]), np.array([1.0]), np.array([3.0]), np.array([0.5]))
+    # f = sqrt: f' = 1/(2 sqrt x), f'' = -1/(4 x^1.5)
+    r = ad.sqrt(x)
+    assert r.d12[0] == pytest.approx(0.5 / (2 * math.sqrt(2)) - 3.0 / (4 * 2 ** 1.5))
+    r = ad.recip(x)
+    assert r.d1[0] == pytest.approx(-0.25) and r.d12[0] == pytest.approx(-0.5 / 4 + 2 * 3 / 8)
+    y = x * x                                   # (x^2)'' = 2: d12 = 2 x d12 + 2 d1 d2
+    assert y.d12[0] == pytest.approx(2 * 2 * 0.5 + 2 * 1 * 3)
+    assert ad.absval(ad.Jet(np.array([0.0]), np.array([1.0]))).d1[0] == 1.0   # sign(0)=+1
+    m = ad.maxval(ad.Jet(np.array([1.0]), np.array([5.0])), ad.Jet(np.array([1.0]), np.array([7.0])))
+    assert m.d1[0] == 5.0                                                    # tie -> first
+
+
+def test_viscous_stress_examples():
+    """d = 0 -> 0; pure shear u_y = s -> tau_xy = mu s; pure
+    dilatation u_x = s -> tau_xx = 4/3 mu s, tau_yy = -2/3 mu s."""
+    w = (np.array(1.0), np.array(0.0), np.array(0.0), np.array(2.5))
+    z = np.array(0.0)
+    s = 0.7
+    F = physics.viscous_flux(NS, w, (z, z, z), (z, z, z), 0)
+    assert all(float(f) == 0.0 for f in F)
+    Fx = physics.viscous_flux(NS, w, (z, z, z), (np.array(s), z, z), 0)
+    assert float(Fx[2]) == pytest.approx(1e-3 * s) and float(Fx[1]) == 0.0
+    Fx = physics.viscous_flux(NS, w, (np.array(s), z, z), (z, z, z), 0)
+    Fy = physics.viscous_flux(NS, w, (np.array(s), z, z), (z, z, z), 1)
+    assert float(Fx[1]) == pytest.approx(4 / 3 * 1e-3 * s)
+    assert float(Fy[2]) == pytest.approx(-2 / 3 * 1e-3 * s)
+    # heat flux: lambda_T = c_p mu / Pr with c_p = 1/(gamma-1) (eps=1)
+    Fx = physics.viscous_flux(NS, w, (z, z, np.array(1.0)), (z, z, z), 0)
+    assert float(Fx[3]) == pytest.approx(2.5 * 1e-3 / 0.72)
+
+
+def test_grad_vars_example():
+    g = GOLD["grad_vars"]
+    w = (np.array(1.0), np.array(0.0), np.array(0.0), np.array(1.0 / 0.4))
+    out = physics.grad_vars(NS, w)
+    np.testing.assert_allclose([float(x) for x in out], g["wgrad"], atol=1e-15)
