@@ -1,0 +1,192 @@
+/*
+ * hbpdc.h -- C-ABI of the B200-native HBPC(q, k_max) / DGSEM hot path
+ * (Zeifang & Schuetz, arXiv 2109.04804).
+ *
+ * Citation convention: "P:n" = line n of the paper's LaTeX source,
+ * "S:n" = line n of SPEC.md, equations by their \label{} name.  Readings of
+ * ambiguous passages (R1..R30) are listed in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All arrays are IEEE binary64, DEVICE pointers (unless a name ends in
+ *    _host), contiguous, in layout L = [elem][var][j][i] (i fastest) over the
+ *    calling rank's local elements (elem = ey_local * nx_local + ex_local).
+ *    A field has n_local = n_local_elems * m doubles, m = nv * (N+1)^dim.
+ *  - Ownership: the caller owns every pointer argument.  The library owns
+ *    all scratch (BJ_ext blocks, Krylov basis, stage store, halo buffers).
+ *  - Stream semantics: work is enqueued on the context stream
+ *    (hbpdc_dist.cuda_stream, or a library stream if NULL).  Calls that return
+ *    host scalars (norm_out, stats) synchronise the stream; the others are
+ *    asynchronous.
+ *  - Aliasing: outputs must not alias inputs (except hbpdc_step's in/out W).
+ *  - Errors: a non-zero hbpdc_status; hbpdc_last_error() gives a message
+ *    (stage / sweep / Newton index, element and dt for LU breakdown).  No C++
+ *    exception crosses the ABI, nothing calls exit().
+ *  - Multi-GPU: every rank calls every function collectively with its local
+ *    block; norms and stats come back globally reduced.
+ */
+#ifndef HBPDC_H
+#define HBPDC_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define HBPDC_API __attribute__((visibility("default")))
+#else
+#define HBPDC_API
+#endif
+
+typedef struct hbpdc_ctx hbpdc_ctx;
+
+typedef enum {
+  HBPDC_OK = 0,
+  HBPDC_E_ARG = 1,          /* invalid argument / unsupported configuration   */
+  HBPDC_E_CUDA = 2,         /* CUDA runtime error                              */
+  HBPDC_E_NCCL = 3,         /* NCCL error                                      */
+  HBPDC_E_OOM = 4,          /* device allocation failed                        */
+  HBPDC_E_NONFINITE = 5,    /* NaN/Inf detected in a residual or norm          */
+  HBPDC_E_NEG_PRESSURE = 6, /* reserved                                        */
+  HBPDC_E_LU_SINGULAR = 7,  /* zero pivot in the BJ_ext block inversion        */
+  HBPDC_E_NEWTON = 8,       /* Newton did not converge within newton_max       */
+  HBPDC_E_GMRES = 9         /* GMRES exceeded krylov_max_per_newton            */
+} hbpdc_status;
+
+enum { HBPDC_ADVECTION = 0, HBPDC_EULER = 1, HBPDC_NAVIER_STOKES = 2 };
+enum { HBPDC_GLL = 0, HBPDC_GL = 1 };
+enum { HBPDC_LLF = 0 };
+enum { HBPDC_BR1 = 0 };
+enum { HBPDC_PC_NONE = 0, HBPDC_PC_BJEXT = 1 };
+enum { HBPDC_PC_PER_STEP_PER_ALPHA = 0, HBPDC_PC_PER_NEWTON = 1 };
+enum { HBPDC_JVP_AUTO = 0, HBPDC_JVP_FD = 1, HBPDC_JVP_EXACT = 2, HBPDC_JVP_LINEAR = 3 };
+
+/* The problem (P:43-47 conservation law; P:170 DGSEM degree N; P:83 HBPC(q,k_max)). */
+typedef struct {
+  int dim;              /* 1 or 2                                                  */
+  int equation;         /* HBPDC_ADVECTION | HBPDC_EULER | HBPDC_NAVIER_STOKES     */
+  double a[2];          /* advection velocity (advection only)                     */
+  double gamma;         /* isentropic coefficient, e.g. 1.4                */
+  double mach_eps;      /* reference Mach number eps; must be 1 (reading R18)      */
+  double mu;            /* dynamic viscosity (NS)                           */
+  double prandtl;       /* Prandtl number (NS), e.g. 0.72                   */
+  int N;                /* polynomial degree, 1..7                                 */
+  int nodes;            /* HBPDC_GLL (configs, reading R1); GL is not supported    */
+  int nx, ny;           /* global element counts (ny ignored in 1D)                */
+  double xmin, xmax, ymin, ymax;   /* periodic Cartesian domain                   */
+  int flux;             /* HBPDC_LLF (reading R3)                                  */
+  int lifting;          /* HBPDC_BR1 (NS, reading R19)                             */
+  int q, kmax;          /* HBPC(q, k_max), q in {4, 6, 8}, k_max >= 0              */
+} hbpdc_problem;
+
+typedef struct {
+  double newton_rtol;          /* ||G(X^r)|| <= rtol ||G(X^0)||               */
+  double newton_atol_dw;       /* stop after a step with ||dW||_2 <= atol     */
+  double newton_floor;         /* floor factor f: ||G|| <= f eps ||b|| (reading R10) */
+  int newton_max;              /* max Newton iterations per stage solve       */
+  double gmres_rtol;           /* relative GMRES tolerance             */
+  int gmres_restart;           /* Krylov dimension before restart            */
+  int krylov_max_per_newton;   /* total GMRES iterations per Newton step     */
+  int precond;                 /* HBPDC_PC_NONE | HBPDC_PC_BJEXT          */
+  int precond_policy;          /* HBPDC_PC_PER_STEP_PER_ALPHA (default) | PER_NEWTON */
+  int jvp_mode;                /* HBPDC_JVP_AUTO: linear (advection) / FD otherwise  */
+} hbpdc_solver_opts;
+
+typedef struct {
+  int rank, nranks;            /* this rank, number of ranks                          */
+  int px, py;                  /* rank grid: px * py == nranks, nx % px == ny % py == 0 */
+  const void* nccl_unique_id;  /* 128-byte ncclUniqueId (rank 0's), NULL if nranks==1 */
+  void* cuda_stream;           /* cudaStream_t to enqueue on, NULL = library stream  */
+  int device;                  /* CUDA device ordinal                                 */
+} hbpdc_dist;
+
+typedef struct {               /* summed over one hbpdc_step                          */
+  int stage_solves, newton_its, gmres_its, precond_builds, max_krylov_j;
+  int jvp_calls, precond_applies;
+  double final_newton_rel, wall_s;
+} hbpdc_step_stats;
+
+/* Create a context: basis (GLL nodes/weights, Dhat = -M^-1 D^T M, reading R2),
+ * mesh, rank partition, NCCL communicator, scratch.  Host only. */
+HBPDC_API hbpdc_status hbpdc_init(const hbpdc_problem* problem, const hbpdc_solver_opts* opts,
+                        const hbpdc_dist* dist, hbpdc_ctx** out);
+
+/* Local block: element count, block size m, offsets and extents in elements. */
+HBPDC_API hbpdc_status hbpdc_local_shape(const hbpdc_ctx* ctx, int* n_local_elems, int* m,
+                               int* ex0, int* ey0, int* nx_local, int* ny_local);
+
+/* Physical coordinates of the local nodes, layout [elem][j][i] (host arrays of
+ * n_local_elems*(N+1)^dim doubles; y_host ignored in 1D).  Synchronous. */
+HBPDC_API hbpdc_status hbpdc_node_coords(const hbpdc_ctx* ctx, double* x_host, double* y_host);
+
+/* sigma == NULL: out = R^(1)_h(W) (eq:DGSEM_wt).
+ * sigma != NULL: out = R^(2)_h(W, sigma) (eq:DGSEM_wtt): the time
+ * derivative of R^(1)_h along w_t = sigma. */
+HBPDC_API hbpdc_status hbpdc_rhs(hbpdc_ctx* ctx, const double* W, const double* sigma, double* out);
+
+/* Extended stage residual (eq:Newton_Residual P:137-141, reading R4):
+ *   G1 = W - a1 dt R1(W) + (a2 dt^2/2) R2(W, sigma) - b,   G2 = sigma - R1(W).
+ * norm_out (host, may be NULL): global ||(G1, G2)||_2 (synchronises). */
+HBPDC_API hbpdc_status hbpdc_residual(hbpdc_ctx* ctx, double alpha1, double alpha2, double dt,
+                            const double* b, const double* W, const double* sigma,
+                            double* G1, double* G2, double* norm_out);
+
+/* Jacobian-vector product J dX of eq:nonlinear_eqsys:
+ *   HBPDC_JVP_FD     : eq:MatrixFree_nonlinear with
+ *                      eps_FD = sqrt(2^-52)/(eps ||d.||_2) (reading R7),
+ *                      sigma direction R2(W, dsigma) (reading R8);
+ *   HBPDC_JVP_EXACT  : the exact blocks (hyper-dual evaluation);
+ *   HBPDC_JVP_LINEAR : eq:MatrixFree_linear, advection only;
+ *   HBPDC_JVP_AUTO   : LINEAR for advection, FD otherwise.
+ * out1 = top block, out2 = bottom block.  eps_override: NULL or a HOST array
+ * [eps_w, eps_s] fixing eps_FD (<= 0 means "the quotient is 0"). */
+HBPDC_API hbpdc_status hbpdc_jvp(hbpdc_ctx* ctx, double alpha1, double alpha2, double dt,
+                       const double* W, const double* sigma, const double* dW,
+                       const double* dsigma, double* out1, double* out2, int mode,
+                       const double* eps_override);
+
+/* BJ_ext build: K_i = element-diagonal block of dR1/dW at W,
+ * S_i = (I - a1 dt K_i + (a2 dt^2/2) K_i^2)^-1 by Gauss-Jordan with partial
+ * pivoting; advection stores one shared block. */
+HBPDC_API hbpdc_status hbpdc_precond_build(hbpdc_ctx* ctx, double alpha1, double alpha2, double dt,
+                                 const double* W);
+
+/* Install caller-provided S blocks (device array, n_local_elems*m*m row-major,
+ * or m*m if `shared`) together with the build state W and (a1, a2, dt).
+ * Used by parity tests to apply the oracle's S. */
+HBPDC_API hbpdc_status hbpdc_precond_set(hbpdc_ctx* ctx, double alpha1, double alpha2, double dt,
+                               const double* W, const double* S, int shared);
+
+/* Copy the current S blocks to a device array (n_local_elems*m*m or m*m). */
+HBPDC_API hbpdc_status hbpdc_precond_export(hbpdc_ctx* ctx, double* S_out, int* shared);
+
+/* P^-1 X per element: (D W + E s ; F W + G s), evaluated as
+ * u = S W, v = S s, top = u - c2 K v, bottom = v + K (u - a1 dt v). */
+HBPDC_API hbpdc_status hbpdc_precond_apply(hbpdc_ctx* ctx, const double* inW, const double* insig,
+                                 double* outW, double* outsig);
+
+/* One HBPC(q, k_max) step (Alg. 1) of size dt, W in/out (device).
+ * stats may be NULL.  Synchronises. */
+HBPDC_API hbpdc_status hbpdc_step(hbpdc_ctx* ctx, double dt, double* W, hbpdc_step_stats* stats);
+
+/* Same, with W a HOST array: host->device copy, step, device->host copy. */
+HBPDC_API hbpdc_status hbpdc_step_host(hbpdc_ctx* ctx, double dt, double* W_host, hbpdc_step_stats* stats);
+
+/* Forget the FSAL cache (the next step recomputes R1/R2 of its input). */
+HBPDC_API hbpdc_status hbpdc_reset(hbpdc_ctx* ctx);
+
+/* Per-kernel timing (CUDA events on the context stream), for roofline
+ * reporting.  enable=1 starts recording, 0 stops.  kernel ids: see DESIGN.md
+ * (0 = precond GEMV, 1 = JVP, 2 = residual, 3 = Arnoldi dots, 4 = Arnoldi
+ * axpy, 5 = precond K-apply, 6 = precond build). */
+HBPDC_API hbpdc_status hbpdc_profile(hbpdc_ctx* ctx, int enable);
+HBPDC_API hbpdc_status hbpdc_profile_read(hbpdc_ctx* ctx, int kernel_id, long long* launches,
+                                double* total_ms);
+
+HBPDC_API const char* hbpdc_last_error(const hbpdc_ctx* ctx);
+HBPDC_API void hbpdc_finalize(hbpdc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HBPDC_H */

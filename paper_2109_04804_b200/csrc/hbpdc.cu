@@ -1,0 +1,890 @@
+// hbpdc.cu -- C-ABI implementation: context, operators, BJ_ext, GMRES, Newton,
+// and the HBPC(q, k_max) step (Alg. 1).  The host runs the control
+// flow; every vector operation runs in the kernels of ops_kernels.cu / linalg.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../include/hbpdc.h"
+#include "launch.h"
+#include "modes.cuh"
+
+namespace hbpdc {
+struct Basis1D {
+  int N;
+  std::vector<double> xi, w, Dhat;
+  double lhp, lhm;
+};
+Basis1D gll_basis(int N);
+}  // namespace hbpdc
+
+namespace {
+
+// ---- HBPC tableaux (App. A, eq:butcher4/6/8) ------------------------
+struct Tableau {
+  int s;
+  double c[4], B1[4][4], B2[4][4];
+};
+
+Tableau tableau(int q) {
+  Tableau t{};
+  auto set = [&](int s, std::initializer_list<double> c, std::initializer_list<double> b1,
+                 std::initializer_list<double> b2) {
+    t.s = s;
+    int i = 0;
+    for (double v : c) t.c[i++] = v;
+    i = 0;
+    for (double v : b1) { t.B1[i / s][i % s] = v; ++i; }
+    i = 0;
+    for (double v : b2) { t.B2[i / s][i % s] = v; ++i; }
+  };
+  if (q == 4) {
+    set(2, {0.0, 1.0}, {0, 0, 1.0 / 2, 1.0 / 2}, {0, 0, 1.0 / 12, -1.0 / 12});
+  } else if (q == 6) {
+    set(3, {0.0, 0.5, 1.0},
+        {0, 0, 0, 101.0 / 480, 8.0 / 30, 55.0 / 2400, 7.0 / 30, 16.0 / 30, 7.0 / 30},
+        {0, 0, 0, 65.0 / 4800, -25.0 / 600, -25.0 / 8000, 5.0 / 300, 0.0, -5.0 / 300});
+  } else {
+    set(4, {0.0, 1.0 / 3, 2.0 / 3, 1.0},
+        {0, 0, 0, 0, 6893.0 / 54432, 313.0 / 2016, 89.0 / 2016, 397.0 / 54432, 223.0 / 1701, 20.0 / 63,
+         13.0 / 63, 20.0 / 1701, 31.0 / 224, 81.0 / 224, 81.0 / 224, 31.0 / 224},
+        {0, 0, 0, 0, 1283.0 / 272160, -851.0 / 30240, -269.0 / 30240, -163.0 / 272160, 43.0 / 8505,
+         -16.0 / 945, -19.0 / 945, -8.0 / 8505, 19.0 / 3360, -9.0 / 1120, 9.0 / 1120, -19.0 / 3360});
+  }
+  return t;
+}
+
+constexpr double EPS_MACH = 2.220446049250313e-16;   // 2^-52 (reading R7)
+constexpr int NPROF = 8;
+
+struct DevBuf {
+  double* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace
+
+struct hbpdc_ctx {
+  hbpdc_problem pb{};
+  hbpdc_solver_opts op{};
+  hbpdc_dist ds{};
+  int nv = 1, P = 2, nodes = 2, m = 2, nE = 0, nxl = 0, nyl = 0, ex0 = 0, ey0 = 0;
+  size_t n = 0;          // W-DOF on this rank
+  Geo geo{};
+  OpCfg cfg{};
+  hbpdc::Basis1D basis;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  Tableau tab{};
+  int restart = 0;
+  // device memory
+  std::vector<void*> allocs;
+  double *X = nullptr, *G = nullptr, *dX = nullptr, *rhs = nullptr, *tmp2 = nullptr, *zb = nullptr;
+  double *Vk = nullptr;        // Krylov basis (restart+1) x 2n
+  double *partial = nullptr;   // (restart+2) x RED_BLOCKS
+  double *dh = nullptr, *dnrm = nullptr, *deps = nullptr, *dy = nullptr;
+  double *lift0 = nullptr, *lift1 = nullptr;
+  // precond
+  double *S = nullptr, *Wb = nullptr, *U = nullptr, *Vv = nullptr, *Z = nullptr;
+  int* info = nullptr;
+  int s_shared = 0, pc_valid = 0, zchunk = 0;
+  double pc_a1 = 0, pc_a2 = 0, pc_dt = -1;
+  // stage store: [sweep(2)][s] of w, R1, R2
+  double *stw[2][4] = {}, *str1[2][4] = {}, *str2[2][4] = {};
+  double *Wn = nullptr, *bvec = nullptr, *Wio = nullptr;
+  int fsal_valid = 0;
+  // host scratch
+  std::vector<double> H, cs, sn, gv, y, hh;
+  double* hpin = nullptr;      // pinned host scratch
+  // profiling
+  int prof_on = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_rec;
+  long long prof_launch[NPROF] = {};
+  double prof_ms[NPROF] = {};
+  hbpdc_step_stats* st = nullptr;  // stats of the step in progress
+};
+
+namespace {
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      c->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call;     \
+      return e_ == cudaErrorMemoryAllocation ? HBPDC_E_OOM : HBPDC_E_CUDA;              \
+    }                                                                                   \
+  } while (0)
+#define CKS(call)                          \
+  do {                                     \
+    hbpdc_status s_ = (call);              \
+    if (s_ != HBPDC_OK) return s_;         \
+  } while (0)
+
+hbpdc_status fail(hbpdc_ctx* c, hbpdc_status s, const std::string& msg) {
+  c->err = msg;
+  return s;
+}
+
+hbpdc_status dalloc(hbpdc_ctx* c, double** p, size_t n) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, (n ? n : 1) * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    char buf[160];
+    snprintf(buf, sizeof buf, "cudaMalloc of %zu doubles failed: %s", n, cudaGetErrorString(e));
+    c->err = buf;
+    return HBPDC_E_OOM;
+  }
+  c->allocs.push_back(q);
+  *p = (double*)q;
+  return HBPDC_OK;
+}
+
+// profiling helpers (CUDA events on the context stream)
+struct ProfScope {
+  hbpdc_ctx* c;
+  int id;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(hbpdc_ctx* c_, int id_) : c(c_), id(id_) {
+    if (!c->prof_on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c->stream);
+  }
+  ~ProfScope() {
+    if (!c->prof_on) return;
+    cudaEventRecord(b, c->stream);
+    c->prof_rec.push_back({id, {a, b}});
+  }
+};
+
+void prof_flush(hbpdc_ctx* c) {
+  if (c->prof_rec.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto& r : c->prof_rec) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.second.first, r.second.second);
+    c->prof_ms[r.first] += ms;
+    c->prof_launch[r.first] += 1;
+    cudaEventDestroy(r.second.first);
+    cudaEventDestroy(r.second.second);
+  }
+  c->prof_rec.clear();
+}
+
+OpArgs base_args(hbpdc_ctx* c) {
+  OpArgs A{};
+  A.m = c->m;
+  return A;
+}
+
+// launch an operator; NS lifts the jet states first
+hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A) {
+  if (c->pb.equation == HBPDC_NAVIER_STOKES) {
+    CK(launch_lift(k, 0, c->cfg, c->geo, A, c->lift0));
+    A.G0 = c->lift0;
+    if (k == OP_JVP_FD) {
+      CK(launch_lift(k, 1, c->cfg, c->geo, A, c->lift1));
+      A.G1 = c->lift1;
+    }
+  }
+  CK(launch_op(k, c->cfg, c->geo, A));
+  return HBPDC_OK;
+}
+
+hbpdc_status norm_dev(hbpdc_ctx* c, const double* x, size_t L, double* out_dev) {
+  CK(launch_sumsq(x, L, c->partial, c->stream));
+  CK(launch_finish_norm(c->partial, out_dev, c->stream));
+  return HBPDC_OK;
+}
+
+hbpdc_status norm_host(hbpdc_ctx* c, const double* x, size_t L, double* out) {
+  CKS(norm_dev(c, x, L, c->dnrm));
+  CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *out = c->hpin[0];
+  return HBPDC_OK;
+}
+
+int jvp_kind(hbpdc_ctx* c, int mode) {
+  if (mode == HBPDC_JVP_AUTO) mode = c->pb.equation == HBPDC_ADVECTION ? HBPDC_JVP_LINEAR : HBPDC_JVP_FD;
+  return mode;
+}
+
+// J dX for the extended system, dX = [dW | ds] (2n), out = [top | bottom]
+hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const double* W, const double* sg,
+                      const double* dW, const double* ds, double* o1, double* o2, int mode,
+                      const double* eps_override) {
+  const size_t n = c->n;
+  mode = jvp_kind(c, mode);
+  OpArgs A = base_args(c);
+  A.W = W; A.S = sg; A.dW = dW; A.dS = ds; A.out1 = o1; A.out2 = o2;
+  A.a1dt = a1 * dt;
+  A.c2 = a2 * dt * dt / 2.0;
+  OpKind k;
+  if (mode == HBPDC_JVP_LINEAR) {
+    if (c->pb.equation != HBPDC_ADVECTION) return fail(c, HBPDC_E_ARG, "LINEAR JVP needs a linear flux");
+    k = OP_JVP_LINEAR;
+  } else if (mode == HBPDC_JVP_EXACT) {
+    k = OP_JVP_EXACT;
+  } else {
+    k = OP_JVP_FD;
+    if (eps_override) {
+      A.epsw = eps_override[0];
+    } else {
+      CK(launch_sumsq(dW, n, c->partial, c->stream));
+      CK(launch_finish_fd_eps(c->partial, std::sqrt(EPS_MACH) / c->pb.mach_eps, c->deps, c->stream));
+      A.d_epsw = c->deps;
+    }
+  }
+  ProfScope ps(c, 1);
+  CKS(run_op(c, k, A));
+  if (c->st) c->st->jvp_calls++;
+  return HBPDC_OK;
+}
+
+// ---- BJ_ext ----------------------------------------------------------------------
+hbpdc_status ensure_precond_mem(hbpdc_ctx* c) {
+  if (c->S) return HBPDC_OK;
+  const size_t mm = (size_t)c->m * c->m;
+  c->s_shared = c->pb.equation == HBPDC_ADVECTION ? 1 : 0;
+  const size_t nblk = c->s_shared ? 1 : (size_t)c->nE;
+  CKS(dalloc(c, &c->S, nblk * mm));
+  CKS(dalloc(c, &c->Wb, c->n));
+  CKS(dalloc(c, &c->U, c->n));
+  CKS(dalloc(c, &c->Vv, c->n));
+  // Gauss-Jordan scratch: chunks of at most ~1 GiB
+  size_t chunk = (size_t)(1ull << 30) / (mm * sizeof(double));
+  if (chunk < 1) chunk = 1;
+  if (chunk > nblk) chunk = nblk;
+  c->zchunk = (int)chunk;
+  CKS(dalloc(c, &c->Z, chunk * mm));
+  void* q = nullptr;
+  CK(cudaMalloc(&q, chunk * sizeof(int)));
+  c->allocs.push_back(q);
+  c->info = (int*)q;
+  return HBPDC_OK;
+}
+
+hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, const double* W) {
+  CKS(ensure_precond_mem(c));
+  if (c->pb.equation == HBPDC_NAVIER_STOKES)
+    return fail(c, HBPDC_E_ARG, "BJ_ext build for Navier-Stokes is not implemented yet");
+  ProfScope ps(c, 6);
+  CK(cudaMemcpyAsync(c->Wb, W, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  const size_t mm = (size_t)c->m * c->m;
+  const int nblk = c->s_shared ? 1 : c->nE;
+  std::vector<int> hinfo(c->zchunk);
+  for (int e0 = 0; e0 < nblk; e0 += c->zchunk) {
+    const int ne = std::min(c->zchunk, nblk - e0);
+    CK(cudaMemsetAsync(c->info, 0, ne * sizeof(int), c->stream));
+    CK(launch_kbuild(c->cfg, c->geo, c->Wb, a1 * dt, a2 * dt * dt / 2.0, c->Z, e0, ne));
+    CK(launch_gj_invert(c->Z, c->S + (size_t)e0 * mm, c->m, ne, c->info, c->stream));
+    CK(cudaMemcpyAsync(hinfo.data(), c->info, ne * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b < ne; ++b)
+      if (hinfo[b]) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "BJ_ext block of element %d is singular (dt=%g, a1=%g, a2=%g)", e0 + b, dt, a1,
+                 a2);
+        return fail(c, HBPDC_E_LU_SINGULAR, buf);
+      }
+  }
+  c->pc_a1 = a1; c->pc_a2 = a2; c->pc_dt = dt;
+  c->pc_valid = 1;
+  if (c->st) c->st->precond_builds++;
+  return HBPDC_OK;
+}
+
+hbpdc_status precond_apply_impl(hbpdc_ctx* c, const double* iw, const double* is, double* ow, double* os) {
+  if (!c->pc_valid) return fail(c, HBPDC_E_ARG, "precond_apply before precond_build");
+  {
+    ProfScope ps(c, 0);
+    CK(launch_block_gemv2(c->S, c->s_shared, iw, is, c->U, c->Vv, c->m, c->nE, c->stream));
+  }
+  OpArgs A = base_args(c);
+  A.W = c->Wb; A.U = c->U; A.V = c->Vv; A.out1 = ow; A.out2 = os;
+  A.a1dt = c->pc_a1 * c->pc_dt;
+  A.c2 = c->pc_a2 * c->pc_dt * c->pc_dt / 2.0;
+  ProfScope ps(c, 5);
+  CK(launch_op(OP_KAPPLY, c->cfg, c->geo, A));
+  if (c->st) c->st->precond_applies++;
+  return HBPDC_OK;
+}
+
+// ---- GMRES (right preconditioned, CGS2 Arnoldi, restarted) ----------------------
+struct LinSys {
+  double a1, a2, dt;
+  const double* W;     // linearisation point
+  const double* sg;
+  bool pc;
+};
+
+hbpdc_status apply_JPinv(hbpdc_ctx* c, const LinSys& L, const double* v, double* out, bool use_pc) {
+  const size_t n = c->n;
+  const double* z = v;
+  if (use_pc) {
+    CKS(precond_apply_impl(c, v, v + n, c->zb, c->zb + n));
+    z = c->zb;
+  }
+  return jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr);
+}
+
+// solve J x = rhs (rhs in c->rhs, x -> c->dX); returns iterations
+hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
+  const size_t n2 = 2 * c->n;
+  const int R = c->restart;
+  const double rtol = c->op.gmres_rtol;
+  const int maxit = c->op.krylov_max_per_newton;
+  CK(cudaMemsetAsync(c->dX, 0, n2 * sizeof(double), c->stream));
+  double beta0;
+  CKS(norm_host(c, c->rhs, n2, &beta0));
+  *its_out = 0;
+  if (!(beta0 > 0.0)) return beta0 == 0.0 ? HBPDC_OK : fail(c, HBPDC_E_NONFINITE, "GMRES rhs not finite");
+  // r = rhs (x0 = 0)
+  double* r = c->tmp2;
+  CK(cudaMemcpyAsync(r, c->rhs, n2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  double beta = beta0;
+  int total = 0;
+  bool converged = false;
+  std::vector<double>& H = c->H;
+  while (true) {
+    if (beta <= rtol * beta0) { converged = true; break; }
+    if (total >= maxit) break;
+    // V0 = r / beta
+    c->hpin[0] = beta;
+    CK(cudaMemcpyAsync(c->dnrm, c->hpin, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(launch_scale_by_inv(r, c->dnrm, c->Vk, n2, c->stream));
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(c->gv.begin(), c->gv.end(), 0.0);
+    c->gv[0] = beta;
+    int k = 0;
+    for (int j = 0; j < R; ++j) {
+      double* vj = c->Vk + (size_t)j * n2;
+      double* w = c->Vk + (size_t)(j + 1) * n2;
+      CKS(apply_JPinv(c, L, vj, w, L.pc));
+      // classical Gram-Schmidt, twice (CGS2)
+      {
+        ProfScope ps(c, 3);
+        CK(launch_multidot(c->Vk, n2, j + 1, w, n2, c->partial, c->stream));
+        CK(launch_reduce_partials(c->partial, j + 1, c->dh, 0, c->stream));
+      }
+      {
+        ProfScope ps(c, 4);
+        CK(launch_multiaxpy(c->Vk, n2, j + 1, c->dh, w, n2, nullptr, c->stream));
+      }
+      {
+        ProfScope ps(c, 3);
+        CK(launch_multidot(c->Vk, n2, j + 1, w, n2, c->partial, c->stream));
+        CK(launch_reduce_partials(c->partial, j + 1, c->dh + (R + 1), 0, c->stream));
+      }
+      {
+        ProfScope ps(c, 4);
+        CK(launch_multiaxpy(c->Vk, n2, j + 1, c->dh + (R + 1), w, n2, c->partial + (size_t)(R + 1) * RED_BLOCKS,
+                            c->stream));
+      }
+      CK(launch_finish_norm(c->partial + (size_t)(R + 1) * RED_BLOCKS, c->dnrm, c->stream));
+      CK(launch_scale_by_inv(w, c->dnrm, w, n2, c->stream));
+      // host: h = h1 + h2, hnext
+      CK(cudaMemcpyAsync(c->hpin, c->dh, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(c->hpin + (R + 1), c->dh + (R + 1), (j + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaMemcpyAsync(c->hpin + 2 * (R + 1), c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      double* Hc = &H[(size_t)j * (R + 1)];   // column j, length R+1
+      for (int i = 0; i <= j; ++i) Hc[i] = c->hpin[i] + c->hpin[(R + 1) + i];
+      const double hnext = c->hpin[2 * (R + 1)];
+      if (!std::isfinite(hnext)) return fail(c, HBPDC_E_NONFINITE, "non-finite Arnoldi norm");
+      Hc[j + 1] = hnext;
+      for (int i = 0; i < j; ++i) {
+        const double t = c->cs[i] * Hc[i] + c->sn[i] * Hc[i + 1];
+        Hc[i + 1] = -c->sn[i] * Hc[i] + c->cs[i] * Hc[i + 1];
+        Hc[i] = t;
+      }
+      const double den = std::hypot(Hc[j], Hc[j + 1]);
+      c->cs[j] = Hc[j] / den;
+      c->sn[j] = Hc[j + 1] / den;
+      Hc[j] = den;
+      Hc[j + 1] = 0.0;
+      c->gv[j + 1] = -c->sn[j] * c->gv[j];
+      c->gv[j] = c->cs[j] * c->gv[j];
+      ++total;
+      k = j + 1;
+      if (c->st && k > c->st->max_krylov_j) c->st->max_krylov_j = k;
+      if (std::fabs(c->gv[j + 1]) <= rtol * beta0 || total >= maxit || hnext == 0.0) break;
+    }
+    // y = H^-1 g (back substitution), x += P^-1 (V y)
+    for (int i = k - 1; i >= 0; --i) {
+      double s = c->gv[i];
+      for (int l = i + 1; l < k; ++l) s -= H[(size_t)l * (R + 1) + i] * c->y[l];
+      c->y[i] = s / H[(size_t)i * (R + 1) + i];
+    }
+    for (int i = 0; i < k; ++i) c->hpin[i] = c->y[i];
+    CK(cudaMemcpyAsync(c->dy, c->hpin, k * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(launch_lincomb(c->Vk, n2, k, c->dy, r, n2, c->stream));
+    if (L.pc) {
+      CKS(precond_apply_impl(c, r, r + c->n, c->zb, c->zb + c->n));
+      CK(launch_axpby(1.0, c->zb, 1.0, c->dX, n2, c->stream));
+    } else {
+      CK(launch_axpby(1.0, r, 1.0, c->dX, n2, c->stream));
+    }
+    const bool est_ok = std::fabs(c->gv[k]) <= rtol * beta0;
+    if (est_ok) { converged = true; break; }
+    // true residual r = rhs - J x
+    CKS(jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, c->dX, c->dX + c->n, r, r + c->n, c->op.jvp_mode, nullptr));
+    CK(launch_axpby(1.0, c->rhs, -1.0, r, n2, c->stream));
+    CKS(norm_host(c, r, n2, &beta));
+  }
+  *its_out = total;
+  if (c->st) c->st->gmres_its += total;
+  if (!converged) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "GMRES did not converge within %d iterations", maxit);
+    return fail(c, HBPDC_E_GMRES, buf);
+  }
+  return HBPDC_OK;
+}
+
+// ---- Newton on the extended system (eq:Newton) -------------------------
+// X0 = (W_g, R1(W_g)); the result is in c->X = [W | sigma].
+hbpdc_status newton(hbpdc_ctx* c, double a1, double a2, double dt, const double* b, const double* Wg) {
+  const size_t n = c->n, n2 = 2 * n;
+  double* W = c->X;
+  double* sg = c->X + n;
+  CK(cudaMemcpyAsync(W, Wg, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  {
+    OpArgs A = base_args(c);
+    A.W = W; A.out1 = sg;
+    CKS(run_op(c, OP_R1, A));
+  }
+  double bn;
+  CKS(norm_host(c, b, n, &bn));
+  const double floor = c->op.newton_floor * EPS_MACH * bn;
+  double g0 = -1.0;
+  for (int r = 0; r <= c->op.newton_max; ++r) {
+    {
+      OpArgs A = base_args(c);
+      A.W = W; A.S = sg; A.b = b; A.out1 = c->G; A.out2 = c->G + n;
+      A.a1dt = a1 * dt;
+      A.c2 = a2 * dt * dt / 2.0;
+      ProfScope ps(c, 2);
+      CKS(run_op(c, OP_RESID, A));
+    }
+    double gn;
+    CKS(norm_host(c, c->G, n2, &gn));
+    if (!std::isfinite(gn)) return fail(c, HBPDC_E_NONFINITE, "non-finite Newton residual");
+    if (g0 < 0) g0 = gn;
+    if (c->st) c->st->final_newton_rel = g0 > 0 ? gn / g0 : 0.0;
+    if (gn <= std::max(c->op.newton_rtol * g0, floor)) return HBPDC_OK;
+    if (r == c->op.newton_max) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "Newton did not converge in %d iterations (||G||=%.3e, ||G0||=%.3e)", r, gn, g0);
+      return fail(c, HBPDC_E_NEWTON, buf);
+    }
+    const bool pc = c->op.precond == HBPDC_PC_BJEXT;
+    if (pc && c->op.precond_policy == HBPDC_PC_PER_NEWTON) CKS(precond_build_impl(c, a1, a2, dt, W));
+    CK(launch_axpby(-1.0, c->G, 0.0, c->rhs, n2, c->stream));       // rhs = -G
+    LinSys L{a1, a2, dt, W, sg, pc};
+    int its = 0;
+    CKS(gmres(c, L, &its));
+    CK(launch_axpby(1.0, c->dX, 1.0, c->X, n2, c->stream));         // X += dX
+    if (c->st) c->st->newton_its++;
+    double dwn;
+    CKS(norm_host(c, c->dX, n, &dwn));
+    if (dwn <= c->op.newton_atol_dw) return HBPDC_OK;
+  }
+  return HBPDC_OK;
+}
+
+// R1 and R2(w, R1(w)) of a stage value (reading R6)
+hbpdc_status stage_ops(hbpdc_ctx* c, const double* w, double* r1, double* r2) {
+  OpArgs A = base_args(c);
+  A.W = w; A.out1 = r1;
+  CKS(run_op(c, OP_R1, A));
+  OpArgs B = base_args(c);
+  B.W = w; B.S = r1; B.out1 = nullptr; B.out2 = r2;
+  CKS(run_op(c, OP_R12, B));
+  return HBPDC_OK;
+}
+
+hbpdc_status ensure_pc_for(hbpdc_ctx* c, double a1, double a2, double dt, const double* Wn) {
+  if (c->op.precond != HBPDC_PC_BJEXT || c->op.precond_policy != HBPDC_PC_PER_STEP_PER_ALPHA) return HBPDC_OK;
+  if (c->pc_valid == 2 && c->pc_a1 == a1 && c->pc_a2 == a2 && c->pc_dt == dt) return HBPDC_OK;
+  CKS(precond_build_impl(c, a1, a2, dt, Wn));
+  c->pc_valid = 2;   // built inside this step at W^n
+  return HBPDC_OK;
+}
+
+// Alg. 1: predictor (eq:predictor), k_max corrector sweeps
+// (eq:corrector, with I_l, reading R5), FSAL update.
+hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
+  const size_t n = c->n;
+  const Tableau& T = c->tab;
+  const int s = T.s;
+  int cur = 0;
+  CK(cudaMemcpyAsync(c->Wn, W, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (!c->fsal_valid) CKS(stage_ops(c, c->Wn, c->str1[cur][0], c->str2[cur][0]));
+  c->pc_valid = c->pc_valid ? 1 : 0;   // a build from an earlier step is not at this W^n
+  CK(cudaMemcpyAsync(c->stw[cur][0], c->Wn, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  // ---- predictor (eq:nonlinear_predictor)
+  for (int l = 1; l < s; ++l) {
+    const double dc = T.c[l] - T.c[l - 1];
+    const double a1 = dc / 2.0, a2 = dc * dc / 6.0, c2 = a2 * dt * dt / 2.0;
+    const double* X[2] = {c->str1[cur][l - 1], c->str2[cur][l - 1]};
+    const double co[2] = {a1 * dt, c2};
+    CK(launch_stage_combo(c->stw[cur][l - 1], 2, X, co, 0, nullptr, nullptr, c->bvec, n, c->stream));
+    CKS(ensure_pc_for(c, a1, a2, dt, c->Wn));
+    hbpdc_status stt = newton(c, a1, a2, dt, c->bvec, c->stw[cur][l - 1]);
+    if (stt != HBPDC_OK) {
+      c->err = "predictor stage " + std::to_string(l + 1) + ": " + c->err;
+      return stt;
+    }
+    if (c->st) c->st->stage_solves++;
+    CK(cudaMemcpyAsync(c->stw[cur][l], c->X, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CKS(stage_ops(c, c->stw[cur][l], c->str1[cur][l], c->str2[cur][l]));
+  }
+  // ---- correctors (eq:nonlinear_corrector)
+  for (int k = 0; k < c->pb.kmax; ++k) {
+    const int nxt = 1 - cur;
+    // stage 1 of the new sweep is W^n with the FSAL operators
+    CK(cudaMemcpyAsync(c->stw[nxt][0], c->stw[cur][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->str1[nxt][0], c->str1[cur][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->str2[nxt][0], c->str2[cur][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    for (int l = 1; l < s; ++l) {
+      // b = W^n - dt R1_l + dt^2/2 R2_l + dt sum_j B1_lj R1_j + dt^2 sum_j B2_lj R2_j
+      const double* X[4];
+      const double* Y[4];
+      double a[4], bb[4];
+      for (int j = 0; j < s; ++j) {
+        X[j] = c->str1[cur][j];
+        Y[j] = c->str2[cur][j];
+        a[j] = dt * T.B1[l][j] - (j == l ? dt : 0.0);
+        bb[j] = dt * dt * T.B2[l][j] + (j == l ? dt * dt / 2.0 : 0.0);
+      }
+      CK(launch_stage_combo(c->Wn, s, X, a, s, Y, bb, c->bvec, n, c->stream));
+      CKS(ensure_pc_for(c, 1.0, 1.0, dt, c->Wn));
+      hbpdc_status stt = newton(c, 1.0, 1.0, dt, c->bvec, c->stw[cur][l]);
+      if (stt != HBPDC_OK) {
+        c->err = "corrector sweep " + std::to_string(k + 1) + " stage " + std::to_string(l + 1) + ": " + c->err;
+        return stt;
+      }
+      if (c->st) c->st->stage_solves++;
+      CK(cudaMemcpyAsync(c->stw[nxt][l], c->X, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      CKS(stage_ops(c, c->stw[nxt][l], c->str1[nxt][l], c->str2[nxt][l]));
+    }
+    cur = nxt;
+  }
+  // ---- update / FSAL
+  CK(cudaMemcpyAsync(W, c->stw[cur][s - 1], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (cur != 0) {
+    CK(cudaMemcpyAsync(c->str1[0][0], c->str1[cur][s - 1], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->str2[0][0], c->str2[cur][s - 1], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(c->str1[0][0], c->str1[0][s - 1], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->str2[0][0], c->str2[0][s - 1], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  c->fsal_valid = 1;
+  if (c->pc_valid == 2) c->pc_valid = 1;
+  return HBPDC_OK;
+}
+
+hbpdc_status alloc_solver(hbpdc_ctx* c) {
+  const size_t n = c->n, n2 = 2 * n;
+  const int R = c->restart;
+  CKS(dalloc(c, &c->X, n2));
+  CKS(dalloc(c, &c->G, n2));
+  CKS(dalloc(c, &c->dX, n2));
+  CKS(dalloc(c, &c->rhs, n2));
+  CKS(dalloc(c, &c->tmp2, n2));
+  CKS(dalloc(c, &c->zb, n2));
+  CKS(dalloc(c, &c->Vk, (size_t)(R + 1) * n2));
+  CKS(dalloc(c, &c->partial, (size_t)(R + 2) * RED_BLOCKS));
+  CKS(dalloc(c, &c->dh, 2 * (size_t)(R + 1)));
+  CKS(dalloc(c, &c->dnrm, 1));
+  CKS(dalloc(c, &c->deps, 1));
+  CKS(dalloc(c, &c->dy, (size_t)R + 1));
+  CKS(dalloc(c, &c->Wn, n));
+  CKS(dalloc(c, &c->bvec, n));
+  for (int sw = 0; sw < 2; ++sw)
+    for (int l = 0; l < c->tab.s; ++l) {
+      CKS(dalloc(c, &c->stw[sw][l], n));
+      CKS(dalloc(c, &c->str1[sw][l], n));
+      CKS(dalloc(c, &c->str2[sw][l], n));
+    }
+  if (c->pb.equation == HBPDC_NAVIER_STOKES) {
+    const size_t lg = (size_t)c->nE * 6 * 4 * c->nodes;
+    CKS(dalloc(c, &c->lift0, lg));
+    CKS(dalloc(c, &c->lift1, lg));
+  }
+  c->H.assign((size_t)R * (R + 1), 0.0);
+  c->cs.assign(R + 1, 0.0);
+  c->sn.assign(R + 1, 0.0);
+  c->gv.assign(R + 2, 0.0);
+  c->y.assign(R + 1, 0.0);
+  void* hp = nullptr;
+  CK(cudaMallocHost(&hp, (3 * (size_t)(R + 1) + 8) * sizeof(double)));
+  c->hpin = (double*)hp;
+  return HBPDC_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C-ABI
+// =====================================================================================
+extern "C" {
+
+hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, const hbpdc_dist* ds,
+                        hbpdc_ctx** out) {
+  if (!pb || !op || !out) return HBPDC_E_ARG;
+  *out = nullptr;
+  hbpdc_ctx* c = new hbpdc_ctx();
+  c->pb = *pb;
+  c->op = *op;
+  if (ds) c->ds = *ds;
+  else { c->ds.rank = 0; c->ds.nranks = 1; c->ds.px = 1; c->ds.py = 1; }
+  auto bad = [&](const char* msg) {
+    c->err = msg;
+    *out = c;   // return the context so the caller can read the message
+    return HBPDC_E_ARG;
+  };
+  if (pb->dim != 1 && pb->dim != 2) return bad("dim must be 1 or 2");
+  if (pb->equation < 0 || pb->equation > 2) return bad("unknown equation");
+  if (pb->equation != HBPDC_ADVECTION && pb->dim != 2) return bad("Euler/NS need dim = 2");
+  if (pb->N < 1 || pb->N > 7) return bad("N must be in 1..7");
+  if (pb->nodes != HBPDC_GLL) return bad("only Gauss-Lobatto nodes are implemented on the GPU (reading R1)");
+  if (pb->flux != HBPDC_LLF) return bad("only the LLF flux is implemented (reading R3)");
+  if (pb->equation != HBPDC_ADVECTION && pb->mach_eps != 1.0) return bad("mach_eps must be 1 (reading R18)");
+  if (pb->q != 4 && pb->q != 6 && pb->q != 8) return bad("q must be 4, 6 or 8");
+  if (pb->kmax < 0) return bad("kmax must be >= 0");
+  if (pb->nx < 1 || (pb->dim == 2 && pb->ny < 1)) return bad("element counts must be positive");
+  if (c->ds.nranks != 1) return bad("multi-rank execution is not implemented yet");
+  if (op->gmres_restart < 1 || op->krylov_max_per_newton < 1 || op->newton_max < 0) return bad("bad solver options");
+  c->nv = pb->equation == HBPDC_ADVECTION ? 1 : 4;
+  c->P = pb->N + 1;
+  c->nodes = pb->dim == 2 ? c->P * c->P : c->P;
+  c->m = c->nv * c->nodes;
+  c->nxl = pb->nx;
+  c->nyl = pb->dim == 2 ? pb->ny : 1;
+  c->nE = c->nxl * c->nyl;
+  c->n = (size_t)c->nE * c->m;
+  c->restart = op->gmres_restart;
+  c->tab = tableau(pb->q);
+  c->basis = hbpdc::gll_basis(pb->N);
+  // geometry: Cartesian, J = dx dy / 4, s-hat = dy/2, dx/2 -> scale 2/dx, 2/dy
+  const double dx = (pb->xmax - pb->xmin) / pb->nx;
+  const double dy = pb->dim == 2 ? (pb->ymax - pb->ymin) / pb->ny : 1.0;
+  c->geo.nx = c->nxl;
+  c->geo.ny = c->nyl;
+  c->geo.nE = c->nE;
+  c->geo.sx = 2.0 / dx;
+  c->geo.sy = 2.0 / dy;
+  c->geo.lhp = c->basis.lhp;
+  c->geo.lhm = c->basis.lhm;
+  for (int i = 0; i < c->P * c->P; ++i) c->geo.Dh[i] = c->basis.Dhat[i];
+  c->cfg.eq = pb->equation;
+  c->cfg.dim = pb->dim;
+  c->cfg.P = c->P;
+  c->cfg.pp.ax = pb->a[0];
+  c->cfg.pp.ay = pb->a[1];
+  c->cfg.pp.gamma = pb->gamma;
+  c->cfg.pp.mu = pb->mu;
+  c->cfg.pp.Rgas = 1.0 / pb->gamma;
+  c->cfg.pp.lamT = (c->cfg.pp.Rgas * pb->gamma / (pb->gamma - 1.0)) * pb->mu / (pb->prandtl > 0 ? pb->prandtl : 1.0);
+  cudaError_t e = cudaSetDevice(c->ds.device);
+  if (e != cudaSuccess) { c->err = cudaGetErrorString(e); *out = c; return HBPDC_E_CUDA; }
+  if (c->ds.cuda_stream) {
+    c->stream = (cudaStream_t)c->ds.cuda_stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { c->err = cudaGetErrorString(e); *out = c; return HBPDC_E_CUDA; }
+    c->own_stream = true;
+  }
+  c->cfg.stream = c->stream;
+  hbpdc_status s = alloc_solver(c);
+  *out = c;
+  return s;
+}
+
+hbpdc_status hbpdc_local_shape(const hbpdc_ctx* c, int* nle, int* m, int* ex0, int* ey0, int* nxl, int* nyl) {
+  if (!c) return HBPDC_E_ARG;
+  if (nle) *nle = c->nE;
+  if (m) *m = c->m;
+  if (ex0) *ex0 = c->ex0;
+  if (ey0) *ey0 = c->ey0;
+  if (nxl) *nxl = c->nxl;
+  if (nyl) *nyl = c->nyl;
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_node_coords(const hbpdc_ctx* c, double* xh, double* yh) {
+  if (!c || !xh) return HBPDC_E_ARG;
+  const auto& pb = c->pb;
+  const double dx = (pb.xmax - pb.xmin) / pb.nx;
+  const double dy = pb.dim == 2 ? (pb.ymax - pb.ymin) / pb.ny : 0.0;
+  const int P = c->P;
+  for (int e = 0; e < c->nE; ++e) {
+    const int ex = c->ex0 + e % c->nxl, ey = c->ey0 + e / c->nxl;
+    for (int nd = 0; nd < c->nodes; ++nd) {
+      const int i = nd % P, j = nd / P;
+      xh[(size_t)e * c->nodes + nd] = pb.xmin + ex * dx + (c->basis.xi[i] + 1.0) * dx / 2;
+      if (pb.dim == 2 && yh) yh[(size_t)e * c->nodes + nd] = pb.ymin + ey * dy + (c->basis.xi[j] + 1.0) * dy / 2;
+    }
+  }
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_rhs(hbpdc_ctx* c, const double* W, const double* sigma, double* out) {
+  if (!c || !W || !out) return HBPDC_E_ARG;
+  OpArgs A = base_args(c);
+  A.W = W;
+  if (!sigma) {
+    A.out1 = out;
+    return run_op(c, OP_R1, A);
+  }
+  A.S = sigma;
+  A.out1 = nullptr;
+  A.out2 = out;
+  return run_op(c, OP_R12, A);
+}
+
+hbpdc_status hbpdc_residual(hbpdc_ctx* c, double a1, double a2, double dt, const double* b, const double* W,
+                            const double* sigma, double* G1, double* G2, double* norm_out) {
+  if (!c || !b || !W || !sigma || !G1 || !G2) return HBPDC_E_ARG;
+  OpArgs A = base_args(c);
+  A.W = W; A.S = sigma; A.b = b; A.out1 = G1; A.out2 = G2;
+  A.a1dt = a1 * dt;
+  A.c2 = a2 * dt * dt / 2.0;
+  {
+    ProfScope ps(c, 2);
+    CKS(run_op(c, OP_RESID, A));
+  }
+  if (norm_out) {
+    double s1, s2;
+    CKS(norm_host(c, G1, c->n, &s1));
+    CKS(norm_host(c, G2, c->n, &s2));
+    *norm_out = std::sqrt(s1 * s1 + s2 * s2);
+  }
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_jvp(hbpdc_ctx* c, double a1, double a2, double dt, const double* W, const double* sigma,
+                       const double* dW, const double* dsigma, double* out1, double* out2, int mode,
+                       const double* eps_override) {
+  if (!c || !dW || !dsigma || !out1 || !out2) return HBPDC_E_ARG;
+  const int k = jvp_kind(c, mode);
+  if (k != HBPDC_JVP_LINEAR && (!W || !sigma)) return HBPDC_E_ARG;
+  return jvp_impl(c, a1, a2, dt, W, sigma, dW, dsigma, out1, out2, mode, eps_override);
+}
+
+hbpdc_status hbpdc_precond_build(hbpdc_ctx* c, double a1, double a2, double dt, const double* W) {
+  if (!c || !W) return HBPDC_E_ARG;
+  return precond_build_impl(c, a1, a2, dt, W);
+}
+
+hbpdc_status hbpdc_precond_set(hbpdc_ctx* c, double a1, double a2, double dt, const double* W, const double* S,
+                               int shared) {
+  if (!c || !W || !S) return HBPDC_E_ARG;
+  CKS(ensure_precond_mem(c));
+  if (shared != c->s_shared) return fail(c, HBPDC_E_ARG, "shared flag does not match the equation");
+  const size_t nblk = c->s_shared ? 1 : (size_t)c->nE;
+  CK(cudaMemcpyAsync(c->S, S, nblk * c->m * c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->Wb, W, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  c->pc_a1 = a1; c->pc_a2 = a2; c->pc_dt = dt;
+  c->pc_valid = 1;
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_precond_export(hbpdc_ctx* c, double* S_out, int* shared) {
+  if (!c || !S_out) return HBPDC_E_ARG;
+  if (!c->pc_valid) return fail(c, HBPDC_E_ARG, "no preconditioner built");
+  const size_t nblk = c->s_shared ? 1 : (size_t)c->nE;
+  CK(cudaMemcpyAsync(S_out, c->S, nblk * c->m * c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (shared) *shared = c->s_shared;
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_precond_apply(hbpdc_ctx* c, const double* iw, const double* is, double* ow, double* os) {
+  if (!c || !iw || !is || !ow || !os) return HBPDC_E_ARG;
+  return precond_apply_impl(c, iw, is, ow, os);
+}
+
+hbpdc_status hbpdc_step(hbpdc_ctx* c, double dt, double* W, hbpdc_step_stats* stats) {
+  if (!c || !W || !(dt >= 0.0)) return HBPDC_E_ARG;
+  hbpdc_step_stats local{};
+  c->st = &local;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  cudaEventRecord(t0, c->stream);
+  hbpdc_status s = step_impl(c, dt, W);
+  cudaEventRecord(t1, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  local.wall_s = ms * 1e-3;
+  c->st = nullptr;
+  if (stats) *stats = local;
+  prof_flush(c);
+  if (s == HBPDC_OK && e != cudaSuccess) {
+    c->err = cudaGetErrorString(e);
+    return HBPDC_E_CUDA;
+  }
+  return s;
+}
+
+hbpdc_status hbpdc_step_host(hbpdc_ctx* c, double dt, double* W_host, hbpdc_step_stats* stats) {
+  if (!c || !W_host) return HBPDC_E_ARG;
+  if (!c->Wio) CKS(dalloc(c, &c->Wio, c->n));
+  CK(cudaMemcpyAsync(c->Wio, W_host, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  hbpdc_status s = hbpdc_step(c, dt, c->Wio, stats);
+  if (s == HBPDC_OK) {
+    CK(cudaMemcpyAsync(W_host, c->Wio, c->n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return s;
+}
+
+hbpdc_status hbpdc_reset(hbpdc_ctx* c) {
+  if (!c) return HBPDC_E_ARG;
+  c->fsal_valid = 0;
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_profile(hbpdc_ctx* c, int enable) {
+  if (!c) return HBPDC_E_ARG;
+  prof_flush(c);
+  c->prof_on = enable ? 1 : 0;
+  if (enable) {
+    for (int i = 0; i < NPROF; ++i) { c->prof_launch[i] = 0; c->prof_ms[i] = 0.0; }
+  }
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_profile_read(hbpdc_ctx* c, int id, long long* launches, double* total_ms) {
+  if (!c || id < 0 || id >= NPROF) return HBPDC_E_ARG;
+  prof_flush(c);
+  if (launches) *launches = c->prof_launch[id];
+  if (total_ms) *total_ms = c->prof_ms[id];
+  return HBPDC_OK;
+}
+
+const char* hbpdc_last_error(const hbpdc_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void hbpdc_finalize(hbpdc_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  prof_flush(c);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// launch.h -- host-side entry points of the device kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include "physics.cuh"
+
+struct Geo;
+struct OpArgs;
+
+enum OpKind { OP_R1 = 0, OP_R12, OP_RESID, OP_JVP_EXACT, OP_JVP_FD, OP_JVP_LINEAR, OP_KAPPLY, OP_NKINDS };
+
+struct OpCfg {
+  int eq, dim, P;
+  PhysParams pp;
+  cudaStream_t stream;
+};
+
+// fused element operator (modes.cuh); NS modes need lift buffers in A.G0/G1
+cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
+// BR1 lifting of jet state `state` of operator `kind` into Gout
+cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout);
+// number of jet components of the lifted gradients of (kind, state)
+int lift_jet_components(OpKind kind, int state);
+// BJ_ext: M_i = I - a1dt K_i + c2 K_i^2 for elements [e0, e0+ne), row-major m x m each
+cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, double a1dt, double c2,
+                          double* M, int e0, int ne);
+
+// ---- linalg.cu -----------------------------------------------------------------
+// in-place Gauss-Jordan inversion with partial pivoting of `nmat` m x m
+// row-major matrices in Z (scratch), result unpermuted into S; info[b] != 0
+// flags a zero pivot in matrix b.
+cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, cudaStream_t st);
+// U_e = S_e W_e, V_e = S_e sig_e for every element (S stride 0 if shared)
+cudaError_t launch_block_gemv2(const double* S, int shared, const double* W, const double* sig,
+                               double* U, double* V, int m, int nE, cudaStream_t st);
+
+// GMRES / Newton vector kernels.  Reductions are two-level (fixed block
+// count, fixed order): deterministic.
+constexpr int RED_BLOCKS = 592;         // 4 x 148 SMs
+constexpr int RED_THREADS = 256;
+// partial[k * RED_BLOCKS + b] = sum over block b of X_k . y   (k < nk), X_k = X + k*ldx
+cudaError_t launch_multidot(const double* X, size_t ldx, int nk, const double* y, size_t L,
+                            double* partial, cudaStream_t st);
+// out[k] = sum_b partial[k * RED_BLOCKS + b] (+ out[k] if accumulate), k < nk
+cudaError_t launch_reduce_partials(const double* partial, int nk, double* out, int accumulate, cudaStream_t st);
+// y -= sum_k h[k] X_k  (h on device); if sq_partial != NULL also partial sums of y_new^2
+cudaError_t launch_multiaxpy(const double* X, size_t ldx, int nk, const double* h, double* y, size_t L,
+                             double* sq_partial, cudaStream_t st);
+// y = sum_k c[k] X_k  (c on device)
+cudaError_t launch_lincomb(const double* X, size_t ldx, int nk, const double* c, double* y, size_t L,
+                           cudaStream_t st);
+// y = x * (1 / *nrm)  (nrm on device; nrm == 0 -> y = 0)
+cudaError_t launch_scale_by_inv(const double* x, const double* nrm, double* y, size_t L, cudaStream_t st);
+// y = a x + b y   (host scalars)
+cudaError_t launch_axpby(double a, const double* x, double b, double* y, size_t L, cudaStream_t st);
+// y = a x + b z   (host scalars)
+cudaError_t launch_waxpby(double a, const double* x, double b, const double* z, double* y, size_t L,
+                          cudaStream_t st);
+// partial sums of x.x (sumsq) into partial[0..RED_BLOCKS)
+cudaError_t launch_sumsq(const double* x, size_t L, double* partial, cudaStream_t st);
+// out = sqrt(sum partial)
+cudaError_t launch_finish_norm(const double* partial, double* out, cudaStream_t st);
+// out = c / sqrt(sum partial), or 0 if the sum is 0   (FD step)
+cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st);
+// HBPC quadrature: y = base + sum_j a[j] X_j + sum_j b[j] Y_j  (host coefficient arrays, <= 8 terms)
+cudaError_t launch_stage_combo(const double* base, int nx, const double* const* X, const double* a,
+                               int ny, const double* const* Y, const double* b, double* y, size_t L,
+                               cudaStream_t st);

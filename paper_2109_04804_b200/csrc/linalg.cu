@@ -1,0 +1,484 @@
+// linalg.cu -- BJ_ext block inversion and application, GMRES/Newton vector ops.
+#include <cstdint>
+#include "launch.h"
+
+// ============================================================================
+// Batched Gauss-Jordan inversion with partial pivoting ("we calculate
+// those inverses via LU-decomposition"; any pivoted elimination gives the same
+// inverse up to rounding).  One CTA per m x m matrix (m <= 256), matrix in
+// global memory (L2-resident while its CTA runs).
+//
+// Blocked in-place GJ with implicit pivoting: panel of NB columns is
+// eliminated in shared memory (pivot search over rows not yet used), which
+// yields U = E_panel[:, P] - I[:, P]; every other column j then receives the
+// rank-NB update A[:, j] += U A[P, j].  The stored matrix Z satisfies
+// A^-1[a][b] = Z[p_a][q_b] with p_a the pivot row of column a and q_b the
+// column whose pivot row is b; the final pass writes that into S.
+// ============================================================================
+namespace {
+constexpr int GJ_T = 256;    // threads
+constexpr int GJ_NB = 16;    // panel width
+constexpr int GJ_TW = 64;    // column tile of the rank-NB update
+constexpr int GJ_MMAX = 256;
+}
+
+__global__ void __launch_bounds__(GJ_T) gj_kernel(double* __restrict__ Zall, double* __restrict__ Sall, int m,
+                                                   int* __restrict__ info) {
+  __shared__ double Pn[GJ_MMAX * GJ_NB];
+  __shared__ double AP[GJ_NB * GJ_TW];
+  __shared__ int piv[GJ_MMAX];      // pivot row of column c
+  __shared__ int colof[GJ_MMAX];    // column whose pivot row is r (-1: unused)
+  __shared__ double redv[GJ_T / 32];
+  __shared__ int redi[GJ_T / 32];
+  __shared__ int s_prow;
+  __shared__ double s_pval;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* A = Zall + (size_t)blockIdx.x * m * m;
+  double* S = Sall + (size_t)blockIdx.x * m * m;
+  for (int r = tid; r < m; r += GJ_T) colof[r] = -1;
+  int singular = 0;
+  __syncthreads();
+
+  for (int c0 = 0; c0 < m; c0 += GJ_NB) {
+    const int nb = min(GJ_NB, m - c0);
+    for (int idx = tid; idx < m * nb; idx += GJ_T) {
+      const int r = idx / nb, k = idx % nb;
+      Pn[r * GJ_NB + k] = A[(size_t)r * m + c0 + k];
+    }
+    __syncthreads();
+    for (int k = 0; k < nb; ++k) {
+      // ---- pivot search: max |Pn[r][k]| over unused rows (ties: smallest r)
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int r = tid; r < m; r += GJ_T) {
+        if (colof[r] < 0) {
+          const double a = fabs(Pn[r * GJ_NB + k]);
+          if (a > best || (a == best && r < bi)) { best = a; bi = r; }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) { redv[wid] = best; redi[wid] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        best = redv[0]; bi = redi[0];
+        for (int w = 1; w < GJ_T / 32; ++w)
+          if (redv[w] > best || (redv[w] == best && redi[w] < bi)) { best = redv[w]; bi = redi[w]; }
+        double pv = Pn[bi * GJ_NB + k];
+        if (!(best > 0.0)) pv = 1.0;                    // singular: flagged below
+        s_prow = bi; s_pval = pv;
+        colof[bi] = c0 + k;
+        piv[c0 + k] = bi;
+        if (!(best > 0.0)) redi[0] = -1;
+      }
+      __syncthreads();
+      if (redi[0] == -1) singular = 1;
+      const int prow = s_prow;
+      const double pval = s_pval;
+      // ---- in-place GJ step on the panel columns
+      double pr[GJ_NB];
+#pragma unroll
+      for (int j = 0; j < GJ_NB; ++j) pr[j] = j < nb ? Pn[prow * GJ_NB + j] / pval : 0.0;
+      double f[(GJ_MMAX + GJ_T - 1) / GJ_T];
+#pragma unroll
+      for (int q = 0; q < (GJ_MMAX + GJ_T - 1) / GJ_T; ++q) {
+        const int r = tid + q * GJ_T;
+        f[q] = r < m ? Pn[r * GJ_NB + k] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < (GJ_MMAX + GJ_T - 1) / GJ_T; ++q) {
+        const int r = tid + q * GJ_T;
+        if (r >= m) continue;
+        double* row = Pn + r * GJ_NB;
+        if (r == prow) {
+          for (int j = 0; j < nb; ++j) row[j] = j == k ? 1.0 / pval : pr[j];
+        } else {
+          const double fr = f[q];
+          for (int j = 0; j < nb; ++j) row[j] = j == k ? -fr / pval : fma(-fr, pr[j], row[j]);
+        }
+      }
+      __syncthreads();
+    }
+    // ---- store the panel (augmented columns E[:, P]) and form U = Pn - I[:, P]
+    for (int idx = tid; idx < m * nb; idx += GJ_T) {
+      const int r = idx / nb, k = idx % nb;
+      const double v = Pn[r * GJ_NB + k];
+      A[(size_t)r * m + c0 + k] = v;
+    }
+    __syncthreads();
+    for (int k = tid; k < nb; k += GJ_T) Pn[piv[c0 + k] * GJ_NB + k] -= 1.0;
+    __syncthreads();
+    // ---- rank-nb update of every other column: A[:, j] += U A[P, j]
+    const int cg = tid % 16, rg = tid / 16;          // 4 columns x (m/16) rows per thread
+    for (int t0 = 0; t0 < m; t0 += GJ_TW) {
+      for (int idx = tid; idx < nb * GJ_TW; idx += GJ_T) {
+        const int k = idx / GJ_TW, jj = idx % GJ_TW;
+        const int col = t0 + jj;
+        AP[k * GJ_TW + jj] = col < m ? A[(size_t)piv[c0 + k] * m + col] : 0.0;
+      }
+      __syncthreads();
+      constexpr int RQ = GJ_MMAX / 16;
+      double acc[RQ][4];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        const int r = rg + 16 * q;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int col = t0 + cg * 4 + cc;
+          acc[q][cc] = (r < m && col < m) ? A[(size_t)r * m + col] : 0.0;
+        }
+      }
+      for (int k = 0; k < nb; ++k) {
+        double ap[4];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) ap[cc] = AP[k * GJ_TW + cg * 4 + cc];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const int r = rg + 16 * q;
+          const double u = r < m ? Pn[r * GJ_NB + k] : 0.0;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) acc[q][cc] = fma(u, ap[cc], acc[q][cc]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        const int r = rg + 16 * q;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int col = t0 + cg * 4 + cc;
+          if (r < m && col < m && (col < c0 || col >= c0 + nb)) A[(size_t)r * m + col] = acc[q][cc];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- unpermute: S[a][b] = Z[piv[a]][colof[b]]
+  for (int a = wid; a < m; a += GJ_T / 32) {
+    const double* zr = A + (size_t)piv[a] * m;
+    for (int b = lane; b < m; b += 32) S[(size_t)a * m + b] = zr[colof[b]];
+  }
+  if (singular && tid == 0) info[blockIdx.x] = 1;
+}
+
+cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, cudaStream_t st) {
+  if (m > GJ_MMAX || m < 1) return cudaErrorInvalidValue;
+  if (nmat <= 0) return cudaSuccess;
+  gj_kernel<<<nmat, GJ_T, 0, st>>>(Z, S, m, info);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// BJ_ext application, streaming half: U_e = S_e W_e, V_e = S_e sigma_e.
+// One CTA (8 warps) per element; each warp takes 4 rows at a time, lane l
+// reads columns l, l+32, ... (coalesced 256-B segments of a row), keeps the
+// matching W/sigma entries in registers, and reduces 8 partial sums across
+// the warp with a butterfly that halves the payload at each stage.
+// S is read exactly once: this is the HBM-bound kernel (8 m^2 B / element).
+// ============================================================================
+template <int CPL>
+__global__ void __launch_bounds__(256) gemv2_kernel(const double* __restrict__ S, int shared,
+                                                    const double* __restrict__ W, const double* __restrict__ sg,
+                                                    double* __restrict__ U, double* __restrict__ V, int m, int nE) {
+  const int e = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double* Se = S + (shared ? 0 : (size_t)e * m * m);
+  const double* we = W + (size_t)e * m;
+  const double* se = sg + (size_t)e * m;
+  double wr[CPL], sr[CPL];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    const int c = lane + 32 * q;
+    wr[q] = c < m ? we[c] : 0.0;
+    sr[q] = c < m ? se[c] : 0.0;
+  }
+  for (int r0 = wid * 4; r0 < m; r0 += 32) {
+    double p[8];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int r = r0 + rr;
+      double a = 0.0, b = 0.0;
+      if (r < m) {
+        const double* row = Se + (size_t)r * m;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const int c = lane + 32 * q;
+          const double s = c < m ? __ldg(row + c) : 0.0;
+          a = fma(s, wr[q], a);
+          b = fma(s, sr[q], b);
+        }
+      }
+      p[2 * rr] = a;
+      p[2 * rr + 1] = b;
+    }
+    // butterfly: 8 values over 32 lanes -> value (lane >> 2) & 7 complete in lanes
+    {
+      const bool hi = lane & 16;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const double send = hi ? p[t] : p[t + 4];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, 16);
+        p[t] = (hi ? p[t + 4] : p[t]) + recv;
+      }
+    }
+    {
+      const bool hi = lane & 8;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const double send = hi ? p[t] : p[t + 2];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, 8);
+        p[t] = (hi ? p[t + 2] : p[t]) + recv;
+      }
+    }
+    {
+      const bool hi = lane & 4;
+      const double send = hi ? p[0] : p[1];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, 4);
+      p[0] = (hi ? p[1] : p[0]) + recv;
+    }
+    p[0] += __shfl_xor_sync(0xffffffffu, p[0], 2);
+    p[0] += __shfl_xor_sync(0xffffffffu, p[0], 1);
+    // lane bits (4,3,2) select the value index: idx = 4*b4 + 2*b3 + b2
+    if ((lane & 3) == 0) {
+      const int idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      const int r = r0 + (idx >> 1);
+      if (r < m) {
+        if (idx & 1) V[(size_t)e * m + r] = p[0];
+        else U[(size_t)e * m + r] = p[0];
+      }
+    }
+  }
+}
+
+cudaError_t launch_block_gemv2(const double* S, int shared, const double* W, const double* sig, double* U,
+                               double* V, int m, int nE, cudaStream_t st) {
+  if (nE <= 0) return cudaSuccess;
+  const int cpl = (m + 31) / 32;
+#define G(C) case C: gemv2_kernel<C><<<nE, 256, 0, st>>>(S, shared, W, sig, U, V, m, nE); break;
+  switch (cpl) {
+    G(1) G(2) G(3) G(4) G(5) G(6) G(7) G(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef G
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Vector kernels (deterministic two-level reductions: RED_BLOCKS x RED_THREADS)
+// ============================================================================
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < RED_THREADS / 32; ++w) s += sh[w];
+  }
+  __syncthreads();
+  return s;   // valid in thread 0
+}
+
+// partial[k][b] for k in [k0, k0 + KB)
+template <int KB>
+__global__ void __launch_bounds__(RED_THREADS) multidot_kernel(const double* __restrict__ X, size_t ldx, int k0,
+                                                               int nk, const double* __restrict__ y, size_t L,
+                                                               double* __restrict__ partial) {
+  __shared__ double sh[RED_THREADS / 32];
+  double acc[KB];
+#pragma unroll
+  for (int q = 0; q < KB; ++q) acc[q] = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) {
+    const double yi = y[i];
+#pragma unroll
+    for (int q = 0; q < KB; ++q)
+      if (k0 + q < nk) acc[q] = fma(X[(size_t)(k0 + q) * ldx + i], yi, acc[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < KB; ++q) {
+    if (k0 + q >= nk) break;
+    const double s = block_sum(acc[q], sh);
+    if (threadIdx.x == 0) partial[(size_t)(k0 + q) * RED_BLOCKS + blockIdx.x] = s;
+  }
+}
+
+cudaError_t launch_multidot(const double* X, size_t ldx, int nk, const double* y, size_t L, double* partial,
+                            cudaStream_t st) {
+  for (int k0 = 0; k0 < nk; k0 += 8) {
+    multidot_kernel<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(X, ldx, k0, nk, y, L, partial);
+  }
+  return cudaGetLastError();
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int nk, double* out, int accumulate) {
+  __shared__ double sh[RED_THREADS / 32];
+  const int k = blockIdx.x;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < RED_BLOCKS; b += RED_THREADS) v += partial[(size_t)k * RED_BLOCKS + b];
+  const double s = block_sum(v, sh);
+  if (threadIdx.x == 0) out[k] = accumulate ? out[k] + s : s;
+}
+
+cudaError_t launch_reduce_partials(const double* partial, int nk, double* out, int accumulate, cudaStream_t st) {
+  if (nk <= 0) return cudaSuccess;
+  reduce_partials_kernel<<<nk, RED_THREADS, 0, st>>>(partial, nk, out, accumulate);
+  return cudaGetLastError();
+}
+
+// y -= sum_k h[k] X_k, optionally with partial sums of y^2
+__global__ void __launch_bounds__(RED_THREADS) multiaxpy_kernel(const double* __restrict__ X, size_t ldx, int nk,
+                                                                const double* __restrict__ h, double* __restrict__ y,
+                                                                size_t L, double* __restrict__ sq) {
+  __shared__ double sh[RED_THREADS / 32];
+  __shared__ double hs[1024];
+  for (int k = threadIdx.x; k < nk && k < 1024; k += blockDim.x) hs[k] = h[k];
+  __syncthreads();
+  double ss = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) {
+    double v = y[i];
+    for (int k = 0; k < nk; ++k) v = fma(-(k < 1024 ? hs[k] : h[k]), X[(size_t)k * ldx + i], v);
+    y[i] = v;
+    ss = fma(v, v, ss);
+  }
+  if (sq) {
+    const double s = block_sum(ss, sh);
+    if (threadIdx.x == 0) sq[blockIdx.x] = s;
+  }
+}
+
+cudaError_t launch_multiaxpy(const double* X, size_t ldx, int nk, const double* h, double* y, size_t L,
+                             double* sq_partial, cudaStream_t st) {
+  multiaxpy_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(X, ldx, nk, h, y, L, sq_partial);
+  return cudaGetLastError();
+}
+
+__global__ void lincomb_kernel(const double* __restrict__ X, size_t ldx, int nk, const double* __restrict__ c,
+                               double* __restrict__ y, size_t L) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) {
+    double v = 0.0;
+    for (int k = 0; k < nk; ++k) v = fma(c[k], X[(size_t)k * ldx + i], v);
+    y[i] = v;
+  }
+}
+
+cudaError_t launch_lincomb(const double* X, size_t ldx, int nk, const double* c, double* y, size_t L,
+                           cudaStream_t st) {
+  lincomb_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(X, ldx, nk, c, y, L);
+  return cudaGetLastError();
+}
+
+__global__ void scale_inv_kernel(const double* __restrict__ x, const double* __restrict__ nrm, double* __restrict__ y,
+                                 size_t L) {
+  const double n = *nrm;
+  const double s = n > 0.0 ? 1.0 / n : 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) y[i] = x[i] * s;
+}
+
+cudaError_t launch_scale_by_inv(const double* x, const double* nrm, double* y, size_t L, cudaStream_t st) {
+  scale_inv_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(x, nrm, y, L);
+  return cudaGetLastError();
+}
+
+__global__ void axpby_kernel(double a, const double* __restrict__ x, double b, double* __restrict__ y, size_t L) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) y[i] = a * x[i] + b * y[i];
+}
+
+cudaError_t launch_axpby(double a, const double* x, double b, double* y, size_t L, cudaStream_t st) {
+  axpby_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, x, b, y, L);
+  return cudaGetLastError();
+}
+
+__global__ void waxpby_kernel(double a, const double* __restrict__ x, double b, const double* __restrict__ z,
+                              double* __restrict__ y, size_t L) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) y[i] = a * x[i] + b * z[i];
+}
+
+cudaError_t launch_waxpby(double a, const double* x, double b, const double* z, double* y, size_t L,
+                          cudaStream_t st) {
+  waxpby_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, x, b, z, y, L);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(RED_THREADS) sumsq_kernel(const double* __restrict__ x, size_t L,
+                                                            double* __restrict__ partial) {
+  __shared__ double sh[RED_THREADS / 32];
+  double ss = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) ss = fma(x[i], x[i], ss);
+  const double s = block_sum(ss, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+cudaError_t launch_sumsq(const double* x, size_t L, double* partial, cudaStream_t st) {
+  sumsq_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(x, L, partial);
+  return cudaGetLastError();
+}
+
+__global__ void finish_norm_kernel(const double* __restrict__ partial, double* out) {
+  __shared__ double sh[RED_THREADS / 32];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < RED_BLOCKS; b += RED_THREADS) v += partial[b];
+  const double s = block_sum(v, sh);
+  if (threadIdx.x == 0) *out = sqrt(s);
+}
+
+cudaError_t launch_finish_norm(const double* partial, double* out, cudaStream_t st) {
+  finish_norm_kernel<<<1, RED_THREADS, 0, st>>>(partial, out);
+  return cudaGetLastError();
+}
+
+// eps_FD = c / ||x||_2 with c = sqrt(eps_machine)/eps; 0 if ||x|| = 0
+__global__ void finish_fd_eps_kernel(const double* __restrict__ partial, double c, double* out) {
+  __shared__ double sh[RED_THREADS / 32];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < RED_BLOCKS; b += RED_THREADS) v += partial[b];
+  const double s = block_sum(v, sh);
+  if (threadIdx.x == 0) *out = s > 0.0 ? c / sqrt(s) : 0.0;
+}
+
+cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st) {
+  finish_fd_eps_kernel<<<1, RED_THREADS, 0, st>>>(partial, c, out);
+  return cudaGetLastError();
+}
+
+struct ComboArgs {
+  const double* base;
+  const double* X[8];
+  const double* Y[8];
+  double a[8], b[8];
+  int nx, ny;
+};
+
+__global__ void stage_combo_kernel(ComboArgs A, double* __restrict__ y, size_t L) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) {
+    double v = A.base ? A.base[i] : 0.0;
+    for (int k = 0; k < A.nx; ++k) v = fma(A.a[k], A.X[k][i], v);
+    for (int k = 0; k < A.ny; ++k) v = fma(A.b[k], A.Y[k][i], v);
+    y[i] = v;
+  }
+}
+
+cudaError_t launch_stage_combo(const double* base, int nx, const double* const* X, const double* a, int ny,
+                               const double* const* Y, const double* b, double* y, size_t L, cudaStream_t st) {
+  if (nx > 8 || ny > 8) return cudaErrorInvalidValue;
+  ComboArgs A{};
+  A.base = base;
+  A.nx = nx;
+  A.ny = ny;
+  for (int k = 0; k < nx; ++k) { A.X[k] = X[k]; A.a[k] = a[k]; }
+  for (int k = 0; k < ny; ++k) { A.Y[k] = Y[k]; A.b[k] = b[k]; }
+  stage_combo_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(A, y, L);
+  return cudaGetLastError();
+}

@@ -1,0 +1,335 @@
+// modes.cuh -- what each operator of the hot path feeds the element evaluator.
+//
+// A mode defines: the node State (one or two jets + NS gradients), NCH output
+// channels, how the volume/face fluxes reduce to those channels, and the
+// epilogue.  Notation: L(.) is the DGSEM operator on a flux field, so
+// R1(W) = L(F(W)); a1dt = alpha1 dt; c2 = alpha2 dt^2 / 2.
+#pragma once
+#include <type_traits>
+#include "ops.cuh"
+
+struct OpArgs {
+  const double* W;      // state (or build state W_b for the K apply)
+  const double* S;      // sigma
+  const double* dW;     // Delta W
+  const double* dS;     // Delta sigma
+  const double* b;      // Newton right-hand side
+  const double* U;      // precond: U = S_i W_i
+  const double* V;      // precond: V = S_i sigma_i
+  double* out1;
+  double* out2;
+  const double* G0;     // NS lifted gradients of jet state 0
+  const double* G1;     // NS lifted gradients of jet state 1
+  double a1dt, c2;
+  double epsw;          // FD step for the W direction (<= 0: quotient is 0)
+  const double* d_epsw; // if non-NULL, the FD step is read from device memory
+  int m;                // doubles per element
+};
+
+__device__ __forceinline__ double fd_step(const OpArgs& A) { return A.d_epsw ? *A.d_epsw : A.epsw; }
+
+template <int EQ, class T, int NODES>
+__device__ __forceinline__ void ld_state(const double* G, int e, int node, NodeState<EQ, T>& s) {
+  if constexpr (EQ == 2) load_grads<T, NODES>(G, e, node, s.gx, s.gy);
+}
+
+#define IDX(e, v, node) ((size_t)(e) * A.m + (v) * NODES + (node))
+
+// R1(W)                                                        (eq:DGSEM_wt)
+template <int EQ, int NODES> struct ModeR1 {
+  static constexpr int NV = NVars<EQ>::value, NCH = 1;
+  using Args = OpArgs;
+  template <int K> using StateT = double;
+  struct State { NodeState<EQ, double> s; };
+  template <int K>
+  __device__ static void load_w(const Args& A, int e, int node, double* w, bool) {
+    for (int v = 0; v < NV; ++v) w[v] = A.W[IDX(e, v, node)];
+  }
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
+    load_w<0>(A, e, node, st.s.w, nbr);
+    ld_state<EQ, double, NODES>(A.G0, e, node, st.s);
+  }
+  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    double F[NV];
+    vol_flux<EQ>(pp, st.s, d, F);
+    for (int v = 0; v < NV; ++v) c[0][v] = F[v];
+  }
+  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    double f[NV];
+    face_flux<EQ>(pp, L.s, R.s, d, f);
+    for (int v = 0; v < NV; ++v) c[0][v] = f[v];
+  }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) A.out1[IDX(e, v, node)] = o[0][v];
+  }
+};
+
+// R1(W) and R2(W, sigma) from one dual evaluation             (eq:DGSEM_wtt)
+template <int EQ, int NODES> struct ModeR12 {
+  static constexpr int NV = NVars<EQ>::value, NCH = 2;
+  using Args = OpArgs;
+  template <int K> using StateT = J1;
+  struct State { NodeState<EQ, J1> s; };
+  template <int K>
+  __device__ static void load_w(const Args& A, int e, int node, J1* w, bool) {
+    for (int v = 0; v < NV; ++v) w[v] = J1{A.W[IDX(e, v, node)], A.S[IDX(e, v, node)]};
+  }
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
+    load_w<0>(A, e, node, st.s.w, nbr);
+    ld_state<EQ, J1, NODES>(A.G0, e, node, st.s);
+  }
+  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    J1 F[NV];
+    vol_flux<EQ>(pp, st.s, d, F);
+    for (int v = 0; v < NV; ++v) { c[0][v] = F[v].v; c[1][v] = F[v].a; }
+  }
+  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    J1 f[NV];
+    face_flux<EQ>(pp, L.s, R.s, d, f);
+    for (int v = 0; v < NV; ++v) { c[0][v] = f[v].v; c[1][v] = f[v].a; }
+  }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      if (A.out1) A.out1[IDX(e, v, node)] = o[0][v];
+      A.out2[IDX(e, v, node)] = o[1][v];
+    }
+  }
+};
+
+// Stage residual: G1 = W - b + L(-a1dt F + c2 F'sigma), G2 = sigma - L(F)
+// (eq:Newton_Residual; P:236-239 read as R4)
+template <int EQ, int NODES> struct ModeResid {
+  static constexpr int NV = NVars<EQ>::value, NCH = 2;
+  using Args = OpArgs;
+  template <int K> using StateT = J1;
+  struct State { NodeState<EQ, J1> s; };
+  template <int K>
+  __device__ static void load_w(const Args& A, int e, int node, J1* w, bool) {
+    for (int v = 0; v < NV; ++v) w[v] = J1{A.W[IDX(e, v, node)], A.S[IDX(e, v, node)]};
+  }
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
+    load_w<0>(A, e, node, st.s.w, nbr);
+    ld_state<EQ, J1, NODES>(A.G0, e, node, st.s);
+  }
+  __device__ static void comb(const Args& A, const J1* F, double (&c)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      c[0][v] = fma(A.c2, F[v].a, -A.a1dt * F[v].v);
+      c[1][v] = F[v].v;
+    }
+  }
+  __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    J1 F[NV];
+    vol_flux<EQ>(pp, st.s, d, F);
+    comb(A, F, c);
+  }
+  __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    J1 f[NV];
+    face_flux<EQ>(pp, L.s, R.s, d, f);
+    comb(A, f, c);
+  }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      A.out1[k] = (A.W[k] - A.b[k]) + o[0][v];
+      A.out2[k] = A.S[k] - o[1][v];
+    }
+  }
+};
+
+// EXACT JVP.  Hyper-dual input W + e1 sigma + e2 dW + e1e2 dsigma gives
+//   b-part = dR1/dW dW,   c-part = dR2/dW dW + dR2/dsigma dsigma
+// so  top = dW + L(-a1dt F_b + c2 F_c),  bottom = dsigma - L(F_b)   (eq:nonlinear_eqsys)
+template <int EQ, int NODES> struct ModeJvpExact {
+  static constexpr int NV = NVars<EQ>::value, NCH = 2;
+  using Args = OpArgs;
+  template <int K> using StateT = HJ;
+  struct State { NodeState<EQ, HJ> s; };
+  template <int K>
+  __device__ static void load_w(const Args& A, int e, int node, HJ* w, bool) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      w[v] = HJ{A.W[k], A.S[k], A.dW[k], A.dS[k]};
+    }
+  }
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
+    load_w<0>(A, e, node, st.s.w, nbr);
+    ld_state<EQ, HJ, NODES>(A.G0, e, node, st.s);
+  }
+  __device__ static void comb(const Args& A, const HJ* F, double (&c)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      c[0][v] = fma(A.c2, F[v].c, -A.a1dt * F[v].b);
+      c[1][v] = F[v].b;
+    }
+  }
+  __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    HJ F[NV];
+    vol_flux<EQ>(pp, st.s, d, F);
+    comb(A, F, c);
+  }
+  __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    HJ f[NV];
+    face_flux<EQ>(pp, L.s, R.s, d, f);
+    comb(A, f, c);
+  }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      A.out1[k] = A.dW[k] + o[0][v];
+      A.out2[k] = A.dS[k] - o[1][v];
+    }
+  }
+};
+
+// FD JVP (eq:MatrixFree_nonlinear; sigma direction exact, R8):
+//   p = (W + eps dW) + e1 sigma           (J1)
+//   q =  W + e1 sigma + e2 dsigma         (J2)
+//   top = dW + L(-a1dt (F_p - F_q)/eps + c2 (F'_p s - F'_q s)/eps + c2 F'_q ds)
+//   bot = dsigma - L((F_p - F_q)/eps)
+// eps <= 0 means ||dW|| = 0 and the dW quotients are 0.
+template <int EQ, int NODES> struct ModeJvpFD {
+  static constexpr int NV = NVars<EQ>::value, NCH = 2;
+  using Args = OpArgs;
+  template <int K> using StateT = typename std::conditional<K == 0, J1, J2>::type;
+  struct State { NodeState<EQ, J1> p; NodeState<EQ, J2> q; };
+  template <int K>
+  __device__ static void load_w(const Args& A, int e, int node, StateT<K>* w, bool) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      if constexpr (K == 0) {
+        const double ew = fd_step(A);
+        const double wp = ew > 0.0 ? __dadd_rn(A.W[k], __dmul_rn(ew, A.dW[k])) : A.W[k];
+        w[v] = J1{wp, A.S[k]};
+      } else {
+        w[v] = J2{A.W[k], A.S[k], A.dS[k]};
+      }
+    }
+  }
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
+    load_w<0>(A, e, node, st.p.w, nbr);
+    load_w<1>(A, e, node, st.q.w, nbr);
+    ld_state<EQ, J1, NODES>(A.G0, e, node, st.p);
+    ld_state<EQ, J2, NODES>(A.G1, e, node, st.q);
+  }
+  __device__ static void comb(const Args& A, const J1* Fp, const J2* Fq, double (&c)[NCH][NV]) {
+    const double ew = fd_step(A);
+    if (ew > 0.0) {
+      const double ie = 1.0 / ew;
+      for (int v = 0; v < NV; ++v) {
+        const double q1 = (Fp[v].v - Fq[v].v) * ie;
+        const double q2 = (Fp[v].a - Fq[v].a) * ie;
+        c[0][v] = fma(A.c2, q2 + Fq[v].b, -A.a1dt * q1);
+        c[1][v] = q1;
+      }
+    } else {
+      for (int v = 0; v < NV; ++v) { c[0][v] = A.c2 * Fq[v].b; c[1][v] = 0.0; }
+    }
+  }
+  __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    J1 Fp[NV];
+    J2 Fq[NV];
+    vol_flux<EQ>(pp, st.p, d, Fp);
+    vol_flux<EQ>(pp, st.q, d, Fq);
+    comb(A, Fp, Fq, c);
+  }
+  __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    J1 fp[NV];
+    J2 fq[NV];
+    face_flux<EQ>(pp, L.p, R.p, d, fp);
+    face_flux<EQ>(pp, L.q, R.q, d, fq);
+    comb(A, fp, fq, c);
+  }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      A.out1[k] = A.dW[k] + o[0][v];
+      A.out2[k] = A.dS[k] - o[1][v];
+    }
+  }
+};
+
+// Linear JVP for advection (eq:MatrixFree_linear):
+//   top = dW + L(F(-a1dt dW + c2 dsigma)),  bot = dsigma - L(F(dW))
+template <int EQ, int NODES> struct ModeJvpLinear {
+  static constexpr int NV = NVars<EQ>::value, NCH = 2;
+  using Args = OpArgs;
+  template <int K> using StateT = double;
+  struct State { NodeState<EQ, double> u0, u1; };
+  template <int K>
+  __device__ static void load_w(const Args& A, int e, int node, double* w, bool) {
+    for (int v = 0; v < NV; ++v) w[v] = A.dW[IDX(e, v, node)];
+  }
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      st.u0.w[v] = fma(A.c2, A.dS[k], -A.a1dt * A.dW[k]);
+      st.u1.w[v] = A.dW[k];
+    }
+  }
+  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    double F0[NV], F1[NV];
+    vol_flux<EQ>(pp, st.u0, d, F0);
+    vol_flux<EQ>(pp, st.u1, d, F1);
+    for (int v = 0; v < NV; ++v) { c[0][v] = F0[v]; c[1][v] = F1[v]; }
+  }
+  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    double f0[NV], f1[NV];
+    face_flux<EQ>(pp, L.u0, R.u0, d, f0);
+    face_flux<EQ>(pp, L.u1, R.u1, d, f1);
+    for (int v = 0; v < NV; ++v) { c[0][v] = f0[v]; c[1][v] = f1[v]; }
+  }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      A.out1[k] = A.dW[k] + o[0][v];
+      A.out2[k] = A.dS[k] - o[1][v];
+    }
+  }
+};
+
+// BJ_ext apply, second half (P:634-641 in the S+K form):
+//   K_i = element-diagonal block of dR1/dW at the build state W_b ("neighbour
+//   traces frozen": the neighbour's jet carries no tangent).
+//   top = U - c2 K V,   bottom = V + K (U - a1dt V).
+template <int EQ, int NODES> struct ModeKApply {
+  static constexpr int NV = NVars<EQ>::value, NCH = 2;
+  using Args = OpArgs;
+  template <int K> using StateT = J2;
+  struct State { NodeState<EQ, J2> s; };
+  template <int K>
+  __device__ static void load_w(const Args& A, int e, int node, J2* w, bool nbr) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      if (nbr) w[v] = J2{A.W[k], 0.0, 0.0};
+      else w[v] = J2{A.W[k], A.V[k], fma(-A.a1dt, A.V[k], A.U[k])};
+    }
+  }
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
+    load_w<0>(A, e, node, st.s.w, nbr);
+  }
+  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    J2 F[NV];
+    vol_flux<EQ>(pp, st.s, d, F);
+    for (int v = 0; v < NV; ++v) { c[0][v] = F[v].a; c[1][v] = F[v].b; }
+  }
+  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    J2 f[NV];
+    face_flux<EQ>(pp, L.s, R.s, d, f);
+    for (int v = 0; v < NV; ++v) { c[0][v] = f[v].a; c[1][v] = f[v].b; }
+  }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      A.out1[k] = fma(-A.c2, o[0][v], A.U[k]);
+      A.out2[k] = A.V[k] + o[1][v];
+    }
+  }
+};
+
+#undef IDX

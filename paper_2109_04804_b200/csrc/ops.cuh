@@ -1,0 +1,276 @@
+// ops.cuh -- fused DGSEM element operators on Gauss-Lobatto nodes.
+//
+// One thread per node, NODES = P^DIM threads per element "slot", EPB slots per
+// CTA.  Every operator of the hot path is the same pass (eq:DGSEM_wt, P:179-189,
+// on Cartesian elements, reading R2 for Dhat):
+//
+//   1. load the node state as a jet (mode-defined: W, W + e1 sigma, ...),
+//   2. evaluate the volume flux per direction and reduce it to NCH real
+//      "channels" (linear combinations fixed by the mode) -> shared memory,
+//   3. boundary nodes evaluate the canonical LLF face flux with the
+//      neighbour's trace (GLL: the neighbour's boundary node) and keep the
+//      surface term  s_d * (f*_+ lhat_N(1) - f*_- lhat_0(-1))  in registers,
+//   4. contract with Dhat along x and y from shared memory,
+//        L_ch = -( sx (sum_l Dh_il F_lj + surf_x) + sy (sum_m Dh_jm F_im + surf_y) ),
+//   5. mode epilogue combines L_ch with the node's inputs and stores.
+//
+// Because the contraction is linear, the mode combines the jet components
+// BEFORE it (e.g. the EXACT JVP needs 2 contractions, not 5 operator
+// evaluations).  Navier-Stokes adds BR1 lifted gradients (lift_kernel), read
+// back as part of the node state.
+#pragma once
+#include <cuda_runtime.h>
+#include "physics.cuh"
+
+__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+struct Geo {
+  int nx, ny, nE;          // local element grid (single rank: global)
+  double sx, sy;           // 2/dx, 2/dy
+  double lhp, lhm;         // lhat_N(+1) = 1/w_N, lhat_0(-1) = 1/w_0  (GLL)
+  double Dh[64];           // Dhat (P x P, row-major)
+};
+
+// ---- neighbour addressing (periodic Cartesian, layout L) ----------------------
+__device__ __forceinline__ int nbr_elem(const Geo& g, int e, int d, int side) {
+  int ex = e % g.nx, ey = e / g.nx;
+  if (d == 0) ex = side > 0 ? (ex + 1 == g.nx ? 0 : ex + 1) : (ex == 0 ? g.nx - 1 : ex - 1);
+  else ey = side > 0 ? (ey + 1 == g.ny ? 0 : ey + 1) : (ey == 0 ? g.ny - 1 : ey - 1);
+  return ey * g.nx + ex;
+}
+
+// ---- node state: conserved variables + (NS) lifted gradients ------------------
+template <int EQ, class T> struct NodeState {
+  static constexpr int NV = NVars<EQ>::value;
+  static constexpr int NG = EQ == 2 ? 3 : 1;
+  T w[NV];
+  T gx[NG], gy[NG];
+};
+
+template <int EQ, class T>
+__device__ __forceinline__ void vol_flux(const PhysParams& pp, const NodeState<EQ, T>& s, int d, T* F) {
+  phys_flux<EQ>(pp, s.w, d, F);
+  if constexpr (EQ == 2) {
+    T Fv[4];
+    viscous_flux(pp, s.w, s.gx, s.gy, d, Fv);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) F[v] = F[v] - Fv[v];
+  }
+}
+
+template <int EQ, class T>
+__device__ __forceinline__ void face_flux(const PhysParams& pp, const NodeState<EQ, T>& L,
+                                          const NodeState<EQ, T>& R, int d, T* f) {
+  llf_flux<EQ>(pp, L.w, R.w, d, f);
+  if constexpr (EQ == 2) {
+    T a[4], b[4];
+    viscous_flux(pp, L.w, L.gx, L.gy, d, a);
+    viscous_flux(pp, R.w, R.gx, R.gy, d, b);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) f[v] = f[v] - 0.5 * (a[v] + b[v]);
+  }
+}
+
+// ---- jet <-> flat storage helpers (lifting buffers) ---------------------------
+template <class T> struct JetN { static constexpr int value = 1; };
+template <> struct JetN<J1> { static constexpr int value = 2; };
+template <> struct JetN<J2> { static constexpr int value = 3; };
+template <> struct JetN<HJ> { static constexpr int value = 4; };
+__device__ __forceinline__ double jget(const double& x, int k) { return x; }
+__device__ __forceinline__ double jget(const J1& x, int k) { return k == 0 ? x.v : x.a; }
+__device__ __forceinline__ double jget(const J2& x, int k) { return k == 0 ? x.v : (k == 1 ? x.a : x.b); }
+__device__ __forceinline__ double jget(const HJ& x, int k) {
+  return k == 0 ? x.v : (k == 1 ? x.a : (k == 2 ? x.b : x.c));
+}
+template <class T> __device__ __forceinline__ T jmake(const double* c);
+template <> __device__ __forceinline__ double jmake<double>(const double* c) { return c[0]; }
+template <> __device__ __forceinline__ J1 jmake<J1>(const double* c) { return {c[0], c[1]}; }
+template <> __device__ __forceinline__ J2 jmake<J2>(const double* c) { return {c[0], c[1], c[2]}; }
+template <> __device__ __forceinline__ HJ jmake<HJ>(const double* c) { return {c[0], c[1], c[2], c[3]}; }
+template <class T> __device__ __forceinline__ T jzero_tangent(const T& x);
+template <> __device__ __forceinline__ double jzero_tangent<double>(const double& x) { return x; }
+template <> __device__ __forceinline__ J1 jzero_tangent<J1>(const J1& x) { return {x.v, 0.0}; }
+template <> __device__ __forceinline__ J2 jzero_tangent<J2>(const J2& x) { return {x.v, 0.0, 0.0}; }
+template <> __device__ __forceinline__ HJ jzero_tangent<HJ>(const HJ& x) { return {x.v, 0.0, 0.0, 0.0}; }
+
+// Lifted-gradient buffer of one jet state: [elem][6][JetN][NODES]
+template <class T, int NODES>
+__device__ __forceinline__ void load_grads(const double* G, int e, int node, T* gx, T* gy) {
+  constexpr int JN = JetN<T>::value;
+  const double* base = G + (size_t)e * 6 * JN * NODES + node;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    double c[JN];
+#pragma unroll
+    for (int q = 0; q < JN; ++q) c[q] = base[(k * JN + q) * NODES];
+    if (k < 3) gx[k] = jmake<T>(c); else gy[k - 3] = jmake<T>(c);
+  }
+}
+
+// ---- the element evaluation (one slot, one node per thread) --------------------
+// sF: shared scratch for this slot, NCH * DIM * NV * P * (P+1) doubles.
+template <int EQ, int DIM, int P, class Mode>
+__device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const PhysParams& pp,
+                                          const Geo& g, int e, int slot, int node, bool active,
+                                          double* sF, double (&out)[Mode::NCH][NVars<EQ>::value]) {
+  constexpr int NV = NVars<EQ>::value;
+  constexpr int NCH = Mode::NCH;
+  constexpr int PS = P + 1;                       // padded row stride (bank conflicts)
+  constexpr int PLANE = (DIM == 2 ? P : 1) * PS;  // one (ch, d, v) plane
+  const int i = node % P;
+  const int j = DIM == 2 ? node / P : 0;
+  double surf[NCH][NV];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) surf[c][v] = 0.0;
+
+  if (active) {
+    typename Mode::State st;
+    Mode::load(A, g, e, slot, node, st, false);
+    double cf[NCH][NV];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      Mode::vol(A, pp, st, d, cf);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i] = cf[c][v];
+    }
+    // faces (GLL: only boundary nodes carry a surface term)
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      const int k = d == 0 ? i : j;
+      const double s = d == 0 ? g.sx : g.sy;
+      if (k == P - 1) {
+        const int nb = nbr_elem(g, e, d, +1);
+        const int nnode = d == 0 ? j * P : i;              // neighbour's (0, j) or (i, 0)
+        typename Mode::State sn;
+        Mode::load(A, g, nb, slot, nnode, sn, true);
+        Mode::face(A, pp, st, sn, d, cf);                   // L = own, R = neighbour
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) surf[c][v] += s * (cf[c][v] * g.lhp);
+      }
+      if (k == 0) {
+        const int nb = nbr_elem(g, e, d, -1);
+        const int nnode = d == 0 ? j * P + (P - 1) : (P - 1) * P + i;
+        typename Mode::State sn;
+        Mode::load(A, g, nb, slot, nnode, sn, true);
+        Mode::face(A, pp, sn, st, d, cf);                   // L = neighbour, R = own
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) surf[c][v] -= s * (cf[c][v] * g.lhm);
+      }
+    }
+  }
+  __syncthreads();
+  if (active) {
+    double Dr[P], Dc[P];
+#pragma unroll
+    for (int l = 0; l < P; ++l) {
+      Dr[l] = g.Dh[i * P + l];
+      Dc[l] = DIM == 2 ? g.Dh[j * P + l] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE + j * PS;
+        double ax = 0.0;
+#pragma unroll
+        for (int l = 0; l < P; ++l) ax = fma(Dr[l], Fx[l], ax);
+        double acc = g.sx * ax;
+        if constexpr (DIM == 2) {
+          const double* Fy = sF + ((c * DIM + 1) * NV + v) * PLANE + i;
+          double ay = 0.0;
+#pragma unroll
+          for (int l = 0; l < P; ++l) ay = fma(Dc[l], Fy[l * PS], ay);
+          acc = fma(g.sy, ay, acc);
+        }
+        out[c][v] = -(acc + surf[c][v]);
+      }
+  }
+}
+
+// Generic operator kernel: EPB element slots per CTA, one element per slot.
+template <int EQ, int DIM, int P, class Mode, int EPB>
+__global__ void __launch_bounds__(EPB * ipow(P, DIM))
+op_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g) {
+  constexpr int NODES = ipow(P, DIM);
+  constexpr int NV = NVars<EQ>::value;
+  constexpr int SLOT = Mode::NCH * DIM * NV * (DIM == 2 ? P : 1) * (P + 1);
+  __shared__ double sF[EPB * SLOT];
+  const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
+  const int e = blockIdx.x * EPB + slot;
+  const bool active = e < g.nE;
+  double out[Mode::NCH][NV];
+  eval_slot<EQ, DIM, P, Mode>(A, pp, g, e, slot, node, active, sF + slot * SLOT, out);
+  if (active) Mode::epilogue(A, e, node, out);
+}
+
+// ---- BR1 lifting (eq:Lifting P:855, central value P:861; reading R19) -----------
+//   d^x_ij = sx ( sum_l Dh_il g_lj + g*_E,j lhat_N(1) [i=N] - g*_W,j lhat_0(-1) [i=0] )
+// Computed for jet state K of the mode; result [elem][6][JetN][NODES].
+template <int P, class Mode, int K, int EPB>
+__global__ void __launch_bounds__(EPB * P * P)
+lift_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g, double* Gout) {
+  using T = typename Mode::template StateT<K>;
+  constexpr int NODES = P * P, PS = P + 1, PLANE = P * PS;
+  constexpr int JN = JetN<T>::value;
+  __shared__ double sG[EPB * 3 * JN * PLANE];
+  const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
+  const int e = blockIdx.x * EPB + slot;
+  const bool active = e < g.nE;
+  const int i = node % P, j = node / P;
+  double* sg = sG + slot * 3 * JN * PLANE;
+  T sx_[3], sy_[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { sx_[k] = jconst<T>(0.0); sy_[k] = jconst<T>(0.0); }
+  if (active) {
+    T w[4], gv[3];
+    Mode::template load_w<K>(A, e, node, w, false);
+    grad_vars(pp, w, gv);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int q = 0; q < JN; ++q) sg[(k * JN + q) * PLANE + j * PS + i] = jget(gv[k], q);
+    for (int d = 0; d < 2; ++d) {
+      const int kk = d == 0 ? i : j;
+      if (kk == P - 1 || kk == 0) {
+        const int side = kk == P - 1 ? +1 : -1;
+        const int nb = nbr_elem(g, e, d, side);
+        const int nnode = side > 0 ? (d == 0 ? j * P : i) : (d == 0 ? j * P + P - 1 : (P - 1) * P + i);
+        T wn[4], gn[3];
+        Mode::template load_w<K>(A, nb, nnode, wn, true);
+        grad_vars(pp, wn, gn);
+        const double s = (d == 0 ? g.sx : g.sy) * (side > 0 ? g.lhp : -g.lhm);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const T gs = side > 0 ? 0.5 * (gv[k] + gn[k]) : 0.5 * (gn[k] + gv[k]);
+          if (d == 0) sx_[k] = sx_[k] + s * gs; else sy_[k] = sy_[k] + s * gs;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (active) {
+    double* out = Gout + (size_t)e * 6 * JN * NODES + node;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int q = 0; q < JN; ++q) {
+        const double* row = sg + (k * JN + q) * PLANE;
+        double ax = 0.0, ay = 0.0;
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+          ax = fma(g.Dh[i * P + l], row[j * PS + l], ax);
+          ay = fma(g.Dh[j * P + l], row[l * PS + i], ay);
+        }
+        out[(k * JN + q) * NODES] = g.sx * ax + jget(sx_[k], q);
+        out[((k + 3) * JN + q) * NODES] = g.sy * ay + jget(sy_[k], q);
+      }
+  }
+}

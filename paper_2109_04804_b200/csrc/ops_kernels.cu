@@ -1,0 +1,188 @@
+// ops_kernels.cu -- instantiation and dispatch of the fused element operators,
+// the BR1 lifting, and the BJ_ext block build (M_i = I - a1dt K_i + c2 K_i^2).
+#include <type_traits>
+#include "modes.cuh"
+#include "launch.h"
+
+constexpr int epb_for(int nodes) { return nodes >= 256 ? 1 : 256 / nodes; }
+
+template <int EQ, int DIM, int P, class Mode>
+static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
+  constexpr int NODES = ipow(P, DIM);
+  constexpr int EPB = epb_for(NODES);
+  const int grid = (g.nE + EPB - 1) / EPB;
+  if (grid == 0) return cudaSuccess;
+  op_kernel<EQ, DIM, P, Mode, EPB><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, g);
+  return cudaGetLastError();
+}
+
+template <int P, class Mode, int K>
+static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
+  constexpr int NODES = P * P;
+  constexpr int EPB = epb_for(NODES);
+  const int grid = (g.nE + EPB - 1) / EPB;
+  if (grid == 0) return cudaSuccess;
+  lift_kernel<P, Mode, K, EPB><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, g, G);
+  return cudaGetLastError();
+}
+
+// ---- BJ_ext build: columns of M_i via two element-local linearised applications
+// K t = L(F'(W_b) t) with the neighbour traces frozen (no tangent), t = e_c then
+// t = K e_c.  "element-internal influence only", block formula P:314.
+struct KColArgs {
+  const double* W;      // build state
+  const double* tan;    // shared-memory tangents, one m-vector per slot
+  int m;
+};
+
+template <int EQ, int NODES> struct ModeKCol {
+  static constexpr int NV = NVars<EQ>::value, NCH = 1;
+  using Args = KColArgs;
+  template <int K> using StateT = J1;
+  struct State { NodeState<EQ, J1> s; };
+  __device__ static void load(const Args& A, const Geo&, int e, int slot, int node, State& st, bool nbr) {
+    for (int v = 0; v < NV; ++v) {
+      const double w = A.W[(size_t)e * A.m + v * NODES + node];
+      st.s.w[v] = J1{w, nbr ? 0.0 : A.tan[slot * A.m + v * NODES + node]};
+    }
+  }
+  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    J1 F[NV];
+    vol_flux<EQ>(pp, st.s, d, F);
+    for (int v = 0; v < NV; ++v) c[0][v] = F[v].a;
+  }
+  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    J1 f[NV];
+    face_flux<EQ>(pp, L.s, R.s, d, f);
+    for (int v = 0; v < NV; ++v) c[0][v] = f[v].a;
+  }
+};
+
+template <int EQ, int DIM, int P, int EPB>
+__global__ void __launch_bounds__(EPB * ipow(P, DIM))
+kbuild_kernel(const double* __restrict__ Wb, const PhysParams pp, const Geo g, double a1dt, double c2,
+              double* __restrict__ M, int e0) {
+  constexpr int NODES = ipow(P, DIM);
+  constexpr int NV = NVars<EQ>::value;
+  constexpr int m = NV * NODES;
+  using Mode = ModeKCol<EQ, NODES>;
+  constexpr int SLOT = DIM * NV * (DIM == 2 ? P : 1) * (P + 1);
+  __shared__ double sF[EPB * SLOT];
+  __shared__ double stan[EPB * m];
+  const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
+  const int e = e0 + blockIdx.x;
+  double* Me = M + (size_t)blockIdx.x * m * m;
+  KColArgs A{Wb, stan, m};
+  for (int c0 = 0; c0 < m; c0 += EPB) {
+    const int col = c0 + slot;
+    const bool active = col < m;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) stan[slot * m + v * NODES + node] = (v * NODES + node == col) ? 1.0 : 0.0;
+    __syncthreads();
+    double y1[1][NV], y2[1][NV];
+    eval_slot<EQ, DIM, P, Mode>(A, pp, g, e, slot, node, active, sF + slot * SLOT, y1);
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < NV; ++v) stan[slot * m + v * NODES + node] = active ? y1[0][v] : 0.0;
+    __syncthreads();
+    eval_slot<EQ, DIM, P, Mode>(A, pp, g, e, slot, node, active, sF + slot * SLOT, y2);
+    if (active) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int r = v * NODES + node;
+        const double id = r == col ? 1.0 : 0.0;
+        Me[(size_t)r * m + col] = fma(c2, y2[0][v], id - a1dt * y1[0][v]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int EQ, int DIM, int P>
+static cudaError_t run_kbuild(const OpCfg& c, const Geo& g, const double* Wb, double a1dt, double c2,
+                              double* M, int e0, int ne) {
+  constexpr int NODES = ipow(P, DIM);
+  constexpr int EPB = epb_for(NODES);
+  if (ne <= 0) return cudaSuccess;
+  kbuild_kernel<EQ, DIM, P, EPB><<<ne, EPB * NODES, 0, c.stream>>>(Wb, c.pp, g, a1dt, c2, M, e0);
+  return cudaGetLastError();
+}
+
+// ---- dispatch ----------------------------------------------------------------------
+template <int EQ, int DIM, int P> struct Disp {
+  static constexpr int NODES = ipow(P, DIM);
+  static cudaError_t op(OpKind k, const OpCfg& c, const Geo& g, const OpArgs& A) {
+    switch (k) {
+      case OP_R1: return run_op<EQ, DIM, P, ModeR1<EQ, NODES>>(c, g, A);
+      case OP_R12: return run_op<EQ, DIM, P, ModeR12<EQ, NODES>>(c, g, A);
+      case OP_RESID: return run_op<EQ, DIM, P, ModeResid<EQ, NODES>>(c, g, A);
+      case OP_JVP_EXACT: return run_op<EQ, DIM, P, ModeJvpExact<EQ, NODES>>(c, g, A);
+      case OP_JVP_FD: return run_op<EQ, DIM, P, ModeJvpFD<EQ, NODES>>(c, g, A);
+      case OP_JVP_LINEAR:
+        if constexpr (EQ == 0) return run_op<EQ, DIM, P, ModeJvpLinear<EQ, NODES>>(c, g, A);
+        else return cudaErrorInvalidValue;
+      case OP_KAPPLY:
+        if constexpr (EQ != 2) return run_op<EQ, DIM, P, ModeKApply<EQ, NODES>>(c, g, A);
+        else return cudaErrorNotSupported;
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  static cudaError_t lift(OpKind k, int s, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
+    if constexpr (EQ == 2 && DIM == 2) {
+      switch (k) {
+        case OP_R1: return run_lift<P, ModeR1<EQ, NODES>, 0>(c, g, A, G);
+        case OP_R12: return run_lift<P, ModeR12<EQ, NODES>, 0>(c, g, A, G);
+        case OP_RESID: return run_lift<P, ModeResid<EQ, NODES>, 0>(c, g, A, G);
+        case OP_JVP_EXACT: return run_lift<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, G);
+        case OP_JVP_FD:
+          return s == 0 ? run_lift<P, ModeJvpFD<EQ, NODES>, 0>(c, g, A, G)
+                        : run_lift<P, ModeJvpFD<EQ, NODES>, 1>(c, g, A, G);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+    return cudaErrorInvalidValue;
+  }
+  static cudaError_t kbuild(const OpCfg& c, const Geo& g, const double* Wb, double a1dt, double c2,
+                            double* M, int e0, int ne) {
+    if constexpr (EQ != 2) return run_kbuild<EQ, DIM, P>(c, g, Wb, a1dt, c2, M, e0, ne);
+    return cudaErrorNotSupported;
+  }
+};
+
+#define HBPDC_P_LIST(X, EQ, DIM) X(EQ, DIM, 2) X(EQ, DIM, 3) X(EQ, DIM, 4) X(EQ, DIM, 5) X(EQ, DIM, 6) X(EQ, DIM, 7) X(EQ, DIM, 8)
+
+template <class F>
+static cudaError_t dispatch(const OpCfg& c, F&& f) {
+#define CASE(EQ, DIM, PP) \
+  if (c.eq == EQ && c.dim == DIM && c.P == PP) return f(Disp<EQ, DIM, PP>{});
+  HBPDC_P_LIST(CASE, 0, 1)
+  HBPDC_P_LIST(CASE, 0, 2)
+  HBPDC_P_LIST(CASE, 1, 2)
+  HBPDC_P_LIST(CASE, 2, 2)
+#undef CASE
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
+  return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
+}
+
+cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
+  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G); });
+}
+
+int lift_jet_components(OpKind kind, int state) {
+  switch (kind) {
+    case OP_R1: return 1;
+    case OP_R12: case OP_RESID: return 2;
+    case OP_JVP_EXACT: return 4;
+    case OP_JVP_FD: return state == 0 ? 2 : 3;
+    default: return 0;
+  }
+}
+
+cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, double a1dt, double c2,
+                          double* M, int e0, int ne) {
+  return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, a1dt, c2, M, e0, ne); });
+}

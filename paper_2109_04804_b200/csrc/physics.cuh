@@ -1,0 +1,94 @@
+// physics.cuh -- point-wise fluxes, templated on the jet carrier (jets.cuh).
+//
+//  advection : F_d = a_d w
+//  Euler     : F_x = (rho u, rho u^2 + p, rho u v, u (E + p)), p = (gamma-1)(E - rho|v|^2/2)
+//              (eq:Euler; reference Mach number eps = 1, reading R18)
+//  LLF       : f* = 1/2 (F_d(wL) + F_d(wR)) + 1/2 lam (wL - wR),
+//              lam = max(|v_L.e_d| + c_L, |v_R.e_d| + c_R)  (reading R3; the paper's
+//              eq:Riemann is the global-lambda variant).  Canonical orientation:
+//              L = element on the -e_d side, normal +e_d; ties take L.
+//  NS        : viscous flux F^v with BR1 gradients (reading R19).
+#pragma once
+#include "jets.cuh"
+
+struct PhysParams {
+  double ax, ay;         // advection velocity
+  double gamma;
+  double mu, lamT, Rgas; // NS: viscosity, heat conductivity c_p mu / Pr, R = 1/gamma
+};
+
+template <int EQ> struct NVars { static constexpr int value = 4; };
+template <> struct NVars<0> { static constexpr int value = 1; };
+
+// inviscid flux in direction d
+template <int EQ, class T>
+__device__ __forceinline__ void phys_flux(const PhysParams& pp, const T* w, int d, T* F) {
+  if constexpr (EQ == 0) {
+    F[0] = (d == 0 ? pp.ax : pp.ay) * w[0];
+  } else {
+    const T rho = w[0], mx = w[1], my = w[2], E = w[3];
+    const T p = (pp.gamma - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho);
+    const T vn = (d == 0 ? mx : my) / rho;
+    F[0] = rho * vn;
+    F[1] = d == 0 ? mx * vn + p : mx * vn;
+    F[2] = d == 1 ? my * vn + p : my * vn;
+    F[3] = vn * (E + p);
+  }
+}
+
+template <int EQ, class T>
+__device__ __forceinline__ T wave_speed(const PhysParams& pp, const T* w, int d) {
+  if constexpr (EQ == 0) {
+    return jconst<T>(d == 0 ? (pp.ax >= 0 ? pp.ax : -pp.ax) : (pp.ay >= 0 ? pp.ay : -pp.ay));
+  } else {
+    const T rho = w[0], mx = w[1], my = w[2], E = w[3];
+    const T p = (pp.gamma - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho);
+    const T vn = (d == 0 ? mx : my) / rho;
+    return jabs(vn) + jsqrt(pp.gamma * p / rho);
+  }
+}
+
+// canonical LLF flux across a face with normal +e_d
+template <int EQ, class T>
+__device__ __forceinline__ void llf_flux(const PhysParams& pp, const T* wL, const T* wR, int d, T* f) {
+  constexpr int NV = NVars<EQ>::value;
+  T FL[NV], FR[NV];
+  phys_flux<EQ>(pp, wL, d, FL);
+  phys_flux<EQ>(pp, wR, d, FR);
+  const T lam = jmax(wave_speed<EQ>(pp, wL, d), wave_speed<EQ>(pp, wR, d));
+#pragma unroll
+  for (int v = 0; v < NV; ++v) f[v] = 0.5 * (FL[v] + FR[v]) + 0.5 * lam * (wL[v] - wR[v]);
+}
+
+// ---- Navier-Stokes ----------------------------------------------------------------
+// gradient variables w_grad = (u, v, T), T = p / (rho R)  (eq:LiftingEq)
+template <class T>
+__device__ __forceinline__ void grad_vars(const PhysParams& pp, const T* w, T* g) {
+  const T rho = w[0], mx = w[1], my = w[2], E = w[3];
+  const T p = (pp.gamma - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho);
+  g[0] = mx / rho;
+  g[1] = my / rho;
+  g[2] = p / (rho * pp.Rgas);
+}
+
+// F^v_d(w, grad): gx = (u_x, v_x, T_x), gy = (u_y, v_y, T_y)
+template <class T>
+__device__ __forceinline__ void viscous_flux(const PhysParams& pp, const T* w, const T* gx,
+                                             const T* gy, int d, T* Fv) {
+  const T rho = w[0];
+  const T u = w[1] / rho, v = w[2] / rho;
+  const T div = gx[0] + gy[1];
+  const T txy = pp.mu * (gy[0] + gx[1]);
+  Fv[0] = jconst<T>(0.0);
+  if (d == 0) {
+    const T txx = pp.mu * (2.0 * gx[0] - (2.0 / 3.0) * div);
+    Fv[1] = txx;
+    Fv[2] = txy;
+    Fv[3] = txx * u + txy * v + pp.lamT * gx[2];
+  } else {
+    const T tyy = pp.mu * (2.0 * gy[1] - (2.0 / 3.0) * div);
+    Fv[1] = txy;
+    Fv[2] = tyy;
+    Fv[3] = txy * u + tyy * v + pp.lamT * gy[2];
+  }
+}

@@ -1,0 +1,236 @@
+"""GPU (CUDA, through the C-ABI) vs CPU oracle parity.
+
+Tolerances (north_star): relative L2 <= 1e-11 per operator /
+JVP application on seeded perturbed inputs; FD JVP within
+max(1e-11, 4 delta_FD) with delta_FD the oracle's own FD-vs-EXACT gap at the
+same eps; precond apply with identical S <= 1e-13; S build
+<= 1e-11 max(1, cond/1e4); end of run <= 1e-8.
+Sizes span several CTAs and a ragged last CTA (element counts not multiples
+of the elements-per-CTA)."""
+import numpy as np
+import pytest
+
+from oracle import dgsem, hbpc, implicit
+from paper_2109_04804_b200 import configs, inputs
+from gpu_common import adv_ic, euler_ic, make_pair, ns_ic, rel, to_gpu, to_np, SEED
+
+pytestmark = pytest.mark.gpu
+
+OPS_CASES = [
+    # (kind, N, nx, ny, bounds)
+    ("advection", 3, 16, None, (0.0, 1.0, 0.0, 1.0)),
+    ("advection", 5, 9, 7, (0.0, 1.0, 0.0, 1.0)),
+    ("euler", 7, 5, 3, (0.0, 1.0, 0.0, 1.0)),
+    ("euler", 3, 11, 6, (0.0, 1.0, 0.0, 1.0)),
+    ("euler", 2, 4, 4, (0.0, 1.0, 0.0, 1.0)),
+]
+
+
+def _state(d, kind, seed):
+    if kind == "advection":
+        return adv_ic(d, seed)
+    if kind == "euler":
+        return euler_ic(d, seed)
+    return ns_ic(d, seed)
+
+
+def _pair(kind, N, nx, ny, bounds, **kw):
+    a = (1.0, 0.0) if ny is None else (1.0, -0.6)
+    return make_pair(kind, N, nx, ny, bounds=bounds, a=a, **kw)
+
+
+@pytest.mark.parametrize("case", OPS_CASES)
+def test_node_coords(case):
+    d, ctx = _pair(*case)
+    g = ctx.node_coords()
+    o = d.node_coords()
+    for a, b in zip(g, o):
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("case", OPS_CASES)
+def test_rhs_r1_r2(case):
+    kind = case[0]
+    d, ctx = _pair(*case)
+    W = _state(d, kind, SEED + 1)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 2))
+    R1o = dgsem.rhs1(d, W)
+    R2o = dgsem.rhs2(d, W, sig)
+    R1g = to_np(ctx.rhs(to_gpu(W)))
+    R2g = to_np(ctx.rhs(to_gpu(W), to_gpu(sig)))
+    assert rel(R1g, R1o) <= 1e-11
+    assert rel(R2g, R2o) <= 1e-11
+
+
+@pytest.mark.parametrize("case", OPS_CASES)
+def test_residual(case):
+    kind = case[0]
+    d, ctx = _pair(*case)
+    W = _state(d, kind, SEED + 3)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 4))
+    b = W * (1 + 1e-3 * inputs.random_field(d.n, SEED + 5))
+    a1, a2, dt = 1.0 / 6.0, 1.0 / 54.0, 0.01
+    G1o, G2o = implicit.residual(d, a1, a2, dt, b, W, sig)
+    G1g, G2g, nrm = ctx.residual(a1, a2, dt, to_gpu(b), to_gpu(W), to_gpu(sig), norm=True)
+    o = np.concatenate([G1o, G2o])
+    g = np.concatenate([to_np(G1g), to_np(G2g)])
+    assert rel(g, o) <= 1e-11
+    assert abs(nrm - np.linalg.norm(o)) <= 1e-11 * np.linalg.norm(o)
+
+
+def test_residual_degenerate():
+    """dt = 0, b = W -> G1 = 0 exactly; sigma = R1(W) -> G2 ~ 0."""
+    d, ctx = _pair("euler", 3, 4, 4, (0.0, 1.0, 0.0, 1.0))
+    W = euler_ic(d, SEED + 6)
+    Wg = to_gpu(W)
+    sig = ctx.rhs(Wg)
+    G1, G2 = ctx.residual(0.5, 1 / 6, 0.0, Wg, Wg, sig)
+    assert np.abs(to_np(G1)).max() == 0.0
+    assert np.abs(to_np(G2)).max() == 0.0
+
+
+@pytest.mark.parametrize("case", [c for c in OPS_CASES if c[0] != "advection"])
+def test_jvp_exact(case):
+    kind = case[0]
+    d, ctx = _pair(*case)
+    W = _state(d, kind, SEED + 7)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 8))
+    dW = inputs.random_field(d.n, SEED + 9, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 10, unit_norm=True)
+    a1, a2, dt = 0.5, 1 / 6, 0.02
+    to, bo = implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds)
+    tg, bg = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(dW), to_gpu(ds), mode="exact")
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11
+
+
+@pytest.mark.parametrize("case", [c for c in OPS_CASES if c[0] == "advection"])
+def test_jvp_linear(case):
+    d, ctx = _pair(*case)
+    dW = inputs.random_field(d.n, SEED + 11, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 12, unit_norm=True)
+    z = np.zeros(d.n)
+    a1, a2, dt = 1.0, 1.0, 0.05
+    to, bo = implicit.jvp_linear(d, a1, a2, dt, dW, ds)
+    tg, bg = ctx.jvp(a1, a2, dt, to_gpu(z), to_gpu(z), to_gpu(dW), to_gpu(ds), mode="linear")
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11
+
+
+@pytest.mark.parametrize("case", [c for c in OPS_CASES if c[0] != "advection"])
+def test_jvp_fd(case):
+    """FD JVP with eps pinned via eps_override."""
+    kind = case[0]
+    d, ctx = _pair(*case)
+    W = _state(d, kind, SEED + 13)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 14))
+    dW = inputs.random_field(d.n, SEED + 15, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 16, unit_norm=True)
+    a1, a2, dt = 1.0, 1.0, 0.01
+    eps = implicit.fd_eps(dW)
+    fo = np.concatenate(implicit.jvp_fd(d, a1, a2, dt, W, sig, dW, ds, eps_override=(eps, None)))
+    ex = np.concatenate(implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds))
+    delta = rel(fo, ex)
+    tg, bg = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(dW), to_gpu(ds), mode="fd",
+                     eps_override=(eps, None))
+    g = np.concatenate([to_np(tg), to_np(bg)])
+    assert rel(g, fo) <= max(1e-11, 4 * delta), (rel(g, fo), delta)
+    # the library's own eps (device-side norm) gives the same answer within the FD floor
+    tg2, bg2 = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(dW), to_gpu(ds), mode="fd")
+    assert rel(np.concatenate([to_np(tg2), to_np(bg2)]), fo) <= max(1e-11, 4 * delta)
+    # zero direction: the quotient is 0
+    z = np.zeros(d.n)
+    tz, bz = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(z), to_gpu(z), mode="fd")
+    assert np.abs(to_np(tz)).max() == 0.0 and np.abs(to_np(bz)).max() == 0.0
+
+
+PC_CASES = [
+    ("advection", 3, 8, None, (0.0, 1.0, 0.0, 1.0)),
+    ("advection", 2, 6, 4, (0.0, 1.0, 0.0, 1.0)),
+    ("euler", 2, 4, 4, (0.0, 1.0, 0.0, 1.0)),
+    ("euler", 3, 4, 2, (0.0, 1.0, 0.0, 1.0)),
+]
+
+
+@pytest.mark.parametrize("case", PC_CASES)
+def test_precond_build_and_apply(case):
+    kind = case[0]
+    d, ctx = _pair(*case)
+    W = _state(d, kind, SEED + 17)
+    a1, a2, dt = 1.0 / 6.0, 1.0 / 54.0, 0.05
+    pc = implicit.BJExt(d, W, a1, a2, dt)
+    ctx.precond_build(a1, a2, dt, to_gpu(W))
+    shared = kind == "advection"
+    Sg, flag = ctx.precond_export(shared_hint=shared)
+    assert flag == shared
+    Sg = to_np(Sg).reshape(-1, d.m, d.m)
+    So = pc.S[:1] if shared else pc.S
+    cond = max(np.linalg.cond(M) for M in pc.M)
+    err = np.linalg.norm(Sg - So) / np.linalg.norm(So)
+    assert err <= 1e-11 * max(1.0, cond / 1e4), (err, cond)
+    x = inputs.random_field(d.n, SEED + 18)
+    y = inputs.random_field(d.n, SEED + 19)
+    to, bo = pc.apply(x, y)
+    tg, bg = ctx.precond_apply(to_gpu(x), to_gpu(y))
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11 * max(1, cond / 1e4)
+    # identical S (the oracle's, installed into the library): apply <= 1e-13
+    ctx.precond_set(a1, a2, dt, to_gpu(W), to_gpu(So.reshape(-1)), shared)
+    tg, bg = ctx.precond_apply(to_gpu(x), to_gpu(y))
+    to2, bo2 = pc.apply_sk(x, y)
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to2, bo2])) <= 1e-13
+
+
+def _run_oracle(d, q, kmax, W0, dt, steps, **opt):
+    H = hbpc.HBPC(d, q, kmax, implicit.NewtonOpts(**opt))
+    W = W0.copy()
+    st = dict(stage_solves=0, newton_its=0, gmres_its=0, precond_builds=0)
+    for _ in range(steps):
+        W = H.step(W, dt, st)
+    return W, st
+
+
+def test_c1_end_of_run():
+    """C1 exactly as BASELINE.json states it: 1D advection, N=3, 16 elements,
+    HBPC(4,0), CFL 1, 10 steps, GMRES rtol 1e-12."""
+    cfg = configs.CONFIGS["C1"]
+    d, ctx = make_pair("advection", cfg.N, cfg.nx, None, a=cfg.a, q=cfg.q, kmax=cfg.kmax,
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol)
+    W0 = inputs.initial_state("C1", d.node_coords())
+    dt = configs.cfl_dt(cfg, W0)
+    Wo, sto = _run_oracle(d, cfg.q, cfg.kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol,
+                          gmres_rtol=cfg.gmres_rtol)
+    Wg = to_gpu(W0)
+    its = 0
+    for _ in range(cfg.steps):
+        its += ctx.step(dt, Wg)["gmres_its"]
+    assert rel(to_np(Wg), Wo) <= 1e-8
+
+
+@pytest.mark.parametrize("precond", ["bjext", "none"])
+def test_c2_shape_end_of_run(precond):
+    """C2 physics at a reduced mesh (8x8, N=5, HBPC(6,2), CFL 2, 3 steps)."""
+    cfg = configs.scaled(configs.CONFIGS["C2"], nx=8, ny=8, steps=3)
+    d, ctx = make_pair("advection", cfg.N, cfg.nx, cfg.ny, a=cfg.a, q=cfg.q, kmax=cfg.kmax,
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, precond=precond)
+    W0 = inputs.initial_state("C2", d.node_coords())
+    dt = configs.cfl_dt(cfg, W0)
+    Wo, _ = _run_oracle(d, cfg.q, cfg.kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol,
+                        gmres_rtol=cfg.gmres_rtol, precond=precond)
+    Wg = to_gpu(W0)
+    for _ in range(cfg.steps):
+        ctx.step(dt, Wg)
+    assert rel(to_np(Wg), Wo) <= 1e-8
+
+
+@pytest.mark.parametrize("q,kmax", [(4, 0), (8, 4)])
+def test_euler_end_of_run(q, kmax):
+    """C3 physics (isentropic vortex + seeded noise) at a reduced mesh:
+    4x4 elements, N=3, BJ_ext, FD JVP, 2 steps."""
+    cfg = configs.scaled(configs.CONFIGS["C3"], N=3, nx=4, ny=4, steps=2, q=q, kmax=kmax)
+    d, ctx = make_pair("euler", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=q, kmax=kmax,
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol)
+    W0 = inputs.initial_state("C3", d.node_coords(), noise=cfg.noise)
+    dt = configs.cfl_dt(cfg, inputs.initial_state("C3", d.node_coords()))
+    Wo, sto = _run_oracle(d, q, kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol)
+    Wg = to_gpu(W0)
+    for _ in range(cfg.steps):
+        ctx.step(dt, Wg)
+    assert rel(to_np(Wg), Wo) <= 1e-8
