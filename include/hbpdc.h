@@ -176,12 +176,17 @@ HBPDC_API hbpdc_status hbpdc_step_host(hbpdc_ctx* ctx, double dt, double* W_host
 HBPDC_API hbpdc_status hbpdc_reset(hbpdc_ctx* ctx);
 
 /* Per-kernel timing (CUDA events on the context stream), for roofline
- * reporting.  enable=1 starts recording, 0 stops.  kernel ids: see DESIGN.md
- * (0 = precond GEMV, 1 = JVP, 2 = residual, 3 = Arnoldi dots, 4 = Arnoldi
- * axpy, 5 = precond K-apply, 6 = precond build). */
+ * reporting.  enable=1 starts recording (and zeroes the counters), 0 stops.
+ * kernel ids: 0 = precond GEMV (S streaming), 1 = JVP, 2 = residual,
+ * 3 = Arnoldi dots, 4 = Arnoldi update, 5 = precond K-apply, 6 = precond
+ * build.  alg_bytes = algorithmic HBM bytes of those launches (DESIGN.md
+ * byte model: each input and output touched once). */
 HBPDC_API hbpdc_status hbpdc_profile(hbpdc_ctx* ctx, int enable);
 HBPDC_API hbpdc_status hbpdc_profile_read(hbpdc_ctx* ctx, int kernel_id, long long* launches,
-                                double* total_ms);
+                                double* total_ms, double* alg_bytes);
+
+/* Number of kernels this process has launched through the library so far. */
+HBPDC_API hbpdc_status hbpdc_launch_count(long long* count);
 
 HBPDC_API const char* hbpdc_last_error(const hbpdc_ctx* ctx);
 HBPDC_API void hbpdc_finalize(hbpdc_ctx* ctx);

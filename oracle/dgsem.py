@@ -125,13 +125,17 @@ def _roll(x, shift, axis):
 
 
 class _Ops:
-    """Tensor-product derivative/trace operators of one discretization."""
+    """Tensor-product derivative/trace operators of one discretization.
+    absolute=True builds the magnitude version used for rounding estimates
+    (|Dhat|, |lhat|, and the - face added instead of subtracted)."""
 
-    def __init__(self, disc: Disc):
+    def __init__(self, disc: Disc, absolute=False):
         b = disc.basis
         self.disc = disc
         self.Dh, self.lp, self.lm = b.Dhat, b.l_plus, b.l_minus
         self.lhp, self.lhm = b.lhat_plus, b.lhat_minus
+        if absolute:
+            self.Dh, self.lhp, self.lhm = np.abs(self.Dh), np.abs(self.lhp), -np.abs(self.lhm)
         self.dim = disc.mesh.dim
 
     # traces: polynomial evaluated at the element end (P:201)
@@ -202,9 +206,12 @@ def lifting(disc: Disc, Wf, ops=None):
     return out[0], out[1]
 
 
-def rhs1_field(disc: Disc, Wf):
-    """R^(1)_h on a field-shaped array (values, duals or hyper-duals)."""
-    ops = _Ops(disc)
+def rhs1_field(disc: Disc, Wf, absolute=False):
+    """R^(1)_h on a field-shaped array (values, duals or hyper-duals).
+    absolute=True returns R1_abs (plain values only): every term of
+    eq:DGSEM_wt replaced by its magnitude -- the scale of R1's rounding."""
+    ops = _Ops(disc, absolute)
+    ab = (lambda xs: [np.abs(x) for x in xs]) if absolute else (lambda xs: xs)
     eq, me = disc.eq, disc.mesh
     dim = me.dim
     va = 2 if dim == 2 else 1
@@ -233,15 +240,22 @@ def rhs1_field(disc: Disc, Wf):
             fvL = physics.viscous_flux(eq, wnm, gxnm, gynm, d)
             fvR = physics.viscous_flux(eq, wm, gxm, gym, d)
             fm = [f - 0.5 * (a + b) for f, a, b in zip(fm, fvL, fvR)]
-        fpa = ad.stack(fp, axis=va)
-        fma = ad.stack(fm, axis=va)
+        if absolute:
+            Fa = ad.stack(ab(F), axis=va)
+        fpa = ad.stack(ab(fp), axis=va)
+        fma = ad.stack(ab(fm), axis=va)
         total = total + _scale(d, me) * (ops.volume(Fa, d) + ops.surface(fpa, fma, d))
-    return -total
+    return total if absolute else -total
 
 
 def rhs1(disc: Disc, W):
     """R^(1)_h(W) for a flat layout-L vector (or Jet of flat vectors)."""
     return disc.to_flat(rhs1_field(disc, disc.to_field(W)))
+
+
+def rhs1_abs(disc: Disc, W):
+    """R1_abs(W): magnitude version of R1 (rounding scale, reading R10b)."""
+    return disc.to_flat(rhs1_field(disc, disc.to_field(np.asarray(W, float)), absolute=True))
 
 
 def rhs2(disc: Disc, W, sigma):

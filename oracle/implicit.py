@@ -12,7 +12,7 @@ import math
 import numpy as np
 
 from . import ad
-from .dgsem import rhs1, rhs2, rhs12, Disc
+from .dgsem import rhs1, rhs1_abs, rhs2, rhs12, Disc
 
 EPS_MACH = 2.0 ** -52            # Fortran epsilon(1d0), reading R7
 
@@ -269,12 +269,17 @@ class NewtonFailure(RuntimeError):
 def newton_solve(disc, a1, a2, dt, b, W_guess, opts: NewtonOpts, pc=None, stats=None):
     """Solve G(X) = 0 from X0 = (W_g, R1(W_g)).  Stops when
     ||G(X^r)|| <= max(rtol ||G(X^0)||, 64 eps ||b||) or after a step with
-    ||dW|| <= atol_dw (reading R10)."""
+    ||dW|| <= atol_dw (reading R10).  The floor also
+    covers the rounding level of the sigma block sigma - R1(W), which cannot
+    be evaluated below ~eps ||R1_abs|| (R1 with |Dhat|, |F|, |f*|): the
+    reason P:924 gives for adding an absolute criterion (reading R10b):
+        floor = max(64 eps ||b||, 4 eps ||R1_abs(W_g)||)."""
     n = disc.n
     mode = default_jvp_mode(disc) if opts.jvp_mode == "auto" else opts.jvp_mode
     W = np.array(W_guess, float)
     sig = rhs1(disc, W)
-    floor = 64.0 * EPS_MACH * float(np.linalg.norm(b))
+    floor = max(64.0 * EPS_MACH * float(np.linalg.norm(b)),
+                4.0 * EPS_MACH * float(np.linalg.norm(rhs1_abs(disc, W))))
     g0 = None
     for r in range(opts.max_newton + 1):
         G1, G2 = residual(disc, a1, a2, dt, b, W, sig)

@@ -73,6 +73,7 @@ struct hbpdc_ctx {
   int nv = 1, P = 2, nodes = 2, m = 2, nE = 0, nxl = 0, nyl = 0, ex0 = 0, ey0 = 0;
   size_t n = 0;          // W-DOF on this rank
   Geo geo{};
+  Geo geo_abs{};         // |Dhat|, -lhat_0(-1): R1_abs (rounding scale, reading R10b)
   OpCfg cfg{};
   hbpdc::Basis1D basis;
   cudaStream_t stream = nullptr;
@@ -105,6 +106,7 @@ struct hbpdc_ctx {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_rec;
   long long prof_launch[NPROF] = {};
   double prof_ms[NPROF] = {};
+  double prof_bytes[NPROF] = {};   // algorithmic bytes (DESIGN.md byte model)
   hbpdc_step_stats* st = nullptr;  // stats of the step in progress
 };
 
@@ -149,8 +151,9 @@ struct ProfScope {
   hbpdc_ctx* c;
   int id;
   cudaEvent_t a = nullptr, b = nullptr;
-  ProfScope(hbpdc_ctx* c_, int id_) : c(c_), id(id_) {
+  ProfScope(hbpdc_ctx* c_, int id_, double alg_bytes = 0.0) : c(c_), id(id_) {
     if (!c->prof_on) return;
+    c->prof_bytes[id] += alg_bytes;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a, c->stream);
@@ -192,7 +195,7 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A) {
       A.G1 = c->lift1;
     }
   }
-  CK(launch_op(k, c->cfg, c->geo, A));
+  CK(launch_op(k, c->cfg, k == OP_R1ABS ? c->geo_abs : c->geo, A));
   return HBPDC_OK;
 }
 
@@ -241,7 +244,7 @@ hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const doubl
       A.d_epsw = c->deps;
     }
   }
-  ProfScope ps(c, 1);
+  ProfScope ps(c, 1, (k == OP_JVP_LINEAR ? 4.0 : 6.0) * n * 8.0);
   CKS(run_op(c, k, A));
   if (c->st) c->st->jvp_calls++;
   return HBPDC_OK;
@@ -274,7 +277,7 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
   CKS(ensure_precond_mem(c));
   if (c->pb.equation == HBPDC_NAVIER_STOKES)
     return fail(c, HBPDC_E_ARG, "BJ_ext build for Navier-Stokes is not implemented yet");
-  ProfScope ps(c, 6);
+  ProfScope ps(c, 6, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + c->n * 8.0);
   CK(cudaMemcpyAsync(c->Wb, W, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   const size_t mm = (size_t)c->m * c->m;
   const int nblk = c->s_shared ? 1 : c->nE;
@@ -303,14 +306,14 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
 hbpdc_status precond_apply_impl(hbpdc_ctx* c, const double* iw, const double* is, double* ow, double* os) {
   if (!c->pc_valid) return fail(c, HBPDC_E_ARG, "precond_apply before precond_build");
   {
-    ProfScope ps(c, 0);
+    ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 4.0 * c->n * 8.0);
     CK(launch_block_gemv2(c->S, c->s_shared, iw, is, c->U, c->Vv, c->m, c->nE, c->stream));
   }
   OpArgs A = base_args(c);
   A.W = c->Wb; A.U = c->U; A.V = c->Vv; A.out1 = ow; A.out2 = os;
   A.a1dt = c->pc_a1 * c->pc_dt;
   A.c2 = c->pc_a2 * c->pc_dt * c->pc_dt / 2.0;
-  ProfScope ps(c, 5);
+  ProfScope ps(c, 5, 5.0 * c->n * 8.0);
   CK(launch_op(OP_KAPPLY, c->cfg, c->geo, A));
   if (c->st) c->st->precond_applies++;
   return HBPDC_OK;
@@ -367,37 +370,32 @@ hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
       double* vj = c->Vk + (size_t)j * n2;
       double* w = c->Vk + (size_t)(j + 1) * n2;
       CKS(apply_JPinv(c, L, vj, w, L.pc));
-      // classical Gram-Schmidt, twice (CGS2)
-      {
-        ProfScope ps(c, 3);
-        CK(launch_multidot(c->Vk, n2, j + 1, w, n2, c->partial, c->stream));
-        CK(launch_reduce_partials(c->partial, j + 1, c->dh, 0, c->stream));
-      }
-      {
-        ProfScope ps(c, 4);
-        CK(launch_multiaxpy(c->Vk, n2, j + 1, c->dh, w, n2, nullptr, c->stream));
-      }
-      {
-        ProfScope ps(c, 3);
-        CK(launch_multidot(c->Vk, n2, j + 1, w, n2, c->partial, c->stream));
-        CK(launch_reduce_partials(c->partial, j + 1, c->dh + (R + 1), 0, c->stream));
-      }
-      {
-        ProfScope ps(c, 4);
-        CK(launch_multiaxpy(c->Vk, n2, j + 1, c->dh + (R + 1), w, n2, c->partial + (size_t)(R + 1) * RED_BLOCKS,
-                            c->stream));
-      }
-      CK(launch_finish_norm(c->partial + (size_t)(R + 1) * RED_BLOCKS, c->dnrm, c->stream));
-      CK(launch_scale_by_inv(w, c->dnrm, w, n2, c->stream));
-      // host: h = h1 + h2, hnext
-      CK(cudaMemcpyAsync(c->hpin, c->dh, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(c->hpin + (R + 1), c->dh + (R + 1), (j + 1) * sizeof(double), cudaMemcpyDeviceToHost,
-                         c->stream));
-      CK(cudaMemcpyAsync(c->hpin + 2 * (R + 1), c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
+      // classical Gram-Schmidt with selective reorthogonalisation: a second
+      // pass only when the first cancelled more than 1/sqrt(2) of ||w||
+      // (Daniel-Gragg-Kaufman-Stewart criterion; the oracle uses MGS)
       double* Hc = &H[(size_t)j * (R + 1)];   // column j, length R+1
-      for (int i = 0; i <= j; ++i) Hc[i] = c->hpin[i] + c->hpin[(R + 1) + i];
-      const double hnext = c->hpin[2 * (R + 1)];
+      double hnext = 0.0;
+      for (int pass = 0; pass < 2; ++pass) {
+        const int nb = arnoldi_dot_blocks(n2);
+        {
+          ProfScope ps(c, 3, (double)(j + 2) * n2 * 8.0);
+          CK(launch_arnoldi_dots(c->Vk, n2, j + 1, w, n2, c->partial, c->stream));
+          CK(launch_reduce_partials_n(c->partial, j + 2, nb, c->dh, c->stream));
+        }
+        {
+          ProfScope ps(c, 4, (double)(j + 3) * n2 * 8.0);
+          CK(launch_arnoldi_axpy(c->Vk, n2, j + 1, c->dh, w, n2, c->partial, c->stream));
+          CK(launch_finish_sqrt(c->partial, nb, c->dnrm, c->stream));
+        }
+        CK(cudaMemcpyAsync(c->hpin, c->dh, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->hpin + (R + 2), c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i <= j; ++i) Hc[i] = (pass ? Hc[i] : 0.0) + c->hpin[i];
+        const double wn_before = std::sqrt(c->hpin[j + 1]);
+        hnext = c->hpin[R + 2];
+        if (!(hnext < 0.70710678118654752 * wn_before)) break;
+      }
+      CK(launch_scale_by_inv(w, c->dnrm, w, n2, c->stream));
       if (!std::isfinite(hnext)) return fail(c, HBPDC_E_NONFINITE, "non-finite Arnoldi norm");
       Hc[j + 1] = hnext;
       for (int i = 0; i < j; ++i) {
@@ -461,9 +459,16 @@ hbpdc_status newton(hbpdc_ctx* c, double a1, double a2, double dt, const double*
     A.W = W; A.out1 = sg;
     CKS(run_op(c, OP_R1, A));
   }
-  double bn;
+  double bn, rabs;
   CKS(norm_host(c, b, n, &bn));
-  const double floor = c->op.newton_floor * EPS_MACH * bn;
+  {
+    OpArgs A = base_args(c);
+    A.W = W; A.out1 = c->G;            // G is scratch here
+    CKS(run_op(c, OP_R1ABS, A));
+  }
+  CKS(norm_host(c, c->G, n, &rabs));
+  // floor = max(64 eps ||b||, 4 eps ||R1_abs(W_g)||)   (readings R10, R10b)
+  const double floor = std::max(c->op.newton_floor * EPS_MACH * bn, 4.0 * EPS_MACH * rabs);
   double g0 = -1.0;
   for (int r = 0; r <= c->op.newton_max; ++r) {
     {
@@ -471,7 +476,7 @@ hbpdc_status newton(hbpdc_ctx* c, double a1, double a2, double dt, const double*
       A.W = W; A.S = sg; A.b = b; A.out1 = c->G; A.out2 = c->G + n;
       A.a1dt = a1 * dt;
       A.c2 = a2 * dt * dt / 2.0;
-      ProfScope ps(c, 2);
+      ProfScope ps(c, 2, 5.0 * n * 8.0);
       CKS(run_op(c, OP_RESID, A));
     }
     double gn;
@@ -602,7 +607,7 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
   CKS(dalloc(c, &c->tmp2, n2));
   CKS(dalloc(c, &c->zb, n2));
   CKS(dalloc(c, &c->Vk, (size_t)(R + 1) * n2));
-  CKS(dalloc(c, &c->partial, (size_t)(R + 2) * RED_BLOCKS));
+  CKS(dalloc(c, &c->partial, (size_t)(R + 2) * std::max(arnoldi_dot_blocks(n2), RED_BLOCKS)));
   CKS(dalloc(c, &c->dh, 2 * (size_t)(R + 1)));
   CKS(dalloc(c, &c->dnrm, 1));
   CKS(dalloc(c, &c->deps, 1));
@@ -686,6 +691,10 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->geo.lhp = c->basis.lhp;
   c->geo.lhm = c->basis.lhm;
   for (int i = 0; i < c->P * c->P; ++i) c->geo.Dh[i] = c->basis.Dhat[i];
+  c->geo_abs = c->geo;
+  for (int i = 0; i < c->P * c->P; ++i) c->geo_abs.Dh[i] = std::fabs(c->basis.Dhat[i]);
+  c->geo_abs.lhm = -std::fabs(c->geo.lhm);
+  c->geo_abs.lhp = std::fabs(c->geo.lhp);
   c->cfg.eq = pb->equation;
   c->cfg.dim = pb->dim;
   c->cfg.P = c->P;
@@ -760,7 +769,7 @@ hbpdc_status hbpdc_residual(hbpdc_ctx* c, double a1, double a2, double dt, const
   A.a1dt = a1 * dt;
   A.c2 = a2 * dt * dt / 2.0;
   {
-    ProfScope ps(c, 2);
+    ProfScope ps(c, 2, 5.0 * c->n * 8.0);
     CKS(run_op(c, OP_RESID, A));
   }
   if (norm_out) {
@@ -862,16 +871,24 @@ hbpdc_status hbpdc_profile(hbpdc_ctx* c, int enable) {
   prof_flush(c);
   c->prof_on = enable ? 1 : 0;
   if (enable) {
-    for (int i = 0; i < NPROF; ++i) { c->prof_launch[i] = 0; c->prof_ms[i] = 0.0; }
+    for (int i = 0; i < NPROF; ++i) { c->prof_launch[i] = 0; c->prof_ms[i] = 0.0; c->prof_bytes[i] = 0.0; }
   }
   return HBPDC_OK;
 }
 
-hbpdc_status hbpdc_profile_read(hbpdc_ctx* c, int id, long long* launches, double* total_ms) {
+hbpdc_status hbpdc_profile_read(hbpdc_ctx* c, int id, long long* launches, double* total_ms,
+                                double* alg_bytes) {
   if (!c || id < 0 || id >= NPROF) return HBPDC_E_ARG;
   prof_flush(c);
   if (launches) *launches = c->prof_launch[id];
   if (total_ms) *total_ms = c->prof_ms[id];
+  if (alg_bytes) *alg_bytes = c->prof_bytes[id];
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_launch_count(long long* count) {
+  if (!count) return HBPDC_E_ARG;
+  *count = g_hbpdc_launches;
   return HBPDC_OK;
 }
 

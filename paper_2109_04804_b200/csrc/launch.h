@@ -6,7 +6,8 @@
 struct Geo;
 struct OpArgs;
 
-enum OpKind { OP_R1 = 0, OP_R12, OP_RESID, OP_JVP_EXACT, OP_JVP_FD, OP_JVP_LINEAR, OP_KAPPLY, OP_NKINDS };
+// OP_R1ABS needs a Geo with |Dhat| and lhm negated (see hbpdc.cu)
+enum OpKind { OP_R1 = 0, OP_R12, OP_RESID, OP_JVP_EXACT, OP_JVP_FD, OP_JVP_LINEAR, OP_KAPPLY, OP_R1ABS, OP_NKINDS };
 
 struct OpCfg {
   int eq, dim, P;
@@ -37,6 +38,19 @@ cudaError_t launch_block_gemv2(const double* S, int shared, const double* W, con
 // count, fixed order): deterministic.
 constexpr int RED_BLOCKS = 592;         // 4 x 148 SMs
 constexpr int RED_THREADS = 256;
+// Arnoldi kernels: per-chunk partials part[k * nb + b], nb = arnoldi_dot_blocks(L)
+int arnoldi_dot_blocks(size_t L);
+// h_k = V_k . w (k < nk) and w . w (k = nk) -> part, nk + 1 rows
+cudaError_t launch_arnoldi_dots(const double* V, size_t ldx, int nk, const double* w, size_t L, double* part,
+                                cudaStream_t st);
+// out[k] = sum_b part[k * nb + b]
+cudaError_t launch_reduce_partials_n(const double* part, int nk, int nb, double* out, cudaStream_t st);
+// w -= sum_k h_k V_k (h on device); per-chunk partial sums of the new w . w -> sq_part[nb]
+cudaError_t launch_arnoldi_axpy(const double* V, size_t ldx, int nk, const double* h, double* w, size_t L,
+                                double* sq_part, cudaStream_t st);
+// out = sqrt(sum part[0..nb))
+cudaError_t launch_finish_sqrt(const double* part, int nb, double* out, cudaStream_t st);
+
 // partial[k * RED_BLOCKS + b] = sum over block b of X_k . y   (k < nk), X_k = X + k*ldx
 cudaError_t launch_multidot(const double* X, size_t ldx, int nk, const double* y, size_t L,
                             double* partial, cudaStream_t st);
@@ -65,3 +79,7 @@ cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, c
 cudaError_t launch_stage_combo(const double* base, int nx, const double* const* X, const double* a,
                                int ny, const double* const* Y, const double* b, double* y, size_t L,
                                cudaStream_t st);
+
+// kernel-launch counter (reported by hbpdc_launch_count)
+extern long long g_hbpdc_launches;
+inline void hbpdc_count_launch() { ++g_hbpdc_launches; }

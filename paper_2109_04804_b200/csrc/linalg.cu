@@ -2,6 +2,8 @@
 #include <cstdint>
 #include "launch.h"
 
+long long g_hbpdc_launches = 0;
+
 // ============================================================================
 // Batched Gauss-Jordan inversion with partial pivoting ("we calculate
 // those inverses via LU-decomposition"; any pivoted elimination gives the same
@@ -169,6 +171,7 @@ cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, c
   if (m > GJ_MMAX || m < 1) return cudaErrorInvalidValue;
   if (nmat <= 0) return cudaSuccess;
   gj_kernel<<<nmat, GJ_T, 0, st>>>(Z, S, m, info);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -264,6 +267,7 @@ cudaError_t launch_block_gemv2(const double* S, int shared, const double* W, con
     default: return cudaErrorInvalidValue;
   }
 #undef G
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -282,6 +286,166 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   }
   __syncthreads();
   return s;   // valid in thread 0
+}
+
+// ---- Arnoldi multi-dot: h_k = V_k . w for k < nk, plus w . w (k = nk) -------------
+// Each CTA owns a chunk of 256 x DOT_T elements of w in registers (w is read
+// once), streams V_k over that chunk for every k, and reduces DOT_KB dot
+// products at a time (warp butterfly + one shared-memory pass).  Partials
+// go to part[k * gridDim.x + block]; launch_reduce_partials_n finishes them.
+constexpr int DOT_T = 8;
+constexpr int DOT_KB = 8;
+
+__global__ void __launch_bounds__(256) arnoldi_dots_kernel(const double* __restrict__ V, size_t ldx, int nk,
+                                                           const double* __restrict__ w, size_t L,
+                                                           double* __restrict__ part) {
+  __shared__ double red[8][DOT_KB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t base = (size_t)blockIdx.x * (256 * DOT_T) + threadIdx.x;
+  double wr[DOT_T];
+#pragma unroll
+  for (int t = 0; t < DOT_T; ++t) {
+    const size_t i = base + (size_t)t * 256;
+    wr[t] = i < L ? w[i] : 0.0;
+  }
+  for (int k0 = 0; k0 <= nk; k0 += DOT_KB) {
+    double acc[DOT_KB];
+#pragma unroll
+    for (int q = 0; q < DOT_KB; ++q) {
+      const int k = k0 + q;
+      double a = 0.0;
+      if (k < nk) {
+        const double* vk = V + (size_t)k * ldx;
+#pragma unroll
+        for (int t = 0; t < DOT_T; ++t) {
+          const size_t i = base + (size_t)t * 256;
+          if (i < L) a = fma(__ldg(vk + i), wr[t], a);
+        }
+      } else if (k == nk) {
+#pragma unroll
+        for (int t = 0; t < DOT_T; ++t) a = fma(wr[t], wr[t], a);
+      }
+      acc[q] = a;
+    }
+#pragma unroll
+    for (int q = 0; q < DOT_KB; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < DOT_KB; ++q) red[wid][q] = acc[q];
+    __syncthreads();
+    if (threadIdx.x < DOT_KB && k0 + (int)threadIdx.x <= nk) {
+      double s = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) s += red[ww][threadIdx.x];
+      part[(size_t)(k0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+int arnoldi_dot_blocks(size_t L) { return (int)((L + 256 * DOT_T - 1) / (256 * DOT_T)); }
+
+cudaError_t launch_arnoldi_dots(const double* V, size_t ldx, int nk, const double* w, size_t L, double* part,
+                                cudaStream_t st) {
+  arnoldi_dots_kernel<<<arnoldi_dot_blocks(L), 256, 0, st>>>(V, ldx, nk, w, L, part);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+// out[k] = sum_b part[k * nb + b], k < nk (deterministic order)
+__global__ void reduce_partials_n_kernel(const double* __restrict__ part, int nb, double* out) {
+  __shared__ double sh[8];
+  const int k = blockIdx.x;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 256) v += part[(size_t)k * nb + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += sh[q];
+    out[k] = s;
+  }
+}
+
+cudaError_t launch_reduce_partials_n(const double* part, int nk, int nb, double* out, cudaStream_t st) {
+  if (nk <= 0) return cudaSuccess;
+  reduce_partials_n_kernel<<<nk, 256, 0, st>>>(part, nb, out);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+// ---- Arnoldi update: w -= sum_k h_k V_k, and partial sums of the new w . w ---------
+__global__ void __launch_bounds__(256) arnoldi_axpy_kernel(const double* __restrict__ V, size_t ldx, int nk,
+                                                           const double* __restrict__ h, double* __restrict__ w,
+                                                           size_t L, double* __restrict__ sq) {
+  __shared__ double hs[1024];
+  __shared__ double red[8];
+  for (int k = threadIdx.x; k < nk && k < 1024; k += 256) hs[k] = h[k];
+  __syncthreads();
+  const size_t base = (size_t)blockIdx.x * (256 * DOT_T) + threadIdx.x;
+  double acc[DOT_T];
+#pragma unroll
+  for (int t = 0; t < DOT_T; ++t) {
+    const size_t i = base + (size_t)t * 256;
+    acc[t] = i < L ? w[i] : 0.0;
+  }
+  for (int k = 0; k < nk; ++k) {
+    const double hk = k < 1024 ? hs[k] : h[k];
+    const double* vk = V + (size_t)k * ldx;
+#pragma unroll
+    for (int t = 0; t < DOT_T; ++t) {
+      const size_t i = base + (size_t)t * 256;
+      if (i < L) acc[t] = fma(-hk, __ldg(vk + i), acc[t]);
+    }
+  }
+  double ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < DOT_T; ++t) {
+    const size_t i = base + (size_t)t * 256;
+    if (i < L) { w[i] = acc[t]; ss = fma(acc[t], acc[t], ss); }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += red[q];
+    sq[blockIdx.x] = s;
+  }
+}
+
+cudaError_t launch_arnoldi_axpy(const double* V, size_t ldx, int nk, const double* h, double* w, size_t L,
+                                double* sq_part, cudaStream_t st) {
+  arnoldi_axpy_kernel<<<arnoldi_dot_blocks(L), 256, 0, st>>>(V, ldx, nk, h, w, L, sq_part);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+// out = sqrt(sum part[0..nb))  (and c / that, if c_fd > 0, into out_fd)
+__global__ void finish_sqrt_kernel(const double* __restrict__ part, int nb, double* out) {
+  __shared__ double sh[8];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 256) v += part[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += sh[q];
+    *out = sqrt(s);
+  }
+}
+
+cudaError_t launch_finish_sqrt(const double* part, int nb, double* out, cudaStream_t st) {
+  finish_sqrt_kernel<<<1, 256, 0, st>>>(part, nb, out);
+  hbpdc_count_launch();
+  return cudaGetLastError();
 }
 
 // partial[k][b] for k in [k0, k0 + KB)
@@ -312,7 +476,9 @@ cudaError_t launch_multidot(const double* X, size_t ldx, int nk, const double* y
                             cudaStream_t st) {
   for (int k0 = 0; k0 < nk; k0 += 8) {
     multidot_kernel<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(X, ldx, k0, nk, y, L, partial);
+    if (k0 > 0) hbpdc_count_launch();
   }
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -328,6 +494,7 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partial, int n
 cudaError_t launch_reduce_partials(const double* partial, int nk, double* out, int accumulate, cudaStream_t st) {
   if (nk <= 0) return cudaSuccess;
   reduce_partials_kernel<<<nk, RED_THREADS, 0, st>>>(partial, nk, out, accumulate);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -356,6 +523,7 @@ __global__ void __launch_bounds__(RED_THREADS) multiaxpy_kernel(const double* __
 cudaError_t launch_multiaxpy(const double* X, size_t ldx, int nk, const double* h, double* y, size_t L,
                              double* sq_partial, cudaStream_t st) {
   multiaxpy_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(X, ldx, nk, h, y, L, sq_partial);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -372,6 +540,7 @@ __global__ void lincomb_kernel(const double* __restrict__ X, size_t ldx, int nk,
 cudaError_t launch_lincomb(const double* X, size_t ldx, int nk, const double* c, double* y, size_t L,
                            cudaStream_t st) {
   lincomb_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(X, ldx, nk, c, y, L);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -385,6 +554,7 @@ __global__ void scale_inv_kernel(const double* __restrict__ x, const double* __r
 
 cudaError_t launch_scale_by_inv(const double* x, const double* nrm, double* y, size_t L, cudaStream_t st) {
   scale_inv_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(x, nrm, y, L);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -395,6 +565,7 @@ __global__ void axpby_kernel(double a, const double* __restrict__ x, double b, d
 
 cudaError_t launch_axpby(double a, const double* x, double b, double* y, size_t L, cudaStream_t st) {
   axpby_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, x, b, y, L);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -407,6 +578,7 @@ __global__ void waxpby_kernel(double a, const double* __restrict__ x, double b, 
 cudaError_t launch_waxpby(double a, const double* x, double b, const double* z, double* y, size_t L,
                           cudaStream_t st) {
   waxpby_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, x, b, z, y, L);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -422,6 +594,7 @@ __global__ void __launch_bounds__(RED_THREADS) sumsq_kernel(const double* __rest
 
 cudaError_t launch_sumsq(const double* x, size_t L, double* partial, cudaStream_t st) {
   sumsq_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(x, L, partial);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -435,6 +608,7 @@ __global__ void finish_norm_kernel(const double* __restrict__ partial, double* o
 
 cudaError_t launch_finish_norm(const double* partial, double* out, cudaStream_t st) {
   finish_norm_kernel<<<1, RED_THREADS, 0, st>>>(partial, out);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -449,6 +623,7 @@ __global__ void finish_fd_eps_kernel(const double* __restrict__ partial, double 
 
 cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st) {
   finish_fd_eps_kernel<<<1, RED_THREADS, 0, st>>>(partial, c, out);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -480,5 +655,6 @@ cudaError_t launch_stage_combo(const double* base, int nx, const double* const* 
   for (int k = 0; k < nx; ++k) { A.X[k] = X[k]; A.a[k] = a[k]; }
   for (int k = 0; k < ny; ++k) { A.Y[k] = Y[k]; A.b[k] = b[k]; }
   stage_combo_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(A, y, L);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }

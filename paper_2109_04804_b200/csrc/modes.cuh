@@ -65,6 +65,28 @@ template <int EQ, int NODES> struct ModeR1 {
   }
 };
 
+// R1_abs(W): every term of eq:DGSEM_wt by magnitude (|Dhat| via the Geo, |F|,
+// |f*|); the rounding scale of R1 used for the Newton floor (reading R10b).
+template <int EQ, int NODES> struct ModeR1Abs : ModeR1<EQ, NODES> {
+  using Base = ModeR1<EQ, NODES>;
+  static constexpr int NV = Base::NV, NCH = 1;
+  using typename Base::State;
+  __device__ static void vol(const OpArgs&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
+    double F[NV];
+    vol_flux<EQ>(pp, st.s, d, F);
+    for (int v = 0; v < NV; ++v) c[0][v] = fabs(F[v]);
+  }
+  __device__ static void face(const OpArgs&, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    double f[NV];
+    face_flux<EQ>(pp, L.s, R.s, d, f);
+    for (int v = 0; v < NV; ++v) c[0][v] = fabs(f[v]);
+  }
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) A.out1[IDX(e, v, node)] = -o[0][v];
+  }
+};
+
 // R1(W) and R2(W, sigma) from one dual evaluation             (eq:DGSEM_wtt)
 template <int EQ, int NODES> struct ModeR12 {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;

@@ -13,6 +13,7 @@ static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
   const int grid = (g.nE + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
   op_kernel<EQ, DIM, P, Mode, EPB><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, g);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -23,6 +24,7 @@ static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, doubl
   const int grid = (g.nE + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
   lift_kernel<P, Mode, K, EPB><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, g, G);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -106,6 +108,7 @@ static cudaError_t run_kbuild(const OpCfg& c, const Geo& g, const double* Wb, do
   constexpr int EPB = epb_for(NODES);
   if (ne <= 0) return cudaSuccess;
   kbuild_kernel<EQ, DIM, P, EPB><<<ne, EPB * NODES, 0, c.stream>>>(Wb, c.pp, g, a1dt, c2, M, e0);
+  hbpdc_count_launch();
   return cudaGetLastError();
 }
 
@@ -115,6 +118,7 @@ template <int EQ, int DIM, int P> struct Disp {
   static cudaError_t op(OpKind k, const OpCfg& c, const Geo& g, const OpArgs& A) {
     switch (k) {
       case OP_R1: return run_op<EQ, DIM, P, ModeR1<EQ, NODES>>(c, g, A);
+      case OP_R1ABS: return run_op<EQ, DIM, P, ModeR1Abs<EQ, NODES>>(c, g, A);
       case OP_R12: return run_op<EQ, DIM, P, ModeR12<EQ, NODES>>(c, g, A);
       case OP_RESID: return run_op<EQ, DIM, P, ModeResid<EQ, NODES>>(c, g, A);
       case OP_JVP_EXACT: return run_op<EQ, DIM, P, ModeJvpExact<EQ, NODES>>(c, g, A);
@@ -131,7 +135,7 @@ template <int EQ, int DIM, int P> struct Disp {
   static cudaError_t lift(OpKind k, int s, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
     if constexpr (EQ == 2 && DIM == 2) {
       switch (k) {
-        case OP_R1: return run_lift<P, ModeR1<EQ, NODES>, 0>(c, g, A, G);
+        case OP_R1: case OP_R1ABS: return run_lift<P, ModeR1<EQ, NODES>, 0>(c, g, A, G);
         case OP_R12: return run_lift<P, ModeR12<EQ, NODES>, 0>(c, g, A, G);
         case OP_RESID: return run_lift<P, ModeResid<EQ, NODES>, 0>(c, g, A, G);
         case OP_JVP_EXACT: return run_lift<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, G);
@@ -174,7 +178,7 @@ cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, co
 
 int lift_jet_components(OpKind kind, int state) {
   switch (kind) {
-    case OP_R1: return 1;
+    case OP_R1: case OP_R1ABS: return 1;
     case OP_R12: case OP_RESID: return 2;
     case OP_JVP_EXACT: return 4;
     case OP_JVP_FD: return state == 0 ? 2 : 3;

@@ -28,7 +28,7 @@ STATUS = {0: "OK", 1: "E_ARG", 2: "E_CUDA", 3: "E_NCCL", 4: "E_OOM", 5: "E_NONFI
 EXPORTS = ["hbpdc_init", "hbpdc_local_shape", "hbpdc_node_coords", "hbpdc_rhs", "hbpdc_residual",
            "hbpdc_jvp", "hbpdc_precond_build", "hbpdc_precond_set", "hbpdc_precond_export",
            "hbpdc_precond_apply", "hbpdc_step", "hbpdc_step_host", "hbpdc_reset", "hbpdc_profile",
-           "hbpdc_profile_read", "hbpdc_last_error", "hbpdc_finalize"]
+           "hbpdc_profile_read", "hbpdc_launch_count", "hbpdc_last_error", "hbpdc_finalize"]
 
 
 class Problem(ctypes.Structure):
@@ -95,7 +95,9 @@ def load():
         "hbpdc_step_host": (I, [P, D, P, ctypes.POINTER(StepStats)]),
         "hbpdc_reset": (I, [P]),
         "hbpdc_profile": (I, [P, I]),
-        "hbpdc_profile_read": (I, [P, I, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(D)]),
+        "hbpdc_profile_read": (I, [P, I, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(D),
+                                   ctypes.POINTER(D)]),
+        "hbpdc_launch_count": (I, [ctypes.POINTER(ctypes.c_longlong)]),
         "hbpdc_last_error": (ctypes.c_char_p, [P]),
         "hbpdc_finalize": (V, [P]),
     }
@@ -105,6 +107,13 @@ def load():
         f.argtypes = args
     _lib = lib
     return lib
+
+
+def launch_count():
+    """Kernels launched by the library in this process so far."""
+    n = ctypes.c_longlong()
+    load().hbpdc_launch_count(ctypes.byref(n))
+    return n.value
 
 
 class HbpdcError(RuntimeError):
@@ -255,11 +264,17 @@ class Context:
     def profile(self, enable):
         self._check(self.lib.hbpdc_profile(self.h, int(enable)))
 
+    PROFILE_IDS = {"gemv": 0, "jvp": 1, "residual": 2, "arnoldi_dots": 3, "arnoldi_update": 4,
+                   "kapply": 5, "build": 6}
+
     def profile_read(self, kernel_id):
+        """(launches, total_ms, algorithmic_bytes) of a profiled kernel id."""
         n = ctypes.c_longlong()
         ms = ctypes.c_double()
-        self._check(self.lib.hbpdc_profile_read(self.h, kernel_id, ctypes.byref(n), ctypes.byref(ms)))
-        return n.value, ms.value
+        by = ctypes.c_double()
+        self._check(self.lib.hbpdc_profile_read(self.h, kernel_id, ctypes.byref(n), ctypes.byref(ms),
+                                                ctypes.byref(by)))
+        return n.value, ms.value, by.value
 
     def close(self):
         if self.h and self.h.value:
