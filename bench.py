@@ -166,6 +166,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    # one dedicated stream for torch and the library (no legacy-default-stream syncs)
+    torch.cuda.set_stream(torch.cuda.Stream(device=local))
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = configs.CONFIGS[CONFIG]

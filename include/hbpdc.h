@@ -96,8 +96,9 @@ typedef struct {
   int rank, nranks;            /* this rank, number of ranks                          */
   int px, py;                  /* rank grid: px * py == nranks, nx % px == ny % py == 0 */
   const void* nccl_unique_id;  /* 128-byte ncclUniqueId (rank 0's), NULL if nranks==1 */
-  void* cuda_stream;           /* cudaStream_t to enqueue on, NULL = library stream  */
+  void* cuda_stream;           /* cudaStream_t to enqueue on (NULL = legacy default)  */
   int device;                  /* CUDA device ordinal                                 */
+  int own_stream;              /* 1: ignore cuda_stream, the library creates a stream */
 } hbpdc_dist;
 
 typedef struct {               /* summed over one hbpdc_step                          */

@@ -651,7 +651,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->pb = *pb;
   c->op = *op;
   if (ds) c->ds = *ds;
-  else { c->ds.rank = 0; c->ds.nranks = 1; c->ds.px = 1; c->ds.py = 1; }
+  else { c->ds.rank = 0; c->ds.nranks = 1; c->ds.px = 1; c->ds.py = 1; c->ds.own_stream = 1; }
   auto bad = [&](const char* msg) {
     c->err = msg;
     *out = c;   // return the context so the caller can read the message
@@ -706,8 +706,8 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->cfg.pp.lamT = (c->cfg.pp.Rgas * pb->gamma / (pb->gamma - 1.0)) * pb->mu / (pb->prandtl > 0 ? pb->prandtl : 1.0);
   cudaError_t e = cudaSetDevice(c->ds.device);
   if (e != cudaSuccess) { c->err = cudaGetErrorString(e); *out = c; return HBPDC_E_CUDA; }
-  if (c->ds.cuda_stream) {
-    c->stream = (cudaStream_t)c->ds.cuda_stream;
+  if (!c->ds.own_stream) {
+    c->stream = (cudaStream_t)c->ds.cuda_stream;   // NULL = legacy default stream
   } else {
     e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) { c->err = cudaGetErrorString(e); *out = c; return HBPDC_E_CUDA; }

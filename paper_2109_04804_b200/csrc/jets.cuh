@@ -127,6 +127,18 @@ __device__ __forceinline__ HJ jsqrt(HJ x) {
 }
 __device__ __forceinline__ HJ jmax(HJ x, HJ y) { return x.v >= y.v ? x : y; }
 
+// 1/x with one fp64 division per carrier
+__device__ __forceinline__ double jrecip(double x) { return 1.0 / x; }
+__device__ __forceinline__ J1 jrecip(J1 x) {
+  const double r = 1.0 / x.v;
+  return {r, -r * r * x.a};
+}
+__device__ __forceinline__ J2 jrecip(J2 x) {
+  const double r = 1.0 / x.v, r2 = -r * r;
+  return {r, r2 * x.a, r2 * x.b};
+}
+__device__ __forceinline__ HJ jrecip(HJ x) { return hj_recip(x); }
+
 template <class T> __device__ __forceinline__ T jconst(double v);
 template <> __device__ __forceinline__ double jconst<double>(double v) { return v; }
 template <> __device__ __forceinline__ J1 jconst<J1>(double v) { return {v, 0.0}; }

@@ -1,8 +1,8 @@
 // modes.cuh -- what each operator of the hot path feeds the element evaluator.
 //
 // A mode defines: the node State (one or two jets + NS gradients), NCH output
-// channels, how the volume/face fluxes reduce to those channels, and the
-// epilogue.  Notation: L(.) is the DGSEM operator on a flux field, so
+// channels, how the volume/face fluxes reduce to those channels ("comb"), and
+// the epilogue.  Notation: L(.) is the DGSEM operator on a flux field, so
 // R1(W) = L(F(W)); a1dt = alpha1 dt; c2 = alpha2 dt^2 / 2.
 #pragma once
 #include <type_traits>
@@ -35,52 +35,57 @@ __device__ __forceinline__ void ld_state(const double* G, int e, int node, NodeS
 
 #define IDX(e, v, node) ((size_t)(e) * A.m + (v) * NODES + (node))
 
-// R1(W)                                                        (eq:DGSEM_wt)
-template <int EQ, int NODES> struct ModeR1 {
-  static constexpr int NV = NVars<EQ>::value, NCH = 1;
+// Single-jet modes: Derived supplies  using J; load_w; comb(A, const J* F, c).
+template <int EQ, int NODES, class Derived, class J, int NCH_>
+struct OneJetMode {
+  static constexpr int NV = NVars<EQ>::value, NCH = NCH_;
   using Args = OpArgs;
-  template <int K> using StateT = double;
-  struct State { NodeState<EQ, double> s; };
+  template <int K> using StateT = J;
+  struct State { NodeState<EQ, J> s; };
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
+    Derived::template load_w<0>(A, e, node, st.s.w, nbr);
+    ld_state<EQ, J, NODES>(A.G0, e, node, st.s);
+  }
+  template <int DIM>
+  __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, double (&c)[DIM][NCH][NV]) {
+    J F[DIM][NV];
+    vol_flux_all<EQ, DIM>(pp, st.s, F);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) Derived::comb(A, F[d], c[d]);
+  }
+  __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
+                              double (&c)[NCH][NV]) {
+    J f[NV];
+    face_flux<EQ>(pp, L.s, R.s, d, f);
+    Derived::comb(A, f, c);
+  }
+};
+
+// R1(W)                                                        (eq:DGSEM_wt)
+template <int EQ, int NODES> struct ModeR1 : OneJetMode<EQ, NODES, ModeR1<EQ, NODES>, double, 1> {
+  static constexpr int NV = NVars<EQ>::value, NCH = 1;
   template <int K>
-  __device__ static void load_w(const Args& A, int e, int node, double* w, bool) {
+  __device__ static void load_w(const OpArgs& A, int e, int node, double* w, bool) {
     for (int v = 0; v < NV; ++v) w[v] = A.W[IDX(e, v, node)];
   }
-  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
-    load_w<0>(A, e, node, st.s.w, nbr);
-    ld_state<EQ, double, NODES>(A.G0, e, node, st.s);
-  }
-  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    double F[NV];
-    vol_flux<EQ>(pp, st.s, d, F);
+  __device__ static void comb(const OpArgs&, const double* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) c[0][v] = F[v];
   }
-  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
-    double f[NV];
-    face_flux<EQ>(pp, L.s, R.s, d, f);
-    for (int v = 0; v < NV; ++v) c[0][v] = f[v];
-  }
-  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) A.out1[IDX(e, v, node)] = o[0][v];
   }
 };
 
 // R1_abs(W): every term of eq:DGSEM_wt by magnitude (|Dhat| via the Geo, |F|,
 // |f*|); the rounding scale of R1 used for the Newton floor (reading R10b).
-template <int EQ, int NODES> struct ModeR1Abs : ModeR1<EQ, NODES> {
-  using Base = ModeR1<EQ, NODES>;
-  static constexpr int NV = Base::NV, NCH = 1;
-  using typename Base::State;
-  __device__ static void vol(const OpArgs&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    double F[NV];
-    vol_flux<EQ>(pp, st.s, d, F);
-    for (int v = 0; v < NV; ++v) c[0][v] = fabs(F[v]);
+template <int EQ, int NODES> struct ModeR1Abs : OneJetMode<EQ, NODES, ModeR1Abs<EQ, NODES>, double, 1> {
+  static constexpr int NV = NVars<EQ>::value, NCH = 1;
+  template <int K>
+  __device__ static void load_w(const OpArgs& A, int e, int node, double* w, bool) {
+    for (int v = 0; v < NV; ++v) w[v] = A.W[IDX(e, v, node)];
   }
-  __device__ static void face(const OpArgs&, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
-    double f[NV];
-    face_flux<EQ>(pp, L.s, R.s, d, f);
-    for (int v = 0; v < NV; ++v) c[0][v] = fabs(f[v]);
+  __device__ static void comb(const OpArgs&, const double* F, double (&c)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) c[0][v] = fabs(F[v]);
   }
   __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) A.out1[IDX(e, v, node)] = -o[0][v];
@@ -88,31 +93,16 @@ template <int EQ, int NODES> struct ModeR1Abs : ModeR1<EQ, NODES> {
 };
 
 // R1(W) and R2(W, sigma) from one dual evaluation             (eq:DGSEM_wtt)
-template <int EQ, int NODES> struct ModeR12 {
+template <int EQ, int NODES> struct ModeR12 : OneJetMode<EQ, NODES, ModeR12<EQ, NODES>, J1, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
-  using Args = OpArgs;
-  template <int K> using StateT = J1;
-  struct State { NodeState<EQ, J1> s; };
   template <int K>
-  __device__ static void load_w(const Args& A, int e, int node, J1* w, bool) {
+  __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool) {
     for (int v = 0; v < NV; ++v) w[v] = J1{A.W[IDX(e, v, node)], A.S[IDX(e, v, node)]};
   }
-  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
-    load_w<0>(A, e, node, st.s.w, nbr);
-    ld_state<EQ, J1, NODES>(A.G0, e, node, st.s);
-  }
-  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    J1 F[NV];
-    vol_flux<EQ>(pp, st.s, d, F);
+  __device__ static void comb(const OpArgs&, const J1* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) { c[0][v] = F[v].v; c[1][v] = F[v].a; }
   }
-  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
-    J1 f[NV];
-    face_flux<EQ>(pp, L.s, R.s, d, f);
-    for (int v = 0; v < NV; ++v) { c[0][v] = f[v].v; c[1][v] = f[v].a; }
-  }
-  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       if (A.out1) A.out1[IDX(e, v, node)] = o[0][v];
       A.out2[IDX(e, v, node)] = o[1][v];
@@ -122,37 +112,19 @@ template <int EQ, int NODES> struct ModeR12 {
 
 // Stage residual: G1 = W - b + L(-a1dt F + c2 F'sigma), G2 = sigma - L(F)
 // (eq:Newton_Residual; P:236-239 read as R4)
-template <int EQ, int NODES> struct ModeResid {
+template <int EQ, int NODES> struct ModeResid : OneJetMode<EQ, NODES, ModeResid<EQ, NODES>, J1, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
-  using Args = OpArgs;
-  template <int K> using StateT = J1;
-  struct State { NodeState<EQ, J1> s; };
   template <int K>
-  __device__ static void load_w(const Args& A, int e, int node, J1* w, bool) {
+  __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool) {
     for (int v = 0; v < NV; ++v) w[v] = J1{A.W[IDX(e, v, node)], A.S[IDX(e, v, node)]};
   }
-  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
-    load_w<0>(A, e, node, st.s.w, nbr);
-    ld_state<EQ, J1, NODES>(A.G0, e, node, st.s);
-  }
-  __device__ static void comb(const Args& A, const J1* F, double (&c)[NCH][NV]) {
+  __device__ static void comb(const OpArgs& A, const J1* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       c[0][v] = fma(A.c2, F[v].a, -A.a1dt * F[v].v);
       c[1][v] = F[v].v;
     }
   }
-  __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    J1 F[NV];
-    vol_flux<EQ>(pp, st.s, d, F);
-    comb(A, F, c);
-  }
-  __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
-    J1 f[NV];
-    face_flux<EQ>(pp, L.s, R.s, d, f);
-    comb(A, f, c);
-  }
-  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
       A.out1[k] = (A.W[k] - A.b[k]) + o[0][v];
@@ -164,40 +136,22 @@ template <int EQ, int NODES> struct ModeResid {
 // EXACT JVP.  Hyper-dual input W + e1 sigma + e2 dW + e1e2 dsigma gives
 //   b-part = dR1/dW dW,   c-part = dR2/dW dW + dR2/dsigma dsigma
 // so  top = dW + L(-a1dt F_b + c2 F_c),  bottom = dsigma - L(F_b)   (eq:nonlinear_eqsys)
-template <int EQ, int NODES> struct ModeJvpExact {
+template <int EQ, int NODES> struct ModeJvpExact : OneJetMode<EQ, NODES, ModeJvpExact<EQ, NODES>, HJ, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
-  using Args = OpArgs;
-  template <int K> using StateT = HJ;
-  struct State { NodeState<EQ, HJ> s; };
   template <int K>
-  __device__ static void load_w(const Args& A, int e, int node, HJ* w, bool) {
+  __device__ static void load_w(const OpArgs& A, int e, int node, HJ* w, bool) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
       w[v] = HJ{A.W[k], A.S[k], A.dW[k], A.dS[k]};
     }
   }
-  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
-    load_w<0>(A, e, node, st.s.w, nbr);
-    ld_state<EQ, HJ, NODES>(A.G0, e, node, st.s);
-  }
-  __device__ static void comb(const Args& A, const HJ* F, double (&c)[NCH][NV]) {
+  __device__ static void comb(const OpArgs& A, const HJ* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       c[0][v] = fma(A.c2, F[v].c, -A.a1dt * F[v].b);
       c[1][v] = F[v].b;
     }
   }
-  __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    HJ F[NV];
-    vol_flux<EQ>(pp, st.s, d, F);
-    comb(A, F, c);
-  }
-  __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
-    HJ f[NV];
-    face_flux<EQ>(pp, L.s, R.s, d, f);
-    comb(A, f, c);
-  }
-  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
       A.out1[k] = A.dW[k] + o[0][v];
@@ -250,20 +204,54 @@ template <int EQ, int NODES> struct ModeJvpFD {
       for (int v = 0; v < NV; ++v) { c[0][v] = A.c2 * Fq[v].b; c[1][v] = 0.0; }
     }
   }
-  __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    J1 Fp[NV];
-    J2 Fq[NV];
-    vol_flux<EQ>(pp, st.p, d, Fp);
-    vol_flux<EQ>(pp, st.q, d, Fq);
-    comb(A, Fp, Fq, c);
+  template <int DIM>
+  __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, double (&c)[DIM][NCH][NV]) {
+    if constexpr (EQ == 1) {
+      // primitives once per jet state, fluxes one direction at a time (short live ranges)
+      const EulerPrim<J1> qp = euler_prim(pp, st.p.w);
+      const EulerPrim<J2> qq = euler_prim(pp, st.q.w);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        J1 Fp[NV];
+        J2 Fq[NV];
+        euler_flux(st.p.w, qp, d, Fp);
+        euler_flux(st.q.w, qq, d, Fq);
+        comb(A, Fp, Fq, c[d]);
+      }
+    } else {
+      J1 Fp[DIM][NV];
+      J2 Fq[DIM][NV];
+      vol_flux_all<EQ, DIM>(pp, st.p, Fp);
+      vol_flux_all<EQ, DIM>(pp, st.q, Fq);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) comb(A, Fp[d], Fq[d], c[d]);
+    }
   }
   __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
                               double (&c)[NCH][NV]) {
-    J1 fp[NV];
+    // p-face first, folded into the channels, then the q-face: the two jet
+    // states are never live together
+    const double ew = fd_step(A);
+    const double ie = ew > 0.0 ? 1.0 / ew : 0.0;
+    double pv[NV], pa[NV];
+    if (ew > 0.0) {
+      J1 fp[NV];
+      face_flux<EQ>(pp, L.p, R.p, d, fp);
+      for (int v = 0; v < NV; ++v) { pv[v] = fp[v].v; pa[v] = fp[v].a; }
+    }
     J2 fq[NV];
-    face_flux<EQ>(pp, L.p, R.p, d, fp);
     face_flux<EQ>(pp, L.q, R.q, d, fq);
-    comb(A, fp, fq, c);
+    for (int v = 0; v < NV; ++v) {
+      if (ew > 0.0) {
+        const double q1 = (pv[v] - fq[v].v) * ie;
+        const double q2 = (pa[v] - fq[v].a) * ie;
+        c[0][v] = fma(A.c2, q2 + fq[v].b, -A.a1dt * q1);
+        c[1][v] = q1;
+      } else {
+        c[0][v] = A.c2 * fq[v].b;
+        c[1][v] = 0.0;
+      }
+    }
   }
   __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
@@ -292,11 +280,14 @@ template <int EQ, int NODES> struct ModeJvpLinear {
       st.u1.w[v] = A.dW[k];
     }
   }
-  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    double F0[NV], F1[NV];
-    vol_flux<EQ>(pp, st.u0, d, F0);
-    vol_flux<EQ>(pp, st.u1, d, F1);
-    for (int v = 0; v < NV; ++v) { c[0][v] = F0[v]; c[1][v] = F1[v]; }
+  template <int DIM>
+  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, double (&c)[DIM][NCH][NV]) {
+    double F0[DIM][NV], F1[DIM][NV];
+    vol_flux_all<EQ, DIM>(pp, st.u0, F0);
+    vol_flux_all<EQ, DIM>(pp, st.u1, F1);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+      for (int v = 0; v < NV; ++v) { c[d][0][v] = F0[d][v]; c[d][1][v] = F1[d][v]; }
   }
   __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
                               double (&c)[NCH][NV]) {
@@ -318,34 +309,20 @@ template <int EQ, int NODES> struct ModeJvpLinear {
 //   K_i = element-diagonal block of dR1/dW at the build state W_b ("neighbour
 //   traces frozen": the neighbour's jet carries no tangent).
 //   top = U - c2 K V,   bottom = V + K (U - a1dt V).
-template <int EQ, int NODES> struct ModeKApply {
+template <int EQ, int NODES> struct ModeKApply : OneJetMode<EQ, NODES, ModeKApply<EQ, NODES>, J2, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
-  using Args = OpArgs;
-  template <int K> using StateT = J2;
-  struct State { NodeState<EQ, J2> s; };
   template <int K>
-  __device__ static void load_w(const Args& A, int e, int node, J2* w, bool nbr) {
+  __device__ static void load_w(const OpArgs& A, int e, int node, J2* w, bool nbr) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
       if (nbr) w[v] = J2{A.W[k], 0.0, 0.0};
       else w[v] = J2{A.W[k], A.V[k], fma(-A.a1dt, A.V[k], A.U[k])};
     }
   }
-  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
-    load_w<0>(A, e, node, st.s.w, nbr);
-  }
-  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    J2 F[NV];
-    vol_flux<EQ>(pp, st.s, d, F);
+  __device__ static void comb(const OpArgs&, const J2* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) { c[0][v] = F[v].a; c[1][v] = F[v].b; }
   }
-  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
-    J2 f[NV];
-    face_flux<EQ>(pp, L.s, R.s, d, f);
-    for (int v = 0; v < NV; ++v) { c[0][v] = f[v].a; c[1][v] = f[v].b; }
-  }
-  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
       A.out1[k] = fma(-A.c2, o[0][v], A.U[k]);

@@ -47,6 +47,28 @@ template <int EQ, class T> struct NodeState {
   T gx[NG], gy[NG];
 };
 
+// volume flux in all DIM directions (primitives computed once per state)
+template <int EQ, int DIM, class T>
+__device__ __forceinline__ void vol_flux_all(const PhysParams& pp, const NodeState<EQ, T>& s,
+                                             T (&F)[DIM][NVars<EQ>::value]) {
+  if constexpr (EQ == 0) {
+    F[0][0] = pp.ax * s.w[0];
+    if constexpr (DIM == 2) F[1][0] = pp.ay * s.w[0];
+  } else {
+    const EulerPrim<T> q = euler_prim(pp, s.w);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      euler_flux(s.w, q, d, F[d]);
+      if constexpr (EQ == 2) {
+        T Fv[4];
+        viscous_flux_uv(pp, q.u, q.v, s.gx, s.gy, d, Fv);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) F[d][v] = F[d][v] - Fv[v];
+      }
+    }
+  }
+}
+
 template <int EQ, class T>
 __device__ __forceinline__ void vol_flux(const PhysParams& pp, const NodeState<EQ, T>& s, int d, T* F) {
   phys_flux<EQ>(pp, s.w, d, F);
@@ -108,7 +130,18 @@ __device__ __forceinline__ void load_grads(const double* G, int e, int node, T* 
 }
 
 // ---- the element evaluation (one slot, one node per thread) --------------------
-// sF: shared scratch for this slot, NCH * DIM * NV * P * (P+1) doubles.
+// Shared scratch per slot: slot_doubles<...>() = volume-flux planes
+// NCH*DIM*NV*P*(P+1) + face fluxes NCH*NV*2*DIM*P^(DIM-1).
+//   phase 1  every thread: node state -> volume fluxes (NCH channels) -> smem
+//   phase 2  threads 0 .. 2*DIM*P^(DIM-1)-1: one face node each (canonical
+//            LLF flux with the neighbour's trace), pre-scaled surface term -> smem
+//   phase 3  every thread: Dhat contraction + its surface terms
+template <int EQ, int DIM, int P, int NCH>
+__host__ __device__ constexpr int slot_doubles() {
+  return NCH * DIM * NVars<EQ>::value * (DIM == 2 ? P : 1) * (P + 1) +
+         NCH * NVars<EQ>::value * 2 * DIM * (DIM == 2 ? P : 1);
+}
+
 template <int EQ, int DIM, int P, class Mode>
 __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const PhysParams& pp,
                                           const Geo& g, int e, int slot, int node, bool active,
@@ -117,54 +150,47 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
   constexpr int NCH = Mode::NCH;
   constexpr int PS = P + 1;                       // padded row stride (bank conflicts)
   constexpr int PLANE = (DIM == 2 ? P : 1) * PS;  // one (ch, d, v) plane
+  constexpr int FN = DIM == 2 ? P : 1;            // nodes per face
+  constexpr int NFN = 2 * DIM * FN;               // face nodes per element
+  double* sFace = sF + NCH * DIM * NV * PLANE;    // [ch][v][face][k]
   const int i = node % P;
   const int j = DIM == 2 ? node / P : 0;
-  double surf[NCH][NV];
-#pragma unroll
-  for (int c = 0; c < NCH; ++c)
-#pragma unroll
-    for (int v = 0; v < NV; ++v) surf[c][v] = 0.0;
 
   if (active) {
     typename Mode::State st;
     Mode::load(A, g, e, slot, node, st, false);
-    double cf[NCH][NV];
+    double cf[DIM][NCH][NV];
+    Mode::template vol<DIM>(A, pp, st, cf);
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      Mode::vol(A, pp, st, d, cf);
+    for (int d = 0; d < DIM; ++d)
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i] = cf[c][v];
-    }
-    // faces (GLL: only boundary nodes carry a surface term)
+        for (int v = 0; v < NV; ++v) sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i] = cf[d][c][v];
+  }
+  constexpr int NODES = DIM == 2 ? P * P : P;
+  // face nodes packed into the first warps (measured faster than spreading
+  // them over all warps: fewer half-empty warps executing the face code)
+  for (int fn = node; active && fn < NFN; fn += NODES) {
+    // face f: 0 = -x, 1 = +x, 2 = -y, 3 = +y; node k along the face
+    const int f = fn / FN, k = fn % FN;
+    const int d = f >> 1;
+    const bool plus = f & 1;
+    const int own_edge = plus ? P - 1 : 0, nbr_edge = plus ? 0 : P - 1;
+    const int own = DIM == 1 ? own_edge : (d == 0 ? k * P + own_edge : own_edge * P + k);
+    const int nnode = DIM == 1 ? nbr_edge : (d == 0 ? k * P + nbr_edge : nbr_edge * P + k);
+    const int nb = nbr_elem(g, e, d, plus ? +1 : -1);
+    typename Mode::State so, sn;
+    Mode::load(A, g, e, slot, own, so, false);
+    Mode::load(A, g, nb, slot, nnode, sn, true);
+    double cf[NCH][NV];
+    if (plus) Mode::face(A, pp, so, sn, d, cf);     // canonical L = own (the -e_d side)
+    else Mode::face(A, pp, sn, so, d, cf);          // canonical L = neighbour
+    const double s = (d == 0 ? g.sx : g.sy) * (plus ? g.lhp : -g.lhm);
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      const int k = d == 0 ? i : j;
-      const double s = d == 0 ? g.sx : g.sy;
-      if (k == P - 1) {
-        const int nb = nbr_elem(g, e, d, +1);
-        const int nnode = d == 0 ? j * P : i;              // neighbour's (0, j) or (i, 0)
-        typename Mode::State sn;
-        Mode::load(A, g, nb, slot, nnode, sn, true);
-        Mode::face(A, pp, st, sn, d, cf);                   // L = own, R = neighbour
+    for (int c = 0; c < NCH; ++c)
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) surf[c][v] += s * (cf[c][v] * g.lhp);
-      }
-      if (k == 0) {
-        const int nb = nbr_elem(g, e, d, -1);
-        const int nnode = d == 0 ? j * P + (P - 1) : (P - 1) * P + i;
-        typename Mode::State sn;
-        Mode::load(A, g, nb, slot, nnode, sn, true);
-        Mode::face(A, pp, sn, st, d, cf);                   // L = neighbour, R = own
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) surf[c][v] -= s * (cf[c][v] * g.lhm);
-      }
-    }
+      for (int v = 0; v < NV; ++v) sFace[((c * NV + v) * 2 * DIM + f) * FN + k] = s * cf[c][v];
   }
   __syncthreads();
   if (active) {
@@ -179,6 +205,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE + j * PS;
+        const double* fs = sFace + (c * NV + v) * 2 * DIM * FN;
         double ax = 0.0;
 #pragma unroll
         for (int l = 0; l < P; ++l) ax = fma(Dr[l], Fx[l], ax);
@@ -190,18 +217,36 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
           for (int l = 0; l < P; ++l) ay = fma(Dc[l], Fy[l * PS], ay);
           acc = fma(g.sy, ay, acc);
         }
-        out[c][v] = -(acc + surf[c][v]);
+        double surf = 0.0;
+        if (i == P - 1) surf += fs[1 * FN + j];
+        if (i == 0) surf += fs[0 * FN + j];
+        if constexpr (DIM == 2) {
+          if (j == P - 1) surf += fs[3 * FN + i];
+          if (j == 0) surf += fs[2 * FN + i];
+        }
+        out[c][v] = -(acc + surf);
       }
   }
 }
 
+#ifndef HBPDC_CTA_THREADS
+#define HBPDC_CTA_THREADS 128
+#endif
+__host__ __device__ constexpr int epb_for(int nodes) {
+  return nodes >= HBPDC_CTA_THREADS ? 1 : HBPDC_CTA_THREADS / nodes;
+}
+
 // Generic operator kernel: EPB element slots per CTA, one element per slot.
+// HBPDC_MINB CTAs per SM are requested from ptxas (register cap).
+#ifndef HBPDC_MINB
+#define HBPDC_MINB 4
+#endif
 template <int EQ, int DIM, int P, class Mode, int EPB>
-__global__ void __launch_bounds__(EPB * ipow(P, DIM))
+__global__ void __launch_bounds__(EPB * ipow(P, DIM), HBPDC_MINB)
 op_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int NV = NVars<EQ>::value;
-  constexpr int SLOT = Mode::NCH * DIM * NV * (DIM == 2 ? P : 1) * (P + 1);
+  constexpr int SLOT = slot_doubles<EQ, DIM, P, Mode::NCH>();
   __shared__ double sF[EPB * SLOT];
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
   const int e = blockIdx.x * EPB + slot;

@@ -4,7 +4,6 @@
 #include "modes.cuh"
 #include "launch.h"
 
-constexpr int epb_for(int nodes) { return nodes >= 256 ? 1 : 256 / nodes; }
 
 template <int EQ, int DIM, int P, class Mode>
 static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
@@ -48,10 +47,12 @@ template <int EQ, int NODES> struct ModeKCol {
       st.s.w[v] = J1{w, nbr ? 0.0 : A.tan[slot * A.m + v * NODES + node]};
     }
   }
-  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, int d, double (&c)[NCH][NV]) {
-    J1 F[NV];
-    vol_flux<EQ>(pp, st.s, d, F);
-    for (int v = 0; v < NV; ++v) c[0][v] = F[v].a;
+  template <int DIM>
+  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, double (&c)[DIM][NCH][NV]) {
+    J1 F[DIM][NV];
+    vol_flux_all<EQ, DIM>(pp, st.s, F);
+    for (int d = 0; d < DIM; ++d)
+      for (int v = 0; v < NV; ++v) c[d][0][v] = F[d][v].a;
   }
   __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
                               double (&c)[NCH][NV]) {
@@ -69,7 +70,7 @@ kbuild_kernel(const double* __restrict__ Wb, const PhysParams pp, const Geo g, d
   constexpr int NV = NVars<EQ>::value;
   constexpr int m = NV * NODES;
   using Mode = ModeKCol<EQ, NODES>;
-  constexpr int SLOT = DIM * NV * (DIM == 2 ? P : 1) * (P + 1);
+  constexpr int SLOT = slot_doubles<EQ, DIM, P, 1>();
   __shared__ double sF[EPB * SLOT];
   __shared__ double stan[EPB * m];
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;

@@ -20,32 +20,46 @@ struct PhysParams {
 template <int EQ> struct NVars { static constexpr int value = 4; };
 template <> struct NVars<0> { static constexpr int value = 1; };
 
+// Euler primitives of a node state, computed once and shared by both flux
+// directions and the wave speed: one jet reciprocal per state.
+template <class T> struct EulerPrim {
+  T u, v, p, H, rinv;   // velocity, pressure, E + p, 1/rho
+};
+
+template <class T>
+__device__ __forceinline__ EulerPrim<T> euler_prim(const PhysParams& pp, const T* w) {
+  EulerPrim<T> q;
+  q.rinv = jrecip(w[0]);
+  q.u = w[1] * q.rinv;
+  q.v = w[2] * q.rinv;
+  q.p = (pp.gamma - 1.0) * (w[3] - 0.5 * (w[1] * q.u + w[2] * q.v));
+  q.H = w[3] + q.p;
+  return q;
+}
+
+// inviscid flux in direction d from the primitives
+template <class T>
+__device__ __forceinline__ void euler_flux(const T* w, const EulerPrim<T>& q, int d, T* F) {
+  const T vn = d == 0 ? q.u : q.v;
+  F[0] = d == 0 ? w[1] : w[2];
+  F[1] = d == 0 ? w[1] * vn + q.p : w[1] * vn;
+  F[2] = d == 1 ? w[2] * vn + q.p : w[2] * vn;
+  F[3] = vn * q.H;
+}
+
 // inviscid flux in direction d
 template <int EQ, class T>
 __device__ __forceinline__ void phys_flux(const PhysParams& pp, const T* w, int d, T* F) {
   if constexpr (EQ == 0) {
     F[0] = (d == 0 ? pp.ax : pp.ay) * w[0];
   } else {
-    const T rho = w[0], mx = w[1], my = w[2], E = w[3];
-    const T p = (pp.gamma - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho);
-    const T vn = (d == 0 ? mx : my) / rho;
-    F[0] = rho * vn;
-    F[1] = d == 0 ? mx * vn + p : mx * vn;
-    F[2] = d == 1 ? my * vn + p : my * vn;
-    F[3] = vn * (E + p);
+    euler_flux(w, euler_prim(pp, w), d, F);
   }
 }
 
-template <int EQ, class T>
-__device__ __forceinline__ T wave_speed(const PhysParams& pp, const T* w, int d) {
-  if constexpr (EQ == 0) {
-    return jconst<T>(d == 0 ? (pp.ax >= 0 ? pp.ax : -pp.ax) : (pp.ay >= 0 ? pp.ay : -pp.ay));
-  } else {
-    const T rho = w[0], mx = w[1], my = w[2], E = w[3];
-    const T p = (pp.gamma - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho);
-    const T vn = (d == 0 ? mx : my) / rho;
-    return jabs(vn) + jsqrt(pp.gamma * p / rho);
-  }
+template <class T>
+__device__ __forceinline__ T euler_speed(const PhysParams& pp, const EulerPrim<T>& q, int d) {
+  return jabs(d == 0 ? q.u : q.v) + jsqrt(pp.gamma * q.p * q.rinv);
 }
 
 // canonical LLF flux across a face with normal +e_d
@@ -53,9 +67,17 @@ template <int EQ, class T>
 __device__ __forceinline__ void llf_flux(const PhysParams& pp, const T* wL, const T* wR, int d, T* f) {
   constexpr int NV = NVars<EQ>::value;
   T FL[NV], FR[NV];
-  phys_flux<EQ>(pp, wL, d, FL);
-  phys_flux<EQ>(pp, wR, d, FR);
-  const T lam = jmax(wave_speed<EQ>(pp, wL, d), wave_speed<EQ>(pp, wR, d));
+  T lam;
+  if constexpr (EQ == 0) {
+    phys_flux<EQ>(pp, wL, d, FL);
+    phys_flux<EQ>(pp, wR, d, FR);
+    lam = jconst<T>(d == 0 ? (pp.ax >= 0 ? pp.ax : -pp.ax) : (pp.ay >= 0 ? pp.ay : -pp.ay));
+  } else {
+    const EulerPrim<T> qL = euler_prim(pp, wL), qR = euler_prim(pp, wR);
+    euler_flux(wL, qL, d, FL);
+    euler_flux(wR, qR, d, FR);
+    lam = jmax(euler_speed(pp, qL, d), euler_speed(pp, qR, d));
+  }
 #pragma unroll
   for (int v = 0; v < NV; ++v) f[v] = 0.5 * (FL[v] + FR[v]) + 0.5 * lam * (wL[v] - wR[v]);
 }
@@ -72,6 +94,25 @@ __device__ __forceinline__ void grad_vars(const PhysParams& pp, const T* w, T* g
 }
 
 // F^v_d(w, grad): gx = (u_x, v_x, T_x), gy = (u_y, v_y, T_y)
+template <class T>
+__device__ __forceinline__ void viscous_flux_uv(const PhysParams& pp, const T& u, const T& v, const T* gx,
+                                                const T* gy, int d, T* Fv) {
+  const T div = gx[0] + gy[1];
+  const T txy = pp.mu * (gy[0] + gx[1]);
+  Fv[0] = jconst<T>(0.0);
+  if (d == 0) {
+    const T txx = pp.mu * (2.0 * gx[0] - (2.0 / 3.0) * div);
+    Fv[1] = txx;
+    Fv[2] = txy;
+    Fv[3] = txx * u + txy * v + pp.lamT * gx[2];
+  } else {
+    const T tyy = pp.mu * (2.0 * gy[1] - (2.0 / 3.0) * div);
+    Fv[1] = txy;
+    Fv[2] = tyy;
+    Fv[3] = txy * u + tyy * v + pp.lamT * gy[2];
+  }
+}
+
 template <class T>
 __device__ __forceinline__ void viscous_flux(const PhysParams& pp, const T* w, const T* gx,
                                              const T* gy, int d, T* Fv) {

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhbpdc.so")
+LIB_PATH = os.environ.get("HBPDC_LIB", os.path.join(_HERE, "libhbpdc.so"))
 
 ADVECTION, EULER, NAVIER_STOKES = 0, 1, 2
 GLL, GL = 0, 1
@@ -52,7 +52,7 @@ class SolverOpts(ctypes.Structure):
 class Dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("px", ctypes.c_int),
                 ("py", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
-                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int)]
+                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int), ("own_stream", ctypes.c_int)]
 
 
 class StepStats(ctypes.Structure):
@@ -158,7 +158,7 @@ class Context:
         self._nccl_id = nccl_id
         ds = Dist(rank=rank, nranks=nranks, px=px, py=py,
                   nccl_unique_id=ctypes.cast(ctypes.c_char_p(nccl_id), ctypes.c_void_p) if nccl_id else None,
-                  cuda_stream=ctypes.c_void_p(stream.cuda_stream), device=device)
+                  cuda_stream=ctypes.c_void_p(stream.cuda_stream), device=device, own_stream=0)
         h = ctypes.c_void_p()
         st = self.lib.hbpdc_init(ctypes.byref(pb), ctypes.byref(op), ctypes.byref(ds), ctypes.byref(h))
         self.h = h

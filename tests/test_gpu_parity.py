@@ -79,14 +79,16 @@ def test_residual(case):
 
 
 def test_residual_degenerate():
-    """dt = 0, b = W -> G1 = 0 exactly; sigma = R1(W) -> G2 ~ 0."""
+    """dt = 0, b = W -> G1 = 0 exactly; sigma = R1(W) -> G2 = 0 up to the
+    rounding of two R1 evaluations (plain vs dual carrier; FMA contraction
+    differs between them)."""
     d, ctx = _pair("euler", 3, 4, 4, (0.0, 1.0, 0.0, 1.0))
     W = euler_ic(d, SEED + 6)
     Wg = to_gpu(W)
     sig = ctx.rhs(Wg)
     G1, G2 = ctx.residual(0.5, 1 / 6, 0.0, Wg, Wg, sig)
     assert np.abs(to_np(G1)).max() == 0.0
-    assert np.abs(to_np(G2)).max() == 0.0
+    assert np.abs(to_np(G2)).max() <= 1e-13 * np.abs(to_np(sig)).max()
 
 
 @pytest.mark.parametrize("case", [c for c in OPS_CASES if c[0] != "advection"])
