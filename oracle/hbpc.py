@@ -44,7 +44,9 @@ class HBPC:
         def precond(a1, a2):
             if opts.precond != "bjext" or opts.precond_policy != "per_step_per_alpha":
                 return None
-            key = (a1, a2)
+            # pairs equal up to rounding share a build: dc is constant across
+            # stages in exact arithmetic for q = 4, 6, 8 (App. A; reading R12)
+            key = (float(f"{a1:.12e}"), float(f"{a2:.12e}"))
             if key not in pcs:
                 pcs[key] = implicit.BJExt(disc, Wn, a1, a2, dt)
                 stats["precond_builds"] += 1

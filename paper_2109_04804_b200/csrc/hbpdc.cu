@@ -518,7 +518,10 @@ hbpdc_status stage_ops(hbpdc_ctx* c, const double* w, double* r1, double* r2) {
 
 hbpdc_status ensure_pc_for(hbpdc_ctx* c, double a1, double a2, double dt, const double* Wn) {
   if (c->op.precond != HBPDC_PC_BJEXT || c->op.precond_policy != HBPDC_PC_PER_STEP_PER_ALPHA) return HBPDC_OK;
-  if (c->pc_valid == 2 && c->pc_a1 == a1 && c->pc_a2 == a2 && c->pc_dt == dt) return HBPDC_OK;
+  // (alpha1, alpha2) pairs equal up to rounding (dc = c_l - c_{l-1} is constant
+  // for q = 4, 6, 8 in exact arithmetic, App. A) share one build (reading R12)
+  auto same = [](double x, double y) { return std::fabs(x - y) <= 1e-12 * std::fabs(y); };
+  if (c->pc_valid == 2 && same(a1, c->pc_a1) && same(a2, c->pc_a2) && c->pc_dt == dt) return HBPDC_OK;
   CKS(precond_build_impl(c, a1, a2, dt, Wn));
   c->pc_valid = 2;   // built inside this step at W^n
   return HBPDC_OK;

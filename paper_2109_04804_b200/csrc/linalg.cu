@@ -257,10 +257,132 @@ __global__ void __launch_bounds__(256) gemv2_kernel(const double* __restrict__ S
   }
 }
 
+// ---- TMA-streamed variant (per-element S): persistent CTAs walk their
+// elements' S blocks in chunks of GT_R rows; thread 0 keeps GT_NST chunks in
+// flight with cp.async.bulk (completion on an mbarrier), the 8 warps reduce
+// one row each per chunk from shared memory.
+namespace {
+constexpr int GT_NST = 4;   // pipeline stages
+constexpr int GT_R = 8;     // rows per chunk (one per warp)
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(256) gemv2_tma_kernel(const double* __restrict__ S, const double* __restrict__ W,
+                                                        const double* __restrict__ sg, double* __restrict__ U,
+                                                        double* __restrict__ V, int m, int nE) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* ring = reinterpret_cast<double*>(smraw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)GT_NST * GT_R * m);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int cpe = (m + GT_R - 1) / GT_R;                               // chunks per element
+  const int nmy = blockIdx.x < nE ? (nE - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int T = nmy * cpe;
+  auto issue = [&](int c) {
+    const int e = blockIdx.x + (c / cpe) * gridDim.x;
+    const int r0 = (c % cpe) * GT_R;
+    const int rows = min(GT_R, m - r0);
+    const unsigned bytes = (unsigned)(rows * m * sizeof(double));
+    unsigned long long* b = &full[c % GT_NST];
+    mbar_expect_tx(b, bytes);
+    tma_load_1d(ring + (size_t)(c % GT_NST) * GT_R * m, S + ((size_t)e * m + r0) * m, bytes, b);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GT_NST; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int c = 0; c < GT_NST && c < T; ++c) issue(c);
+  }
+  __syncthreads();
+  double wr[CPL], sr[CPL];
+  for (int c = 0; c < T; ++c) {
+    const int e = blockIdx.x + (c / cpe) * gridDim.x;
+    const int r0 = (c % cpe) * GT_R;
+    if (r0 == 0) {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int col = lane + 32 * q;
+        wr[q] = col < m ? W[(size_t)e * m + col] : 0.0;
+        sr[q] = col < m ? sg[(size_t)e * m + col] : 0.0;
+      }
+    }
+    mbar_wait(&full[c % GT_NST], (unsigned)((c / GT_NST) & 1));
+    const int r = r0 + wid;
+    if (r < m) {
+      const double* row = ring + ((size_t)(c % GT_NST) * GT_R + wid) * m;
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int col = lane + 32 * q;
+        const double s = col < m ? row[col] : 0.0;
+        a = fma(s, wr[q], a);
+        b = fma(s, sr[q], b);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      if (lane == 0) {
+        U[(size_t)e * m + r] = a;
+        V[(size_t)e * m + r] = b;
+      }
+    }
+    __syncthreads();                       // stage (c % GT_NST) is free again
+    if (threadIdx.x == 0 && c + GT_NST < T) issue(c + GT_NST);
+  }
+}
+
 cudaError_t launch_block_gemv2(const double* S, int shared, const double* W, const double* sig, double* U,
                                double* V, int m, int nE, cudaStream_t st) {
   if (nE <= 0) return cudaSuccess;
   const int cpl = (m + 31) / 32;
+  if (!shared && (m * sizeof(double)) % 16 == 0) {
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const size_t smem = (size_t)GT_NST * GT_R * m * sizeof(double) + GT_NST * sizeof(unsigned long long);
+    const int grid = std::min(nE, nsm * 3);
+#define GT(C)                                                                                  \
+  case C:                                                                                      \
+    cudaFuncSetAttribute(gemv2_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    gemv2_tma_kernel<C><<<grid, 256, smem, st>>>(S, W, sig, U, V, m, nE);                       \
+    break;
+    switch (cpl) {
+      GT(1) GT(2) GT(3) GT(4) GT(5) GT(6) GT(7) GT(8)
+      default: return cudaErrorInvalidValue;
+    }
+#undef GT
+    hbpdc_count_launch();
+    return cudaGetLastError();
+  }
 #define G(C) case C: gemv2_kernel<C><<<nE, 256, 0, st>>>(S, shared, W, sig, U, V, m, nE); break;
   switch (cpl) {
     G(1) G(2) G(3) G(4) G(5) G(6) G(7) G(8)

@@ -18,7 +18,8 @@ for s in range(steps):
     t = time.time(); st = ctx.step(dt, W); torch.cuda.synchronize()
     print("step", s, f"{time.time()-t:.3f}s", st, flush=True)
 names = ["gemv", "jvp", "resid", "dots", "axpy", "kapply", "build"]
+torch.cuda.set_stream(torch.cuda.Stream())
 for k in range(7):
-    n, ms = ctx.profile_read(k)
-    print(f"{names[k]:8s} launches {n:6d} total {ms:9.2f} ms avg {ms/max(n,1):.4f} ms")
+    n, ms, by = ctx.profile_read(k)
+    print(f"{names[k]:8s} launches {n:6d} total {ms:9.2f} ms avg {ms/max(n,1):.4f} ms  {by/max(ms,1e-9)/1e6:8.1f} GB/s")
 print("mem GB", torch.cuda.max_memory_allocated()/1e9, torch.cuda.mem_get_info())
