@@ -98,7 +98,7 @@ struct hbpdc_ctx {
   double *Wn = nullptr, *bvec = nullptr, *Wio = nullptr;
   int fsal_valid = 0;
   // host scratch
-  std::vector<double> H, cs, sn, gv, y, hh;
+  std::vector<double> H, Hraw, cs, sn, gv, y, hh;
   double* hpin = nullptr;      // pinned host scratch
   // profiling
   int prof_on = 0;
@@ -363,57 +363,112 @@ hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
     CK(cudaMemcpyAsync(c->dnrm, c->hpin, sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CK(launch_scale_by_inv(r, c->dnrm, c->Vk, n2, c->stream));
     std::fill(H.begin(), H.end(), 0.0);
+    std::fill(c->Hraw.begin(), c->Hraw.end(), 0.0);
     std::fill(c->gv.begin(), c->gv.end(), 0.0);
     c->gv[0] = beta;
-    int k = 0;
-    for (int j = 0; j < R; ++j) {
-      double* vj = c->Vk + (size_t)j * n2;
-      double* w = c->Vk + (size_t)(j + 1) * n2;
-      CKS(apply_JPinv(c, L, vj, w, L.pc));
-      // classical Gram-Schmidt with selective reorthogonalisation: a second
-      // pass only when the first cancelled more than 1/sqrt(2) of ||w||
-      // (Daniel-Gragg-Kaufman-Stewart criterion; the oracle uses MGS)
-      double* Hc = &H[(size_t)j * (R + 1)];   // column j, length R+1
-      double hnext = 0.0;
-      for (int pass = 0; pass < 2; ++pass) {
-        const int nb = arnoldi_dot_blocks(n2);
-        {
-          ProfScope ps(c, 3, (double)(j + 2) * n2 * 8.0);
-          CK(launch_arnoldi_dots(c->Vk, n2, j + 1, w, n2, c->partial, c->stream));
-          CK(launch_reduce_partials_n(c->partial, j + 2, nb, c->dh, c->stream));
-        }
-        {
-          ProfScope ps(c, 4, (double)(j + 3) * n2 * 8.0);
-          CK(launch_arnoldi_axpy(c->Vk, n2, j + 1, c->dh, w, n2, c->partial, c->stream));
-          CK(launch_finish_sqrt(c->partial, nb, c->dnrm, c->stream));
-        }
-        CK(cudaMemcpyAsync(c->hpin, c->dh, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(c->hpin + (R + 2), c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    // Arnoldi with delayed classical Gram-Schmidt reorthogonalisation (DCGS2,
+    // Swirydowicz et al. 2020 / Bielich et al. 2022; the oracle uses MGS):
+    // iteration j applies the operator to the once-orthogonalised u_j, and ONE
+    // reduction gives both the lagged reorthogonalisation of u_j and the
+    // projections of w = B u_j; ONE update pass writes q_j and u_{j+1}.
+    // Column j-1 of the Hessenberg matrix becomes final (and its Givens
+    // rotation applied) one iteration later.
+    std::vector<double>& Hr = c->Hraw;          // unrotated Hessenberg, column-major (R+1) x R
+    auto HR = [&](int row, int col) -> double& { return Hr[(size_t)col * (R + 1) + row]; };
+    auto HQ = [&](int row, int col) -> double& { return H[(size_t)col * (R + 1) + row]; };
+    int k = 0;                                   // finalized columns
+    bool flush_next = false;
+    bool est_ok = false;
+    const int nb = arnoldi_dot_blocks(n2);
+    std::vector<double> a, bvec, t, hp, d;
+    for (int j = 1; j <= R + 1; ++j) {
+      const bool flush = flush_next || j == R + 1;
+      double* u = c->Vk + (size_t)(j - 1) * n2;   // u_j (once orthogonalised)
+      double* w = c->Vk + (size_t)j * n2;
+      if (!flush) {
+        CKS(apply_JPinv(c, L, u, w, L.pc));
+        ++total;
+      }
+      const int nk = j - 1;
+      {
+        ProfScope ps(c, 3, (double)(nk + (flush ? 1 : 2)) * n2 * 8.0);
+        CK(launch_dcgs2_dots(c->Vk, n2, nk, u, flush ? nullptr : w, n2, c->partial, c->stream));
+        CK(launch_reduce_partials_n(c->partial, 2 * nk + 3, nb, c->dh, c->stream));
+      }
+      CK(cudaMemcpyAsync(c->hpin, c->dh, (2 * nk + 3) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      a.assign(nk, 0.0);
+      bvec.assign(nk, 0.0);
+      double sa = 0.0, ab = 0.0;
+      for (int q = 0; q < nk; ++q) {
+        a[q] = c->hpin[2 * q];
+        bvec[q] = c->hpin[2 * q + 1];
+        sa += a[q] * a[q];
+        ab += a[q] * bvec[q];
+      }
+      const double uu = c->hpin[2 * nk], uw = c->hpin[2 * nk + 1];
+      double b2 = uu - sa;
+      bool explicit_q = false;
+      if (nk > 0 && !(b2 >= 0.25 * uu)) {
+        // severe cancellation in the lagged step: form q_j explicitly
+        for (int q = 0; q < nk; ++q) c->hpin[q] = a[q];
+        CK(cudaMemcpyAsync(c->dy, c->hpin, nk * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(launch_arnoldi_axpy(c->Vk, n2, nk, c->dy, u, n2, c->partial, c->stream));
+        CK(launch_finish_sqrt(c->partial, nb, c->dnrm, c->stream));
+        CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        for (int i = 0; i <= j; ++i) Hc[i] = (pass ? Hc[i] : 0.0) + c->hpin[i];
-        const double wn_before = std::sqrt(c->hpin[j + 1]);
-        hnext = c->hpin[R + 2];
-        if (!(hnext < 0.70710678118654752 * wn_before)) break;
+        b2 = c->hpin[0] * c->hpin[0];
+        explicit_q = true;
       }
-      CK(launch_scale_by_inv(w, c->dnrm, w, n2, c->stream));
-      if (!std::isfinite(hnext)) return fail(c, HBPDC_E_NONFINITE, "non-finite Arnoldi norm");
-      Hc[j + 1] = hnext;
-      for (int i = 0; i < j; ++i) {
-        const double t = c->cs[i] * Hc[i] + c->sn[i] * Hc[i + 1];
-        Hc[i + 1] = -c->sn[i] * Hc[i] + c->cs[i] * Hc[i + 1];
-        Hc[i] = t;
+      const double bu = std::sqrt(std::max(b2, 0.0));
+      if (!std::isfinite(bu)) return fail(c, HBPDC_E_NONFINITE, "non-finite Arnoldi norm");
+      if (j >= 2) {
+        // finalize column j-2: lagged correction + subdiagonal, then Givens
+        const int col = j - 2;
+        for (int q = 0; q < nk; ++q) HR(q, col) += a[q];
+        HR(j - 1, col) = bu;
+        for (int q = 0; q <= j - 1; ++q) HQ(q, col) = HR(q, col);
+        for (int i = 0; i < col; ++i) {
+          const double tt = c->cs[i] * HQ(i, col) + c->sn[i] * HQ(i + 1, col);
+          HQ(i + 1, col) = -c->sn[i] * HQ(i, col) + c->cs[i] * HQ(i + 1, col);
+          HQ(i, col) = tt;
+        }
+        const double den = std::hypot(HQ(col, col), HQ(col + 1, col));
+        c->cs[col] = HQ(col, col) / den;
+        c->sn[col] = HQ(col + 1, col) / den;
+        HQ(col, col) = den;
+        HQ(col + 1, col) = 0.0;
+        c->gv[col + 1] = -c->sn[col] * c->gv[col];
+        c->gv[col] = c->cs[col] * c->gv[col];
+        k = col + 1;
+        if (c->st && k > c->st->max_krylov_j) c->st->max_krylov_j = k;
+        if (std::fabs(c->gv[k]) <= rtol * beta0) { est_ok = true; break; }
       }
-      const double den = std::hypot(Hc[j], Hc[j + 1]);
-      c->cs[j] = Hc[j] / den;
-      c->sn[j] = Hc[j + 1] / den;
-      Hc[j] = den;
-      Hc[j + 1] = 0.0;
-      c->gv[j + 1] = -c->sn[j] * c->gv[j];
-      c->gv[j] = c->cs[j] * c->gv[j];
-      ++total;
-      k = j + 1;
-      if (c->st && k > c->st->max_krylov_j) c->st->max_krylov_j = k;
-      if (std::fabs(c->gv[j + 1]) <= rtol * beta0 || total >= maxit || hnext == 0.0) break;
+      if (flush || bu == 0.0) break;
+      // first-pass projections of B q_j onto Q_j (provisional column j-1)
+      t.assign(j, 0.0);
+      for (int col = 0; col < nk; ++col)
+        for (int i = 0; i <= col + 1 && i < j; ++i) t[i] += HR(i, col) * a[col];
+      hp.assign(j, 0.0);
+      for (int i = 0; i < nk; ++i) hp[i] = (bvec[i] - t[i]) / bu;
+      const double qw = (uw - ab) / bu;
+      hp[j - 1] = (qw - t[j - 1]) / bu;
+      for (int i = 0; i < j; ++i) HR(i, j - 1) = hp[i];
+      const double cj = t[j - 1] / bu + hp[j - 1];
+      d.assign(nk, 0.0);
+      for (int q = 0; q < nk; ++q) d[q] = t[q] / bu + hp[q] - (explicit_q ? 0.0 : a[q] * cj / bu);
+      for (int q = 0; q < nk; ++q) {
+        c->hpin[q] = explicit_q ? 0.0 : a[q];
+        c->hpin[(R + 1) + q] = d[q];
+      }
+      CK(cudaMemcpyAsync(c->dy, c->hpin, nk * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->dy + (R + 1), c->hpin + (R + 1), nk * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
+      {
+        ProfScope ps(c, 4, (double)(nk + 4) * n2 * 8.0);
+        CK(launch_dcgs2_update(c->Vk, n2, nk, c->dy, c->dy + (R + 1), u, w, 1.0 / bu, cj / bu, n2, c->stream));
+      }
+      if (total >= maxit) flush_next = true;
     }
     // y = H^-1 g (back substitution), x += P^-1 (V y)
     for (int i = k - 1; i >= 0; --i) {
@@ -430,7 +485,6 @@ hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
     } else {
       CK(launch_axpby(1.0, r, 1.0, c->dX, n2, c->stream));
     }
-    const bool est_ok = std::fabs(c->gv[k]) <= rtol * beta0;
     if (est_ok) { converged = true; break; }
     // true residual r = rhs - J x
     CKS(jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, c->dX, c->dX + c->n, r, r + c->n, c->op.jvp_mode, nullptr));
@@ -610,11 +664,11 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
   CKS(dalloc(c, &c->tmp2, n2));
   CKS(dalloc(c, &c->zb, n2));
   CKS(dalloc(c, &c->Vk, (size_t)(R + 1) * n2));
-  CKS(dalloc(c, &c->partial, (size_t)(R + 2) * std::max(arnoldi_dot_blocks(n2), RED_BLOCKS)));
-  CKS(dalloc(c, &c->dh, 2 * (size_t)(R + 1)));
+  CKS(dalloc(c, &c->partial, (size_t)(2 * R + 4) * std::max(arnoldi_dot_blocks(n2), RED_BLOCKS)));
+  CKS(dalloc(c, &c->dh, 2 * (size_t)R + 4));
   CKS(dalloc(c, &c->dnrm, 1));
   CKS(dalloc(c, &c->deps, 1));
-  CKS(dalloc(c, &c->dy, (size_t)R + 1));
+  CKS(dalloc(c, &c->dy, 2 * (size_t)R + 4));
   CKS(dalloc(c, &c->Wn, n));
   CKS(dalloc(c, &c->bvec, n));
   for (int sw = 0; sw < 2; ++sw)
@@ -629,6 +683,7 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     CKS(dalloc(c, &c->lift1, lg));
   }
   c->H.assign((size_t)R * (R + 1), 0.0);
+  c->Hraw.assign((size_t)R * (R + 1), 0.0);
   c->cs.assign(R + 1, 0.0);
   c->sn.assign(R + 1, 0.0);
   c->gv.assign(R + 2, 0.0);

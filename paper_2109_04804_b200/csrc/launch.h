@@ -50,6 +50,12 @@ cudaError_t launch_arnoldi_axpy(const double* V, size_t ldx, int nk, const doubl
                                 double* sq_part, cudaStream_t st);
 // out = sqrt(sum part[0..nb))
 cudaError_t launch_finish_sqrt(const double* part, int nb, double* out, cudaStream_t st);
+// DCGS2: rows 2k, 2k+1 = Q_k.u, Q_k.w (k < nk); rows 2nk.. = u.u, u.w, w.w  (w may be NULL)
+cudaError_t launch_dcgs2_dots(const double* Q, size_t ldx, int nk, const double* u, const double* w, size_t L,
+                              double* part, cudaStream_t st);
+// DCGS2: u <- (u - Q a) ib ;  w <- w ib - Q d - u_old cb   (a, d on device)
+cudaError_t launch_dcgs2_update(const double* Q, size_t ldx, int nk, const double* a, const double* d, double* u,
+                                double* w, double ib, double cb, size_t L, cudaStream_t st);
 
 // partial[k * RED_BLOCKS + b] = sum over block b of X_k . y   (k < nk), X_k = X + k*ldx
 cudaError_t launch_multidot(const double* X, size_t ldx, int nk, const double* y, size_t L,

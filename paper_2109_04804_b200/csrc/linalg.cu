@@ -469,6 +469,137 @@ __global__ void __launch_bounds__(256) arnoldi_dots_kernel(const double* __restr
 
 int arnoldi_dot_blocks(size_t L) { return (int)((L + 256 * DOT_T - 1) / (256 * DOT_T)); }
 
+// ---- DCGS2 (delayed reorthogonalisation) reduction: one pass over Q_0..Q_{nk-1}
+// with two right-hand sides u, w (w may be NULL):
+//   rows 2k, 2k+1: Q_k.u, Q_k.w  (k < nk);  rows 2nk, 2nk+1, 2nk+2: u.u, u.w, w.w
+__global__ void __launch_bounds__(256) dcgs2_dots_kernel(const double* __restrict__ Q, size_t ldx, int nk,
+                                                         const double* __restrict__ u,
+                                                         const double* __restrict__ w, size_t L,
+                                                         double* __restrict__ part) {
+  constexpr int KB = 8;                    // basis vectors per reduction round (2 KB results)
+  __shared__ double red[8][2 * KB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t base = (size_t)blockIdx.x * (256 * DOT_T) + threadIdx.x;
+  double ur[DOT_T], wr[DOT_T];
+#pragma unroll
+  for (int t = 0; t < DOT_T; ++t) {
+    const size_t i = base + (size_t)t * 256;
+    ur[t] = i < L ? u[i] : 0.0;
+    wr[t] = (w && i < L) ? w[i] : 0.0;
+  }
+  const int nrows = 2 * nk + 3;
+  for (int k0 = 0; k0 < nk + 2; k0 += KB) {
+    double acc[2 * KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      const int k = k0 + q;
+      double a = 0.0, b = 0.0;
+      if (k < nk) {
+        const double* qk = Q + (size_t)k * ldx;
+#pragma unroll
+        for (int t = 0; t < DOT_T; ++t) {
+          const size_t i = base + (size_t)t * 256;
+          if (i < L) {
+            const double x = __ldg(qk + i);
+            a = fma(x, ur[t], a);
+            b = fma(x, wr[t], b);
+          }
+        }
+      } else if (k == nk) {              // u.u, u.w
+#pragma unroll
+        for (int t = 0; t < DOT_T; ++t) { a = fma(ur[t], ur[t], a); b = fma(ur[t], wr[t], b); }
+      } else if (k == nk + 1) {          // w.w
+#pragma unroll
+        for (int t = 0; t < DOT_T; ++t) a = fma(wr[t], wr[t], a);
+      }
+      acc[2 * q] = a;
+      acc[2 * q + 1] = b;
+    }
+    // transpose reduction: 16 values over 32 lanes in 16 shuffles; afterwards
+    // lanes with bit 0 clear hold value (lane >> 1) & 15 summed over the warp
+#pragma unroll
+    for (int s = 8; s >= 1; s >>= 1) {
+      const bool hi = lane & (2 * s);
+#pragma unroll
+      for (int q = 0; q < s; ++q) {
+        const double send = hi ? acc[q] : acc[q + s];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, 2 * s);
+        acc[q] = (hi ? acc[q + s] : acc[q]) + recv;
+      }
+    }
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+    if ((lane & 1) == 0) {
+      // index bits: lane bit 4 -> 8, bit 3 -> 4, bit 2 -> 2, bit 1 -> 1
+      const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+      red[wid][idx] = acc[0];
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * KB) {
+      const int row = 2 * k0 + threadIdx.x;   // rows 2k, 2k+1 for k = k0 + threadIdx.x/2
+      if (row < nrows) {
+        double s = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += red[ww][threadIdx.x];
+        part[(size_t)row * gridDim.x + blockIdx.x] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_dcgs2_dots(const double* Q, size_t ldx, int nk, const double* u, const double* w, size_t L,
+                              double* part, cudaStream_t st) {
+  dcgs2_dots_kernel<<<arnoldi_dot_blocks(L), 256, 0, st>>>(Q, ldx, nk, u, w, L, part);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+// ---- DCGS2 update: one pass over Q_0..Q_{nk-1} producing
+//   q_j     = (u - sum a_k Q_k) * ib                 (written over u)
+//   u_{j+1} =  w * ib - sum d_k Q_k - u * cb         (written over w)
+__global__ void __launch_bounds__(256) dcgs2_update_kernel(const double* __restrict__ Q, size_t ldx, int nk,
+                                                           const double* __restrict__ a,
+                                                           const double* __restrict__ d, double* __restrict__ u,
+                                                           double* __restrict__ w, double ib, double cb, size_t L) {
+  __shared__ double as[1024], ds[1024];
+  for (int k = threadIdx.x; k < nk && k < 1024; k += 256) { as[k] = a[k]; ds[k] = d[k]; }
+  __syncthreads();
+  const size_t base = (size_t)blockIdx.x * (256 * DOT_T) + threadIdx.x;
+  double qa[DOT_T], qd[DOT_T];
+#pragma unroll
+  for (int t = 0; t < DOT_T; ++t) { qa[t] = 0.0; qd[t] = 0.0; }
+  for (int k = 0; k < nk; ++k) {
+    const double ak = k < 1024 ? as[k] : a[k];
+    const double dk = k < 1024 ? ds[k] : d[k];
+    const double* qk = Q + (size_t)k * ldx;
+#pragma unroll
+    for (int t = 0; t < DOT_T; ++t) {
+      const size_t i = base + (size_t)t * 256;
+      if (i < L) {
+        const double x = __ldg(qk + i);
+        qa[t] = fma(ak, x, qa[t]);
+        qd[t] = fma(dk, x, qd[t]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < DOT_T; ++t) {
+    const size_t i = base + (size_t)t * 256;
+    if (i < L) {
+      const double ui = u[i], wi = w[i];
+      u[i] = (ui - qa[t]) * ib;
+      w[i] = fma(wi, ib, -qd[t]) - ui * cb;
+    }
+  }
+}
+
+cudaError_t launch_dcgs2_update(const double* Q, size_t ldx, int nk, const double* a, const double* d, double* u,
+                                double* w, double ib, double cb, size_t L, cudaStream_t st) {
+  dcgs2_update_kernel<<<arnoldi_dot_blocks(L), 256, 0, st>>>(Q, ldx, nk, a, d, u, w, ib, cb, L);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_arnoldi_dots(const double* V, size_t ldx, int nk, const double* w, size_t L, double* part,
                                 cudaStream_t st) {
   arnoldi_dots_kernel<<<arnoldi_dot_blocks(L), 256, 0, st>>>(V, ldx, nk, w, L, part);
