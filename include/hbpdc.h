@@ -92,13 +92,28 @@ typedef struct {
   int jvp_mode;                /* HBPDC_JVP_AUTO: linear (advection) / FD otherwise  */
 } hbpdc_solver_opts;
 
+/* Element partition (the mesh is decomposed, W and sigma share the
+ * partition).  Rank r owns the element block (rx, ry) = (r % px, r / px) of
+ * nx/px x ny/py elements; its local elements are numbered ey_l * nx_l + ex_l.
+ * Face traces of the neighbouring blocks are exchanged before every operator
+ * (halo), global norms and Krylov dot products are summed over ranks; the
+ * BJ_ext preconditioner is rank-local.  See DESIGN.md "Multi-GPU". */
+enum { HBPDC_COMM_AUTO = 0,      /* nranks == 1: none; else NCCL                      */
+       HBPDC_COMM_NCCL = 1,      /* one process per GPU, NCCL over NVLink/NVSwitch    */
+       HBPDC_COMM_LOOPBACK = 2   /* ranks are host threads of one process sharing a   */
+};                               /* loopback group (tests the partition on one GPU)  */
 typedef struct {
   int rank, nranks;            /* this rank, number of ranks                          */
   int px, py;                  /* rank grid: px * py == nranks, nx % px == ny % py == 0 */
-  const void* nccl_unique_id;  /* 128-byte ncclUniqueId (rank 0's), NULL if nranks==1 */
+  const void* nccl_unique_id;  /* 128-byte ncclUniqueId of rank 0 (COMM_NCCL)         */
   void* cuda_stream;           /* cudaStream_t to enqueue on (NULL = legacy default)  */
   int device;                  /* CUDA device ordinal                                 */
   int own_stream;              /* 1: ignore cuda_stream, the library creates a stream */
+  int comm;                    /* HBPDC_COMM_*                                        */
+  void* loopback_group;        /* from hbpdc_loopback_group_create (COMM_LOOPBACK)    */
+  int force_halo;              /* 1: exchange halos even with oneself (periodic wrap
+                                  of a 1-rank direction goes through the transport);
+                                  a test hook for the transport on a single GPU      */
 } hbpdc_dist;
 
 typedef struct {               /* summed over one hbpdc_step                          */
@@ -111,6 +126,22 @@ typedef struct {               /* summed over one hbpdc_step                    
  * mesh, rank partition, NCCL communicator, scratch.  Host only. */
 HBPDC_API hbpdc_status hbpdc_init(const hbpdc_problem* problem, const hbpdc_solver_opts* opts,
                         const hbpdc_dist* dist, hbpdc_ctx** out);
+
+/* Host-only partition arithmetic (no device, no context): the element block of
+ * `rank` on a px x py rank grid over an nx x ny mesh (ny = 1 in 1D) and its four
+ * neighbour ranks [-x, +x, -y, +y] (periodic).  HBPDC_E_ARG if the grid does not
+ * divide the mesh. */
+HBPDC_API hbpdc_status hbpdc_partition(int dim, int nx, int ny, int px, int py, int rank, int* ex0, int* ey0,
+                             int* nx_local, int* ny_local, int* nbr4);
+
+/* Rank 0 creates the NCCL unique id (128 bytes, host) that every rank passes in
+ * hbpdc_dist.nccl_unique_id; the caller distributes it (torch.distributed). */
+HBPDC_API hbpdc_status hbpdc_nccl_unique_id(void* out128);
+
+/* A loopback group for `nranks` ranks living as host threads of this process
+ * (HBPDC_COMM_LOOPBACK).  Destroy after every context of the group is finalized. */
+HBPDC_API hbpdc_status hbpdc_loopback_group_create(int nranks, void** group);
+HBPDC_API void hbpdc_loopback_group_destroy(void* group);
 
 /* Local block: element count, block size m, offsets and extents in elements. */
 HBPDC_API hbpdc_status hbpdc_local_shape(const hbpdc_ctx* ctx, int* n_local_elems, int* m,

@@ -3,11 +3,13 @@
 // flow; every vector operation runs in the kernels of ops_kernels.cu / linalg.cu.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 #include <cuda_runtime.h>
 #include "../../include/hbpdc.h"
+#include "comm.h"
 #include "launch.h"
 #include "modes.cuh"
 
@@ -90,6 +92,7 @@ struct hbpdc_ctx {
   double *lift0 = nullptr, *lift1 = nullptr;
   // precond
   double *S = nullptr, *Wb = nullptr, *U = nullptr, *Vv = nullptr, *Z = nullptr;
+  double *Kst = nullptr, *KV = nullptr, *KT = nullptr, *tseed = nullptr, *y1 = nullptr, *y2 = nullptr;  // NS
   int* info = nullptr;
   int s_shared = 0, pc_valid = 0, zchunk = 0;
   double pc_a1 = 0, pc_a2 = 0, pc_dt = -1;
@@ -108,6 +111,14 @@ struct hbpdc_ctx {
   double prof_ms[NPROF] = {};
   double prof_bytes[NPROF] = {};   // algorithmic bytes (DESIGN.md byte model)
   hbpdc_step_stats* st = nullptr;  // stats of the step in progress
+  // element partition
+  hbpdc::Comm* comm = nullptr;     // nullptr: single rank, no halo
+  int nbr[4] = {0, 0, 0, 0};       // neighbour ranks -x, +x, -y, +y
+  HaloLayout hl{};
+  double *gW = nullptr, *gS = nullptr, *gdW = nullptr, *gdS = nullptr, *gWb = nullptr;  // ghosts
+  double *hsend = nullptr, *hrecv = nullptr;
+  bool halo() const { return hl.active[0] || hl.active[2]; }
+  int debug_sync = 0;              // HBPDC_DEBUG_SYNC=1: synchronise + check after every launch group
 };
 
 namespace {
@@ -182,11 +193,71 @@ void prof_flush(hbpdc_ctx* c) {
 OpArgs base_args(hbpdc_ctx* c) {
   OpArgs A{};
   A.m = c->m;
+  A.nE = c->nE;
   return A;
 }
 
-// launch an operator; NS lifts the jet states first
-hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A) {
+// debugging aid: with HBPDC_DEBUG_SYNC=1 every operator / exchange is followed
+// by a stream synchronisation, so an asynchronous fault names its call site
+hbpdc_status dbg_sync(hbpdc_ctx* c, const char* where) {
+  if (!c->debug_sync) return HBPDC_OK;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, HBPDC_E_CUDA, std::string("CUDA error after ") + where + ": " + cudaGetErrorString(e));
+  return HBPDC_OK;
+}
+
+// sum over ranks of n doubles in device memory (no-op on a single rank)
+hbpdc_status allreduce(hbpdc_ctx* c, double* d, int n) {
+  if (!c->comm) return HBPDC_OK;
+  std::string e;
+  if (c->comm->allreduce_sum(d, n, c->stream, e)) return fail(c, HBPDC_E_NCCL, e);
+  return HBPDC_OK;
+}
+
+// halo exchange of nf fields into their ghost copies
+hbpdc_status halo_exchange(hbpdc_ctx* c, int nf, const double* const* src, double* const* dst) {
+  size_t off[4], len[4];
+  halo_segments(c->hl, nf, off, len);
+  CK(launch_halo_pack(c->hl, nf, src, c->hsend, c->stream));
+  CKS(dbg_sync(c, "halo pack"));
+  std::string e;
+  if (c->comm->halo(c->hsend, c->hrecv, off, len, c->nbr, c->hl.active, c->stream, e))
+    return fail(c, HBPDC_E_NCCL, e);
+  CKS(dbg_sync(c, "halo transport"));
+  CK(launch_halo_unpack(c->hl, nf, c->hrecv, dst, c->stream));
+  CKS(dbg_sync(c, "halo unpack"));
+  return HBPDC_OK;
+}
+
+// fields of an operator that neighbours read (bits: 1 W, 2 sigma, 4 dW, 8 dsigma)
+int halo_fields(OpKind k) {
+  switch (k) {
+    case OP_R1: case OP_R1ABS: return 1;
+    case OP_R12: case OP_RESID: return 3;
+    case OP_JVP_EXACT: case OP_JVP_FD: return 15;
+    case OP_JVP_LINEAR: return 12;
+    default: return 0;
+  }
+}
+
+// launch an operator; exchange the halos of the fields in `xmask` first (the
+// ghosts of the other fields are assumed current); NS lifts the jet states first
+hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
+  if (c->halo()) {
+    if (xmask < 0) xmask = halo_fields(k);
+    xmask &= halo_fields(k);
+    const double* src[4];
+    double* dst[4];
+    int nf = 0;
+    if (xmask & 1) { src[nf] = A.W; dst[nf++] = c->gW; }
+    if (xmask & 2) { src[nf] = A.S; dst[nf++] = c->gS; }
+    if (xmask & 4) { src[nf] = A.dW; dst[nf++] = c->gdW; }
+    if (xmask & 8) { src[nf] = A.dS; dst[nf++] = c->gdS; }
+    if (nf) CKS(halo_exchange(c, nf, src, dst));
+    A.gW = k == OP_KAPPLY ? c->gWb : c->gW;
+    A.gS = c->gS; A.gdW = c->gdW; A.gdS = c->gdS;
+  }
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {
     CK(launch_lift(k, 0, c->cfg, c->geo, A, c->lift0));
     A.G0 = c->lift0;
@@ -196,17 +267,25 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A) {
     }
   }
   CK(launch_op(k, c->cfg, k == OP_R1ABS ? c->geo_abs : c->geo, A));
-  return HBPDC_OK;
-}
-
-hbpdc_status norm_dev(hbpdc_ctx* c, const double* x, size_t L, double* out_dev) {
-  CK(launch_sumsq(x, L, c->partial, c->stream));
-  CK(launch_finish_norm(c->partial, out_dev, c->stream));
+  {
+    char w[32];
+    snprintf(w, sizeof w, "operator kind %d", (int)k);
+    CKS(dbg_sync(c, w));
+  }
   return HBPDC_OK;
 }
 
 hbpdc_status norm_host(hbpdc_ctx* c, const double* x, size_t L, double* out) {
-  CKS(norm_dev(c, x, L, c->dnrm));
+  CK(launch_sumsq(x, L, c->partial, c->stream));
+  if (c->comm) {
+    CK(launch_reduce_partials_n(c->partial, 1, RED_BLOCKS, c->dnrm, c->stream));
+    CKS(allreduce(c, c->dnrm, 1));
+    CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = std::sqrt(c->hpin[0]);
+    return HBPDC_OK;
+  }
+  CK(launch_finish_norm(c->partial, c->dnrm, c->stream));
   CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   *out = c->hpin[0];
@@ -219,9 +298,11 @@ int jvp_kind(hbpdc_ctx* c, int mode) {
 }
 
 // J dX for the extended system, dX = [dW | ds] (2n), out = [top | bottom]
+// ws_ghosts: the halos of (W, sigma) are current (GMRES inside one Newton
+// iteration: the linearisation point is fixed), exchange only (dW, dsigma)
 hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const double* W, const double* sg,
                       const double* dW, const double* ds, double* o1, double* o2, int mode,
-                      const double* eps_override) {
+                      const double* eps_override, bool ws_ghosts = false) {
   const size_t n = c->n;
   mode = jvp_kind(c, mode);
   OpArgs A = base_args(c);
@@ -240,12 +321,18 @@ hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const doubl
       A.epsw = eps_override[0];
     } else {
       CK(launch_sumsq(dW, n, c->partial, c->stream));
-      CK(launch_finish_fd_eps(c->partial, std::sqrt(EPS_MACH) / c->pb.mach_eps, c->deps, c->stream));
+      if (c->comm) {   // global ||dW|| (reading R7)
+        CK(launch_reduce_partials_n(c->partial, 1, RED_BLOCKS, c->deps + 1, c->stream));
+        CKS(allreduce(c, c->deps + 1, 1));
+        CK(launch_fd_eps_from_sum(c->deps + 1, std::sqrt(EPS_MACH) / c->pb.mach_eps, c->deps, c->stream));
+      } else {
+        CK(launch_finish_fd_eps(c->partial, std::sqrt(EPS_MACH) / c->pb.mach_eps, c->deps, c->stream));
+      }
       A.d_epsw = c->deps;
     }
   }
   ProfScope ps(c, 1, (k == OP_JVP_LINEAR ? 4.0 : 6.0) * n * 8.0);
-  CKS(run_op(c, k, A));
+  CKS(run_op(c, k, A, ws_ghosts ? 12 : -1));
   if (c->st) c->st->jvp_calls++;
   return HBPDC_OK;
 }
@@ -260,6 +347,14 @@ hbpdc_status ensure_precond_mem(hbpdc_ctx* c) {
   CKS(dalloc(c, &c->Wb, c->n));
   CKS(dalloc(c, &c->U, c->n));
   CKS(dalloc(c, &c->Vv, c->n));
+  if (c->pb.equation == HBPDC_NAVIER_STOKES) {   // explicit K_i (two-hop BR1 path) + colouring scratch
+    CKS(dalloc(c, &c->Kst, nblk * mm));
+    CKS(dalloc(c, &c->KV, c->n));
+    CKS(dalloc(c, &c->KT, c->n));
+    CKS(dalloc(c, &c->tseed, c->n));
+    CKS(dalloc(c, &c->y1, c->n));
+    CKS(dalloc(c, &c->y2, c->n));
+  }
   // Gauss-Jordan scratch: chunks of at most ~1 GiB
   size_t chunk = (size_t)(1ull << 30) / (mm * sizeof(double));
   if (chunk < 1) chunk = 1;
@@ -273,29 +368,74 @@ hbpdc_status ensure_precond_mem(hbpdc_ctx* c) {
   return HBPDC_OK;
 }
 
+// ghost copy of the BJ_ext build state (K_i reads the neighbours' frozen traces)
+hbpdc_status wb_halo(hbpdc_ctx* c) {
+  if (!c->halo()) return HBPDC_OK;
+  const double* src[1] = {c->Wb};
+  double* dst[1] = {c->gWb};
+  return halo_exchange(c, 1, src, dst);
+}
+
 hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, const double* W) {
   CKS(ensure_precond_mem(c));
-  if (c->pb.equation == HBPDC_NAVIER_STOKES)
-    return fail(c, HBPDC_E_ARG, "BJ_ext build for Navier-Stokes is not implemented yet");
-  ProfScope ps(c, 6, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + c->n * 8.0);
+  const bool ns = c->pb.equation == HBPDC_NAVIER_STOKES;
+  ProfScope ps(c, 6, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 * (ns ? 2.0 : 1.0) + c->n * 8.0);
   CK(cudaMemcpyAsync(c->Wb, W, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CKS(wb_halo(c));
   const size_t mm = (size_t)c->m * c->m;
   const int nblk = c->s_shared ? 1 : c->nE;
+  const double a1dt = a1 * dt, c2 = a2 * dt * dt / 2.0;
+  if (ns) {
+    // columns of K_i and M_i for all elements by colouring (ops_kernels.cu); M goes to S,
+    // then each chunk is copied to Z and inverted back into S
+    auto period = [](int n) { for (int P = 3; P <= n; ++P) if (n % P == 0) return P; return n; };
+    const int Px = period(c->nxl), Py = period(c->nyl);
+    for (int cy = 0; cy < Py; ++cy)
+      for (int cx = 0; cx < Px; ++cx)
+        for (int col = 0; col < c->m; ++col) {
+          CK(launch_colour_seed(c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, col, c->stream));
+          OpArgs A = base_args(c);
+          A.W = c->Wb; A.S = c->tseed; A.out1 = nullptr; A.out2 = c->y1;
+          CKS(run_op(c, OP_R12, A));
+          CK(launch_colour_restrict(c->y1, c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, c->stream));
+          A.out2 = c->y2;
+          CKS(run_op(c, OP_R12, A));
+          CK(launch_colour_gather(c->y1, c->y2, c->Kst, c->S, c->nE, c->nxl, c->m, Px, Py, cx, cy, col, a1dt, c2,
+                                  c->stream));
+        }
+  }
   std::vector<int> hinfo(c->zchunk);
   for (int e0 = 0; e0 < nblk; e0 += c->zchunk) {
     const int ne = std::min(c->zchunk, nblk - e0);
     CK(cudaMemsetAsync(c->info, 0, ne * sizeof(int), c->stream));
-    CK(launch_kbuild(c->cfg, c->geo, c->Wb, a1 * dt, a2 * dt * dt / 2.0, c->Z, e0, ne));
+    if (ns)
+      CK(cudaMemcpyAsync(c->Z, c->S + (size_t)e0 * mm, ne * mm * sizeof(double), cudaMemcpyDeviceToDevice,
+                         c->stream));
+    else
+      CK(launch_kbuild(c->cfg, c->geo, c->Wb, c->halo() ? c->gWb : c->Wb, a1dt, c2, c->Z, e0, ne));
+    CKS(dbg_sync(c, "BJ_ext K/M build"));
     CK(launch_gj_invert(c->Z, c->S + (size_t)e0 * mm, c->m, ne, c->info, c->stream));
+    CKS(dbg_sync(c, "Gauss-Jordan"));
     CK(cudaMemcpyAsync(hinfo.data(), c->info, ne * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (int b = 0; b < ne; ++b)
-      if (hinfo[b]) {
-        char buf[160];
-        snprintf(buf, sizeof buf, "BJ_ext block of element %d is singular (dt=%g, a1=%g, a2=%g)", e0 + b, dt, a1,
-                 a2);
-        return fail(c, HBPDC_E_LU_SINGULAR, buf);
-      }
+    int bad = -1;
+    for (int b = 0; b < ne && bad < 0; ++b)
+      if (hinfo[b]) bad = b;
+    if (c->comm) {   // every rank leaves together (no rank waits in a collective alone)
+      c->hpin[0] = bad >= 0 ? 1.0 : 0.0;
+      CK(cudaMemcpyAsync(c->dnrm, c->hpin, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      CKS(allreduce(c, c->dnrm, 1));
+      CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (c->hpin[0] > 0.0 && bad < 0)
+        return fail(c, HBPDC_E_LU_SINGULAR, "BJ_ext block singular on another rank");
+    }
+    if (bad >= 0) {
+      char buf[200];
+      snprintf(buf, sizeof buf, "BJ_ext block of element %d (rank %d) is singular (dt=%g, a1=%g, a2=%g)", e0 + bad,
+               c->ds.rank, dt, a1, a2);
+      return fail(c, HBPDC_E_LU_SINGULAR, buf);
+    }
   }
   c->pc_a1 = a1; c->pc_a2 = a2; c->pc_dt = dt;
   c->pc_valid = 1;
@@ -308,13 +448,27 @@ hbpdc_status precond_apply_impl(hbpdc_ctx* c, const double* iw, const double* is
   {
     ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 4.0 * c->n * 8.0);
     CK(launch_block_gemv2(c->S, c->s_shared, iw, is, c->U, c->Vv, c->m, c->nE, c->stream));
+    CKS(dbg_sync(c, "BJ_ext GEMV"));
+  }
+  const double a1dt = c->pc_a1 * c->pc_dt, c2 = c->pc_a2 * c->pc_dt * c->pc_dt / 2.0;
+  if (c->pb.equation == HBPDC_NAVIER_STOKES) {
+    // explicit K_i: (K V, K (U - a1dt V)) in one 2-RHS pass over the stored blocks
+    ProfScope ps(c, 5, (double)c->nE * c->m * c->m * 8.0 + 8.0 * c->n * 8.0);
+    CK(launch_waxpby(1.0, c->U, -a1dt, c->Vv, c->y1, c->n, c->stream));
+    CK(launch_block_gemv2(c->Kst, 0, c->Vv, c->y1, c->KV, c->KT, c->m, c->nE, c->stream));
+    CK(launch_waxpby(1.0, c->U, -c2, c->KV, ow, c->n, c->stream));
+    CK(launch_waxpby(1.0, c->Vv, 1.0, c->KT, os, c->n, c->stream));
+    if (c->st) c->st->precond_applies++;
+    return HBPDC_OK;
   }
   OpArgs A = base_args(c);
   A.W = c->Wb; A.U = c->U; A.V = c->Vv; A.out1 = ow; A.out2 = os;
-  A.a1dt = c->pc_a1 * c->pc_dt;
-  A.c2 = c->pc_a2 * c->pc_dt * c->pc_dt / 2.0;
+  A.a1dt = a1dt;
+  A.c2 = c2;
+  A.gW = c->halo() ? c->gWb : c->Wb;
   ProfScope ps(c, 5, 5.0 * c->n * 8.0);
   CK(launch_op(OP_KAPPLY, c->cfg, c->geo, A));
+  CKS(dbg_sync(c, "BJ_ext K apply"));
   if (c->st) c->st->precond_applies++;
   return HBPDC_OK;
 }
@@ -334,7 +488,7 @@ hbpdc_status apply_JPinv(hbpdc_ctx* c, const LinSys& L, const double* v, double*
     CKS(precond_apply_impl(c, v, v + n, c->zb, c->zb + n));
     z = c->zb;
   }
-  return jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr);
+  return jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr, true);
 }
 
 // solve J x = rhs (rhs in c->rhs, x -> c->dX); returns iterations
@@ -394,6 +548,7 @@ hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
         ProfScope ps(c, 3, (double)(nk + (flush ? 1 : 2)) * n2 * 8.0);
         CK(launch_dcgs2_dots(c->Vk, n2, nk, u, flush ? nullptr : w, n2, c->partial, c->stream));
         CK(launch_reduce_partials_n(c->partial, 2 * nk + 3, nb, c->dh, c->stream));
+        CKS(allreduce(c, c->dh, 2 * nk + 3));
       }
       CK(cudaMemcpyAsync(c->hpin, c->dh, (2 * nk + 3) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
@@ -414,10 +569,18 @@ hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
         for (int q = 0; q < nk; ++q) c->hpin[q] = a[q];
         CK(cudaMemcpyAsync(c->dy, c->hpin, nk * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         CK(launch_arnoldi_axpy(c->Vk, n2, nk, c->dy, u, n2, c->partial, c->stream));
-        CK(launch_finish_sqrt(c->partial, nb, c->dnrm, c->stream));
-        CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        b2 = c->hpin[0] * c->hpin[0];
+        if (c->comm) {
+          CK(launch_reduce_partials_n(c->partial, 1, nb, c->dnrm, c->stream));
+          CKS(allreduce(c, c->dnrm, 1));
+          CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+          CK(cudaStreamSynchronize(c->stream));
+          b2 = c->hpin[0];
+        } else {
+          CK(launch_finish_sqrt(c->partial, nb, c->dnrm, c->stream));
+          CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+          CK(cudaStreamSynchronize(c->stream));
+          b2 = c->hpin[0] * c->hpin[0];
+        }
         explicit_q = true;
       }
       const double bu = std::sqrt(std::max(b2, 0.0));
@@ -487,7 +650,7 @@ hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
     }
     if (est_ok) { converged = true; break; }
     // true residual r = rhs - J x
-    CKS(jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, c->dX, c->dX + c->n, r, r + c->n, c->op.jvp_mode, nullptr));
+    CKS(jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, c->dX, c->dX + c->n, r, r + c->n, c->op.jvp_mode, nullptr, true));
     CK(launch_axpby(1.0, c->rhs, -1.0, r, n2, c->stream));
     CKS(norm_host(c, r, n2, &beta));
   }
@@ -667,7 +830,7 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
   CKS(dalloc(c, &c->partial, (size_t)(2 * R + 4) * std::max(arnoldi_dot_blocks(n2), RED_BLOCKS)));
   CKS(dalloc(c, &c->dh, 2 * (size_t)R + 4));
   CKS(dalloc(c, &c->dnrm, 1));
-  CKS(dalloc(c, &c->deps, 1));
+  CKS(dalloc(c, &c->deps, 2));
   CKS(dalloc(c, &c->dy, 2 * (size_t)R + 4));
   CKS(dalloc(c, &c->Wn, n));
   CKS(dalloc(c, &c->bvec, n));
@@ -677,6 +840,19 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
       CKS(dalloc(c, &c->str1[sw][l], n));
       CKS(dalloc(c, &c->str2[sw][l], n));
     }
+  if (c->halo()) {
+    const size_t ng = (size_t)(c->pb.dim == 2 ? 2 * (c->nxl + c->nyl) : 2) * c->m;
+    CKS(dalloc(c, &c->gW, ng));
+    CKS(dalloc(c, &c->gS, ng));
+    CKS(dalloc(c, &c->gdW, ng));
+    CKS(dalloc(c, &c->gdS, ng));
+    CKS(dalloc(c, &c->gWb, ng));
+    size_t off[4], len[4];
+    halo_segments(c->hl, HALO_MAX_FIELDS, off, len);
+    const size_t hb = off[3] + len[3];
+    CKS(dalloc(c, &c->hsend, hb));
+    CKS(dalloc(c, &c->hrecv, hb));
+  }
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {
     const size_t lg = (size_t)c->nE * 6 * 4 * c->nodes;
     CKS(dalloc(c, &c->lift0, lg));
@@ -725,14 +901,34 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->q != 4 && pb->q != 6 && pb->q != 8) return bad("q must be 4, 6 or 8");
   if (pb->kmax < 0) return bad("kmax must be >= 0");
   if (pb->nx < 1 || (pb->dim == 2 && pb->ny < 1)) return bad("element counts must be positive");
-  if (c->ds.nranks != 1) return bad("multi-rank execution is not implemented yet");
+  if (c->ds.nranks < 1 || c->ds.rank < 0 || c->ds.rank >= c->ds.nranks) return bad("bad rank / nranks");
+  if (c->ds.px < 1 || c->ds.py < 1) { c->ds.px = c->ds.nranks; c->ds.py = 1; }
+  if (c->ds.px * c->ds.py != c->ds.nranks) return bad("px * py must equal nranks");
+  if (pb->dim == 1 && c->ds.py != 1) return bad("1D partitions need py = 1");
+  if (pb->nx % c->ds.px || (pb->dim == 2 && pb->ny % c->ds.py)) return bad("px must divide nx and py divide ny");
+  const bool halo = c->ds.nranks > 1 || c->ds.force_halo;
+  if (halo && pb->equation == HBPDC_NAVIER_STOKES)
+    return bad("the element partition of Navier-Stokes (two-hop BR1 halo) is not implemented yet");
   if (op->gmres_restart < 1 || op->krylov_max_per_newton < 1 || op->newton_max < 0) return bad("bad solver options");
   c->nv = pb->equation == HBPDC_ADVECTION ? 1 : 4;
   c->P = pb->N + 1;
   c->nodes = pb->dim == 2 ? c->P * c->P : c->P;
   c->m = c->nv * c->nodes;
-  c->nxl = pb->nx;
-  c->nyl = pb->dim == 2 ? pb->ny : 1;
+  c->nxl = pb->nx / c->ds.px;
+  c->nyl = pb->dim == 2 ? pb->ny / c->ds.py : 1;
+  {
+    const int rx = c->ds.rank % c->ds.px, ry = c->ds.rank / c->ds.px;
+    c->ex0 = rx * c->nxl;
+    c->ey0 = ry * c->nyl;
+    c->nbr[0] = ry * c->ds.px + (rx + c->ds.px - 1) % c->ds.px;
+    c->nbr[1] = ry * c->ds.px + (rx + 1) % c->ds.px;
+    c->nbr[2] = ((ry + c->ds.py - 1) % c->ds.py) * c->ds.px + rx;
+    c->nbr[3] = ((ry + 1) % c->ds.py) * c->ds.px + rx;
+    // a direction exchanges halos when it is split over ranks (or forced)
+    const int hx = halo && (c->ds.px > 1 || c->ds.force_halo);
+    const int hy = halo && pb->dim == 2 && (c->ds.py > 1 || c->ds.force_halo);
+    c->hl = HaloLayout{c->nxl, c->nyl, pb->equation == HBPDC_ADVECTION ? 1 : 4, pb->N + 1, pb->dim, {hx, hx, hy, hy}};
+  }
   c->nE = c->nxl * c->nyl;
   c->n = (size_t)c->nE * c->m;
   c->restart = op->gmres_restart;
@@ -744,6 +940,8 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->geo.nx = c->nxl;
   c->geo.ny = c->nyl;
   c->geo.nE = c->nE;
+  c->geo.hx = c->hl.active[0];
+  c->geo.hy = c->hl.active[2];
   c->geo.sx = 2.0 / dx;
   c->geo.sy = 2.0 / dy;
   c->geo.lhp = c->basis.lhp;
@@ -772,10 +970,59 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
     c->own_stream = true;
   }
   c->cfg.stream = c->stream;
+  if (halo) {
+    std::string err;
+    int kind = c->ds.comm;
+    if (kind == HBPDC_COMM_AUTO) kind = HBPDC_COMM_NCCL;
+    if (kind == HBPDC_COMM_NCCL) c->comm = hbpdc::make_nccl_comm(c->ds.rank, c->ds.nranks, c->ds.nccl_unique_id, err);
+    else if (kind == HBPDC_COMM_LOOPBACK)
+      c->comm = hbpdc::make_loopback_comm((hbpdc::LoopbackGroup*)c->ds.loopback_group, c->ds.rank);
+    else err = "unknown comm kind";
+    if (!c->comm) {
+      c->err = err.empty() ? "cannot create the communicator" : err;
+      *out = c;
+      return HBPDC_E_NCCL;
+    }
+  }
+  { const char* dbg = std::getenv("HBPDC_DEBUG_SYNC"); c->debug_sync = dbg && dbg[0] == '1'; }
   hbpdc_status s = alloc_solver(c);
   *out = c;
   return s;
 }
+
+hbpdc_status hbpdc_partition(int dim, int nx, int ny, int px, int py, int rank, int* ex0, int* ey0, int* nxl,
+                             int* nyl, int* nbr4) {
+  if (dim == 1) ny = 1;
+  if (nx < 1 || ny < 1 || px < 1 || py < 1 || (dim == 1 && py != 1) || nx % px || ny % py || rank < 0 ||
+      rank >= px * py)
+    return HBPDC_E_ARG;
+  const int rx = rank % px, ry = rank / px;
+  if (ex0) *ex0 = rx * (nx / px);
+  if (ey0) *ey0 = ry * (ny / py);
+  if (nxl) *nxl = nx / px;
+  if (nyl) *nyl = ny / py;
+  if (nbr4) {
+    nbr4[0] = ry * px + (rx + px - 1) % px;
+    nbr4[1] = ry * px + (rx + 1) % px;
+    nbr4[2] = ((ry + py - 1) % py) * px + rx;
+    nbr4[3] = ((ry + 1) % py) * px + rx;
+  }
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_nccl_unique_id(void* out128) {
+  if (!out128) return HBPDC_E_ARG;
+  std::string e;
+  return hbpdc::nccl_unique_id(out128, e) ? HBPDC_E_NCCL : HBPDC_OK;
+}
+
+hbpdc_status hbpdc_loopback_group_create(int nranks, void** group) {
+  if (!group || nranks < 1) return HBPDC_E_ARG;
+  *group = hbpdc::loopback_group_create(nranks);
+  return HBPDC_OK;
+}
+
+void hbpdc_loopback_group_destroy(void* group) { hbpdc::loopback_group_destroy((hbpdc::LoopbackGroup*)group); }
 
 hbpdc_status hbpdc_local_shape(const hbpdc_ctx* c, int* nle, int* m, int* ex0, int* ey0, int* nxl, int* nyl) {
   if (!c) return HBPDC_E_ARG;
@@ -857,10 +1104,13 @@ hbpdc_status hbpdc_precond_set(hbpdc_ctx* c, double a1, double a2, double dt, co
                                int shared) {
   if (!c || !W || !S) return HBPDC_E_ARG;
   CKS(ensure_precond_mem(c));
+  if (c->pb.equation == HBPDC_NAVIER_STOKES)
+    return fail(c, HBPDC_E_ARG, "precond_set: Navier-Stokes applies the stored K_i too; build it instead");
   if (shared != c->s_shared) return fail(c, HBPDC_E_ARG, "shared flag does not match the equation");
   const size_t nblk = c->s_shared ? 1 : (size_t)c->nE;
   CK(cudaMemcpyAsync(c->S, S, nblk * c->m * c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaMemcpyAsync(c->Wb, W, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CKS(wb_halo(c));
   c->pc_a1 = a1; c->pc_a2 = a2; c->pc_dt = dt;
   c->pc_valid = 1;
   return HBPDC_OK;
@@ -958,6 +1208,7 @@ void hbpdc_finalize(hbpdc_ctx* c) {
   prof_flush(c);
   for (void* p : c->allocs) cudaFree(p);
   if (c->hpin) cudaFreeHost(c->hpin);
+  delete c->comm;
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -1,5 +1,7 @@
 // launch.h -- host-side entry points of the device kernels (internal).
 #pragma once
+#include <algorithm>
+#include <cstddef>
 #include <cuda_runtime.h>
 #include "physics.cuh"
 
@@ -22,8 +24,17 @@ cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, co
 // number of jet components of the lifted gradients of (kind, state)
 int lift_jet_components(OpKind kind, int state);
 // BJ_ext: M_i = I - a1dt K_i + c2 K_i^2 for elements [e0, e0+ne), row-major m x m each
-cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, double a1dt, double c2,
+cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
                           double* M, int e0, int ne);
+
+// BJ_ext build by element colouring (NS): seed e_col in the colour's elements,
+// restrict a vector to them, gather K and M columns of the seeded elements
+cudaError_t launch_colour_seed(double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy, int col,
+                               cudaStream_t st);
+cudaError_t launch_colour_restrict(const double* y, double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy,
+                                   cudaStream_t st);
+cudaError_t launch_colour_gather(const double* y1, const double* y2, double* K, double* M, int nE, int nx, int m,
+                                 int Px, int Py, int cx, int cy, int col, double a1dt, double c2, cudaStream_t st);
 
 // ---- linalg.cu -----------------------------------------------------------------
 // in-place Gauss-Jordan inversion with partial pivoting of `nmat` m x m
@@ -85,6 +96,20 @@ cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, c
 cudaError_t launch_stage_combo(const double* base, int nx, const double* const* X, const double* a,
                                int ny, const double* const* Y, const double* b, double* y, size_t L,
                                cudaStream_t st);
+
+// ---- halo.cu: face-trace halo of the element partition (comm.h) -----------------
+constexpr int HALO_MAX_FIELDS = 4;
+struct HaloLayout {
+  int nx, ny, nv, P, dim;   // local element grid, variables, nodes per direction, dimension
+  int active[4];            // sides taking part: -x, +x, -y, +y
+};
+// segment offsets / lengths (doubles) of an exchange of nf fields
+void halo_segments(const HaloLayout& L, int nf, size_t off[4], size_t len[4]);
+// send <- boundary-node values of src[0..nf) ; dst[f] ghost elements <- recv
+cudaError_t launch_halo_pack(const HaloLayout& L, int nf, const double* const* src, double* send, cudaStream_t st);
+cudaError_t launch_halo_unpack(const HaloLayout& L, int nf, const double* recv, double* const* dst, cudaStream_t st);
+// out = c / sqrt(*sum), or 0 if *sum == 0
+cudaError_t launch_fd_eps_from_sum(const double* sum, double c, double* out, cudaStream_t st);
 
 // kernel-launch counter (reported by hbpdc_launch_count)
 extern long long g_hbpdc_launches;

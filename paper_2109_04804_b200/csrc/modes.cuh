@@ -24,6 +24,8 @@ struct OpArgs {
   double epsw;          // FD step for the W direction (<= 0: quotient is 0)
   const double* d_epsw; // if non-NULL, the FD step is read from device memory
   int m;                // doubles per element
+  int nE;               // local elements; e >= nE addresses a ghost element (halo)
+  const double *gW, *gS, *gdW, *gdS;   // ghost copies (neighbour ranks' face traces)
 };
 
 __device__ __forceinline__ double fd_step(const OpArgs& A) { return A.d_epsw ? *A.d_epsw : A.epsw; }
@@ -34,6 +36,9 @@ __device__ __forceinline__ void ld_state(const double* G, int e, int node, NodeS
 }
 
 #define IDX(e, v, node) ((size_t)(e) * A.m + (v) * NODES + (node))
+// field F at (e, v, node) for a node-state load: elements e >= A.nE are ghosts
+// (halo copies of a neighbouring rank's face traces, same layout, comm.h)
+#define FV(F, e, v, node) ((e) < A.nE ? A.F[IDX(e, v, node)] : A.g##F[IDX((e) - A.nE, v, node)])
 
 // Single-jet modes: Derived supplies  using J; load_w; comb(A, const J* F, c).
 template <int EQ, int NODES, class Derived, class J, int NCH_>
@@ -66,7 +71,7 @@ template <int EQ, int NODES> struct ModeR1 : OneJetMode<EQ, NODES, ModeR1<EQ, NO
   static constexpr int NV = NVars<EQ>::value, NCH = 1;
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, double* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = A.W[IDX(e, v, node)];
+    for (int v = 0; v < NV; ++v) w[v] = FV(W, e, v, node);
   }
   __device__ static void comb(const OpArgs&, const double* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) c[0][v] = F[v];
@@ -82,7 +87,7 @@ template <int EQ, int NODES> struct ModeR1Abs : OneJetMode<EQ, NODES, ModeR1Abs<
   static constexpr int NV = NVars<EQ>::value, NCH = 1;
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, double* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = A.W[IDX(e, v, node)];
+    for (int v = 0; v < NV; ++v) w[v] = FV(W, e, v, node);
   }
   __device__ static void comb(const OpArgs&, const double* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) c[0][v] = fabs(F[v]);
@@ -97,7 +102,7 @@ template <int EQ, int NODES> struct ModeR12 : OneJetMode<EQ, NODES, ModeR12<EQ, 
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = J1{A.W[IDX(e, v, node)], A.S[IDX(e, v, node)]};
+    for (int v = 0; v < NV; ++v) w[v] = J1{FV(W, e, v, node), FV(S, e, v, node)};
   }
   __device__ static void comb(const OpArgs&, const J1* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) { c[0][v] = F[v].v; c[1][v] = F[v].a; }
@@ -116,7 +121,7 @@ template <int EQ, int NODES> struct ModeResid : OneJetMode<EQ, NODES, ModeResid<
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = J1{A.W[IDX(e, v, node)], A.S[IDX(e, v, node)]};
+    for (int v = 0; v < NV; ++v) w[v] = J1{FV(W, e, v, node), FV(S, e, v, node)};
   }
   __device__ static void comb(const OpArgs& A, const J1* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
@@ -141,8 +146,7 @@ template <int EQ, int NODES> struct ModeJvpExact : OneJetMode<EQ, NODES, ModeJvp
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, HJ* w, bool) {
     for (int v = 0; v < NV; ++v) {
-      const size_t k = IDX(e, v, node);
-      w[v] = HJ{A.W[k], A.S[k], A.dW[k], A.dS[k]};
+      w[v] = HJ{FV(W, e, v, node), FV(S, e, v, node), FV(dW, e, v, node), FV(dS, e, v, node)};
     }
   }
   __device__ static void comb(const OpArgs& A, const HJ* F, double (&c)[NCH][NV]) {
@@ -174,13 +178,13 @@ template <int EQ, int NODES> struct ModeJvpFD {
   template <int K>
   __device__ static void load_w(const Args& A, int e, int node, StateT<K>* w, bool) {
     for (int v = 0; v < NV; ++v) {
-      const size_t k = IDX(e, v, node);
+      const double Wk = FV(W, e, v, node), Sk = FV(S, e, v, node);
       if constexpr (K == 0) {
         const double ew = fd_step(A);
-        const double wp = ew > 0.0 ? __dadd_rn(A.W[k], __dmul_rn(ew, A.dW[k])) : A.W[k];
-        w[v] = J1{wp, A.S[k]};
+        const double wp = ew > 0.0 ? __dadd_rn(Wk, __dmul_rn(ew, FV(dW, e, v, node))) : Wk;
+        w[v] = J1{wp, Sk};
       } else {
-        w[v] = J2{A.W[k], A.S[k], A.dS[k]};
+        w[v] = J2{Wk, Sk, FV(dS, e, v, node)};
       }
     }
   }
@@ -271,13 +275,13 @@ template <int EQ, int NODES> struct ModeJvpLinear {
   struct State { NodeState<EQ, double> u0, u1; };
   template <int K>
   __device__ static void load_w(const Args& A, int e, int node, double* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = A.dW[IDX(e, v, node)];
+    for (int v = 0; v < NV; ++v) w[v] = FV(dW, e, v, node);
   }
   __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool) {
     for (int v = 0; v < NV; ++v) {
-      const size_t k = IDX(e, v, node);
-      st.u0.w[v] = fma(A.c2, A.dS[k], -A.a1dt * A.dW[k]);
-      st.u1.w[v] = A.dW[k];
+      const double dw = FV(dW, e, v, node);
+      st.u0.w[v] = fma(A.c2, FV(dS, e, v, node), -A.a1dt * dw);
+      st.u1.w[v] = dw;
     }
   }
   template <int DIM>
@@ -314,9 +318,12 @@ template <int EQ, int NODES> struct ModeKApply : OneJetMode<EQ, NODES, ModeKAppl
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, J2* w, bool nbr) {
     for (int v = 0; v < NV; ++v) {
-      const size_t k = IDX(e, v, node);
-      if (nbr) w[v] = J2{A.W[k], 0.0, 0.0};
-      else w[v] = J2{A.W[k], A.V[k], fma(-A.a1dt, A.V[k], A.U[k])};
+      if (nbr) {
+        w[v] = J2{FV(W, e, v, node), 0.0, 0.0};
+      } else {
+        const size_t k = IDX(e, v, node);
+        w[v] = J2{A.W[k], A.V[k], fma(-A.a1dt, A.V[k], A.U[k])};
+      }
     }
   }
   __device__ static void comb(const OpArgs&, const J2* F, double (&c)[NCH][NV]) {
@@ -331,4 +338,5 @@ template <int EQ, int NODES> struct ModeKApply : OneJetMode<EQ, NODES, ModeKAppl
   }
 };
 
+#undef FV
 #undef IDX

@@ -25,17 +25,32 @@
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
 struct Geo {
-  int nx, ny, nE;          // local element grid (single rank: global)
+  int nx, ny, nE;          // local element grid
+  int hx, hy;              // 1: the -x/+x (-y/+y) neighbours are ghosts (halo), not a local wrap
   double sx, sy;           // 2/dx, 2/dy
   double lhp, lhm;         // lhat_N(+1) = 1/w_N, lhat_0(-1) = 1/w_0  (GLL)
   double Dh[64];           // Dhat (P x P, row-major)
 };
 
 // ---- neighbour addressing (periodic Cartesian, layout L) ----------------------
+// Across a partition boundary (hx / hy) the neighbour is a ghost element
+// nE + g, g = [-x: ey | +x: ny + ey | -y: 2ny + ex | +y: 2ny + nx + ex]
+// (1D: ny = 1), whose face traces the halo exchange filled in (comm.h).
 __device__ __forceinline__ int nbr_elem(const Geo& g, int e, int d, int side) {
   int ex = e % g.nx, ey = e / g.nx;
-  if (d == 0) ex = side > 0 ? (ex + 1 == g.nx ? 0 : ex + 1) : (ex == 0 ? g.nx - 1 : ex - 1);
-  else ey = side > 0 ? (ey + 1 == g.ny ? 0 : ey + 1) : (ey == 0 ? g.ny - 1 : ey - 1);
+  if (d == 0) {
+    if (side > 0) {
+      if (ex + 1 == g.nx) { if (g.hx) return g.nE + g.ny + ey; ex = 0; } else ++ex;
+    } else {
+      if (ex == 0) { if (g.hx) return g.nE + ey; ex = g.nx - 1; } else --ex;
+    }
+  } else {
+    if (side > 0) {
+      if (ey + 1 == g.ny) { if (g.hy) return g.nE + 2 * g.ny + g.nx + ex; ey = 0; } else ++ey;
+    } else {
+      if (ey == 0) { if (g.hy) return g.nE + 2 * g.ny + ex; ey = g.ny - 1; } else --ey;
+    }
+  }
   return ey * g.nx + ex;
 }
 

@@ -32,8 +32,9 @@ static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, doubl
 // t = K e_c.  "element-internal influence only", block formula P:314.
 struct KColArgs {
   const double* W;      // build state
+  const double* gW;     // its ghost copy (halo), elements e >= nE
   const double* tan;    // shared-memory tangents, one m-vector per slot
-  int m;
+  int m, nE;
 };
 
 template <int EQ, int NODES> struct ModeKCol {
@@ -43,7 +44,8 @@ template <int EQ, int NODES> struct ModeKCol {
   struct State { NodeState<EQ, J1> s; };
   __device__ static void load(const Args& A, const Geo&, int e, int slot, int node, State& st, bool nbr) {
     for (int v = 0; v < NV; ++v) {
-      const double w = A.W[(size_t)e * A.m + v * NODES + node];
+      const double w = e < A.nE ? A.W[(size_t)e * A.m + v * NODES + node]
+                                : A.gW[(size_t)(e - A.nE) * A.m + v * NODES + node];
       st.s.w[v] = J1{w, nbr ? 0.0 : A.tan[slot * A.m + v * NODES + node]};
     }
   }
@@ -64,7 +66,7 @@ template <int EQ, int NODES> struct ModeKCol {
 
 template <int EQ, int DIM, int P, int EPB>
 __global__ void __launch_bounds__(EPB * ipow(P, DIM))
-kbuild_kernel(const double* __restrict__ Wb, const PhysParams pp, const Geo g, double a1dt, double c2,
+kbuild_kernel(const double* __restrict__ Wb, const double* __restrict__ gWb, const PhysParams pp, const Geo g, double a1dt, double c2,
               double* __restrict__ M, int e0) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int NV = NVars<EQ>::value;
@@ -76,7 +78,7 @@ kbuild_kernel(const double* __restrict__ Wb, const PhysParams pp, const Geo g, d
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
   const int e = e0 + blockIdx.x;
   double* Me = M + (size_t)blockIdx.x * m * m;
-  KColArgs A{Wb, stan, m};
+  KColArgs A{Wb, gWb, stan, m, g.nE};
   for (int c0 = 0; c0 < m; c0 += EPB) {
     const int col = c0 + slot;
     const bool active = col < m;
@@ -103,12 +105,12 @@ kbuild_kernel(const double* __restrict__ Wb, const PhysParams pp, const Geo g, d
 }
 
 template <int EQ, int DIM, int P>
-static cudaError_t run_kbuild(const OpCfg& c, const Geo& g, const double* Wb, double a1dt, double c2,
+static cudaError_t run_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
                               double* M, int e0, int ne) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int EPB = epb_for(NODES);
   if (ne <= 0) return cudaSuccess;
-  kbuild_kernel<EQ, DIM, P, EPB><<<ne, EPB * NODES, 0, c.stream>>>(Wb, c.pp, g, a1dt, c2, M, e0);
+  kbuild_kernel<EQ, DIM, P, EPB><<<ne, EPB * NODES, 0, c.stream>>>(Wb, gWb, c.pp, g, a1dt, c2, M, e0);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -148,9 +150,9 @@ template <int EQ, int DIM, int P> struct Disp {
     }
     return cudaErrorInvalidValue;
   }
-  static cudaError_t kbuild(const OpCfg& c, const Geo& g, const double* Wb, double a1dt, double c2,
+  static cudaError_t kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
                             double* M, int e0, int ne) {
-    if constexpr (EQ != 2) return run_kbuild<EQ, DIM, P>(c, g, Wb, a1dt, c2, M, e0, ne);
+    if constexpr (EQ != 2) return run_kbuild<EQ, DIM, P>(c, g, Wb, gWb, a1dt, c2, M, e0, ne);
     return cudaErrorNotSupported;
   }
 };
@@ -187,7 +189,74 @@ int lift_jet_components(OpKind kind, int state) {
   }
 }
 
-cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, double a1dt, double c2,
+cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
                           double* M, int e0, int ne) {
-  return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, a1dt, c2, M, e0, ne); });
+  return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, gWb, a1dt, c2, M, e0, ne); });
+}
+
+// ---- BJ_ext build by element colouring (Navier-Stokes, BR1 stencil radius 2) ----
+// The element block K_i of dR1/dW includes the two-hop path through the
+// neighbours' lifted gradients (their central face value depends on W_i).  All
+// elements of one colour class (ex mod Px, ey mod Py), Px, Py > 2, are seeded
+// with e_c at once: no two seeded elements reach each other, so the seeded
+// elements' outputs of the linearised operator are exactly K_i e_c (the other
+// tangents are exact zeros).  Same colouring as the oracle (oracle element_jacobians).
+namespace {
+__device__ __forceinline__ bool in_colour(int e, int nx, int Px, int Py, int cx, int cy) {
+  const int ex = e % nx, ey = e / nx;
+  return ex % Px == cx && ey % Py == cy;
+}
+
+__global__ void colour_seed_kernel(double* __restrict__ t, int nE, int nx, int m, int Px, int Py, int cx, int cy,
+                                   int col) {
+  const size_t n = (size_t)nE * m;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(k / m), r = (int)(k % m);
+    t[k] = (r == col && in_colour(e, nx, Px, Py, cx, cy)) ? 1.0 : 0.0;
+  }
+}
+
+__global__ void colour_restrict_kernel(const double* __restrict__ y, double* __restrict__ t, int nE, int nx, int m,
+                                       int Px, int Py, int cx, int cy) {
+  const size_t n = (size_t)nE * m;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(k / m);
+    t[k] = in_colour(e, nx, Px, Py, cx, cy) ? y[k] : 0.0;
+  }
+}
+
+// K[e][r][col] = y1, M[e][r][col] = delta - a1dt y1 + c2 y2 for the seeded elements
+__global__ void colour_gather_kernel(const double* __restrict__ y1, const double* __restrict__ y2,
+                                     double* __restrict__ K, double* __restrict__ M, int nE, int nx, int m, int Px,
+                                     int Py, int cx, int cy, int col, double a1dt, double c2) {
+  const size_t n = (size_t)nE * m;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(k / m), r = (int)(k % m);
+    if (!in_colour(e, nx, Px, Py, cx, cy)) continue;
+    const size_t o = ((size_t)e * m + r) * m + col;
+    K[o] = y1[k];
+    M[o] = fma(c2, y2[k], (r == col ? 1.0 : 0.0) - a1dt * y1[k]);
+  }
+}
+}  // namespace
+
+cudaError_t launch_colour_seed(double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy, int col,
+                               cudaStream_t st) {
+  colour_seed_kernel<<<1184, 256, 0, st>>>(t, nE, nx, m, Px, Py, cx, cy, col);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colour_restrict(const double* y, double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy,
+                                   cudaStream_t st) {
+  colour_restrict_kernel<<<1184, 256, 0, st>>>(y, t, nE, nx, m, Px, Py, cx, cy);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colour_gather(const double* y1, const double* y2, double* K, double* M, int nE, int nx, int m,
+                                 int Px, int Py, int cx, int cy, int col, double a1dt, double c2, cudaStream_t st) {
+  colour_gather_kernel<<<1184, 256, 0, st>>>(y1, y2, K, M, nE, nx, m, Px, Py, cx, cy, col, a1dt, c2);
+  hbpdc_count_launch();
+  return cudaGetLastError();
 }

@@ -28,7 +28,11 @@ STATUS = {0: "OK", 1: "E_ARG", 2: "E_CUDA", 3: "E_NCCL", 4: "E_OOM", 5: "E_NONFI
 EXPORTS = ["hbpdc_init", "hbpdc_local_shape", "hbpdc_node_coords", "hbpdc_rhs", "hbpdc_residual",
            "hbpdc_jvp", "hbpdc_precond_build", "hbpdc_precond_set", "hbpdc_precond_export",
            "hbpdc_precond_apply", "hbpdc_step", "hbpdc_step_host", "hbpdc_reset", "hbpdc_profile",
-           "hbpdc_profile_read", "hbpdc_launch_count", "hbpdc_last_error", "hbpdc_finalize"]
+           "hbpdc_profile_read", "hbpdc_launch_count", "hbpdc_last_error", "hbpdc_finalize",
+           "hbpdc_partition", "hbpdc_nccl_unique_id", "hbpdc_loopback_group_create",
+           "hbpdc_loopback_group_destroy"]
+COMM_AUTO, COMM_NCCL, COMM_LOOPBACK = 0, 1, 2
+_COMM = {"auto": COMM_AUTO, "nccl": COMM_NCCL, "loopback": COMM_LOOPBACK}
 
 
 class Problem(ctypes.Structure):
@@ -52,7 +56,8 @@ class SolverOpts(ctypes.Structure):
 class Dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("px", ctypes.c_int),
                 ("py", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
-                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int), ("own_stream", ctypes.c_int)]
+                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int), ("own_stream", ctypes.c_int),
+                ("comm", ctypes.c_int), ("loopback_group", ctypes.c_void_p), ("force_halo", ctypes.c_int)]
 
 
 class StepStats(ctypes.Structure):
@@ -100,6 +105,10 @@ def load():
         "hbpdc_launch_count": (I, [ctypes.POINTER(ctypes.c_longlong)]),
         "hbpdc_last_error": (ctypes.c_char_p, [P]),
         "hbpdc_finalize": (V, [P]),
+        "hbpdc_partition": (I, [I, I, I, I, I, I] + [ctypes.POINTER(ctypes.c_int)] * 5),
+        "hbpdc_nccl_unique_id": (I, [P]),
+        "hbpdc_loopback_group_create": (I, [I, ctypes.POINTER(P)]),
+        "hbpdc_loopback_group_destroy": (V, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -107,6 +116,41 @@ def load():
         f.argtypes = args
     _lib = lib
     return lib
+
+
+def partition(dim, nx, ny, px, py, rank):
+    """Host-only partition arithmetic of the library: (ex0, ey0, nx_local,
+    ny_local, [nbr -x, +x, -y, +y])."""
+    v = [ctypes.c_int() for _ in range(4)]
+    nb = (ctypes.c_int * 4)()
+    st = load().hbpdc_partition(dim, nx, ny, px, py, rank, *[ctypes.byref(x) for x in v], nb)
+    if st != 0:
+        raise HbpdcError(st, "invalid partition")
+    return tuple(x.value for x in v) + (list(nb),)
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id (rank 0 creates it, torch.distributed distributes it)."""
+    buf = ctypes.create_string_buffer(128)
+    st = load().hbpdc_nccl_unique_id(buf)
+    if st != 0:
+        raise HbpdcError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+class LoopbackGroup:
+    """Ranks living as host threads of this process (COMM_LOOPBACK)."""
+
+    def __init__(self, nranks):
+        self.h = ctypes.c_void_p()
+        st = load().hbpdc_loopback_group_create(nranks, ctypes.byref(self.h))
+        if st != 0:
+            raise HbpdcError(st, "loopback group")
+
+    def close(self):
+        if self.h and self.h.value:
+            load().hbpdc_loopback_group_destroy(self.h)
+            self.h = ctypes.c_void_p()
 
 
 def launch_count():
@@ -138,7 +182,8 @@ class Context:
                  gamma=1.4, mu=0.0, prandtl=0.72, q=4, kmax=0, newton_rtol=1e-10,
                  newton_atol_dw=1e-12, newton_floor=64.0, newton_max=50, gmres_rtol=1e-6,
                  restart=700, max_krylov=7000, precond="bjext", precond_policy="per_step_per_alpha",
-                 jvp_mode="auto", rank=0, nranks=1, px=1, py=1, nccl_id=None, stream=None, device=0):
+                 jvp_mode="auto", rank=0, nranks=1, px=1, py=1, nccl_id=None, stream=None, device=0,
+                 comm="auto", loopback=None, force_halo=False):
         import torch
         self.lib = load()
         if not torch.cuda.is_available():
@@ -158,7 +203,10 @@ class Context:
         self._nccl_id = nccl_id
         ds = Dist(rank=rank, nranks=nranks, px=px, py=py,
                   nccl_unique_id=ctypes.cast(ctypes.c_char_p(nccl_id), ctypes.c_void_p) if nccl_id else None,
-                  cuda_stream=ctypes.c_void_p(stream.cuda_stream), device=device, own_stream=0)
+                  cuda_stream=ctypes.c_void_p(stream.cuda_stream), device=device, own_stream=0,
+                  comm=_COMM[comm], loopback_group=loopback.h if loopback is not None else None,
+                  force_halo=int(force_halo))
+        self._ds = ds
         h = ctypes.c_void_p()
         st = self.lib.hbpdc_init(ctypes.byref(pb), ctypes.byref(op), ctypes.byref(ds), ctypes.byref(h))
         self.h = h
@@ -174,6 +222,7 @@ class Context:
         self.n = self.n_elem * self.m
         self.dim, self.N = dim, N
         self.device = device
+        self.rank, self.nranks, self.px, self.py = rank, nranks, px, py
 
     # -- helpers ---------------------------------------------------------------------
     def _check(self, st):

@@ -63,16 +63,34 @@ def layout(vars_, dim):
 CASE_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
 
 
-def initial_state(case, coords, noise=None, gamma=GAMMA):
+def initial_state(case, coords, noise=None, gamma=GAMMA, stream=0):
     """Nodal interpolation of the IC in layout L, plus the seeded
     uniform noise of amplitude `noise` on every conserved variable (C3:
-    1e-6), drawn in layout order from default_rng(MASTER_SEED + k)."""
+    1e-6), drawn in layout order from default_rng(MASTER_SEED + k).
+    stream > 0 (the rank of a tiled multi-GPU bench block) draws from
+    default_rng(MASTER_SEED + k + 1000 * stream) instead."""
     dim = len(coords)
     W = layout(ic_primitive(case, *coords, gamma=gamma), dim)
     if noise:
-        rng = np.random.default_rng(MASTER_SEED + CASE_INDEX[case])
+        rng = np.random.default_rng(MASTER_SEED + CASE_INDEX[case] + 1000 * stream)
         W = W + rng.uniform(-noise, noise, size=W.shape)
     return W
+
+
+def tile_coords(coords, bounds):
+    """Map node coordinates of a mesh made of repeated copies of a config's
+    periodic domain back into the copy at [xmin, xmax) x [ymin, ymax): each
+    element is shifted by whole periods according to its centre, so every
+    tile sees exactly the config's own nodes (the multi-GPU bench repeats
+    C3's tile).  Identity on the config's own mesh."""
+    out = []
+    for d, c in enumerate(coords):
+        c = np.asarray(c)
+        lo, hi = bounds[2 * d], bounds[2 * d + 1]
+        ctr = c.mean(axis=tuple(range(c.ndim - (len(coords)), c.ndim)), keepdims=True)
+        tile = np.floor((ctr - lo) / (hi - lo))
+        out.append(c - tile * (hi - lo))
+    return tuple(out)
 
 
 def perturbed_state(W_ic, seed, rel=1e-2):

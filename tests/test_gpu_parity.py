@@ -23,7 +23,11 @@ OPS_CASES = [
     ("euler", 7, 5, 3, (0.0, 1.0, 0.0, 1.0)),
     ("euler", 3, 11, 6, (0.0, 1.0, 0.0, 1.0)),
     ("euler", 2, 4, 4, (0.0, 1.0, 0.0, 1.0)),
+    ("navier_stokes", 3, 4, 4, (0.0, 2 * np.pi, 0.0, 2 * np.pi)),
+    ("navier_stokes", 5, 5, 3, (0.0, 2 * np.pi, 0.0, 2 * np.pi)),
 ]
+
+NS_MU = 0.05      # viscosity for NS operator tests: viscous terms O(1) relative (C5 uses 1e-3)
 
 
 def _state(d, kind, seed):
@@ -36,6 +40,8 @@ def _state(d, kind, seed):
 
 def _pair(kind, N, nx, ny, bounds, **kw):
     a = (1.0, 0.0) if ny is None else (1.0, -0.6)
+    if kind == "navier_stokes":
+        kw.setdefault("mu", NS_MU)
     return make_pair(kind, N, nx, ny, bounds=bounds, a=a, **kw)
 
 
@@ -149,6 +155,8 @@ PC_CASES = [
     ("advection", 2, 6, 4, (0.0, 1.0, 0.0, 1.0)),
     ("euler", 2, 4, 4, (0.0, 1.0, 0.0, 1.0)),
     ("euler", 3, 4, 2, (0.0, 1.0, 0.0, 1.0)),
+    ("navier_stokes", 2, 4, 3, (0.0, 2 * np.pi, 0.0, 2 * np.pi)),
+    ("navier_stokes", 3, 3, 3, (0.0, 2 * np.pi, 0.0, 2 * np.pi)),
 ]
 
 
@@ -173,6 +181,8 @@ def test_precond_build_and_apply(case):
     to, bo = pc.apply(x, y)
     tg, bg = ctx.precond_apply(to_gpu(x), to_gpu(y))
     assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11 * max(1, cond / 1e4)
+    if kind == "navier_stokes":
+        return        # NS applies its stored K_i as well; precond_set installs S only
     # identical S (the oracle's, installed into the library): apply <= 1e-13
     ctx.precond_set(a1, a2, dt, to_gpu(W), to_gpu(So.reshape(-1)), shared)
     tg, bg = ctx.precond_apply(to_gpu(x), to_gpu(y))
@@ -235,6 +245,22 @@ def test_euler_end_of_run(q, kmax):
     W0 = inputs.initial_state("C3", d.node_coords(), noise=cfg.noise)
     dt = configs.cfl_dt(cfg, inputs.initial_state("C3", d.node_coords()))
     Wo, sto = _run_oracle(d, q, kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol)
+    Wg = to_gpu(W0)
+    for _ in range(cfg.steps):
+        ctx.step(dt, Wg)
+    assert rel(to_np(Wg), Wo) <= 1e-8
+
+
+def test_c5_shape_end_of_run():
+    """C5 physics (2D Navier-Stokes, BR1, TGV-type vortex at Mach 0.1, mu = 1e-3,
+    Pr 0.72) at a reduced mesh: 4x4 elements, N=3, HBPC(6,2), BJ_ext, FD JVP,
+    2 steps of the CFL-1 step; GPU vs oracle <= 1e-8."""
+    cfg = configs.scaled(configs.CONFIGS["C5"], N=3, nx=4, ny=4, steps=2)
+    d, ctx = make_pair("navier_stokes", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, mu=cfg.mu, q=cfg.q,
+                       kmax=cfg.kmax, gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol)
+    W0 = inputs.initial_state("C5", d.node_coords())
+    dt = configs.cfl_dt(cfg, W0)
+    Wo, sto = _run_oracle(d, cfg.q, cfg.kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol)
     Wg = to_gpu(W0)
     for _ in range(cfg.steps):
         ctx.step(dt, Wg)
