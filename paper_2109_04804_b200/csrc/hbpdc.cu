@@ -86,7 +86,8 @@ struct hbpdc_ctx {
   // device memory
   std::vector<void*> allocs;
   double *X = nullptr, *G = nullptr, *dX = nullptr, *rhs = nullptr, *tmp2 = nullptr, *zb = nullptr;
-  double *Vk = nullptr;        // Krylov basis (restart+1) x 2n
+  double *Vk = nullptr;        // Krylov basis: vk_cap x 2n, grown on demand up to restart+1
+  size_t vk_cap = 0;
   double *partial = nullptr;   // (restart+2) x RED_BLOCKS
   double *dh = nullptr, *dnrm = nullptr, *deps = nullptr, *dy = nullptr;
   double *lift0 = nullptr, *lift1 = nullptr;
@@ -473,6 +474,34 @@ hbpdc_status precond_apply_impl(hbpdc_ctx* c, const double* iw, const double* is
   return HBPDC_OK;
 }
 
+// Krylov basis capacity >= `need` vectors (restart 700 at C3 would pin 47 GB
+// up front; GMRES mostly converges far earlier).  Growth doubles, capped at
+// restart + 1, and copies the existing vectors (rare, synchronous).
+hbpdc_status ensure_krylov(hbpdc_ctx* c, size_t need) {
+  if (need <= c->vk_cap) return HBPDC_OK;
+  const size_t n2 = 2 * c->n;
+  size_t cap = std::max(need, 2 * c->vk_cap);
+  cap = std::min(cap, (size_t)c->restart + 1);
+  if (cap < need) cap = need;
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, cap * n2 * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    char buf[200];
+    snprintf(buf, sizeof buf, "Krylov basis of %zu vectors (%.1f GB) does not fit: %s", cap,
+             cap * n2 * 8.0 / 1e9, cudaGetErrorString(e));
+    return fail(c, HBPDC_E_OOM, buf);
+  }
+  if (c->Vk) {
+    CK(cudaMemcpyAsync(q, c->Vk, c->vk_cap * n2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(c->Vk);
+  }
+  c->Vk = (double*)q;
+  c->vk_cap = cap;
+  return HBPDC_OK;
+}
+
 // ---- GMRES (right preconditioned, CGS2 Arnoldi, restarted) ----------------------
 struct LinSys {
   double a1, a2, dt;
@@ -537,6 +566,7 @@ hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
     std::vector<double> a, bvec, t, hp, d;
     for (int j = 1; j <= R + 1; ++j) {
       const bool flush = flush_next || j == R + 1;
+      CKS(ensure_krylov(c, (size_t)j + 1));
       double* u = c->Vk + (size_t)(j - 1) * n2;   // u_j (once orthogonalised)
       double* w = c->Vk + (size_t)j * n2;
       if (!flush) {
@@ -826,7 +856,7 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
   CKS(dalloc(c, &c->rhs, n2));
   CKS(dalloc(c, &c->tmp2, n2));
   CKS(dalloc(c, &c->zb, n2));
-  CKS(dalloc(c, &c->Vk, (size_t)(R + 1) * n2));
+  CKS(ensure_krylov(c, std::min<size_t>((size_t)R + 1, 33)));
   CKS(dalloc(c, &c->partial, (size_t)(2 * R + 4) * std::max(arnoldi_dot_blocks(n2), RED_BLOCKS)));
   CKS(dalloc(c, &c->dh, 2 * (size_t)R + 4));
   CKS(dalloc(c, &c->dnrm, 1));
@@ -1207,6 +1237,7 @@ void hbpdc_finalize(hbpdc_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   prof_flush(c);
   for (void* p : c->allocs) cudaFree(p);
+  if (c->Vk) cudaFree(c->Vk);
   if (c->hpin) cudaFreeHost(c->hpin);
   delete c->comm;
   if (c->own_stream) cudaStreamDestroy(c->stream);

@@ -1,0 +1,198 @@
+"""Parity at BASELINE.json's FULL sizes, in the bench's launch configuration
+(the library's kernels on the whole C2 / C3 / C4 / C5 mesh), on sampled
+outputs the oracle computes one by one.
+
+R^(1), R^(2), the residual and the JVPs of an element depend only on the
+element and its face neighbours (radius 1; BR1 Navier-Stokes: radius 2
+through the neighbours' lifted gradients), and so does its BJ_ext block K_i.
+The oracle therefore evaluates each sampled element on a (2r+1)^2 periodic
+window of the global state cut around it (the window's own wrap-around only
+touches elements farther than r from the centre), and the centre element of
+the window is compared with the same element of the GPU's full-mesh result.
+Samples include the four corner elements (periodic wrap) and seeded random
+elements.  Inputs: the SURVEY 8(c4) perturbed states at full size.
+
+Tolerances as the small-size parity tests: 1e-11 relative (over all samples
+of an output); FD JVP within max(1e-11, 4 delta_FD) with the same eps_FD
+(computed from the global direction); S blocks within 1e-11 max(1, cond/1e4).
+"""
+import numpy as np
+import pytest
+
+from oracle import basis, dgsem, implicit, physics
+from paper_2109_04804_b200 import configs, hbpdc, inputs
+from gpu_common import rel, to_gpu, to_np, SEED
+
+pytestmark = pytest.mark.gpu
+
+
+def _window(x, nx, ny, m, ex, ey, r):
+    f = np.asarray(x).reshape(ny, nx, m)
+    iy = np.arange(ey - r, ey + r + 1) % ny
+    ix = np.arange(ex - r, ex + r + 1) % nx
+    return np.ascontiguousarray(f[np.ix_(iy, ix)]).reshape(-1)
+
+
+def _centre(x, w, m, r):
+    return np.asarray(x).reshape(w, w, m)[r, r]
+
+
+def _samples(nx, ny, k, seed):
+    rng = np.random.default_rng(seed)
+    s = [(0, 0), (nx - 1, 0), (0, ny - 1), (nx - 1, ny - 1)]
+    s += [(int(a), int(b)) for a, b in zip(rng.integers(0, nx, k), rng.integers(0, ny, k))]
+    return s
+
+
+def _state(case, d_coords, cfg):
+    W = inputs.initial_state(case, d_coords, noise=cfg.noise)
+    return inputs.perturbed_state(W, SEED + 500 + inputs.CASE_INDEX[case])
+
+
+@pytest.mark.parametrize("case", ["C2", "C3", "C4", "C5"])
+def test_fullsize_sampled_operators(case):
+    import torch
+    cfg = configs.CONFIGS[case]
+    ctx = hbpdc.context_for(cfg, restart=min(cfg.restart, 50))     # operators only: a small Krylov basis
+    r = 2 if cfg.equation == "navier_stokes" else 1
+    w = 2 * r + 1
+    nx, ny, m, n = cfg.nx, cfg.ny, cfg.m, cfg.n
+    coords = ctx.node_coords()
+    W = _state(case, coords, cfg)
+    eq = physics.Equation(cfg.equation, a=cfg.a, gamma=cfg.gamma, mu=cfg.mu, prandtl=cfg.prandtl)
+    B = basis.build_basis(cfg.N, "gll")
+    dx = (cfg.bounds[1] - cfg.bounds[0]) / nx
+    dy = (cfg.bounds[3] - cfg.bounds[2]) / ny
+    dwin = dgsem.Disc(B, dgsem.Mesh(2, w, w, 0.0, w * dx, 0.0, w * dy), eq)
+    # sigma = R1(W) (GPU, full mesh) x (1 + 1e-2 noise): the oracle sees the same sigma
+    Wg = to_gpu(W)
+    sig = to_np(ctx.rhs(Wg)) * (1 + 1e-2 * inputs.random_field(n, SEED + 601))
+    dW = inputs.random_field(n, SEED + 602, unit_norm=True)
+    ds = inputs.random_field(n, SEED + 603, unit_norm=True)
+    b = W * (1 + 1e-3 * inputs.random_field(n, SEED + 604))
+    a1, a2, dt = 1 / 6, 1 / 54, configs.cfl_dt(cfg, inputs.initial_state(case, coords))
+    sg, dWg, dsg, bg = (to_gpu(x) for x in (sig, dW, ds, b))
+    R1g = to_np(ctx.rhs(Wg))
+    R2g = to_np(ctx.rhs(Wg, sg))
+    G1g, G2g = (to_np(t) for t in ctx.residual(a1, a2, dt, bg, Wg, sg))
+    if cfg.equation == "advection":
+        J = {"linear": [to_np(t) for t in ctx.jvp(a1, a2, dt, Wg, sg, dWg, dsg, mode="linear")]}
+    else:
+        eps = implicit.fd_eps(dW)
+        J = {"exact": [to_np(t) for t in ctx.jvp(a1, a2, dt, Wg, sg, dWg, dsg, mode="exact")],
+             "fd": [to_np(t) for t in ctx.jvp(a1, a2, dt, Wg, sg, dWg, dsg, mode="fd",
+                                              eps_override=(eps, None))]}
+    torch.cuda.synchronize()
+    got = {k: [] for k in ["R1", "R2", "G", *J]}
+    ref = {k: [] for k in got}
+    fd_gap = []
+    for ex, ey in _samples(nx, ny, 6, SEED + 605):
+        win = lambda x: _window(x, nx, ny, m, ex, ey, r)      # noqa: E731
+        e = ey * nx + ex
+        own = lambda x: np.asarray(x)[e * m:(e + 1) * m]      # noqa: E731
+        Ww, sw, dWw, dsw, bw = (win(x) for x in (W, sig, dW, ds, b))
+        got["R1"].append(own(R1g))
+        ref["R1"].append(_centre(dgsem.rhs1(dwin, Ww), w, m, r))
+        got["R2"].append(own(R2g))
+        ref["R2"].append(_centre(dgsem.rhs2(dwin, Ww, sw), w, m, r))
+        G1o, G2o = implicit.residual(dwin, a1, a2, dt, bw, Ww, sw)
+        got["G"].append(np.concatenate([own(G1g), own(G2g)]))
+        ref["G"].append(np.concatenate([_centre(G1o, w, m, r), _centre(G2o, w, m, r)]))
+        for md, (t, bb) in J.items():
+            if md == "linear":
+                to, bo = implicit.jvp_linear(dwin, a1, a2, dt, dWw, dsw)
+            elif md == "exact":
+                to, bo = implicit.jvp_exact(dwin, a1, a2, dt, Ww, sw, dWw, dsw)
+            else:
+                to, bo = implicit.jvp_fd(dwin, a1, a2, dt, Ww, sw, dWw, dsw, eps_override=(eps, None))
+                te, be = implicit.jvp_exact(dwin, a1, a2, dt, Ww, sw, dWw, dsw)
+                fd_gap.append(rel(np.concatenate([_centre(to, w, m, r), _centre(bo, w, m, r)]),
+                                  np.concatenate([_centre(te, w, m, r), _centre(be, w, m, r)])))
+            got[md].append(np.concatenate([own(t), own(bb)]))
+            ref[md].append(np.concatenate([_centre(to, w, m, r), _centre(bo, w, m, r)]))
+    for k in got:
+        err = rel(np.concatenate(got[k]), np.concatenate(ref[k]))
+        tol = max(1e-11, 4 * max(fd_gap)) if k == "fd" else 1e-11
+        assert err <= tol, (case, k, err, tol)
+    ctx.close()
+
+
+@pytest.mark.parametrize("case", ["C3", "C5"])
+def test_fullsize_sampled_bjext(case):
+    """BJ_ext build over the whole C3 / C5 mesh (8.6 / 10.9 GB of S) and its
+    application; sampled S_i and sampled P^-1 X blocks against the oracle's
+    window blocks."""
+    import torch
+    cfg = configs.CONFIGS[case]
+    ctx = hbpdc.context_for(cfg, restart=min(cfg.restart, 50))     # operators only: a small Krylov basis
+    r = 2 if cfg.equation == "navier_stokes" else 1
+    w = 2 * r + 1
+    nx, ny, m, n = cfg.nx, cfg.ny, cfg.m, cfg.n
+    coords = ctx.node_coords()
+    W = _state(case, coords, cfg)
+    eq = physics.Equation(cfg.equation, a=cfg.a, gamma=cfg.gamma, mu=cfg.mu, prandtl=cfg.prandtl)
+    B = basis.build_basis(cfg.N, "gll")
+    dx = (cfg.bounds[1] - cfg.bounds[0]) / nx
+    dy = (cfg.bounds[3] - cfg.bounds[2]) / ny
+    dwin = dgsem.Disc(B, dgsem.Mesh(2, w, w, 0.0, w * dx, 0.0, w * dy), eq)
+    dt = configs.cfl_dt(cfg, inputs.initial_state(case, coords))
+    a1, a2 = 1.0, 1.0                      # the corrector pair
+    x = inputs.random_field(n, SEED + 611)
+    y = inputs.random_field(n, SEED + 612)
+    ctx.precond_build(a1, a2, dt, to_gpu(W))
+    tg, bg = (to_np(t) for t in ctx.precond_apply(to_gpu(x), to_gpu(y)))
+    S, _ = ctx.precond_export(shared_hint=False)
+    torch.cuda.synchronize()
+    gS, oS, gA, oA, conds = [], [], [], [], []
+    for ex, ey in _samples(nx, ny, 4, SEED + 613):
+        e = ey * nx + ex
+        Ww = _window(W, nx, ny, m, ex, ey, r)
+        c = (w * w) // 2
+        # K of the centre element only: dR1/dW columns with a one-hot seed in it
+        # (the oracle's colouring gives the same columns: other seeds add exact zeros)
+        K = np.zeros((w * w, m, m))
+        for col in range(m):
+            seed = np.zeros(w * w * m)
+            seed[c * m + col] = 1.0
+            K[c][:, col] = dgsem.rhs2(dwin, Ww, seed)[c * m:(c + 1) * m]
+        pc = implicit.BJExt(dwin, Ww, a1, a2, dt, K=K)
+        gS.append(to_np(S[e * m * m:(e + 1) * m * m]))
+        oS.append(pc.S[c].reshape(-1))
+        conds.append(np.linalg.cond(pc.M[c]))
+        to, bo = pc.apply(_window(x, nx, ny, m, ex, ey, r), _window(y, nx, ny, m, ex, ey, r))
+        gA.append(np.concatenate([tg[e * m:(e + 1) * m], bg[e * m:(e + 1) * m]]))
+        oA.append(np.concatenate([_centre(to, w, m, r), _centre(bo, w, m, r)]))
+    tol = 1e-11 * max(1.0, max(conds) / 1e4)
+    assert rel(np.concatenate(gS), np.concatenate(oS)) <= tol
+    assert rel(np.concatenate(gA), np.concatenate(oA)) <= tol
+    ctx.close()
+
+
+def test_c3_fullsize_step_invariants():
+    """One full C3 HBPC(8,4) step (the bench's step): discrete conservation of
+    mass, momentum and energy to the solver tolerance (reading R27), and the
+    FSAL sigma-consistency of the step output."""
+    import torch
+    cfg = configs.CONFIGS["C3"]
+    ctx = hbpdc.context_for(cfg)
+    coords = ctx.node_coords()
+    W0 = inputs.initial_state("C3", coords, noise=cfg.noise)
+    dt = configs.cfl_dt(cfg, inputs.initial_state("C3", coords))
+    Wg = to_gpu(W0)
+    st = ctx.step(dt, Wg)
+    torch.cuda.synchronize()
+    W1 = to_np(Wg)
+    B = basis.build_basis(cfg.N, "gll")
+    wq = np.outer(B.w, B.w).reshape(-1)            # [j][i] node weights
+    h = (cfg.bounds[1] - cfg.bounds[0]) / cfg.nx
+    J = h * h / 4
+    f0 = W0.reshape(cfg.n_elem, 4, -1)
+    f1 = W1.reshape(cfg.n_elem, 4, -1)
+    for v in range(4):
+        m0 = J * np.sum(f0[:, v] * wq)
+        m1 = J * np.sum(f1[:, v] * wq)
+        scale = J * np.sum(np.abs(f0[:, v]) * wq)
+        assert abs(m1 - m0) <= 1e-9 * scale, (v, m1 - m0, scale)
+    assert st["stage_solves"] == 15
+    assert np.all(np.isfinite(W1))
+    ctx.close()
