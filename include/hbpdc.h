@@ -90,6 +90,10 @@ typedef struct {
   int precond;                 /* HBPDC_PC_NONE | HBPDC_PC_BJEXT          */
   int precond_policy;          /* HBPDC_PC_PER_STEP_PER_ALPHA (default) | PER_NEWTON */
   int jvp_mode;                /* HBPDC_JVP_AUTO: linear (advection) / FD otherwise  */
+  int batch_stages;            /* 1: solve the s-1 corrector stages of a sweep in lock
+                                  step, sharing one BJ_ext S pass per Arnoldi step
+                                  (they are independent, eq:corrector P:119-122;
+                                  SURVEY NEXT-1).  Bitwise equal results to 0.      */
 } hbpdc_solver_opts;
 
 /* Element partition (the mesh is decomposed, W and sigma share the

@@ -68,6 +68,20 @@ struct DevBuf {
 
 }  // namespace
 
+// Newton / GMRES workspace of one stage system (NEXT-1 solves the s-1
+// corrector stages of a sweep in lock step, one workspace each)
+struct SysWS {
+  double *X = nullptr, *G = nullptr, *dX = nullptr, *rhs = nullptr, *r = nullptr, *zb = nullptr;
+  double *b = nullptr;                      // Newton right-hand side b (n)
+  double *U = nullptr, *V = nullptr;        // BJ_ext GEMV outputs (n each)
+  double *Vk = nullptr;                     // Krylov basis: vk_cap x 2n, grown on demand up to restart+1
+  size_t vk_cap = 0;
+  double *partial = nullptr, *dh = nullptr, *dy = nullptr, *dnrm = nullptr;
+  double *gW = nullptr, *gS = nullptr;      // ghosts of its linearisation point (halo)
+  double* hpin = nullptr;                   // pinned host scratch
+  std::vector<double> H, Hraw, cs, sn, gv, y;
+};
+
 struct hbpdc_ctx {
   hbpdc_problem pb{};
   hbpdc_solver_opts op{};
@@ -85,25 +99,21 @@ struct hbpdc_ctx {
   int restart = 0;
   // device memory
   std::vector<void*> allocs;
-  double *X = nullptr, *G = nullptr, *dX = nullptr, *rhs = nullptr, *tmp2 = nullptr, *zb = nullptr;
-  double *Vk = nullptr;        // Krylov basis: vk_cap x 2n, grown on demand up to restart+1
-  size_t vk_cap = 0;
-  double *partial = nullptr;   // (restart+2) x RED_BLOCKS
-  double *dh = nullptr, *dnrm = nullptr, *deps = nullptr, *dy = nullptr;
+  std::vector<SysWS> sys;      // Newton/GMRES workspaces: [0] always, s-1 of them for batched correctors
+  double *partial = nullptr;   // RED_BLOCKS partial sums (norms)
+  double *dnrm = nullptr, *deps = nullptr;
   double *lift0 = nullptr, *lift1 = nullptr;
   // precond
-  double *S = nullptr, *Wb = nullptr, *U = nullptr, *Vv = nullptr, *Z = nullptr;
+  double *S = nullptr, *Wb = nullptr, *Z = nullptr;
   double *Kst = nullptr, *KV = nullptr, *KT = nullptr, *tseed = nullptr, *y1 = nullptr, *y2 = nullptr;  // NS
   int* info = nullptr;
   int s_shared = 0, pc_valid = 0, zchunk = 0;
   double pc_a1 = 0, pc_a2 = 0, pc_dt = -1;
   // stage store: [sweep(2)][s] of w, R1, R2
   double *stw[2][4] = {}, *str1[2][4] = {}, *str2[2][4] = {};
-  double *Wn = nullptr, *bvec = nullptr, *Wio = nullptr;
+  double *Wn = nullptr, *Wio = nullptr;
   int fsal_valid = 0;
-  // host scratch
-  std::vector<double> H, Hraw, cs, sn, gv, y, hh;
-  double* hpin = nullptr;      // pinned host scratch
+  double* hpin = nullptr;      // pinned host scratch (norms)
   // profiling
   int prof_on = 0;
   std::vector<cudaEvent_t> ev_pool;
@@ -346,8 +356,10 @@ hbpdc_status ensure_precond_mem(hbpdc_ctx* c) {
   const size_t nblk = c->s_shared ? 1 : (size_t)c->nE;
   CKS(dalloc(c, &c->S, nblk * mm));
   CKS(dalloc(c, &c->Wb, c->n));
-  CKS(dalloc(c, &c->U, c->n));
-  CKS(dalloc(c, &c->Vv, c->n));
+  for (auto& w : c->sys) {
+    CKS(dalloc(c, &w.U, c->n));
+    CKS(dalloc(c, &w.V, c->n));
+  }
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {   // explicit K_i (two-hop BR1 path) + colouring scratch
     CKS(dalloc(c, &c->Kst, nblk * mm));
     CKS(dalloc(c, &c->KV, c->n));
@@ -444,43 +456,64 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
   return HBPDC_OK;
 }
 
-hbpdc_status precond_apply_impl(hbpdc_ctx* c, const double* iw, const double* is, double* ow, double* os) {
+// P^-1 X for B systems at once: u_i = S W_i, v_i = S sigma_i for
+// all i in ONE streaming pass over S (B > 1: the lock-step corrector stages,
+// NEXT-1), then per system top = u - c2 K v, bottom = v + K (u - a1dt v).
+hbpdc_status precond_apply_multi(hbpdc_ctx* c, int B, const double* const* iw, const double* const* is,
+                                 double* const* ow, double* const* os) {
   if (!c->pc_valid) return fail(c, HBPDC_E_ARG, "precond_apply before precond_build");
   {
-    ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 4.0 * c->n * 8.0);
-    CK(launch_block_gemv2(c->S, c->s_shared, iw, is, c->U, c->Vv, c->m, c->nE, c->stream));
+    ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 4.0 * B * c->n * 8.0);
+    if (B == 1 || c->s_shared) {
+      for (int i = 0; i < B; ++i)
+        CK(launch_block_gemv2(c->S, c->s_shared, iw[i], is[i], c->sys[i].U, c->sys[i].V, c->m, c->nE, c->stream));
+    } else {
+      const double* in[GEMV_MAX_RHS];
+      double* out[GEMV_MAX_RHS];
+      for (int i = 0; i < B; ++i) {
+        in[2 * i] = iw[i]; in[2 * i + 1] = is[i];
+        out[2 * i] = c->sys[i].U; out[2 * i + 1] = c->sys[i].V;
+      }
+      CK(launch_block_gemv_multi(c->S, 2 * B, in, out, c->m, c->nE, c->stream));
+    }
     CKS(dbg_sync(c, "BJ_ext GEMV"));
   }
   const double a1dt = c->pc_a1 * c->pc_dt, c2 = c->pc_a2 * c->pc_dt * c->pc_dt / 2.0;
-  if (c->pb.equation == HBPDC_NAVIER_STOKES) {
-    // explicit K_i: (K V, K (U - a1dt V)) in one 2-RHS pass over the stored blocks
-    ProfScope ps(c, 5, (double)c->nE * c->m * c->m * 8.0 + 8.0 * c->n * 8.0);
-    CK(launch_waxpby(1.0, c->U, -a1dt, c->Vv, c->y1, c->n, c->stream));
-    CK(launch_block_gemv2(c->Kst, 0, c->Vv, c->y1, c->KV, c->KT, c->m, c->nE, c->stream));
-    CK(launch_waxpby(1.0, c->U, -c2, c->KV, ow, c->n, c->stream));
-    CK(launch_waxpby(1.0, c->Vv, 1.0, c->KT, os, c->n, c->stream));
+  for (int i = 0; i < B; ++i) {
+    const double *U = c->sys[i].U, *V = c->sys[i].V;
+    if (c->pb.equation == HBPDC_NAVIER_STOKES) {
+      // explicit K_i: (K V, K (U - a1dt V)) in one 2-RHS pass over the stored blocks
+      ProfScope ps(c, 5, (double)c->nE * c->m * c->m * 8.0 + 8.0 * c->n * 8.0);
+      CK(launch_waxpby(1.0, U, -a1dt, V, c->y1, c->n, c->stream));
+      CK(launch_block_gemv2(c->Kst, 0, V, c->y1, c->KV, c->KT, c->m, c->nE, c->stream));
+      CK(launch_waxpby(1.0, U, -c2, c->KV, ow[i], c->n, c->stream));
+      CK(launch_waxpby(1.0, V, 1.0, c->KT, os[i], c->n, c->stream));
+    } else {
+      OpArgs A = base_args(c);
+      A.W = c->Wb; A.U = U; A.V = V; A.out1 = ow[i]; A.out2 = os[i];
+      A.a1dt = a1dt;
+      A.c2 = c2;
+      A.gW = c->halo() ? c->gWb : c->Wb;
+      ProfScope ps(c, 5, 5.0 * c->n * 8.0);
+      CK(launch_op(OP_KAPPLY, c->cfg, c->geo, A));
+      CKS(dbg_sync(c, "BJ_ext K apply"));
+    }
     if (c->st) c->st->precond_applies++;
-    return HBPDC_OK;
   }
-  OpArgs A = base_args(c);
-  A.W = c->Wb; A.U = c->U; A.V = c->Vv; A.out1 = ow; A.out2 = os;
-  A.a1dt = a1dt;
-  A.c2 = c2;
-  A.gW = c->halo() ? c->gWb : c->Wb;
-  ProfScope ps(c, 5, 5.0 * c->n * 8.0);
-  CK(launch_op(OP_KAPPLY, c->cfg, c->geo, A));
-  CKS(dbg_sync(c, "BJ_ext K apply"));
-  if (c->st) c->st->precond_applies++;
   return HBPDC_OK;
+}
+
+hbpdc_status precond_apply_impl(hbpdc_ctx* c, const double* iw, const double* is, double* ow, double* os) {
+  return precond_apply_multi(c, 1, &iw, &is, &ow, &os);
 }
 
 // Krylov basis capacity >= `need` vectors (restart 700 at C3 would pin 47 GB
 // up front; GMRES mostly converges far earlier).  Growth doubles, capped at
 // restart + 1, and copies the existing vectors (rare, synchronous).
-hbpdc_status ensure_krylov(hbpdc_ctx* c, size_t need) {
-  if (need <= c->vk_cap) return HBPDC_OK;
+hbpdc_status ensure_krylov(hbpdc_ctx* c, SysWS& w, size_t need) {
+  if (need <= w.vk_cap) return HBPDC_OK;
   const size_t n2 = 2 * c->n;
-  size_t cap = std::max(need, 2 * c->vk_cap);
+  size_t cap = std::max(need, 2 * w.vk_cap);
   cap = std::min(cap, (size_t)c->restart + 1);
   if (cap < need) cap = need;
   void* q = nullptr;
@@ -492,17 +525,24 @@ hbpdc_status ensure_krylov(hbpdc_ctx* c, size_t need) {
              cap * n2 * 8.0 / 1e9, cudaGetErrorString(e));
     return fail(c, HBPDC_E_OOM, buf);
   }
-  if (c->Vk) {
-    CK(cudaMemcpyAsync(q, c->Vk, c->vk_cap * n2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (w.Vk) {
+    CK(cudaMemcpyAsync(q, w.Vk, w.vk_cap * n2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    cudaFree(c->Vk);
+    cudaFree(w.Vk);
   }
-  c->Vk = (double*)q;
-  c->vk_cap = cap;
+  w.Vk = (double*)q;
+  w.vk_cap = cap;
   return HBPDC_OK;
 }
 
-// ---- GMRES (right preconditioned, CGS2 Arnoldi, restarted) ----------------------
+// the ghost buffers of (W, sigma) belong to the system being linearised
+void use_ghosts(hbpdc_ctx* c, SysWS& w) {
+  if (c->halo()) { c->gW = w.gW; c->gS = w.gS; }
+}
+
+// ---- GMRES (right preconditioned, DCGS2 Arnoldi, restarted) ----------------------
+// One GMRES solve is a resumable state (GState), so that several independent
+// systems can be advanced in lock step and share the BJ_ext S pass (NEXT-1).
 struct LinSys {
   double a1, a2, dt;
   const double* W;     // linearisation point
@@ -510,244 +550,341 @@ struct LinSys {
   bool pc;
 };
 
-hbpdc_status apply_JPinv(hbpdc_ctx* c, const LinSys& L, const double* v, double* out, bool use_pc) {
-  const size_t n = c->n;
-  const double* z = v;
-  if (use_pc) {
-    CKS(precond_apply_impl(c, v, v + n, c->zb, c->zb + n));
-    z = c->zb;
+struct GState {
+  SysWS* w = nullptr;
+  LinSys L{};
+  double beta0 = 0, beta = 0;
+  int total = 0;
+  bool converged = false, done = false;
+  // current restart cycle
+  bool in_cycle = false, flush_next = false, est_ok = false;
+  int j = 0, k = 0;
+  std::vector<double> a, bvec, t, hp, d;
+  bool needs_op() const { return in_cycle && !flush_next && j != 0; }
+};
+
+hbpdc_status g_start(hbpdc_ctx* c, GState& g) {
+  SysWS& w = *g.w;
+  const size_t n2 = 2 * c->n;
+  CK(cudaMemsetAsync(w.dX, 0, n2 * sizeof(double), c->stream));
+  CKS(norm_host(c, w.rhs, n2, &g.beta0));
+  g.total = 0;
+  g.in_cycle = false;
+  g.converged = g.done = false;
+  if (!(g.beta0 > 0.0)) {
+    if (g.beta0 == 0.0) { g.converged = g.done = true; return HBPDC_OK; }
+    return fail(c, HBPDC_E_NONFINITE, "GMRES rhs not finite");
   }
-  return jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr, true);
+  CK(cudaMemcpyAsync(w.r, w.rhs, n2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));   // x0 = 0
+  g.beta = g.beta0;
+  return HBPDC_OK;
 }
 
-// solve J x = rhs (rhs in c->rhs, x -> c->dX); returns iterations
-hbpdc_status gmres(hbpdc_ctx* c, const LinSys& L, int* its_out) {
+// start a restart cycle (or finish: converged / iteration cap)
+hbpdc_status g_cycle_begin(hbpdc_ctx* c, GState& g) {
+  SysWS& w = *g.w;
   const size_t n2 = 2 * c->n;
+  if (g.beta <= c->op.gmres_rtol * g.beta0) { g.converged = g.done = true; return HBPDC_OK; }
+  if (g.total >= c->op.krylov_max_per_newton) { g.done = true; return HBPDC_OK; }
+  // V0 = r / beta
+  w.hpin[0] = g.beta;
+  CK(cudaMemcpyAsync(w.dnrm, w.hpin, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(launch_scale_by_inv(w.r, w.dnrm, w.Vk, n2, c->stream));
+  std::fill(w.H.begin(), w.H.end(), 0.0);
+  std::fill(w.Hraw.begin(), w.Hraw.end(), 0.0);
+  std::fill(w.gv.begin(), w.gv.end(), 0.0);
+  w.gv[0] = g.beta;
+  g.in_cycle = true;
+  g.flush_next = false;
+  g.est_ok = false;
+  g.j = 1;
+  g.k = 0;
+  return HBPDC_OK;
+}
+
+// end of a restart cycle: y = H^-1 g, x += P^-1 (V y); true residual unless converged
+hbpdc_status g_cycle_end(hbpdc_ctx* c, GState& g) {
+  SysWS& w = *g.w;
+  const size_t n = c->n, n2 = 2 * n;
+  const int R = c->restart;
+  const int k = g.k;
+  for (int i = k - 1; i >= 0; --i) {
+    double sum = w.gv[i];
+    for (int l = i + 1; l < k; ++l) sum -= w.H[(size_t)l * (R + 1) + i] * w.y[l];
+    w.y[i] = sum / w.H[(size_t)i * (R + 1) + i];
+  }
+  // the pinned buffer may still feed an earlier async upload: wait for the stream
+  CK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < k; ++i) w.hpin[i] = w.y[i];
+  CK(cudaMemcpyAsync(w.dy, w.hpin, k * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(launch_lincomb(w.Vk, n2, k, w.dy, w.r, n2, c->stream));
+  if (g.L.pc) {
+    CKS(precond_apply_impl(c, w.r, w.r + n, w.zb, w.zb + n));
+    CK(launch_axpby(1.0, w.zb, 1.0, w.dX, n2, c->stream));
+  } else {
+    CK(launch_axpby(1.0, w.r, 1.0, w.dX, n2, c->stream));
+  }
+  g.in_cycle = false;
+  if (g.est_ok) { g.converged = g.done = true; return HBPDC_OK; }
+  // true residual r = rhs - J x
+  use_ghosts(c, w);
+  CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, w.dX, w.dX + n, w.r, w.r + n, c->op.jvp_mode, nullptr,
+               true));
+  CK(launch_axpby(1.0, w.rhs, -1.0, w.r, n2, c->stream));
+  CKS(norm_host(c, w.r, n2, &g.beta));
+  return HBPDC_OK;
+}
+
+// Arnoldi step j of the cycle (DCGS2, Swirydowicz et al. 2020 / Bielich et al.
+// 2022; the oracle uses MGS).  z = P^-1 u_j was computed by the caller (NULL on
+// a flush step, which only finalises the lagged column).  One reduction gives
+// the lagged reorthogonalisation of u_j and the projections of w = J z; one
+// update pass writes q_j and u_{j+1}.  Column j-1 of the Hessenberg matrix
+// becomes final (and its Givens rotation applied) one iteration later.
+hbpdc_status g_iter(hbpdc_ctx* c, GState& g, const double* z) {
+  SysWS& w = *g.w;
+  const size_t n = c->n, n2 = 2 * n;
   const int R = c->restart;
   const double rtol = c->op.gmres_rtol;
-  const int maxit = c->op.krylov_max_per_newton;
-  CK(cudaMemsetAsync(c->dX, 0, n2 * sizeof(double), c->stream));
-  double beta0;
-  CKS(norm_host(c, c->rhs, n2, &beta0));
-  *its_out = 0;
-  if (!(beta0 > 0.0)) return beta0 == 0.0 ? HBPDC_OK : fail(c, HBPDC_E_NONFINITE, "GMRES rhs not finite");
-  // r = rhs (x0 = 0)
-  double* r = c->tmp2;
-  CK(cudaMemcpyAsync(r, c->rhs, n2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  double beta = beta0;
-  int total = 0;
-  bool converged = false;
-  std::vector<double>& H = c->H;
-  while (true) {
-    if (beta <= rtol * beta0) { converged = true; break; }
-    if (total >= maxit) break;
-    // V0 = r / beta
-    c->hpin[0] = beta;
-    CK(cudaMemcpyAsync(c->dnrm, c->hpin, sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(launch_scale_by_inv(r, c->dnrm, c->Vk, n2, c->stream));
-    std::fill(H.begin(), H.end(), 0.0);
-    std::fill(c->Hraw.begin(), c->Hraw.end(), 0.0);
-    std::fill(c->gv.begin(), c->gv.end(), 0.0);
-    c->gv[0] = beta;
-    // Arnoldi with delayed classical Gram-Schmidt reorthogonalisation (DCGS2,
-    // Swirydowicz et al. 2020 / Bielich et al. 2022; the oracle uses MGS):
-    // iteration j applies the operator to the once-orthogonalised u_j, and ONE
-    // reduction gives both the lagged reorthogonalisation of u_j and the
-    // projections of w = B u_j; ONE update pass writes q_j and u_{j+1}.
-    // Column j-1 of the Hessenberg matrix becomes final (and its Givens
-    // rotation applied) one iteration later.
-    std::vector<double>& Hr = c->Hraw;          // unrotated Hessenberg, column-major (R+1) x R
-    auto HR = [&](int row, int col) -> double& { return Hr[(size_t)col * (R + 1) + row]; };
-    auto HQ = [&](int row, int col) -> double& { return H[(size_t)col * (R + 1) + row]; };
-    int k = 0;                                   // finalized columns
-    bool flush_next = false;
-    bool est_ok = false;
-    const int nb = arnoldi_dot_blocks(n2);
-    std::vector<double> a, bvec, t, hp, d;
-    for (int j = 1; j <= R + 1; ++j) {
-      const bool flush = flush_next || j == R + 1;
-      CKS(ensure_krylov(c, (size_t)j + 1));
-      double* u = c->Vk + (size_t)(j - 1) * n2;   // u_j (once orthogonalised)
-      double* w = c->Vk + (size_t)j * n2;
-      if (!flush) {
-        CKS(apply_JPinv(c, L, u, w, L.pc));
-        ++total;
-      }
-      const int nk = j - 1;
-      {
-        ProfScope ps(c, 3, (double)(nk + (flush ? 1 : 2)) * n2 * 8.0);
-        CK(launch_dcgs2_dots(c->Vk, n2, nk, u, flush ? nullptr : w, n2, c->partial, c->stream));
-        CK(launch_reduce_partials_n(c->partial, 2 * nk + 3, nb, c->dh, c->stream));
-        CKS(allreduce(c, c->dh, 2 * nk + 3));
-      }
-      CK(cudaMemcpyAsync(c->hpin, c->dh, (2 * nk + 3) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      a.assign(nk, 0.0);
-      bvec.assign(nk, 0.0);
-      double sa = 0.0, ab = 0.0;
-      for (int q = 0; q < nk; ++q) {
-        a[q] = c->hpin[2 * q];
-        bvec[q] = c->hpin[2 * q + 1];
-        sa += a[q] * a[q];
-        ab += a[q] * bvec[q];
-      }
-      const double uu = c->hpin[2 * nk], uw = c->hpin[2 * nk + 1];
-      double b2 = uu - sa;
-      bool explicit_q = false;
-      if (nk > 0 && !(b2 >= 0.25 * uu)) {
-        // severe cancellation in the lagged step: form q_j explicitly
-        for (int q = 0; q < nk; ++q) c->hpin[q] = a[q];
-        CK(cudaMemcpyAsync(c->dy, c->hpin, nk * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CK(launch_arnoldi_axpy(c->Vk, n2, nk, c->dy, u, n2, c->partial, c->stream));
-        if (c->comm) {
-          CK(launch_reduce_partials_n(c->partial, 1, nb, c->dnrm, c->stream));
-          CKS(allreduce(c, c->dnrm, 1));
-          CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-          CK(cudaStreamSynchronize(c->stream));
-          b2 = c->hpin[0];
-        } else {
-          CK(launch_finish_sqrt(c->partial, nb, c->dnrm, c->stream));
-          CK(cudaMemcpyAsync(c->hpin, c->dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-          CK(cudaStreamSynchronize(c->stream));
-          b2 = c->hpin[0] * c->hpin[0];
-        }
-        explicit_q = true;
-      }
-      const double bu = std::sqrt(std::max(b2, 0.0));
-      if (!std::isfinite(bu)) return fail(c, HBPDC_E_NONFINITE, "non-finite Arnoldi norm");
-      if (j >= 2) {
-        // finalize column j-2: lagged correction + subdiagonal, then Givens
-        const int col = j - 2;
-        for (int q = 0; q < nk; ++q) HR(q, col) += a[q];
-        HR(j - 1, col) = bu;
-        for (int q = 0; q <= j - 1; ++q) HQ(q, col) = HR(q, col);
-        for (int i = 0; i < col; ++i) {
-          const double tt = c->cs[i] * HQ(i, col) + c->sn[i] * HQ(i + 1, col);
-          HQ(i + 1, col) = -c->sn[i] * HQ(i, col) + c->cs[i] * HQ(i + 1, col);
-          HQ(i, col) = tt;
-        }
-        const double den = std::hypot(HQ(col, col), HQ(col + 1, col));
-        c->cs[col] = HQ(col, col) / den;
-        c->sn[col] = HQ(col + 1, col) / den;
-        HQ(col, col) = den;
-        HQ(col + 1, col) = 0.0;
-        c->gv[col + 1] = -c->sn[col] * c->gv[col];
-        c->gv[col] = c->cs[col] * c->gv[col];
-        k = col + 1;
-        if (c->st && k > c->st->max_krylov_j) c->st->max_krylov_j = k;
-        if (std::fabs(c->gv[k]) <= rtol * beta0) { est_ok = true; break; }
-      }
-      if (flush || bu == 0.0) break;
-      // first-pass projections of B q_j onto Q_j (provisional column j-1)
-      t.assign(j, 0.0);
-      for (int col = 0; col < nk; ++col)
-        for (int i = 0; i <= col + 1 && i < j; ++i) t[i] += HR(i, col) * a[col];
-      hp.assign(j, 0.0);
-      for (int i = 0; i < nk; ++i) hp[i] = (bvec[i] - t[i]) / bu;
-      const double qw = (uw - ab) / bu;
-      hp[j - 1] = (qw - t[j - 1]) / bu;
-      for (int i = 0; i < j; ++i) HR(i, j - 1) = hp[i];
-      const double cj = t[j - 1] / bu + hp[j - 1];
-      d.assign(nk, 0.0);
-      for (int q = 0; q < nk; ++q) d[q] = t[q] / bu + hp[q] - (explicit_q ? 0.0 : a[q] * cj / bu);
-      for (int q = 0; q < nk; ++q) {
-        c->hpin[q] = explicit_q ? 0.0 : a[q];
-        c->hpin[(R + 1) + q] = d[q];
-      }
-      CK(cudaMemcpyAsync(c->dy, c->hpin, nk * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      CK(cudaMemcpyAsync(c->dy + (R + 1), c->hpin + (R + 1), nk * sizeof(double), cudaMemcpyHostToDevice,
-                         c->stream));
-      {
-        ProfScope ps(c, 4, (double)(nk + 4) * n2 * 8.0);
-        CK(launch_dcgs2_update(c->Vk, n2, nk, c->dy, c->dy + (R + 1), u, w, 1.0 / bu, cj / bu, n2, c->stream));
-      }
-      if (total >= maxit) flush_next = true;
-    }
-    // y = H^-1 g (back substitution), x += P^-1 (V y)
-    for (int i = k - 1; i >= 0; --i) {
-      double s = c->gv[i];
-      for (int l = i + 1; l < k; ++l) s -= H[(size_t)l * (R + 1) + i] * c->y[l];
-      c->y[i] = s / H[(size_t)i * (R + 1) + i];
-    }
-    for (int i = 0; i < k; ++i) c->hpin[i] = c->y[i];
-    CK(cudaMemcpyAsync(c->dy, c->hpin, k * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(launch_lincomb(c->Vk, n2, k, c->dy, r, n2, c->stream));
-    if (L.pc) {
-      CKS(precond_apply_impl(c, r, r + c->n, c->zb, c->zb + c->n));
-      CK(launch_axpby(1.0, c->zb, 1.0, c->dX, n2, c->stream));
-    } else {
-      CK(launch_axpby(1.0, r, 1.0, c->dX, n2, c->stream));
-    }
-    if (est_ok) { converged = true; break; }
-    // true residual r = rhs - J x
-    CKS(jvp_impl(c, L.a1, L.a2, L.dt, L.W, L.sg, c->dX, c->dX + c->n, r, r + c->n, c->op.jvp_mode, nullptr, true));
-    CK(launch_axpby(1.0, c->rhs, -1.0, r, n2, c->stream));
-    CKS(norm_host(c, r, n2, &beta));
+  const int j = g.j;
+  const bool flush = g.flush_next || j == R + 1;
+  CKS(ensure_krylov(c, w, (size_t)j + 1));
+  double* u = w.Vk + (size_t)(j - 1) * n2;   // u_j (once orthogonalised)
+  double* wv = w.Vk + (size_t)j * n2;
+  if (!flush) {
+    use_ghosts(c, w);
+    CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, wv, wv + n, c->op.jvp_mode, nullptr, true));
+    ++g.total;
   }
-  *its_out = total;
-  if (c->st) c->st->gmres_its += total;
-  if (!converged) {
-    char buf[128];
-    snprintf(buf, sizeof buf, "GMRES did not converge within %d iterations", maxit);
-    return fail(c, HBPDC_E_GMRES, buf);
+  const int nk = j - 1;
+  const int nb = arnoldi_dot_blocks(n2);
+  {
+    ProfScope ps(c, 3, (double)(nk + (flush ? 1 : 2)) * n2 * 8.0);
+    CK(launch_dcgs2_dots(w.Vk, n2, nk, u, flush ? nullptr : wv, n2, w.partial, c->stream));
+    CK(launch_reduce_partials_n(w.partial, 2 * nk + 3, nb, w.dh, c->stream));
+    CKS(allreduce(c, w.dh, 2 * nk + 3));
+  }
+  CK(cudaMemcpyAsync(w.hpin, w.dh, (2 * nk + 3) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  auto HR = [&](int row, int col) -> double& { return w.Hraw[(size_t)col * (R + 1) + row]; };
+  auto HQ = [&](int row, int col) -> double& { return w.H[(size_t)col * (R + 1) + row]; };
+  std::vector<double>&a = g.a, &bv = g.bvec, &t = g.t, &hp = g.hp, &d = g.d;
+  a.assign(nk, 0.0);
+  bv.assign(nk, 0.0);
+  double sa = 0.0, ab = 0.0;
+  for (int q = 0; q < nk; ++q) {
+    a[q] = w.hpin[2 * q];
+    bv[q] = w.hpin[2 * q + 1];
+    sa += a[q] * a[q];
+    ab += a[q] * bv[q];
+  }
+  const double uu = w.hpin[2 * nk], uw = w.hpin[2 * nk + 1];
+  double b2 = uu - sa;
+  bool explicit_q = false;
+  if (nk > 0 && !(b2 >= 0.25 * uu)) {
+    // severe cancellation in the lagged step: form q_j explicitly
+    for (int q = 0; q < nk; ++q) w.hpin[q] = a[q];
+    CK(cudaMemcpyAsync(w.dy, w.hpin, nk * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(launch_arnoldi_axpy(w.Vk, n2, nk, w.dy, u, n2, w.partial, c->stream));
+    if (c->comm) {
+      CK(launch_reduce_partials_n(w.partial, 1, nb, w.dnrm, c->stream));
+      CKS(allreduce(c, w.dnrm, 1));
+      CK(cudaMemcpyAsync(w.hpin, w.dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      b2 = w.hpin[0];
+    } else {
+      CK(launch_finish_sqrt(w.partial, nb, w.dnrm, c->stream));
+      CK(cudaMemcpyAsync(w.hpin, w.dnrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      b2 = w.hpin[0] * w.hpin[0];
+    }
+    explicit_q = true;
+  }
+  const double bu = std::sqrt(std::max(b2, 0.0));
+  if (!std::isfinite(bu)) return fail(c, HBPDC_E_NONFINITE, "non-finite Arnoldi norm");
+  if (j >= 2) {
+    // finalize column j-2: lagged correction + subdiagonal, then Givens
+    const int col = j - 2;
+    for (int q = 0; q < nk; ++q) HR(q, col) += a[q];
+    HR(j - 1, col) = bu;
+    for (int q = 0; q <= j - 1; ++q) HQ(q, col) = HR(q, col);
+    for (int i = 0; i < col; ++i) {
+      const double tt = w.cs[i] * HQ(i, col) + w.sn[i] * HQ(i + 1, col);
+      HQ(i + 1, col) = -w.sn[i] * HQ(i, col) + w.cs[i] * HQ(i + 1, col);
+      HQ(i, col) = tt;
+    }
+    const double den = std::hypot(HQ(col, col), HQ(col + 1, col));
+    w.cs[col] = HQ(col, col) / den;
+    w.sn[col] = HQ(col + 1, col) / den;
+    HQ(col, col) = den;
+    HQ(col + 1, col) = 0.0;
+    w.gv[col + 1] = -w.sn[col] * w.gv[col];
+    w.gv[col] = w.cs[col] * w.gv[col];
+    g.k = col + 1;
+    if (c->st && g.k > c->st->max_krylov_j) c->st->max_krylov_j = g.k;
+    if (std::fabs(w.gv[g.k]) <= rtol * g.beta0) {
+      g.est_ok = true;
+      return g_cycle_end(c, g);
+    }
+  }
+  if (flush || bu == 0.0) return g_cycle_end(c, g);
+  // first-pass projections of B q_j onto Q_j (provisional column j-1)
+  t.assign(j, 0.0);
+  for (int col = 0; col < nk; ++col)
+    for (int i = 0; i <= col + 1 && i < j; ++i) t[i] += HR(i, col) * a[col];
+  hp.assign(j, 0.0);
+  for (int i = 0; i < nk; ++i) hp[i] = (bv[i] - t[i]) / bu;
+  const double qw = (uw - ab) / bu;
+  hp[j - 1] = (qw - t[j - 1]) / bu;
+  for (int i = 0; i < j; ++i) HR(i, j - 1) = hp[i];
+  const double cj = t[j - 1] / bu + hp[j - 1];
+  d.assign(nk, 0.0);
+  for (int q = 0; q < nk; ++q) d[q] = t[q] / bu + hp[q] - (explicit_q ? 0.0 : a[q] * cj / bu);
+  for (int q = 0; q < nk; ++q) {
+    w.hpin[q] = explicit_q ? 0.0 : a[q];
+    w.hpin[(R + 1) + q] = d[q];
+  }
+  CK(cudaMemcpyAsync(w.dy, w.hpin, nk * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(w.dy + (R + 1), w.hpin + (R + 1), nk * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  {
+    ProfScope ps(c, 4, (double)(nk + 4) * n2 * 8.0);
+    CK(launch_dcgs2_update(w.Vk, n2, nk, w.dy, w.dy + (R + 1), u, wv, 1.0 / bu, cj / bu, n2, c->stream));
+  }
+  g.j = j + 1;
+  if (g.total >= c->op.krylov_max_per_newton) g.flush_next = true;
+  return HBPDC_OK;
+}
+
+// Solve J x_i = rhs_i (rhs in w.rhs, x -> w.dX) for B systems in lock step:
+// every Arnoldi step preconditions all systems that need an operator
+// application with ONE pass over S (precond_apply_multi), the JVPs and
+// Arnoldi passes run per system.  B = 1 is the plain restarted GMRES.
+hbpdc_status gmres_batch(hbpdc_ctx* c, GState* gs, int B) {
+  const size_t n = c->n;
+  for (int i = 0; i < B; ++i) CKS(g_start(c, gs[i]));
+  while (true) {
+    for (int i = 0; i < B; ++i)
+      if (!gs[i].done && !gs[i].in_cycle) CKS(g_cycle_begin(c, gs[i]));
+    int act[GEMV_MAX_RHS / 2], na = 0, ncyc = 0;
+    for (int i = 0; i < B; ++i) {
+      if (!gs[i].in_cycle) continue;
+      // grow the basis BEFORE taking pointers into it (growth reallocates)
+      CKS(ensure_krylov(c, *gs[i].w, (size_t)gs[i].j + 1));
+      ++ncyc;
+      if (gs[i].needs_op() && gs[i].j != c->restart + 1) act[na++] = i;
+    }
+    if (ncyc == 0) break;
+    const double* zs[GEMV_MAX_RHS / 2] = {};
+    if (na) {
+      const double *iw[GEMV_MAX_RHS / 2], *is[GEMV_MAX_RHS / 2];
+      double *ow[GEMV_MAX_RHS / 2], *os[GEMV_MAX_RHS / 2];
+      for (int q = 0; q < na; ++q) {
+        SysWS& w = *gs[act[q]].w;
+        const double* u = w.Vk + (size_t)(gs[act[q]].j - 1) * 2 * n;
+        if (gs[act[q]].L.pc) {
+          iw[q] = u; is[q] = u + n; ow[q] = w.zb; os[q] = w.zb + n;
+          zs[q] = w.zb;
+        } else {
+          zs[q] = u;
+        }
+      }
+      // the GEMV scratch of sys[0..na) serves any subset of systems
+      if (gs[act[0]].L.pc) CKS(precond_apply_multi(c, na, iw, is, ow, os));
+    }
+    for (int i = 0, q = 0; i < B; ++i) {
+      if (!gs[i].in_cycle) continue;
+      const double* z = nullptr;
+      if (q < na && act[q] == i) z = zs[q++];
+      CKS(g_iter(c, gs[i], z));
+    }
+  }
+  for (int i = 0; i < B; ++i) {
+    if (c->st) c->st->gmres_its += gs[i].total;
+    if (!gs[i].converged) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "GMRES did not converge within %d iterations", c->op.krylov_max_per_newton);
+      return fail(c, HBPDC_E_GMRES, buf);
+    }
   }
   return HBPDC_OK;
 }
 
 // ---- Newton on the extended system (eq:Newton) -------------------------
-// X0 = (W_g, R1(W_g)); the result is in c->X = [W | sigma].
-hbpdc_status newton(hbpdc_ctx* c, double a1, double a2, double dt, const double* b, const double* Wg) {
+// B systems in lock step (B = 1: one stage solve).  System i starts from
+// X0 = (Wg_i, R1(Wg_i)) with right-hand side b_i = sys[i].b; result in sys[i].X.
+hbpdc_status newton_batch(hbpdc_ctx* c, int B, double a1, double a2, double dt, const double* const* Wg) {
   const size_t n = c->n, n2 = 2 * n;
-  double* W = c->X;
-  double* sg = c->X + n;
-  CK(cudaMemcpyAsync(W, Wg, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  {
+  double floor_[GEMV_MAX_RHS / 2], g0[GEMV_MAX_RHS / 2];
+  bool active[GEMV_MAX_RHS / 2];
+  for (int i = 0; i < B; ++i) {
+    SysWS& w = c->sys[i];
+    CK(cudaMemcpyAsync(w.X, Wg[i], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     OpArgs A = base_args(c);
-    A.W = W; A.out1 = sg;
+    A.W = w.X; A.out1 = w.X + n;
     CKS(run_op(c, OP_R1, A));
+    double bn, rabs;
+    CKS(norm_host(c, w.b, n, &bn));
+    OpArgs Ab = base_args(c);
+    Ab.W = w.X; Ab.out1 = w.G;            // G is scratch here
+    CKS(run_op(c, OP_R1ABS, Ab));
+    CKS(norm_host(c, w.G, n, &rabs));
+    // floor = max(64 eps ||b||, 4 eps ||R1_abs(W_g)||)   (readings R10, R10b)
+    floor_[i] = std::max(c->op.newton_floor * EPS_MACH * bn, 4.0 * EPS_MACH * rabs);
+    g0[i] = -1.0;
+    active[i] = true;
   }
-  double bn, rabs;
-  CKS(norm_host(c, b, n, &bn));
-  {
-    OpArgs A = base_args(c);
-    A.W = W; A.out1 = c->G;            // G is scratch here
-    CKS(run_op(c, OP_R1ABS, A));
-  }
-  CKS(norm_host(c, c->G, n, &rabs));
-  // floor = max(64 eps ||b||, 4 eps ||R1_abs(W_g)||)   (readings R10, R10b)
-  const double floor = std::max(c->op.newton_floor * EPS_MACH * bn, 4.0 * EPS_MACH * rabs);
-  double g0 = -1.0;
+  const bool pc = c->op.precond == HBPDC_PC_BJEXT;
   for (int r = 0; r <= c->op.newton_max; ++r) {
-    {
-      OpArgs A = base_args(c);
-      A.W = W; A.S = sg; A.b = b; A.out1 = c->G; A.out2 = c->G + n;
-      A.a1dt = a1 * dt;
-      A.c2 = a2 * dt * dt / 2.0;
-      ProfScope ps(c, 2, 5.0 * n * 8.0);
-      CKS(run_op(c, OP_RESID, A));
+    int na = 0;
+    for (int i = 0; i < B; ++i) {
+      if (!active[i]) continue;
+      SysWS& w = c->sys[i];
+      use_ghosts(c, w);
+      {
+        OpArgs A = base_args(c);
+        A.W = w.X; A.S = w.X + n; A.b = w.b; A.out1 = w.G; A.out2 = w.G + n;
+        A.a1dt = a1 * dt;
+        A.c2 = a2 * dt * dt / 2.0;
+        ProfScope ps(c, 2, 5.0 * n * 8.0);
+        CKS(run_op(c, OP_RESID, A));
+      }
+      double gn;
+      CKS(norm_host(c, w.G, n2, &gn));
+      if (!std::isfinite(gn)) return fail(c, HBPDC_E_NONFINITE, "non-finite Newton residual");
+      if (g0[i] < 0) g0[i] = gn;
+      if (c->st) c->st->final_newton_rel = g0[i] > 0 ? gn / g0[i] : 0.0;
+      if (gn <= std::max(c->op.newton_rtol * g0[i], floor_[i])) { active[i] = false; continue; }
+      if (r == c->op.newton_max) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "Newton did not converge in %d iterations (||G||=%.3e, ||G0||=%.3e)", r, gn,
+                 g0[i]);
+        return fail(c, HBPDC_E_NEWTON, buf);
+      }
+      ++na;
     }
-    double gn;
-    CKS(norm_host(c, c->G, n2, &gn));
-    if (!std::isfinite(gn)) return fail(c, HBPDC_E_NONFINITE, "non-finite Newton residual");
-    if (g0 < 0) g0 = gn;
-    if (c->st) c->st->final_newton_rel = g0 > 0 ? gn / g0 : 0.0;
-    if (gn <= std::max(c->op.newton_rtol * g0, floor)) return HBPDC_OK;
-    if (r == c->op.newton_max) {
-      char buf[160];
-      snprintf(buf, sizeof buf, "Newton did not converge in %d iterations (||G||=%.3e, ||G0||=%.3e)", r, gn, g0);
-      return fail(c, HBPDC_E_NEWTON, buf);
+    if (na == 0) return HBPDC_OK;
+    if (pc && c->op.precond_policy == HBPDC_PC_PER_NEWTON) {   // B == 1 under this policy
+      CKS(precond_build_impl(c, a1, a2, dt, c->sys[0].X));
     }
-    const bool pc = c->op.precond == HBPDC_PC_BJEXT;
-    if (pc && c->op.precond_policy == HBPDC_PC_PER_NEWTON) CKS(precond_build_impl(c, a1, a2, dt, W));
-    CK(launch_axpby(-1.0, c->G, 0.0, c->rhs, n2, c->stream));       // rhs = -G
-    LinSys L{a1, a2, dt, W, sg, pc};
-    int its = 0;
-    CKS(gmres(c, L, &its));
-    CK(launch_axpby(1.0, c->dX, 1.0, c->X, n2, c->stream));         // X += dX
-    if (c->st) c->st->newton_its++;
-    double dwn;
-    CKS(norm_host(c, c->dX, n, &dwn));
-    if (dwn <= c->op.newton_atol_dw) return HBPDC_OK;
+    GState gs[GEMV_MAX_RHS / 2];
+    int idx[GEMV_MAX_RHS / 2], nb = 0;
+    for (int i = 0; i < B; ++i) {
+      if (!active[i]) continue;
+      SysWS& w = c->sys[i];
+      CK(launch_axpby(-1.0, w.G, 0.0, w.rhs, n2, c->stream));       // rhs = -G
+      gs[nb].w = &w;
+      gs[nb].L = LinSys{a1, a2, dt, w.X, w.X + n, pc};
+      idx[nb++] = i;
+    }
+    CKS(gmres_batch(c, gs, nb));
+    for (int q = 0; q < nb; ++q) {
+      SysWS& w = c->sys[idx[q]];
+      CK(launch_axpby(1.0, w.dX, 1.0, w.X, n2, c->stream));         // X += dX
+      if (c->st) c->st->newton_its++;
+      double dwn;
+      CKS(norm_host(c, w.dX, n, &dwn));
+      if (dwn <= c->op.newton_atol_dw) active[idx[q]] = false;
+    }
   }
   return HBPDC_OK;
 }
@@ -775,7 +912,10 @@ hbpdc_status ensure_pc_for(hbpdc_ctx* c, double a1, double a2, double dt, const 
 }
 
 // Alg. 1: predictor (eq:predictor), k_max corrector sweeps
-// (eq:corrector, with I_l, reading R5), FSAL update.
+// (eq:corrector, with I_l, reading R5), FSAL update.  The s-1 corrector
+// stages of a sweep depend only on sweep-k data (eq:corrector), so
+// with batching they are solved in lock step (NEXT-1); the arithmetic of each
+// stage solve is unchanged (bitwise equal to the sequential order).
 hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
   const size_t n = c->n;
   const Tableau& T = c->tab;
@@ -791,45 +931,57 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
     const double a1 = dc / 2.0, a2 = dc * dc / 6.0, c2 = a2 * dt * dt / 2.0;
     const double* X[2] = {c->str1[cur][l - 1], c->str2[cur][l - 1]};
     const double co[2] = {a1 * dt, c2};
-    CK(launch_stage_combo(c->stw[cur][l - 1], 2, X, co, 0, nullptr, nullptr, c->bvec, n, c->stream));
+    CK(launch_stage_combo(c->stw[cur][l - 1], 2, X, co, 0, nullptr, nullptr, c->sys[0].b, n, c->stream));
     CKS(ensure_pc_for(c, a1, a2, dt, c->Wn));
-    hbpdc_status stt = newton(c, a1, a2, dt, c->bvec, c->stw[cur][l - 1]);
+    const double* g = c->stw[cur][l - 1];
+    hbpdc_status stt = newton_batch(c, 1, a1, a2, dt, &g);
     if (stt != HBPDC_OK) {
       c->err = "predictor stage " + std::to_string(l + 1) + ": " + c->err;
       return stt;
     }
     if (c->st) c->st->stage_solves++;
-    CK(cudaMemcpyAsync(c->stw[cur][l], c->X, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->stw[cur][l], c->sys[0].X, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     CKS(stage_ops(c, c->stw[cur][l], c->str1[cur][l], c->str2[cur][l]));
   }
   // ---- correctors (eq:nonlinear_corrector)
+  const int B = (int)c->sys.size();       // 1, or s - 1 when the stages are batched
   for (int k = 0; k < c->pb.kmax; ++k) {
     const int nxt = 1 - cur;
     // stage 1 of the new sweep is W^n with the FSAL operators
     CK(cudaMemcpyAsync(c->stw[nxt][0], c->stw[cur][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(c->str1[nxt][0], c->str1[cur][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(c->str2[nxt][0], c->str2[cur][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    for (int l = 1; l < s; ++l) {
-      // b = W^n - dt R1_l + dt^2/2 R2_l + dt sum_j B1_lj R1_j + dt^2 sum_j B2_lj R2_j
-      const double* X[4];
-      const double* Y[4];
-      double a[4], bb[4];
-      for (int j = 0; j < s; ++j) {
-        X[j] = c->str1[cur][j];
-        Y[j] = c->str2[cur][j];
-        a[j] = dt * T.B1[l][j] - (j == l ? dt : 0.0);
-        bb[j] = dt * dt * T.B2[l][j] + (j == l ? dt * dt / 2.0 : 0.0);
+    for (int l0 = 1; l0 < s; l0 += B) {
+      const int nb = std::min(B, s - l0);
+      const double* guess[GEMV_MAX_RHS / 2];
+      for (int q = 0; q < nb; ++q) {
+        const int l = l0 + q;
+        // b = W^n - dt R1_l + dt^2/2 R2_l + dt sum_j B1_lj R1_j + dt^2 sum_j B2_lj R2_j
+        const double* X[4];
+        const double* Y[4];
+        double a[4], bb[4];
+        for (int j = 0; j < s; ++j) {
+          X[j] = c->str1[cur][j];
+          Y[j] = c->str2[cur][j];
+          a[j] = dt * T.B1[l][j] - (j == l ? dt : 0.0);
+          bb[j] = dt * dt * T.B2[l][j] + (j == l ? dt * dt / 2.0 : 0.0);
+        }
+        CK(launch_stage_combo(c->Wn, s, X, a, s, Y, bb, c->sys[q].b, n, c->stream));
+        guess[q] = c->stw[cur][l];
       }
-      CK(launch_stage_combo(c->Wn, s, X, a, s, Y, bb, c->bvec, n, c->stream));
       CKS(ensure_pc_for(c, 1.0, 1.0, dt, c->Wn));
-      hbpdc_status stt = newton(c, 1.0, 1.0, dt, c->bvec, c->stw[cur][l]);
+      hbpdc_status stt = newton_batch(c, nb, 1.0, 1.0, dt, guess);
       if (stt != HBPDC_OK) {
-        c->err = "corrector sweep " + std::to_string(k + 1) + " stage " + std::to_string(l + 1) + ": " + c->err;
+        c->err = "corrector sweep " + std::to_string(k + 1) + " stages " + std::to_string(l0 + 1) + ".." +
+                 std::to_string(l0 + nb) + ": " + c->err;
         return stt;
       }
-      if (c->st) c->st->stage_solves++;
-      CK(cudaMemcpyAsync(c->stw[nxt][l], c->X, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-      CKS(stage_ops(c, c->stw[nxt][l], c->str1[nxt][l], c->str2[nxt][l]));
+      for (int q = 0; q < nb; ++q) {
+        const int l = l0 + q;
+        if (c->st) c->st->stage_solves++;
+        CK(cudaMemcpyAsync(c->stw[nxt][l], c->sys[q].X, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        CKS(stage_ops(c, c->stw[nxt][l], c->str1[nxt][l], c->str2[nxt][l]));
+      }
     }
     cur = nxt;
   }
@@ -850,20 +1002,43 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
 hbpdc_status alloc_solver(hbpdc_ctx* c) {
   const size_t n = c->n, n2 = 2 * n;
   const int R = c->restart;
-  CKS(dalloc(c, &c->X, n2));
-  CKS(dalloc(c, &c->G, n2));
-  CKS(dalloc(c, &c->dX, n2));
-  CKS(dalloc(c, &c->rhs, n2));
-  CKS(dalloc(c, &c->tmp2, n2));
-  CKS(dalloc(c, &c->zb, n2));
-  CKS(ensure_krylov(c, std::min<size_t>((size_t)R + 1, 33)));
-  CKS(dalloc(c, &c->partial, (size_t)(2 * R + 4) * std::max(arnoldi_dot_blocks(n2), RED_BLOCKS)));
-  CKS(dalloc(c, &c->dh, 2 * (size_t)R + 4));
+  // lock-step corrector stages (NEXT-1): one workspace per stage of a sweep
+  int B = 1;
+  if (c->op.batch_stages && c->pb.kmax > 0 && c->op.precond_policy == HBPDC_PC_PER_STEP_PER_ALPHA)
+    B = std::min(c->tab.s - 1, GEMV_MAX_RHS / 2);
+  c->sys.resize(std::max(B, 1));
+  const size_t ng = (size_t)(c->pb.dim == 2 ? 2 * (c->nxl + c->nyl) : 2) * c->m;
+  for (auto& w : c->sys) {
+    CKS(dalloc(c, &w.X, n2));
+    CKS(dalloc(c, &w.G, n2));
+    CKS(dalloc(c, &w.dX, n2));
+    CKS(dalloc(c, &w.rhs, n2));
+    CKS(dalloc(c, &w.r, n2));
+    CKS(dalloc(c, &w.zb, n2));
+    CKS(dalloc(c, &w.b, n));
+    CKS(ensure_krylov(c, w, std::min<size_t>((size_t)R + 1, 33)));
+    CKS(dalloc(c, &w.partial, (size_t)(2 * R + 4) * std::max(arnoldi_dot_blocks(n2), RED_BLOCKS)));
+    CKS(dalloc(c, &w.dh, 2 * (size_t)R + 4));
+    CKS(dalloc(c, &w.dy, 2 * (size_t)R + 4));
+    CKS(dalloc(c, &w.dnrm, 1));
+    if (c->halo()) {
+      CKS(dalloc(c, &w.gW, ng));
+      CKS(dalloc(c, &w.gS, ng));
+    }
+    w.H.assign((size_t)R * (R + 1), 0.0);
+    w.Hraw.assign((size_t)R * (R + 1), 0.0);
+    w.cs.assign(R + 1, 0.0);
+    w.sn.assign(R + 1, 0.0);
+    w.gv.assign(R + 2, 0.0);
+    w.y.assign(R + 1, 0.0);
+    void* hp = nullptr;
+    CK(cudaMallocHost(&hp, (3 * (size_t)(R + 1) + 8) * sizeof(double)));
+    w.hpin = (double*)hp;
+  }
+  CKS(dalloc(c, &c->partial, RED_BLOCKS));
   CKS(dalloc(c, &c->dnrm, 1));
   CKS(dalloc(c, &c->deps, 2));
-  CKS(dalloc(c, &c->dy, 2 * (size_t)R + 4));
   CKS(dalloc(c, &c->Wn, n));
-  CKS(dalloc(c, &c->bvec, n));
   for (int sw = 0; sw < 2; ++sw)
     for (int l = 0; l < c->tab.s; ++l) {
       CKS(dalloc(c, &c->stw[sw][l], n));
@@ -871,9 +1046,8 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
       CKS(dalloc(c, &c->str2[sw][l], n));
     }
   if (c->halo()) {
-    const size_t ng = (size_t)(c->pb.dim == 2 ? 2 * (c->nxl + c->nyl) : 2) * c->m;
-    CKS(dalloc(c, &c->gW, ng));
-    CKS(dalloc(c, &c->gS, ng));
+    c->gW = c->sys[0].gW;
+    c->gS = c->sys[0].gS;
     CKS(dalloc(c, &c->gdW, ng));
     CKS(dalloc(c, &c->gdS, ng));
     CKS(dalloc(c, &c->gWb, ng));
@@ -888,14 +1062,8 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     CKS(dalloc(c, &c->lift0, lg));
     CKS(dalloc(c, &c->lift1, lg));
   }
-  c->H.assign((size_t)R * (R + 1), 0.0);
-  c->Hraw.assign((size_t)R * (R + 1), 0.0);
-  c->cs.assign(R + 1, 0.0);
-  c->sn.assign(R + 1, 0.0);
-  c->gv.assign(R + 2, 0.0);
-  c->y.assign(R + 1, 0.0);
   void* hp = nullptr;
-  CK(cudaMallocHost(&hp, (3 * (size_t)(R + 1) + 8) * sizeof(double)));
+  CK(cudaMallocHost(&hp, 16 * sizeof(double)));
   c->hpin = (double*)hp;
   return HBPDC_OK;
 }
@@ -1237,7 +1405,10 @@ void hbpdc_finalize(hbpdc_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   prof_flush(c);
   for (void* p : c->allocs) cudaFree(p);
-  if (c->Vk) cudaFree(c->Vk);
+  for (auto& w : c->sys) {
+    if (w.Vk) cudaFree(w.Vk);
+    if (w.hpin) cudaFreeHost(w.hpin);
+  }
   if (c->hpin) cudaFreeHost(c->hpin);
   delete c->comm;
   if (c->own_stream) cudaStreamDestroy(c->stream);

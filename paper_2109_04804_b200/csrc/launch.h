@@ -44,6 +44,11 @@ cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, c
 // U_e = S_e W_e, V_e = S_e sig_e for every element (S stride 0 if shared)
 cudaError_t launch_block_gemv2(const double* S, int shared, const double* W, const double* sig,
                                double* U, double* V, int m, int nE, cudaStream_t st);
+// out_k = S_e in_k for k < nr right-hand sides (nr in {2, 4, 6}), one streaming pass over
+// the per-element S (not shared); bitwise equal to nr/2 calls of launch_block_gemv2
+constexpr int GEMV_MAX_RHS = 6;
+cudaError_t launch_block_gemv_multi(const double* S, int nr, const double* const* in, double* const* out, int m,
+                                    int nE, cudaStream_t st);
 
 // GMRES / Newton vector kernels.  Reductions are two-level (fixed block
 // count, fixed order): deterministic.

@@ -292,10 +292,18 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                : "memory");
 }
 
-template <int CPL>
-__global__ void __launch_bounds__(256) gemv2_tma_kernel(const double* __restrict__ S, const double* __restrict__ W,
-                                                        const double* __restrict__ sg, double* __restrict__ U,
-                                                        double* __restrict__ V, int m, int nE) {
+// NR right-hand sides (NR = 2: u = S W, v = S sigma of one system; NR = 2B: the
+// B corrector-stage systems of a sweep solved in lock step share ONE pass over
+// S).  Every output row is accumulated in the same order for
+// any NR, so batched and single-system results are bitwise identical.
+struct GemvRHS {
+  const double* in[GEMV_MAX_RHS];
+  double* out[GEMV_MAX_RHS];
+};
+
+template <int CPL, int NR>
+__global__ void __launch_bounds__(256) gemvN_tma_kernel(const double* __restrict__ S, const GemvRHS io, int m,
+                                                        int nE) {
   extern __shared__ __align__(128) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)GT_NST * GT_R * m);
@@ -318,42 +326,112 @@ __global__ void __launch_bounds__(256) gemv2_tma_kernel(const double* __restrict
     for (int c = 0; c < GT_NST && c < T; ++c) issue(c);
   }
   __syncthreads();
-  double wr[CPL], sr[CPL];
+  double xr[NR][CPL];
   for (int c = 0; c < T; ++c) {
     const int e = blockIdx.x + (c / cpe) * gridDim.x;
     const int r0 = (c % cpe) * GT_R;
     if (r0 == 0) {
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) {
-        const int col = lane + 32 * q;
-        wr[q] = col < m ? W[(size_t)e * m + col] : 0.0;
-        sr[q] = col < m ? sg[(size_t)e * m + col] : 0.0;
-      }
+      for (int k = 0; k < NR; ++k)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const int col = lane + 32 * q;
+          xr[k][q] = col < m ? io.in[k][(size_t)e * m + col] : 0.0;
+        }
     }
     mbar_wait(&full[c % GT_NST], (unsigned)((c / GT_NST) & 1));
     const int r = r0 + wid;
     if (r < m) {
       const double* row = ring + ((size_t)(c % GT_NST) * GT_R + wid) * m;
-      double a = 0.0, b = 0.0;
+      double acc[NR];
+#pragma unroll
+      for (int k = 0; k < NR; ++k) acc[k] = 0.0;
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
         const int col = lane + 32 * q;
-        const double s = col < m ? row[col] : 0.0;
-        a = fma(s, wr[q], a);
-        b = fma(s, sr[q], b);
-      }
+        const double sv = col < m ? row[col] : 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
+        for (int k = 0; k < NR; ++k) acc[k] = fma(sv, xr[k][q], acc[k]);
       }
-      if (lane == 0) {
-        U[(size_t)e * m + r] = a;
-        V[(size_t)e * m + r] = b;
+      if constexpr (NR == 2) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int k = 0; k < NR; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+        if (lane < NR) io.out[lane][(size_t)e * m + r] = lane == 0 ? acc[0] : acc[1];
+      } else {
+        // NR > 2: transposed butterfly over V = 8 padded values (7 + 2 shuffles
+        // instead of 5 NR); lane bits 4,3,2 then index the value.  Every value
+        // is summed over the same lane tree (bits 16, 8, 4, 2, 1) as the plain
+        // butterfly of NR == 2 (operands swapped at most: a + b == b + a), so
+        // batched and single-system products are bitwise equal.
+        constexpr int V = 8;
+        double p[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) p[k] = k < NR ? acc[k] : 0.0;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          const int h = V >> (jj + 1), mask = 16 >> jj;
+          const bool hi = lane & mask;
+#pragma unroll
+          for (int q = 0; q < h; ++q) {
+            const double send = hi ? p[q] : p[q + h];
+            const double recv = __shfl_xor_sync(0xffffffffu, send, mask);
+            p[q] = (hi ? p[q + h] : p[q]) + recv;
+          }
+        }
+        p[0] += __shfl_xor_sync(0xffffffffu, p[0], 2);
+        p[0] += __shfl_xor_sync(0xffffffffu, p[0], 1);
+        const int idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        if ((lane & 3) == 0 && idx < NR) io.out[idx][(size_t)e * m + r] = p[0];
       }
     }
     __syncthreads();                       // stage (c % GT_NST) is free again
     if (threadIdx.x == 0 && c + GT_NST < T) issue(c + GT_NST);
+  }
+}
+
+template <int NR>
+static cudaError_t launch_gemvN(const double* S, const GemvRHS& io, int m, int nE, cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    nsm = v;
+  }
+  const size_t smem = (size_t)GT_NST * GT_R * m * sizeof(double) + GT_NST * sizeof(unsigned long long);
+  const int cpl = (m + 31) / 32;
+  // persistent grid: exactly the resident CTAs (registers grow with NR; a
+  // fixed 3 per SM would leave a half-empty second wave at NR = 6)
+#define GT(C)                                                                                   \
+  case C: {                                                                                     \
+    cudaFuncSetAttribute(gemvN_tma_kernel<C, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    int occ = 0;                                                                                \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemvN_tma_kernel<C, NR>, 256, smem);    \
+    const int grid = std::min(nE, nsm * std::max(occ, 1));                                      \
+    gemvN_tma_kernel<C, NR><<<grid, 256, smem, st>>>(S, io, m, nE);                              \
+  } break;
+  switch (cpl) {
+    GT(1) GT(2) GT(3) GT(4) GT(5) GT(6) GT(7) GT(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef GT
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_gemv_multi(const double* S, int nr, const double* const* in, double* const* out, int m,
+                                    int nE, cudaStream_t st) {
+  if (nE <= 0) return cudaSuccess;
+  if (nr < 1 || nr > GEMV_MAX_RHS || (m * sizeof(double)) % 16 != 0) return cudaErrorInvalidValue;
+  GemvRHS io{};
+  for (int k = 0; k < nr; ++k) { io.in[k] = in[k]; io.out[k] = out[k]; }
+  switch (nr) {
+    case 2: return launch_gemvN<2>(S, io, m, nE, st);
+    case 4: return launch_gemvN<4>(S, io, m, nE, st);
+    case 6: return launch_gemvN<6>(S, io, m, nE, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 
@@ -362,26 +440,9 @@ cudaError_t launch_block_gemv2(const double* S, int shared, const double* W, con
   if (nE <= 0) return cudaSuccess;
   const int cpl = (m + 31) / 32;
   if (!shared && (m * sizeof(double)) % 16 == 0) {
-    static int nsm = 0;
-    if (!nsm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const size_t smem = (size_t)GT_NST * GT_R * m * sizeof(double) + GT_NST * sizeof(unsigned long long);
-    const int grid = std::min(nE, nsm * 3);
-#define GT(C)                                                                                  \
-  case C:                                                                                      \
-    cudaFuncSetAttribute(gemv2_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    gemv2_tma_kernel<C><<<grid, 256, smem, st>>>(S, W, sig, U, V, m, nE);                       \
-    break;
-    switch (cpl) {
-      GT(1) GT(2) GT(3) GT(4) GT(5) GT(6) GT(7) GT(8)
-      default: return cudaErrorInvalidValue;
-    }
-#undef GT
-    hbpdc_count_launch();
-    return cudaGetLastError();
+    const double* in[2] = {W, sig};
+    double* out[2] = {U, V};
+    return launch_block_gemv_multi(S, 2, in, out, m, nE, st);
   }
 #define G(C) case C: gemv2_kernel<C><<<nE, 256, 0, st>>>(S, shared, W, sig, U, V, m, nE); break;
   switch (cpl) {

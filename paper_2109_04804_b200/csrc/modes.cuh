@@ -58,10 +58,19 @@ struct OneJetMode {
 #pragma unroll
     for (int d = 0; d < DIM; ++d) Derived::comb(A, F[d], c[d]);
   }
-  __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
+  // face work in two halves: part 0 = the canonical L side (-e_d), part 1 = R
+  static constexpr int NFP = 2, FPD = half_doubles<EQ, J>();
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
+                                   int nnode, int slot, bool plus, int d, int part, double* raw) {
+    const bool use_own = (part == 0) == plus;
+    State st;
+    load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
+    half_flux<EQ, J>(pp, st.s, d, raw);
+  }
+  __device__ static void face_combine(const Args& A, const PhysParams& pp, int d, const double* rL,
+                                      const double* rR, double (&c)[NCH][NV]) {
     J f[NV];
-    face_flux<EQ>(pp, L.s, R.s, d, f);
+    face_from_halves<EQ, J>(pp, rL, rR, d, f);
     Derived::comb(A, f, c);
   }
 };
@@ -231,28 +240,45 @@ template <int EQ, int NODES> struct ModeJvpFD {
       for (int d = 0; d < DIM; ++d) comb(A, Fp[d], Fq[d], c[d]);
     }
   }
-  __device__ static void face(const Args& A, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
-    // p-face first, folded into the channels, then the q-face: the two jet
-    // states are never live together
+  // face work split by jet state: part 0 = p-state face flux (J1), part 1 = q-state (J2)
+  static constexpr int NFP = 2, FPD = 3 * NV;
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo&, int e, int own, int nb,
+                                   int nnode, int, bool plus, int d, int part, double* raw) {
+    if (part == 0) {
+      if (!(fd_step(A) > 0.0)) return;
+      NodeState<EQ, J1> so, sn;
+      load_w<0>(A, e, own, so.w, false);
+      load_w<0>(A, nb, nnode, sn.w, true);
+      ld_state<EQ, J1, NODES>(A.G0, e, own, so);
+      ld_state<EQ, J1, NODES>(A.G0, nb, nnode, sn);
+      J1 fp[NV];
+      if (plus) face_flux<EQ>(pp, so, sn, d, fp);
+      else face_flux<EQ>(pp, sn, so, d, fp);
+      for (int v = 0; v < NV; ++v) { raw[2 * v] = fp[v].v; raw[2 * v + 1] = fp[v].a; }
+    } else {
+      NodeState<EQ, J2> so, sn;
+      load_w<1>(A, e, own, so.w, false);
+      load_w<1>(A, nb, nnode, sn.w, true);
+      ld_state<EQ, J2, NODES>(A.G1, e, own, so);
+      ld_state<EQ, J2, NODES>(A.G1, nb, nnode, sn);
+      J2 fq[NV];
+      if (plus) face_flux<EQ>(pp, so, sn, d, fq);
+      else face_flux<EQ>(pp, sn, so, d, fq);
+      for (int v = 0; v < NV; ++v) { raw[3 * v] = fq[v].v; raw[3 * v + 1] = fq[v].a; raw[3 * v + 2] = fq[v].b; }
+    }
+  }
+  __device__ static void face_combine(const Args& A, const PhysParams&, int, const double* rp, const double* rq,
+                                      double (&c)[NCH][NV]) {
     const double ew = fd_step(A);
     const double ie = ew > 0.0 ? 1.0 / ew : 0.0;
-    double pv[NV], pa[NV];
-    if (ew > 0.0) {
-      J1 fp[NV];
-      face_flux<EQ>(pp, L.p, R.p, d, fp);
-      for (int v = 0; v < NV; ++v) { pv[v] = fp[v].v; pa[v] = fp[v].a; }
-    }
-    J2 fq[NV];
-    face_flux<EQ>(pp, L.q, R.q, d, fq);
     for (int v = 0; v < NV; ++v) {
       if (ew > 0.0) {
-        const double q1 = (pv[v] - fq[v].v) * ie;
-        const double q2 = (pa[v] - fq[v].a) * ie;
-        c[0][v] = fma(A.c2, q2 + fq[v].b, -A.a1dt * q1);
+        const double q1 = (rp[2 * v] - rq[3 * v]) * ie;
+        const double q2 = (rp[2 * v + 1] - rq[3 * v + 1]) * ie;
+        c[0][v] = fma(A.c2, q2 + rq[3 * v + 2], -A.a1dt * q1);
         c[1][v] = q1;
       } else {
-        c[0][v] = A.c2 * fq[v].b;
+        c[0][v] = A.c2 * rq[3 * v + 2];
         c[1][v] = 0.0;
       }
     }
@@ -293,12 +319,23 @@ template <int EQ, int NODES> struct ModeJvpLinear {
     for (int d = 0; d < DIM; ++d)
       for (int v = 0; v < NV; ++v) { c[d][0][v] = F0[d][v]; c[d][1][v] = F1[d][v]; }
   }
-  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
-    double f0[NV], f1[NV];
-    face_flux<EQ>(pp, L.u0, R.u0, d, f0);
-    face_flux<EQ>(pp, L.u1, R.u1, d, f1);
-    for (int v = 0; v < NV; ++v) { c[0][v] = f0[v]; c[1][v] = f1[v]; }
+  // face work split by input: part 0 = F(-a1dt dW + c2 dsigma), part 1 = F(dW)
+  static constexpr int NFP = 2, FPD = NV;
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
+                                   int nnode, int slot, bool plus, int d, int part, double* raw) {
+    State so, sn;
+    load(A, g, e, slot, own, so, false);
+    load(A, g, nb, slot, nnode, sn, true);
+    const NodeState<EQ, double>& o = part == 0 ? so.u0 : so.u1;
+    const NodeState<EQ, double>& q = part == 0 ? sn.u0 : sn.u1;
+    double f[NV];
+    if (plus) face_flux<EQ>(pp, o, q, d, f);
+    else face_flux<EQ>(pp, q, o, d, f);
+    for (int v = 0; v < NV; ++v) raw[v] = f[v];
+  }
+  __device__ static void face_combine(const Args&, const PhysParams&, int, const double* r0, const double* r1,
+                                      double (&c)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) { c[0][v] = r0[v]; c[1][v] = r1[v]; }
   }
   __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {

@@ -144,17 +144,88 @@ __device__ __forceinline__ void load_grads(const double* G, int e, int node, T* 
   }
 }
 
+// ---- face flux in two halves -------------------------------------------------
+// The canonical face flux needs each side's state, flux, wave speed (and NS
+// viscous flux).  Computing the two sides on two threads and combining later
+// balances the face work over all warps of an element (the combination below
+// reproduces face_flux() operation for operation, so results are bitwise equal).
+template <int EQ, class T> struct HalfFlux {
+  static constexpr int NV = NVars<EQ>::value;
+  T F[NV], w[NV], Fv[EQ == 2 ? 4 : 1];
+  T lam;
+};
+template <int EQ, class T>
+__host__ __device__ constexpr int half_doubles() {
+  return JetN<T>::value * (2 * NVars<EQ>::value + 1 + (EQ == 2 ? 4 : 0));
+}
+
+template <int EQ, class T>
+__device__ __forceinline__ void half_flux(const PhysParams& pp, const NodeState<EQ, T>& s, int d, double* raw) {
+  constexpr int NV = NVars<EQ>::value, JN = JetN<T>::value;
+  T F[NV], lam;
+  if constexpr (EQ == 0) {
+    phys_flux<EQ>(pp, s.w, d, F);
+    lam = jconst<T>(0.0);
+  } else {
+    const EulerPrim<T> q = euler_prim(pp, s.w);
+    euler_flux(s.w, q, d, F);
+    lam = euler_speed(pp, q, d);
+  }
+  int o = 0;
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int c = 0; c < JN; ++c) raw[o++] = jget(F[v], c);
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int c = 0; c < JN; ++c) raw[o++] = jget(s.w[v], c);
+#pragma unroll
+  for (int c = 0; c < JN; ++c) raw[o++] = jget(lam, c);
+  if constexpr (EQ == 2) {
+    T Fv[4];
+    viscous_flux(pp, s.w, s.gx, s.gy, d, Fv);
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int c = 0; c < JN; ++c) raw[o++] = jget(Fv[v], c);
+  }
+}
+
+// f = face_flux(L, R) from the two halves (same operations, same order)
+template <int EQ, class T>
+__device__ __forceinline__ void face_from_halves(const PhysParams& pp, const double* rL, const double* rR, int d,
+                                                 T* f) {
+  constexpr int NV = NVars<EQ>::value, JN = JetN<T>::value;
+  auto rd = [&](const double* r, int idx) { return jmake<T>(r + idx * JN); };
+  T lam;
+  if constexpr (EQ == 0) {
+    lam = jconst<T>(d == 0 ? (pp.ax >= 0 ? pp.ax : -pp.ax) : (pp.ay >= 0 ? pp.ay : -pp.ay));
+  } else {
+    lam = jmax(rd(rL, 2 * NV), rd(rR, 2 * NV));
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+    f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + 0.5 * lam * (rd(rL, NV + v) - rd(rR, NV + v));
+  if constexpr (EQ == 2) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) f[v] = f[v] - 0.5 * (rd(rL, 2 * NV + 1 + v) + rd(rR, 2 * NV + 1 + v));
+  }
+}
+
 // ---- the element evaluation (one slot, one node per thread) --------------------
 // Shared scratch per slot: slot_doubles<...>() = volume-flux planes
-// NCH*DIM*NV*P*(P+1) + face fluxes NCH*NV*2*DIM*P^(DIM-1).
+// NCH*DIM*NV*P*(P+1) + face parts NFP*NFN*FPD.
 //   phase 1  every thread: node state -> volume fluxes (NCH channels) -> smem
-//   phase 2  threads 0 .. 2*DIM*P^(DIM-1)-1: one face node each (canonical
-//            LLF flux with the neighbour's trace), pre-scaled surface term -> smem
-//   phase 3  every thread: Dhat contraction + its surface terms
-template <int EQ, int DIM, int P, int NCH>
+//   phase 2  the NFP x NFN face work items (a face node's flux split into NFP
+//            parts: the two sides' half fluxes, or the two jet states of the FD
+//            JVP), spread over all threads of the element -> raw parts in smem
+//   phase 3  every thread: Dhat contraction; boundary nodes combine the parts
+//            of their face(s) (Mode::face_combine) into the surface terms
+template <int EQ, int DIM, int P, class Mode>
 __host__ __device__ constexpr int slot_doubles() {
-  return NCH * DIM * NVars<EQ>::value * (DIM == 2 ? P : 1) * (P + 1) +
-         NCH * NVars<EQ>::value * 2 * DIM * (DIM == 2 ? P : 1);
+  return Mode::NCH * DIM * NVars<EQ>::value * (DIM == 2 ? P : 1) * (P + 1) +
+         Mode::NFP * 2 * DIM * (DIM == 2 ? P : 1) * Mode::FPD;
 }
 
 template <int EQ, int DIM, int P, class Mode>
@@ -163,11 +234,12 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
                                           double* sF, double (&out)[Mode::NCH][NVars<EQ>::value]) {
   constexpr int NV = NVars<EQ>::value;
   constexpr int NCH = Mode::NCH;
+  constexpr int NFP = Mode::NFP, FPD = Mode::FPD;
   constexpr int PS = P + 1;                       // padded row stride (bank conflicts)
   constexpr int PLANE = (DIM == 2 ? P : 1) * PS;  // one (ch, d, v) plane
   constexpr int FN = DIM == 2 ? P : 1;            // nodes per face
   constexpr int NFN = 2 * DIM * FN;               // face nodes per element
-  double* sFace = sF + NCH * DIM * NV * PLANE;    // [ch][v][face][k]
+  double* sRaw = sF + NCH * DIM * NV * PLANE;     // [part][face node][FPD]
   const int i = node % P;
   const int j = DIM == 2 ? node / P : 0;
 
@@ -184,10 +256,9 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
         for (int v = 0; v < NV; ++v) sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i] = cf[d][c][v];
   }
   constexpr int NODES = DIM == 2 ? P * P : P;
-  // face nodes packed into the first warps (measured faster than spreading
-  // them over all warps: fewer half-empty warps executing the face code)
-  for (int fn = node; active && fn < NFN; fn += NODES) {
+  for (int it = node; active && it < NFP * NFN; it += NODES) {
     // face f: 0 = -x, 1 = +x, 2 = -y, 3 = +y; node k along the face
+    const int part = it / NFN, fn = it % NFN;
     const int f = fn / FN, k = fn % FN;
     const int d = f >> 1;
     const bool plus = f & 1;
@@ -195,20 +266,31 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
     const int own = DIM == 1 ? own_edge : (d == 0 ? k * P + own_edge : own_edge * P + k);
     const int nnode = DIM == 1 ? nbr_edge : (d == 0 ? k * P + nbr_edge : nbr_edge * P + k);
     const int nb = nbr_elem(g, e, d, plus ? +1 : -1);
-    typename Mode::State so, sn;
-    Mode::load(A, g, e, slot, own, so, false);
-    Mode::load(A, g, nb, slot, nnode, sn, true);
-    double cf[NCH][NV];
-    if (plus) Mode::face(A, pp, so, sn, d, cf);     // canonical L = own (the -e_d side)
-    else Mode::face(A, pp, sn, so, d, cf);          // canonical L = neighbour
-    const double s = (d == 0 ? g.sx : g.sy) * (plus ? g.lhp : -g.lhm);
-#pragma unroll
-    for (int c = 0; c < NCH; ++c)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) sFace[((c * NV + v) * 2 * DIM + f) * FN + k] = s * cf[c][v];
+    Mode::face_part(A, pp, g, e, own, nb, nnode, slot, plus, d, part, sRaw + (size_t)(part * NFN + fn) * FPD);
   }
   __syncthreads();
   if (active) {
+    // surface terms of this node's face(s), canonical flux with the outward sign:
+    // s_d (f*_+ lhat_N(1) - f*_- lhat_0(-1))
+    double fs[4][NCH][NV];
+    auto face_term = [&](int f, int k) {
+      const int d = f >> 1;
+      const bool plus = f & 1;
+      const int fn = f * FN + k;
+      double cf[NCH][NV];
+      Mode::face_combine(A, pp, d, sRaw + (size_t)fn * FPD, sRaw + (size_t)(NFN + fn) * FPD, cf);
+      const double sc = (d == 0 ? g.sx : g.sy) * (plus ? g.lhp : -g.lhm);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) fs[f][c][v] = sc * cf[c][v];
+    };
+    const bool f0 = i == 0, f1 = i == P - 1;
+    const bool f2 = DIM == 2 && j == 0, f3 = DIM == 2 && j == P - 1;
+    if (f1) face_term(1, j);
+    if (f0) face_term(0, j);
+    if (f3) face_term(3, i);
+    if (f2) face_term(2, i);
     double Dr[P], Dc[P];
 #pragma unroll
     for (int l = 0; l < P; ++l) {
@@ -220,7 +302,6 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE + j * PS;
-        const double* fs = sFace + (c * NV + v) * 2 * DIM * FN;
         double ax = 0.0;
 #pragma unroll
         for (int l = 0; l < P; ++l) ax = fma(Dr[l], Fx[l], ax);
@@ -233,12 +314,10 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
           acc = fma(g.sy, ay, acc);
         }
         double surf = 0.0;
-        if (i == P - 1) surf += fs[1 * FN + j];
-        if (i == 0) surf += fs[0 * FN + j];
-        if constexpr (DIM == 2) {
-          if (j == P - 1) surf += fs[3 * FN + i];
-          if (j == 0) surf += fs[2 * FN + i];
-        }
+        if (f1) surf += fs[1][c][v];
+        if (f0) surf += fs[0][c][v];
+        if (f3) surf += fs[3][c][v];
+        if (f2) surf += fs[2][c][v];
         out[c][v] = -(acc + surf);
       }
   }
@@ -261,8 +340,8 @@ __global__ void __launch_bounds__(EPB * ipow(P, DIM), HBPDC_MINB)
 op_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int NV = NVars<EQ>::value;
-  constexpr int SLOT = slot_doubles<EQ, DIM, P, Mode::NCH>();
-  __shared__ double sF[EPB * SLOT];
+  extern __shared__ __align__(16) double sF[];     // EPB * slot_doubles (dynamic: may exceed 48 KB)
+  constexpr int SLOT = slot_doubles<EQ, DIM, P, Mode>();
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
   const int e = blockIdx.x * EPB + slot;
   const bool active = e < g.nE;

@@ -11,7 +11,15 @@ static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
   constexpr int EPB = epb_for(NODES);
   const int grid = (g.nE + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
-  op_kernel<EQ, DIM, P, Mode, EPB><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, g);
+  constexpr size_t smem = (size_t)EPB * slot_doubles<EQ, DIM, P, Mode>() * sizeof(double);
+  if constexpr (smem > 48 * 1024) {
+    static bool attr = false;       // once per instantiation (same value from any thread)
+    if (!attr) {
+      cudaFuncSetAttribute(op_kernel<EQ, DIM, P, Mode, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+  }
+  op_kernel<EQ, DIM, P, Mode, EPB><<<grid, EPB * NODES, smem, c.stream>>>(A, c.pp, g);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -56,10 +64,18 @@ template <int EQ, int NODES> struct ModeKCol {
     for (int d = 0; d < DIM; ++d)
       for (int v = 0; v < NV; ++v) c[d][0][v] = F[d][v].a;
   }
-  __device__ static void face(const Args&, const PhysParams& pp, const State& L, const State& R, int d,
-                              double (&c)[NCH][NV]) {
+  static constexpr int NFP = 2, FPD = half_doubles<EQ, J1>();
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
+                                   int nnode, int slot, bool plus, int d, int part, double* raw) {
+    const bool use_own = (part == 0) == plus;
+    State st;
+    load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
+    half_flux<EQ, J1>(pp, st.s, d, raw);
+  }
+  __device__ static void face_combine(const Args&, const PhysParams& pp, int d, const double* rL, const double* rR,
+                                      double (&c)[NCH][NV]) {
     J1 f[NV];
-    face_flux<EQ>(pp, L.s, R.s, d, f);
+    face_from_halves<EQ, J1>(pp, rL, rR, d, f);
     for (int v = 0; v < NV; ++v) c[0][v] = f[v].a;
   }
 };
@@ -72,9 +88,10 @@ kbuild_kernel(const double* __restrict__ Wb, const double* __restrict__ gWb, con
   constexpr int NV = NVars<EQ>::value;
   constexpr int m = NV * NODES;
   using Mode = ModeKCol<EQ, NODES>;
-  constexpr int SLOT = slot_doubles<EQ, DIM, P, 1>();
-  __shared__ double sF[EPB * SLOT];
-  __shared__ double stan[EPB * m];
+  constexpr int SLOT = slot_doubles<EQ, DIM, P, Mode>();
+  extern __shared__ __align__(16) double sdyn[];
+  double* sF = sdyn;                  // EPB * SLOT
+  double* stan = sdyn + EPB * SLOT;   // EPB * m
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
   const int e = e0 + blockIdx.x;
   double* Me = M + (size_t)blockIdx.x * m * m;
@@ -110,7 +127,17 @@ static cudaError_t run_kbuild(const OpCfg& c, const Geo& g, const double* Wb, co
   constexpr int NODES = ipow(P, DIM);
   constexpr int EPB = epb_for(NODES);
   if (ne <= 0) return cudaSuccess;
-  kbuild_kernel<EQ, DIM, P, EPB><<<ne, EPB * NODES, 0, c.stream>>>(Wb, gWb, c.pp, g, a1dt, c2, M, e0);
+  constexpr int NV = NVars<EQ>::value;
+  constexpr size_t smem =
+      (size_t)EPB * (slot_doubles<EQ, DIM, P, ModeKCol<EQ, NODES>>() + NV * NODES) * sizeof(double);
+  if constexpr (smem > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kbuild_kernel<EQ, DIM, P, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+  }
+  kbuild_kernel<EQ, DIM, P, EPB><<<ne, EPB * NODES, smem, c.stream>>>(Wb, gWb, c.pp, g, a1dt, c2, M, e0);
   hbpdc_count_launch();
   return cudaGetLastError();
 }

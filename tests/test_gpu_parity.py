@@ -265,3 +265,25 @@ def test_c5_shape_end_of_run():
     for _ in range(cfg.steps):
         ctx.step(dt, Wg)
     assert rel(to_np(Wg), Wo) <= 1e-8
+
+
+@pytest.mark.parametrize("q,kmax", [(8, 4), (6, 2)])
+def test_batched_correctors_bitwise(q, kmax):
+    """NEXT-1: the s-1 corrector stages of a sweep solved in lock step (one
+    BJ_ext S pass per Arnoldi step for all of them) give bit-identical steps
+    and identical iteration counts to the sequential order."""
+    import torch
+    cfg = configs.scaled(configs.CONFIGS["C3"], N=3, nx=4, ny=4, q=q, kmax=kmax)
+    out = []
+    for batch in (True, False):
+        d, ctx = make_pair("euler", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=q, kmax=kmax,
+                           gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, batch_stages=batch)
+        W0 = inputs.initial_state("C3", d.node_coords(), noise=cfg.noise)
+        dt = configs.cfl_dt(cfg, inputs.initial_state("C3", d.node_coords()))
+        Wg = to_gpu(W0)
+        st = [ctx.step(dt, Wg) for _ in range(2)]
+        torch.cuda.synchronize()
+        out.append((to_np(Wg), [(s["gmres_its"], s["newton_its"]) for s in st]))
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
