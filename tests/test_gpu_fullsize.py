@@ -196,3 +196,32 @@ def test_c3_fullsize_step_invariants():
     assert st["stage_solves"] == 15
     assert np.all(np.isfinite(W1))
     ctx.close()
+
+
+@pytest.mark.parametrize("case", ["C1", "C2"])
+def test_fullsize_linear_end_of_run(case):
+    """C1 and C2 EXACTLY as BASELINE.json states them (full mesh, all steps),
+    end of run against the oracle's closed-form Alg. 1 for w' = K w (exact
+    stage solves, per Fourier mode of the element grid; oracle/linear.py),
+    <= 1e-8 relative.  The GPU runs Newton-GMRES with BJ_ext at a GMRES
+    tolerance of 1e-12 (C1's own; C2's 1e-6 would bound the agreement at
+    ~1e-6 instead of testing the arithmetic), everything else as configured."""
+    import torch
+    from oracle import linear
+    cfg = configs.CONFIGS[case]
+    ctx = hbpdc.context_for(cfg, gmres_rtol=1e-12)
+    coords = ctx.node_coords()
+    W0 = inputs.initial_state(case, coords)
+    dt = configs.cfl_dt(cfg, W0)
+    eq = physics.Equation("advection", a=cfg.a)
+    d = dgsem.Disc(basis.build_basis(cfg.N, "gll"),
+                   dgsem.Mesh(cfg.dim, cfg.nx, cfg.ny, *cfg.bounds), eq)
+    ref = linear.run_fourier(d, cfg.q, cfg.kmax, dt, W0, cfg.steps)
+    Wg = to_gpu(W0)
+    its = 0
+    for _ in range(cfg.steps):
+        its += ctx.step(dt, Wg)["gmres_its"]
+    torch.cuda.synchronize()
+    err = rel(to_np(Wg), ref)
+    assert err <= 1e-8, (case, err, its)
+    ctx.close()
