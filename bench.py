@@ -168,7 +168,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     # one dedicated stream for torch and the library (no legacy-default-stream syncs)
     torch.cuda.set_stream(torch.cuda.Stream(device=local))
-    if world > 1:
+    # torchrun sets MASTER_ADDR/RANK even for one process: the distributed
+    # plumbing then runs at N = 1 too (with --self-halo it is fully exercised)
+    use_dist = world > 1 or ("MASTER_ADDR" in os.environ and "RANK" in os.environ)
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = configs.CONFIGS[CONFIG]
     # N > 1: ONE global problem, C3's 128x128-element tile repeated on a px x py
@@ -178,13 +181,15 @@ def run_ours(args):
     # Per-GPU work is C3's: weak scaling.  DESIGN.md "Multi-GPU".
     px, py = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}.get(world, (world, 1))
     kw = {}
-    if world > 1:
+    if world > 1 or args.self_halo:
         nid = [hbpdc.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(nid, src=0)
+        if use_dist:
+            dist.broadcast_object_list(nid, src=0)
         kw = dict(nx=cfg.nx * px, ny=cfg.ny * py,
                   bounds=(cfg.bounds[0], cfg.bounds[0] + px * (cfg.bounds[1] - cfg.bounds[0]),
                           cfg.bounds[2], cfg.bounds[2] + py * (cfg.bounds[3] - cfg.bounds[2])),
-                  rank=rank, nranks=world, px=px, py=py, comm="nccl", nccl_id=nid[0])
+                  rank=rank, nranks=world, px=px, py=py, comm="nccl", nccl_id=nid[0],
+                  force_halo=bool(args.self_halo))
     ctx = hbpdc.context_for(cfg, device=local, **kw)
     coords = inputs.tile_coords(ctx.node_coords(), cfg.bounds)
     W0 = inputs.initial_state(CONFIG, coords, noise=cfg.noise, stream=rank)
@@ -194,7 +199,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         ctx.step(dt, W)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     clocks = Clocks(local)
     clocks.start()
@@ -215,7 +220,7 @@ def run_ours(args):
     ctx.profile(False)
     ck = clocks.stop()
     t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * args.steps / (ms_max / 1e3)
@@ -260,13 +265,13 @@ def run_ours(args):
         ctx.reset()
         ctx.step_host(dt, Wh.numpy())                 # warm
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             ctx.step_host(dt, Wh.numpy())
         te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
-        if world > 1:
+        if use_dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": world * args.e2e_steps / float(te.item()), "unit": UNIT,
                "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8, "steps": args.e2e_steps}
@@ -289,7 +294,8 @@ def run_ours(args):
                                    "BJ_ext, FD JVP, Newton/GMRES rtol 1e-10, restart 700",
                        "dt": dt, "n_dof_per_gpu": n, "n_dof": n * world,
                        "parallelism": (f"element partition {px}x{py} of a {cfg.nx * px}x{cfg.ny * py} mesh "
-                                       "(C3 tile per GPU), NCCL halos + all-reduces") if world > 1 else "1 GPU",
+                                       "(C3 tile per GPU), NCCL halos + all-reduces") if world > 1 else
+                                      ("1 GPU, NCCL self-halo" if args.self_halo else "1 GPU"),
                        "l2": "working set > L2 (BJ_ext blocks 8.6 GB, Krylov basis up to 47 GB)"},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -305,7 +311,7 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 
@@ -318,6 +324,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--self-halo", action="store_true",
+                    help="test hook: route the periodic wrap through the NCCL transport (N = 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

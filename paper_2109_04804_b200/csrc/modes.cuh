@@ -61,16 +61,17 @@ struct OneJetMode {
   // face work in two halves: part 0 = the canonical L side (-e_d), part 1 = R
   static constexpr int NFP = 2, FPD = half_doubles<EQ, J>();
   __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
-                                   int nnode, int slot, bool plus, int d, int part, double* raw) {
+                                   int nnode, int slot, bool plus, int d, int part, double* raw,
+                                   int rs) {
     const bool use_own = (part == 0) == plus;
     State st;
     load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
-    half_flux<EQ, J>(pp, st.s, d, raw);
+    half_flux<EQ, J>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args& A, const PhysParams& pp, int d, const double* rL,
-                                      const double* rR, double (&c)[NCH][NV]) {
+                                      const double* rR, int rs, double (&c)[NCH][NV]) {
     J f[NV];
-    face_from_halves<EQ, J>(pp, rL, rR, d, f);
+    face_from_halves<EQ, J>(pp, rL, rR, rs, d, f);
     Derived::comb(A, f, c);
   }
 };
@@ -243,7 +244,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
   // face work split by jet state: part 0 = p-state face flux (J1), part 1 = q-state (J2)
   static constexpr int NFP = 2, FPD = 3 * NV;
   __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo&, int e, int own, int nb,
-                                   int nnode, int, bool plus, int d, int part, double* raw) {
+                                   int nnode, int, bool plus, int d, int part, double* raw,
+                                   int rs) {
     if (part == 0) {
       if (!(fd_step(A) > 0.0)) return;
       NodeState<EQ, J1> so, sn;
@@ -254,7 +256,7 @@ template <int EQ, int NODES> struct ModeJvpFD {
       J1 fp[NV];
       if (plus) face_flux<EQ>(pp, so, sn, d, fp);
       else face_flux<EQ>(pp, sn, so, d, fp);
-      for (int v = 0; v < NV; ++v) { raw[2 * v] = fp[v].v; raw[2 * v + 1] = fp[v].a; }
+      for (int v = 0; v < NV; ++v) { raw[rs * (2 * v)] = fp[v].v; raw[rs * (2 * v + 1)] = fp[v].a; }
     } else {
       NodeState<EQ, J2> so, sn;
       load_w<1>(A, e, own, so.w, false);
@@ -264,21 +266,23 @@ template <int EQ, int NODES> struct ModeJvpFD {
       J2 fq[NV];
       if (plus) face_flux<EQ>(pp, so, sn, d, fq);
       else face_flux<EQ>(pp, sn, so, d, fq);
-      for (int v = 0; v < NV; ++v) { raw[3 * v] = fq[v].v; raw[3 * v + 1] = fq[v].a; raw[3 * v + 2] = fq[v].b; }
+      for (int v = 0; v < NV; ++v) {
+        raw[rs * (3 * v)] = fq[v].v; raw[rs * (3 * v + 1)] = fq[v].a; raw[rs * (3 * v + 2)] = fq[v].b;
+      }
     }
   }
   __device__ static void face_combine(const Args& A, const PhysParams&, int, const double* rp, const double* rq,
-                                      double (&c)[NCH][NV]) {
+                                      int rs, double (&c)[NCH][NV]) {
     const double ew = fd_step(A);
     const double ie = ew > 0.0 ? 1.0 / ew : 0.0;
     for (int v = 0; v < NV; ++v) {
       if (ew > 0.0) {
-        const double q1 = (rp[2 * v] - rq[3 * v]) * ie;
-        const double q2 = (rp[2 * v + 1] - rq[3 * v + 1]) * ie;
-        c[0][v] = fma(A.c2, q2 + rq[3 * v + 2], -A.a1dt * q1);
+        const double q1 = (rp[rs * (2 * v)] - rq[rs * (3 * v)]) * ie;
+        const double q2 = (rp[rs * (2 * v + 1)] - rq[rs * (3 * v + 1)]) * ie;
+        c[0][v] = fma(A.c2, q2 + rq[rs * (3 * v + 2)], -A.a1dt * q1);
         c[1][v] = q1;
       } else {
-        c[0][v] = A.c2 * rq[3 * v + 2];
+        c[0][v] = A.c2 * rq[rs * (3 * v + 2)];
         c[1][v] = 0.0;
       }
     }
@@ -322,7 +326,8 @@ template <int EQ, int NODES> struct ModeJvpLinear {
   // face work split by input: part 0 = F(-a1dt dW + c2 dsigma), part 1 = F(dW)
   static constexpr int NFP = 2, FPD = NV;
   __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
-                                   int nnode, int slot, bool plus, int d, int part, double* raw) {
+                                   int nnode, int slot, bool plus, int d, int part, double* raw,
+                                   int rs) {
     State so, sn;
     load(A, g, e, slot, own, so, false);
     load(A, g, nb, slot, nnode, sn, true);
@@ -331,11 +336,11 @@ template <int EQ, int NODES> struct ModeJvpLinear {
     double f[NV];
     if (plus) face_flux<EQ>(pp, o, q, d, f);
     else face_flux<EQ>(pp, q, o, d, f);
-    for (int v = 0; v < NV; ++v) raw[v] = f[v];
+    for (int v = 0; v < NV; ++v) raw[rs * v] = f[v];
   }
   __device__ static void face_combine(const Args&, const PhysParams&, int, const double* r0, const double* r1,
-                                      double (&c)[NCH][NV]) {
-    for (int v = 0; v < NV; ++v) { c[0][v] = r0[v]; c[1][v] = r1[v]; }
+                                      int rs, double (&c)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) { c[0][v] = r0[rs * v]; c[1][v] = r1[rs * v]; }
   }
   __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {

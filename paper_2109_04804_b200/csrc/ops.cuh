@@ -160,7 +160,8 @@ __host__ __device__ constexpr int half_doubles() {
 }
 
 template <int EQ, class T>
-__device__ __forceinline__ void half_flux(const PhysParams& pp, const NodeState<EQ, T>& s, int d, double* raw) {
+__device__ __forceinline__ void half_flux(const PhysParams& pp, const NodeState<EQ, T>& s, int d, double* raw,
+                                          int rs) {
   constexpr int NV = NVars<EQ>::value, JN = JetN<T>::value;
   T F[NV], lam;
   if constexpr (EQ == 0) {
@@ -175,29 +176,34 @@ __device__ __forceinline__ void half_flux(const PhysParams& pp, const NodeState<
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
-    for (int c = 0; c < JN; ++c) raw[o++] = jget(F[v], c);
+    for (int c = 0; c < JN; ++c) raw[rs * o++] = jget(F[v], c);
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
-    for (int c = 0; c < JN; ++c) raw[o++] = jget(s.w[v], c);
+    for (int c = 0; c < JN; ++c) raw[rs * o++] = jget(s.w[v], c);
 #pragma unroll
-  for (int c = 0; c < JN; ++c) raw[o++] = jget(lam, c);
+  for (int c = 0; c < JN; ++c) raw[rs * o++] = jget(lam, c);
   if constexpr (EQ == 2) {
     T Fv[4];
     viscous_flux(pp, s.w, s.gx, s.gy, d, Fv);
 #pragma unroll
     for (int v = 0; v < 4; ++v)
 #pragma unroll
-      for (int c = 0; c < JN; ++c) raw[o++] = jget(Fv[v], c);
+      for (int c = 0; c < JN; ++c) raw[rs * o++] = jget(Fv[v], c);
   }
 }
 
 // f = face_flux(L, R) from the two halves (same operations, same order)
 template <int EQ, class T>
-__device__ __forceinline__ void face_from_halves(const PhysParams& pp, const double* rL, const double* rR, int d,
-                                                 T* f) {
+__device__ __forceinline__ void face_from_halves(const PhysParams& pp, const double* rL, const double* rR, int rs,
+                                                 int d, T* f) {
   constexpr int NV = NVars<EQ>::value, JN = JetN<T>::value;
-  auto rd = [&](const double* r, int idx) { return jmake<T>(r + idx * JN); };
+  auto rd = [&](const double* r, int idx) {
+    double c[JN];
+#pragma unroll
+    for (int q = 0; q < JN; ++q) c[q] = r[rs * (idx * JN + q)];
+    return jmake<T>(c);
+  };
   T lam;
   if constexpr (EQ == 0) {
     lam = jconst<T>(d == 0 ? (pp.ax >= 0 ? pp.ax : -pp.ax) : (pp.ay >= 0 ? pp.ay : -pp.ay));
@@ -239,7 +245,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
   constexpr int PLANE = (DIM == 2 ? P : 1) * PS;  // one (ch, d, v) plane
   constexpr int FN = DIM == 2 ? P : 1;            // nodes per face
   constexpr int NFN = 2 * DIM * FN;               // face nodes per element
-  double* sRaw = sF + NCH * DIM * NV * PLANE;     // [part][face node][FPD]
+  double* sRaw = sF + NCH * DIM * NV * PLANE;     // [FPD][part][face node] (conflict-free)
   const int i = node % P;
   const int j = DIM == 2 ? node / P : 0;
 
@@ -266,7 +272,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
     const int own = DIM == 1 ? own_edge : (d == 0 ? k * P + own_edge : own_edge * P + k);
     const int nnode = DIM == 1 ? nbr_edge : (d == 0 ? k * P + nbr_edge : nbr_edge * P + k);
     const int nb = nbr_elem(g, e, d, plus ? +1 : -1);
-    Mode::face_part(A, pp, g, e, own, nb, nnode, slot, plus, d, part, sRaw + (size_t)(part * NFN + fn) * FPD);
+    Mode::face_part(A, pp, g, e, own, nb, nnode, slot, plus, d, part, sRaw + part * NFN + fn, NFP * NFN);
   }
   __syncthreads();
   if (active) {
@@ -278,7 +284,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       const bool plus = f & 1;
       const int fn = f * FN + k;
       double cf[NCH][NV];
-      Mode::face_combine(A, pp, d, sRaw + (size_t)fn * FPD, sRaw + (size_t)(NFN + fn) * FPD, cf);
+      Mode::face_combine(A, pp, d, sRaw + fn, sRaw + NFN + fn, NFP * NFN, cf);
       const double sc = (d == 0 ? g.sx : g.sy) * (plus ? g.lhp : -g.lhm);
 #pragma unroll
       for (int c = 0; c < NCH; ++c)

@@ -66,16 +66,17 @@ template <int EQ, int NODES> struct ModeKCol {
   }
   static constexpr int NFP = 2, FPD = half_doubles<EQ, J1>();
   __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
-                                   int nnode, int slot, bool plus, int d, int part, double* raw) {
+                                   int nnode, int slot, bool plus, int d, int part, double* raw,
+                                   int rs) {
     const bool use_own = (part == 0) == plus;
     State st;
     load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
-    half_flux<EQ, J1>(pp, st.s, d, raw);
+    half_flux<EQ, J1>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args&, const PhysParams& pp, int d, const double* rL, const double* rR,
-                                      double (&c)[NCH][NV]) {
+                                      int rs, double (&c)[NCH][NV]) {
     J1 f[NV];
-    face_from_halves<EQ, J1>(pp, rL, rR, d, f);
+    face_from_halves<EQ, J1>(pp, rL, rR, rs, d, f);
     for (int v = 0; v < NV; ++v) c[0][v] = f[v].a;
   }
 };
