@@ -233,10 +233,14 @@ def run_ours(args):
     kernels = {k: {"launches": v[0], "ms": round(v[1], 3), "share": round(v[1] / ms, 4),
                    "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1) if v[1] > 0 else None}
                for k, v in prof.items()}
+    # DRAM traffic per launch: average algorithmic bytes x the DRAM/algorithmic
+    # ratio measured by ncu for this kernel (profiles/ncu_traffic.json)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(dname)
+    if os.path.exists(tp) and dn:
+        ratio = json.load(open(tp)).get(dname)
+        if isinstance(ratio, (int, float)):
+            traffic = round(dbytes / dn * ratio)
 
     # matrix-free FD JVP throughput on the C3 state (second headline of the metric)
     n = ctx.n

@@ -20,11 +20,11 @@ long long g_hbpdc_launches = 0;
 namespace {
 constexpr int GJ_T = 256;    // threads
 constexpr int GJ_NB = 16;    // panel width
-constexpr int GJ_TW = 64;    // column tile of the rank-NB update
+constexpr int GJ_TW = 32;    // column tile of the rank-NB update (2 columns x 16 rows per thread)
 constexpr int GJ_MMAX = 256;
 }
 
-__global__ void __launch_bounds__(GJ_T) gj_kernel(double* __restrict__ Zall, double* __restrict__ Sall, int m,
+__global__ void __launch_bounds__(GJ_T, 3) gj_kernel(double* __restrict__ Zall, double* __restrict__ Sall, int m,
                                                    int* __restrict__ info) {
   __shared__ double Pn[GJ_MMAX * GJ_NB];
   __shared__ double AP[GJ_NB * GJ_TW];
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(GJ_T) gj_kernel(double* __restrict__ Zall, dou
     for (int k = tid; k < nb; k += GJ_T) Pn[piv[c0 + k] * GJ_NB + k] -= 1.0;
     __syncthreads();
     // ---- rank-nb update of every other column: A[:, j] += U A[P, j]
-    const int cg = tid % 16, rg = tid / 16;          // 4 columns x (m/16) rows per thread
+    const int cg = tid % 16, rg = tid / 16;          // 2 columns x (m/16) rows per thread
     for (int t0 = 0; t0 < m; t0 += GJ_TW) {
       for (int idx = tid; idx < nb * GJ_TW; idx += GJ_T) {
         const int k = idx / GJ_TW, jj = idx % GJ_TW;
@@ -125,34 +125,34 @@ __global__ void __launch_bounds__(GJ_T) gj_kernel(double* __restrict__ Zall, dou
       }
       __syncthreads();
       constexpr int RQ = GJ_MMAX / 16;
-      double acc[RQ][4];
+      double acc[RQ][2];
 #pragma unroll
       for (int q = 0; q < RQ; ++q) {
         const int r = rg + 16 * q;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int col = t0 + cg * 4 + cc;
+        for (int cc = 0; cc < 2; ++cc) {
+          const int col = t0 + cg * 2 + cc;
           acc[q][cc] = (r < m && col < m) ? A[(size_t)r * m + col] : 0.0;
         }
       }
       for (int k = 0; k < nb; ++k) {
-        double ap[4];
+        double ap[2];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) ap[cc] = AP[k * GJ_TW + cg * 4 + cc];
+        for (int cc = 0; cc < 2; ++cc) ap[cc] = AP[k * GJ_TW + cg * 2 + cc];
 #pragma unroll
         for (int q = 0; q < RQ; ++q) {
           const int r = rg + 16 * q;
           const double u = r < m ? Pn[r * GJ_NB + k] : 0.0;
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) acc[q][cc] = fma(u, ap[cc], acc[q][cc]);
+          for (int cc = 0; cc < 2; ++cc) acc[q][cc] = fma(u, ap[cc], acc[q][cc]);
         }
       }
 #pragma unroll
       for (int q = 0; q < RQ; ++q) {
         const int r = rg + 16 * q;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int col = t0 + cg * 4 + cc;
+        for (int cc = 0; cc < 2; ++cc) {
+          const int col = t0 + cg * 2 + cc;
           if (r < m && col < m && (col < c0 || col >= c0 + nb)) A[(size_t)r * m + col] = acc[q][cc];
         }
       }
