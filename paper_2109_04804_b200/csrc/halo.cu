@@ -8,7 +8,8 @@
 //
 // Buffer layout: side segments s = 0 (-x), 1 (+x), 2 (-y), 3 (+y); inside a
 // segment [pos][field][var][k], pos = ey (x-sides) or ex (y-sides), k the
-// node index along the face.
+// node index along the face.  A field has nvf "variables" of NODES values per
+// element (nvf = n_v for states; 6 x jet components for NS lifted gradients).
 #include "launch.h"
 
 namespace {
@@ -83,10 +84,10 @@ __global__ void halo_unpack_kernel(HaloArgs H, const double* __restrict__ recv) 
   }
 }
 
-HaloArgs make_args(const HaloLayout& L, int nf) {
+HaloArgs make_args(const HaloLayout& L, int nf, int nvf) {
   HaloArgs H{};
   H.nf = nf;
-  H.nx = L.nx; H.ny = L.ny; H.nE = L.nx * L.ny; H.nv = L.nv; H.P = L.P; H.dim = L.dim;
+  H.nx = L.nx; H.ny = L.ny; H.nE = L.nx * L.ny; H.nv = nvf > 0 ? nvf : L.nv; H.P = L.P; H.dim = L.dim;
   H.nodes = L.dim == 2 ? L.P * L.P : L.P;
   H.m = H.nv * H.nodes;
   const int FN = L.dim == 2 ? L.P : 1;
@@ -102,8 +103,8 @@ HaloArgs make_args(const HaloLayout& L, int nf) {
 
 }  // namespace
 
-void halo_segments(const HaloLayout& L, int nf, size_t off[4], size_t len[4]) {
-  const HaloArgs H = make_args(L, nf);
+void halo_segments(const HaloLayout& L, int nf, size_t off[4], size_t len[4], int nvf) {
+  const HaloArgs H = make_args(L, nf, nvf);
   const int FN = L.dim == 2 ? L.P : 1;
   for (int s = 0; s < 4; ++s) {
     off[s] = H.off[s];
@@ -112,9 +113,9 @@ void halo_segments(const HaloLayout& L, int nf, size_t off[4], size_t len[4]) {
 }
 
 cudaError_t launch_halo_pack(const HaloLayout& L, int nf, const double* const* src, double* send,
-                             cudaStream_t st) {
+                             cudaStream_t st, int nvf) {
   if (nf < 1 || nf > HALO_MAX_FIELDS) return cudaErrorInvalidValue;
-  HaloArgs H = make_args(L, nf);
+  HaloArgs H = make_args(L, nf, nvf);
   for (int f = 0; f < nf; ++f) H.src[f] = src[f];
   if (H.total == 0) return cudaSuccess;
   const int grid = (int)std::min<size_t>((H.total + 255) / 256, 1184);
@@ -124,9 +125,9 @@ cudaError_t launch_halo_pack(const HaloLayout& L, int nf, const double* const* s
 }
 
 cudaError_t launch_halo_unpack(const HaloLayout& L, int nf, const double* recv, double* const* dst,
-                               cudaStream_t st) {
+                               cudaStream_t st, int nvf) {
   if (nf < 1 || nf > HALO_MAX_FIELDS) return cudaErrorInvalidValue;
-  HaloArgs H = make_args(L, nf);
+  HaloArgs H = make_args(L, nf, nvf);
   for (int f = 0; f < nf; ++f) H.dst[f] = dst[f];
   if (H.total == 0) return cudaSuccess;
   const int grid = (int)std::min<size_t>((H.total + 255) / 256, 1184);

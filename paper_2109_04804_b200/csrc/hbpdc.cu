@@ -127,6 +127,7 @@ struct hbpdc_ctx {
   int nbr[4] = {0, 0, 0, 0};       // neighbour ranks -x, +x, -y, +y
   HaloLayout hl{};
   double *gW = nullptr, *gS = nullptr, *gdW = nullptr, *gdS = nullptr, *gWb = nullptr;  // ghosts
+  double *gG0 = nullptr, *gG1 = nullptr;                  // NS: ghost lifted gradients (second halo)
   double *hsend = nullptr, *hrecv = nullptr;
   bool halo() const { return hl.active[0] || hl.active[2]; }
   int debug_sync = 0;              // HBPDC_DEBUG_SYNC=1: synchronise + check after every launch group
@@ -227,16 +228,16 @@ hbpdc_status allreduce(hbpdc_ctx* c, double* d, int n) {
 }
 
 // halo exchange of nf fields into their ghost copies
-hbpdc_status halo_exchange(hbpdc_ctx* c, int nf, const double* const* src, double* const* dst) {
+hbpdc_status halo_exchange(hbpdc_ctx* c, int nf, const double* const* src, double* const* dst, int nvf = 0) {
   size_t off[4], len[4];
-  halo_segments(c->hl, nf, off, len);
-  CK(launch_halo_pack(c->hl, nf, src, c->hsend, c->stream));
+  halo_segments(c->hl, nf, off, len, nvf);
+  CK(launch_halo_pack(c->hl, nf, src, c->hsend, c->stream, nvf));
   CKS(dbg_sync(c, "halo pack"));
   std::string e;
   if (c->comm->halo(c->hsend, c->hrecv, off, len, c->nbr, c->hl.active, c->stream, e))
     return fail(c, HBPDC_E_NCCL, e);
   CKS(dbg_sync(c, "halo transport"));
-  CK(launch_halo_unpack(c->hl, nf, c->hrecv, dst, c->stream));
+  CK(launch_halo_unpack(c->hl, nf, c->hrecv, dst, c->stream, nvf));
   CKS(dbg_sync(c, "halo unpack"));
   return HBPDC_OK;
 }
@@ -270,11 +271,25 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
     A.gS = c->gS; A.gdW = c->gdW; A.gdS = c->gdS;
   }
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {
+    // BR1: lift the jet state(s), then (partitioned) exchange the lifted
+    // gradients' face traces -- the second halo of the radius-2 stencil
     CK(launch_lift(k, 0, c->cfg, c->geo, A, c->lift0));
     A.G0 = c->lift0;
     if (k == OP_JVP_FD) {
       CK(launch_lift(k, 1, c->cfg, c->geo, A, c->lift1));
       A.G1 = c->lift1;
+    }
+    if (c->halo()) {
+      const double* s0[1] = {c->lift0};
+      double* d0[1] = {c->gG0};
+      CKS(halo_exchange(c, 1, s0, d0, 6 * lift_jet_components(k, 0)));
+      A.gG0 = c->gG0;
+      if (k == OP_JVP_FD) {
+        const double* s1[1] = {c->lift1};
+        double* d1[1] = {c->gG1};
+        CKS(halo_exchange(c, 1, s1, d1, 6 * lift_jet_components(k, 1)));
+        A.gG1 = c->gG1;
+      }
     }
   }
   CK(launch_op(k, c->cfg, k == OP_R1ABS ? c->geo_abs : c->geo, A));
@@ -403,6 +418,8 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
     // then each chunk is copied to Z and inverted back into S
     auto period = [](int n) { for (int P = 3; P <= n; ++P) if (n % P == 0) return P; return n; };
     const int Px = period(c->nxl), Py = period(c->nyl);
+    if (Px < 3 || Py < 3)    // two seeded elements of one colour must be > 2 elements apart
+      return fail(c, HBPDC_E_ARG, "Navier-Stokes BJ_ext needs local element counts with a divisor >= 3");
     for (int cy = 0; cy < Py; ++cy)
       for (int cx = 0; cx < Px; ++cx)
         for (int col = 0; col < c->m; ++col) {
@@ -1053,7 +1070,14 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     CKS(dalloc(c, &c->gWb, ng));
     size_t off[4], len[4];
     halo_segments(c->hl, HALO_MAX_FIELDS, off, len);
-    const size_t hb = off[3] + len[3];
+    size_t hb = off[3] + len[3];
+    if (c->pb.equation == HBPDC_NAVIER_STOKES) {
+      const size_t ngg = (size_t)(c->pb.dim == 2 ? 2 * (c->nxl + c->nyl) : 2) * 6 * 4 * c->nodes;
+      CKS(dalloc(c, &c->gG0, ngg));
+      CKS(dalloc(c, &c->gG1, ngg));
+      halo_segments(c->hl, 1, off, len, 6 * 4);          // lifted gradients, hyper-dual jets
+      hb = std::max(hb, off[3] + len[3]);
+    }
     CKS(dalloc(c, &c->hsend, hb));
     CKS(dalloc(c, &c->hrecv, hb));
   }
@@ -1105,8 +1129,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->dim == 1 && c->ds.py != 1) return bad("1D partitions need py = 1");
   if (pb->nx % c->ds.px || (pb->dim == 2 && pb->ny % c->ds.py)) return bad("px must divide nx and py divide ny");
   const bool halo = c->ds.nranks > 1 || c->ds.force_halo;
-  if (halo && pb->equation == HBPDC_NAVIER_STOKES)
-    return bad("the element partition of Navier-Stokes (two-hop BR1 halo) is not implemented yet");
+
   if (op->gmres_restart < 1 || op->krylov_max_per_newton < 1 || op->newton_max < 0) return bad("bad solver options");
   c->nv = pb->equation == HBPDC_ADVECTION ? 1 : 4;
   c->P = pb->N + 1;

@@ -20,6 +20,7 @@ struct OpArgs {
   double* out2;
   const double* G0;     // NS lifted gradients of jet state 0
   const double* G1;     // NS lifted gradients of jet state 1
+  const double *gG0, *gG1;   // their ghost copies (halo of the lifted gradients)
   double a1dt, c2;
   double epsw;          // FD step for the W direction (<= 0: quotient is 0)
   const double* d_epsw; // if non-NULL, the FD step is read from device memory
@@ -31,8 +32,12 @@ struct OpArgs {
 __device__ __forceinline__ double fd_step(const OpArgs& A) { return A.d_epsw ? *A.d_epsw : A.epsw; }
 
 template <int EQ, class T, int NODES>
-__device__ __forceinline__ void ld_state(const double* G, int e, int node, NodeState<EQ, T>& s) {
-  if constexpr (EQ == 2) load_grads<T, NODES>(G, e, node, s.gx, s.gy);
+__device__ __forceinline__ void ld_state(const double* G, const double* Gg, int nE, int e, int node,
+                                         NodeState<EQ, T>& s) {
+  if constexpr (EQ == 2) {
+    if (e < nE) load_grads<T, NODES>(G, e, node, s.gx, s.gy);
+    else load_grads<T, NODES>(Gg, e - nE, node, s.gx, s.gy);
+  }
 }
 
 #define IDX(e, v, node) ((size_t)(e) * A.m + (v) * NODES + (node))
@@ -49,7 +54,7 @@ struct OneJetMode {
   struct State { NodeState<EQ, J> s; };
   __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
     Derived::template load_w<0>(A, e, node, st.s.w, nbr);
-    ld_state<EQ, J, NODES>(A.G0, e, node, st.s);
+    ld_state<EQ, J, NODES>(A.G0, A.gG0, A.nE, e, node, st.s);
   }
   template <int DIM>
   __device__ static void vol(const Args& A, const PhysParams& pp, const State& st, double (&c)[DIM][NCH][NV]) {
@@ -201,8 +206,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
   __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
     load_w<0>(A, e, node, st.p.w, nbr);
     load_w<1>(A, e, node, st.q.w, nbr);
-    ld_state<EQ, J1, NODES>(A.G0, e, node, st.p);
-    ld_state<EQ, J2, NODES>(A.G1, e, node, st.q);
+    ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, e, node, st.p);
+    ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, e, node, st.q);
   }
   __device__ static void comb(const Args& A, const J1* Fp, const J2* Fq, double (&c)[NCH][NV]) {
     const double ew = fd_step(A);
@@ -251,8 +256,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
       NodeState<EQ, J1> so, sn;
       load_w<0>(A, e, own, so.w, false);
       load_w<0>(A, nb, nnode, sn.w, true);
-      ld_state<EQ, J1, NODES>(A.G0, e, own, so);
-      ld_state<EQ, J1, NODES>(A.G0, nb, nnode, sn);
+      ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, e, own, so);
+      ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, nb, nnode, sn);
       J1 fp[NV];
       if (plus) face_flux<EQ>(pp, so, sn, d, fp);
       else face_flux<EQ>(pp, sn, so, d, fp);
@@ -261,8 +266,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
       NodeState<EQ, J2> so, sn;
       load_w<1>(A, e, own, so.w, false);
       load_w<1>(A, nb, nnode, sn.w, true);
-      ld_state<EQ, J2, NODES>(A.G1, e, own, so);
-      ld_state<EQ, J2, NODES>(A.G1, nb, nnode, sn);
+      ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, e, own, so);
+      ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, nb, nnode, sn);
       J2 fq[NV];
       if (plus) face_flux<EQ>(pp, so, sn, d, fq);
       else face_flux<EQ>(pp, sn, so, d, fq);

@@ -19,7 +19,10 @@ import pytest
 
 from oracle import dgsem, hbpc, implicit
 from paper_2109_04804_b200 import configs, hbpdc, inputs
-from gpu_common import adv_ic, euler_ic, make_pair, rel, to_gpu, to_np, SEED
+from gpu_common import adv_ic, euler_ic, make_pair, ns_ic, rel, to_gpu, to_np, SEED
+
+TWO_PI = 2 * np.pi
+NS_MU = 0.05
 
 pytestmark = pytest.mark.gpu
 
@@ -52,10 +55,15 @@ def _run_threads(fns):
     return res
 
 
+def _ns_kw(kind):
+    return dict(bounds=(0.0, TWO_PI, 0.0, TWO_PI), mu=NS_MU) if kind == "navier_stokes" else {}
+
+
 def _rank_contexts(kind, N, nx, ny, px, py, group, **kw):
     import torch
     dim = 1 if ny is None else 2
     a = (1.0, 0.0) if dim == 1 else (1.0, -0.6)
+    kw.update(_ns_kw(kind))
     out = []
     for r in range(px * py):
         s = torch.cuda.Stream()
@@ -72,6 +80,10 @@ CASES = [
     ("euler", 4, 6, 4, 3, 2),
     ("advection", 3, 4, 4, 2, 2),
     ("advection", 3, 8, None, 2, 1),
+    # Navier-Stokes (BR1): second halo of the lifted gradients; local grids
+    # keep a colouring period >= 3 for the two-hop BJ_ext blocks
+    ("navier_stokes", 2, 6, 6, 2, 2),
+    ("navier_stokes", 3, 8, 4, 2, 1),
 ]
 
 
@@ -80,8 +92,8 @@ def test_loopback_operators_bitwise(case):
     import torch
     kind, N, nx, ny, px, py = case
     dim = 1 if ny is None else 2
-    d, ctx1 = make_pair(kind, N, nx, ny, a=(1.0, 0.0) if dim == 1 else (1.0, -0.6))
-    W = adv_ic(d, SEED + 31) if kind == "advection" else euler_ic(d, SEED + 31)
+    d, ctx1 = make_pair(kind, N, nx, ny, a=(1.0, 0.0) if dim == 1 else (1.0, -0.6), **_ns_kw(kind))
+    W = {"advection": adv_ic, "euler": euler_ic, "navier_stokes": ns_ic}[kind](d, SEED + 31)
     sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 32))
     dW = inputs.random_field(d.n, SEED + 33, unit_norm=True)
     ds = inputs.random_field(d.n, SEED + 34, unit_norm=True)
