@@ -246,6 +246,49 @@ template <int EQ, int NODES> struct ModeJvpFD {
       for (int d = 0; d < DIM; ++d) comb(A, Fp[d], Fq[d], c[d]);
     }
   }
+  // volume fluxes in two passes (the two jet states are never live together):
+  // pass 0 leaves the p-state flux (tangent, value) in the output slots, pass 1
+  // combines them with the q-state flux into the channels (same arithmetic as comb)
+  static constexpr int VOL_PASSES = 2;
+  template <int DIM>
+  __device__ static void vol_pass0(const Args& A, const PhysParams& pp, int e, int node,
+                                   double (&t)[DIM][NCH][NV]) {
+    if (!(fd_step(A) > 0.0)) return;
+    NodeState<EQ, J1> p;
+    load_w<0>(A, e, node, p.w, false);
+    ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, e, node, p);
+    J1 F[DIM][NV];
+    vol_flux_all<EQ, DIM>(pp, p, F);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) { t[d][0][v] = F[d][v].a; t[d][1][v] = F[d][v].v; }
+  }
+  template <int DIM>
+  __device__ static void vol_pass1(const Args& A, const PhysParams& pp, int e, int node,
+                                   double (&t)[DIM][NCH][NV]) {
+    NodeState<EQ, J2> q;
+    load_w<1>(A, e, node, q.w, false);
+    ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, e, node, q);
+    J2 F[DIM][NV];
+    vol_flux_all<EQ, DIM>(pp, q, F);
+    const double ew = fd_step(A);
+    const double ie = ew > 0.0 ? 1.0 / ew : 0.0;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if (ew > 0.0) {
+          const double q1 = (t[d][1][v] - F[d][v].v) * ie;
+          const double q2 = (t[d][0][v] - F[d][v].a) * ie;
+          t[d][0][v] = fma(A.c2, q2 + F[d][v].b, -A.a1dt * q1);
+          t[d][1][v] = q1;
+        } else {
+          t[d][0][v] = A.c2 * F[d][v].b;
+          t[d][1][v] = 0.0;
+        }
+      }
+  }
   // face work split by jet state: part 0 = p-state face flux (J1), part 1 = q-state (J2)
   static constexpr int NFP = 2, FPD = 3 * NV;
   __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo&, int e, int own, int nb,

@@ -19,6 +19,7 @@
 // evaluations).  Navier-Stokes adds BR1 lifted gradients (lift_kernel), read
 // back as part of the node state.
 #pragma once
+#include <type_traits>
 #include <cuda_runtime.h>
 #include "physics.cuh"
 
@@ -219,6 +220,16 @@ __device__ __forceinline__ void face_from_halves(const PhysParams& pp, const dou
   }
 }
 
+// argument packs carrying a device-resident FD step (OpArgs::d_epsw)
+template <class A, class = void> struct HasDevEps : std::false_type {};
+template <class A> struct HasDevEps<A, std::void_t<decltype(A::d_epsw)>> : std::true_type {};
+
+// modes may evaluate their volume fluxes in two passes (VOL_PASSES = 2)
+template <class M, class = void> struct VolPasses { static constexpr int value = 1; };
+template <class M> struct VolPasses<M, std::void_t<decltype(M::VOL_PASSES)>> {
+  static constexpr int value = M::VOL_PASSES;
+};
+
 // ---- the element evaluation (one slot, one node per thread) --------------------
 // Shared scratch per slot: slot_doubles<...>() = volume-flux planes
 // NCH*DIM*NV*P*(P+1) + face parts NFP*NFN*FPD.
@@ -240,7 +251,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
                                           double* sF, double (&out)[Mode::NCH][NVars<EQ>::value]) {
   constexpr int NV = NVars<EQ>::value;
   constexpr int NCH = Mode::NCH;
-  constexpr int NFP = Mode::NFP, FPD = Mode::FPD;
+  constexpr int NFP = Mode::NFP;
   constexpr int PS = P + 1;                       // padded row stride (bank conflicts)
   constexpr int PLANE = (DIM == 2 ? P : 1) * PS;  // one (ch, d, v) plane
   constexpr int FN = DIM == 2 ? P : 1;            // nodes per face
@@ -250,16 +261,36 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
   const int j = DIM == 2 ? node / P : 0;
 
   if (active) {
-    typename Mode::State st;
-    Mode::load(A, g, e, slot, node, st, false);
-    double cf[DIM][NCH][NV];
-    Mode::template vol<DIM>(A, pp, st, cf);
+    auto put = [&](const double (&cf)[DIM][NCH][NV]) {
 #pragma unroll
-    for (int d = 0; d < DIM; ++d)
+      for (int d = 0; d < DIM; ++d)
 #pragma unroll
-      for (int c = 0; c < NCH; ++c)
+        for (int c = 0; c < NCH; ++c)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i] = cf[d][c][v];
+          for (int v = 0; v < NV; ++v) sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i] = cf[d][c][v];
+    };
+    if constexpr (VolPasses<Mode>::value == 2) {
+      // two jet states evaluated one after the other, the first parked in this
+      // node's own output slots (no barrier: the same thread reads them back)
+      double cf[DIM][NCH][NV];
+      Mode::template vol_pass0<DIM>(A, pp, e, node, cf);
+      put(cf);
+      double cg[DIM][NCH][NV];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) cg[d][c][v] = sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i];
+      Mode::template vol_pass1<DIM>(A, pp, e, node, cg);
+      put(cg);
+    } else {
+      typename Mode::State st;
+      Mode::load(A, g, e, slot, node, st, false);
+      double cf[DIM][NCH][NV];
+      Mode::template vol<DIM>(A, pp, st, cf);
+      put(cf);
+    }
   }
   constexpr int NODES = DIM == 2 ? P * P : P;
   for (int it = node; active && it < NFP * NFN; it += NODES) {
@@ -277,9 +308,13 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
   __syncthreads();
   if (active) {
     // surface terms of this node's face(s), canonical flux with the outward sign:
-    // s_d (f*_+ lhat_N(1) - f*_- lhat_0(-1))
-    double fs[4][NCH][NV];
-    auto face_term = [&](int f, int k) {
+    // s_d (f*_+ lhat_N(1) - f*_- lhat_0(-1)), summed in the order +x, -x, +y, -y
+    double sf[NCH][NV];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sf[c][v] = 0.0;
+    auto add_face = [&](int f, int k) {
       const int d = f >> 1;
       const bool plus = f & 1;
       const int fn = f * FN + k;
@@ -289,14 +324,12 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) fs[f][c][v] = sc * cf[c][v];
+        for (int v = 0; v < NV; ++v) sf[c][v] += __dmul_rn(sc, cf[c][v]);
     };
-    const bool f0 = i == 0, f1 = i == P - 1;
-    const bool f2 = DIM == 2 && j == 0, f3 = DIM == 2 && j == P - 1;
-    if (f1) face_term(1, j);
-    if (f0) face_term(0, j);
-    if (f3) face_term(3, i);
-    if (f2) face_term(2, i);
+    if (i == P - 1) add_face(1, j);
+    if (i == 0) add_face(0, j);
+    if (DIM == 2 && j == P - 1) add_face(3, i);
+    if (DIM == 2 && j == 0) add_face(2, i);
     double Dr[P], Dc[P];
 #pragma unroll
     for (int l = 0; l < P; ++l) {
@@ -319,12 +352,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
           for (int l = 0; l < P; ++l) ay = fma(Dc[l], Fy[l * PS], ay);
           acc = fma(g.sy, ay, acc);
         }
-        double surf = 0.0;
-        if (f1) surf += fs[1][c][v];
-        if (f0) surf += fs[0][c][v];
-        if (f3) surf += fs[3][c][v];
-        if (f2) surf += fs[2][c][v];
-        out[c][v] = -(acc + surf);
+        out[c][v] = -(acc + sf[c][v]);
       }
   }
 }
@@ -352,8 +380,13 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g) {
   const int e = blockIdx.x * EPB + slot;
   const bool active = e < g.nE;
   double out[Mode::NCH][NV];
-  eval_slot<EQ, DIM, P, Mode>(A, pp, g, e, slot, node, active, sF + slot * SLOT, out);
-  if (active) Mode::epilogue(A, e, node, out);
+  typename Mode::Args Al = A;
+  if constexpr (HasDevEps<typename Mode::Args>::value) {
+    // the FD step lives in device memory (norm computed on the device): read it once
+    if (Al.d_epsw) { Al.epsw = __ldg(Al.d_epsw); Al.d_epsw = nullptr; }
+  }
+  eval_slot<EQ, DIM, P, Mode>(Al, pp, g, e, slot, node, active, sF + slot * SLOT, out);
+  if (active) Mode::epilogue(Al, e, node, out);
 }
 
 // ---- BR1 lifting (eq:Lifting P:855, central value P:861; reading R19) -----------
