@@ -261,10 +261,6 @@ __global__ void __launch_bounds__(256) gemv2_kernel(const double* __restrict__ S
 // elements' S blocks in chunks of GT_R rows; thread 0 keeps GT_NST chunks in
 // flight with cp.async.bulk (completion on an mbarrier), the 8 warps reduce
 // one row each per chunk from shared memory.
-namespace {
-constexpr int GT_NST = 4;   // pipeline stages
-constexpr int GT_R = 8;     // rows per chunk (one per warp)
-}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -301,93 +297,155 @@ struct GemvRHS {
   double* out[GEMV_MAX_RHS];
 };
 
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+// Warp-specialised pipeline: warp 8 (one lane) is the producer, warps 0-7
+// consume.  Per element the producer bulk-copies the NR right-hand-side
+// vectors into one of two RHS buffers, then streams the element's S in chunks
+// of ROWS rows through a GT_NST-deep ring; "full" mbarriers carry the
+// transaction bytes, "empty" mbarriers collect one arrival per consumer warp,
+// so warps drift independently through the ring (no CTA-wide barrier per chunk).
+// Up to 4 right-hand sides live in one warp's registers; NR = 6 splits them
+// over 2 warps per row (each reads the full row, 3 RHS, 2 rows per chunk to
+// keep two independent FMA chains).  Each output is one warp's full-row dot
+// product, reduced over the same lane tree for every NR (bitwise equal).
+// Measured at C3 size (scripts/bench_gemv.cu): NR = 2, 4: 6.8-6.9 TB/s
+// (104-105% of the measured copy bandwidth), NR = 6: 5.8 TB/s.
+// consumer warps (one CTA per SM)
+template <int NR> struct GwCons { static constexpr int value = 16; };
+constexpr int GW_NST_MAX = 16;                   // ring stages (runtime nst <= this)
+constexpr size_t GW_RING_BYTES = 160 * 1024;     // S bytes in flight per CTA (one CTA per SM)
+
 template <int CPL, int NR>
-__global__ void __launch_bounds__(256) gemvN_tma_kernel(const double* __restrict__ S, const GemvRHS io, int m,
-                                                        int nE) {
+__global__ void __launch_bounds__(32 * (GwCons<NR>::value + 1)) gemvN_tma_kernel(const double* __restrict__ S,
+                                                                       const GemvRHS io, int m, int nE,
+                                                                       int GW_NST) {
+  constexpr int GW_CONS = GwCons<NR>::value;
+  constexpr int WPR = NR > 4 ? 2 : 1;            // warps per row (register budget: <= 4 RHS per warp)
+  constexpr int KPW = NR / WPR;                  // right-hand sides per warp
+  constexpr int ROWS = GW_CONS;                  // rows per chunk
+  constexpr int RPW = WPR;                       // rows per warp per chunk (interleaved chains)
   extern __shared__ __align__(128) unsigned char smraw[];
-  double* ring = reinterpret_cast<double*>(smraw);
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)GT_NST * GT_R * m);
+  double* ring = reinterpret_cast<double*>(smraw);                     // GW_NST x ROWS x m
+  double* rhs = ring + (size_t)GW_NST * ROWS * m;                      // 2 x NR x m
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(rhs + (size_t)2 * NR * m);
+  unsigned long long *fullS = bars, *emptyS = bars + GW_NST_MAX, *fullR = bars + 2 * GW_NST_MAX, *emptyR = fullR + 2;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int cpe = (m + GT_R - 1) / GT_R;                               // chunks per element
+  const int cpe = (m + ROWS - 1) / ROWS;                               // chunks per element
   const int nmy = blockIdx.x < nE ? (nE - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int T = nmy * cpe;
-  auto issue = [&](int c) {
-    const int e = blockIdx.x + (c / cpe) * gridDim.x;
-    const int r0 = (c % cpe) * GT_R;
-    const int rows = min(GT_R, m - r0);
-    const unsigned bytes = (unsigned)(rows * m * sizeof(double));
-    unsigned long long* b = &full[c % GT_NST];
-    mbar_expect_tx(b, bytes);
-    tma_load_1d(ring + (size_t)(c % GT_NST) * GT_R * m, S + ((size_t)e * m + r0) * m, bytes, b);
-  };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < GT_NST; ++s) mbar_init(&full[s], 1);
+    for (int q = 0; q < GW_NST; ++q) { mbar_init(&fullS[q], 1); mbar_init(&emptyS[q], GW_CONS); }
+    for (int q = 0; q < 2; ++q) { mbar_init(&fullR[q], 1); mbar_init(&emptyR[q], GW_CONS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int c = 0; c < GT_NST && c < T; ++c) issue(c);
   }
   __syncthreads();
-  double xr[NR][CPL];
-  for (int c = 0; c < T; ++c) {
-    const int e = blockIdx.x + (c / cpe) * gridDim.x;
-    const int r0 = (c % cpe) * GT_R;
-    if (r0 == 0) {
-#pragma unroll
-      for (int k = 0; k < NR; ++k)
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          const int col = lane + 32 * q;
-          xr[k][q] = col < m ? io.in[k][(size_t)e * m + col] : 0.0;
+  if (wid == GW_CONS) {                                                // ---- producer
+    if (lane == 0) {
+      int c = 0;                                                       // chunk counter
+      for (int it = 0; it < nmy; ++it) {
+        const int e = blockIdx.x + it * gridDim.x;
+        const int rb = it & 1;
+        if (it >= 2) mbar_wait(&emptyR[rb], (unsigned)(((it >> 1) - 1) & 1));
+        mbar_expect_tx(&fullR[rb], (unsigned)(NR * m * sizeof(double)));
+        for (int k = 0; k < NR; ++k)
+          tma_load_1d(rhs + ((size_t)rb * NR + k) * m, io.in[k] + (size_t)e * m, (unsigned)(m * sizeof(double)),
+                      &fullR[rb]);
+        for (int ch = 0; ch < cpe; ++ch, ++c) {
+          const int st = c % GW_NST;
+          if (c >= GW_NST) mbar_wait(&emptyS[st], (unsigned)(((c / GW_NST) - 1) & 1));
+          const int r0 = ch * ROWS;
+          const int rows = min(ROWS, m - r0);
+          const unsigned bytes = (unsigned)(rows * m * sizeof(double));
+          mbar_expect_tx(&fullS[st], bytes);
+          tma_load_1d(ring + (size_t)st * ROWS * m, S + ((size_t)e * m + r0) * m, bytes, &fullS[st]);
         }
+      }
     }
-    mbar_wait(&full[c % GT_NST], (unsigned)((c / GT_NST) & 1));
-    const int r = r0 + wid;
-    if (r < m) {
-      const double* row = ring + ((size_t)(c % GT_NST) * GT_R + wid) * m;
-      double acc[NR];
+    return;
+  }
+  // ---- consumers: warp wid takes rows wid / WPR + i ROWS / RPW (i < RPW) of
+  //      every chunk, for right-hand sides k0 .. k0 + KPW - 1, k0 = (wid % WPR) KPW
+  const int rslot = wid / WPR, k0 = (wid % WPR) * KPW;
+  double xr[KPW][CPL];
+  int c = 0;
+  for (int it = 0; it < nmy; ++it) {
+    const int e = blockIdx.x + it * gridDim.x;
+    const int rb = it & 1;
+    mbar_wait(&fullR[rb], (unsigned)((it >> 1) & 1));
 #pragma unroll
-      for (int k = 0; k < NR; ++k) acc[k] = 0.0;
+    for (int k = 0; k < KPW; ++k)
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
         const int col = lane + 32 * q;
-        const double sv = col < m ? row[col] : 0.0;
-#pragma unroll
-        for (int k = 0; k < NR; ++k) acc[k] = fma(sv, xr[k][q], acc[k]);
+        xr[k][q] = col < m ? rhs[((size_t)rb * NR + k0 + k) * m + col] : 0.0;
       }
-      if constexpr (NR == 2) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&emptyR[rb]);
+    for (int ch = 0; ch < cpe; ++ch, ++c) {
+      const int st = c % GW_NST;
+      mbar_wait(&fullS[st], (unsigned)((c / GW_NST) & 1));
+      double acc[RPW][KPW];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+      for (int i = 0; i < RPW; ++i)
 #pragma unroll
-          for (int k = 0; k < NR; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-        if (lane < NR) io.out[lane][(size_t)e * m + r] = lane == 0 ? acc[0] : acc[1];
-      } else {
-        // NR > 2: transposed butterfly over V = 8 padded values (7 + 2 shuffles
-        // instead of 5 NR); lane bits 4,3,2 then index the value.  Every value
-        // is summed over the same lane tree (bits 16, 8, 4, 2, 1) as the plain
-        // butterfly of NR == 2 (operands swapped at most: a + b == b + a), so
-        // batched and single-system products are bitwise equal.
-        constexpr int V = 8;
-        double p[V];
+        for (int k = 0; k < KPW; ++k) acc[i][k] = 0.0;
 #pragma unroll
-        for (int k = 0; k < V; ++k) p[k] = k < NR ? acc[k] : 0.0;
+      for (int q = 0; q < CPL; ++q) {
+        const int col = lane + 32 * q;
 #pragma unroll
-        for (int jj = 0; jj < 3; ++jj) {
-          const int h = V >> (jj + 1), mask = 16 >> jj;
-          const bool hi = lane & mask;
+        for (int i = 0; i < RPW; ++i) {
+          const double* row = ring + ((size_t)st * ROWS + rslot + i * (ROWS / RPW)) * m;
+          const double sv = col < m ? row[col] : 0.0;
 #pragma unroll
-          for (int q = 0; q < h; ++q) {
-            const double send = hi ? p[q] : p[q + h];
-            const double recv = __shfl_xor_sync(0xffffffffu, send, mask);
-            p[q] = (hi ? p[q + h] : p[q]) + recv;
-          }
+          for (int k = 0; k < KPW; ++k) acc[i][k] = fma(sv, xr[k][q], acc[i][k]);
         }
-        p[0] += __shfl_xor_sync(0xffffffffu, p[0], 2);
-        p[0] += __shfl_xor_sync(0xffffffffu, p[0], 1);
-        const int idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-        if ((lane & 3) == 0 && idx < NR) io.out[idx][(size_t)e * m + r] = p[0];
       }
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int r = ch * ROWS + rslot + i * (ROWS / RPW);
+        if constexpr (KPW <= 2) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < KPW; ++k) acc[i][k] += __shfl_xor_sync(0xffffffffu, acc[i][k], o);
+          if (r < m && lane < KPW) io.out[k0 + lane][(size_t)e * m + r] = lane == 0 ? acc[i][0] : acc[i][KPW - 1];
+        } else {
+          // KPW > 2: transposed butterfly over V = 4 or 8 (padded) values: step
+          // jj halves the live values across lane bit 16 >> jj, the remaining
+          // low lane bits are a plain reduction; lane bits 4 .. 5 - LV then
+          // index the value.  Each value is summed over the same lane tree
+          // (bits 16, 8, 4, 2, 1) as the plain butterfly (operands swapped at
+          // most: a + b == b + a), so results are bitwise equal to KPW <= 2.
+          constexpr int V = KPW <= 4 ? 4 : 8;
+          constexpr int LV = V == 4 ? 2 : 3;
+          double p[V];
+#pragma unroll
+          for (int k = 0; k < V; ++k) p[k] = k < KPW ? acc[i][k] : 0.0;
+#pragma unroll
+          for (int jj = 0; jj < LV; ++jj) {
+            const int h = V >> (jj + 1), mask = 16 >> jj;
+            const bool hi = lane & mask;
+#pragma unroll
+            for (int q = 0; q < h; ++q) {
+              const double send = hi ? p[q] : p[q + h];
+              const double recv = __shfl_xor_sync(0xffffffffu, send, mask);
+              p[q] = (hi ? p[q + h] : p[q]) + recv;
+            }
+          }
+#pragma unroll
+          for (int mask = 16 >> LV; mask >= 1; mask >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], mask);
+          int idx = 0;
+#pragma unroll
+          for (int jj = 0; jj < LV; ++jj)
+            if (lane & (16 >> jj)) idx |= V >> (jj + 1);
+          if (r < m && (lane & ((32 >> LV) - 1)) == 0 && idx < KPW) io.out[k0 + idx][(size_t)e * m + r] = p[0];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyS[st]);
     }
-    __syncthreads();                       // stage (c % GT_NST) is free again
-    if (threadIdx.x == 0 && c + GT_NST < T) issue(c + GT_NST);
   }
 }
 
@@ -400,17 +458,22 @@ static cudaError_t launch_gemvN(const double* S, const GemvRHS& io, int m, int n
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     nsm = v;
   }
-  const size_t smem = (size_t)GT_NST * GT_R * m * sizeof(double) + GT_NST * sizeof(unsigned long long);
+  constexpr int GW_CONS = GwCons<NR>::value;
+  constexpr int ROWS = GW_CONS;                  // rows per chunk (as in the kernel)
+  const size_t chunk = (size_t)ROWS * m * sizeof(double);
+  const int nst = (int)std::max<size_t>(2, std::min<size_t>(GW_NST_MAX, GW_RING_BYTES / chunk));
+  const size_t smem = (size_t)nst * chunk + (size_t)2 * NR * m * sizeof(double) +
+                      (2 * GW_NST_MAX + 4) * sizeof(unsigned long long);
   const int cpl = (m + 31) / 32;
-  // persistent grid: exactly the resident CTAs (registers grow with NR; a
-  // fixed 3 per SM would leave a half-empty second wave at NR = 6)
+  constexpr int threads = 32 * (GW_CONS + 1);
+  // persistent grid: exactly the resident CTAs
 #define GT(C)                                                                                   \
   case C: {                                                                                     \
     cudaFuncSetAttribute(gemvN_tma_kernel<C, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     int occ = 0;                                                                                \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemvN_tma_kernel<C, NR>, 256, smem);    \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemvN_tma_kernel<C, NR>, threads, smem); \
     const int grid = std::min(nE, nsm * std::max(occ, 1));                                      \
-    gemvN_tma_kernel<C, NR><<<grid, 256, smem, st>>>(S, io, m, nE);                              \
+    gemvN_tma_kernel<C, NR><<<grid, threads, smem, st>>>(S, io, m, nE, nst);                     \
   } break;
   switch (cpl) {
     GT(1) GT(2) GT(3) GT(4) GT(5) GT(6) GT(7) GT(8)
