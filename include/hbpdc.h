@@ -94,6 +94,11 @@ typedef struct {
                                   step, sharing one BJ_ext S pass per Arnoldi step
                                   (they are independent, eq:corrector P:119-122;
                                   SURVEY NEXT-1).  Bitwise equal results to 0.      */
+  int gmres_sstep;             /* Arnoldi schedule: 0/1 = DCGS2 (one JVP per block,
+                                  2 passes over the basis per iteration); s = 2, 4, 8:
+                                  s-step blocks (s Newton-basis powers, then block CGS2
+                                  + CholQR2: 4 passes over the basis per s iterations).
+                                  Same Krylov space and GMRES iterates, other rounding. */
 } hbpdc_solver_opts;
 
 /* Element partition (the mesh is decomposed, W and sigma share the

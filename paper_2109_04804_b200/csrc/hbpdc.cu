@@ -1,6 +1,7 @@
 // hbpdc.cu -- C-ABI implementation: context, operators, BJ_ext, GMRES, Newton,
 // and the HBPC(q, k_max) step (Alg. 1).  The host runs the control
 // flow; every vector operation runs in the kernels of ops_kernels.cu / linalg.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -97,6 +98,7 @@ struct hbpdc_ctx {
   std::string err;
   Tableau tab{};
   int restart = 0;
+  int sstep = 1;                   // s-step Arnoldi block size (1: DCGS2)
   // device memory
   std::vector<void*> allocs;
   std::vector<SysWS> sys;      // Newton/GMRES workspaces: [0] always, s-1 of them for batched correctors
@@ -577,6 +579,10 @@ struct GState {
   bool in_cycle = false, flush_next = false, est_ok = false;
   int j = 0, k = 0;
   std::vector<double> a, bvec, t, hp, d;
+  // s-step mode (sstep > 1): Newton-basis matrix powers w_i = (A - theta) w_{i-1}
+  // from w_0 = q_kb, then one block Gram-Schmidt per block of sstep vectors
+  int sstep = 1, pi = 0, kb = 0;
+  double theta = 1.0;
   bool needs_op() const { return in_cycle && !flush_next && j != 0; }
 };
 
@@ -616,6 +622,8 @@ hbpdc_status g_cycle_begin(hbpdc_ctx* c, GState& g) {
   g.est_ok = false;
   g.j = 1;
   g.k = 0;
+  g.pi = 0;
+  g.kb = 0;
   return HBPDC_OK;
 }
 
@@ -772,6 +780,197 @@ hbpdc_status g_iter(hbpdc_ctx* c, GState& g, const double* z) {
   return HBPDC_OK;
 }
 
+// ---- s-step Arnoldi (communication-avoiding GMRES, Hoemmen 2010 / Carson 2015) ----
+// A = J P^-1.  From the last orthonormal vector q_kb the block computes the
+// Newton-basis powers w_i = A w_{i-1} - theta w_{i-1} (i = 1..s, one operator
+// application each, like s ordinary Arnoldi steps), then orthogonalises the
+// whole block against Q = [q_0..q_kb] with block CGS2 (two projection passes,
+// each one streaming pass over Q) and the block itself with CholQR2.  With the
+// coordinates r_i of w_i in [Q, Q_new] (r_0 = e_kb), A w_i = w_{i+1} + theta w_i
+// gives the Hessenberg columns kb+i (i < s) by forward substitution:
+//   h_{kb+i} = ( r_{i+1} + theta r_i - sum_{j < kb+i} r_i[j] h_j ) / r_i[kb+i].
+// The Krylov space and the GMRES iterate are those of s ordinary Arnoldi steps
+// (the paper's GMRES); only the orthogonalisation schedule differs.
+// Q traffic: 4 passes per s iterations instead of 2 per iteration (DCGS2).
+
+// Cholesky T = R^T R of a small SPD matrix (row-major s x s); false if not SPD
+static bool small_chol(std::vector<double>& T, int sb, std::vector<double>& R) {
+  R.assign((size_t)sb * sb, 0.0);
+  for (int i = 0; i < sb; ++i) {
+    for (int j = i; j < sb; ++j) {
+      double v = T[(size_t)i * sb + j];
+      for (int k = 0; k < i; ++k) v -= R[(size_t)k * sb + i] * R[(size_t)k * sb + j];
+      if (i == j) {
+        if (!(v > 0.0)) return false;
+        R[(size_t)i * sb + i] = std::sqrt(v);
+      } else {
+        R[(size_t)i * sb + j] = v / R[(size_t)i * sb + i];
+      }
+    }
+  }
+  return true;
+}
+static void upper_inv(const std::vector<double>& R, int sb, std::vector<double>& Ri) {
+  Ri.assign((size_t)sb * sb, 0.0);
+  for (int j = 0; j < sb; ++j) {
+    Ri[(size_t)j * sb + j] = 1.0 / R[(size_t)j * sb + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double v = 0.0;
+      for (int k = i + 1; k <= j; ++k) v += R[(size_t)i * sb + k] * Ri[(size_t)k * sb + j];
+      Ri[(size_t)i * sb + j] = -v / R[(size_t)i * sb + i];
+    }
+  }
+}
+
+// block reduction: rows of launch_block_dots, summed over ranks, to the host
+hbpdc_status block_dots_host(hbpdc_ctx* c, SysWS& w, int nq, const double* W, int sb, std::vector<double>& out) {
+  const size_t n2 = 2 * c->n;
+  const int rows = nq * sb + sb * sb;
+  const int nb = block_dot_blocks(n2);
+  {
+    ProfScope ps(c, 3, (double)(nq + sb) * n2 * 8.0);
+    CK(launch_block_dots(w.Vk, n2, nq, W, n2, sb, n2, w.partial, c->stream));
+    CK(launch_reduce_partials_n(w.partial, rows, nb, w.dh, c->stream));
+    CKS(allreduce(c, w.dh, rows));
+  }
+  CK(cudaMemcpyAsync(w.hpin, w.dh, rows * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  out.assign(w.hpin, w.hpin + rows);
+  return HBPDC_OK;
+}
+
+hbpdc_status block_update_dev(hbpdc_ctx* c, SysWS& w, int nq, double* W, int sb, const std::vector<double>& C,
+                              const std::vector<double>* Rinv) {
+  const size_t n2 = 2 * c->n;
+  const int nc = nq * sb;
+  CK(cudaStreamSynchronize(c->stream));      // the pinned staging buffer is free
+  for (int q = 0; q < nc; ++q) w.hpin[q] = C[q];
+  if (Rinv) for (int q = 0; q < sb * sb; ++q) w.hpin[nc + q] = (*Rinv)[q];
+  const int tot = nc + (Rinv ? sb * sb : 0);
+  if (tot) CK(cudaMemcpyAsync(w.dy, w.hpin, tot * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  ProfScope ps(c, 4, (double)(nq + 2 * sb) * n2 * 8.0);
+  CK(launch_block_update(w.Vk, n2, nq, W, n2, sb, w.dy, Rinv ? w.dy + nc : nullptr, n2, c->stream));
+  return HBPDC_OK;
+}
+
+// the block of s powers is complete: orthogonalise it, extend H, apply Givens
+hbpdc_status g_block(hbpdc_ctx* c, GState& g) {
+  SysWS& w = *g.w;
+  const size_t n2 = 2 * c->n;
+  const int R = c->restart;
+  const int sb = g.sstep, kb = g.kb, nq = kb + 1;
+  double* W = w.Vk + (size_t)(kb + 1) * n2;
+  std::vector<double> r1, r2, r3, T, Rw, Rwi, R3, R3i;
+  // pass 1 + 2: C1 = Q^T W, W1 = W - Q C1
+  CKS(block_dots_host(c, w, nq, W, sb, r1));
+  std::vector<double> C1(r1.begin(), r1.begin() + (size_t)nq * sb);
+  CKS(block_update_dev(c, w, nq, W, sb, C1, nullptr));
+  // pass 3 + 4: C2 = Q^T W1, G2 = W1^T W1; Q_new = (W1 - Q C2) Rw^-1, Rw^T Rw = G2 - C2^T C2
+  CKS(block_dots_host(c, w, nq, W, sb, r2));
+  std::vector<double> C2(r2.begin(), r2.begin() + (size_t)nq * sb);
+  T.assign((size_t)sb * sb, 0.0);
+  for (int a = 0; a < sb; ++a)
+    for (int b = 0; b < sb; ++b) {
+      double v = r2[(size_t)nq * sb + a * sb + b];
+      for (int j = 0; j < nq; ++j) v -= C2[(size_t)j * sb + a] * C2[(size_t)j * sb + b];
+      T[(size_t)a * sb + b] = v;
+    }
+  bool ok = small_chol(T, sb, Rw);
+  if (ok) {
+    upper_inv(Rw, sb, Rwi);
+    CKS(block_update_dev(c, w, nq, W, sb, C2, &Rwi));
+    // CholQR2 of the block itself
+    std::vector<double> none;
+    CKS(block_dots_host(c, w, 0, W, sb, r3));
+    T.assign(r3.begin(), r3.begin() + (size_t)sb * sb);
+    ok = small_chol(T, sb, R3);
+    if (ok) {
+      upper_inv(R3, sb, R3i);
+      CKS(block_update_dev(c, w, 0, W, sb, none, &R3i));
+    }
+  }
+  if (!ok) {
+    // numerically dependent block (near a happy breakdown or an ill-conditioned
+    // power basis): finish the cycle with the columns so far, continue with DCGS2
+    g.sstep = 1;
+    return g_cycle_end(c, g);
+  }
+  // R_total = R3 Rw (upper triangular)
+  std::vector<double> Rt((size_t)sb * sb, 0.0);
+  for (int i = 0; i < sb; ++i)
+    for (int j = i; j < sb; ++j) {
+      double v = 0.0;
+      for (int k = i; k <= j; ++k) v += R3[(size_t)i * sb + k] * Rw[(size_t)k * sb + j];
+      Rt[(size_t)i * sb + j] = v;
+    }
+  // coordinates r_i (i = 0..sb) of w_i in [q_0 .. q_{kb+sb}]
+  const int dimc = nq + sb;
+  std::vector<std::vector<double>> rc(sb + 1, std::vector<double>(dimc, 0.0));
+  rc[0][kb] = 1.0;
+  for (int i = 1; i <= sb; ++i) {
+    for (int j = 0; j < nq; ++j) rc[i][j] = C1[(size_t)j * sb + i - 1] + C2[(size_t)j * sb + i - 1];
+    for (int m = 0; m < sb; ++m) rc[i][nq + m] = Rt[(size_t)m * sb + i - 1];
+  }
+  auto HR = [&](int row, int col) -> double& { return w.Hraw[(size_t)col * (R + 1) + row]; };
+  auto HQ = [&](int row, int col) -> double& { return w.H[(size_t)col * (R + 1) + row]; };
+  for (int i = 0; i < sb; ++i) {
+    const int col = kb + i;
+    std::vector<double> h(dimc, 0.0);
+    for (int r = 0; r < dimc; ++r) h[r] = rc[i + 1][r] + g.theta * rc[i][r];
+    for (int j = 0; j < col; ++j) {
+      const double cj = rc[i][j];
+      if (cj == 0.0) continue;
+      for (int r = 0; r <= j + 1 && r < dimc; ++r) h[r] -= cj * HR(r, j);
+    }
+    const double piv = rc[i][col];
+    for (int r = 0; r <= col + 1; ++r) HR(r, col) = h[r] / piv;
+    // Givens on the new column
+    for (int r = 0; r <= col + 1; ++r) HQ(r, col) = HR(r, col);
+    for (int q = 0; q < col; ++q) {
+      const double tt = w.cs[q] * HQ(q, col) + w.sn[q] * HQ(q + 1, col);
+      HQ(q + 1, col) = -w.sn[q] * HQ(q, col) + w.cs[q] * HQ(q + 1, col);
+      HQ(q, col) = tt;
+    }
+    const double den = std::hypot(HQ(col, col), HQ(col + 1, col));
+    w.cs[col] = HQ(col, col) / den;
+    w.sn[col] = HQ(col + 1, col) / den;
+    HQ(col, col) = den;
+    HQ(col + 1, col) = 0.0;
+    w.gv[col + 1] = -w.sn[col] * w.gv[col];
+    w.gv[col] = w.cs[col] * w.gv[col];
+    g.k = col + 1;
+    if (c->st && g.k > c->st->max_krylov_j) c->st->max_krylov_j = g.k;
+    if (!std::isfinite(w.gv[g.k])) return fail(c, HBPDC_E_NONFINITE, "non-finite s-step Arnoldi");
+    if (std::fabs(w.gv[g.k]) <= c->op.gmres_rtol * g.beta0) {
+      g.est_ok = true;
+      return g_cycle_end(c, g);
+    }
+  }
+  // next block from q_{kb+sb}
+  g.kb = kb + sb;
+  g.pi = 0;
+  g.j = g.kb + 1;
+  if (g.kb + sb > R || g.total >= c->op.krylov_max_per_newton) return g_cycle_end(c, g);
+  return HBPDC_OK;
+}
+
+// one matrix-powers step of the s-step block: w_{pi+1} = A w_pi - theta w_pi, z = P^-1 w_pi given
+hbpdc_status g_power(hbpdc_ctx* c, GState& g, const double* z) {
+  SysWS& w = *g.w;
+  const size_t n = c->n, n2 = 2 * n;
+  CKS(ensure_krylov(c, w, (size_t)g.j + 1));
+  double* prev = w.Vk + (size_t)(g.j - 1) * n2;
+  double* out = w.Vk + (size_t)g.j * n2;
+  use_ghosts(c, w);
+  CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr, true));
+  CK(launch_axpby(-g.theta, prev, 1.0, out, n2, c->stream));
+  ++g.total;
+  ++g.pi;
+  ++g.j;
+  if (g.pi == g.sstep) return g_block(c, g);
+  return HBPDC_OK;
+}
+
 // Solve J x_i = rhs_i (rhs in w.rhs, x -> w.dX) for B systems in lock step:
 // every Arnoldi step preconditions all systems that need an operator
 // application with ONE pass over S (precond_apply_multi), the JVPs and
@@ -812,7 +1011,8 @@ hbpdc_status gmres_batch(hbpdc_ctx* c, GState* gs, int B) {
       if (!gs[i].in_cycle) continue;
       const double* z = nullptr;
       if (q < na && act[q] == i) z = zs[q++];
-      CKS(g_iter(c, gs[i], z));
+      if (gs[i].sstep > 1 && z) CKS(g_power(c, gs[i], z));
+      else CKS(g_iter(c, gs[i], z));
     }
   }
   for (int i = 0; i < B; ++i) {
@@ -891,6 +1091,7 @@ hbpdc_status newton_batch(hbpdc_ctx* c, int B, double a1, double a2, double dt, 
       CK(launch_axpby(-1.0, w.G, 0.0, w.rhs, n2, c->stream));       // rhs = -G
       gs[nb].w = &w;
       gs[nb].L = LinSys{a1, a2, dt, w.X, w.X + n, pc};
+      gs[nb].sstep = c->sstep;
       idx[nb++] = i;
     }
     CKS(gmres_batch(c, gs, nb));
@@ -1034,9 +1235,11 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     CKS(dalloc(c, &w.zb, n2));
     CKS(dalloc(c, &w.b, n));
     CKS(ensure_krylov(c, w, std::min<size_t>((size_t)R + 1, 33)));
-    CKS(dalloc(c, &w.partial, (size_t)(2 * R + 4) * std::max(arnoldi_dot_blocks(n2), RED_BLOCKS)));
-    CKS(dalloc(c, &w.dh, 2 * (size_t)R + 4));
-    CKS(dalloc(c, &w.dy, 2 * (size_t)R + 4));
+    // reduction rows: DCGS2 2j + 3, s-step (j + 1) s + s^2
+    const size_t rows = std::max<size_t>(2 * (size_t)R + 4, ((size_t)R + 1) * c->sstep + (size_t)c->sstep * c->sstep);
+    CKS(dalloc(c, &w.partial, rows * std::max({arnoldi_dot_blocks(n2), block_dot_blocks(n2), RED_BLOCKS})));
+    CKS(dalloc(c, &w.dh, rows));
+    CKS(dalloc(c, &w.dy, rows));
     CKS(dalloc(c, &w.dnrm, 1));
     if (c->halo()) {
       CKS(dalloc(c, &w.gW, ng));
@@ -1049,7 +1252,9 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     w.gv.assign(R + 2, 0.0);
     w.y.assign(R + 1, 0.0);
     void* hp = nullptr;
-    CK(cudaMallocHost(&hp, (3 * (size_t)(R + 1) + 8) * sizeof(double)));
+    CK(cudaMallocHost(&hp, std::max<size_t>(3 * (size_t)(R + 1) + 8,
+                                             ((size_t)R + 1) * c->sstep + (size_t)c->sstep * c->sstep + 8) *
+                               sizeof(double)));
     w.hpin = (double*)hp;
   }
   CKS(dalloc(c, &c->partial, RED_BLOCKS));
@@ -1153,6 +1358,9 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->nE = c->nxl * c->nyl;
   c->n = (size_t)c->nE * c->m;
   c->restart = op->gmres_restart;
+  c->sstep = op->gmres_sstep > 1 ? op->gmres_sstep : 1;
+  if (c->sstep != 1 && c->sstep != 2 && c->sstep != 4 && c->sstep != 8) return bad("gmres_sstep must be 1, 2, 4 or 8");
+  if (c->sstep > c->restart) c->sstep = 1;
   c->tab = tableau(pb->q);
   c->basis = hbpdc::gll_basis(pb->N);
   // geometry: Cartesian, J = dx dy / 4, s-hat = dy/2, dx/2 -> scale 2/dx, 2/dy

@@ -119,6 +119,15 @@ cudaError_t launch_halo_unpack(const HaloLayout& L, int nf, const double* recv, 
 // out = c / sqrt(*sum), or 0 if *sum == 0
 cudaError_t launch_fd_eps_from_sum(const double* sum, double c, double* out, cudaStream_t st);
 
+// ---- sstep.cu: block Gram-Schmidt of the s-step Arnoldi process ------------------
+int block_dot_blocks(size_t L);
+// part rows j*s + l = Q_j . W_l (j < nq), rows nq*s + a*s + b = W_a . W_b; s in {2, 4, 8}
+cudaError_t launch_block_dots(const double* Q, size_t ldq, int nq, const double* W, size_t ldw, int s, size_t L,
+                              double* part, cudaStream_t st);
+// W_l <- sum_m (W_m - sum_j Q_j C[j*s + m]) Rinv[m*s + l]  (Rinv upper triangular, NULL = I)
+cudaError_t launch_block_update(const double* Q, size_t ldq, int nq, double* W, size_t ldw, int s, const double* C,
+                                const double* Rinv, size_t L, cudaStream_t st);
+
 // kernel-launch counter (reported by hbpdc_launch_count)
 extern long long g_hbpdc_launches;
 inline void hbpdc_count_launch() { ++g_hbpdc_launches; }

@@ -50,7 +50,8 @@ class SolverOpts(ctypes.Structure):
                 ("newton_floor", ctypes.c_double), ("newton_max", ctypes.c_int),
                 ("gmres_rtol", ctypes.c_double), ("gmres_restart", ctypes.c_int),
                 ("krylov_max_per_newton", ctypes.c_int), ("precond", ctypes.c_int),
-                ("precond_policy", ctypes.c_int), ("jvp_mode", ctypes.c_int), ("batch_stages", ctypes.c_int)]
+                ("precond_policy", ctypes.c_int), ("jvp_mode", ctypes.c_int), ("batch_stages", ctypes.c_int),
+                ("gmres_sstep", ctypes.c_int)]
 
 
 class Dist(ctypes.Structure):
@@ -182,7 +183,7 @@ class Context:
                  gamma=1.4, mu=0.0, prandtl=0.72, q=4, kmax=0, newton_rtol=1e-10,
                  newton_atol_dw=1e-12, newton_floor=64.0, newton_max=50, gmres_rtol=1e-6,
                  restart=700, max_krylov=7000, precond="bjext", precond_policy="per_step_per_alpha",
-                 jvp_mode="auto", batch_stages=True, rank=0, nranks=1, px=1, py=1, nccl_id=None, stream=None, device=0,
+                 jvp_mode="auto", batch_stages=True, gmres_sstep=1, rank=0, nranks=1, px=1, py=1, nccl_id=None, stream=None, device=0,
                  comm="auto", loopback=None, force_halo=False):
         import torch
         self.lib = load()
@@ -196,7 +197,8 @@ class Context:
                         newton_max=newton_max, gmres_rtol=gmres_rtol, gmres_restart=restart,
                         krylov_max_per_newton=max_krylov, precond=_PC[precond],
                         precond_policy=0 if precond_policy == "per_step_per_alpha" else 1,
-                        jvp_mode=_JVP[jvp_mode], batch_stages=int(batch_stages))
+                        jvp_mode=_JVP[jvp_mode], batch_stages=int(batch_stages),
+                        gmres_sstep=int(gmres_sstep))
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream

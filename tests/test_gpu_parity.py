@@ -287,3 +287,45 @@ def test_batched_correctors_bitwise(q, kmax):
         ctx.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
+
+
+@pytest.mark.parametrize("s", [2, 4, 8])
+@pytest.mark.parametrize("q,kmax", [(4, 0), (8, 4)])
+def test_sstep_gmres_end_of_run(s, q, kmax):
+    """s-step (communication-avoiding) Arnoldi: Newton-basis powers + block
+    CGS2/CholQR2.  Same GMRES iterates in exact arithmetic: end of run vs the
+    oracle <= 1e-8, iteration counts close to the DCGS2 schedule's."""
+    import torch
+    cfg = configs.scaled(configs.CONFIGS["C3"], N=3, nx=4, ny=4, steps=2, q=q, kmax=kmax)
+    d, ctx = make_pair("euler", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=q, kmax=kmax,
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, gmres_sstep=s)
+    d1, ctx1 = make_pair("euler", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=q, kmax=kmax,
+                         gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol)
+    W0 = inputs.initial_state("C3", d.node_coords(), noise=cfg.noise)
+    dt = configs.cfl_dt(cfg, inputs.initial_state("C3", d.node_coords()))
+    Wo, _ = _run_oracle(d, q, kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol)
+    its = []
+    for cx in (ctx, ctx1):
+        Wg = to_gpu(W0)
+        n = 0
+        for _ in range(cfg.steps):
+            n += cx.step(dt, Wg)["gmres_its"]
+        torch.cuda.synchronize()
+        its.append(n)
+        assert rel(to_np(Wg), Wo) <= 1e-8
+    assert its[0] <= 1.25 * its[1] + 2 * s, its
+
+
+@pytest.mark.parametrize("precond,cfl", [("bjext", 2.0), ("none", 0.25)])
+def test_sstep_advection_end_of_run(precond, cfl):
+    cfg = configs.scaled(configs.CONFIGS["C2"], nx=8, ny=8, steps=3, cfl=cfl)
+    d, ctx = make_pair("advection", cfg.N, cfg.nx, cfg.ny, a=cfg.a, q=cfg.q, kmax=cfg.kmax,
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, precond=precond, gmres_sstep=4)
+    W0 = inputs.initial_state("C2", d.node_coords())
+    dt = configs.cfl_dt(cfg, W0)
+    Wo, _ = _run_oracle(d, cfg.q, cfg.kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol,
+                        gmres_rtol=cfg.gmres_rtol, precond=precond)
+    Wg = to_gpu(W0)
+    for _ in range(cfg.steps):
+        ctx.step(dt, Wg)
+    assert rel(to_np(Wg), Wo) <= 1e-8
