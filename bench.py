@@ -329,7 +329,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--gmres-sstep", type=int, default=4,
+    ap.add_argument("--gmres-sstep", type=int, default=8,
                     help="Arnoldi schedule: 1 = DCGS2, 2/4/8 = s-step blocks")
     ap.add_argument("--self-halo", action="store_true",
                     help="test hook: route the periodic wrap through the NCCL transport (N = 1)")

@@ -128,6 +128,13 @@ cudaError_t launch_block_dots(const double* Q, size_t ldq, int nq, const double*
 cudaError_t launch_block_update(const double* Q, size_t ldq, int nq, double* W, size_t ldw, int s, const double* C,
                                 const double* Rinv, size_t L, cudaStream_t st);
 
+// fp64 tensor-core (mma.sync m8n8k4 f64) versions, s in {4, 8}; same row layout
+int block_dot_blocks_mma(size_t L);
+cudaError_t launch_block_dots_mma(const double* Q, size_t ldq, int nq, const double* W, size_t ldw, int s, size_t L,
+                                  double* part, cudaStream_t st);
+cudaError_t launch_block_update_mma(const double* Q, size_t ldq, int nq, double* W, size_t ldw, int s,
+                                    const double* C, const double* Rinv, size_t L, cudaStream_t st);
+
 // kernel-launch counter (reported by hbpdc_launch_count)
 extern long long g_hbpdc_launches;
 inline void hbpdc_count_launch() { ++g_hbpdc_launches; }
