@@ -328,15 +328,18 @@ int jvp_kind(hbpdc_ctx* c, int mode) {
 // J dX for the extended system, dX = [dW | ds] (2n), out = [top | bottom]
 // ws_ghosts: the halos of (W, sigma) are current (GMRES inside one Newton
 // iteration: the linearisation point is fixed), exchange only (dW, dsigma)
+// shift_src (2n, optional): out -= shift * shift_src, fused into the epilogue
 hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const double* W, const double* sg,
                       const double* dW, const double* ds, double* o1, double* o2, int mode,
-                      const double* eps_override, bool ws_ghosts = false) {
+                      const double* eps_override, bool ws_ghosts = false, const double* shift_src = nullptr,
+                      double shift = 0.0) {
   const size_t n = c->n;
   mode = jvp_kind(c, mode);
   OpArgs A = base_args(c);
   A.W = W; A.S = sg; A.dW = dW; A.dS = ds; A.out1 = o1; A.out2 = o2;
   A.a1dt = a1 * dt;
   A.c2 = a2 * dt * dt / 2.0;
+  if (shift_src) { A.shw = shift_src; A.shs = shift_src + n; A.shift = shift; }
   OpKind k;
   if (mode == HBPDC_JVP_LINEAR) {
     if (c->pb.equation != HBPDC_ADVECTION) return fail(c, HBPDC_E_ARG, "LINEAR JVP needs a linear flux");
@@ -967,8 +970,8 @@ hbpdc_status g_power(hbpdc_ctx* c, GState& g, const double* z) {
   double* prev = w.Vk + (size_t)(g.j - 1) * n2;
   double* out = w.Vk + (size_t)g.j * n2;
   use_ghosts(c, w);
-  CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr, true));
-  CK(launch_axpby(-g.theta, prev, 1.0, out, n2, c->stream));
+  CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr, true,
+               prev, g.theta));
   ++g.total;
   ++g.pi;
   ++g.j;

@@ -21,6 +21,8 @@ struct OpArgs {
   const double* G0;     // NS lifted gradients of jet state 0
   const double* G1;     // NS lifted gradients of jet state 1
   const double *gG0, *gG1;   // their ghost copies (halo of the lifted gradients)
+  const double *shw, *shs;   // JVP epilogue shift: out -= shift * (shw | shs)  (s-step Newton basis)
+  double shift;
   double a1dt, c2;
   double epsw;          // FD step for the W direction (<= 0: quotient is 0)
   const double* d_epsw; // if non-NULL, the FD step is read from device memory
@@ -173,8 +175,10 @@ template <int EQ, int NODES> struct ModeJvpExact : OneJetMode<EQ, NODES, ModeJvp
   __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      A.out1[k] = A.dW[k] + o[0][v];
-      A.out2[k] = A.dS[k] - o[1][v];
+      double t1 = A.dW[k] + o[0][v], t2 = A.dS[k] - o[1][v];
+      if (A.shw) { t1 = fma(-A.shift, A.shw[k], t1); t2 = fma(-A.shift, A.shs[k], t2); }
+      A.out1[k] = t1;
+      A.out2[k] = t2;
     }
   }
 };
@@ -338,8 +342,10 @@ template <int EQ, int NODES> struct ModeJvpFD {
   __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      A.out1[k] = A.dW[k] + o[0][v];
-      A.out2[k] = A.dS[k] - o[1][v];
+      double t1 = A.dW[k] + o[0][v], t2 = A.dS[k] - o[1][v];
+      if (A.shw) { t1 = fma(-A.shift, A.shw[k], t1); t2 = fma(-A.shift, A.shs[k], t2); }
+      A.out1[k] = t1;
+      A.out2[k] = t2;
     }
   }
 };
@@ -393,8 +399,10 @@ template <int EQ, int NODES> struct ModeJvpLinear {
   __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      A.out1[k] = A.dW[k] + o[0][v];
-      A.out2[k] = A.dS[k] - o[1][v];
+      double t1 = A.dW[k] + o[0][v], t2 = A.dS[k] - o[1][v];
+      if (A.shw) { t1 = fma(-A.shift, A.shw[k], t1); t2 = fma(-A.shift, A.shs[k], t2); }
+      A.out1[k] = t1;
+      A.out2[k] = t2;
     }
   }
 };
