@@ -829,12 +829,15 @@ static void upper_inv(const std::vector<double>& R, int sb, std::vector<double>&
 hbpdc_status block_dots_host(hbpdc_ctx* c, SysWS& w, int nq, const double* W, int sb, std::vector<double>& out) {
   const size_t n2 = 2 * c->n;
   const int rows = nq * sb + sb * sb;
-  // s = 4, 8: fp64 tensor-core kernel (scripts/bench_block.cu: 5.5-5.8 TB/s vs 5.4 / 2.4 with FMAs)
+  // s = 4, 8: fp64 tensor-core kernels (scripts/bench_block.cu: 5.5-5.8 TB/s vs 5.4 / 2.4 with FMAs);
+  // s = 8 and a short basis: the TMA-streamed one (scripts/bench_block_tma.cu: faster for nq <= 64)
+  const bool tma = sb == 8 && nq <= BLOCK_TMA_DOTS_MAX_NQ;
   const bool mma = sb >= 4;
-  const int nb = mma ? block_dot_blocks_mma(n2) : block_dot_blocks(n2);
+  const int nb = tma ? block_dot_parts_tma() : (mma ? block_dot_blocks_mma(n2) : block_dot_blocks(n2));
   {
     ProfScope ps(c, 3, (double)(nq + sb) * n2 * 8.0);
-    if (mma) CK(launch_block_dots_mma(w.Vk, n2, nq, W, n2, sb, n2, w.partial, c->stream));
+    if (tma) CK(launch_block_dots_tma8(w.Vk, n2, nq, W, n2, n2, w.partial, c->stream));
+    else if (mma) CK(launch_block_dots_mma(w.Vk, n2, nq, W, n2, sb, n2, w.partial, c->stream));
     else CK(launch_block_dots(w.Vk, n2, nq, W, n2, sb, n2, w.partial, c->stream));
     CK(launch_reduce_partials_n(w.partial, rows, nb, w.dh, c->stream));
     CKS(allreduce(c, w.dh, rows));
@@ -855,8 +858,12 @@ hbpdc_status block_update_dev(hbpdc_ctx* c, SysWS& w, int nq, double* W, int sb,
   const int tot = nc + (Rinv ? sb * sb : 0);
   if (tot) CK(cudaMemcpyAsync(w.dy, w.hpin, tot * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   ProfScope ps(c, 4, (double)(nq + 2 * sb) * n2 * 8.0);
-  // s = 8: fp64 tensor-core kernel (5.8 TB/s vs 4.0 with FMAs); s <= 4: FMA kernel (6.1 TB/s)
-  if (sb == 8) CK(launch_block_update_mma(w.Vk, n2, nq, W, n2, sb, w.dy, Rinv ? w.dy + nc : nullptr, n2, c->stream));
+  // s = 8: fp64 tensor-core kernel (5.8 TB/s vs 4.0 with FMAs), TMA-streamed for a short basis
+  // (scripts/bench_block_tma.cu: 3.3 / 5.4 / 6.6 TB/s at nq = 1 / 17 / 64 vs 2.8 / 4.1 / 5.8);
+  // s <= 4: FMA kernel (6.1 TB/s)
+  if (sb == 8 && nq >= 1 && nq <= BLOCK_TMA_UPDATE_MAX_NQ)
+    CK(launch_block_update_tma8(w.Vk, n2, nq, W, n2, w.dy, Rinv ? w.dy + nc : nullptr, n2, c->stream));
+  else if (sb == 8) CK(launch_block_update_mma(w.Vk, n2, nq, W, n2, sb, w.dy, Rinv ? w.dy + nc : nullptr, n2, c->stream));
   else CK(launch_block_update(w.Vk, n2, nq, W, n2, sb, w.dy, Rinv ? w.dy + nc : nullptr, n2, c->stream));
   return HBPDC_OK;
 }
@@ -1245,7 +1252,7 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     CKS(ensure_krylov(c, w, std::min<size_t>((size_t)R + 1, 33)));
     // reduction rows: DCGS2 2j + 3, s-step (j + 1) s + s^2
     const size_t rows = std::max<size_t>(2 * (size_t)R + 4, ((size_t)R + 1) * c->sstep + (size_t)c->sstep * c->sstep);
-    CKS(dalloc(c, &w.partial, rows * std::max({arnoldi_dot_blocks(n2), block_dot_blocks(n2), block_dot_blocks_mma(n2), RED_BLOCKS})));
+    CKS(dalloc(c, &w.partial, rows * std::max({arnoldi_dot_blocks(n2), block_dot_blocks(n2), block_dot_blocks_mma(n2), block_dot_parts_tma(), RED_BLOCKS})));
     CKS(dalloc(c, &w.dh, rows));
     CKS(dalloc(c, &w.dy, rows));
     CKS(dalloc(c, &w.dnrm, 1));

@@ -134,6 +134,17 @@ cudaError_t launch_block_dots_mma(const double* Q, size_t ldq, int nq, const dou
                                   double* part, cudaStream_t st);
 cudaError_t launch_block_update_mma(const double* Q, size_t ldq, int nq, double* W, size_t ldw, int s,
                                     const double* C, const double* Rinv, size_t L, cudaStream_t st);
+// TMA-streamed persistent versions for s = 8 (one CTA per SM, same row layout;
+// dots partials: block_dot_parts_tma() per row).  Used while the basis is short
+// (measured crossover with the register-streamed DMMA kernels, bench_block_tma.cu).
+constexpr int BLOCK_TMA_DOTS_MAX_NQ = 72;
+constexpr int BLOCK_TMA_UPDATE_MAX_NQ = 100;
+int block_dot_blocks_tma();
+int block_dot_parts_tma();
+cudaError_t launch_block_dots_tma8(const double* Q, size_t ldq, int nq, const double* W, size_t ldw, size_t L,
+                                   double* part, cudaStream_t st);
+cudaError_t launch_block_update_tma8(const double* Q, size_t ldq, int nq, double* W, size_t ldw, const double* C,
+                                     const double* Rinv, size_t L, cudaStream_t st);
 
 // kernel-launch counter (reported by hbpdc_launch_count)
 extern long long g_hbpdc_launches;

@@ -1,6 +1,7 @@
 // linalg.cu -- BJ_ext block inversion and application, GMRES/Newton vector ops.
 #include <cstdint>
 #include "launch.h"
+#include "tma.cuh"
 
 long long g_hbpdc_launches = 0;
 
@@ -262,32 +263,6 @@ __global__ void __launch_bounds__(256) gemv2_kernel(const double* __restrict__ S
 // flight with cp.async.bulk (completion on an mbarrier), the 8 warps reduce
 // one row each per chunk from shared memory.
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(b))
-               : "memory");
-}
-
 // NR right-hand sides (NR = 2: u = S W, v = S sigma of one system; NR = 2B: the
 // B corrector-stage systems of a sweep solved in lock step share ONE pass over
 // S).  Every output row is accumulated in the same order for
@@ -297,9 +272,6 @@ struct GemvRHS {
   double* out[GEMV_MAX_RHS];
 };
 
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
 
 // Warp-specialised pipeline: warp 8 (one lane) is the producer, warps 0-7
 // consume.  Per element the producer bulk-copies the NR right-hand-side

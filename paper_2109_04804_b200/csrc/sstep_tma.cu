@@ -1,0 +1,307 @@
+// sstep_tma.cu -- TMA-streamed persistent block Gram-Schmidt kernels of the
+// s-step Arnoldi process for s = 8 (one CTA per SM).
+//
+// The DMMA kernels of sstep.cu load Q straight into registers: every batch of
+// loads is consumed before the next one is issued, so per CTA a pass is a
+// chain of dependent DRAM round trips (ncu at C3: ~4.8 TB/s, 59% of DRAM peak,
+// issue active 24%, 2 CTAs/SM).  Here the Q rows are bulk-copied
+// (cp.async.bulk + mbarrier) into shared-memory rings that stay several
+// stages ahead of the fp64 tensor-core (mma.sync m8n8k4 f64) consumers.
+//
+//   block_dots_tma8    rows j*8 + l : V_j . W_l,  V = [Q_0 .. Q_{nq-1}, W_0 .. W_7]
+//   block_update_tma8  W_l <- sum_m (W_m - sum_j Q_j C[j*8 + m]) Rinv[m*8 + l]
+//
+// Same row layout / semantics as launch_block_dots_mma / launch_block_update_mma;
+// deterministic (fixed chunk -> CTA map, fixed accumulation order).
+#include "launch.h"
+#include "tma.cuh"
+
+namespace {
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+constexpr int TD_E = 512;          // dots: elements per chunk (4 KB row copies: 2 KB ones cap the
+                                   // stream at ~4.1 TB/s, 4 KB ones reach 6.5 TB/s, measured)
+constexpr int TD_P = TD_E + 4;     // padded row (doubles): conflict-free A fragments
+constexpr int TD_W = 16;           // consumer warps (8 cannot issue DMMAs fast enough: 4.1 TB/s)
+constexpr int TD_R = 6;            // ring stages (shared by the consumer warps)
+constexpr int TD_G = 16;           // tiles per group
+constexpr int TD_C = 1;            // accumulator chains per tile
+constexpr int TU_E = 256;          // update: elements per chunk
+constexpr int TU_P = TU_E + 4;     // padded row: conflict-free B fragments
+constexpr int TU_R = 8;            // ring stages (shared by the 8 consumer warps)
+constexpr int TU_NB = TU_E / 64;   // n-blocks (8 elements) per consumer warp
+}  // namespace
+
+int block_dot_blocks_tma() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
+}
+int block_dot_parts_tma() { return TD_W * block_dot_blocks_tma(); }
+
+// Vector tile t = the 8 vectors 8t .. 8t+7 of V; tiles are taken in groups of
+// up to TD_G (one group while nq + 8 <= 8 TD_G).  Per group the CTA walks its
+// chunks (TD_E elements) and warp TD_W (one lane) streams every tile-chunk of
+// the group through a TD_R-stage ring.  All TD_W consumer warps read every
+// stage, warp w the k-steps of elements (TD_E / TD_W) w + 4 ks + t of the
+// chunk, with its B fragments (W) in registers, prefetched one chunk ahead,
+// and one accumulator per tile of the group.  Each consumer warp writes its
+// own partial (deterministic: fixed element -> warp map; part has
+// block_dot_parts_tma() columns per row).
+__global__ void __launch_bounds__(32 * (TD_W + 1), 1) block_dots_tma8_kernel(const double* __restrict__ Q, size_t ldq, int nq,
+                                                                 const double* __restrict__ W, size_t ldw,
+                                                                 size_t L, double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* ring = reinterpret_cast<double*>(smraw);                            // TD_R x 8 x TD_P
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)TD_R * 8 * TD_P);
+  unsigned long long* empty = full + TD_R;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < TD_R * 8 * TD_P; k += blockDim.x) ring[k] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < TD_R; ++r) { mbar_init(&full[r], 1); mbar_init(&empty[r], TD_W); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  const int nv = nq + 8;
+  const int T = (nv + 7) / 8;
+  const size_t nch = (L + TD_E - 1) / TD_E;
+  const size_t nmy = blockIdx.x < nch ? (nch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (wid == TD_W) {                                                             // ---- producer
+    if (lane == 0) {
+      size_t k = 0;
+      for (int t0 = 0; t0 < T; t0 += TD_G) {
+        const int ng = min(TD_G, T - t0);
+        for (size_t ci = 0; ci < nmy; ++ci) {
+          const size_t e0 = (blockIdx.x + ci * gridDim.x) * TD_E;
+          const int ne = (int)min((size_t)TD_E, L - e0);
+          for (int tg = 0; tg < ng; ++tg, ++k) {
+            const int st = (int)(k % TD_R);
+            if (k >= (size_t)TD_R) mbar_wait(&empty[st], (unsigned)(((k / TD_R) - 1) & 1));
+            const int tile = t0 + tg;
+            const int nrow = min(8, nv - 8 * tile);
+            mbar_expect_tx(&full[st], (unsigned)(nrow * ne * sizeof(double)));
+            for (int r = 0; r < nrow; ++r) {
+              const int j = 8 * tile + r;
+              const double* src = j < nq ? Q + (size_t)j * ldq + e0 : W + (size_t)(j - nq) * ldw + e0;
+              tma_load_1d(ring + ((size_t)st * 8 + r) * TD_P, src, (unsigned)(ne * sizeof(double)), &full[st]);
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  constexpr int KW = TD_E / (4 * TD_W);          // k-steps per warp per stage (TD_E / TD_W elements)
+  auto load_b = [&](size_t ci, double (&o)[KW]) {
+    const size_t e0 = (blockIdx.x + ci * gridDim.x) * TD_E + (TD_E / TD_W) * wid;
+    const double* wg = W + (size_t)g * ldw;
+#pragma unroll
+    for (int ks = 0; ks < KW; ++ks) {
+      const size_t e = e0 + 4 * ks + t;
+      o[ks] = e < L ? __ldg(wg + e) : 0.0;
+    }
+  };
+  size_t k = 0;
+  for (int t0 = 0; t0 < T; t0 += TD_G) {
+    const int ng = min(TD_G, T - t0);
+    double acc[TD_G][TD_C][2];
+#pragma unroll
+    for (int i = 0; i < TD_G; ++i)
+#pragma unroll
+      for (int c = 0; c < TD_C; ++c) { acc[i][c][0] = 0.0; acc[i][c][1] = 0.0; }
+    double b[KW], bn[KW];
+    if (nmy > 0) load_b(0, bn);
+    for (size_t ci = 0; ci < nmy; ++ci) {
+#pragma unroll
+      for (int ks = 0; ks < KW; ++ks) b[ks] = bn[ks];
+      if (ci + 1 < nmy) load_b(ci + 1, bn);
+      // one stage at a time (the ring stays as full as possible); its KW
+      // k-steps go to TD_C accumulators per tile (a DMMA's latency is long:
+      // a single chain per stage would serialise KW of them)
+#pragma unroll
+      for (int tg = 0; tg < TD_G; ++tg) {
+        if (tg < ng) {
+          const int st = (int)(k % TD_R);
+          mbar_wait(&full[st], (unsigned)((k / TD_R) & 1));
+          const double* sa = ring + (size_t)st * 8 * TD_P + g * TD_P + (TD_E / TD_W) * wid + t;
+#pragma unroll
+          for (int ks = 0; ks < KW; ++ks) dmma(acc[tg][ks % TD_C], sa[4 * ks], b[ks]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
+          ++k;
+        }
+      }
+    }
+    // one partial per consumer warp: part[row][TD_W * blockIdx + wid]
+#pragma unroll
+    for (int tg = 0; tg < TD_G; ++tg) {
+      const int j = 8 * (t0 + tg) + g;
+      if (tg < ng && j < nv) {
+        double s0 = acc[tg][0][0], s1 = acc[tg][0][1];
+#pragma unroll
+        for (int c = 1; c < TD_C; ++c) { s0 += acc[tg][c][0]; s1 += acc[tg][c][1]; }
+        const size_t col = (size_t)blockIdx.x * TD_W + wid, ncol = (size_t)gridDim.x * TD_W;
+        part[((size_t)j * 8 + 2 * t) * ncol + col] = s0;
+        part[((size_t)j * 8 + 2 * t + 1) * ncol + col] = s1;
+      }
+    }
+  }
+}
+
+// nq >= 1.  Warp 8 (one lane) streams, per chunk of TU_E elements, the Q tiles
+// (8 vectors each) through a TU_R-stage ring; the 8 consumer warps take TU_NB
+// n-blocks of 8 elements each: D (8 W x 8 elements) += A (C^T, 8 x 4, shared
+// memory) x B (4 Q vectors x 8 elements, the stage).  Then tmp = W - D and
+// out_l = sum_{m <= l} Rinv[m][l] tmp_m with the 8 tmp rows gathered by shuffles.
+__global__ void __launch_bounds__(288, 1) block_update_tma8_kernel(const double* __restrict__ Q, size_t ldq, int nq,
+                                                                   double* __restrict__ W, size_t ldw,
+                                                                   const double* __restrict__ C,
+                                                                   const double* __restrict__ Rinv, size_t L) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nq8 = (nq + 7) / 8 * 8;
+  double* ring = reinterpret_cast<double*>(smraw);                            // TU_R x 8 x TU_P
+  double* sC = ring + (size_t)TU_R * 8 * TU_P;                                // C (zero padded to nq8 x 8)
+  double* sR = sC + (size_t)nq8 * 8;                                          // Rinv (or I), 8 x 8
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sR + 64);
+  unsigned long long* empty = full + TU_R;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < TU_R * 8 * TU_P; k += blockDim.x) ring[k] = 0.0;
+  for (int k = threadIdx.x; k < nq8 * 8; k += blockDim.x) sC[k] = k < nq * 8 ? C[k] : 0.0;
+  for (int k = threadIdx.x; k < 64; k += blockDim.x) sR[k] = Rinv ? Rinv[k] : ((k / 8 == k % 8) ? 1.0 : 0.0);
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < TU_R; ++r) { mbar_init(&full[r], 1); mbar_init(&empty[r], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  const int T = nq8 / 8;
+  const size_t nch = (L + TU_E - 1) / TU_E;
+  const size_t nmy = blockIdx.x < nch ? (nch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (wid == 8) {                                                             // ---- producer
+    if (lane == 0) {
+      size_t k = 0;
+      for (size_t ci = 0; ci < nmy; ++ci) {
+        const size_t e0 = (blockIdx.x + ci * gridDim.x) * TU_E;
+        const int ne = (int)min((size_t)TU_E, L - e0);
+        for (int tile = 0; tile < T; ++tile, ++k) {
+          const int st = (int)(k % TU_R);
+          if (k >= (size_t)TU_R) mbar_wait(&empty[st], (unsigned)(((k / TU_R) - 1) & 1));
+          const int nrow = min(8, nq - 8 * tile);
+          mbar_expect_tx(&full[st], (unsigned)(nrow * ne * sizeof(double)));
+          for (int r = 0; r < nrow; ++r)
+            tma_load_1d(ring + ((size_t)st * 8 + r) * TU_P, Q + (size_t)(8 * tile + r) * ldq + e0,
+                        (unsigned)(ne * sizeof(double)), &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  auto load_w = [&](size_t ci, double (&o)[TU_NB][2]) {
+    const size_t e0 = (blockIdx.x + ci * gridDim.x) * TU_E;
+    const double* wg = W + (size_t)g * ldw;
+#pragma unroll
+    for (int nb = 0; nb < TU_NB; ++nb) {
+      const size_t e = e0 + (size_t)(wid * TU_NB + nb) * 8 + 2 * t;
+      if (e + 1 < L) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(wg + e));
+        o[nb][0] = v.x;
+        o[nb][1] = v.y;
+      } else {
+        o[nb][0] = e < L ? wg[e] : 0.0;
+        o[nb][1] = 0.0;
+      }
+    }
+  };
+  double wv[TU_NB][2], wn[TU_NB][2];
+  if (nmy > 0) load_w(0, wn);
+  size_t k = 0;
+  for (size_t ci = 0; ci < nmy; ++ci) {
+    const size_t e0 = (blockIdx.x + ci * gridDim.x) * TU_E;
+#pragma unroll
+    for (int nb = 0; nb < TU_NB; ++nb) { wv[nb][0] = wn[nb][0]; wv[nb][1] = wn[nb][1]; }
+    if (ci + 1 < nmy) load_w(ci + 1, wn);
+    double acc[TU_NB][2];
+#pragma unroll
+    for (int nb = 0; nb < TU_NB; ++nb) { acc[nb][0] = 0.0; acc[nb][1] = 0.0; }
+    for (int tile = 0; tile < T; ++tile, ++k) {
+      const int st = (int)(k % TU_R);
+      mbar_wait(&full[st], (unsigned)((k / TU_R) & 1));
+      const double* sb = ring + (size_t)st * 8 * TU_P + (size_t)(wid * TU_NB) * 8 + g;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const double a = sC[(8 * tile + 4 * kk + t) * 8 + g];
+#pragma unroll
+        for (int nb = 0; nb < TU_NB; ++nb) dmma(acc[nb], a, sb[(4 * kk + t) * TU_P + nb * 8]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    // lane (g, t) holds D[g][e] for e = n-block base + 2t, 2t + 1
+#pragma unroll
+    for (int nb = 0; nb < TU_NB; ++nb) {
+      const double t0 = wv[nb][0] - acc[nb][0], t1 = wv[nb][1] - acc[nb][1];
+      double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const double v0 = __shfl_sync(0xffffffffu, t0, m * 4 + t);
+        const double v1 = __shfl_sync(0xffffffffu, t1, m * 4 + t);
+        if (m <= g) {
+          const double r = sR[m * 8 + g];
+          o0 = fma(v0, r, o0);
+          o1 = fma(v1, r, o1);
+        }
+      }
+      const size_t e = e0 + (size_t)(wid * TU_NB + nb) * 8 + 2 * t;
+      double* wg = W + (size_t)g * ldw;
+      if (e + 1 < L) {
+        *reinterpret_cast<double2*>(wg + e) = make_double2(o0, o1);
+      } else if (e < L) {
+        wg[e] = o0;
+      }
+    }
+  }
+}
+
+cudaError_t launch_block_dots_tma8(const double* Q, size_t ldq, int nq, const double* W, size_t ldw, size_t L,
+                                   double* part, cudaStream_t st) {
+  if ((ldq & 1) || (ldw & 1)) return cudaErrorInvalidValue;     // 16-B aligned rows for the bulk copies
+  const size_t smem = (size_t)TD_R * 8 * TD_P * sizeof(double) +
+                      2 * TD_R * sizeof(unsigned long long);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(block_dots_tma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  block_dots_tma8_kernel<<<block_dot_blocks_tma(), 32 * (TD_W + 1), smem, st>>>(Q, ldq, nq, W, ldw, L, part);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_update_tma8(const double* Q, size_t ldq, int nq, double* W, size_t ldw, const double* C,
+                                     const double* Rinv, size_t L, cudaStream_t st) {
+  if (nq < 1) return launch_block_update_mma(Q, ldq, nq, W, ldw, 8, C, Rinv, L, st);
+  if ((ldq & 1) || (ldw & 1)) return cudaErrorInvalidValue;
+  const int nq8 = (nq + 7) / 8 * 8;
+  const size_t smem = ((size_t)TU_R * 8 * TU_P + (size_t)nq8 * 8 + 64) * sizeof(double) +
+                      2 * TU_R * sizeof(unsigned long long);
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(block_update_tma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return cudaErrorInvalidValue;
+    attr = smem;
+  }
+  block_update_tma8_kernel<<<block_dot_blocks_tma(), 288, smem, st>>>(Q, ldq, nq, W, ldw, C, Rinv, L);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}

@@ -316,11 +316,13 @@ def test_sstep_gmres_end_of_run(s, q, kmax):
     assert its[0] <= 1.25 * its[1] + 2 * s, its
 
 
+@pytest.mark.parametrize("s", [4, 8])
 @pytest.mark.parametrize("precond,cfl", [("bjext", 2.0), ("none", 0.25)])
-def test_sstep_advection_end_of_run(precond, cfl):
+def test_sstep_advection_end_of_run(precond, cfl, s):
+    """s = 8 runs the TMA-streamed block kernels on a ragged length (2n = 4608)."""
     cfg = configs.scaled(configs.CONFIGS["C2"], nx=8, ny=8, steps=3, cfl=cfl)
     d, ctx = make_pair("advection", cfg.N, cfg.nx, cfg.ny, a=cfg.a, q=cfg.q, kmax=cfg.kmax,
-                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, precond=precond, gmres_sstep=4)
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, precond=precond, gmres_sstep=s)
     W0 = inputs.initial_state("C2", d.node_coords())
     dt = configs.cfl_dt(cfg, W0)
     Wo, _ = _run_oracle(d, cfg.q, cfg.kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol,
