@@ -19,16 +19,26 @@ long long g_hbpdc_launches = 0;
 // column whose pivot row is b; the final pass writes that into S.
 // ============================================================================
 namespace {
+__device__ __forceinline__ void gj_dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
 constexpr int GJ_T = 256;    // threads
 constexpr int GJ_NB = 16;    // panel width
-constexpr int GJ_TW = 32;    // column tile of the rank-NB update (2 columns x 16 rows per thread)
+constexpr int GJ_PS = GJ_NB + 1;   // panel row stride in shared memory
+constexpr int GJ_TW = 32;    // column tile of the rank-NB update
+constexpr int GJ_APS = GJ_TW + 4;  // pivot-row tile stride (conflict-free B fragments)
 constexpr int GJ_MMAX = 256;
+#ifndef GJ_MINB
+#define GJ_MINB 2
+#endif
 }
 
-__global__ void __launch_bounds__(GJ_T, 3) gj_kernel(double* __restrict__ Zall, double* __restrict__ Sall, int m,
+__global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ Zall, double* __restrict__ Sall, int m,
                                                    int* __restrict__ info) {
-  __shared__ double Pn[GJ_MMAX * GJ_NB];
-  __shared__ double AP[GJ_NB * GJ_TW];
+  __shared__ double Pn[GJ_MMAX * GJ_PS];    // panel, row stride GJ_PS (odd: conflict-free columns)
+  __shared__ double AP[GJ_NB * GJ_APS];
   __shared__ int piv[GJ_MMAX];      // pivot row of column c
   __shared__ int colof[GJ_MMAX];    // column whose pivot row is r (-1: unused)
   __shared__ double redv[GJ_T / 32];
@@ -46,7 +56,7 @@ __global__ void __launch_bounds__(GJ_T, 3) gj_kernel(double* __restrict__ Zall, 
     const int nb = min(GJ_NB, m - c0);
     for (int idx = tid; idx < m * nb; idx += GJ_T) {
       const int r = idx / nb, k = idx % nb;
-      Pn[r * GJ_NB + k] = A[(size_t)r * m + c0 + k];
+      Pn[r * GJ_PS + k] = A[(size_t)r * m + c0 + k];
     }
     __syncthreads();
     for (int k = 0; k < nb; ++k) {
@@ -55,7 +65,7 @@ __global__ void __launch_bounds__(GJ_T, 3) gj_kernel(double* __restrict__ Zall, 
       int bi = 0x7fffffff;
       for (int r = tid; r < m; r += GJ_T) {
         if (colof[r] < 0) {
-          const double a = fabs(Pn[r * GJ_NB + k]);
+          const double a = fabs(Pn[r * GJ_PS + k]);
           if (a > best || (a == best && r < bi)) { best = a; bi = r; }
         }
       }
@@ -71,9 +81,9 @@ __global__ void __launch_bounds__(GJ_T, 3) gj_kernel(double* __restrict__ Zall, 
         best = redv[0]; bi = redi[0];
         for (int w = 1; w < GJ_T / 32; ++w)
           if (redv[w] > best || (redv[w] == best && redi[w] < bi)) { best = redv[w]; bi = redi[w]; }
-        double pv = Pn[bi * GJ_NB + k];
+        double pv = Pn[bi * GJ_PS + k];
         if (!(best > 0.0)) pv = 1.0;                    // singular: flagged below
-        s_prow = bi; s_pval = pv;
+        s_prow = bi; s_pval = 1.0 / pv;         // reciprocal of the pivot
         colof[bi] = c0 + k;
         piv[c0 + k] = bi;
         if (!(best > 0.0)) redi[0] = -1;
@@ -81,28 +91,32 @@ __global__ void __launch_bounds__(GJ_T, 3) gj_kernel(double* __restrict__ Zall, 
       __syncthreads();
       if (redi[0] == -1) singular = 1;
       const int prow = s_prow;
-      const double pval = s_pval;
+      const double pinv = s_pval;
       // ---- in-place GJ step on the panel columns
       double pr[GJ_NB];
 #pragma unroll
-      for (int j = 0; j < GJ_NB; ++j) pr[j] = j < nb ? Pn[prow * GJ_NB + j] / pval : 0.0;
+      for (int j = 0; j < GJ_NB; ++j) pr[j] = j < nb ? Pn[prow * GJ_PS + j] * pinv : 0.0;
       double f[(GJ_MMAX + GJ_T - 1) / GJ_T];
 #pragma unroll
       for (int q = 0; q < (GJ_MMAX + GJ_T - 1) / GJ_T; ++q) {
         const int r = tid + q * GJ_T;
-        f[q] = r < m ? Pn[r * GJ_NB + k] : 0.0;
+        f[q] = r < m ? Pn[r * GJ_PS + k] : 0.0;
       }
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < (GJ_MMAX + GJ_T - 1) / GJ_T; ++q) {
         const int r = tid + q * GJ_T;
         if (r >= m) continue;
-        double* row = Pn + r * GJ_NB;
+        double* row = Pn + r * GJ_PS;
         if (r == prow) {
-          for (int j = 0; j < nb; ++j) row[j] = j == k ? 1.0 / pval : pr[j];
+#pragma unroll
+          for (int j = 0; j < GJ_NB; ++j)
+            if (j < nb) row[j] = j == k ? pinv : pr[j];
         } else {
           const double fr = f[q];
-          for (int j = 0; j < nb; ++j) row[j] = j == k ? -fr / pval : fma(-fr, pr[j], row[j]);
+#pragma unroll
+          for (int j = 0; j < GJ_NB; ++j)
+            if (j < nb) row[j] = j == k ? -fr * pinv : fma(-fr, pr[j], row[j]);
         }
       }
       __syncthreads();
@@ -110,51 +124,63 @@ __global__ void __launch_bounds__(GJ_T, 3) gj_kernel(double* __restrict__ Zall, 
     // ---- store the panel (augmented columns E[:, P]) and form U = Pn - I[:, P]
     for (int idx = tid; idx < m * nb; idx += GJ_T) {
       const int r = idx / nb, k = idx % nb;
-      const double v = Pn[r * GJ_NB + k];
+      const double v = Pn[r * GJ_PS + k];
       A[(size_t)r * m + c0 + k] = v;
     }
     __syncthreads();
-    for (int k = tid; k < nb; k += GJ_T) Pn[piv[c0 + k] * GJ_NB + k] -= 1.0;
+    for (int k = tid; k < nb; k += GJ_T) Pn[piv[c0 + k] * GJ_PS + k] -= 1.0;
     __syncthreads();
-    // ---- rank-nb update of every other column: A[:, j] += U A[P, j]
-    const int cg = tid % 16, rg = tid / 16;          // 2 columns x (m/16) rows per thread
+    // ---- rank-nb update of every other column: A[:, j] += U A[P, j], on the fp64
+    //      tensor cores: per 32-column tile warp w owns rows 32w .. 32w + 31 as
+    //      4 x 4 DMMA tiles (8 x 8), k = the panel's 16 columns in 4 k-steps;
+    //      A fragments (U) from the panel, B fragments (pivot rows) from AP
+    const int g = lane >> 2, t4 = lane & 3;
     for (int t0 = 0; t0 < m; t0 += GJ_TW) {
-      for (int idx = tid; idx < nb * GJ_TW; idx += GJ_T) {
+      for (int idx = tid; idx < GJ_NB * GJ_TW; idx += GJ_T) {
         const int k = idx / GJ_TW, jj = idx % GJ_TW;
         const int col = t0 + jj;
-        AP[k * GJ_TW + jj] = col < m ? A[(size_t)piv[c0 + k] * m + col] : 0.0;
+        AP[k * GJ_APS + jj] = (k < nb && col < m) ? A[(size_t)piv[c0 + k] * m + col] : 0.0;
       }
       __syncthreads();
-      constexpr int RQ = GJ_MMAX / 16;
-      double acc[RQ][2];
+      if (32 * wid < m) {
+        double acc[4][4][2];
 #pragma unroll
-      for (int q = 0; q < RQ; ++q) {
-        const int r = rg + 16 * q;
+        for (int rb = 0; rb < 4; ++rb) {
+          const int r = 32 * wid + 8 * rb + g;
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int col = t0 + cg * 2 + cc;
-          acc[q][cc] = (r < m && col < m) ? A[(size_t)r * m + col] : 0.0;
+          for (int cb = 0; cb < 4; ++cb) {
+            const int col = t0 + 8 * cb + 2 * t4;
+            acc[rb][cb][0] = (r < m && col < m) ? A[(size_t)r * m + col] : 0.0;
+            acc[rb][cb][1] = (r < m && col + 1 < m) ? A[(size_t)r * m + col + 1] : 0.0;
+          }
         }
-      }
-      for (int k = 0; k < nb; ++k) {
-        double ap[2];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) ap[cc] = AP[k * GJ_TW + cg * 2 + cc];
+        for (int ks = 0; ks < GJ_NB / 4; ++ks) {
+          const int kk = 4 * ks + t4;
+          double av[4], bv[4];
 #pragma unroll
-        for (int q = 0; q < RQ; ++q) {
-          const int r = rg + 16 * q;
-          const double u = r < m ? Pn[r * GJ_NB + k] : 0.0;
+          for (int rb = 0; rb < 4; ++rb) {
+            const int r = 32 * wid + 8 * rb + g;
+            av[rb] = (r < m && kk < nb) ? Pn[r * GJ_PS + kk] : 0.0;
+          }
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc) acc[q][cc] = fma(u, ap[cc], acc[q][cc]);
+          for (int cb = 0; cb < 4; ++cb) bv[cb] = AP[kk * GJ_APS + 8 * cb + g];
+#pragma unroll
+          for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) gj_dmma(acc[rb][cb], av[rb], bv[cb]);
         }
-      }
 #pragma unroll
-      for (int q = 0; q < RQ; ++q) {
-        const int r = rg + 16 * q;
+        for (int rb = 0; rb < 4; ++rb) {
+          const int r = 32 * wid + 8 * rb + g;
+          if (r >= m) continue;
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int col = t0 + cg * 2 + cc;
-          if (r < m && col < m && (col < c0 || col >= c0 + nb)) A[(size_t)r * m + col] = acc[q][cc];
+          for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int col = t0 + 8 * cb + 2 * t4 + h;
+              if (col < m && (col < c0 || col >= c0 + nb)) A[(size_t)r * m + col] = acc[rb][cb][h];
+            }
         }
       }
       __syncthreads();
