@@ -133,6 +133,7 @@ struct hbpdc_ctx {
   double *hsend = nullptr, *hrecv = nullptr;
   bool halo() const { return hl.active[0] || hl.active[2]; }
   int debug_sync = 0;              // HBPDC_DEBUG_SYNC=1: synchronise + check after every launch group
+  int trace = 0;                   // HBPDC_TRACE=1: per stage / Newton / GMRES trace on stderr
 };
 
 namespace {
@@ -1084,6 +1085,7 @@ hbpdc_status newton_batch(hbpdc_ctx* c, int B, double a1, double a2, double dt, 
       CKS(norm_host(c, w.G, n2, &gn));
       if (!std::isfinite(gn)) return fail(c, HBPDC_E_NONFINITE, "non-finite Newton residual");
       if (g0[i] < 0) g0[i] = gn;
+      if (c->trace) fprintf(stderr, "[hbpdc] newton sys %d it %d |G| %.3e |G0| %.3e floor %.3e\n", i, r, gn, g0[i], floor_[i]);
       if (c->st) c->st->final_newton_rel = g0[i] > 0 ? gn / g0[i] : 0.0;
       if (gn <= std::max(c->op.newton_rtol * g0[i], floor_[i])) { active[i] = false; continue; }
       if (r == c->op.newton_max) {
@@ -1110,6 +1112,8 @@ hbpdc_status newton_batch(hbpdc_ctx* c, int B, double a1, double a2, double dt, 
       idx[nb++] = i;
     }
     CKS(gmres_batch(c, gs, nb));
+    if (c->trace)
+      for (int q = 0; q < nb; ++q) fprintf(stderr, "[hbpdc] gmres sys %d its %d\n", idx[q], gs[q].total);
     for (int q = 0; q < nb; ++q) {
       SysWS& w = c->sys[idx[q]];
       CK(launch_axpby(1.0, w.dX, 1.0, w.X, n2, c->stream));         // X += dX
@@ -1167,6 +1171,7 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
     CK(launch_stage_combo(c->stw[cur][l - 1], 2, X, co, 0, nullptr, nullptr, c->sys[0].b, n, c->stream));
     CKS(ensure_pc_for(c, a1, a2, dt, c->Wn));
     const double* g = c->stw[cur][l - 1];
+    if (c->trace) fprintf(stderr, "[hbpdc] predictor stage %d\n", l + 1);
     hbpdc_status stt = newton_batch(c, 1, a1, a2, dt, &g);
     if (stt != HBPDC_OK) {
       c->err = "predictor stage " + std::to_string(l + 1) + ": " + c->err;
@@ -1203,6 +1208,7 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
         guess[q] = c->stw[cur][l];
       }
       CKS(ensure_pc_for(c, 1.0, 1.0, dt, c->Wn));
+      if (c->trace) fprintf(stderr, "[hbpdc] corrector sweep %d stages %d..%d\n", k + 1, l0 + 1, l0 + nb);
       hbpdc_status stt = newton_batch(c, nb, 1.0, 1.0, dt, guess);
       if (stt != HBPDC_OK) {
         c->err = "corrector sweep " + std::to_string(k + 1) + " stages " + std::to_string(l0 + 1) + ".." +
@@ -1429,6 +1435,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
     }
   }
   { const char* dbg = std::getenv("HBPDC_DEBUG_SYNC"); c->debug_sync = dbg && dbg[0] == '1'; }
+  { const char* tr = std::getenv("HBPDC_TRACE"); c->trace = tr && tr[0] == '1'; }   // solver trace on stderr
   hbpdc_status s = alloc_solver(c);
   *out = c;
   return s;

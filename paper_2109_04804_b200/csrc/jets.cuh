@@ -50,9 +50,10 @@ __device__ __forceinline__ J1 operator/(double s, J1 y) {
 }
 __device__ __forceinline__ double jval(J1 x) { return x.v; }
 __device__ __forceinline__ J1 jabs(J1 x) { return x.v >= 0.0 ? x : J1{-x.v, -x.a}; }
+// sqrt of a jet from one reciprocal square root: s = x r, s' = x' r / 2 (no division)
 __device__ __forceinline__ J1 jsqrt(J1 x) {
-  double s = sqrt(x.v);
-  return {s, 0.5 * x.a / s};
+  const double r = rsqrt(x.v);
+  return {x.v * r, 0.5 * r * x.a};
 }
 __device__ __forceinline__ J1 jmax(J1 x, J1 y) { return x.v >= y.v ? x : y; }
 
@@ -81,8 +82,8 @@ __device__ __forceinline__ J2 operator/(double s, J2 y) {
 __device__ __forceinline__ double jval(J2 x) { return x.v; }
 __device__ __forceinline__ J2 jabs(J2 x) { return x.v >= 0.0 ? x : J2{-x.v, -x.a, -x.b}; }
 __device__ __forceinline__ J2 jsqrt(J2 x) {
-  double s = sqrt(x.v), h = 0.5 / s;
-  return {s, h * x.a, h * x.b};
+  const double r = rsqrt(x.v), h = 0.5 * r;
+  return {x.v * r, h * x.a, h * x.b};
 }
 __device__ __forceinline__ J2 jmax(J2 x, J2 y) { return x.v >= y.v ? x : y; }
 

@@ -313,6 +313,9 @@ struct GemvRHS {
 // (104-105% of the measured copy bandwidth), NR = 6: 5.8 TB/s.
 // consumer warps (one CTA per SM)
 template <int NR> struct GwCons { static constexpr int value = 16; };
+#ifndef GW_WPR_MAXK
+#define GW_WPR_MAXK 4                            // right-hand sides one warp keeps in registers
+#endif
 constexpr int GW_NST_MAX = 16;                   // ring stages (runtime nst <= this)
 constexpr size_t GW_RING_BYTES = 160 * 1024;     // S bytes in flight per CTA (one CTA per SM)
 
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(32 * (GwCons<NR>::value + 1)) gemvN_tma_kernel
                                                                        const GemvRHS io, int m, int nE,
                                                                        int GW_NST) {
   constexpr int GW_CONS = GwCons<NR>::value;
-  constexpr int WPR = NR > 4 ? 2 : 1;            // warps per row (register budget: <= 4 RHS per warp)
+  constexpr int WPR = NR > GW_WPR_MAXK ? 2 : 1;  // warps per row
   constexpr int KPW = NR / WPR;                  // right-hand sides per warp
   constexpr int ROWS = GW_CONS;                  // rows per chunk
   constexpr int RPW = WPR;                       // rows per warp per chunk (interleaved chains)

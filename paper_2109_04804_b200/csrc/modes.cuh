@@ -25,6 +25,7 @@ struct OpArgs {
   double shift;
   double a1dt, c2;
   double epsw;          // FD step for the W direction (<= 0: quotient is 0)
+  double iepsw;         // 1 / epsw (0 if epsw <= 0), set by op_kernel
   const double* d_epsw; // if non-NULL, the FD step is read from device memory
   int m;                // doubles per element
   int nE;               // local elements; e >= nE addresses a ghost element (halo)
@@ -216,7 +217,7 @@ template <int EQ, int NODES> struct ModeJvpFD {
   __device__ static void comb(const Args& A, const J1* Fp, const J2* Fq, double (&c)[NCH][NV]) {
     const double ew = fd_step(A);
     if (ew > 0.0) {
-      const double ie = 1.0 / ew;
+      const double ie = A.iepsw;
       for (int v = 0; v < NV; ++v) {
         const double q1 = (Fp[v].v - Fq[v].v) * ie;
         const double q2 = (Fp[v].a - Fq[v].a) * ie;
@@ -277,7 +278,7 @@ template <int EQ, int NODES> struct ModeJvpFD {
     J2 F[DIM][NV];
     vol_flux_all<EQ, DIM>(pp, q, F);
     const double ew = fd_step(A);
-    const double ie = ew > 0.0 ? 1.0 / ew : 0.0;
+    const double ie = A.iepsw;
 #pragma unroll
     for (int d = 0; d < DIM; ++d)
 #pragma unroll
@@ -326,7 +327,7 @@ template <int EQ, int NODES> struct ModeJvpFD {
   __device__ static void face_combine(const Args& A, const PhysParams&, int, const double* rp, const double* rq,
                                       int rs, double (&c)[NCH][NV]) {
     const double ew = fd_step(A);
-    const double ie = ew > 0.0 ? 1.0 / ew : 0.0;
+    const double ie = A.iepsw;
     for (int v = 0; v < NV; ++v) {
       if (ew > 0.0) {
         const double q1 = (rp[rs * (2 * v)] - rq[rs * (3 * v)]) * ie;

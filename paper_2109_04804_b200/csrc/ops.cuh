@@ -384,6 +384,7 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g) {
   if constexpr (HasDevEps<typename Mode::Args>::value) {
     // the FD step lives in device memory (norm computed on the device): read it once
     if (Al.d_epsw) { Al.epsw = __ldg(Al.d_epsw); Al.d_epsw = nullptr; }
+    Al.iepsw = Al.epsw > 0.0 ? 1.0 / Al.epsw : 0.0;    // once per thread (was: per face and pass)
   }
   eval_slot<EQ, DIM, P, Mode>(Al, pp, g, e, slot, node, active, sF + slot * SLOT, out);
   if (active) Mode::epilogue(Al, e, node, out);
