@@ -450,6 +450,143 @@ __global__ void __launch_bounds__(32 * (GwCons<NR>::value + 1)) gemvN_tma_kernel
   }
 }
 
+// ---- fp64 tensor-core variant (all NR through the same kernel, so batched and
+// single-system outputs stay bitwise equal): per element, out (m x 8, NR used
+// columns) = S_e (m x m) X (m x 8) with mma.sync m8n8k4 f64.  Same producer /
+// ring as gemvN_tma_kernel (chunks of GD_ROWS rows).  Consumer warp w takes row
+// block w & 1 (8 rows) of each chunk and k-range w >> 1 (kw k-steps, two per
+// 16-byte shared load: column 4 kr kw + 8 p + 2 t + (ks & 1)), with its B
+// fragments (the right-hand sides) in registers for the whole element.  The 8
+// k-range partials of a row block are summed in warp order through shared
+// memory (one named barrier per chunk, double-buffered), so every output has a
+// fixed summation order independent of NR.  Why: the FMA kernel reads each S value once per
+// 3 right-hand sides and is issue-bound at 6 (5.6 TB/s); here one 16-byte
+// load feeds two DMMAs of all 8 columns.
+constexpr int GD_CONS = 16;                       // consumer warps
+constexpr int GD_ROWS = 16;                       // rows per chunk
+constexpr int GD_KWMAX = 8;                       // k-steps per warp (m <= 256)
+
+template <int NR>
+__global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const double* __restrict__ S,
+                                                                         const GemvRHS io, int m, int nE,
+                                                                         int GW_NST, int kw) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* ring = reinterpret_cast<double*>(smraw);                     // GW_NST x GD_ROWS x m
+  double* rhs = ring + (size_t)GW_NST * GD_ROWS * m;                   // 2 x NR x m
+  double* red = rhs + (size_t)2 * NR * m;                              // 2 x GD_CONS x 64
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(red + 2 * GD_CONS * 64);
+  unsigned long long *fullS = bars, *emptyS = bars + GW_NST_MAX, *fullR = bars + 2 * GW_NST_MAX, *emptyR = fullR + 2;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int cpe = (m + GD_ROWS - 1) / GD_ROWS;
+  const int nmy = blockIdx.x < nE ? (nE - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < GW_NST; ++q) { mbar_init(&fullS[q], 1); mbar_init(&emptyS[q], GD_CONS); }
+    for (int q = 0; q < 2; ++q) { mbar_init(&fullR[q], 1); mbar_init(&emptyR[q], GD_CONS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (wid == GD_CONS) {                                                // ---- producer
+    if (lane == 0) {
+      int c = 0;
+      for (int it = 0; it < nmy; ++it) {
+        const int e = blockIdx.x + it * gridDim.x;
+        const int rb = it & 1;
+        if (it >= 2) mbar_wait(&emptyR[rb], (unsigned)(((it >> 1) - 1) & 1));
+        mbar_expect_tx(&fullR[rb], (unsigned)(NR * m * sizeof(double)));
+        for (int k = 0; k < NR; ++k)
+          tma_load_1d(rhs + ((size_t)rb * NR + k) * m, io.in[k] + (size_t)e * m, (unsigned)(m * sizeof(double)),
+                      &fullR[rb]);
+        for (int ch = 0; ch < cpe; ++ch, ++c) {
+          const int st = c % GW_NST;
+          if (c >= GW_NST) mbar_wait(&emptyS[st], (unsigned)(((c / GW_NST) - 1) & 1));
+          const int r0 = ch * GD_ROWS;
+          const int rows = min(GD_ROWS, m - r0);
+          const unsigned bytes = (unsigned)(rows * m * sizeof(double));
+          mbar_expect_tx(&fullS[st], bytes);
+          tma_load_1d(ring + (size_t)st * GD_ROWS * m, S + ((size_t)e * m + r0) * m, bytes, &fullS[st]);
+        }
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  const int rbk = wid & 1, kr = wid >> 1;
+  const int cbase = 4 * kr * kw + 2 * t;          // + 8 p + (ks & 1)
+  int c = 0;
+  for (int it = 0; it < nmy; ++it) {
+    const int e = blockIdx.x + it * gridDim.x;
+    const int rb = it & 1;
+    mbar_wait(&fullR[rb], (unsigned)((it >> 1) & 1));
+    double b[GD_KWMAX];
+#pragma unroll
+    for (int ks = 0; ks < GD_KWMAX; ++ks) {
+      const int col = cbase + 8 * (ks >> 1) + (ks & 1);
+      b[ks] = (ks < kw && g < NR && col < m) ? rhs[((size_t)rb * NR + g) * m + col] : 0.0;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&emptyR[rb]);
+    for (int ch = 0; ch < cpe; ++ch, ++c) {
+      const int st = c % GW_NST;
+      const int buf = c & 1;
+      mbar_wait(&fullS[st], (unsigned)((c / GW_NST) & 1));
+      const double* ar = ring + ((size_t)st * GD_ROWS + 8 * rbk + g) * m;
+      double ae[2] = {0.0, 0.0}, ao[2] = {0.0, 0.0};
+#pragma unroll
+      for (int p = 0; p < GD_KWMAX / 2; ++p) {
+        if (2 * p < kw) {
+          const int col = cbase + 8 * p;
+          double2 a2 = make_double2(0.0, 0.0);
+          if (col < m) a2 = *reinterpret_cast<const double2*>(ar + col);
+          gj_dmma(ae, a2.x, b[2 * p]);
+          gj_dmma(ao, a2.y, b[2 * p + 1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyS[st]);
+      double* rw = red + ((size_t)buf * GD_CONS + wid) * 64 + g * 8 + 2 * t;
+      rw[0] = ae[0] + ao[0];
+      rw[1] = ae[1] + ao[1];
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * GD_CONS) : "memory");
+      if (threadIdx.x < GD_ROWS * NR) {
+        const int r = threadIdx.x / NR, j = threadIdx.x % NR;
+        const double* rr = red + (size_t)buf * GD_CONS * 64 + (r >> 3) * 64 + (r & 7) * 8 + j;
+        double sum = 0.0;
+#pragma unroll
+        for (int q = 0; q < GD_CONS / 2; ++q) sum += rr[(size_t)2 * q * 64];
+        const int row = ch * GD_ROWS + r;
+        if (row < m) io.out[j][(size_t)e * m + row] = sum;
+      }
+    }
+  }
+}
+
+template <int NR>
+static cudaError_t launch_gemv_dmma(const double* S, const GemvRHS& io, int m, int nE, cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    nsm = v;
+  }
+  if (m > 4 * GD_KWMAX * (GD_CONS / 2) || (m & 1)) return cudaErrorInvalidValue;
+  int kw = ((m + 3) / 4 + GD_CONS / 2 - 1) / (GD_CONS / 2);
+  kw += kw & 1;                                   // k-steps in pairs (16-byte loads)
+  const size_t chunk = (size_t)GD_ROWS * m * sizeof(double);
+  const size_t fixed = (size_t)2 * NR * m * sizeof(double) + (size_t)2 * GD_CONS * 64 * sizeof(double) +
+                       (2 * GW_NST_MAX + 4) * sizeof(unsigned long long);
+  const int nst = (int)std::max<size_t>(2, std::min<size_t>(GW_NST_MAX, GW_RING_BYTES / chunk));
+  const size_t smem = (size_t)nst * chunk + fixed;
+  constexpr int threads = 32 * (GD_CONS + 1);
+  cudaFuncSetAttribute(gemv_dmma_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_dmma_kernel<NR>, threads, smem);
+  const int grid = std::min(nE, nsm * std::max(occ, 1));
+  gemv_dmma_kernel<NR><<<grid, threads, smem, st>>>(S, io, m, nE, nst, kw);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
 template <int NR>
 static cudaError_t launch_gemvN(const double* S, const GemvRHS& io, int m, int nE, cudaStream_t st) {
   static int nsm = 0;
@@ -491,6 +628,17 @@ cudaError_t launch_block_gemv_multi(const double* S, int nr, const double* const
   if (nr < 1 || nr > GEMV_MAX_RHS || (m * sizeof(double)) % 16 != 0) return cudaErrorInvalidValue;
   GemvRHS io{};
   for (int k = 0; k < nr; ++k) { io.in[k] = in[k]; io.out[k] = out[k]; }
+#ifndef GEMV_USE_DMMA
+#define GEMV_USE_DMMA 1
+#endif
+  if (GEMV_USE_DMMA && m <= 4 * GD_KWMAX * (GD_CONS / 2)) {
+    switch (nr) {
+      case 2: return launch_gemv_dmma<2>(S, io, m, nE, st);
+      case 4: return launch_gemv_dmma<4>(S, io, m, nE, st);
+      case 6: return launch_gemv_dmma<6>(S, io, m, nE, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (nr) {
     case 2: return launch_gemvN<2>(S, io, m, nE, st);
     case 4: return launch_gemvN<4>(S, io, m, nE, st);

@@ -59,7 +59,7 @@ int main() {
   cudaStreamCreate(&st);
   bool ok = true;
   for (size_t L : {LMAX, (size_t)1000006}) {
-    for (int nq : {1, 9, 17, 64, 126}) {
+    for (int nq : {1, 9, 17, 64, 96, 126}) {
       const int r = nq * 8 + 64;
       const double bd = (double)(nq + 8) * L * 8, bu = (double)(nq + 16) * L * 8;
       const int nbm = block_dot_blocks_mma(L), nbt = block_dot_parts_tma();
