@@ -220,7 +220,7 @@ HBPDC_API hbpdc_status hbpdc_reset(hbpdc_ctx* ctx);
  * reporting.  enable=1 starts recording (and zeroes the counters), 0 stops.
  * kernel ids: 0 = precond GEMV (S streaming), 1 = JVP, 2 = residual,
  * 3 = Arnoldi dots, 4 = Arnoldi update, 5 = precond K-apply, 6 = precond
- * build.  alg_bytes = algorithmic HBM bytes of those launches (DESIGN.md
+ * build, 7 = fused Arnoldi update + re-projection (s-step, s = 8).  alg_bytes = algorithmic HBM bytes of those launches (DESIGN.md
  * byte model: each input and output touched once). */
 HBPDC_API hbpdc_status hbpdc_profile(hbpdc_ctx* ctx, int enable);
 HBPDC_API hbpdc_status hbpdc_profile_read(hbpdc_ctx* ctx, int kernel_id, long long* launches,

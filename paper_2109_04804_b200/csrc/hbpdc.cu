@@ -134,6 +134,7 @@ struct hbpdc_ctx {
   bool halo() const { return hl.active[0] || hl.active[2]; }
   int debug_sync = 0;              // HBPDC_DEBUG_SYNC=1: synchronise + check after every launch group
   int trace = 0;                   // HBPDC_TRACE=1: per stage / Newton / GMRES trace on stderr
+  int fuse_cgs = 1;                // HBPDC_FUSE_CGS=0: unfused block CGS2 passes (A/B checks)
 };
 
 namespace {
@@ -869,6 +870,28 @@ hbpdc_status block_update_dev(hbpdc_ctx* c, SysWS& w, int nq, double* W, int sb,
   return HBPDC_OK;
 }
 
+// fused W <- W - Q C (the first CGS2 update) and the rows of the second
+// projection [Q W]^T W of the updated block, one pass over Q (s = 8, short basis)
+hbpdc_status block_update_dots_host(hbpdc_ctx* c, SysWS& w, int nq, double* W, const std::vector<double>& C,
+                                    std::vector<double>& out) {
+  const size_t n2 = 2 * c->n;
+  const int sb = 8, nc = nq * sb, rows = nq * sb + sb * sb;
+  CK(cudaStreamSynchronize(c->stream));      // the pinned staging buffer is free
+  for (int q = 0; q < nc; ++q) w.hpin[q] = C[q];
+  CK(cudaMemcpyAsync(w.dy, w.hpin, nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  {
+    // algorithmic bytes: Q once, W read + written
+    ProfScope ps(c, 7, (double)(nq + 2 * sb) * n2 * 8.0);
+    CK(launch_block_update_dots_tma8(w.Vk, n2, nq, W, n2, w.dy, n2, w.partial, c->stream));
+    CK(launch_reduce_partials_n(w.partial, rows, block_fused_parts_tma(), w.dh, c->stream));
+    CKS(allreduce(c, w.dh, rows));
+  }
+  CK(cudaMemcpyAsync(w.hpin, w.dh, rows * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  out.assign(w.hpin, w.hpin + rows);
+  return HBPDC_OK;
+}
+
 // the block of s powers is complete: orthogonalise it, extend H, apply Givens
 hbpdc_status g_block(hbpdc_ctx* c, GState& g) {
   SysWS& w = *g.w;
@@ -880,9 +903,14 @@ hbpdc_status g_block(hbpdc_ctx* c, GState& g) {
   // pass 1 + 2: C1 = Q^T W, W1 = W - Q C1
   CKS(block_dots_host(c, w, nq, W, sb, r1));
   std::vector<double> C1(r1.begin(), r1.begin() + (size_t)nq * sb);
-  CKS(block_update_dev(c, w, nq, W, sb, C1, nullptr));
   // pass 3 + 4: C2 = Q^T W1, G2 = W1^T W1; Q_new = (W1 - Q C2) Rw^-1, Rw^T Rw = G2 - C2^T C2
-  CKS(block_dots_host(c, w, nq, W, sb, r2));
+  // (s = 8 with a short basis: pass 2 and the projection of pass 3 fused, Q read once)
+  if (sb == 8 && nq <= block_fused_max_nq() && c->fuse_cgs) {
+    CKS(block_update_dots_host(c, w, nq, W, C1, r2));
+  } else {
+    CKS(block_update_dev(c, w, nq, W, sb, C1, nullptr));
+    CKS(block_dots_host(c, w, nq, W, sb, r2));
+  }
   std::vector<double> C2(r2.begin(), r2.begin() + (size_t)nq * sb);
   T.assign((size_t)sb * sb, 0.0);
   for (int a = 0; a < sb; ++a)
@@ -1436,6 +1464,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   }
   { const char* dbg = std::getenv("HBPDC_DEBUG_SYNC"); c->debug_sync = dbg && dbg[0] == '1'; }
   { const char* tr = std::getenv("HBPDC_TRACE"); c->trace = tr && tr[0] == '1'; }   // solver trace on stderr
+  { const char* fc = std::getenv("HBPDC_FUSE_CGS"); c->fuse_cgs = !(fc && fc[0] == '0'); }
   hbpdc_status s = alloc_solver(c);
   *out = c;
   return s;

@@ -145,6 +145,12 @@ cudaError_t launch_block_dots_tma8(const double* Q, size_t ldq, int nq, const do
                                    double* part, cudaStream_t st);
 cudaError_t launch_block_update_tma8(const double* Q, size_t ldq, int nq, double* W, size_t ldw, const double* C,
                                      const double* Rinv, size_t L, cudaStream_t st);
+// fused W <- W - Q C (Rinv = I) and rows of [Q W]^T W of the updated W in one
+// pass over Q (1 <= nq <= block_fused_max_nq(); partials: block_fused_parts_tma() per row)
+int block_fused_parts_tma();
+int block_fused_max_nq();
+cudaError_t launch_block_update_dots_tma8(const double* Q, size_t ldq, int nq, double* W, size_t ldw,
+                                          const double* C, size_t L, double* part, cudaStream_t st);
 
 // kernel-launch counter (reported by hbpdc_launch_count)
 extern long long g_hbpdc_launches;

@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(32 * (GwCons<NR>::value + 1)) gemvN_tma_kernel
         const int col = lane + 32 * q;
         xr[k][q] = col < m ? rhs[((size_t)rb * NR + k0 + k) * m + col] : 0.0;
       }
+    fence_proxy_async_smem();            // order this lane's reads before the buffer's next bulk copy
     __syncwarp();
     if (lane == 0) mbar_arrive(&emptyR[rb]);
     for (int ch = 0; ch < cpe; ++ch, ++c) {
@@ -444,6 +445,7 @@ __global__ void __launch_bounds__(32 * (GwCons<NR>::value + 1)) gemvN_tma_kernel
           if (r < m && (lane & ((32 >> LV) - 1)) == 0 && idx < KPW) io.out[k0 + idx][(size_t)e * m + r] = p[0];
         }
       }
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyS[st]);
     }
@@ -523,6 +525,7 @@ __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const 
       const int col = cbase + 8 * (ks >> 1) + (ks & 1);
       b[ks] = (ks < kw && g < NR && col < m) ? rhs[((size_t)rb * NR + g) * m + col] : 0.0;
     }
+    fence_proxy_async_smem();            // order this lane's reads before the buffer's next bulk copy
     __syncwarp();
     if (lane == 0) mbar_arrive(&emptyR[rb]);
     for (int ch = 0; ch < cpe; ++ch, ++c) {
@@ -541,6 +544,7 @@ __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const 
           gj_dmma(ao, a2.y, b[2 * p + 1]);
         }
       }
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyS[st]);
       double* rw = red + ((size_t)buf * GD_CONS + wid) * 64 + g * 8 + 2 * t;

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(32 * (TD_W + 1), 1) block_dots_tma8_kernel(con
           const double* sa = ring + (size_t)st * 8 * TD_P + g * TD_P + (TD_E / TD_W) * wid + t;
 #pragma unroll
           for (int ks = 0; ks < KW; ++ks) dmma(acc[tg][ks % TD_C], sa[4 * ks], b[ks]);
+          fence_proxy_async_smem();      // order this lane's reads before the stage's next bulk copy
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[st]);
           ++k;
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(288, 1) block_update_tma8_kernel(const double*
 #pragma unroll
         for (int nb = 0; nb < TU_NB; ++nb) dmma(acc[nb], a, sb[(4 * kk + t) * TU_P + nb * 8]);
       }
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
@@ -302,6 +304,213 @@ cudaError_t launch_block_update_tma8(const double* Q, size_t ldq, int nq, double
     attr = smem;
   }
   block_update_tma8_kernel<<<block_dot_blocks_tma(), 288, smem, st>>>(Q, ldq, nq, W, ldw, C, Rinv, L);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// Fused first update + second projection of block CGS2 (s = 8):
+//   W1 = W - Q C1                      (written back to W)
+//   part rows j*8 + l   : Q_j . W1_l   (j < nq)
+//   part rows nq*8 + a*8 + b : W1_a . W1_b
+// i.e. block_update (Rinv = I) followed by block_dots, in ONE pass over Q from
+// HBM: per chunk the producer streams the Q tiles twice, the second time from
+// L2 (a chunk's tiles are nq x 2 KB per CTA, ~40 MB over all CTAs at nq = 126,
+// well inside the 126 MB L2).  Phase U is block_update_tma8's consumer loop;
+// W1 stays in registers, its B fragments (element 4 kk + t of an n-block,
+// vector g) are gathered by shuffles, and phase D accumulates Q_tile^T W1 on
+// the tensor cores into per-warp accumulators that persist over the CTA's
+// chunks (one partial per consumer warp, as block_dots_tma8).
+// ============================================================================
+namespace {
+constexpr int TF_MAXT = 20;        // Q tiles (nq <= 160) kept in accumulators
+#ifndef TF_E_
+#define TF_E_ 512
+#endif
+#ifndef TF_PAR_
+#define TF_PAR_ 1
+#endif
+constexpr int TF_E = TF_E_;        // elements per chunk (row copies of 8 TF_E bytes)
+constexpr int TF_P = TF_E + 4;     // padded row: conflict-free fragments
+#ifndef TF_R_
+#define TF_R_ ((200 * 1024) / (8 * TF_P * 8))
+#endif
+constexpr int TF_R = TF_R_;        // ring stages
+constexpr int TF_NB = TF_E / 64;   // n-blocks per consumer warp
+}
+int block_fused_parts_tma() { return 8 * block_dot_blocks_tma(); }
+int block_fused_max_nq() { return 8 * TF_MAXT; }
+
+__global__ void __launch_bounds__(288, 1) block_update_dots_tma8_kernel(const double* __restrict__ Q, size_t ldq,
+                                                                        int nq, double* __restrict__ W, size_t ldw,
+                                                                        const double* __restrict__ C, size_t L,
+                                                                        double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nq8 = (nq + 7) / 8 * 8;
+  double* ring = reinterpret_cast<double*>(smraw);                            // TF_R x 8 x TF_P
+  double* sC = ring + (size_t)TF_R * 8 * TF_P;                                // C1 (zero padded to nq8 x 8)
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sC + (size_t)nq8 * 8);
+  unsigned long long* empty = full + TF_R;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < TF_R * 8 * TF_P; k += blockDim.x) ring[k] = 0.0;
+  for (int k = threadIdx.x; k < nq8 * 8; k += blockDim.x) sC[k] = k < nq * 8 ? C[k] : 0.0;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < TF_R; ++r) { mbar_init(&full[r], 1); mbar_init(&empty[r], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  const int T = nq8 / 8;
+  const size_t nch = (L + TF_E - 1) / TF_E;
+  const size_t nmy = blockIdx.x < nch ? (nch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (wid == 8) {                                                             // ---- producer
+    // lane 0 waits / arms the stage, lanes 0..7 issue one row copy each
+    size_t k = 0;
+    for (size_t ci = 0; ci < nmy; ++ci) {
+      const size_t e0 = (blockIdx.x + ci * gridDim.x) * TF_E;
+      const int ne = (int)min((size_t)TF_E, L - e0);
+      for (int pass = 0; pass < 2; ++pass)                                    // phase U, then phase D (L2)
+        for (int tile = 0; tile < T; ++tile, ++k) {
+          const int st = (int)(k % TF_R);
+          const int nrow = min(8, nq - 8 * tile);
+          if (lane == 0) {
+            if (k >= (size_t)TF_R) mbar_wait(&empty[st], (unsigned)(((k / TF_R) - 1) & 1));
+            mbar_expect_tx(&full[st], (unsigned)(nrow * ne * sizeof(double)));
+          }
+          __syncwarp();
+          if (TF_PAR_) {
+            if (lane < nrow)
+              tma_load_1d(ring + ((size_t)st * 8 + lane) * TF_P, Q + (size_t)(8 * tile + lane) * ldq + e0,
+                          (unsigned)(ne * sizeof(double)), &full[st]);
+          } else if (lane == 0) {
+            for (int r = 0; r < nrow; ++r)
+              tma_load_1d(ring + ((size_t)st * 8 + r) * TF_P, Q + (size_t)(8 * tile + r) * ldq + e0,
+                          (unsigned)(ne * sizeof(double)), &full[st]);
+          }
+        }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  auto load_w = [&](size_t ci, double (&o)[TF_NB][2]) {
+    const size_t e0 = (blockIdx.x + ci * gridDim.x) * TF_E;
+    const double* wg = W + (size_t)g * ldw;
+#pragma unroll
+    for (int nb = 0; nb < TF_NB; ++nb) {
+      const size_t e = e0 + (size_t)(wid * TF_NB + nb) * 8 + 2 * t;
+      if (e + 1 < L) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(wg + e));
+        o[nb][0] = v.x;
+        o[nb][1] = v.y;
+      } else {
+        o[nb][0] = e < L ? wg[e] : 0.0;
+        o[nb][1] = 0.0;
+      }
+    }
+  };
+  double dacc[TF_MAXT][2], gacc[2] = {0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < TF_MAXT; ++i) { dacc[i][0] = 0.0; dacc[i][1] = 0.0; }
+  size_t k = 0;
+  for (size_t ci = 0; ci < nmy; ++ci) {
+    const size_t e0 = (blockIdx.x + ci * gridDim.x) * TF_E;
+    double wv[TF_NB][2];
+    load_w(ci, wv);                    // consumed after phase U: the latency hides behind it
+    // ---- phase U: D = C1^T Q over the chunk (block_update_tma8)
+    double acc[TF_NB][2];
+#pragma unroll
+    for (int nb = 0; nb < TF_NB; ++nb) { acc[nb][0] = 0.0; acc[nb][1] = 0.0; }
+    for (int tile = 0; tile < T; ++tile, ++k) {
+      const int st = (int)(k % TF_R);
+      mbar_wait(&full[st], (unsigned)((k / TF_R) & 1));
+      const double* sb = ring + (size_t)st * 8 * TF_P + (size_t)(wid * TF_NB) * 8 + g;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const double a = sC[(8 * tile + 4 * kk + t) * 8 + g];
+#pragma unroll
+        for (int nb = 0; nb < TF_NB; ++nb) dmma(acc[nb], a, sb[(4 * kk + t) * TF_P + nb * 8]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    // W1 = W - D (lane (g, t): vector g, elements 2t, 2t + 1 of each n-block) -> W
+    double (&w1)[TF_NB][2] = acc;
+#pragma unroll
+    for (int nb = 0; nb < TF_NB; ++nb) {
+      const size_t e = e0 + (size_t)(wid * TF_NB + nb) * 8 + 2 * t;
+      w1[nb][0] = e < L ? wv[nb][0] - acc[nb][0] : 0.0;          // beyond L: 0 (stale ring rows)
+      w1[nb][1] = e + 1 < L ? wv[nb][1] - acc[nb][1] : 0.0;
+      double* wg = W + (size_t)g * ldw;
+      if (e + 1 < L) {
+        *reinterpret_cast<double2*>(wg + e) = make_double2(w1[nb][0], w1[nb][1]);
+      } else if (e < L) {
+        wg[e] = w1[nb][0];
+      }
+    }
+    // B fragments of W1: k-step (nb, kk) covers elements 4 kk + t of n-block nb,
+    // held by lane g*4 + 2kk + t/2 at position t & 1 (elements >= L are 0)
+    double bf[TF_NB][2];
+#pragma unroll
+    for (int nb = 0; nb < TF_NB; ++nb)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int src = g * 4 + 2 * kk + (t >> 1);
+        const double v0 = __shfl_sync(0xffffffffu, w1[nb][0], src);
+        const double v1 = __shfl_sync(0xffffffffu, w1[nb][1], src);
+        bf[nb][kk] = (t & 1) ? v1 : v0;
+      }
+    // Gram W1^T W1: A fragment (vector g, element k) equals the B fragment
+#pragma unroll
+    for (int nb = 0; nb < TF_NB; ++nb)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) dmma(gacc, bf[nb][kk], bf[nb][kk]);
+    // ---- phase D: Q_tile^T W1 over the chunk (tiles re-streamed, from L2)
+#pragma unroll
+    for (int tile = 0; tile < TF_MAXT; ++tile) {
+      if (tile < T) {
+        const int st = (int)(k % TF_R);
+        mbar_wait(&full[st], (unsigned)((k / TF_R) & 1));
+        const double* sa = ring + (size_t)st * 8 * TF_P + (size_t)g * TF_P + (size_t)(wid * TF_NB) * 8 + t;
+#pragma unroll
+        for (int nb = 0; nb < TF_NB; ++nb)
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) dmma(dacc[tile], sa[nb * 8 + 4 * kk], bf[nb][kk]);
+        fence_proxy_async_smem();      // order this lane's reads before the stage's next bulk copy
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        ++k;
+      }
+    }
+  }
+  // one partial per consumer warp: part[row][8 * blockIdx + wid]
+  const size_t col = (size_t)blockIdx.x * 8 + wid, ncol = (size_t)gridDim.x * 8;
+#pragma unroll
+  for (int tile = 0; tile < TF_MAXT; ++tile) {
+    const int j = 8 * tile + g;
+    if (tile < T && j < nq) {
+      part[((size_t)j * 8 + 2 * t) * ncol + col] = dacc[tile][0];
+      part[((size_t)j * 8 + 2 * t + 1) * ncol + col] = dacc[tile][1];
+    }
+  }
+  part[((size_t)nq * 8 + g * 8 + 2 * t) * ncol + col] = gacc[0];
+  part[((size_t)nq * 8 + g * 8 + 2 * t + 1) * ncol + col] = gacc[1];
+}
+
+cudaError_t launch_block_update_dots_tma8(const double* Q, size_t ldq, int nq, double* W, size_t ldw,
+                                          const double* C, size_t L, double* part, cudaStream_t st) {
+  if (nq < 1 || nq > block_fused_max_nq() || (ldq & 1) || (ldw & 1)) return cudaErrorInvalidValue;
+  const int nq8 = (nq + 7) / 8 * 8;
+  const size_t smem = ((size_t)TF_R * 8 * TF_P + (size_t)nq8 * 8) * sizeof(double) +
+                      2 * TF_R * sizeof(unsigned long long);
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(block_update_dots_tma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return cudaErrorInvalidValue;
+    attr = smem;
+  }
+  block_update_dots_tma8_kernel<<<block_dot_blocks_tma(), 288, smem, st>>>(Q, ldq, nq, W, ldw, C, L, part);
   hbpdc_count_launch();
   return cudaGetLastError();
 }

@@ -316,7 +316,7 @@ class Context:
         self._check(self.lib.hbpdc_profile(self.h, int(enable)))
 
     PROFILE_IDS = {"gemv": 0, "jvp": 1, "residual": 2, "arnoldi_dots": 3, "arnoldi_update": 4,
-                   "kapply": 5, "build": 6}
+                   "kapply": 5, "build": 6, "arnoldi_fused": 7}
 
     def profile_read(self, kernel_id):
         """(launches, total_ms, algorithmic_bytes) of a profiled kernel id."""

@@ -26,9 +26,10 @@ float timeit(F f, cudaStream_t st, int R = 5) {
   return ms / R;
 }
 
-int main() {
-  const size_t LMAX = 8388608;
-  const int NQMAX = 130;
+int main(int argc, char** argv) {
+  const bool quick = argc > 1;             // fused kernel check only, small L (for compute-sanitizer)
+  const size_t LMAX = quick ? 262144 : 8388608;
+  const int NQMAX = 160;
   double *Q, *W, *W2, *W3, *part, *out1, *out2, *C;
   cudaMalloc(&Q, (size_t)NQMAX * LMAX * 8);
   cudaMalloc(&W, 8 * LMAX * 8);
@@ -59,6 +60,7 @@ int main() {
   cudaStreamCreate(&st);
   bool ok = true;
   for (size_t L : {LMAX, (size_t)1000006}) {
+    if (quick) break;
     for (int nq : {1, 9, 17, 64, 96, 126}) {
       const int r = nq * 8 + 64;
       const double bd = (double)(nq + 8) * L * 8, bu = (double)(nq + 16) * L * 8;
@@ -98,6 +100,50 @@ int main() {
              "update: mma %7.1f us %5.0f GB/s | tma %7.1f us %5.0f GB/s | diff %.1e tail %.1e\n",
              L, nq, t1 * 1e3, bd / (t1 * 1e-3) / 1e9, t2 * 1e3, bd / (t2 * 1e-3) / 1e9, rd, t3 * 1e3,
              bu / (t3 * 1e-3) / 1e9, t4 * 1e3, bu / (t4 * 1e-3) / 1e9, ru, tail);
+    }
+  }
+  // fused update + re-projection vs update then dots (separate kernels)
+  double* part2;
+  cudaMalloc(&part2, (size_t)rows * block_fused_parts_tma() * 8);
+  for (size_t L : {LMAX, quick ? (size_t)100006 : (size_t)1000006}) {
+    for (int nq : {1, 9, 17, 64, 126, 152}) {
+      if (quick && nq != 17) continue;
+      const int r = nq * 8 + 64;
+      cudaMemcpy(W2, W, 8 * LMAX * 8, cudaMemcpyDeviceToDevice);
+      cudaMemcpy(W3, W, 8 * LMAX * 8, cudaMemcpyDeviceToDevice);
+      launch_block_update_mma(Q, LMAX, nq, W2, LMAX, 8, C, nullptr, L, st);
+      launch_block_dots_mma(Q, LMAX, nq, W2, LMAX, 8, L, part, st);
+      launch_reduce_partials_n(part, r, block_dot_blocks_mma(L), out1, st);
+      launch_block_update_dots_tma8(Q, LMAX, nq, W3, LMAX, C, L, part2, st);
+      launch_reduce_partials_n(part2, r, block_fused_parts_tma(), out2, st);
+      std::vector<double> a(r), b(r);
+      cudaMemcpy(a.data(), out1, r * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(b.data(), out2, r * 8, cudaMemcpyDeviceToHost);
+      double md = 0, mx = 0;
+      for (int i = 0; i < r; ++i) { md = std::max(md, std::abs(a[i] - b[i])); mx = std::max(mx, std::abs(a[i])); }
+      for (int i = 0; i < r; ++i)
+        if (std::abs(a[i] - b[i]) > 1e-12 * mx) printf("   bad row %d (j %d l %d): %.6e vs %.6e\n", i, i / 8, i % 8, a[i], b[i]);
+      std::vector<double> u(8 * LMAX), v(8 * LMAX);
+      cudaMemcpy(u.data(), W2, 8 * LMAX * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(v.data(), W3, 8 * LMAX * 8, cudaMemcpyDeviceToHost);
+      double num = 0, den = 0, tail = 0;
+      for (int k = 0; k < 8; ++k)
+        for (size_t i = 0; i < LMAX; ++i) {
+          const double x = u[k * LMAX + i], y = v[k * LMAX + i];
+          if (i < L) { num += (x - y) * (x - y); den += x * x; }
+          else tail = std::max(tail, std::abs(y - x));
+        }
+      cudaMemcpy(W2, W, 8 * LMAX * 8, cudaMemcpyDeviceToDevice);
+      float ts = timeit([&] {
+        launch_block_update_mma(Q, LMAX, nq, W2, LMAX, 8, C, nullptr, L, st);
+        launch_block_dots_mma(Q, LMAX, nq, W2, LMAX, 8, L, part, st);
+      }, st);
+      float tf = timeit([&] { launch_block_update_dots_tma8(Q, LMAX, nq, W2, LMAX, C, L, part2, st); }, st);
+      const double rd = md / mx, ru = std::sqrt(num / den);
+      ok = ok && rd < 1e-12 && ru < 1e-13 && tail == 0.0;
+      const double bq = (double)nq * L * 8;
+      printf("L=%zu nq=%3d fused: separate %7.1f us | fused %7.1f us (Q stream %5.0f GB/s) | dots diff %.1e W diff %.1e tail %.1e\n",
+             L, nq, ts * 1e3, tf * 1e3, bq / (tf * 1e-3) / 1e9, rd, ru, tail);
     }
   }
   printf("status: %s  check: %s\n", cudaGetErrorString(cudaGetLastError()), ok ? "OK" : "FAIL");
