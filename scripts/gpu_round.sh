@@ -14,9 +14,14 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=
 cat $OUT/bench.json
 SHORT="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline"
 timeout 400 $SHORT > $OUT/short_plain.log 2>&1 && \
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 30000 --csv \
     --log-file $OUT/launches.csv $SHORT > $OUT/ncu_launches.log 2>&1; echo "ncu launches rc=$?" | tee -a $OUT/summary.txt
-for K in gemvN_tma block_dots_mma block_update_mma op_kernel; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 30 -c 1 \
-      -o $OUT/prof_$K $SHORT > $OUT/ncu_full_$K.log 2>&1; echo "ncu full $K rc=$?" | tee -a $OUT/summary.txt
+# representative launches: the 6-RHS GEMV of a corrector sweep, the fused CGS pass and the
+# block dots at a grown basis, the FD JVP, the Gauss-Jordan build
+for KS in "gemv_dmma_kernel<\(int\)6>:20" "gemv_dmma_kernel<\(int\)2>:20" "block_update_dots_tma8:60" "block_dots_mma_kernel:40" \
+          "block_update_mma_kernel:40" "ModeJvpFD:200" "ModeKApply:200" "gj_kernel:2"; do
+  K=${KS%%:*}; S=${KS##*:}; F=$(echo $K | tr -c 'a-zA-Z0-9_\n' '_')
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k "regex:$K" -s $S -c 1 -o $OUT/prof_$F $SHORT > $OUT/ncu_full_$F.log 2>&1
+  echo "ncu full $K rc=$?" | tee -a $OUT/summary.txt
 done
