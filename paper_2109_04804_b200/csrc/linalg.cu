@@ -26,7 +26,7 @@ __device__ __forceinline__ void gj_dmma(double (&d)[2], double a, double b) {
 }
 constexpr int GJ_T = 256;    // threads
 constexpr int GJ_NB = 16;    // panel width
-constexpr int GJ_PS = GJ_NB + 1;   // panel row stride in shared memory
+constexpr int GJ_PS = GJ_NB + 4;   // panel row stride (== 4 mod 16: conflict-free DMMA A fragments)
 constexpr int GJ_TW = 32;    // column tile of the rank-NB update
 constexpr int GJ_APS = GJ_TW + 4;  // pivot-row tile stride (conflict-free B fragments)
 constexpr int GJ_MMAX = 256;
@@ -43,32 +43,32 @@ __global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ 
   __shared__ int colof[GJ_MMAX];    // column whose pivot row is r (-1: unused)
   __shared__ double redv[GJ_T / 32];
   __shared__ int redi[GJ_T / 32];
-  __shared__ int s_prow;
+  __shared__ double prb[GJ_NB];      // pivot row / pivot of the current column
   __shared__ double s_pval;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double* A = Zall + (size_t)blockIdx.x * m * m;
   double* S = Sall + (size_t)blockIdx.x * m * m;
-  for (int r = tid; r < m; r += GJ_T) colof[r] = -1;
+  for (int q = tid; q < m; q += GJ_T) colof[q] = -1;
   int singular = 0;
   __syncthreads();
 
+  // thread r owns panel row r in registers (m <= GJ_T): two barriers per column
+  const int r = tid;
+  bool used = false;
   for (int c0 = 0; c0 < m; c0 += GJ_NB) {
     const int nb = min(GJ_NB, m - c0);
-    for (int idx = tid; idx < m * nb; idx += GJ_T) {
-      const int r = idx / nb, k = idx % nb;
-      Pn[r * GJ_PS + k] = A[(size_t)r * m + c0 + k];
-    }
-    __syncthreads();
-    for (int k = 0; k < nb; ++k) {
-      // ---- pivot search: max |Pn[r][k]| over unused rows (ties: smallest r)
-      double best = -1.0;
-      int bi = 0x7fffffff;
-      for (int r = tid; r < m; r += GJ_T) {
-        if (colof[r] < 0) {
-          const double a = fabs(Pn[r * GJ_PS + k]);
-          if (a > best || (a == best && r < bi)) { best = a; bi = r; }
-        }
-      }
+    {
+    double row[GJ_NB];
+#pragma unroll
+    for (int j = 0; j < GJ_NB; ++j) row[j] = (r < m && j < nb) ? A[(size_t)r * m + c0 + j] : 0.0;
+    int mycol = -1;                                  // panel column this row pivoted
+#pragma unroll
+    for (int k = 0; k < GJ_NB; ++k) {
+      if (k >= nb) break;
+      // ---- pivot search: max |row[k]| over unused rows (ties: smallest r)
+      const bool cand = r < m && !used;
+      double best = cand ? fabs(row[k]) : -1.0;
+      int bi = cand ? r : 0x7fffffff;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -77,58 +77,46 @@ __global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ 
       }
       if (lane == 0) { redv[wid] = best; redi[wid] = bi; }
       __syncthreads();
-      if (tid == 0) {
-        best = redv[0]; bi = redi[0];
-        for (int w = 1; w < GJ_T / 32; ++w)
-          if (redv[w] > best || (redv[w] == best && redi[w] < bi)) { best = redv[w]; bi = redi[w]; }
-        double pv = Pn[bi * GJ_PS + k];
-        if (!(best > 0.0)) pv = 1.0;                    // singular: flagged below
-        s_prow = bi; s_pval = 1.0 / pv;         // reciprocal of the pivot
-        colof[bi] = c0 + k;
-        piv[c0 + k] = bi;
-        if (!(best > 0.0)) redi[0] = -1;
+      best = redv[0]; bi = redi[0];
+#pragma unroll
+      for (int w = 1; w < GJ_T / 32; ++w)
+        if (redv[w] > best || (redv[w] == best && redi[w] < bi)) { best = redv[w]; bi = redi[w]; }
+      const bool sing = !(best > 0.0);
+      if (r == bi) {                                 // the pivot row: broadcast it scaled by 1/pivot
+        const double pinv = 1.0 / (sing ? 1.0 : row[k]);
+#pragma unroll
+        for (int j = 0; j < GJ_NB; ++j) prb[j] = row[j] * pinv;
+        s_pval = pinv;
+        used = true;
+        mycol = k;
+        colof[r] = c0 + k;
+        piv[c0 + k] = r;
       }
       __syncthreads();
-      if (redi[0] == -1) singular = 1;
-      const int prow = s_prow;
+      if (sing) singular = 1;
       const double pinv = s_pval;
       // ---- in-place GJ step on the panel columns
-      double pr[GJ_NB];
+      if (r < m) {
+        if (r == bi) {
 #pragma unroll
-      for (int j = 0; j < GJ_NB; ++j) pr[j] = j < nb ? Pn[prow * GJ_PS + j] * pinv : 0.0;
-      double f[(GJ_MMAX + GJ_T - 1) / GJ_T];
-#pragma unroll
-      for (int q = 0; q < (GJ_MMAX + GJ_T - 1) / GJ_T; ++q) {
-        const int r = tid + q * GJ_T;
-        f[q] = r < m ? Pn[r * GJ_PS + k] : 0.0;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < (GJ_MMAX + GJ_T - 1) / GJ_T; ++q) {
-        const int r = tid + q * GJ_T;
-        if (r >= m) continue;
-        double* row = Pn + r * GJ_PS;
-        if (r == prow) {
-#pragma unroll
-          for (int j = 0; j < GJ_NB; ++j)
-            if (j < nb) row[j] = j == k ? pinv : pr[j];
+          for (int j = 0; j < GJ_NB; ++j) row[j] = j == k ? pinv : prb[j];
         } else {
-          const double fr = f[q];
+          const double fr = row[k];
 #pragma unroll
-          for (int j = 0; j < GJ_NB; ++j)
-            if (j < nb) row[j] = j == k ? -fr * pinv : fma(-fr, pr[j], row[j]);
+          for (int j = 0; j < GJ_NB; ++j) row[j] = j == k ? -fr * pinv : fma(-fr, prb[j], row[j]);
         }
       }
-      __syncthreads();
     }
-    // ---- store the panel (augmented columns E[:, P]) and form U = Pn - I[:, P]
-    for (int idx = tid; idx < m * nb; idx += GJ_T) {
-      const int r = idx / nb, k = idx % nb;
-      const double v = Pn[r * GJ_PS + k];
-      A[(size_t)r * m + c0 + k] = v;
+    // ---- store the panel (augmented columns E[:, P]); U = panel - I[:, P] to shared memory
+    if (r < m) {
+#pragma unroll
+      for (int j = 0; j < GJ_NB; ++j)
+        if (j < nb) {
+          A[(size_t)r * m + c0 + j] = row[j];
+          Pn[r * GJ_PS + j] = j == mycol ? row[j] - 1.0 : row[j];
+        }
     }
-    __syncthreads();
-    for (int k = tid; k < nb; k += GJ_T) Pn[piv[c0 + k] * GJ_PS + k] -= 1.0;
+    }
     __syncthreads();
     // ---- rank-nb update of every other column: A[:, j] += U A[P, j], on the fp64
     //      tensor cores: per 32-column tile warp w owns rows 32w .. 32w + 31 as

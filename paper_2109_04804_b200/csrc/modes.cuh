@@ -48,6 +48,10 @@ __device__ __forceinline__ void ld_state(const double* G, const double* Gg, int 
 // (halo copies of a neighbouring rank's face traces, same layout, comm.h)
 #define FV(F, e, v, node) ((e) < A.nE ? A.F[IDX(e, v, node)] : A.g##F[IDX((e) - A.nE, v, node)])
 
+// modes whose neighbour states are frozen (no tangent) declare FROZEN_NBR and load_value()
+template <class M, class = void> struct FrozenNbr : std::false_type {};
+template <class M> struct FrozenNbr<M, std::void_t<decltype(M::FROZEN_NBR)>> : std::bool_constant<M::FROZEN_NBR> {};
+
 // Single-jet modes: Derived supplies  using J; load_w; comb(A, const J* F, c).
 template <int EQ, int NODES, class Derived, class J, int NCH_>
 struct OneJetMode {
@@ -72,6 +76,24 @@ struct OneJetMode {
                                    int nnode, int slot, bool plus, int d, int part, double* raw,
                                    int rs) {
     const bool use_own = (part == 0) == plus;
+    if constexpr (FrozenNbr<Derived>::value && EQ != 2) {
+      // the neighbour's state carries no tangent (K_i is the element-diagonal block):
+      // its half flux in plain doubles, tangent slots zero (same values as the jet)
+      if (!use_own) {
+        NodeState<EQ, double> sd;
+        Derived::load_value(A, nb, nnode, sd.w);
+        constexpr int NR = 2 * NV + 1, JN = JetN<J>::value;
+        double tmp[NR];
+        half_flux<EQ, double>(pp, sd, d, tmp, 1);
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+          raw[rs * (i * JN)] = tmp[i];
+#pragma unroll
+          for (int c = 1; c < JN; ++c) raw[rs * (i * JN + c)] = 0.0;
+        }
+        return;
+      }
+    }
     State st;
     load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
     half_flux<EQ, J>(pp, st.s, d, raw, rs);
@@ -414,6 +436,10 @@ template <int EQ, int NODES> struct ModeJvpLinear {
 //   top = U - c2 K V,   bottom = V + K (U - a1dt V).
 template <int EQ, int NODES> struct ModeKApply : OneJetMode<EQ, NODES, ModeKApply<EQ, NODES>, J2, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
+  static constexpr bool FROZEN_NBR = true;
+  __device__ static void load_value(const OpArgs& A, int e, int node, double* w) {
+    for (int v = 0; v < NV; ++v) w[v] = FV(W, e, v, node);
+  }
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, J2* w, bool nbr) {
     for (int v = 0; v < NV; ++v) {
