@@ -892,6 +892,39 @@ hbpdc_status block_update_dots_host(hbpdc_ctx* c, SysWS& w, int nq, double* W, c
   return HBPDC_OK;
 }
 
+// s = 8: second update W <- (W - Q C) Rinv with the Gram rows of the updated block
+// computed in the same pass (the CholQR2 reduction), then summed to the host
+hbpdc_status block_update_gram_host(hbpdc_ctx* c, SysWS& w, int nq, double* W, const std::vector<double>& C,
+                                    const std::vector<double>& Rinv, std::vector<double>& out) {
+  const size_t n2 = 2 * c->n;
+  const int sb = 8, nc = nq * sb, rows = sb * sb;
+  CK(cudaStreamSynchronize(c->stream));      // the pinned staging buffer is free
+  for (int q = 0; q < nc; ++q) w.hpin[q] = C[q];
+  for (int q = 0; q < sb * sb; ++q) w.hpin[nc + q] = Rinv[q];
+  CK(cudaMemcpyAsync(w.dy, w.hpin, (nc + sb * sb) * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  {
+    ProfScope ps(c, 4, (double)(nq + 2 * sb) * n2 * 8.0);
+    CK(launch_block_update_tma8(w.Vk, n2, nq, W, n2, w.dy, w.dy + nc, n2, c->stream, w.partial));
+    CK(launch_reduce_partials_n(w.partial, rows, block_fused_parts_tma(), w.dh, c->stream));
+    CKS(allreduce(c, w.dh, rows));
+  }
+  CK(cudaMemcpyAsync(w.hpin, w.dh, rows * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  out.assign(w.hpin, w.hpin + rows);
+  return HBPDC_OK;
+}
+
+// s = 8: W <- W Rinv (second CholQR pass), one streaming pass over the block
+hbpdc_status block_scale_dev(hbpdc_ctx* c, SysWS& w, double* W, const std::vector<double>& Rinv) {
+  const size_t n2 = 2 * c->n;
+  CK(cudaStreamSynchronize(c->stream));
+  for (int q = 0; q < 64; ++q) w.hpin[q] = Rinv[q];
+  CK(cudaMemcpyAsync(w.dy, w.hpin, 64 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  ProfScope ps(c, 4, 2.0 * 8 * n2 * 8.0);
+  CK(launch_block_scale_w8(W, n2, w.dy, n2, c->stream));
+  return HBPDC_OK;
+}
+
 // the block of s powers is complete: orthogonalise it, extend H, apply Givens
 hbpdc_status g_block(hbpdc_ctx* c, GState& g) {
   SysWS& w = *g.w;
@@ -922,15 +955,24 @@ hbpdc_status g_block(hbpdc_ctx* c, GState& g) {
   bool ok = small_chol(T, sb, Rw);
   if (ok) {
     upper_inv(Rw, sb, Rwi);
-    CKS(block_update_dev(c, w, nq, W, sb, C2, &Rwi));
-    // CholQR2 of the block itself
-    std::vector<double> none;
-    CKS(block_dots_host(c, w, 0, W, sb, r3));
+    // CholQR2 of the block itself: its Gram from the update pass (s = 8) or a separate pass
+    const bool fused = sb == 8 && c->fuse_cgs;
+    if (fused) {
+      CKS(block_update_gram_host(c, w, nq, W, C2, Rwi, r3));
+    } else {
+      CKS(block_update_dev(c, w, nq, W, sb, C2, &Rwi));
+      CKS(block_dots_host(c, w, 0, W, sb, r3));
+    }
     T.assign(r3.begin(), r3.begin() + (size_t)sb * sb);
     ok = small_chol(T, sb, R3);
     if (ok) {
       upper_inv(R3, sb, R3i);
-      CKS(block_update_dev(c, w, 0, W, sb, none, &R3i));
+      if (fused) {
+        CKS(block_scale_dev(c, w, W, R3i));
+      } else {
+        std::vector<double> none;
+        CKS(block_update_dev(c, w, 0, W, sb, none, &R3i));
+      }
     }
   }
   if (!ok) {

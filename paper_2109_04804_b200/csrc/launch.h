@@ -143,8 +143,11 @@ int block_dot_blocks_tma();
 int block_dot_parts_tma();
 cudaError_t launch_block_dots_tma8(const double* Q, size_t ldq, int nq, const double* W, size_t ldw, size_t L,
                                    double* part, cudaStream_t st);
+// gram (optional, nq >= 1): Gram rows a*8 + b of the OUTPUT block, block_fused_parts_tma() partials per row
 cudaError_t launch_block_update_tma8(const double* Q, size_t ldq, int nq, double* W, size_t ldw, const double* C,
-                                     const double* Rinv, size_t L, cudaStream_t st);
+                                     const double* Rinv, size_t L, cudaStream_t st, double* gram = nullptr);
+// W_l <- sum_{m <= l} W_m Rinv[m][l] for the 8 vectors of a block (second CholQR pass)
+cudaError_t launch_block_scale_w8(double* W, size_t ldw, const double* Rinv, size_t L, cudaStream_t st);
 // fused W <- W - Q C (Rinv = I) and rows of [Q W]^T W of the updated W in one
 // pass over Q (1 <= nq <= block_fused_max_nq(); partials: block_fused_parts_tma() per row)
 int block_fused_parts_tma();

@@ -13,6 +13,7 @@
 //
 // Same row layout / semantics as launch_block_dots_mma / launch_block_update_mma;
 // deterministic (fixed chunk -> CTA map, fixed accumulation order).
+#include <algorithm>
 #include "launch.h"
 #include "tma.cuh"
 
@@ -166,7 +167,8 @@ __global__ void __launch_bounds__(32 * (TD_W + 1), 1) block_dots_tma8_kernel(con
 __global__ void __launch_bounds__(288, 1) block_update_tma8_kernel(const double* __restrict__ Q, size_t ldq, int nq,
                                                                    double* __restrict__ W, size_t ldw,
                                                                    const double* __restrict__ C,
-                                                                   const double* __restrict__ Rinv, size_t L) {
+                                                                   const double* __restrict__ Rinv, size_t L,
+                                                                   double* __restrict__ gram) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int nq8 = (nq + 7) / 8 * 8;
   double* ring = reinterpret_cast<double*>(smraw);                            // TU_R x 8 x TU_P
@@ -223,6 +225,7 @@ __global__ void __launch_bounds__(288, 1) block_update_tma8_kernel(const double*
       }
     }
   };
+  double gacc[2] = {0.0, 0.0};
   double wv[TU_NB][2], wn[TU_NB][2];
   if (nmy > 0) load_w(0, wn);
   size_t k = 0;
@@ -270,6 +273,45 @@ __global__ void __launch_bounds__(288, 1) block_update_tma8_kernel(const double*
       } else if (e < L) {
         wg[e] = o0;
       }
+      if (gram) {
+        // Gram of the output block (the next CholQR pass) from registers: B fragment
+        // (element 4 kk + t of the n-block, vector g) gathered by shuffles; beyond L: 0
+        const double u0 = e < L ? o0 : 0.0, u1 = e + 1 < L ? o1 : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int src = g * 4 + 2 * kk + (t >> 1);
+          const double v0 = __shfl_sync(0xffffffffu, u0, src);
+          const double v1 = __shfl_sync(0xffffffffu, u1, src);
+          const double bfv = (t & 1) ? v1 : v0;
+          dmma(gacc, bfv, bfv);
+        }
+      }
+    }
+  }
+  if (gram) {   // one partial per consumer warp: gram[(a * 8 + b)][8 * blockIdx + wid]
+    const size_t col = (size_t)blockIdx.x * 8 + wid, ncol = (size_t)gridDim.x * 8;
+    gram[((size_t)g * 8 + 2 * t) * ncol + col] = gacc[0];
+    gram[((size_t)g * 8 + 2 * t + 1) * ncol + col] = gacc[1];
+  }
+}
+
+// W_l <- sum_{m <= l} W_m Rinv[m][l] (Rinv upper triangular, 8 x 8): the second
+// CholQR pass of a block, one streaming read + write of the 8 vectors
+__global__ void __launch_bounds__(256) block_scale_w8_kernel(double* __restrict__ W, size_t ldw,
+                                                            const double* __restrict__ Rinv, size_t L) {
+  __shared__ double sR[64];
+  if (threadIdx.x < 64) sR[threadIdx.x] = Rinv[threadIdx.x];
+  __syncthreads();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += (size_t)gridDim.x * blockDim.x) {
+    double x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = __ldcs(W + (size_t)m * ldw + i);
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      double o = 0.0;
+#pragma unroll
+      for (int m = 0; m <= l; ++m) o = fma(x[m], sR[m * 8 + l], o);
+      __stcs(W + (size_t)l * ldw + i, o);
     }
   }
 }
@@ -289,9 +331,17 @@ cudaError_t launch_block_dots_tma8(const double* Q, size_t ldq, int nq, const do
   return cudaGetLastError();
 }
 
+cudaError_t launch_block_scale_w8(double* W, size_t ldw, const double* Rinv, size_t L, cudaStream_t st) {
+  const int grid = (int)std::min<size_t>((L + 255) / 256, (size_t)block_dot_blocks_tma() * 8);
+  block_scale_w8_kernel<<<grid, 256, 0, st>>>(W, ldw, Rinv, L);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_block_update_tma8(const double* Q, size_t ldq, int nq, double* W, size_t ldw, const double* C,
-                                     const double* Rinv, size_t L, cudaStream_t st) {
-  if (nq < 1) return launch_block_update_mma(Q, ldq, nq, W, ldw, 8, C, Rinv, L, st);
+                                     const double* Rinv, size_t L, cudaStream_t st, double* gram) {
+  if (nq < 1 && !gram) return launch_block_update_mma(Q, ldq, nq, W, ldw, 8, C, Rinv, L, st);
+  if (nq < 1) return cudaErrorInvalidValue;
   if ((ldq & 1) || (ldw & 1)) return cudaErrorInvalidValue;
   const int nq8 = (nq + 7) / 8 * 8;
   const size_t smem = ((size_t)TU_R * 8 * TU_P + (size_t)nq8 * 8 + 64) * sizeof(double) +
@@ -303,7 +353,7 @@ cudaError_t launch_block_update_tma8(const double* Q, size_t ldq, int nq, double
       return cudaErrorInvalidValue;
     attr = smem;
   }
-  block_update_tma8_kernel<<<block_dot_blocks_tma(), 288, smem, st>>>(Q, ldq, nq, W, ldw, C, Rinv, L);
+  block_update_tma8_kernel<<<block_dot_blocks_tma(), 288, smem, st>>>(Q, ldq, nq, W, ldw, C, Rinv, L, gram);
   hbpdc_count_launch();
   return cudaGetLastError();
 }

@@ -146,6 +146,43 @@ int main(int argc, char** argv) {
              L, nq, ts * 1e3, tf * 1e3, bq / (tf * 1e-3) / 1e9, rd, ru, tail);
     }
   }
+  // update with the Gram of its output, and the W-only scale, vs the separate kernels
+  for (size_t L : {LMAX, quick ? (size_t)100006 : (size_t)1000006}) {
+    for (int nq : {1, 17, 126}) {
+      cudaMemcpy(W2, W, 8 * LMAX * 8, cudaMemcpyDeviceToDevice);
+      cudaMemcpy(W3, W, 8 * LMAX * 8, cudaMemcpyDeviceToDevice);
+      launch_block_update_mma(Q, LMAX, nq, W2, LMAX, 8, C, Rinv, L, st);
+      launch_block_dots_mma(Q, LMAX, 0, W2, LMAX, 8, L, part, st);
+      launch_reduce_partials_n(part, 64, block_dot_blocks_mma(L), out1, st);
+      launch_block_update_tma8(Q, LMAX, nq, W3, LMAX, C, Rinv, L, st, part2);
+      launch_reduce_partials_n(part2, 64, block_fused_parts_tma(), out2, st);
+      std::vector<double> a(64), b(64);
+      cudaMemcpy(a.data(), out1, 64 * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(b.data(), out2, 64 * 8, cudaMemcpyDeviceToHost);
+      double md = 0, mx = 0;
+      for (int i = 0; i < 64; ++i) { md = std::max(md, std::abs(a[i] - b[i])); mx = std::max(mx, std::abs(a[i])); }
+      // scale: W2 <- W2 Rinv by both kernels
+      launch_block_update_mma(Q, LMAX, 0, W2, LMAX, 8, C, Rinv, L, st);
+      launch_block_scale_w8(W3, LMAX, Rinv, L, st);
+      std::vector<double> u(8 * LMAX), v(8 * LMAX);
+      cudaMemcpy(u.data(), W2, 8 * LMAX * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(v.data(), W3, 8 * LMAX * 8, cudaMemcpyDeviceToHost);
+      double num = 0, den = 0, tail = 0;
+      for (int k = 0; k < 8; ++k)
+        for (size_t i = 0; i < LMAX; ++i) {
+          const double x = u[k * LMAX + i], y = v[k * LMAX + i];
+          if (i < L) { num += (x - y) * (x - y); den += x * x; }
+          else tail = std::max(tail, std::abs(y - x));
+        }
+      float ts = timeit([&] { launch_block_update_mma(Q, LMAX, 0, W2, LMAX, 8, C, Rinv, L, st); }, st);
+      float tn = timeit([&] { launch_block_scale_w8(W3, LMAX, Rinv, L, st); }, st);
+      float tg = timeit([&] { launch_block_update_tma8(Q, LMAX, nq, W3, LMAX, C, Rinv, L, st, part2); }, st);
+      const double rd = md / mx, ru = std::sqrt(num / den);
+      ok = ok && rd < 1e-13 && ru < 1e-13 && tail == 0.0;
+      printf("L=%zu nq=%3d gram: update+gram %7.1f us, gram diff %.1e | scale: mma %6.1f us / new %6.1f us (%5.0f GB/s) diff %.1e tail %.1e\n",
+             L, nq, tg * 1e3, rd, ts * 1e3, tn * 1e3, 16.0 * L * 8 / (tn * 1e-3) / 1e9, ru, tail);
+    }
+  }
   printf("status: %s  check: %s\n", cudaGetErrorString(cudaGetLastError()), ok ? "OK" : "FAIL");
   return ok ? 0 : 1;
 }
