@@ -468,6 +468,8 @@ __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const 
   unsigned long long *fullS = bars, *emptyS = bars + GW_NST_MAX, *fullR = bars + 2 * GW_NST_MAX, *emptyR = fullR + 2;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int cpe = (m + GD_ROWS - 1) / GD_ROWS;
+  __shared__ double* sOut[NR];                                         // output pointers (indexed per thread)
+  if (threadIdx.x < NR) sOut[threadIdx.x] = io.out[threadIdx.x];
   const int nmy = blockIdx.x < nE ? (nE - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (threadIdx.x == 0) {
     for (int q = 0; q < GW_NST; ++q) { mbar_init(&fullS[q], 1); mbar_init(&emptyS[q], GD_CONS); }
@@ -542,11 +544,14 @@ __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const 
       if (threadIdx.x < GD_ROWS * NR) {
         const int r = threadIdx.x / NR, j = threadIdx.x % NR;
         const double* rr = red + (size_t)buf * GD_CONS * 64 + (r >> 3) * 64 + (r & 7) * 8 + j;
-        double sum = 0.0;
+        double s0 = 0.0, s1 = 0.0;                  // two chains, fixed order
 #pragma unroll
-        for (int q = 0; q < GD_CONS / 2; ++q) sum += rr[(size_t)2 * q * 64];
+        for (int q = 0; q < GD_CONS / 2; q += 2) {
+          s0 += rr[(size_t)2 * q * 64];
+          s1 += rr[(size_t)2 * (q + 1) * 64];
+        }
         const int row = ch * GD_ROWS + r;
-        if (row < m) io.out[j][(size_t)e * m + row] = sum;
+        if (row < m) sOut[j][(size_t)e * m + row] = s0 + s1;
       }
     }
   }
