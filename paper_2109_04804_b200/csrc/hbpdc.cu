@@ -75,6 +75,8 @@ struct SysWS {
   double *X = nullptr, *G = nullptr, *dX = nullptr, *rhs = nullptr, *r = nullptr, *zb = nullptr;
   double *b = nullptr;                      // Newton right-hand side b (n)
   double *U = nullptr, *V = nullptr;        // BJ_ext GEMV outputs (n each)
+  double* npart = nullptr;                  // K-apply per-CTA partials of ||out1||^2 ...
+  const double* npart_of = nullptr;         // ... valid for this vector (the next FD JVP's dW)
   double *Vk = nullptr;                     // Krylov basis: vk_cap x 2n, grown on demand up to restart+1
   size_t vk_cap = 0;
   double *partial = nullptr, *dh = nullptr, *dy = nullptr, *dnrm = nullptr;
@@ -327,6 +329,16 @@ int jvp_kind(hbpdc_ctx* c, int mode) {
   return mode;
 }
 
+// the K-apply norm partials recorded for vector z (GEMV slot that produced it), consumed once
+const double* take_npart(hbpdc_ctx* c, const double* z) {
+  for (auto& s : c->sys)
+    if (s.npart_of == z) {
+      s.npart_of = nullptr;
+      return s.npart;
+    }
+  return nullptr;
+}
+
 // J dX for the extended system, dX = [dW | ds] (2n), out = [top | bottom]
 // ws_ghosts: the halos of (W, sigma) are current (GMRES inside one Newton
 // iteration: the linearisation point is fixed), exchange only (dW, dsigma)
@@ -334,7 +346,7 @@ int jvp_kind(hbpdc_ctx* c, int mode) {
 hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const double* W, const double* sg,
                       const double* dW, const double* ds, double* o1, double* o2, int mode,
                       const double* eps_override, bool ws_ghosts = false, const double* shift_src = nullptr,
-                      double shift = 0.0) {
+                      double shift = 0.0, const double* dw_part = nullptr) {
   const size_t n = c->n;
   mode = jvp_kind(c, mode);
   OpArgs A = base_args(c);
@@ -353,13 +365,19 @@ hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const doubl
     if (eps_override) {
       A.epsw = eps_override[0];
     } else {
-      CK(launch_sumsq(dW, n, c->partial, c->stream));
+      // ||dW||^2 partials: from the K-apply that produced dW (dw_part), else one sumsq pass
+      const double* part = dw_part;
+      int np = dw_part ? op_grid(c->cfg, c->geo) : RED_BLOCKS;
+      if (!part) {
+        CK(launch_sumsq(dW, n, c->partial, c->stream));
+        part = c->partial;
+      }
       if (c->comm) {   // global ||dW|| (reading R7)
-        CK(launch_reduce_partials_n(c->partial, 1, RED_BLOCKS, c->deps + 1, c->stream));
+        CK(launch_reduce_partials_n(part, 1, np, c->deps + 1, c->stream));
         CKS(allreduce(c, c->deps + 1, 1));
         CK(launch_fd_eps_from_sum(c->deps + 1, std::sqrt(EPS_MACH) / c->pb.mach_eps, c->deps, c->stream));
       } else {
-        CK(launch_finish_fd_eps(c->partial, std::sqrt(EPS_MACH) / c->pb.mach_eps, c->deps, c->stream));
+        CK(launch_finish_fd_eps(part, std::sqrt(EPS_MACH) / c->pb.mach_eps, c->deps, c->stream, np));
       }
       A.d_epsw = c->deps;
     }
@@ -381,6 +399,7 @@ hbpdc_status ensure_precond_mem(hbpdc_ctx* c) {
   for (auto& w : c->sys) {
     CKS(dalloc(c, &w.U, c->n));
     CKS(dalloc(c, &w.V, c->n));
+    CKS(dalloc(c, &w.npart, (size_t)op_grid(c->cfg, c->geo) + 1));
   }
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {   // explicit K_i (two-hop BR1 path) + colouring scratch
     CKS(dalloc(c, &c->Kst, nblk * mm));
@@ -518,8 +537,10 @@ hbpdc_status precond_apply_multi(hbpdc_ctx* c, int B, const double* const* iw, c
       A.a1dt = a1dt;
       A.c2 = c2;
       A.gW = c->halo() ? c->gWb : c->Wb;
+      A.nrm_part = c->sys[i].npart;             // ||out1||^2 partials for the next FD JVP
       ProfScope ps(c, 5, 5.0 * c->n * 8.0);
       CK(launch_op(OP_KAPPLY, c->cfg, c->geo, A));
+      c->sys[i].npart_of = ow[i];
       CKS(dbg_sync(c, "BJ_ext K apply"));
     }
     if (c->st) c->st->precond_applies++;
@@ -683,7 +704,8 @@ hbpdc_status g_iter(hbpdc_ctx* c, GState& g, const double* z) {
   double* wv = w.Vk + (size_t)j * n2;
   if (!flush) {
     use_ghosts(c, w);
-    CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, wv, wv + n, c->op.jvp_mode, nullptr, true));
+    CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, wv, wv + n, c->op.jvp_mode, nullptr, true,
+                 nullptr, 0.0, take_npart(c, z)));
     ++g.total;
   }
   const int nk = j - 1;
@@ -1049,7 +1071,7 @@ hbpdc_status g_power(hbpdc_ctx* c, GState& g, const double* z) {
   double* out = w.Vk + (size_t)g.j * n2;
   use_ghosts(c, w);
   CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr, true,
-               prev, g.theta));
+               prev, g.theta, take_npart(c, z)));
   ++g.total;
   ++g.pi;
   ++g.j;

@@ -19,6 +19,8 @@ struct OpCfg {
 
 // fused element operator (modes.cuh); NS modes need lift buffers in A.G0/G1
 cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
+// CTAs of an operator launch (per-CTA partials, e.g. the K-apply norm epilogue)
+int op_grid(const OpCfg& c, const Geo& g);
 // BR1 lifting of jet state `state` of operator `kind` into Gout
 cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout);
 // number of jet components of the lifted gradients of (kind, state)
@@ -96,7 +98,8 @@ cudaError_t launch_sumsq(const double* x, size_t L, double* partial, cudaStream_
 // out = sqrt(sum partial)
 cudaError_t launch_finish_norm(const double* partial, double* out, cudaStream_t st);
 // out = c / sqrt(sum partial), or 0 if the sum is 0   (FD step)
-cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st);
+// eps_FD from np partial sums of ||dW||^2 (np <= 0: RED_BLOCKS)
+cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st, int np = 0);
 // HBPC quadrature: y = base + sum_j a[j] X_j + sum_j b[j] Y_j  (host coefficient arrays, <= 8 terms)
 cudaError_t launch_stage_combo(const double* base, int nx, const double* const* X, const double* a,
                                int ny, const double* const* Y, const double* b, double* y, size_t L,

@@ -1173,16 +1173,16 @@ cudaError_t launch_finish_norm(const double* partial, double* out, cudaStream_t 
 }
 
 // eps_FD = c / ||x||_2 with c = sqrt(eps_machine)/eps; 0 if ||x|| = 0
-__global__ void finish_fd_eps_kernel(const double* __restrict__ partial, double c, double* out) {
+__global__ void finish_fd_eps_kernel(const double* __restrict__ partial, int np, double c, double* out) {
   __shared__ double sh[RED_THREADS / 32];
   double v = 0.0;
-  for (int b = threadIdx.x; b < RED_BLOCKS; b += RED_THREADS) v += partial[b];
+  for (int b = threadIdx.x; b < np; b += RED_THREADS) v += partial[b];
   const double s = block_sum(v, sh);
   if (threadIdx.x == 0) *out = s > 0.0 ? c / sqrt(s) : 0.0;
 }
 
-cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st) {
-  finish_fd_eps_kernel<<<1, RED_THREADS, 0, st>>>(partial, c, out);
+cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st, int np) {
+  finish_fd_eps_kernel<<<1, RED_THREADS, 0, st>>>(partial, np > 0 ? np : RED_BLOCKS, c, out);
   hbpdc_count_launch();
   return cudaGetLastError();
 }

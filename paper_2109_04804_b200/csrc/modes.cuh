@@ -22,6 +22,7 @@ struct OpArgs {
   const double* G1;     // NS lifted gradients of jet state 1
   const double *gG0, *gG1;   // their ghost copies (halo of the lifted gradients)
   const double *shw, *shs;   // JVP epilogue shift: out -= shift * (shw | shs)  (s-step Newton basis)
+  double* nrm_part;     // K-apply: per-CTA partial sums of out1^2 (the next FD JVP's ||dW||), or NULL
   double shift;
   double a1dt, c2;
   double epsw;          // FD step for the W direction (<= 0: quotient is 0)
@@ -455,11 +456,20 @@ template <int EQ, int NODES> struct ModeKApply : OneJetMode<EQ, NODES, ModeKAppl
     for (int v = 0; v < NV; ++v) { c[0][v] = F[v].a; c[1][v] = F[v].b; }
   }
   __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
+    (void)epilogue_ss(A, e, node, o);
+  }
+  // epilogue that also returns this node's sum of out1^2 (op_kernel reduces it per CTA)
+  static constexpr bool NORM_EPILOGUE = true;
+  __device__ static double epilogue_ss(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
+    double ss = 0.0;
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      A.out1[k] = fma(-A.c2, o[0][v], A.U[k]);
+      const double t1 = fma(-A.c2, o[0][v], A.U[k]);
+      A.out1[k] = t1;
       A.out2[k] = A.V[k] + o[1][v];
+      ss = fma(t1, t1, ss);
     }
+    return ss;
   }
 };
 

@@ -220,6 +220,10 @@ __device__ __forceinline__ void face_from_halves(const PhysParams& pp, const dou
   }
 }
 
+// modes whose epilogue also returns the node's sum of out1^2 (epilogue_ss)
+template <class M, class = void> struct NormEpilogue : std::false_type {};
+template <class M> struct NormEpilogue<M, std::void_t<decltype(M::NORM_EPILOGUE)>> : std::true_type {};
+
 // argument packs carrying a device-resident FD step (OpArgs::d_epsw)
 template <class A, class = void> struct HasDevEps : std::false_type {};
 template <class A> struct HasDevEps<A, std::void_t<decltype(A::d_epsw)>> : std::true_type {};
@@ -387,7 +391,25 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g) {
     Al.iepsw = Al.epsw > 0.0 ? 1.0 / Al.epsw : 0.0;    // once per thread (was: per face and pass)
   }
   eval_slot<EQ, DIM, P, Mode>(Al, pp, g, e, slot, node, active, sF + slot * SLOT, out);
-  if (active) Mode::epilogue(Al, e, node, out);
+  if constexpr (NormEpilogue<Mode>::value) {
+    // per-CTA partial of sum(out1^2), fixed reduction order (warp tree, then warps in order)
+    double ss = 0.0;
+    if (active) ss = Mode::epilogue_ss(Al, e, node, out);
+    if (Al.nrm_part) {
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o2);
+      __syncthreads();                              // sF is reused as the warp-sum scratch
+      if ((threadIdx.x & 31) == 0) sF[threadIdx.x >> 5] = ss;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sF[w];
+        Al.nrm_part[blockIdx.x] = t;
+      }
+    }
+  } else {
+    if (active) Mode::epilogue(Al, e, node, out);
+  }
 }
 
 // ---- BR1 lifting (eq:Lifting P:855, central value P:861; reading R19) -----------

@@ -199,6 +199,12 @@ static cudaError_t dispatch(const OpCfg& c, F&& f) {
   return cudaErrorInvalidValue;
 }
 
+int op_grid(const OpCfg& c, const Geo& g) {
+  const int nodes = ipow(c.P, c.dim);
+  const int epb = epb_for(nodes);
+  return (g.nE + epb - 1) / epb;
+}
+
 cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
   return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
 }
