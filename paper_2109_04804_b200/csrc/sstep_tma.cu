@@ -373,7 +373,10 @@ cudaError_t launch_block_update_tma8(const double* Q, size_t ldq, int nq, double
 // chunks (one partial per consumer warp, as block_dots_tma8).
 // ============================================================================
 namespace {
-constexpr int TF_MAXT = 20;        // Q tiles (nq <= 160) kept in accumulators
+#ifndef TF_MAXT_
+#define TF_MAXT_ 20
+#endif
+constexpr int TF_MAXT = TF_MAXT_;  // Q tiles (nq <= 8 TF_MAXT) kept in accumulators
 #ifndef TF_E_
 #define TF_E_ 512
 #endif
@@ -386,12 +389,19 @@ constexpr int TF_P = TF_E + 4;     // padded row: conflict-free fragments
 #define TF_R_ ((200 * 1024) / (8 * TF_P * 8))
 #endif
 constexpr int TF_R = TF_R_;        // ring stages
-constexpr int TF_NB = TF_E / 64;   // n-blocks per consumer warp
+#ifndef TF_W_
+#define TF_W_ 8
+#endif
+constexpr int TF_W = TF_W_;        // consumer warps
+constexpr int TF_NB = TF_E / (8 * TF_W);   // n-blocks per consumer warp
 }
-int block_fused_parts_tma() { return 8 * block_dot_blocks_tma(); }
+int block_fused_parts_tma() {
+  static_assert(TF_W == 8, "block_update_tma8's Gram partials share this column count");
+  return TF_W * block_dot_blocks_tma();
+}
 int block_fused_max_nq() { return 8 * TF_MAXT; }
 
-__global__ void __launch_bounds__(288, 1) block_update_dots_tma8_kernel(const double* __restrict__ Q, size_t ldq,
+__global__ void __launch_bounds__(32 * (TF_W + 1), 1) block_update_dots_tma8_kernel(const double* __restrict__ Q, size_t ldq,
                                                                         int nq, double* __restrict__ W, size_t ldw,
                                                                         const double* __restrict__ C, size_t L,
                                                                         double* __restrict__ part) {
@@ -405,7 +415,7 @@ __global__ void __launch_bounds__(288, 1) block_update_dots_tma8_kernel(const do
   for (int k = threadIdx.x; k < TF_R * 8 * TF_P; k += blockDim.x) ring[k] = 0.0;
   for (int k = threadIdx.x; k < nq8 * 8; k += blockDim.x) sC[k] = k < nq * 8 ? C[k] : 0.0;
   if (threadIdx.x == 0) {
-    for (int r = 0; r < TF_R; ++r) { mbar_init(&full[r], 1); mbar_init(&empty[r], 8); }
+    for (int r = 0; r < TF_R; ++r) { mbar_init(&full[r], 1); mbar_init(&empty[r], TF_W); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_proxy_async_smem();
@@ -413,7 +423,7 @@ __global__ void __launch_bounds__(288, 1) block_update_dots_tma8_kernel(const do
   const int T = nq8 / 8;
   const size_t nch = (L + TF_E - 1) / TF_E;
   const size_t nmy = blockIdx.x < nch ? (nch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  if (wid == 8) {                                                             // ---- producer
+  if (wid == TF_W) {                                                          // ---- producer
     // lane 0 waits / arms the stage, lanes 0..7 issue one row copy each
     size_t k = 0;
     for (size_t ci = 0; ci < nmy; ++ci) {
@@ -533,8 +543,8 @@ __global__ void __launch_bounds__(288, 1) block_update_dots_tma8_kernel(const do
       }
     }
   }
-  // one partial per consumer warp: part[row][8 * blockIdx + wid]
-  const size_t col = (size_t)blockIdx.x * 8 + wid, ncol = (size_t)gridDim.x * 8;
+  // one partial per consumer warp: part[row][TF_W * blockIdx + wid]
+  const size_t col = (size_t)blockIdx.x * TF_W + wid, ncol = (size_t)gridDim.x * TF_W;
 #pragma unroll
   for (int tile = 0; tile < TF_MAXT; ++tile) {
     const int j = 8 * tile + g;
@@ -560,7 +570,7 @@ cudaError_t launch_block_update_dots_tma8(const double* Q, size_t ldq, int nq, d
       return cudaErrorInvalidValue;
     attr = smem;
   }
-  block_update_dots_tma8_kernel<<<block_dot_blocks_tma(), 288, smem, st>>>(Q, ldq, nq, W, ldw, C, L, part);
+  block_update_dots_tma8_kernel<<<block_dot_blocks_tma(), 32 * (TF_W + 1), smem, st>>>(Q, ldq, nq, W, ldw, C, L, part);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
