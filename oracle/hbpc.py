@@ -42,13 +42,13 @@ class HBPC:
         pcs = {}
 
         def precond(a1, a2):
-            if opts.precond != "bjext" or opts.precond_policy != "per_step_per_alpha":
+            if opts.precond not in ("bjext", "bjext_h") or opts.precond_policy != "per_step_per_alpha":
                 return None
             # pairs equal up to rounding share a build: dc is constant across
             # stages in exact arithmetic for q = 4, 6, 8 (App. A; reading R12)
             key = (float(f"{a1:.12e}"), float(f"{a2:.12e}"))
             if key not in pcs:
-                pcs[key] = implicit.BJExt(disc, Wn, a1, a2, dt)
+                pcs[key] = implicit.make_precond(opts.precond, disc, Wn, a1, a2, dt)
                 stats["precond_builds"] += 1
             return pcs[key]
 

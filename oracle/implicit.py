@@ -189,6 +189,90 @@ class BJExt:
         return top.reshape(-1), bot.reshape(-1)
 
 
+def element_hessian_blocks(disc: Disc, W, sig):
+    """H_i = element-diagonal block dR2_i/dW_i at fixed sigma (the Hessian
+    contribution of BJ^H_ext), (nE, m, m).
+
+    R2(W, sigma) is the e1 part of R1(W + e1 sigma); column c of H_i is the
+    e1e2 part of R1(W + e1 sigma + e2 seed) restricted to element i, with the
+    seed e_c in element i only (sigma everywhere, "element-internal influence
+    only") -- the hyper-dual product used by jvp_exact.  Same colouring
+    as element_jacobians (R2 has the stencil of R1)."""
+    me = disc.mesh
+    nE, m = me.n_elem, disc.m
+    radius = 2 if disc.eq.viscous else 1
+    Px = _period(me.nx, radius)
+    Py = _period(me.ny, radius) if me.dim == 2 else 1
+    ex = np.arange(nE) % me.nx
+    ey = np.arange(nE) // me.nx
+    H = np.zeros((nE, m, m))
+    W = np.asarray(W, float)
+    sig = np.asarray(sig, float)
+    for cy in range(Py):
+        for cx in range(Px):
+            sel = (ex % Px == cx) & (ey % Py == cy)
+            for c in range(m):
+                seed = np.zeros((nE, m))
+                seed[sel, c] = 1.0
+                J = rhs1(disc, ad.Jet(W, sig, seed.reshape(-1), 0.0))
+                R = np.broadcast_to(J.d12, W.shape).reshape(nE, m)
+                H[sel, :, c] = R[sel, :]
+    return H
+
+
+class BJExtH:
+    """BJ^H_ext: the extended block-Jacobi preconditioner WITH the
+    Hessian contribution,
+        A^H_i = I - a1 dt K_i + c2 H_i,   B_i = c2 K_i,   C_i = -K_i,
+        D^H = (A^H - B C)^-1,  E^H = -(A^H - B C)^-1 B,
+        F^H = -C (A^H - B C)^-1,  G^H = I + C (A^H - B C)^-1 B,
+    one inverse per element by LU.  sigma is the build point's
+    sigma (the library builds at X = (W, R1(W)), reading R31)."""
+
+    def __init__(self, disc, W, sig, a1, a2, dt, K=None, H=None):
+        self.disc, self.a1, self.a2, self.dt = disc, a1, a2, dt
+        self.c2 = a2 * dt * dt / 2.0
+        self.K = element_jacobians(disc, W) if K is None else K
+        self.H = element_hessian_blocks(disc, W, sig) if H is None else H
+        m = disc.m
+        I = np.eye(m)
+        A = I[None] - a1 * dt * self.K + self.c2 * self.H     # A^H_i (P:277)
+        B = self.c2 * self.K                                  # B_i (P:278)
+        C = -self.K                                           # C_i (P:279)
+        self.A, self.B, self.C = A, B, C
+        self.M = A - B @ C                                    # I - a1 dt K + c2 (H + K^2)
+        self.S = np.linalg.inv(self.M)                        # LAPACK getrf/getri (P:296)
+        self.D = self.S                                       # P:284
+        self.E = -self.S @ B                                  # P:285
+        self.F = -C @ self.S                                  # P:286
+        self.G = I[None] + C @ self.S @ B                     # P:287
+
+    def apply(self, XW, Xs):
+        """P^-1 X per element: (D x + E y ; F x + G y)."""
+        nE, m = self.disc.mesh.n_elem, self.disc.m
+        w, s = XW.reshape(nE, m, 1), Xs.reshape(nE, m, 1)
+        top = (self.D @ w + self.E @ s).reshape(-1)
+        bot = (self.F @ w + self.G @ s).reshape(-1)
+        return top, bot
+
+    def apply_sk(self, XW, Xs):
+        """Equivalent S+K form: u = S (x - c2 K y);  top = u;  bot = y + K u."""
+        nE, m = self.disc.mesh.n_elem, self.disc.m
+        w, s = XW.reshape(nE, m, 1), Xs.reshape(nE, m, 1)
+        u = self.S @ (w - self.c2 * (self.K @ s))
+        bot = s + self.K @ u
+        return u.reshape(-1), bot.reshape(-1)
+
+
+def make_precond(kind, disc, W, a1, a2, dt):
+    """'bjext' (P:298-316) or 'bjext_h' (P:269-296, sigma = R1(W))."""
+    if kind == "bjext":
+        return BJExt(disc, W, a1, a2, dt)
+    if kind == "bjext_h":
+        return BJExtH(disc, W, rhs1(disc, W), a1, a2, dt)
+    raise ValueError(kind)
+
+
 # ---------------------------------------------------------------------------
 # GMRES (right preconditioned, modified Gram-Schmidt, restarted)
 
@@ -290,8 +374,8 @@ def newton_solve(disc, a1, a2, dt, b, W_guess, opts: NewtonOpts, pc=None, stats=
             break
         if r == opts.max_newton:
             raise NewtonFailure(f"Newton did not converge: ||G||={gn:.3e}, ||G0||={g0:.3e}")
-        if opts.precond == "bjext" and opts.precond_policy == "per_newton":
-            pc = BJExt(disc, W, a1, a2, dt)
+        if opts.precond in ("bjext", "bjext_h") and opts.precond_policy == "per_newton":
+            pc = make_precond(opts.precond, disc, W, a1, a2, dt)
             if stats is not None:
                 stats["precond_builds"] += 1
         Wc, sc = W.copy(), sig.copy()

@@ -186,6 +186,81 @@ def test_bjext_dt_zero():
     np.testing.assert_allclose(b, Kx + y, atol=1e-12)
 
 
+def test_element_hessian_brute_force():
+    """H_i (hyper-dual seeds) equals central differences of R2(., sigma)
+    restricted to element i with the W perturbation confined to element i."""
+    d = make("euler", 2, 3, 3)
+    W = euler_state(d, 20)
+    sig = dgsem.rhs1(d, W) * (1 + 0.1 * np.random.default_rng(21).standard_normal(d.n))
+    H = implicit.element_hessian_blocks(d, W, sig)
+    m, h = d.m, 1e-6
+    for e in (0, 4):
+        for c in (0, 7, m - 1):
+            x = np.zeros(d.n); x[e * m + c] = h
+            col = (dgsem.rhs2(d, W + x, sig) - dgsem.rhs2(d, W - x, sig))[e * m:(e + 1) * m] / (2 * h)
+            np.testing.assert_allclose(H[e][:, c], col, rtol=1e-6, atol=1e-5 * np.abs(col).max())
+
+
+def test_bjext_h_identities():
+    """BJ^H_ext (P:284-287): P P^-1 = I per element with A^H = I - a1 dt K + c2 H;
+    the literal D,E,F,G apply equals the S+K form u = S(x - c2 K y), (u, y + K u)."""
+    d = make("euler", 2, 3, 3)
+    W = euler_state(d, 22)
+    pc = implicit.BJExtH(d, W, dgsem.rhs1(d, W), 0.5, 1 / 6, 0.3)
+    assert np.abs(pc.H).max() > 0.0                      # the Hessian term is present for Euler
+    m = d.m
+    I = np.eye(m)
+    for e in range(d.mesh.n_elem):
+        P = np.block([[pc.A[e], pc.B[e]], [pc.C[e], I]])
+        Pi = np.block([[pc.D[e], pc.E[e]], [pc.F[e], pc.G[e]]])
+        assert np.abs(P @ Pi - np.eye(2 * m)).max() < 1e-10
+    rng = np.random.default_rng(23)
+    x, y = rng.standard_normal(d.n), rng.standard_normal(d.n)
+    t1, b1 = pc.apply(x, y)
+    t2, b2 = pc.apply_sk(x, y)
+    assert np.abs(t1 - t2).max() < 1e-11 * np.abs(t1).max()
+    assert np.abs(b1 - b2).max() < 1e-11 * np.abs(b1).max()
+
+
+def test_bjext_h_reduces_to_bjext():
+    """Linear flux: R2(W, sigma) = R1(sigma) does not depend on W, so H = 0 and
+    BJ^H_ext == BJ_ext; dt = 0 gives [[I, 0], [K, I]] for both."""
+    d = make("advection", 2, 3, 3, a=(1.0, 0.5))
+    W = np.random.default_rng(24).standard_normal(d.n)
+    ph = implicit.BJExtH(d, W, dgsem.rhs1(d, W), 0.5, 1 / 6, 0.3)
+    pb = implicit.BJExt(d, W, 0.5, 1 / 6, 0.3)
+    assert np.abs(ph.H).max() == 0.0
+    rng = np.random.default_rng(25)
+    x, y = rng.standard_normal(d.n), rng.standard_normal(d.n)
+    for u, v in zip(ph.apply(x, y), pb.apply(x, y)):
+        assert np.abs(u - v).max() < 1e-12 * np.abs(v).max()
+    de = make("euler", 2, 2, 2)
+    We = euler_state(de, 26)
+    p0 = implicit.BJExtH(de, We, dgsem.rhs1(de, We), 1.0, 1.0, 0.0)
+    xe, ye = rng.standard_normal(de.n), rng.standard_normal(de.n)
+    t, b = p0.apply(xe, ye)
+    np.testing.assert_allclose(t, xe, atol=1e-14)
+    np.testing.assert_allclose(b, (p0.K @ xe.reshape(-1, de.m, 1)).reshape(-1) + ye, atol=1e-12)
+
+
+def test_newton_bjext_h():
+    """A stage solve preconditioned with BJ^H_ext converges to the BJ_ext
+    solution (same tolerances); the Hessian-including block is at least as good
+    an approximation of J ('only a small influence on the iterations')."""
+    d = make("euler", 2, 3, 3)
+    W0 = euler_state(d, 27)
+    dt = 0.02
+    b = W0 + 0.5 * dt * dgsem.rhs1(d, W0)
+    res = {}
+    for kind in ("bjext", "bjext_h"):
+        opts = implicit.NewtonOpts(rtol=1e-10, gmres_rtol=1e-10, precond=kind, precond_policy="per_newton")
+        st = dict(stage_solves=0, newton_its=0, gmres_its=0, precond_builds=0)
+        Wk, _ = implicit.newton_solve(d, 0.5, 1 / 6, dt, b, W0, opts, None, st)
+        res[kind] = (Wk, st["gmres_its"])
+    assert np.abs(res["bjext"][0] - res["bjext_h"][0]).max() < 1e-9
+    assert res["bjext_h"][1] <= res["bjext"][1] + 2
+
+
 def test_advection_blocks_identical():
     d = make("advection", 3, 4, 4, a=(1.0, 1.0))
     K = implicit.element_jacobians(d, np.zeros(d.n))
