@@ -190,6 +190,8 @@ def run_ours(args):
                           cfg.bounds[2], cfg.bounds[2] + py * (cfg.bounds[3] - cfg.bounds[2])),
                   rank=rank, nranks=world, px=px, py=py, comm="nccl", nccl_id=nid[0],
                   force_halo=bool(args.self_halo))
+    if args.precond:
+        kw["precond"] = args.precond
     ctx = hbpdc.context_for(cfg, device=local, gmres_sstep=args.gmres_sstep, **kw)
     coords = inputs.tile_coords(ctx.node_coords(), cfg.bounds)
     W0 = inputs.initial_state(CONFIG, coords, noise=cfg.noise, stream=rank)
@@ -297,6 +299,7 @@ def run_ours(args):
                                    "noise, [-5,5]^2 periodic, 128x128 elements, N=7 GLL, LLF, HBPC(8,4), "
                                    "BJ_ext, FD JVP, Newton/GMRES rtol 1e-10, restart 700",
                        "arnoldi": ("DCGS2" if args.gmres_sstep <= 1 else f"s-step s={args.gmres_sstep} (block CGS2)"),
+                       "precond": args.precond or cfg.precond,
                        "dt": dt, "n_dof_per_gpu": n, "n_dof": n * world,
                        "parallelism": (f"element partition {px}x{py} of a {cfg.nx * px}x{cfg.ny * py} mesh "
                                        "(C3 tile per GPU), NCCL halos + all-reduces") if world > 1 else
@@ -329,6 +332,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precond", default=None, choices=["bjext", "bjext_h", "none"],
+                    help="override the config's preconditioner (default: C3's BJ_ext)")
     ap.add_argument("--gmres-sstep", type=int, default=8,
                     help="Arnoldi schedule: 1 = DCGS2, 2/4/8 = s-step blocks")
     ap.add_argument("--self-halo", action="store_true",

@@ -57,7 +57,7 @@ enum { HBPDC_ADVECTION = 0, HBPDC_EULER = 1, HBPDC_NAVIER_STOKES = 2 };
 enum { HBPDC_GLL = 0, HBPDC_GL = 1 };
 enum { HBPDC_LLF = 0 };
 enum { HBPDC_BR1 = 0 };
-enum { HBPDC_PC_NONE = 0, HBPDC_PC_BJEXT = 1 };
+enum { HBPDC_PC_NONE = 0, HBPDC_PC_BJEXT = 1, HBPDC_PC_BJEXT_H = 2 };
 enum { HBPDC_PC_PER_STEP_PER_ALPHA = 0, HBPDC_PC_PER_NEWTON = 1 };
 enum { HBPDC_JVP_AUTO = 0, HBPDC_JVP_FD = 1, HBPDC_JVP_EXACT = 2, HBPDC_JVP_LINEAR = 3 };
 
@@ -87,7 +87,9 @@ typedef struct {
   double gmres_rtol;           /* relative GMRES tolerance             */
   int gmres_restart;           /* Krylov dimension before restart            */
   int krylov_max_per_newton;   /* total GMRES iterations per Newton step     */
-  int precond;                 /* HBPDC_PC_NONE | HBPDC_PC_BJEXT          */
+  int precond;                 /* HBPDC_PC_NONE | HBPDC_PC_BJEXT |
+                                  HBPDC_PC_BJEXT_H (with the Hessian block, P:269-296;
+                                  advection / Euler; built at (W, R1(W)))              */
   int precond_policy;          /* HBPDC_PC_PER_STEP_PER_ALPHA (default) | PER_NEWTON */
   int jvp_mode;                /* HBPDC_JVP_AUTO: linear (advection) / FD otherwise  */
   int batch_stages;            /* 1: solve the s-1 corrector stages of a sweep in lock

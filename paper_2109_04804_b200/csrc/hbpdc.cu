@@ -106,6 +106,7 @@ struct hbpdc_ctx {
   std::vector<SysWS> sys;      // Newton/GMRES workspaces: [0] always, s-1 of them for batched correctors
   double *partial = nullptr;   // RED_BLOCKS partial sums (norms)
   double *dnrm = nullptr, *deps = nullptr;
+  double *Sb = nullptr, *gSb = nullptr;   // BJ^H_ext: sigma at the build point, R1(Wb), and its ghosts
   double *lift0 = nullptr, *lift1 = nullptr;
   // precond
   double *S = nullptr, *Wb = nullptr, *Z = nullptr;
@@ -436,6 +437,22 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
   ProfScope ps(c, 6, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 * (ns ? 2.0 : 1.0) + c->n * 8.0);
   CK(cudaMemcpyAsync(c->Wb, W, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   CKS(wb_halo(c));
+  const bool hess = c->op.precond == HBPDC_PC_BJEXT_H;
+  if (hess) {
+    // BJ^H_ext: the Hessian block dR2/dW at (Wb, sigma_b = R1(Wb)) (reading R31)
+    if (!c->Sb) {
+      CKS(dalloc(c, &c->Sb, c->n));
+      if (c->halo()) CKS(dalloc(c, &c->gSb, (size_t)(c->pb.dim == 2 ? 2 * (c->nxl + c->nyl) : 2) * c->m));
+    }
+    OpArgs A = base_args(c);
+    A.W = c->Wb; A.out1 = c->Sb;
+    CKS(run_op(c, OP_R1, A));
+    if (c->halo()) {
+      const double* src[1] = {c->Sb};
+      double* dst[1] = {c->gSb};
+      CKS(halo_exchange(c, 1, src, dst));
+    }
+  }
   const size_t mm = (size_t)c->m * c->m;
   const int nblk = c->s_shared ? 1 : c->nE;
   const double a1dt = a1 * dt, c2 = a2 * dt * dt / 2.0;
@@ -468,7 +485,8 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
       CK(cudaMemcpyAsync(c->Z, c->S + (size_t)e0 * mm, ne * mm * sizeof(double), cudaMemcpyDeviceToDevice,
                          c->stream));
     else
-      CK(launch_kbuild(c->cfg, c->geo, c->Wb, c->halo() ? c->gWb : c->Wb, a1dt, c2, c->Z, e0, ne));
+      CK(launch_kbuild(c->cfg, c->geo, c->Wb, c->halo() ? c->gWb : c->Wb, a1dt, c2, c->Z, e0, ne,
+                       hess ? c->Sb : nullptr, hess ? (c->halo() ? c->gSb : c->Sb) : nullptr));
     CKS(dbg_sync(c, "BJ_ext K/M build"));
     CK(launch_gj_invert(c->Z, c->S + (size_t)e0 * mm, c->m, ne, c->info, c->stream));
     CKS(dbg_sync(c, "Gauss-Jordan"));
@@ -505,7 +523,7 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
 hbpdc_status precond_apply_multi(hbpdc_ctx* c, int B, const double* const* iw, const double* const* is,
                                  double* const* ow, double* const* os) {
   if (!c->pc_valid) return fail(c, HBPDC_E_ARG, "precond_apply before precond_build");
-  {
+  if (c->op.precond != HBPDC_PC_BJEXT_H) {
     ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 4.0 * B * c->n * 8.0);
     if (B == 1 || c->s_shared) {
       for (int i = 0; i < B; ++i)
@@ -522,6 +540,37 @@ hbpdc_status precond_apply_multi(hbpdc_ctx* c, int B, const double* const* iw, c
     CKS(dbg_sync(c, "BJ_ext GEMV"));
   }
   const double a1dt = c->pc_a1 * c->pc_dt, c2 = c->pc_a2 * c->pc_dt * c->pc_dt / 2.0;
+  if (c->op.precond == HBPDC_PC_BJEXT_H) {
+    // P^-1 (x, y) with the Hessian block: u = S^H (x - c2 K y); top = u; bottom = y + K u
+    for (int i = 0; i < B; ++i) {
+      OpArgs A = base_args(c);
+      A.W = c->Wb; A.gW = c->halo() ? c->gWb : c->Wb;
+      A.dW = is[i]; A.b = iw[i]; A.a1dt = -c2; A.out1 = c->sys[i].U;
+      ProfScope ps(c, 5, 3.0 * c->n * 8.0);
+      CK(launch_op(OP_KLIN, c->cfg, c->geo, A));
+    }
+    {
+      ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 2.0 * B * c->n * 8.0);
+      if (c->s_shared) {
+        for (int i = 0; i < B; ++i)   // shared block: the 2-RHS kernel with a dummy second vector
+          CK(launch_block_gemv2(c->S, 1, c->sys[i].U, c->sys[i].U, ow[i], c->sys[i].V, c->m, c->nE, c->stream));
+      } else {
+        const double* in[GEMV_MAX_RHS];
+        double* out[GEMV_MAX_RHS];
+        for (int i = 0; i < B; ++i) { in[i] = c->sys[i].U; out[i] = ow[i]; }
+        CK(launch_block_gemv_multi(c->S, B, in, out, c->m, c->nE, c->stream));
+      }
+    }
+    for (int i = 0; i < B; ++i) {
+      OpArgs A = base_args(c);
+      A.W = c->Wb; A.gW = c->halo() ? c->gWb : c->Wb;
+      A.dW = ow[i]; A.b = is[i]; A.a1dt = 1.0; A.out1 = os[i];
+      ProfScope ps(c, 5, 3.0 * c->n * 8.0);
+      CK(launch_op(OP_KLIN, c->cfg, c->geo, A));
+      if (c->st) c->st->precond_applies++;
+    }
+    return HBPDC_OK;
+  }
   for (int i = 0; i < B; ++i) {
     const double *U = c->sys[i].U, *V = c->sys[i].V;
     if (c->pb.equation == HBPDC_NAVIER_STOKES) {
@@ -1158,7 +1207,7 @@ hbpdc_status newton_batch(hbpdc_ctx* c, int B, double a1, double a2, double dt, 
     g0[i] = -1.0;
     active[i] = true;
   }
-  const bool pc = c->op.precond == HBPDC_PC_BJEXT;
+  const bool pc = c->op.precond != HBPDC_PC_NONE;
   for (int r = 0; r <= c->op.newton_max; ++r) {
     int na = 0;
     for (int i = 0; i < B; ++i) {
@@ -1230,7 +1279,7 @@ hbpdc_status stage_ops(hbpdc_ctx* c, const double* w, double* r1, double* r2) {
 }
 
 hbpdc_status ensure_pc_for(hbpdc_ctx* c, double a1, double a2, double dt, const double* Wn) {
-  if (c->op.precond != HBPDC_PC_BJEXT || c->op.precond_policy != HBPDC_PC_PER_STEP_PER_ALPHA) return HBPDC_OK;
+  if (c->op.precond == HBPDC_PC_NONE || c->op.precond_policy != HBPDC_PC_PER_STEP_PER_ALPHA) return HBPDC_OK;
   // (alpha1, alpha2) pairs equal up to rounding (dc = c_l - c_{l-1} is constant
   // for q = 4, 6, 8 in exact arithmetic, App. A) share one build (reading R12)
   auto same = [](double x, double y) { return std::fabs(x - y) <= 1e-12 * std::fabs(y); };
@@ -1472,6 +1521,9 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->n = (size_t)c->nE * c->m;
   c->restart = op->gmres_restart;
   c->sstep = op->gmres_sstep > 1 ? op->gmres_sstep : 1;
+  if (op->precond < HBPDC_PC_NONE || op->precond > HBPDC_PC_BJEXT_H) return bad("unknown precond");
+  if (op->precond == HBPDC_PC_BJEXT_H && pb->equation == HBPDC_NAVIER_STOKES)
+    return bad("BJ^H_ext is implemented for advection and Euler (Navier-Stokes: BJ_ext)");
   if (c->sstep != 1 && c->sstep != 2 && c->sstep != 4 && c->sstep != 8) return bad("gmres_sstep must be 1, 2, 4 or 8");
   if (c->sstep > c->restart) c->sstep = 1;
   c->tab = tableau(pb->q);
@@ -1655,6 +1707,7 @@ hbpdc_status hbpdc_precond_set(hbpdc_ctx* c, double a1, double a2, double dt, co
   CK(cudaMemcpyAsync(c->S, S, nblk * c->m * c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaMemcpyAsync(c->Wb, W, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   CKS(wb_halo(c));
+
   c->pc_a1 = a1; c->pc_a2 = a2; c->pc_dt = dt;
   c->pc_valid = 1;
   return HBPDC_OK;

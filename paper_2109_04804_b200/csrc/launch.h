@@ -9,7 +9,8 @@ struct Geo;
 struct OpArgs;
 
 // OP_R1ABS needs a Geo with |Dhat| and lhm negated (see hbpdc.cu)
-enum OpKind { OP_R1 = 0, OP_R12, OP_RESID, OP_JVP_EXACT, OP_JVP_FD, OP_JVP_LINEAR, OP_KAPPLY, OP_R1ABS, OP_NKINDS };
+enum OpKind { OP_R1 = 0, OP_R12, OP_RESID, OP_JVP_EXACT, OP_JVP_FD, OP_JVP_LINEAR, OP_KAPPLY, OP_R1ABS, OP_KLIN,
+              OP_NKINDS };
 
 struct OpCfg {
   int eq, dim, P;
@@ -26,8 +27,9 @@ cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, co
 // number of jet components of the lifted gradients of (kind, state)
 int lift_jet_components(OpKind kind, int state);
 // BJ_ext: M_i = I - a1dt K_i + c2 K_i^2 for elements [e0, e0+ne), row-major m x m each
+// Sb / gSb (BJ^H_ext): sigma at the build point and its ghosts; NULL for BJ_ext
 cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
-                          double* M, int e0, int ne);
+                          double* M, int e0, int ne, const double* Sb = nullptr, const double* gSb = nullptr);
 
 // BJ_ext build by element colouring (NS): seed e_col in the colour's elements,
 // restrict a vector to them, gather K and M columns of the seeded elements

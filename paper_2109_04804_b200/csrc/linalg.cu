@@ -630,7 +630,9 @@ cudaError_t launch_block_gemv_multi(const double* S, int nr, const double* const
 #endif
   if (GEMV_USE_DMMA && m <= 4 * GD_KWMAX * (GD_CONS / 2)) {
     switch (nr) {
+      case 1: return launch_gemv_dmma<1>(S, io, m, nE, st);     // BJ^H_ext: one RHS per system
       case 2: return launch_gemv_dmma<2>(S, io, m, nE, st);
+      case 3: return launch_gemv_dmma<3>(S, io, m, nE, st);
       case 4: return launch_gemv_dmma<4>(S, io, m, nE, st);
       case 6: return launch_gemv_dmma<6>(S, io, m, nE, st);
       default: return cudaErrorInvalidValue;

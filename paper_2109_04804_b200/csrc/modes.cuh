@@ -473,5 +473,29 @@ template <int EQ, int NODES> struct ModeKApply : OneJetMode<EQ, NODES, ModeKAppl
   }
 };
 
+// BJ^H_ext apply pieces: out1 = b + a1dt * (K_i t), t = dW on the own element,
+// neighbour states frozen (K_i = element block of dR1/dW at the build state W).
+// (OpArgs reuse: W = build state, dW = t, b = base vector, a1dt = the scale.)
+template <int EQ, int NODES> struct ModeKLin : OneJetMode<EQ, NODES, ModeKLin<EQ, NODES>, J1, 1> {
+  static constexpr int NV = NVars<EQ>::value, NCH = 1;
+  static constexpr bool FROZEN_NBR = true;
+  __device__ static void load_value(const OpArgs& A, int e, int node, double* w) {
+    for (int v = 0; v < NV; ++v) w[v] = FV(W, e, v, node);
+  }
+  template <int K>
+  __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool nbr) {
+    for (int v = 0; v < NV; ++v) w[v] = J1{FV(W, e, v, node), nbr ? 0.0 : A.dW[IDX(e, v, node)]};
+  }
+  __device__ static void comb(const OpArgs&, const J1* F, double (&c)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) c[0][v] = F[v].a;
+  }
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(e, v, node);
+      A.out1[k] = fma(A.a1dt, o[0][v], A.b[k]);
+    }
+  }
+};
+
 #undef FV
 #undef IDX

@@ -1,5 +1,6 @@
 // ops_kernels.cu -- instantiation and dispatch of the fused element operators,
 // the BR1 lifting, and the BJ_ext block build (M_i = I - a1dt K_i + c2 K_i^2).
+#include <algorithm>
 #include <type_traits>
 #include "modes.cuh"
 #include "launch.h"
@@ -43,6 +44,8 @@ struct KColArgs {
   const double* gW;     // its ghost copy (halo), elements e >= nE
   const double* tan;    // shared-memory tangents, one m-vector per slot
   int m, nE;
+  const double* S;      // BJ^H_ext: sigma at the build point (R1(W)), NULL otherwise
+  const double* gS;     // its ghost copy
 };
 
 template <int EQ, int NODES> struct ModeKCol {
@@ -81,22 +84,63 @@ template <int EQ, int NODES> struct ModeKCol {
   }
 };
 
-template <int EQ, int DIM, int P, int EPB>
+// t = H e_c: the element block of dR2/dW at fixed sigma (BJ^H_ext),
+// the e1e2 part of R1(W + e1 sigma + e2 t) with t on the own element only
+// (neighbour states carry sigma but no W tangent: "element-internal influence only").
+template <int EQ, int NODES> struct ModeHCol {
+  static constexpr int NV = NVars<EQ>::value, NCH = 1;
+  using Args = KColArgs;
+  template <int K> using StateT = HJ;
+  struct State { NodeState<EQ, HJ> s; };
+  __device__ static void load(const Args& A, const Geo&, int e, int slot, int node, State& st, bool nbr) {
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = e < A.nE ? (size_t)e * A.m + v * NODES + node : (size_t)(e - A.nE) * A.m + v * NODES + node;
+      const double w = e < A.nE ? A.W[k] : A.gW[k];
+      const double sg = e < A.nE ? A.S[k] : A.gS[k];
+      st.s.w[v] = HJ{w, sg, nbr ? 0.0 : A.tan[slot * A.m + v * NODES + node], 0.0};
+    }
+  }
+  template <int DIM>
+  __device__ static void vol(const Args&, const PhysParams& pp, const State& st, double (&c)[DIM][NCH][NV]) {
+    HJ F[DIM][NV];
+    vol_flux_all<EQ, DIM>(pp, st.s, F);
+    for (int d = 0; d < DIM; ++d)
+      for (int v = 0; v < NV; ++v) c[d][0][v] = F[d][v].c;
+  }
+  static constexpr int NFP = 2, FPD = half_doubles<EQ, HJ>();
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
+                                   int nnode, int slot, bool plus, int d, int part, double* raw,
+                                   int rs) {
+    const bool use_own = (part == 0) == plus;
+    State st;
+    load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
+    half_flux<EQ, HJ>(pp, st.s, d, raw, rs);
+  }
+  __device__ static void face_combine(const Args&, const PhysParams& pp, int d, const double* rL, const double* rR,
+                                      int rs, double (&c)[NCH][NV]) {
+    HJ f[NV];
+    face_from_halves<EQ, HJ>(pp, rL, rR, rs, d, f);
+    for (int v = 0; v < NV; ++v) c[0][v] = f[v].c;
+  }
+};
+
+template <int EQ, int DIM, int P, int EPB, bool HESS>
 __global__ void __launch_bounds__(EPB * ipow(P, DIM))
 kbuild_kernel(const double* __restrict__ Wb, const double* __restrict__ gWb, const PhysParams pp, const Geo g, double a1dt, double c2,
-              double* __restrict__ M, int e0) {
+              double* __restrict__ M, int e0, const double* __restrict__ Sb, const double* __restrict__ gSb) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int NV = NVars<EQ>::value;
   constexpr int m = NV * NODES;
   using Mode = ModeKCol<EQ, NODES>;
-  constexpr int SLOT = slot_doubles<EQ, DIM, P, Mode>();
+  constexpr int SLOT = HESS ? std::max(slot_doubles<EQ, DIM, P, Mode>(), slot_doubles<EQ, DIM, P, ModeHCol<EQ, NODES>>())
+                            : slot_doubles<EQ, DIM, P, Mode>();
   extern __shared__ __align__(16) double sdyn[];
   double* sF = sdyn;                  // EPB * SLOT
   double* stan = sdyn + EPB * SLOT;   // EPB * m
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
   const int e = e0 + blockIdx.x;
   double* Me = M + (size_t)blockIdx.x * m * m;
-  KColArgs A{Wb, gWb, stan, m, g.nE};
+  KColArgs A{Wb, gWb, stan, m, g.nE, Sb, gSb};
   for (int c0 = 0; c0 < m; c0 += EPB) {
     const int col = c0 + slot;
     const bool active = col < m;
@@ -110,6 +154,17 @@ kbuild_kernel(const double* __restrict__ Wb, const double* __restrict__ gWb, con
     for (int v = 0; v < NV; ++v) stan[slot * m + v * NODES + node] = active ? y1[0][v] : 0.0;
     __syncthreads();
     eval_slot<EQ, DIM, P, Mode>(A, pp, g, e, slot, node, active, sF + slot * SLOT, y2);
+    if constexpr (HESS) {
+      // BJ^H_ext: + c2 H e_col (hyper-dual, sigma at the build point)
+      __syncthreads();
+#pragma unroll
+      for (int v = 0; v < NV; ++v) stan[slot * m + v * NODES + node] = (v * NODES + node == col) ? 1.0 : 0.0;
+      __syncthreads();
+      double y3[1][NV];
+      eval_slot<EQ, DIM, P, ModeHCol<EQ, NODES>>(A, pp, g, e, slot, node, active, sF + slot * SLOT, y3);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) y2[0][v] += y3[0][v];
+    }
     if (active) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -122,25 +177,35 @@ kbuild_kernel(const double* __restrict__ Wb, const double* __restrict__ gWb, con
   }
 }
 
-template <int EQ, int DIM, int P>
-static cudaError_t run_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
-                              double* M, int e0, int ne) {
+template <int EQ, int DIM, int P, bool HESS>
+static cudaError_t run_kbuild_t(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
+                                double c2, double* M, int e0, int ne, const double* Sb, const double* gSb) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int EPB = epb_for(NODES);
   if (ne <= 0) return cudaSuccess;
   constexpr int NV = NVars<EQ>::value;
-  constexpr size_t smem =
-      (size_t)EPB * (slot_doubles<EQ, DIM, P, ModeKCol<EQ, NODES>>() + NV * NODES) * sizeof(double);
+  constexpr int SLOT = HESS ? std::max(slot_doubles<EQ, DIM, P, ModeKCol<EQ, NODES>>(),
+                                       slot_doubles<EQ, DIM, P, ModeHCol<EQ, NODES>>())
+                            : slot_doubles<EQ, DIM, P, ModeKCol<EQ, NODES>>();
+  constexpr size_t smem = (size_t)EPB * (SLOT + NV * NODES) * sizeof(double);
   if constexpr (smem > 48 * 1024) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(kbuild_kernel<EQ, DIM, P, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(kbuild_kernel<EQ, DIM, P, EPB, HESS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
       attr = true;
     }
   }
-  kbuild_kernel<EQ, DIM, P, EPB><<<ne, EPB * NODES, smem, c.stream>>>(Wb, gWb, c.pp, g, a1dt, c2, M, e0);
+  kbuild_kernel<EQ, DIM, P, EPB, HESS><<<ne, EPB * NODES, smem, c.stream>>>(Wb, gWb, c.pp, g, a1dt, c2, M, e0, Sb, gSb);
   hbpdc_count_launch();
   return cudaGetLastError();
+}
+
+template <int EQ, int DIM, int P>
+static cudaError_t run_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
+                              double* M, int e0, int ne, const double* Sb, const double* gSb) {
+  if (Sb) return run_kbuild_t<EQ, DIM, P, true>(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb);
+  return run_kbuild_t<EQ, DIM, P, false>(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb);
 }
 
 // ---- dispatch ----------------------------------------------------------------------
@@ -159,6 +224,9 @@ template <int EQ, int DIM, int P> struct Disp {
         else return cudaErrorInvalidValue;
       case OP_KAPPLY:
         if constexpr (EQ != 2) return run_op<EQ, DIM, P, ModeKApply<EQ, NODES>>(c, g, A);
+        else return cudaErrorNotSupported;
+      case OP_KLIN:
+        if constexpr (EQ != 2) return run_op<EQ, DIM, P, ModeKLin<EQ, NODES>>(c, g, A);
         else return cudaErrorNotSupported;
       default: return cudaErrorInvalidValue;
     }
@@ -179,8 +247,8 @@ template <int EQ, int DIM, int P> struct Disp {
     return cudaErrorInvalidValue;
   }
   static cudaError_t kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
-                            double* M, int e0, int ne) {
-    if constexpr (EQ != 2) return run_kbuild<EQ, DIM, P>(c, g, Wb, gWb, a1dt, c2, M, e0, ne);
+                            double* M, int e0, int ne, const double* Sb, const double* gSb) {
+    if constexpr (EQ != 2) return run_kbuild<EQ, DIM, P>(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb);
     return cudaErrorNotSupported;
   }
 };
@@ -224,8 +292,8 @@ int lift_jet_components(OpKind kind, int state) {
 }
 
 cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
-                          double* M, int e0, int ne) {
-  return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, gWb, a1dt, c2, M, e0, ne); });
+                          double* M, int e0, int ne, const double* Sb, const double* gSb) {
+  return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb); });
 }
 
 // ---- BJ_ext build by element colouring (Navier-Stokes, BR1 stencil radius 2) ----

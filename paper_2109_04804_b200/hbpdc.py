@@ -15,11 +15,11 @@ LIB_PATH = os.environ.get("HBPDC_LIB", os.path.join(_HERE, "libhbpdc.so"))
 
 ADVECTION, EULER, NAVIER_STOKES = 0, 1, 2
 GLL, GL = 0, 1
-PC_NONE, PC_BJEXT = 0, 1
+PC_NONE, PC_BJEXT, PC_BJEXT_H = 0, 1, 2
 PC_PER_STEP_PER_ALPHA, PC_PER_NEWTON = 0, 1
 JVP_AUTO, JVP_FD, JVP_EXACT, JVP_LINEAR = 0, 1, 2, 3
 _EQ = {"advection": ADVECTION, "euler": EULER, "navier_stokes": NAVIER_STOKES}
-_PC = {"none": PC_NONE, "bjext": PC_BJEXT}
+_PC = {"none": PC_NONE, "bjext": PC_BJEXT, "bjext_h": PC_BJEXT_H}
 _JVP = {"auto": JVP_AUTO, "fd": JVP_FD, "exact": JVP_EXACT, "linear": JVP_LINEAR}
 
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_CUDA", 3: "E_NCCL", 4: "E_OOM", 5: "E_NONFINITE",

@@ -331,3 +331,55 @@ def test_sstep_advection_end_of_run(precond, cfl, s):
     for _ in range(cfg.steps):
         ctx.step(dt, Wg)
     assert rel(to_np(Wg), Wo) <= 1e-8
+
+
+# ---- NEXT-2: BJ^H_ext (the Hessian block included) -----------------------
+
+@pytest.mark.parametrize("case", [c for c in PC_CASES if c[0] != "navier_stokes"])
+def test_precond_bjext_h_build_and_apply(case):
+    """S^H = (I - a1 dt K + c2 (H + K^2))^-1 per element and the apply
+    u = S^H (x - c2 K y), (u, y + K u) vs the oracle's literal D^H,E^H,F^H,G^H
+    blocks (built at (W, R1(W)), reading R31)."""
+    kind = case[0]
+    d, ctx = _pair(*case, precond="bjext_h")
+    W = _state(d, kind, SEED + 27)
+    a1, a2, dt = 1.0 / 6.0, 1.0 / 54.0, 0.05
+    pc = implicit.BJExtH(d, W, dgsem.rhs1(d, W), a1, a2, dt)
+    ctx.precond_build(a1, a2, dt, to_gpu(W))
+    shared = kind == "advection"
+    Sg, flag = ctx.precond_export(shared_hint=shared)
+    Sg = to_np(Sg).reshape(-1, d.m, d.m)
+    So = pc.S[:1] if shared else pc.S
+    cond = max(np.linalg.cond(M) for M in pc.M)
+    assert np.linalg.norm(Sg - So) / np.linalg.norm(So) <= 1e-11 * max(1.0, cond / 1e4)
+    x = inputs.random_field(d.n, SEED + 28)
+    y = inputs.random_field(d.n, SEED + 29)
+    to, bo = pc.apply(x, y)
+    tg, bg = ctx.precond_apply(to_gpu(x), to_gpu(y))
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11 * max(1, cond / 1e4)
+    # identical S^H installed: the K pieces alone differ by rounding
+    ctx.precond_set(a1, a2, dt, to_gpu(W), to_gpu(So.reshape(-1)), shared)
+    tg, bg = ctx.precond_apply(to_gpu(x), to_gpu(y))
+    to2, bo2 = pc.apply_sk(x, y)
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to2, bo2])) <= 1e-13
+
+
+@pytest.mark.parametrize("batch", [False, True])
+def test_euler_end_of_run_bjext_h(batch):
+    """C3 physics at 4x4 elements, N=3, HBPC(8,4) with BJ^H_ext: end of run vs the
+    oracle <= 1e-8; lock-step correctors (3 systems, 1-RHS GEMV each) as well."""
+    q, kmax = 8, 4
+    cfg = configs.scaled(configs.CONFIGS["C3"], N=3, nx=4, ny=4, steps=2, q=q, kmax=kmax)
+    d, ctx = make_pair("euler", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=q, kmax=kmax,
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, precond="bjext_h",
+                       batch_stages=batch)
+    W0 = inputs.initial_state("C3", d.node_coords(), noise=cfg.noise)
+    dt = configs.cfl_dt(cfg, inputs.initial_state("C3", d.node_coords()))
+    Wo, sto = _run_oracle(d, q, kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol,
+                          precond="bjext_h")
+    Wg = to_gpu(W0)
+    its = 0
+    for _ in range(cfg.steps):
+        its += ctx.step(dt, Wg)["gmres_its"]
+    assert rel(to_np(Wg), Wo) <= 1e-8
+    assert its <= 1.25 * sto["gmres_its"] + 10, (its, sto["gmres_its"])
