@@ -229,8 +229,8 @@ def rhs1_field(disc: Disc, Wf, absolute=False):
         Fa = ad.stack(F, axis=va)
         # traces of the state (and of the lifted gradients for NS)
         wp, wnp, wnm, wm = [_split(t, va) for t in ops.faces(Wf, d)]
-        fp = list(physics.llf(eq, wp, wnp, d))           # + face: L = own, R = nbr
-        fm = list(physics.llf(eq, wnm, wm, d))           # - face: L = nbr, R = own
+        fp = list(physics.numerical_flux(eq, wp, wnp, d))   # + face: L = own, R = nbr
+        fm = list(physics.numerical_flux(eq, wnm, wm, d))   # - face: L = nbr, R = own
         if eq.viscous:
             gxp, gxnp, gxnm, gxm = [_split(t, 2) for t in ops.faces(Gx, d)]
             gyp, gynp, gynm, gym = [_split(t, 2) for t in ops.faces(Gy, d)]

@@ -35,6 +35,7 @@ class Equation:
     gamma: float = 1.4
     mu: float = 0.0
     prandtl: float = 0.72
+    numflux: str = "llf"       # "llf" (configs, reading R3) | "glf" (the paper's eq:Riemann)
 
     @property
     def nv(self):
@@ -79,6 +80,26 @@ def llf(eq, wL, wR, d):
     lam = ad.maxval(wave_speed(eq, wL, d), wave_speed(eq, wR, d))
     return tuple(0.5 * (fl + fr) + 0.5 * lam * (l - r)
                  for fl, fr, l, r in zip(FL, FR, wL, wR))
+
+
+def glf(eq, wL, wR, d):
+    """The paper's numerical flux eq:Riemann: global Lax-Friedrichs
+    with a constant dissipation matrix, lambda = |a.n| for advection and
+    Lambda = diag(1/eps, 1, 1, 1/eps) for Euler / NS with the reference
+    Mach number eps = 1 (reading R18), i.e. Lambda = I.  Canonical orientation."""
+    FL, FR = flux(eq, wL, d), flux(eq, wR, d)
+    if eq.kind == "advection":
+        lam = (abs(eq.a[d]),)
+    else:
+        eps = 1.0
+        lam = (1.0 / eps, 1.0, 1.0, 1.0 / eps)
+    return tuple(0.5 * (fl + fr) + 0.5 * lv * (l - r)
+                 for fl, fr, l, r, lv in zip(FL, FR, wL, wR, lam))
+
+
+def numerical_flux(eq, wL, wR, d):
+    """f*(wL, wR; e_d) of the equation's choice (LLF or the paper's GLF)."""
+    return glf(eq, wL, wR, d) if eq.numflux == "glf" else llf(eq, wL, wR, d)
 
 
 # ---- Navier-Stokes --------------------------------------------------------

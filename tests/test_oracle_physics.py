@@ -131,3 +131,48 @@ def test_grad_vars_example():
     w = (np.array(1.0), np.array(0.0), np.array(0.0), np.array(1.0 / 0.4))
     out = physics.grad_vars(NS, w)
     np.testing.assert_allclose([float(x) for x in out], g["wgrad"], atol=1e-15)
+
+
+def test_glf_paper_flux():
+    """The paper's eq:Riemann with Lambda = diag(1/eps,1,1,1/eps),
+    eps = 1 (R18): consistency f*(w, w) = F(w); the dissipation is exactly
+    1/2 (wL - wR) per variable; conservation under the mirror map; advection:
+    lambda = |a.n|, i.e. identical to the upwind / LLF flux."""
+    EG = physics.Equation("euler", numflux="glf")
+    rng = np.random.default_rng(31)
+    wL = (1.2, 0.3, -0.2, 2.6)
+    wR = (0.9, -0.1, 0.4, 2.2)
+    for d in (0, 1):
+        fc = physics.glf(EG, wL, wL, d)
+        F = physics.flux(EG, wL, d)
+        assert all(abs(a - b) < 1e-15 for a, b in zip(fc, F))
+        f = physics.glf(EG, wL, wR, d)
+        FL, FR = physics.flux(EG, wL, d), physics.flux(EG, wR, d)
+        for v in range(4):
+            assert f[v] == pytest.approx(0.5 * (FL[v] + FR[v]) + 0.5 * (wL[v] - wR[v]), abs=1e-15)
+    ea = physics.Equation("advection", a=(0.7, -0.4), numflux="glf")
+    el = physics.Equation("advection", a=(0.7, -0.4))
+    for d in (0, 1):
+        l, r = (rng.standard_normal(5),), (rng.standard_normal(5),)
+        np.testing.assert_allclose(physics.glf(ea, l, r, d)[0], physics.llf(el, l, r, d)[0], rtol=0, atol=1e-15)
+
+
+def test_glf_free_stream_and_conservation():
+    """R1 with the paper's flux: a constant state has a zero residual; the
+    quadrature-weighted sum of R1 vanishes (periodic conservation)."""
+    from oracle import basis, dgsem
+    eq = physics.Equation("euler", numflux="glf")
+    d = dgsem.Disc(basis.build_basis(3, "gll"), dgsem.Mesh(2, 3, 4), eq)
+    W = np.zeros(d.field_shape())
+    for v, x in enumerate([1.1, 0.2, -0.3, 2.4]):
+        W[:, :, v] = x
+    R = dgsem.rhs1(d, W.reshape(-1))
+    assert np.abs(R).max() < 1e-12
+    rng = np.random.default_rng(32)
+    W2 = (W.reshape(-1) * (1 + 0.05 * rng.uniform(-1, 1, d.n)))
+    R2 = dgsem.rhs1(d, W2).reshape(d.mesh.n_elem, 4, -1)
+    B = basis.build_basis(3, "gll")
+    wq = np.outer(B.w, B.w).reshape(-1)
+    for v in range(4):
+        tot = np.sum(R2[:, v] * wq)
+        assert abs(tot) <= 1e-12 * np.sum(np.abs(R2[:, v]) * wq)
