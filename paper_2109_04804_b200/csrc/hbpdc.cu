@@ -1521,6 +1521,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->n = (size_t)c->nE * c->m;
   c->restart = op->gmres_restart;
   c->sstep = op->gmres_sstep > 1 ? op->gmres_sstep : 1;
+  if (pb->flux != HBPDC_LLF && pb->flux != HBPDC_GLF_PAPER) return bad("flux must be HBPDC_LLF or HBPDC_GLF_PAPER");
   if (op->precond < HBPDC_PC_NONE || op->precond > HBPDC_PC_BJEXT_H) return bad("unknown precond");
   if (op->precond == HBPDC_PC_BJEXT_H && pb->equation == HBPDC_NAVIER_STOKES)
     return bad("BJ^H_ext is implemented for advection and Euler (Navier-Stokes: BJ_ext)");
@@ -1551,6 +1552,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->cfg.pp.ax = pb->a[0];
   c->cfg.pp.ay = pb->a[1];
   c->cfg.pp.gamma = pb->gamma;
+  c->cfg.pp.glf = pb->flux == HBPDC_GLF_PAPER ? 1 : 0;
   c->cfg.pp.mu = pb->mu;
   c->cfg.pp.Rgas = 1.0 / pb->gamma;
   c->cfg.pp.lamT = (c->cfg.pp.Rgas * pb->gamma / (pb->gamma - 1.0)) * pb->mu / (pb->prandtl > 0 ? pb->prandtl : 1.0);

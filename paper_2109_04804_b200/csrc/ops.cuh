@@ -209,7 +209,7 @@ __device__ __forceinline__ void face_from_halves(const PhysParams& pp, const dou
   if constexpr (EQ == 0) {
     lam = jconst<T>(d == 0 ? (pp.ax >= 0 ? pp.ax : -pp.ax) : (pp.ay >= 0 ? pp.ay : -pp.ay));
   } else {
-    lam = jmax(rd(rL, 2 * NV), rd(rR, 2 * NV));
+    lam = pp.glf ? jconst<T>(1.0) : jmax(rd(rL, 2 * NV), rd(rR, 2 * NV));
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v)

@@ -7,6 +7,9 @@
 //              lam = max(|v_L.e_d| + c_L, |v_R.e_d| + c_R)  (reading R3; the paper's
 //              eq:Riemann is the global-lambda variant).  Canonical orientation:
 //              L = element on the -e_d side, normal +e_d; ties take L.
+//  GLF       : (pp.glf, HBPDC_GLF_PAPER) the paper's eq:Riemann with the constant
+//              Lambda = diag(1/eps, 1, 1, 1/eps) of P:395 at eps = 1, i.e. lam = 1;
+//              advection |a_d| as LLF.
 //  NS        : viscous flux F^v with BR1 gradients (reading R19).
 #pragma once
 #include "jets.cuh"
@@ -15,6 +18,7 @@ struct PhysParams {
   double ax, ay;         // advection velocity
   double gamma;
   double mu, lamT, Rgas; // NS: viscosity, heat conductivity c_p mu / Pr, R = 1/gamma
+  int glf;               // 1: the paper's global LF flux (Lambda = I at eps = 1), 0: LLF
 };
 
 template <int EQ> struct NVars { static constexpr int value = 4; };
@@ -76,7 +80,7 @@ __device__ __forceinline__ void llf_flux(const PhysParams& pp, const T* wL, cons
     const EulerPrim<T> qL = euler_prim(pp, wL), qR = euler_prim(pp, wR);
     euler_flux(wL, qL, d, FL);
     euler_flux(wR, qR, d, FR);
-    lam = jmax(euler_speed(pp, qL, d), euler_speed(pp, qR, d));
+    lam = pp.glf ? jconst<T>(1.0) : jmax(euler_speed(pp, qL, d), euler_speed(pp, qR, d));
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v) f[v] = 0.5 * (FL[v] + FR[v]) + 0.5 * lam * (wL[v] - wR[v]);

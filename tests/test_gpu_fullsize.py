@@ -198,6 +198,30 @@ def test_c3_fullsize_step_invariants():
     ctx.close()
 
 
+def test_c3_fullsize_sstep_pipeline():
+    """The bench's Arnoldi pipeline at full C3 size (s-step s = 8: TMA-streamed
+    and fused block Gram-Schmidt, DMMA GEMV with 2 and 6 right-hand sides, K-apply
+    norm epilogue) against the DCGS2 schedule (s = 1): one HBPC(8,4) step each,
+    both converged to Newton/GMRES 1e-10, end states equal to the solver
+    tolerance (reading R28)."""
+    import torch
+    cfg = configs.CONFIGS["C3"]
+    out = {}
+    for s in (8, 1):
+        ctx = hbpdc.context_for(cfg, gmres_sstep=s)
+        coords = ctx.node_coords()
+        W0 = inputs.initial_state("C3", coords, noise=cfg.noise)
+        dt = configs.cfl_dt(cfg, inputs.initial_state("C3", coords))
+        Wg = to_gpu(W0)
+        st = ctx.step(dt, Wg)
+        torch.cuda.synchronize()
+        out[s] = (to_np(Wg), st)
+        ctx.close()
+    assert rel(out[8][0], out[1][0]) <= 1e-8
+    assert out[8][1]["stage_solves"] == out[1][1]["stage_solves"] == 15
+    assert out[8][1]["gmres_its"] <= 1.25 * out[1][1]["gmres_its"] + 64
+
+
 @pytest.mark.parametrize("case", ["C1", "C2"])
 def test_fullsize_linear_end_of_run(case):
     """C1 and C2 EXACTLY as BASELINE.json states them (full mesh, all steps),

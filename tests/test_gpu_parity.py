@@ -383,3 +383,55 @@ def test_euler_end_of_run_bjext_h(batch):
         its += ctx.step(dt, Wg)["gmres_its"]
     assert rel(to_np(Wg), Wo) <= 1e-8
     assert its <= 1.25 * sto["gmres_its"] + 10, (its, sto["gmres_its"])
+
+
+# ---- NEXT-3 (part): the paper's numerical flux eq:Riemann (global LF, Lambda = I at eps = 1) ----
+
+GLF_CASES = [("euler", 3, 5, 4, (0.0, 1.0, 0.0, 1.0)),
+             ("euler", 7, 3, 3, (0.0, 1.0, 0.0, 1.0)),
+             ("navier_stokes", 3, 4, 4, (0.0, 2 * np.pi, 0.0, 2 * np.pi))]
+
+
+@pytest.mark.parametrize("case", GLF_CASES)
+def test_glf_operators(case):
+    """R1, R2, residual, EXACT JVP and (Euler) BJ_ext with flux = GLF_PAPER vs the
+    oracle's Equation(numflux='glf'), <= 1e-11."""
+    kind = case[0]
+    d, ctx = _pair(*case, flux="glf")
+    W = _state(d, kind, SEED + 41)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 42))
+    assert rel(to_np(ctx.rhs(to_gpu(W))), dgsem.rhs1(d, W)) <= 1e-11
+    assert rel(to_np(ctx.rhs(to_gpu(W), to_gpu(sig))), dgsem.rhs2(d, W, sig)) <= 1e-11
+    b = W * (1 + 1e-3 * inputs.random_field(d.n, SEED + 43))
+    a1, a2, dt = 0.5, 1 / 6, 0.02
+    G1o, G2o = implicit.residual(d, a1, a2, dt, b, W, sig)
+    G1g, G2g = ctx.residual(a1, a2, dt, to_gpu(b), to_gpu(W), to_gpu(sig))
+    assert rel(np.concatenate([to_np(G1g), to_np(G2g)]), np.concatenate([G1o, G2o])) <= 1e-11
+    dW = inputs.random_field(d.n, SEED + 44, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 45, unit_norm=True)
+    to, bo = implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds)
+    tg, bg = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(dW), to_gpu(ds), mode="exact")
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11
+    if kind == "euler":
+        pc = implicit.BJExt(d, W, a1, a2, dt)
+        ctx.precond_build(a1, a2, dt, to_gpu(W))
+        cond = max(np.linalg.cond(M) for M in pc.M)
+        to, bo = pc.apply(dW, ds)
+        tg, bg = ctx.precond_apply(to_gpu(dW), to_gpu(ds))
+        assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11 * max(1, cond / 1e4)
+
+
+def test_glf_euler_end_of_run():
+    """C3 physics at 4x4 elements, N=3, HBPC(6,2) with the paper's flux: end of run
+    vs the oracle <= 1e-8."""
+    q, kmax = 6, 2
+    cfg = configs.scaled(configs.CONFIGS["C3"], N=3, nx=4, ny=4, steps=2, q=q, kmax=kmax)
+    d, ctx = make_pair("euler", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=q, kmax=kmax,
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, flux="glf")
+    W0 = inputs.initial_state("C3", d.node_coords(), noise=cfg.noise)
+    dt = configs.cfl_dt(cfg, inputs.initial_state("C3", d.node_coords()))
+    Wo, _ = _run_oracle(d, q, kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol)
+    Wg = to_gpu(W0)
+    for _ in range(cfg.steps):
+        ctx.step(dt, Wg)
+    assert rel(to_np(Wg), Wo) <= 1e-8
