@@ -9,7 +9,9 @@ hyper-duals.
   advection     F = a w                                   (C1/C2)
   euler         F_x = (rho u, rho u^2 + p, rho u v, u (E + p))      (eq:Euler,
                 p = (gamma-1)(E - rho |v|^2 / 2)                     P:388-394)
-                with reference Mach number eps = 1 (reading R18)
+                and the reference Mach number eps of eq:Euler: momentum flux
+                rho v v + p / eps^2, p = (gamma-1)(E - eps^2 rho |v|^2 / 2)
+                (configs: eps = 1, reading R18; NS only at eps = 1)
   navier_stokes F - F^v, F^v = (0, tau, tau.v + q), tau = mu(grad v +
                 grad v^T - 2/3 div v I), q = lambda_T grad T, lambda_T = c_p mu/Pr,
                 c_p = R gamma/(gamma-1), R = 1/gamma, T = p/(rho R)
@@ -36,6 +38,7 @@ class Equation:
     mu: float = 0.0
     prandtl: float = 0.72
     numflux: str = "llf"       # "llf" (configs, reading R3) | "glf" (the paper's eq:Riemann)
+    mach: float = 1.0          # reference Mach number eps of eq:Euler; configs: 1 (R18)
 
     @property
     def nv(self):
@@ -47,8 +50,10 @@ class Equation:
 
 
 def pressure(eq, w):
+    """p = (gamma - 1)(E - eps^2/2 rho |v|^2)."""
     rho, mx, my, E = w
-    return (eq.gamma - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho)
+    e2 = eq.mach * eq.mach
+    return (eq.gamma - 1.0) * (E - 0.5 * e2 * (mx * mx + my * my) / rho)
 
 
 def flux(eq, w, d):
@@ -57,10 +62,11 @@ def flux(eq, w, d):
         return (eq.a[d] * w[0],)
     rho, mx, my, E = w
     p = pressure(eq, w)
+    pe = p / (eq.mach * eq.mach)             # p / eps^2 in the momentum flux (eq:Euler)
     vn = (mx if d == 0 else my) / rho
     return (rho * vn,
-            mx * vn + (p if d == 0 else 0.0),
-            my * vn + (p if d == 1 else 0.0),
+            mx * vn + (pe if d == 0 else 0.0),
+            my * vn + (pe if d == 1 else 0.0),
             vn * (E + p))
 
 
@@ -71,7 +77,7 @@ def wave_speed(eq, w, d):
     rho, mx, my, E = w
     p = pressure(eq, w)
     vn = (mx if d == 0 else my) / rho
-    return ad.absval(vn) + ad.sqrt(eq.gamma * p / rho)
+    return ad.absval(vn) + ad.sqrt(eq.gamma * p / rho) / eq.mach   # eigenvalues v.n +- c / eps
 
 
 def llf(eq, wL, wR, d):
@@ -85,13 +91,13 @@ def llf(eq, wL, wR, d):
 def glf(eq, wL, wR, d):
     """The paper's numerical flux eq:Riemann: global Lax-Friedrichs
     with a constant dissipation matrix, lambda = |a.n| for advection and
-    Lambda = diag(1/eps, 1, 1, 1/eps) for Euler / NS with the reference
-    Mach number eps = 1 (reading R18), i.e. Lambda = I.  Canonical orientation."""
+    Lambda = diag(1/eps, 1, 1, 1/eps) for Euler / NS, eps the reference
+    Mach number (configs: eps = 1, reading R18).  Canonical orientation."""
     FL, FR = flux(eq, wL, d), flux(eq, wR, d)
     if eq.kind == "advection":
         lam = (abs(eq.a[d]),)
     else:
-        eps = 1.0
+        eps = eq.mach
         lam = (1.0 / eps, 1.0, 1.0, 1.0 / eps)
     return tuple(0.5 * (fl + fr) + 0.5 * lv * (l - r)
                  for fl, fr, l, r, lv in zip(FL, FR, wL, wR, lam))

@@ -176,3 +176,49 @@ def test_glf_free_stream_and_conservation():
     for v in range(4):
         tot = np.sum(R2[:, v] * wq)
         assert abs(tot) <= 1e-12 * np.sum(np.abs(R2[:, v]) * wq)
+
+
+def test_reference_mach_scaling():
+    """eq:Euler with reference Mach number eps is the standard Euler
+    system (eps = 1) in the variables W~ = T W, T = diag(1, eps, eps, 1), with time
+    scaled by 1/eps: F~(T w) = eps T F_eps(w), and with the LLF flux (lambda~ =
+    eps lambda_eps) R1_eps(W) = T^-1 R1_1(T W) / eps node by node."""
+    from oracle import basis, dgsem
+    eps = 0.1
+    rng = np.random.default_rng(33)
+    e1 = physics.Equation("euler")
+    ee = physics.Equation("euler", mach=eps)
+    w = (1.1, 0.3, -0.2, 25.0)
+    T = (1.0, eps, eps, 1.0)
+    wt = tuple(t * x for t, x in zip(T, w))
+    for d in (0, 1):
+        F1 = physics.flux(e1, wt, d)
+        Fe = physics.flux(ee, w, d)
+        for v in range(4):
+            assert F1[v] == pytest.approx(eps * T[v] * Fe[v], rel=1e-14)
+        assert physics.wave_speed(e1, wt, d) == pytest.approx(eps * physics.wave_speed(ee, w, d), rel=1e-14)
+    mesh = dgsem.Mesh(2, 3, 3)
+    B = basis.build_basis(3, "gll")
+    d1, de = dgsem.Disc(B, mesh, e1), dgsem.Disc(B, mesh, ee)
+    W = np.zeros(de.field_shape())
+    for v, x in enumerate([1.0, 0.5, -0.3, 30.0]):
+        W[:, :, v] = x
+    W = W * (1 + 0.02 * rng.uniform(-1, 1, W.shape))
+    Wt = (W.reshape(mesh.n_elem, 4, -1) * np.array(T)[None, :, None]).reshape(-1)
+    R1e = dgsem.rhs1(de, W.reshape(-1)).reshape(mesh.n_elem, 4, -1)
+    R11 = dgsem.rhs1(d1, Wt).reshape(mesh.n_elem, 4, -1)
+    np.testing.assert_allclose(R1e, R11 / (eps * np.array(T)[None, :, None]), rtol=1e-10,
+                               atol=1e-12 * np.abs(R1e).max())
+
+
+@pytest.mark.parametrize("numflux", ["llf", "glf"])
+def test_reference_mach_free_stream(numflux):
+    """eps = 0.01: a constant state has a zero residual with either flux."""
+    from oracle import basis, dgsem
+    eq = physics.Equation("euler", mach=0.01, numflux=numflux)
+    d = dgsem.Disc(basis.build_basis(3, "gll"), dgsem.Mesh(2, 3, 4), eq)
+    W = np.zeros(d.field_shape())
+    for v, x in enumerate([1.1, 0.2, -0.3, 2.4]):
+        W[:, :, v] = x
+    R = dgsem.rhs1(d, W.reshape(-1))
+    assert np.abs(R).max() < 1e-9
