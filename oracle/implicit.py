@@ -62,11 +62,13 @@ def fd_eps(dv, mach=1.0, eps_machine=EPS_MACH):
 
 
 def jvp_fd(disc, a1, a2, dt, W, sig, dW, dsig, eps_override=None,
-           sigma_literal=False, mach=1.0):
+           sigma_literal=False, mach=None):
     """Matrix-free FD product eq:MatrixFree_nonlinear.
     sigma direction: R2(W, dsigma) exactly (reading R8) unless
     sigma_literal, which uses (R2(W, sig + eps dsig) - R2(W, sig)) / eps."""
     c2 = a2 * dt * dt / 2.0
+    if mach is None:                 # the reference Mach number of the equation (P:606-611)
+        mach = getattr(disc.eq, "mach", 1.0)
     if eps_override is not None:
         ew, es = eps_override
     else:

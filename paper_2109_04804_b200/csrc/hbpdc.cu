@@ -1486,7 +1486,9 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->N < 1 || pb->N > 7) return bad("N must be in 1..7");
   if (pb->nodes != HBPDC_GLL) return bad("only Gauss-Lobatto nodes are implemented on the GPU (reading R1)");
   if (pb->flux != HBPDC_LLF) return bad("only the LLF flux is implemented (reading R3)");
-  if (pb->equation != HBPDC_ADVECTION && pb->mach_eps != 1.0) return bad("mach_eps must be 1 (reading R18)");
+  if (!(pb->mach_eps > 0.0)) return bad("mach_eps must be positive");
+  if (pb->equation == HBPDC_NAVIER_STOKES && pb->mach_eps != 1.0)
+    return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");
   if (pb->q != 4 && pb->q != 6 && pb->q != 8) return bad("q must be 4, 6 or 8");
   if (pb->kmax < 0) return bad("kmax must be >= 0");
   if (pb->nx < 1 || (pb->dim == 2 && pb->ny < 1)) return bad("element counts must be positive");
@@ -1553,6 +1555,9 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->cfg.pp.ay = pb->a[1];
   c->cfg.pp.gamma = pb->gamma;
   c->cfg.pp.glf = pb->flux == HBPDC_GLF_PAPER ? 1 : 0;
+  c->cfg.pp.ieps = 1.0 / pb->mach_eps;
+  c->cfg.pp.eps2 = pb->mach_eps * pb->mach_eps;
+  c->cfg.pp.ieps2 = 1.0 / c->cfg.pp.eps2;
   c->cfg.pp.mu = pb->mu;
   c->cfg.pp.Rgas = 1.0 / pb->gamma;
   c->cfg.pp.lamT = (c->cfg.pp.Rgas * pb->gamma / (pb->gamma - 1.0)) * pb->mu / (pb->prandtl > 0 ? pb->prandtl : 1.0);

@@ -212,8 +212,14 @@ __device__ __forceinline__ void face_from_halves(const PhysParams& pp, const dou
     lam = pp.glf ? jconst<T>(1.0) : jmax(rd(rL, 2 * NV), rd(rR, 2 * NV));
   }
 #pragma unroll
-  for (int v = 0; v < NV; ++v)
-    f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + 0.5 * lam * (rd(rL, NV + v) - rd(rR, NV + v));
+  for (int v = 0; v < NV; ++v) {
+    if (EQ != 0 && pp.glf) {       // as llf_flux: constant Lambda = diag(1/eps, 1, 1, 1/eps)
+      const double lv = (v == 0 || v == NV - 1) ? pp.ieps : 1.0;
+      f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + (0.5 * lv) * (rd(rL, NV + v) - rd(rR, NV + v));
+    } else {
+      f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + 0.5 * lam * (rd(rL, NV + v) - rd(rR, NV + v));
+    }
+  }
   if constexpr (EQ == 2) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) f[v] = f[v] - 0.5 * (rd(rL, 2 * NV + 1 + v) + rd(rR, 2 * NV + 1 + v));

@@ -2,14 +2,15 @@
 //
 //  advection : F_d = a_d w
 //  Euler     : F_x = (rho u, rho u^2 + p, rho u v, u (E + p)), p = (gamma-1)(E - rho|v|^2/2)
-//              (eq:Euler; reference Mach number eps = 1, reading R18)
+//              (eq:Euler; configs: reference Mach number eps = 1, reading R18)
 //  LLF       : f* = 1/2 (F_d(wL) + F_d(wR)) + 1/2 lam (wL - wR),
 //              lam = max(|v_L.e_d| + c_L, |v_R.e_d| + c_R)  (reading R3; the paper's
 //              eq:Riemann is the global-lambda variant).  Canonical orientation:
 //              L = element on the -e_d side, normal +e_d; ties take L.
 //  GLF       : (pp.glf, HBPDC_GLF_PAPER) the paper's eq:Riemann with the constant
-//              Lambda = diag(1/eps, 1, 1, 1/eps) of P:395 at eps = 1, i.e. lam = 1;
-//              advection |a_d| as LLF.
+//              Lambda = diag(1/eps, 1, 1, 1/eps) of P:395; advection |a_d| as LLF.
+//  eps       : reference Mach number (mach_eps): momentum flux p / eps^2, p with eps^2 in
+//              the kinetic energy, wave speed |v.n| + c / eps (Euler; NS only at eps = 1).
 //  NS        : viscous flux F^v with BR1 gradients (reading R19).
 #pragma once
 #include "jets.cuh"
@@ -18,7 +19,8 @@ struct PhysParams {
   double ax, ay;         // advection velocity
   double gamma;
   double mu, lamT, Rgas; // NS: viscosity, heat conductivity c_p mu / Pr, R = 1/gamma
-  int glf;               // 1: the paper's global LF flux (Lambda = I at eps = 1), 0: LLF
+  int glf;               // 1: the paper's global LF flux (Lambda = diag(1/eps,1,1,1/eps)), 0: LLF
+  double ieps, eps2, ieps2;   // reference Mach number eps of eq:Euler: 1/eps, eps^2, 1/eps^2
 };
 
 template <int EQ> struct NVars { static constexpr int value = 4; };
@@ -28,6 +30,7 @@ template <> struct NVars<0> { static constexpr int value = 1; };
 // directions and the wave speed: one jet reciprocal per state.
 template <class T> struct EulerPrim {
   T u, v, p, H, rinv;   // velocity, pressure, E + p, 1/rho
+  T pe;                 // p / eps^2 (momentum flux, eq:Euler)
 };
 
 template <class T>
@@ -36,8 +39,9 @@ __device__ __forceinline__ EulerPrim<T> euler_prim(const PhysParams& pp, const T
   q.rinv = jrecip(w[0]);
   q.u = w[1] * q.rinv;
   q.v = w[2] * q.rinv;
-  q.p = (pp.gamma - 1.0) * (w[3] - 0.5 * (w[1] * q.u + w[2] * q.v));
+  q.p = (pp.gamma - 1.0) * (w[3] - (0.5 * pp.eps2) * (w[1] * q.u + w[2] * q.v));
   q.H = w[3] + q.p;
+  q.pe = pp.ieps2 * q.p;
   return q;
 }
 
@@ -46,8 +50,8 @@ template <class T>
 __device__ __forceinline__ void euler_flux(const T* w, const EulerPrim<T>& q, int d, T* F) {
   const T vn = d == 0 ? q.u : q.v;
   F[0] = d == 0 ? w[1] : w[2];
-  F[1] = d == 0 ? w[1] * vn + q.p : w[1] * vn;
-  F[2] = d == 1 ? w[2] * vn + q.p : w[2] * vn;
+  F[1] = d == 0 ? w[1] * vn + q.pe : w[1] * vn;
+  F[2] = d == 1 ? w[2] * vn + q.pe : w[2] * vn;
   F[3] = vn * q.H;
 }
 
@@ -63,7 +67,7 @@ __device__ __forceinline__ void phys_flux(const PhysParams& pp, const T* w, int 
 
 template <class T>
 __device__ __forceinline__ T euler_speed(const PhysParams& pp, const EulerPrim<T>& q, int d) {
-  return jabs(d == 0 ? q.u : q.v) + jsqrt(pp.gamma * q.p * q.rinv);
+  return jabs(d == 0 ? q.u : q.v) + pp.ieps * jsqrt(pp.gamma * q.p * q.rinv);   // |v.n| + c / eps
 }
 
 // canonical LLF flux across a face with normal +e_d
@@ -83,7 +87,14 @@ __device__ __forceinline__ void llf_flux(const PhysParams& pp, const T* wL, cons
     lam = pp.glf ? jconst<T>(1.0) : jmax(euler_speed(pp, qL, d), euler_speed(pp, qR, d));
   }
 #pragma unroll
-  for (int v = 0; v < NV; ++v) f[v] = 0.5 * (FL[v] + FR[v]) + 0.5 * lam * (wL[v] - wR[v]);
+  for (int v = 0; v < NV; ++v) {
+    if (EQ != 0 && pp.glf) {       // constant Lambda = diag(1/eps, 1, 1, 1/eps)
+      const double lv = (v == 0 || v == NV - 1) ? pp.ieps : 1.0;
+      f[v] = 0.5 * (FL[v] + FR[v]) + (0.5 * lv) * (wL[v] - wR[v]);
+    } else {
+      f[v] = 0.5 * (FL[v] + FR[v]) + 0.5 * lam * (wL[v] - wR[v]);
+    }
+  }
 }
 
 // ---- Navier-Stokes ----------------------------------------------------------------

@@ -435,3 +435,41 @@ def test_glf_euler_end_of_run():
     for _ in range(cfg.steps):
         ctx.step(dt, Wg)
     assert rel(to_np(Wg), Wo) <= 1e-8
+
+
+@pytest.mark.parametrize("flux", ["llf", "glf"])
+@pytest.mark.parametrize("mach", [0.1, 0.01])
+def test_reference_mach_operators(flux, mach):
+    """eq:Euler with a reference Mach number eps < 1 (the paper's
+    fig:Euler_eps setups): R1, R2, residual and EXACT JVP vs the oracle <= 1e-11."""
+    d, ctx = _pair("euler", 3, 5, 4, (0.0, 1.0, 0.0, 1.0), flux=flux, mach=mach)
+    W = euler_ic(d, SEED + 51)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 52))
+    assert rel(to_np(ctx.rhs(to_gpu(W))), dgsem.rhs1(d, W)) <= 1e-11
+    assert rel(to_np(ctx.rhs(to_gpu(W), to_gpu(sig))), dgsem.rhs2(d, W, sig)) <= 1e-11
+    b = W * (1 + 1e-3 * inputs.random_field(d.n, SEED + 53))
+    a1, a2, dt = 0.5, 1 / 6, 0.002
+    G1o, G2o = implicit.residual(d, a1, a2, dt, b, W, sig)
+    G1g, G2g = ctx.residual(a1, a2, dt, to_gpu(b), to_gpu(W), to_gpu(sig))
+    assert rel(np.concatenate([to_np(G1g), to_np(G2g)]), np.concatenate([G1o, G2o])) <= 1e-11
+    dW = inputs.random_field(d.n, SEED + 54, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 55, unit_norm=True)
+    to, bo = implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds)
+    tg, bg = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(dW), to_gpu(ds), mode="exact")
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11
+
+
+def test_reference_mach_end_of_run():
+    """eps = 0.1 with the paper's flux and BJ_ext: 4x4 elements, N = 3, HBPC(4,0),
+    2 steps of an acoustic-CFL-1 step, FD JVP (eps_FD with the Mach number):
+    end of run vs the oracle <= 1e-8."""
+    mach = 0.1
+    d, ctx = make_pair("euler", 3, 4, 4, q=4, kmax=0, gmres_rtol=1e-10, newton_rtol=1e-10, flux="glf", mach=mach)
+    W0 = euler_ic(d, SEED + 56, rel_noise=1e-3)
+    h = 1.0 / 4
+    dt = 1.0 * h / 7 ** 2 * mach        # ~acoustic CFL for c/eps ~ 10 c
+    Wo, _ = _run_oracle(d, 4, 0, W0, dt, 2, rtol=1e-10, gmres_rtol=1e-10)
+    Wg = to_gpu(W0)
+    for _ in range(2):
+        ctx.step(dt, Wg)
+    assert rel(to_np(Wg), Wo) <= 1e-8
