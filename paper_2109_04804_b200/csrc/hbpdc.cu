@@ -383,7 +383,7 @@ hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const doubl
       A.d_epsw = c->deps;
     }
   }
-  ProfScope ps(c, 1, (k == OP_JVP_LINEAR ? 4.0 : 6.0) * n * 8.0);
+  ProfScope ps(c, 1, ((k == OP_JVP_LINEAR ? 4.0 : 6.0) + (shift_src ? 2.0 : 0.0)) * n * 8.0);
   CKS(run_op(c, k, A, ws_ghosts ? 12 : -1));
   if (c->st) c->st->jvp_calls++;
   return HBPDC_OK;
