@@ -1485,7 +1485,6 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->equation != HBPDC_ADVECTION && pb->dim != 2) return bad("Euler/NS need dim = 2");
   if (pb->N < 1 || pb->N > 7) return bad("N must be in 1..7");
   if (pb->nodes != HBPDC_GLL) return bad("only Gauss-Lobatto nodes are implemented on the GPU (reading R1)");
-  if (pb->flux != HBPDC_LLF) return bad("only the LLF flux is implemented (reading R3)");
   if (!(pb->mach_eps > 0.0)) return bad("mach_eps must be positive");
   if (pb->equation == HBPDC_NAVIER_STOKES && pb->mach_eps != 1.0)
     return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");
