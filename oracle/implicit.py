@@ -342,10 +342,11 @@ def gmres(matvec, rhs, precond=None, rtol=1e-6, restart=50, max_total=7000):
 class NewtonOpts:
     def __init__(self, rtol=1e-10, atol_dw=1e-12, max_newton=50, gmres_rtol=1e-6,
                  restart=700, max_krylov=7000, precond="bjext",
-                 precond_policy="per_step_per_alpha", jvp_mode="auto"):
+                 precond_policy="per_step_per_alpha", jvp_mode="auto", schur=False):
         self.rtol, self.atol_dw, self.max_newton = rtol, atol_dw, max_newton
         self.gmres_rtol, self.restart, self.max_krylov = gmres_rtol, restart, max_krylov
         self.precond, self.precond_policy, self.jvp_mode = precond, precond_policy, jvp_mode
+        self.schur = schur           # solve the Schur complement system instead of eq:Newton
 
 
 class NewtonFailure(RuntimeError):
@@ -381,16 +382,32 @@ def newton_solve(disc, a1, a2, dt, b, W_guess, opts: NewtonOpts, pc=None, stats=
             if stats is not None:
                 stats["precond_builds"] += 1
         Wc, sc = W.copy(), sig.copy()
+        if opts.schur:
+            # Schur complement: J_S dw = -G1 + c2 dR2/dsigma G2, dsigma = -G2 + dR1/dW dw,
+            # J_S = I - a1 dt K + c2 dR2/dW + c2 K^2 (eq:nonlinear_eqsys_Schur) applied matrix-free as
+            # the top block of J (v, K v); K v = dR1/dW v = R2(W, v) exactly (R2 linear in sigma)
+            c2 = a2 * dt * dt / 2.0
+            Kv = lambda v: rhs2(disc, Wc, v)
 
-        def matvec(v):
-            t, bt = jvp(disc, mode, a1, a2, dt, Wc, sc, v[:n], v[n:])
-            return np.concatenate([t, bt])
+            def matvec_s(v):
+                return jvp(disc, mode, a1, a2, dt, Wc, sc, v, Kv(v))[0]
 
-        precond = None
-        if pc is not None:
-            precond = lambda v: np.concatenate(pc.apply(v[:n], v[n:]))
-        dX, its, ok = gmres(matvec, -np.concatenate([G1, G2]), precond,
-                            opts.gmres_rtol, opts.restart, opts.max_krylov)
+            precond_s = None
+            if pc is not None:       # element-block Jacobi of J_S: the D block of BJ_ext / BJ^H_ext (reading R32)
+                precond_s = lambda v: (pc.S @ v.reshape(-1, disc.m, 1)).reshape(-1)
+            dw, its, ok = gmres(matvec_s, -G1 + c2 * Kv(G2), precond_s,
+                                opts.gmres_rtol, opts.restart, opts.max_krylov)
+            dX = np.concatenate([dw, -G2 + Kv(dw)])
+        else:
+            def matvec(v):
+                t, bt = jvp(disc, mode, a1, a2, dt, Wc, sc, v[:n], v[n:])
+                return np.concatenate([t, bt])
+
+            precond = None
+            if pc is not None:
+                precond = lambda v: np.concatenate(pc.apply(v[:n], v[n:]))
+            dX, its, ok = gmres(matvec, -np.concatenate([G1, G2]), precond,
+                                opts.gmres_rtol, opts.restart, opts.max_krylov)
         if stats is not None:
             stats["gmres_its"] += its
             stats["newton_its"] += 1

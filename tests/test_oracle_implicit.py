@@ -319,3 +319,42 @@ def test_newton_euler_quadratic():
     assert stats["newton_its"] <= 4
     # sigma-consistency
     assert np.linalg.norm(sig - dgsem.rhs1(d, W)) <= 1e-10 * np.linalg.norm(sig)
+
+
+def test_schur_operator_is_the_schur_complement():
+    """eq:nonlinear_eqsys_Schur: J = [[A, B], [C, I]] with B = c2 K, C = -K, so the
+    Schur complement A - B C = I - a1 dt K + c2 dR2/dW + c2 K^2 is applied by the
+    top block of J (v, K v) (EXACT products, K v = R2(W, v)); checked against the
+    blocks of the brute-force assembled Jacobian of G (3x3 Euler, N = 2)."""
+    d = make("euler", 2, 3, 3)
+    n = d.n
+    W = euler_state(d, 40)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * np.random.default_rng(41).standard_normal(n))
+    a1, a2, dt = 0.5, 1 / 6, 0.05
+    b = W.copy()
+    J = assembled_jacobian(d, a1, a2, dt, b, W, sig)
+    A, B, C = J[:n, :n], J[:n, n:], J[n:, :n]
+    np.testing.assert_allclose(J[n:, n:], np.eye(n), atol=1e-6)
+    JS = A - B @ C
+    v = np.random.default_rng(42).standard_normal(n)
+    Kv = dgsem.rhs2(d, W, v)
+    top, _ = implicit.jvp_exact(d, a1, a2, dt, W, sig, v, Kv)
+    np.testing.assert_allclose(top, JS @ v, rtol=1e-6, atol=1e-6 * np.abs(top).max())
+
+
+@pytest.mark.parametrize("precond", ["bjext_h", "none"])
+def test_newton_schur_equals_extended(precond):
+    """The Schur-complement Newton iteration solves the same stage
+    equation: same W and sigma as the extended system to the Newton tolerance."""
+    d = make("euler", 2, 3, 3)
+    W0 = euler_state(d, 43)
+    dt = 0.02
+    b = W0 + 0.5 * dt * dgsem.rhs1(d, W0)
+    out = []
+    for schur in (False, True):
+        opts = implicit.NewtonOpts(rtol=1e-10, gmres_rtol=1e-10, precond=precond, precond_policy="per_newton",
+                                   schur=schur)
+        W, sig = implicit.newton_solve(d, 0.5, 1 / 6, dt, b, W0, opts)
+        out.append((W, sig))
+    assert np.abs(out[0][0] - out[1][0]).max() < 1e-9
+    assert np.abs(out[0][1] - out[1][1]).max() < 1e-8 * np.abs(out[0][1]).max()
