@@ -67,7 +67,8 @@ typedef struct {
   int equation;         /* HBPDC_ADVECTION | HBPDC_EULER | HBPDC_NAVIER_STOKES     */
   double a[2];          /* advection velocity (advection only)                     */
   double gamma;         /* isentropic coefficient, e.g. 1.4                */
-  double mach_eps;      /* reference Mach number eps; must be 1 (reading R18)      */
+  double mach_eps;      /* reference Mach number eps of eq:Euler (configs: 1, R18;
+                           Navier-Stokes: must be 1)                               */
   double mu;            /* dynamic viscosity (NS)                           */
   double prandtl;       /* Prandtl number (NS), e.g. 0.72                   */
   int N;                /* polynomial degree, 1..7                                 */
@@ -102,6 +103,12 @@ typedef struct {
                                   s-step blocks (s Newton-basis powers, then block CGS2
                                   + CholQR2: 4 passes over the basis per s iterations).
                                   Same Krylov space and GMRES iterates, other rounding. */
+  int schur;                   /* 0: Newton on the extended system (eq:Newton);
+                                  1: Schur complement: GMRES on
+                                  J_S dw = -G1 + c2 K G2 (J_S = I - a1 dt K + c2 dR2/dW
+                                  + c2 K^2, applied as the top block of J (v, K v)),
+                                  dsigma = -G2 + K dw; preconditioned by the D block of
+                                  BJ_ext / BJ^H_ext (element-block Jacobi, reading R32). */
 } hbpdc_solver_opts;
 
 /* Element partition (the mesh is decomposed, W and sigma share the

@@ -75,6 +75,7 @@ struct SysWS {
   double *X = nullptr, *G = nullptr, *dX = nullptr, *rhs = nullptr, *r = nullptr, *zb = nullptr;
   double *b = nullptr;                      // Newton right-hand side b (n)
   double *U = nullptr, *V = nullptr;        // BJ_ext GEMV outputs (n each)
+  double *ks = nullptr, *ks2 = nullptr;     // Schur mode: K v and a discarded JVP half (n each)
   double* npart = nullptr;                  // K-apply per-CTA partials of ||out1||^2 ...
   const double* npart_of = nullptr;         // ... valid for this vector (the next FD JVP's dW)
   double *Vk = nullptr;                     // Krylov basis: vk_cap x 2n, grown on demand up to restart+1
@@ -389,6 +390,13 @@ hbpdc_status jvp_impl(hbpdc_ctx* c, double a1, double a2, double dt, const doubl
   return HBPDC_OK;
 }
 
+// K v = dR1/dW v at W, exactly: R2(W, v) (R2 is linear in sigma)
+hbpdc_status k_apply_global(hbpdc_ctx* c, const double* W, const double* v, double* out) {
+  OpArgs A = base_args(c);
+  A.W = W; A.S = v; A.out1 = nullptr; A.out2 = out;
+  return run_op(c, OP_R12, A);
+}
+
 // ---- BJ_ext ----------------------------------------------------------------------
 hbpdc_status ensure_precond_mem(hbpdc_ctx* c) {
   if (c->S) return HBPDC_OK;
@@ -523,6 +531,24 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
 hbpdc_status precond_apply_multi(hbpdc_ctx* c, int B, const double* const* iw, const double* const* is,
                                  double* const* ow, double* const* os) {
   if (!c->pc_valid) return fail(c, HBPDC_E_ARG, "precond_apply before precond_build");
+  if (c->op.schur) {
+    // element-block Jacobi of J_S (reading R32): the D block S (or S^H) on the W half, sigma half 0
+    ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 2.0 * B * c->n * 8.0);
+    if (c->s_shared) {
+      for (int i = 0; i < B; ++i)
+        CK(launch_block_gemv2(c->S, 1, iw[i], iw[i], ow[i], c->sys[i].V, c->m, c->nE, c->stream));
+    } else {
+      const double* in[GEMV_MAX_RHS];
+      double* out[GEMV_MAX_RHS];
+      for (int i = 0; i < B; ++i) { in[i] = iw[i]; out[i] = ow[i]; }
+      CK(launch_block_gemv_multi(c->S, B, in, out, c->m, c->nE, c->stream));
+    }
+    for (int i = 0; i < B; ++i) {
+      CK(cudaMemsetAsync(os[i], 0, c->n * sizeof(double), c->stream));
+      if (c->st) c->st->precond_applies++;
+    }
+    return HBPDC_OK;
+  }
   if (c->op.precond != HBPDC_PC_BJEXT_H) {
     ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 4.0 * B * c->n * 8.0);
     if (B == 1 || c->s_shared) {
@@ -661,6 +687,23 @@ struct GState {
   bool needs_op() const { return in_cycle && !flush_next && j != 0; }
 };
 
+// the Newton system's operator on a GMRES vector (2n): J z, or in Schur mode
+// (J_S z_W, 0) with J_S z = top block of J (z, K z), K z = R2(W, z)
+hbpdc_status sys_matvec(hbpdc_ctx* c, GState& g, const double* z, double* out, const double* shift_src = nullptr,
+                        double shift = 0.0, const double* dw_part = nullptr) {
+  const size_t n = c->n;
+  if (!c->op.schur)
+    return jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr,
+                    true, shift_src, shift, dw_part);
+  SysWS& w = *g.w;
+  CKS(k_apply_global(c, g.L.W, z, w.ks));
+  // ws_ghosts = false: k_apply_global's exchange reused the sigma ghost buffer (partitioned runs)
+  CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, w.ks, out, w.ks2, c->op.jvp_mode, nullptr, false,
+               shift_src, shift, nullptr));
+  CK(cudaMemsetAsync(out + n, 0, n * sizeof(double), c->stream));
+  return HBPDC_OK;
+}
+
 hbpdc_status g_start(hbpdc_ctx* c, GState& g) {
   SysWS& w = *g.w;
   const size_t n2 = 2 * c->n;
@@ -728,8 +771,7 @@ hbpdc_status g_cycle_end(hbpdc_ctx* c, GState& g) {
   if (g.est_ok) { g.converged = g.done = true; return HBPDC_OK; }
   // true residual r = rhs - J x
   use_ghosts(c, w);
-  CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, w.dX, w.dX + n, w.r, w.r + n, c->op.jvp_mode, nullptr,
-               true));
+  CKS(sys_matvec(c, g, w.dX, w.r));
   CK(launch_axpby(1.0, w.rhs, -1.0, w.r, n2, c->stream));
   CKS(norm_host(c, w.r, n2, &g.beta));
   return HBPDC_OK;
@@ -753,8 +795,7 @@ hbpdc_status g_iter(hbpdc_ctx* c, GState& g, const double* z) {
   double* wv = w.Vk + (size_t)j * n2;
   if (!flush) {
     use_ghosts(c, w);
-    CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, wv, wv + n, c->op.jvp_mode, nullptr, true,
-                 nullptr, 0.0, take_npart(c, z)));
+    CKS(sys_matvec(c, g, z, wv, nullptr, 0.0, take_npart(c, z)));
     ++g.total;
   }
   const int nk = j - 1;
@@ -1119,8 +1160,7 @@ hbpdc_status g_power(hbpdc_ctx* c, GState& g, const double* z) {
   double* prev = w.Vk + (size_t)(g.j - 1) * n2;
   double* out = w.Vk + (size_t)g.j * n2;
   use_ghosts(c, w);
-  CKS(jvp_impl(c, g.L.a1, g.L.a2, g.L.dt, g.L.W, g.L.sg, z, z + n, out, out + n, c->op.jvp_mode, nullptr, true,
-               prev, g.theta, take_npart(c, z)));
+  CKS(sys_matvec(c, g, z, out, prev, g.theta, take_npart(c, z)));
   ++g.total;
   ++g.pi;
   ++g.j;
@@ -1246,7 +1286,14 @@ hbpdc_status newton_batch(hbpdc_ctx* c, int B, double a1, double a2, double dt, 
     for (int i = 0; i < B; ++i) {
       if (!active[i]) continue;
       SysWS& w = c->sys[i];
-      CK(launch_axpby(-1.0, w.G, 0.0, w.rhs, n2, c->stream));       // rhs = -G
+      if (c->op.schur) {
+        // Schur complement: rhs = (-G1 + c2 K G2, 0)
+        CKS(k_apply_global(c, w.X, w.G + n, w.ks));
+        CK(launch_waxpby(-1.0, w.G, a2 * dt * dt / 2.0, w.ks, w.rhs, n, c->stream));
+        CK(cudaMemsetAsync(w.rhs + n, 0, n * sizeof(double), c->stream));
+      } else {
+        CK(launch_axpby(-1.0, w.G, 0.0, w.rhs, n2, c->stream));       // rhs = -G
+      }
       gs[nb].w = &w;
       gs[nb].L = LinSys{a1, a2, dt, w.X, w.X + n, pc};
       gs[nb].sstep = c->sstep;
@@ -1257,6 +1304,10 @@ hbpdc_status newton_batch(hbpdc_ctx* c, int B, double a1, double a2, double dt, 
       for (int q = 0; q < nb; ++q) fprintf(stderr, "[hbpdc] gmres sys %d its %d\n", idx[q], gs[q].total);
     for (int q = 0; q < nb; ++q) {
       SysWS& w = c->sys[idx[q]];
+      if (c->op.schur) {                                              // dsigma = -G2 + K dw
+        CKS(k_apply_global(c, w.X, w.dX, w.ks));
+        CK(launch_waxpby(-1.0, w.G + n, 1.0, w.ks, w.dX + n, n, c->stream));
+      }
       CK(launch_axpby(1.0, w.dX, 1.0, w.X, n2, c->stream));         // X += dX
       if (c->st) c->st->newton_its++;
       double dwn;
@@ -1396,6 +1447,10 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     CKS(dalloc(c, &w.r, n2));
     CKS(dalloc(c, &w.zb, n2));
     CKS(dalloc(c, &w.b, n));
+    if (c->op.schur) {
+      CKS(dalloc(c, &w.ks, n));
+      CKS(dalloc(c, &w.ks2, n));
+    }
     CKS(ensure_krylov(c, w, std::min<size_t>((size_t)R + 1, 33)));
     // reduction rows: DCGS2 2j + 3, s-step (j + 1) s + s^2
     const size_t rows = std::max<size_t>(2 * (size_t)R + 4, ((size_t)R + 1) * c->sstep + (size_t)c->sstep * c->sstep);

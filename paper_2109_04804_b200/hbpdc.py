@@ -51,7 +51,7 @@ class SolverOpts(ctypes.Structure):
                 ("gmres_rtol", ctypes.c_double), ("gmres_restart", ctypes.c_int),
                 ("krylov_max_per_newton", ctypes.c_int), ("precond", ctypes.c_int),
                 ("precond_policy", ctypes.c_int), ("jvp_mode", ctypes.c_int), ("batch_stages", ctypes.c_int),
-                ("gmres_sstep", ctypes.c_int)]
+                ("gmres_sstep", ctypes.c_int), ("schur", ctypes.c_int)]
 
 
 class Dist(ctypes.Structure):
@@ -184,7 +184,7 @@ class Context:
                  newton_atol_dw=1e-12, newton_floor=64.0, newton_max=50, gmres_rtol=1e-6,
                  restart=700, max_krylov=7000, precond="bjext", precond_policy="per_step_per_alpha",
                  jvp_mode="auto", batch_stages=True, gmres_sstep=1, rank=0, nranks=1, px=1, py=1, nccl_id=None, stream=None, device=0,
-                 comm="auto", loopback=None, force_halo=False, flux="llf", mach=1.0):
+                 comm="auto", loopback=None, force_halo=False, flux="llf", mach=1.0, schur=False):
         import torch
         self.lib = load()
         if not torch.cuda.is_available():
@@ -198,7 +198,7 @@ class Context:
                         krylov_max_per_newton=max_krylov, precond=_PC[precond],
                         precond_policy=0 if precond_policy == "per_step_per_alpha" else 1,
                         jvp_mode=_JVP[jvp_mode], batch_stages=int(batch_stages),
-                        gmres_sstep=int(gmres_sstep))
+                        gmres_sstep=int(gmres_sstep), schur=int(schur))
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream

@@ -42,9 +42,11 @@ def initial(kind, X, Y, mach=1.0):
 
 
 def gmres_iterations(kind, precond, dt, N=5, ne=16, mach=1.0, flux="llf"):
+    schur = precond.startswith("schur")
+    pc = {"schur_bj": "bjext_h", "schur": "none"}.get(precond, precond)
     ctx = hbpdc.Context(dim=2, equation=kind, N=N, nx=ne, ny=ne, bounds=(-1.0, 1.0, -1.0, 1.0),
                         a=(0.3, 0.3), q=4, kmax=0, newton_rtol=1e-8, gmres_rtol=1e-3, restart=700,
-                        max_krylov=7000, precond=precond, mach=mach, flux=flux)
+                        max_krylov=7000, precond=pc, mach=mach, flux=flux, schur=schur)
     X, Y = ctx.node_coords()
     W = torch.tensor(inputs.layout(initial(kind, X, Y, mach), 2), dtype=torch.float64, device="cuda")
     try:
@@ -73,9 +75,10 @@ def main():
     for kind, mach, flux in cases:
         title = kind if kind == "advection" else f"euler, reference Mach eps = {mach}, flux {flux.upper()}"
         print(f"## {title}\n")
-        print("| dt | " + " | ".join(("BJ_ext", "BJ^H_ext", "none")) + " |")
-        print("|---|---|---|---|")
-        res = {pc: [] for pc in ("bjext", "bjext_h", "none")}
+        names = ("BJ_ext", "BJ^H_ext", "none", "Schur + BJ", "Schur, none")
+        print("| dt | " + " | ".join(names) + " |")
+        print("|---" * (len(names) + 1) + "|")
+        res = {pc: [] for pc in ("bjext", "bjext_h", "none", "schur_bj", "schur")}
         for dt in dts:
             row = []
             for pc in res:

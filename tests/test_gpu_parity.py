@@ -473,3 +473,29 @@ def test_reference_mach_end_of_run():
     for _ in range(2):
         ctx.step(dt, Wg)
     assert rel(to_np(Wg), Wo) <= 1e-8
+
+
+# ---- NEXT-2: the Schur-complement formulation --------------------------
+
+@pytest.mark.parametrize("precond,sstep", [("bjext_h", 1), ("bjext_h", 8), ("none", 1)])
+def test_schur_end_of_run(precond, sstep):
+    """Newton on the Schur complement J_S dw = -G1 + c2 K G2, dsigma = -G2 + K dw
+    (J_S applied as the top block of J (v, K v)), element-block Jacobi from the
+    BJ^H_ext D block (reading R32) or unpreconditioned: C3 physics at 4x4
+    elements, N = 3, HBPC(6,2), 2 steps, end of run vs the oracle <= 1e-8."""
+    q, kmax = 6, 2
+    cfg = configs.scaled(configs.CONFIGS["C3"], N=3, nx=4, ny=4, steps=2, q=q, kmax=kmax)
+    cfl_scale = 1.0 if precond != "none" else 0.25
+    d, ctx = make_pair("euler", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=q, kmax=kmax,
+                       gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, precond=precond,
+                       schur=True, gmres_sstep=sstep)
+    W0 = inputs.initial_state("C3", d.node_coords(), noise=cfg.noise)
+    dt = cfl_scale * configs.cfl_dt(cfg, inputs.initial_state("C3", d.node_coords()))
+    Wo, sto = _run_oracle(d, q, kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol,
+                          precond=precond, schur=True)
+    Wg = to_gpu(W0)
+    its = 0
+    for _ in range(cfg.steps):
+        its += ctx.step(dt, Wg)["gmres_its"]
+    assert rel(to_np(Wg), Wo) <= 1e-8
+    assert its <= 1.25 * sto["gmres_its"] + 2 * sstep + 8, (its, sto["gmres_its"])
