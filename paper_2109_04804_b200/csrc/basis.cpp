@@ -1,6 +1,8 @@
-// basis.cpp -- Gauss-Lobatto nodes, weights and the weak-form derivative matrix
-// Dhat = -M^-1 D^T M (reading R2: the transposed weight ratio of
-// SPEC S:35, which preserves free streams), computed in long double.
+// basis.cpp -- Gauss-Lobatto (configs) and Gauss-Legendre (NEXT-3) nodes,
+// weights and the weak-form derivative matrix Dhat = -M^-1 D^T M (
+// reading R2: the transposed weight ratio of SPEC S:35, which preserves free
+// streams), the edge values l_i(+-1) and lhat_i(+-1) = l_i(+-1) / w_i,
+// computed in long double.
 #include <cmath>
 #include <vector>
 
@@ -23,9 +25,78 @@ static void legendre(int N, long double x, long double& p, long double& dp, long
 
 struct Basis1D {
   int N;
+  int gl;                             // 0: Gauss-Lobatto, 1: Gauss-Legendre
   std::vector<double> xi, w, Dhat;   // Dhat row-major (N+1)^2
-  double lhp, lhm;                    // lhat_N(+1) = 1/w_N, lhat_0(-1) = 1/w_0
+  double lhp, lhm;                    // GLL: lhat_N(+1) = 1/w_N, lhat_0(-1) = 1/w_0
+  std::vector<double> lp, lm;         // l_i(+1), l_i(-1)
+  std::vector<double> lhpv, lhmv;     // lhat_i(+1), lhat_i(-1)
 };
+
+// barycentric weights, D_ij = l_j'(x_i), edge values and Dhat of a node set
+static void finish_basis(Basis1D& b, const std::vector<long double>& x, const std::vector<long double>& w) {
+  const int n = (int)x.size(), N = n - 1;
+  std::vector<long double> lam(n, 1.0L), D(n * n, 0.0L), lp(n), lm(n);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k)
+      if (k != j) lam[j] /= (x[j] - x[k]);
+  for (int i = 0; i < n; ++i) {
+    long double s = 0.0L;
+    for (int j = 0; j < n; ++j)
+      if (i != j) { D[i * n + j] = (lam[j] / lam[i]) / (x[i] - x[j]); s += D[i * n + j]; }
+    D[i * n + i] = -s;
+  }
+  for (int j = 0; j < n; ++j) {                       // l_j(+-1) = prod_{k != j} (+-1 - x_k) / (x_j - x_k)
+    long double a = 1.0L, c = 1.0L;
+    for (int k = 0; k < n; ++k)
+      if (k != j) { a *= (1.0L - x[k]) / (x[j] - x[k]); c *= (-1.0L - x[k]) / (x[j] - x[k]); }
+    lp[j] = a; lm[j] = c;
+  }
+  b.N = N;
+  b.xi.resize(n); b.w.resize(n); b.Dhat.resize(n * n);
+  b.lp.resize(n); b.lm.resize(n); b.lhpv.resize(n); b.lhmv.resize(n);
+  for (int i = 0; i < n; ++i) {
+    b.xi[i] = (double)x[i]; b.w[i] = (double)w[i];
+    b.lp[i] = (double)lp[i]; b.lm[i] = (double)lm[i];
+    b.lhpv[i] = (double)(lp[i] / w[i]); b.lhmv[i] = (double)(lm[i] / w[i]);
+  }
+  b.lhp = (double)(1.0L / w[N]);
+  b.lhm = (double)(1.0L / w[0]);
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < n; ++j) b.Dhat[i * n + j] = (double)(-(w[j] / w[i]) * D[j * n + i]);
+    // enforce the free-stream row identity  sum_l Dhat_il = -lhat_i(1) + lhat_i(-1)
+    long double target = -(long double)b.lhpv[i] + (long double)b.lhmv[i];
+    long double off = 0.0L;
+    for (int j = 0; j < n; ++j) if (j != i) off += b.Dhat[i * n + j];
+    b.Dhat[i * n + i] = (double)(target - off);
+  }
+}
+
+// Gauss-Legendre: roots of P_{N+1}, w_i = 2 / ((1 - x_i^2) P_{N+1}'(x_i)^2)
+Basis1D gl_basis(int N) {
+  const int n = N + 1;
+  const long double PI = 3.141592653589793238462643383279502884L;
+  std::vector<long double> x(n), w(n);
+  for (int k = 0; k < n; ++k) {
+    long double t = -cosl(PI * (k + 0.75L) / (n + 0.5L));
+    for (int it = 0; it < 100; ++it) {
+      long double p, dp, ddp;
+      legendre(n, t, p, dp, ddp);
+      long double dt = p / dp;
+      t -= dt;
+      if (fabsl(dt) < 1e-19L) break;
+    }
+    x[k] = t;
+  }
+  for (int i = 0; i < n; ++i) {
+    long double p, dp, ddp;
+    legendre(n, x[i], p, dp, ddp);
+    w[i] = 2.0L / ((1.0L - x[i] * x[i]) * dp * dp);
+  }
+  Basis1D b;
+  b.gl = 1;
+  finish_basis(b, x, w);
+  return b;
+}
 
 Basis1D gll_basis(int N) {
   const int n = N + 1;
@@ -48,31 +119,9 @@ Basis1D gll_basis(int N) {
     legendre(N, x[i], p, dp, ddp);
     w[i] = 2.0L / (N * (N + 1) * p * p);
   }
-  // barycentric weights and D_ij = l_j'(x_i)
-  std::vector<long double> lam(n, 1.0L), D(n * n, 0.0L);
-  for (int j = 0; j < n; ++j)
-    for (int k = 0; k < n; ++k)
-      if (k != j) lam[j] /= (x[j] - x[k]);
-  for (int i = 0; i < n; ++i) {
-    long double s = 0.0L;
-    for (int j = 0; j < n; ++j)
-      if (i != j) { D[i * n + j] = (lam[j] / lam[i]) / (x[i] - x[j]); s += D[i * n + j]; }
-    D[i * n + i] = -s;
-  }
   Basis1D b;
-  b.N = N;
-  b.xi.resize(n); b.w.resize(n); b.Dhat.resize(n * n);
-  for (int i = 0; i < n; ++i) { b.xi[i] = (double)x[i]; b.w[i] = (double)w[i]; }
-  b.lhp = (double)(1.0L / w[N]);
-  b.lhm = (double)(1.0L / w[0]);
-  for (int i = 0; i < n; ++i) {
-    for (int j = 0; j < n; ++j) b.Dhat[i * n + j] = (double)(-(w[j] / w[i]) * D[j * n + i]);
-    // enforce the free-stream row identity  sum_l Dhat_il = -lhat_i(1) + lhat_i(-1)
-    long double target = (i == N ? -(long double)b.lhp : 0.0L) + (i == 0 ? (long double)b.lhm : 0.0L);
-    long double off = 0.0L;
-    for (int j = 0; j < n; ++j) if (j != i) off += b.Dhat[i * n + j];
-    b.Dhat[i * n + i] = (double)(target - off);
-  }
+  b.gl = 0;
+  finish_basis(b, x, w);
   return b;
 }
 

@@ -17,10 +17,14 @@
 namespace hbpdc {
 struct Basis1D {
   int N;
+  int gl;
   std::vector<double> xi, w, Dhat;
   double lhp, lhm;
+  std::vector<double> lp, lm;
+  std::vector<double> lhpv, lhmv;
 };
 Basis1D gll_basis(int N);
+Basis1D gl_basis(int N);
 }  // namespace hbpdc
 
 namespace {
@@ -1539,7 +1543,11 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->equation < 0 || pb->equation > 2) return bad("unknown equation");
   if (pb->equation != HBPDC_ADVECTION && pb->dim != 2) return bad("Euler/NS need dim = 2");
   if (pb->N < 1 || pb->N > 7) return bad("N must be in 1..7");
-  if (pb->nodes != HBPDC_GLL) return bad("only Gauss-Lobatto nodes are implemented on the GPU (reading R1)");
+  if (pb->nodes != HBPDC_GLL && pb->nodes != HBPDC_GL) return bad("nodes must be HBPDC_GLL or HBPDC_GL");
+  if (pb->nodes == HBPDC_GL && pb->equation == HBPDC_NAVIER_STOKES)
+    return bad("Gauss-Legendre nodes: advection and Euler only (Navier-Stokes: GLL)");
+  if (pb->nodes == HBPDC_GL && (c->ds.nranks > 1 || c->ds.force_halo))
+    return bad("Gauss-Legendre nodes: single partition only (the halo carries GLL edge nodes)");
   if (!(pb->mach_eps > 0.0)) return bad("mach_eps must be positive");
   if (pb->equation == HBPDC_NAVIER_STOKES && pb->mach_eps != 1.0)
     return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");
@@ -1584,7 +1592,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (c->sstep != 1 && c->sstep != 2 && c->sstep != 4 && c->sstep != 8) return bad("gmres_sstep must be 1, 2, 4 or 8");
   if (c->sstep > c->restart) c->sstep = 1;
   c->tab = tableau(pb->q);
-  c->basis = hbpdc::gll_basis(pb->N);
+  c->basis = pb->nodes == HBPDC_GL ? hbpdc::gl_basis(pb->N) : hbpdc::gll_basis(pb->N);
   // geometry: Cartesian, J = dx dy / 4, s-hat = dy/2, dx/2 -> scale 2/dx, 2/dy
   const double dx = (pb->xmax - pb->xmin) / pb->nx;
   const double dy = pb->dim == 2 ? (pb->ymax - pb->ymin) / pb->ny : 1.0;
@@ -1598,10 +1606,23 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->geo.lhp = c->basis.lhp;
   c->geo.lhm = c->basis.lhm;
   for (int i = 0; i < c->P * c->P; ++i) c->geo.Dh[i] = c->basis.Dhat[i];
+  c->geo.gl = c->basis.gl;
+  c->geo.P = c->P;
+  c->geo.dim = pb->dim;
+  for (int i = 0; i < c->P; ++i) {
+    c->geo.lp[i] = c->basis.lp[i];
+    c->geo.lm[i] = c->basis.lm[i];
+    c->geo.lhpv[i] = c->basis.lhpv[i];
+    c->geo.lhmv[i] = c->basis.lhmv[i];
+  }
   c->geo_abs = c->geo;
   for (int i = 0; i < c->P * c->P; ++i) c->geo_abs.Dh[i] = std::fabs(c->basis.Dhat[i]);
   c->geo_abs.lhm = -std::fabs(c->geo.lhm);
   c->geo_abs.lhp = std::fabs(c->geo.lhp);
+  for (int i = 0; i < c->P; ++i) {     // R1_abs: |lhat|, the - face added (traces keep l)
+    c->geo_abs.lhpv[i] = std::fabs(c->geo.lhpv[i]);
+    c->geo_abs.lhmv[i] = -std::fabs(c->geo.lhmv[i]);
+  }
   c->cfg.eq = pb->equation;
   c->cfg.dim = pb->dim;
   c->cfg.P = c->P;

@@ -73,7 +73,8 @@ struct OneJetMode {
   }
   // face work in two halves: part 0 = the canonical L side (-e_d), part 1 = R
   static constexpr int NFP = 2, FPD = half_doubles<EQ, J>();
-  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
+  template <class G>
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const G& g, int e, int own, int nb,
                                    int nnode, int slot, bool plus, int d, int part, double* raw,
                                    int rs) {
     const bool use_own = (part == 0) == plus;
@@ -82,7 +83,7 @@ struct OneJetMode {
       // its half flux in plain doubles, tangent slots zero (same values as the jet)
       if (!use_own) {
         NodeState<EQ, double> sd;
-        Derived::load_value(A, nb, nnode, sd.w);
+        trace_load(g, nnode, d, sd, [=](int nd, NodeState<EQ, double>& s) { Derived::load_value(A, nb, nd, s.w); });
         constexpr int NR = 2 * NV + 1, JN = JetN<J>::value;
         double tmp[NR];
         half_flux<EQ, double>(pp, sd, d, tmp, 1);
@@ -96,7 +97,9 @@ struct OneJetMode {
       }
     }
     State st;
-    load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
+    const int le = use_own ? e : nb;
+    trace_load(g, use_own ? own : nnode, d, st,
+               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); });
     half_flux<EQ, J>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args& A, const PhysParams& pp, int d, const double* rL,
@@ -319,14 +322,15 @@ template <int EQ, int NODES> struct ModeJvpFD {
   }
   // face work split by jet state: part 0 = p-state face flux (J1), part 1 = q-state (J2)
   static constexpr int NFP = 2, FPD = 3 * NV;
-  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo&, int e, int own, int nb,
+  template <class G>
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const G& g, int e, int own, int nb,
                                    int nnode, int, bool plus, int d, int part, double* raw,
                                    int rs) {
     if (part == 0) {
       if (!(fd_step(A) > 0.0)) return;
       NodeState<EQ, J1> so, sn;
-      load_w<0>(A, e, own, so.w, false);
-      load_w<0>(A, nb, nnode, sn.w, true);
+      trace_load(g, own, d, so, [=](int nd, NodeState<EQ, J1>& s) { load_w<0>(A, e, nd, s.w, false); });
+      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J1>& s) { load_w<0>(A, nb, nd, s.w, true); });
       ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, e, own, so);
       ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, nb, nnode, sn);
       J1 fp[NV];
@@ -335,8 +339,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
       for (int v = 0; v < NV; ++v) { raw[rs * (2 * v)] = fp[v].v; raw[rs * (2 * v + 1)] = fp[v].a; }
     } else {
       NodeState<EQ, J2> so, sn;
-      load_w<1>(A, e, own, so.w, false);
-      load_w<1>(A, nb, nnode, sn.w, true);
+      trace_load(g, own, d, so, [=](int nd, NodeState<EQ, J2>& s) { load_w<1>(A, e, nd, s.w, false); });
+      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J2>& s) { load_w<1>(A, nb, nd, s.w, true); });
       ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, e, own, so);
       ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, nb, nnode, sn);
       J2 fq[NV];
@@ -403,12 +407,13 @@ template <int EQ, int NODES> struct ModeJvpLinear {
   }
   // face work split by input: part 0 = F(-a1dt dW + c2 dsigma), part 1 = F(dW)
   static constexpr int NFP = 2, FPD = NV;
-  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
+  template <class G>
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const G& g, int e, int own, int nb,
                                    int nnode, int slot, bool plus, int d, int part, double* raw,
                                    int rs) {
     State so, sn;
-    load(A, g, e, slot, own, so, false);
-    load(A, g, nb, slot, nnode, sn, true);
+    trace_load(g, own, d, so, [=](int nd, State& s) { load(A, g, e, slot, nd, s, false); });
+    trace_load(g, nnode, d, sn, [=](int nd, State& s) { load(A, g, nb, slot, nd, s, true); });
     const NodeState<EQ, double>& o = part == 0 ? so.u0 : so.u1;
     const NodeState<EQ, double>& q = part == 0 ? sn.u0 : sn.u1;
     double f[NV];

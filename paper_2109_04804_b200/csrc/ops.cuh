@@ -31,7 +31,50 @@ struct Geo {
   double sx, sy;           // 2/dx, 2/dy
   double lhp, lhm;         // lhat_N(+1) = 1/w_N, lhat_0(-1) = 1/w_0  (GLL)
   double Dh[64];           // Dhat (P x P, row-major)
+  int gl, P, dim;          // gl: Gauss-Legendre nodes (no node on the element edge)
+  double lp[8], lm[8];     // GL: l_i(+1), l_i(-1)  (traces)
+  double lhpv[8], lhmv[8]; // GL: lhat_i(+1), lhat_i(-1)  (surface terms, eq:DGSEM_wt)
 };
+
+// Node set selected at compile time (the GL kernels are a separate instantiation,
+// ops_kernels_gl.cu, so the GLL hot path is compiled exactly as without GL).
+template <bool GL_> struct GeoSel : Geo {
+  static constexpr bool GL = GL_;
+};
+
+// Face trace of a node state.  GLL: the edge node n itself.  GL: the
+// line sum  sum_l l_l(+-1) S(line node l)  through n in direction d (the side
+// is the edge n sits on), accumulated component-wise (a jet is linear in its
+// components).  St is a plain aggregate of doubles; ld(node, St&) loads one node.
+template <class G, class St, class Ld>
+__device__ __forceinline__ void trace_load(const G& g, int n, int d, St& st, Ld ld) {
+  if constexpr (G::GL) {
+    constexpr int NW = sizeof(St) / sizeof(double);
+    const int P = g.P;
+    const int i = n % P, j = g.dim == 2 ? n / P : 0;
+    const bool plus = (d == 0 ? i : j) == P - 1;
+    const double* l = plus ? g.lp : g.lm;
+    double acc[NW];
+#pragma unroll
+    for (int q = 0; q < NW; ++q) acc[q] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < P; ++k) {
+      const int nk = g.dim == 1 ? k : (d == 0 ? j * P + k : k * P + i);
+      St t;
+      double* tp = reinterpret_cast<double*>(&t);
+#pragma unroll
+      for (int q = 0; q < NW; ++q) tp[q] = 0.0;
+      ld(nk, t);
+#pragma unroll
+      for (int q = 0; q < NW; ++q) acc[q] = fma(l[k], tp[q], acc[q]);
+    }
+    double* sp = reinterpret_cast<double*>(&st);
+#pragma unroll
+    for (int q = 0; q < NW; ++q) sp[q] = acc[q];
+  } else {
+    ld(n, st);
+  }
+}
 
 // ---- neighbour addressing (periodic Cartesian, layout L) ----------------------
 // Across a partition boundary (hx / hy) the neighbour is a ghost element
@@ -255,9 +298,9 @@ __host__ __device__ constexpr int slot_doubles() {
          Mode::NFP * 2 * DIM * (DIM == 2 ? P : 1) * Mode::FPD;
 }
 
-template <int EQ, int DIM, int P, class Mode>
+template <int EQ, int DIM, int P, class Mode, class G>
 __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const PhysParams& pp,
-                                          const Geo& g, int e, int slot, int node, bool active,
+                                          const G& g, int e, int slot, int node, bool active,
                                           double* sF, double (&out)[Mode::NCH][NVars<EQ>::value]) {
   constexpr int NV = NVars<EQ>::value;
   constexpr int NCH = Mode::NCH;
@@ -324,22 +367,31 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
     for (int c = 0; c < NCH; ++c)
 #pragma unroll
       for (int v = 0; v < NV; ++v) sf[c][v] = 0.0;
-    auto add_face = [&](int f, int k) {
+    auto add_face = [&](int f, int k, double lh) {
       const int d = f >> 1;
-      const bool plus = f & 1;
       const int fn = f * FN + k;
       double cf[NCH][NV];
       Mode::face_combine(A, pp, d, sRaw + fn, sRaw + NFN + fn, NFP * NFN, cf);
-      const double sc = (d == 0 ? g.sx : g.sy) * (plus ? g.lhp : -g.lhm);
+      const double sc = (d == 0 ? g.sx : g.sy) * lh;
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
         for (int v = 0; v < NV; ++v) sf[c][v] += __dmul_rn(sc, cf[c][v]);
     };
-    if (i == P - 1) add_face(1, j);
-    if (i == 0) add_face(0, j);
-    if (DIM == 2 && j == P - 1) add_face(3, i);
-    if (DIM == 2 && j == 0) add_face(2, i);
+    if constexpr (G::GL) {
+      // Gauss-Legendre: every node receives all faces, weighted by lhat_i(+-1) (eq:DGSEM_wt)
+#pragma unroll 1
+      for (int f = 0; f < 2 * DIM; ++f) {
+        const int d = f >> 1, plus = f & 1;
+        const int t = d == 0 ? i : j;
+        add_face(plus ? 1 + 2 * d : 2 * d, d == 0 ? j : i, plus ? g.lhpv[t] : -g.lhmv[t]);
+      }
+    } else {
+      if (i == P - 1) add_face(1, j, g.lhp);
+      if (i == 0) add_face(0, j, -g.lhm);
+      if (DIM == 2 && j == P - 1) add_face(3, i, g.lhp);
+      if (DIM == 2 && j == 0) add_face(2, i, -g.lhm);
+    }
     double Dr[P], Dc[P];
 #pragma unroll
     for (int l = 0; l < P; ++l) {
@@ -379,9 +431,9 @@ __host__ __device__ constexpr int epb_for(int nodes) {
 #ifndef HBPDC_MINB
 #define HBPDC_MINB 4
 #endif
-template <int EQ, int DIM, int P, class Mode, int EPB>
+template <int EQ, int DIM, int P, class Mode, int EPB, bool GL>
 __global__ void __launch_bounds__(EPB * ipow(P, DIM), HBPDC_MINB)
-op_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g) {
+op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int NV = NVars<EQ>::value;
   extern __shared__ __align__(16) double sF[];     // EPB * slot_doubles (dynamic: may exceed 48 KB)

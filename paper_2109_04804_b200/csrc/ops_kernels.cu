@@ -5,6 +5,19 @@
 #include "modes.cuh"
 #include "launch.h"
 
+// This file is compiled twice: GLL nodes (the product configuration, also the
+// public entry points) and, as ops_kernels_gl.cu with HBPDC_OPS_GL=1, the
+// Gauss-Legendre instantiations (advection and Euler), reached through *_gl.
+#ifndef HBPDC_OPS_GL
+#define HBPDC_OPS_GL 0
+#endif
+static constexpr bool kGL = HBPDC_OPS_GL;
+using GeoK = GeoSel<kGL>;
+static GeoK geo_sel(const Geo& g) {
+  GeoK s;
+  static_cast<Geo&>(s) = g;
+  return s;
+}
 
 template <int EQ, int DIM, int P, class Mode>
 static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
@@ -16,11 +29,11 @@ static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
   if constexpr (smem > 48 * 1024) {
     static bool attr = false;       // once per instantiation (same value from any thread)
     if (!attr) {
-      cudaFuncSetAttribute(op_kernel<EQ, DIM, P, Mode, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(op_kernel<EQ, DIM, P, Mode, EPB, kGL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
   }
-  op_kernel<EQ, DIM, P, Mode, EPB><<<grid, EPB * NODES, smem, c.stream>>>(A, c.pp, g);
+  op_kernel<EQ, DIM, P, Mode, EPB, kGL><<<grid, EPB * NODES, smem, c.stream>>>(A, c.pp, geo_sel(g));
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -68,12 +81,15 @@ template <int EQ, int NODES> struct ModeKCol {
       for (int v = 0; v < NV; ++v) c[d][0][v] = F[d][v].a;
   }
   static constexpr int NFP = 2, FPD = half_doubles<EQ, J1>();
-  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
+  template <class G>
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const G& g, int e, int own, int nb,
                                    int nnode, int slot, bool plus, int d, int part, double* raw,
                                    int rs) {
     const bool use_own = (part == 0) == plus;
     State st;
-    load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
+    const int le = use_own ? e : nb;
+    trace_load(g, use_own ? own : nnode, d, st,
+               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); });
     half_flux<EQ, J1>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args&, const PhysParams& pp, int d, const double* rL, const double* rR,
@@ -108,12 +124,15 @@ template <int EQ, int NODES> struct ModeHCol {
       for (int v = 0; v < NV; ++v) c[d][0][v] = F[d][v].c;
   }
   static constexpr int NFP = 2, FPD = half_doubles<EQ, HJ>();
-  __device__ static void face_part(const Args& A, const PhysParams& pp, const Geo& g, int e, int own, int nb,
+  template <class G>
+  __device__ static void face_part(const Args& A, const PhysParams& pp, const G& g, int e, int own, int nb,
                                    int nnode, int slot, bool plus, int d, int part, double* raw,
                                    int rs) {
     const bool use_own = (part == 0) == plus;
     State st;
-    load(A, g, use_own ? e : nb, slot, use_own ? own : nnode, st, !use_own);
+    const int le = use_own ? e : nb;
+    trace_load(g, use_own ? own : nnode, d, st,
+               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); });
     half_flux<EQ, HJ>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args&, const PhysParams& pp, int d, const double* rL, const double* rR,
@@ -126,7 +145,7 @@ template <int EQ, int NODES> struct ModeHCol {
 
 template <int EQ, int DIM, int P, int EPB, bool HESS>
 __global__ void __launch_bounds__(EPB * ipow(P, DIM))
-kbuild_kernel(const double* __restrict__ Wb, const double* __restrict__ gWb, const PhysParams pp, const Geo g, double a1dt, double c2,
+kbuild_kernel(const double* __restrict__ Wb, const double* __restrict__ gWb, const PhysParams pp, const GeoK g, double a1dt, double c2,
               double* __restrict__ M, int e0, const double* __restrict__ Sb, const double* __restrict__ gSb) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int NV = NVars<EQ>::value;
@@ -196,7 +215,7 @@ static cudaError_t run_kbuild_t(const OpCfg& c, const Geo& g, const double* Wb, 
       attr = true;
     }
   }
-  kbuild_kernel<EQ, DIM, P, EPB, HESS><<<ne, EPB * NODES, smem, c.stream>>>(Wb, gWb, c.pp, g, a1dt, c2, M, e0, Sb, gSb);
+  kbuild_kernel<EQ, DIM, P, EPB, HESS><<<ne, EPB * NODES, smem, c.stream>>>(Wb, gWb, c.pp, geo_sel(g), a1dt, c2, M, e0, Sb, gSb);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -262,11 +281,23 @@ static cudaError_t dispatch(const OpCfg& c, F&& f) {
   HBPDC_P_LIST(CASE, 0, 1)
   HBPDC_P_LIST(CASE, 0, 2)
   HBPDC_P_LIST(CASE, 1, 2)
+#if !HBPDC_OPS_GL
   HBPDC_P_LIST(CASE, 2, 2)
+#endif
 #undef CASE
   return cudaErrorInvalidValue;
 }
 
+#if HBPDC_OPS_GL
+cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
+  return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
+}
+
+cudaError_t launch_kbuild_gl(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
+                             double c2, double* M, int e0, int ne, const double* Sb, const double* gSb) {
+  return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb); });
+}
+#else
 int op_grid(const OpCfg& c, const Geo& g) {
   const int nodes = ipow(c.P, c.dim);
   const int epb = epb_for(nodes);
@@ -274,10 +305,12 @@ int op_grid(const OpCfg& c, const Geo& g) {
 }
 
 cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
+  if (g.gl) return launch_op_gl(kind, c, g, A);
   return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
 }
 
 cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
+  if (g.gl) return cudaErrorNotSupported;       // GL: no Navier-Stokes
   return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G); });
 }
 
@@ -293,6 +326,7 @@ int lift_jet_components(OpKind kind, int state) {
 
 cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
                           double* M, int e0, int ne, const double* Sb, const double* gSb) {
+  if (g.gl) return launch_kbuild_gl(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb);
   return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb); });
 }
 
@@ -362,3 +396,4 @@ cudaError_t launch_colour_gather(const double* y1, const double* y2, double* K, 
   hbpdc_count_launch();
   return cudaGetLastError();
 }
+#endif  // HBPDC_OPS_GL

@@ -184,13 +184,14 @@ class Context:
                  newton_atol_dw=1e-12, newton_floor=64.0, newton_max=50, gmres_rtol=1e-6,
                  restart=700, max_krylov=7000, precond="bjext", precond_policy="per_step_per_alpha",
                  jvp_mode="auto", batch_stages=True, gmres_sstep=1, rank=0, nranks=1, px=1, py=1, nccl_id=None, stream=None, device=0,
-                 comm="auto", loopback=None, force_halo=False, flux="llf", mach=1.0, schur=False):
+                 comm="auto", loopback=None, force_halo=False, flux="llf", mach=1.0, schur=False,
+                 nodes="gll"):
         import torch
         self.lib = load()
         if not torch.cuda.is_available():
             raise RuntimeError("hbpdc needs a CUDA device (no CPU fallback)")
         pb = Problem(dim=dim, equation=_EQ[equation], gamma=gamma, mach_eps=mach, mu=mu, prandtl=prandtl,
-                     N=N, nodes=GLL, nx=nx, ny=ny, xmin=bounds[0], xmax=bounds[1], ymin=bounds[2],
+                     N=N, nodes={"gll": GLL, "gl": GL}[nodes], nx=nx, ny=ny, xmin=bounds[0], xmax=bounds[1], ymin=bounds[2],
                      ymax=bounds[3], flux={"llf": 0, "glf": 1}[flux], lifting=0, q=q, kmax=kmax)
         pb.a[0], pb.a[1] = a[0], a[1]
         op = SolverOpts(newton_rtol=newton_rtol, newton_atol_dw=newton_atol_dw, newton_floor=newton_floor,

@@ -1,0 +1,143 @@
+"""NEXT-3: Gauss-Legendre nodes (the element has no node on its edge, so
+the face trace is the line sum sum_l l_l(+-1) W_l and every node receives the
+surface terms weighted by lhat_i(+-1), eq:DGSEM_wt) -- GPU (C-ABI) vs the
+oracle's build_basis(N, "gl") discretisation.
+
+Tolerances as test_gpu_parity.py: operators / JVPs <= 1e-11 relative, FD JVP
+within max(1e-11, 4 delta_FD), BJ_ext build <= 1e-11 max(1, cond/1e4), end of
+run <= 1e-8.  Sizes span several CTAs with a ragged last CTA."""
+import numpy as np
+import pytest
+
+from oracle import dgsem, hbpc, implicit
+from paper_2109_04804_b200 import inputs
+from gpu_common import adv_ic, euler_ic, make_pair, rel, to_gpu, to_np, SEED
+
+pytestmark = pytest.mark.gpu
+
+GL_CASES = [
+    # (kind, N, nx, ny)
+    ("advection", 3, 10, None),
+    ("advection", 4, 7, 5),
+    ("euler", 3, 5, 4),
+    ("euler", 7, 3, 3),
+    ("euler", 1, 6, 5),
+]
+
+
+def _pair(kind, N, nx, ny, **kw):
+    a = (1.0, 0.0) if ny is None else (1.0, -0.6)
+    return make_pair(kind, N, nx, ny, a=a, nodes="gl", **kw)
+
+
+def _state(d, kind, seed):
+    return adv_ic(d, seed) if kind == "advection" else euler_ic(d, seed)
+
+
+@pytest.mark.parametrize("case", GL_CASES)
+def test_gl_node_coords(case):
+    d, ctx = _pair(*case)
+    for a, b in zip(ctx.node_coords(), d.node_coords()):
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("case", GL_CASES)
+def test_gl_operators(case):
+    """R1, R2, residual and the JVPs (EXACT for Euler, LINEAR for advection)."""
+    kind = case[0]
+    d, ctx = _pair(*case)
+    W = _state(d, kind, SEED + 61)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 62))
+    assert rel(to_np(ctx.rhs(to_gpu(W))), dgsem.rhs1(d, W)) <= 1e-11
+    assert rel(to_np(ctx.rhs(to_gpu(W), to_gpu(sig))), dgsem.rhs2(d, W, sig)) <= 1e-11
+    b = W * (1 + 1e-3 * inputs.random_field(d.n, SEED + 63))
+    a1, a2, dt = 0.5, 1 / 6, 0.02
+    G1o, G2o = implicit.residual(d, a1, a2, dt, b, W, sig)
+    G1g, G2g = ctx.residual(a1, a2, dt, to_gpu(b), to_gpu(W), to_gpu(sig))
+    assert rel(np.concatenate([to_np(G1g), to_np(G2g)]), np.concatenate([G1o, G2o])) <= 1e-11
+    dW = inputs.random_field(d.n, SEED + 64, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 65, unit_norm=True)
+    if kind == "advection":
+        z = np.zeros(d.n)
+        to, bo = implicit.jvp_linear(d, a1, a2, dt, dW, ds)
+        tg, bg = ctx.jvp(a1, a2, dt, to_gpu(z), to_gpu(z), to_gpu(dW), to_gpu(ds), mode="linear")
+    else:
+        to, bo = implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds)
+        tg, bg = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(dW), to_gpu(ds), mode="exact")
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11
+
+
+@pytest.mark.parametrize("case", [c for c in GL_CASES if c[0] == "euler"])
+def test_gl_jvp_fd(case):
+    kind = case[0]
+    d, ctx = _pair(*case)
+    W = _state(d, kind, SEED + 66)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 67))
+    dW = inputs.random_field(d.n, SEED + 68, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 69, unit_norm=True)
+    a1, a2, dt = 1.0, 1.0, 0.01
+    eps = implicit.fd_eps(dW)
+    fo = np.concatenate(implicit.jvp_fd(d, a1, a2, dt, W, sig, dW, ds, eps_override=(eps, None)))
+    ex = np.concatenate(implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds))
+    delta = rel(fo, ex)
+    tg, bg = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(dW), to_gpu(ds), mode="fd",
+                     eps_override=(eps, None))
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), fo) <= max(1e-11, 4 * delta)
+
+
+@pytest.mark.parametrize("precond", ["bjext", "bjext_h"])
+@pytest.mark.parametrize("case", [("advection", 3, 8, None), ("advection", 2, 6, 4), ("euler", 3, 4, 3)])
+def test_gl_precond(case, precond):
+    """BJ_ext / BJ^H_ext on GL nodes: the element blocks see the full line traces."""
+    kind = case[0]
+    d, ctx = _pair(*case, precond=precond)
+    W = _state(d, kind, SEED + 70)
+    a1, a2, dt = 1.0 / 6.0, 1.0 / 54.0, 0.05
+    pc = implicit.make_precond(precond, d, W, a1, a2, dt)
+    ctx.precond_build(a1, a2, dt, to_gpu(W))
+    cond = max(np.linalg.cond(M) for M in pc.M)
+    x = inputs.random_field(d.n, SEED + 71)
+    y = inputs.random_field(d.n, SEED + 72)
+    to, bo = pc.apply(x, y)
+    tg, bg = ctx.precond_apply(to_gpu(x), to_gpu(y))
+    assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11 * max(1, cond / 1e4)
+
+
+def test_gl_free_stream():
+    """A uniform Euler state is a steady solution on GL nodes too (the free-stream
+    row identity of Dhat, reading R2): |R1| at rounding level."""
+    d, ctx = _pair("euler", 5, 4, 3)
+    X = d.node_coords()[0]
+    W = inputs.layout([np.full_like(X, v) for v in (1.2, 0.3, -0.2, 2.5)], 2)
+    r = to_np(ctx.rhs(to_gpu(W)))
+    assert np.abs(r).max() <= 1e-12
+
+
+def _run_oracle(d, q, kmax, W0, dt, steps, **opt):
+    H = hbpc.HBPC(d, q, kmax, implicit.NewtonOpts(**opt))
+    W = W0.copy()
+    st = dict(stage_solves=0, newton_its=0, gmres_its=0, precond_builds=0)
+    for _ in range(steps):
+        W = H.step(W, dt, st)
+    return W
+
+
+@pytest.mark.parametrize("kind,q,kmax,sstep", [("advection", 6, 2, 1), ("euler", 4, 0, 1), ("euler", 4, 0, 4)])
+def test_gl_end_of_run(kind, q, kmax, sstep):
+    """HBPC(q, k_max) with BJ_ext on GL nodes, 2 steps: end of run vs the oracle <= 1e-8."""
+    ny = 4
+    d, ctx = _pair(kind, 3, 5, ny, q=q, kmax=kmax, gmres_rtol=1e-10, newton_rtol=1e-10, gmres_sstep=sstep)
+    W0 = _state(d, kind, SEED + 73)
+    dt = 0.02 if kind == "advection" else 0.01
+    Wo = _run_oracle(d, q, kmax, W0, dt, 2, rtol=1e-10, gmres_rtol=1e-10)
+    Wg = to_gpu(W0)
+    for _ in range(2):
+        ctx.step(dt, Wg)
+    assert rel(to_np(Wg), Wo) <= 1e-8
+
+
+def test_gl_rejects_partitions():
+    """GL on several partitions is refused at init (the halo carries GLL edge nodes)."""
+    from paper_2109_04804_b200 import hbpdc
+    with pytest.raises(Exception, match="single partition"):
+        hbpdc.Context(dim=2, equation="euler", N=3, nx=4, ny=4, nodes="gl", force_halo=True)
