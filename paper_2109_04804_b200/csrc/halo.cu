@@ -6,6 +6,10 @@
 // neighbour's into ghost elements (layout L, only face nodes written) that the
 // operator kernels address as elements nE + g (ops.cuh nbr_elem).
 //
+// Gauss-Legendre nodes (no node on the edge): the sender interpolates the
+// trace sum_l l_l(+-1) w_l along the line through face node k and the ghost's
+// edge-node slot holds that trace (the GL kernels read ghosts directly).
+//
 // Buffer layout: side segments s = 0 (-x), 1 (+x), 2 (-y), 3 (+y); inside a
 // segment [pos][field][var][k], pos = ey (x-sides) or ex (y-sides), k the
 // node index along the face.  A field has nvf "variables" of NODES values per
@@ -21,6 +25,8 @@ struct HaloArgs {
   int nel[4];           // elements along side s (0 if the side is inactive)
   int nf, nx, ny, nE, nv, P, dim, m, nodes;
   size_t total;
+  int gl;
+  double lp[8], lm[8];
 };
 
 __device__ __forceinline__ int face_node(int s, int k, int P, int dim) {
@@ -63,7 +69,19 @@ __global__ void halo_pack_kernel(HaloArgs H, double* __restrict__ send) {
       case 2: e = p; break;
       default: e = (H.ny - 1) * H.nx + p; break;
     }
-    send[flat] = H.src[f][(size_t)e * H.m + v * H.nodes + face_node(s, k, H.P, H.dim)];
+    const double* base = H.src[f] + (size_t)e * H.m + v * H.nodes;
+    if (H.gl) {
+      // trace on face s: line through face node k across the element (x-sides: row k, y-sides: column k)
+      const double* l = (s & 1) ? H.lp : H.lm;
+      double acc = 0.0;
+      for (int q = 0; q < H.P; ++q) {
+        const int nd = H.dim == 1 ? q : (s < 2 ? k * H.P + q : q * H.P + k);
+        acc = fma(l[q], base[nd], acc);
+      }
+      send[flat] = acc;
+    } else {
+      send[flat] = base[face_node(s, k, H.P, H.dim)];
+    }
   }
 }
 
@@ -90,6 +108,8 @@ HaloArgs make_args(const HaloLayout& L, int nf, int nvf) {
   H.nx = L.nx; H.ny = L.ny; H.nE = L.nx * L.ny; H.nv = nvf > 0 ? nvf : L.nv; H.P = L.P; H.dim = L.dim;
   H.nodes = L.dim == 2 ? L.P * L.P : L.P;
   H.m = H.nv * H.nodes;
+  H.gl = L.gl;
+  for (int q = 0; q < 8; ++q) { H.lp[q] = L.lp[q]; H.lm[q] = L.lm[q]; }
   const int FN = L.dim == 2 ? L.P : 1;
   size_t acc = 0;
   for (int s = 0; s < 4; ++s) {

@@ -1546,8 +1546,6 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->nodes != HBPDC_GLL && pb->nodes != HBPDC_GL) return bad("nodes must be HBPDC_GLL or HBPDC_GL");
   if (pb->nodes == HBPDC_GL && pb->equation == HBPDC_NAVIER_STOKES)
     return bad("Gauss-Legendre nodes: advection and Euler only (Navier-Stokes: GLL)");
-  if (pb->nodes == HBPDC_GL && (c->ds.nranks > 1 || c->ds.force_halo))
-    return bad("Gauss-Legendre nodes: single partition only (the halo carries GLL edge nodes)");
   if (!(pb->mach_eps > 0.0)) return bad("mach_eps must be positive");
   if (pb->equation == HBPDC_NAVIER_STOKES && pb->mach_eps != 1.0)
     return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");
@@ -1607,6 +1605,8 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->geo.lhm = c->basis.lhm;
   for (int i = 0; i < c->P * c->P; ++i) c->geo.Dh[i] = c->basis.Dhat[i];
   c->geo.gl = c->basis.gl;
+  c->hl.gl = c->basis.gl;                // GL halos carry interpolated traces
+  for (int i = 0; i < c->P; ++i) { c->hl.lp[i] = c->basis.lp[i]; c->hl.lm[i] = c->basis.lm[i]; }
   c->geo.P = c->P;
   c->geo.dim = pb->dim;
   for (int i = 0; i < c->P; ++i) {

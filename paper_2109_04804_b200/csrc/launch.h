@@ -116,6 +116,8 @@ constexpr int HALO_MAX_FIELDS = 4;
 struct HaloLayout {
   int nx, ny, nv, P, dim;   // local element grid, variables, nodes per direction, dimension
   int active[4];            // sides taking part: -x, +x, -y, +y
+  int gl;                   // Gauss-Legendre: send the interpolated traces sum_l l_l(+-1) w_l
+  double lp[8], lm[8];      // l_l(+1), l_l(-1)
 };
 // segment offsets / lengths (doubles) of an exchange of nf fields
 // (nvf: variables per element of each field; 0 = the state's n_v)

@@ -83,7 +83,8 @@ struct OneJetMode {
       // its half flux in plain doubles, tangent slots zero (same values as the jet)
       if (!use_own) {
         NodeState<EQ, double> sd;
-        trace_load(g, nnode, d, sd, [=](int nd, NodeState<EQ, double>& s) { Derived::load_value(A, nb, nd, s.w); });
+        trace_load(g, nnode, d, sd, [=](int nd, NodeState<EQ, double>& s) { Derived::load_value(A, nb, nd, s.w); },
+                   nb >= A.nE);
         constexpr int NR = 2 * NV + 1, JN = JetN<J>::value;
         double tmp[NR];
         half_flux<EQ, double>(pp, sd, d, tmp, 1);
@@ -99,7 +100,7 @@ struct OneJetMode {
     State st;
     const int le = use_own ? e : nb;
     trace_load(g, use_own ? own : nnode, d, st,
-               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); });
+               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); }, le >= A.nE);
     half_flux<EQ, J>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args& A, const PhysParams& pp, int d, const double* rL,
@@ -330,7 +331,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
       if (!(fd_step(A) > 0.0)) return;
       NodeState<EQ, J1> so, sn;
       trace_load(g, own, d, so, [=](int nd, NodeState<EQ, J1>& s) { load_w<0>(A, e, nd, s.w, false); });
-      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J1>& s) { load_w<0>(A, nb, nd, s.w, true); });
+      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J1>& s) { load_w<0>(A, nb, nd, s.w, true); },
+                 nb >= A.nE);
       ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, e, own, so);
       ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, nb, nnode, sn);
       J1 fp[NV];
@@ -340,7 +342,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
     } else {
       NodeState<EQ, J2> so, sn;
       trace_load(g, own, d, so, [=](int nd, NodeState<EQ, J2>& s) { load_w<1>(A, e, nd, s.w, false); });
-      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J2>& s) { load_w<1>(A, nb, nd, s.w, true); });
+      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J2>& s) { load_w<1>(A, nb, nd, s.w, true); },
+                 nb >= A.nE);
       ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, e, own, so);
       ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, nb, nnode, sn);
       J2 fq[NV];
@@ -413,7 +416,7 @@ template <int EQ, int NODES> struct ModeJvpLinear {
                                    int rs) {
     State so, sn;
     trace_load(g, own, d, so, [=](int nd, State& s) { load(A, g, e, slot, nd, s, false); });
-    trace_load(g, nnode, d, sn, [=](int nd, State& s) { load(A, g, nb, slot, nd, s, true); });
+    trace_load(g, nnode, d, sn, [=](int nd, State& s) { load(A, g, nb, slot, nd, s, true); }, nb >= A.nE);
     const NodeState<EQ, double>& o = part == 0 ? so.u0 : so.u1;
     const NodeState<EQ, double>& q = part == 0 ? sn.u0 : sn.u1;
     double f[NV];

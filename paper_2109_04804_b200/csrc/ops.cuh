@@ -46,9 +46,12 @@ template <bool GL_> struct GeoSel : Geo {
 // line sum  sum_l l_l(+-1) S(line node l)  through n in direction d (the side
 // is the edge n sits on), accumulated component-wise (a jet is linear in its
 // components).  St is a plain aggregate of doubles; ld(node, St&) loads one node.
+// A ghost element (ghost = true) already holds the trace at its edge node
+// (halo.cu interpolates on the sending rank).
 template <class G, class St, class Ld>
-__device__ __forceinline__ void trace_load(const G& g, int n, int d, St& st, Ld ld) {
+__device__ __forceinline__ void trace_load(const G& g, int n, int d, St& st, Ld ld, bool ghost = false) {
   if constexpr (G::GL) {
+    if (ghost) { ld(n, st); return; }
     constexpr int NW = sizeof(St) / sizeof(double);
     const int P = g.P;
     const int i = n % P, j = g.dim == 2 ? n / P : 0;

@@ -89,7 +89,7 @@ template <int EQ, int NODES> struct ModeKCol {
     State st;
     const int le = use_own ? e : nb;
     trace_load(g, use_own ? own : nnode, d, st,
-               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); });
+               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); }, le >= A.nE);
     half_flux<EQ, J1>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args&, const PhysParams& pp, int d, const double* rL, const double* rR,
@@ -132,7 +132,7 @@ template <int EQ, int NODES> struct ModeHCol {
     State st;
     const int le = use_own ? e : nb;
     trace_load(g, use_own ? own : nnode, d, st,
-               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); });
+               [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); }, le >= A.nE);
     half_flux<EQ, HJ>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args&, const PhysParams& pp, int d, const double* rL, const double* rR,

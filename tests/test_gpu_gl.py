@@ -136,8 +136,129 @@ def test_gl_end_of_run(kind, q, kmax, sstep):
     assert rel(to_np(Wg), Wo) <= 1e-8
 
 
-def test_gl_rejects_partitions():
-    """GL on several partitions is refused at init (the halo carries GLL edge nodes)."""
+def test_gl_rejects_navier_stokes():
+    """GL with Navier-Stokes is refused at init (the BR1 lifting is GLL-only)."""
     from paper_2109_04804_b200 import hbpdc
-    with pytest.raises(Exception, match="single partition"):
-        hbpdc.Context(dim=2, equation="euler", N=3, nx=4, ny=4, nodes="gl", force_halo=True)
+    with pytest.raises(Exception, match="Gauss-Legendre"):
+        hbpdc.Context(dim=2, equation="navier_stokes", N=3, nx=4, ny=4, nodes="gl", mu=0.01)
+
+
+# ---- element partition (loopback ranks on one GPU; the halo carries interpolated traces) ----
+GL_PART_CASES = [
+    # kind, N, nx, ny, px, py
+    ("euler", 3, 4, 4, 2, 2),
+    ("euler", 4, 6, 4, 3, 1),
+    ("advection", 3, 4, 6, 1, 2),
+    ("advection", 3, 8, None, 2, 1),
+]
+
+
+@pytest.mark.parametrize("case", GL_PART_CASES)
+def test_gl_loopback_operators(case):
+    """Per-rank operators of a partitioned GL problem vs the single-rank result.
+    The ghost trace is interpolated by the sender (per field), the local one from
+    the loaded jet state, so the two agree to rounding (<= 1e-13) rather than
+    bitwise; the FD JVP within its own FD noise (vs the oracle, as test_gl_jvp_fd)."""
+    import torch
+    from paper_2109_04804_b200 import hbpdc
+    from test_gpu_partition import _block, _run_threads
+    kind, N, nx, ny, px, py = case
+    dim = 1 if ny is None else 2
+    d, ctx1 = _pair(kind, N, nx, ny)
+    W = _state(d, kind, SEED + 81)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 82))
+    dW = inputs.random_field(d.n, SEED + 83, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 84, unit_norm=True)
+    b = W * (1 + 1e-3 * inputs.random_field(d.n, SEED + 85))
+    a1, a2, dt = 1 / 6, 1 / 54, 0.02
+    eps = implicit.fd_eps(dW)
+    modes = ["linear"] if kind == "advection" else ["exact", "fd"]
+
+    def ops(ctx, blk):
+        Wg, sg, dWg, dsg, bg = (to_gpu(blk(x)) for x in (W, sig, dW, ds, b))
+        torch.cuda.synchronize()
+        out = {"R1": ctx.rhs(Wg), "R2": ctx.rhs(Wg, sg), "G": ctx.residual(a1, a2, dt, bg, Wg, sg)}
+        for md in modes:
+            out["jvp_" + md] = ctx.jvp(a1, a2, dt, Wg, sg, dWg, dsg, mode=md,
+                                       eps_override=(eps, None) if md == "fd" else None)
+        ctx.precond_build(a1, a2, dt, Wg)
+        out["pc"] = ctx.precond_apply(dWg, dsg)
+        torch.cuda.synchronize()
+        return {k: (np.concatenate([to_np(x) for x in v]) if isinstance(v, tuple) else to_np(v))
+                for k, v in out.items()}
+
+    ref = ops(ctx1, lambda x: x)
+    assert rel(ref["R1"], dgsem.rhs1(d, W)) <= 1e-11
+    fd_tol = None
+    if kind == "euler":
+        fo = np.concatenate(implicit.jvp_fd(d, a1, a2, dt, W, sig, dW, ds, eps_override=(eps, None)))
+        ex = np.concatenate(implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds))
+        fd_tol = max(1e-11, 4 * rel(fo, ex))
+    group = hbpdc.LoopbackGroup(px * py)
+    a = (1.0, 0.0) if dim == 1 else (1.0, -0.6)
+    ctxs = [hbpdc.Context(dim=dim, equation=kind, N=N, nx=nx, ny=ny or 1, a=a, rank=r, nranks=px * py, px=px,
+                          py=py, comm="loopback", loopback=group, stream=torch.cuda.Stream(), nodes="gl")
+            for r in range(px * py)]
+    try:
+        def blk_of(c):
+            return lambda x: _block(x, dim, nx, ny or 1, d.m, c.ex0, c.ey0, c.nx_local, c.ny_local)
+        outs = _run_threads([lambda c=c: ops(c, blk_of(c)) for c in ctxs])
+        for c, o in zip(ctxs, outs):
+            blk = blk_of(c)
+            for key, r in ref.items():
+                rb = np.concatenate([blk(r[:d.n]), blk(r[d.n:])]) if r.size == 2 * d.n else blk(r)
+                tol = fd_tol if key == "jvp_fd" else 1e-13
+                assert rel(o[key], rb) <= tol, (key, c.rank, rel(o[key], rb))
+    finally:
+        for c in ctxs:
+            c.close()
+        group.close()
+
+
+def test_gl_loopback_hbpc_step():
+    """Euler HBPC(4,0) on GL nodes, 2 x 2 loopback ranks: one step vs the oracle <= 1e-8."""
+    import torch
+    from paper_2109_04804_b200 import hbpdc
+    from test_gpu_partition import _block, _run_threads
+    N, nx, ny, px, py = 3, 4, 4, 2, 2
+    d, _ = _pair("euler", N, nx, ny)
+    W0 = _state(d, "euler", SEED + 86)
+    dt = 0.01
+    Wo = _run_oracle(d, 4, 0, W0, dt, 1, rtol=1e-10, gmres_rtol=1e-10)
+    group = hbpdc.LoopbackGroup(px * py)
+    ctxs = [hbpdc.Context(dim=2, equation="euler", N=N, nx=nx, ny=ny, a=(1.0, -0.6), q=4, kmax=0,
+                          gmres_rtol=1e-10, newton_rtol=1e-10, rank=r, nranks=px * py, px=px, py=py,
+                          comm="loopback", loopback=group, stream=torch.cuda.Stream(), nodes="gl")
+            for r in range(px * py)]
+    try:
+        def run(c):
+            Wl = to_gpu(_block(W0, 2, nx, ny, d.m, c.ex0, c.ey0, c.nx_local, c.ny_local))
+            torch.cuda.synchronize()
+            c.step(dt, Wl)
+            torch.cuda.synchronize()
+            return to_np(Wl)
+        outs = _run_threads([lambda c=c: run(c) for c in ctxs])
+        for c, Wl in zip(ctxs, outs):
+            blk = _block(Wo, 2, nx, ny, d.m, c.ex0, c.ey0, c.nx_local, c.ny_local)
+            assert rel(Wl, blk) <= 1e-8, (c.rank, rel(Wl, blk))
+    finally:
+        for c in ctxs:
+            c.close()
+        group.close()
+
+
+def test_gl_nccl_self_halo():
+    """GL through the NCCL transport with a forced self halo (1 rank): R1 and one step vs single rank."""
+    from paper_2109_04804_b200 import hbpdc
+    d, ctx1 = _pair("euler", 3, 4, 4)
+    ctxn = hbpdc.Context(dim=2, equation="euler", N=3, nx=4, ny=4, a=(1.0, -0.6), comm="nccl",
+                         nccl_id=hbpdc.nccl_unique_id(), force_halo=True, nodes="gl")
+    try:
+        W = _state(d, "euler", SEED + 87)
+        assert rel(to_np(ctxn.rhs(to_gpu(W))), to_np(ctx1.rhs(to_gpu(W)))) <= 1e-13
+        W1, Wn = to_gpu(W), to_gpu(W)
+        ctx1.step(0.01, W1)
+        ctxn.step(0.01, Wn)
+        assert rel(to_np(Wn), to_np(W1)) <= 1e-10
+    finally:
+        ctxn.close()
