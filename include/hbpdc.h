@@ -73,7 +73,7 @@ typedef struct {
   double prandtl;       /* Prandtl number (NS), e.g. 0.72                   */
   int N;                /* polynomial degree, 1..7                                 */
   int nodes;            /* HBPDC_GLL (configs, reading R1) or HBPDC_GL (
-                           advection / Euler; not Navier-Stokes)                  */
+                           Navier-Stokes on GL: one partition only)               */
   int nx, ny;           /* global element counts (ny ignored in 1D)                */
   double xmin, xmax, ymin, ymax;   /* periodic Cartesian domain                   */
   int flux;             /* HBPDC_LLF (reading R3) | HBPDC_GLF_PAPER (eq:Riemann, P:197-201:
@@ -142,7 +142,7 @@ typedef struct {               /* summed over one hbpdc_step                    
   double final_newton_rel, wall_s;
 } hbpdc_step_stats;
 
-/* Create a context: basis (GLL nodes/weights, Dhat = -M^-1 D^T M, reading R2),
+/* Create a context: basis (GLL or GL nodes/weights, Dhat = -M^-1 D^T M, reading R2),
  * mesh, rank partition, NCCL communicator, scratch.  Host only. */
 HBPDC_API hbpdc_status hbpdc_init(const hbpdc_problem* problem, const hbpdc_solver_opts* opts,
                         const hbpdc_dist* dist, hbpdc_ctx** out);

@@ -1544,8 +1544,9 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->equation != HBPDC_ADVECTION && pb->dim != 2) return bad("Euler/NS need dim = 2");
   if (pb->N < 1 || pb->N > 7) return bad("N must be in 1..7");
   if (pb->nodes != HBPDC_GLL && pb->nodes != HBPDC_GL) return bad("nodes must be HBPDC_GLL or HBPDC_GL");
-  if (pb->nodes == HBPDC_GL && pb->equation == HBPDC_NAVIER_STOKES)
-    return bad("Gauss-Legendre nodes: advection and Euler only (Navier-Stokes: GLL)");
+  if (pb->nodes == HBPDC_GL && pb->equation == HBPDC_NAVIER_STOKES && (c->ds.nranks > 1 || c->ds.force_halo))
+    return bad("Gauss-Legendre nodes with Navier-Stokes: single partition only (the BR1 lifting needs the "
+               "traces of g(w), the halo carries those of w)");
   if (!(pb->mach_eps > 0.0)) return bad("mach_eps must be positive");
   if (pb->equation == HBPDC_NAVIER_STOKES && pb->mach_eps != 1.0)
     return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");

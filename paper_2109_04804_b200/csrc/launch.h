@@ -24,6 +24,7 @@ cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A
 int op_grid(const OpCfg& c, const Geo& g);
 // Gauss-Legendre instantiations (ops_kernels_gl.cu), reached from launch_op / launch_kbuild when g.gl
 cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
+cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout);
 cudaError_t launch_kbuild_gl(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
                              double c2, double* M, int e0, int ne, const double* Sb, const double* gSb);
 // BR1 lifting of jet state `state` of operator `kind` into Gout

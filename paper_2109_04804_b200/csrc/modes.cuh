@@ -330,22 +330,28 @@ template <int EQ, int NODES> struct ModeJvpFD {
     if (part == 0) {
       if (!(fd_step(A) > 0.0)) return;
       NodeState<EQ, J1> so, sn;
-      trace_load(g, own, d, so, [=](int nd, NodeState<EQ, J1>& s) { load_w<0>(A, e, nd, s.w, false); });
-      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J1>& s) { load_w<0>(A, nb, nd, s.w, true); },
-                 nb >= A.nE);
-      ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, e, own, so);
-      ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, nb, nnode, sn);
+      trace_load(g, own, d, so, [=](int nd, NodeState<EQ, J1>& s) {
+        load_w<0>(A, e, nd, s.w, false);
+        ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, e, nd, s);
+      });
+      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J1>& s) {
+        load_w<0>(A, nb, nd, s.w, true);
+        ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, nb, nd, s);
+      }, nb >= A.nE);
       J1 fp[NV];
       if (plus) face_flux<EQ>(pp, so, sn, d, fp);
       else face_flux<EQ>(pp, sn, so, d, fp);
       for (int v = 0; v < NV; ++v) { raw[rs * (2 * v)] = fp[v].v; raw[rs * (2 * v + 1)] = fp[v].a; }
     } else {
       NodeState<EQ, J2> so, sn;
-      trace_load(g, own, d, so, [=](int nd, NodeState<EQ, J2>& s) { load_w<1>(A, e, nd, s.w, false); });
-      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J2>& s) { load_w<1>(A, nb, nd, s.w, true); },
-                 nb >= A.nE);
-      ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, e, own, so);
-      ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, nb, nnode, sn);
+      trace_load(g, own, d, so, [=](int nd, NodeState<EQ, J2>& s) {
+        load_w<1>(A, e, nd, s.w, false);
+        ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, e, nd, s);
+      });
+      trace_load(g, nnode, d, sn, [=](int nd, NodeState<EQ, J2>& s) {
+        load_w<1>(A, nb, nd, s.w, true);
+        ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, nb, nd, s);
+      }, nb >= A.nE);
       J2 fq[NV];
       if (plus) face_flux<EQ>(pp, so, sn, d, fq);
       else face_flux<EQ>(pp, sn, so, d, fq);

@@ -476,9 +476,9 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g) 
 // ---- BR1 lifting (eq:Lifting P:855, central value P:861; reading R19) -----------
 //   d^x_ij = sx ( sum_l Dh_il g_lj + g*_E,j lhat_N(1) [i=N] - g*_W,j lhat_0(-1) [i=0] )
 // Computed for jet state K of the mode; result [elem][6][JetN][NODES].
-template <int P, class Mode, int K, int EPB>
+template <int P, class Mode, int K, int EPB, bool GL>
 __global__ void __launch_bounds__(EPB * P * P)
-lift_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g, double* Gout) {
+lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g, double* Gout) {
   using T = typename Mode::template StateT<K>;
   constexpr int NODES = P * P, PS = P + 1, PLANE = P * PS;
   constexpr int JN = JetN<T>::value;
@@ -491,7 +491,57 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g, doubl
   T sx_[3], sy_[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) { sx_[k] = jconst<T>(0.0); sy_[k] = jconst<T>(0.0); }
-  if (active) {
+  if constexpr (GL) {
+    // Gauss-Legendre: g* = 1/2 (own + neighbour trace), traces sum_l l_l(+-1) g(w_l) of the
+    // nodal gradient variables (oracle lifting()), on every node weighted by lhat(+-1)
+    if (active) {
+      T w[4], gv[3];
+      Mode::template load_w<K>(A, e, node, w, false);
+      grad_vars(pp, w, gv);
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int q = 0; q < JN; ++q) sg[(k * JN + q) * PLANE + j * PS + i] = jget(gv[k], q);
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll 1
+      for (int f = 0; f < 4; ++f) {
+        const int d = f >> 1, side = (f & 1) ? +1 : -1;
+        const double* lo = side > 0 ? g.lp : g.lm;      // own trace on this face
+        const double* ln = side > 0 ? g.lm : g.lp;      // the neighbour's opposite face
+        const int nb = nbr_elem(g, e, d, side);
+        double own[3][JN], nbr[3][JN];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int q = 0; q < JN; ++q) { own[k][q] = 0.0; nbr[k][q] = 0.0; }
+#pragma unroll 1
+        for (int l = 0; l < P; ++l) {
+          const int ii = d == 0 ? l : i, jj = d == 0 ? j : l;
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < JN; ++q) own[k][q] = fma(lo[l], sg[(k * JN + q) * PLANE + jj * PS + ii], own[k][q]);
+          T wn[4], gn[3];
+          Mode::template load_w<K>(A, nb, jj * P + ii, wn, true);
+          grad_vars(pp, wn, gn);
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < JN; ++q) nbr[k][q] = fma(ln[l], jget(gn[k], q), nbr[k][q]);
+        }
+        const int t = d == 0 ? i : j;
+        const double s = (d == 0 ? g.sx : g.sy) * (side > 0 ? g.lhpv[t] : -g.lhmv[t]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const T go = jmake<T>(own[k]), gn = jmake<T>(nbr[k]);
+          const T gs = side > 0 ? 0.5 * (go + gn) : 0.5 * (gn + go);
+          if (d == 0) sx_[k] = sx_[k] + s * gs; else sy_[k] = sy_[k] + s * gs;
+        }
+      }
+    }
+  } else if (active) {
     T w[4], gv[3];
     Mode::template load_w<K>(A, e, node, w, false);
     grad_vars(pp, w, gv);

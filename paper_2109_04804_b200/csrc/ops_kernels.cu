@@ -44,7 +44,7 @@ static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, doubl
   constexpr int EPB = epb_for(NODES);
   const int grid = (g.nE + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
-  lift_kernel<P, Mode, K, EPB><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, g, G);
+  lift_kernel<P, Mode, K, EPB, kGL><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -281,14 +281,16 @@ static cudaError_t dispatch(const OpCfg& c, F&& f) {
   HBPDC_P_LIST(CASE, 0, 1)
   HBPDC_P_LIST(CASE, 0, 2)
   HBPDC_P_LIST(CASE, 1, 2)
-#if !HBPDC_OPS_GL
   HBPDC_P_LIST(CASE, 2, 2)
-#endif
 #undef CASE
   return cudaErrorInvalidValue;
 }
 
 #if HBPDC_OPS_GL
+cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
+  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G); });
+}
+
 cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
   return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
 }
@@ -310,7 +312,7 @@ cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A
 }
 
 cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
-  if (g.gl) return cudaErrorNotSupported;       // GL: no Navier-Stokes
+  if (g.gl) return launch_lift_gl(kind, state, c, g, A, G);
   return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G); });
 }
 

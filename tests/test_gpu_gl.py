@@ -11,7 +11,7 @@ import pytest
 
 from oracle import dgsem, hbpc, implicit
 from paper_2109_04804_b200 import inputs
-from gpu_common import adv_ic, euler_ic, make_pair, rel, to_gpu, to_np, SEED
+from gpu_common import adv_ic, euler_ic, make_pair, ns_ic, rel, to_gpu, to_np, SEED
 
 pytestmark = pytest.mark.gpu
 
@@ -22,16 +22,22 @@ GL_CASES = [
     ("euler", 3, 5, 4),
     ("euler", 7, 3, 3),
     ("euler", 1, 6, 5),
+    ("navier_stokes", 3, 4, 4),
+    ("navier_stokes", 5, 3, 5),
 ]
+NS_MU = 0.05      # viscous terms O(1) relative, as test_gpu_parity.py
 
 
 def _pair(kind, N, nx, ny, **kw):
     a = (1.0, 0.0) if ny is None else (1.0, -0.6)
+    if kind == "navier_stokes":
+        kw.setdefault("mu", NS_MU)
+        kw.setdefault("bounds", (0.0, 2 * np.pi, 0.0, 2 * np.pi))
     return make_pair(kind, N, nx, ny, a=a, nodes="gl", **kw)
 
 
 def _state(d, kind, seed):
-    return adv_ic(d, seed) if kind == "advection" else euler_ic(d, seed)
+    return {"advection": adv_ic, "euler": euler_ic, "navier_stokes": ns_ic}[kind](d, seed)
 
 
 @pytest.mark.parametrize("case", GL_CASES)
@@ -67,7 +73,7 @@ def test_gl_operators(case):
     assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11
 
 
-@pytest.mark.parametrize("case", [c for c in GL_CASES if c[0] == "euler"])
+@pytest.mark.parametrize("case", [c for c in GL_CASES if c[0] != "advection"])
 def test_gl_jvp_fd(case):
     kind = case[0]
     d, ctx = _pair(*case)
@@ -86,10 +92,14 @@ def test_gl_jvp_fd(case):
 
 
 @pytest.mark.parametrize("precond", ["bjext", "bjext_h"])
-@pytest.mark.parametrize("case", [("advection", 3, 8, None), ("advection", 2, 6, 4), ("euler", 3, 4, 3)])
+@pytest.mark.parametrize("case", [("advection", 3, 8, None), ("advection", 2, 6, 4), ("euler", 3, 4, 3),
+                                  ("navier_stokes", 2, 4, 3)])
 def test_gl_precond(case, precond):
-    """BJ_ext / BJ^H_ext on GL nodes: the element blocks see the full line traces."""
+    """BJ_ext / BJ^H_ext on GL nodes: the element blocks see the full line traces
+    (Navier-Stokes: BJ_ext by the two-hop colouring)."""
     kind = case[0]
+    if kind == "navier_stokes" and precond == "bjext_h":
+        pytest.skip("BJ^H_ext is implemented for advection and Euler")
     d, ctx = _pair(*case, precond=precond)
     W = _state(d, kind, SEED + 70)
     a1, a2, dt = 1.0 / 6.0, 1.0 / 54.0, 0.05
@@ -122,7 +132,8 @@ def _run_oracle(d, q, kmax, W0, dt, steps, **opt):
     return W
 
 
-@pytest.mark.parametrize("kind,q,kmax,sstep", [("advection", 6, 2, 1), ("euler", 4, 0, 1), ("euler", 4, 0, 4)])
+@pytest.mark.parametrize("kind,q,kmax,sstep", [("advection", 6, 2, 1), ("euler", 4, 0, 1), ("euler", 4, 0, 4),
+                                               ("navier_stokes", 4, 0, 1)])
 def test_gl_end_of_run(kind, q, kmax, sstep):
     """HBPC(q, k_max) with BJ_ext on GL nodes, 2 steps: end of run vs the oracle <= 1e-8."""
     ny = 4
@@ -136,11 +147,12 @@ def test_gl_end_of_run(kind, q, kmax, sstep):
     assert rel(to_np(Wg), Wo) <= 1e-8
 
 
-def test_gl_rejects_navier_stokes():
-    """GL with Navier-Stokes is refused at init (the BR1 lifting is GLL-only)."""
+def test_gl_rejects_navier_stokes_partitions():
+    """GL Navier-Stokes on several partitions is refused at init (the BR1 lifting
+    needs traces of g(w); the halo carries those of w)."""
     from paper_2109_04804_b200 import hbpdc
-    with pytest.raises(Exception, match="Gauss-Legendre"):
-        hbpdc.Context(dim=2, equation="navier_stokes", N=3, nx=4, ny=4, nodes="gl", mu=0.01)
+    with pytest.raises(Exception, match="single partition"):
+        hbpdc.Context(dim=2, equation="navier_stokes", N=3, nx=4, ny=4, nodes="gl", mu=0.01, force_halo=True)
 
 
 # ---- element partition (loopback ranks on one GPU; the halo carries interpolated traces) ----
