@@ -96,3 +96,38 @@ def test_fsal_and_stage1():
     W1 = H.step(W0, 0.05)
     r1 = dgsem.rhs1(d, W1)
     np.testing.assert_array_equal(H.cache[0], r1)
+
+
+def test_navier_stokes_run_converges_to_rk4():
+    """The Navier-Stokes end of run, pinned to something other than HBPC itself:
+    HBPC(4,0) steps of the BR1 semi-discretisation (whose R1 is pinned in
+    test_oracle_dgsem.py) converge at order 4 to an independent
+    classical RK4 solution of the same ODE W' = R1(W) with 200 steps (its own
+    error ~1e-12, far below the HBPC errors).  A wrong NS R2 = dR1/dt (e.g. a
+    dropped lifting-derivative term) would reduce the order to 2."""
+    eq = physics.Equation("navier_stokes", mu=0.05)
+    d = dgsem.Disc(basis.build_basis(2, "gll"), dgsem.Mesh(2, 3, 3, 0.0, 2 * np.pi, 0.0, 2 * np.pi), eq)
+    X, Y = d.node_coords()
+    W0 = inputs.perturbed_state(inputs.initial_state("C5", (X, Y)), 7, 1e-2)
+    T = 0.04
+
+    def rk4(W, n):
+        h = T / n
+        for _ in range(n):
+            k1 = dgsem.rhs1(d, W)
+            k2 = dgsem.rhs1(d, W + h / 2 * k1)
+            k3 = dgsem.rhs1(d, W + h / 2 * k2)
+            k4 = dgsem.rhs1(d, W + h * k3)
+            W = W + h / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+        return W
+
+    ref = rk4(W0, 200)
+    errs = []
+    for n_steps in (1, 2):
+        H = hbpc.HBPC(d, 4, 0, implicit.NewtonOpts(rtol=1e-12, gmres_rtol=1e-10, jvp_mode="exact"))
+        W = W0.copy()
+        for _ in range(n_steps):
+            W = H.step(W, T / n_steps)
+        errs.append(np.linalg.norm(W - ref) / np.linalg.norm(ref))
+    eoc = np.log2(errs[0] / errs[1])
+    assert errs[1] < 1e-5 and abs(eoc - 4) < 0.4, (errs, eoc)
