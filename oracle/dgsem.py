@@ -25,7 +25,9 @@ Navier-Stokes (C5): BR1 lifting (reading R19; the paper uses BR2,
 P:834): d = lifted gradient of w_grad = (u, v, T) from the weak form
 eq:Lifting (P:855) with the central surface value 1/2(g_L + g_R) (P:861);
 face gradients d^L, d^R are the traces of the lifted polynomial.  The
-viscous surface flux is 1/2(F^v_L + F^v_R).n.
+viscous surface flux is 1/2(F^v_L + F^v_R).n.  Equation.lifting =
+"br2": the volume keeps d, the face gradients come from the per-face local
+lifting of P:865 (lifting_br2_faces, reading R33).
 """
 from dataclasses import dataclass
 
@@ -206,6 +208,56 @@ def lifting(disc: Disc, Wf, ops=None):
     return out[0], out[1]
 
 
+def _deriv_strong(disc: Disc, G, d):
+    """Strong-form derivative (2/h_d) sum_l D_il g_l along direction d (nodal)."""
+    D = disc.basis.D
+    sc = _scale(d, disc.mesh)
+    if d == 0:
+        return sc * _lin(lambda c: np.einsum("il,...jl->...ji", D, c), G)
+    return sc * _lin(lambda c: np.einsum("jm,...mi->...ji", D, c), G)
+
+
+def lifting_br2_faces(disc: Disc, Wf, ops=None):
+    """BR2 face gradients (reading R33).  For each face f of an element,
+    the local lifting keeps the volume part of eq:Lifting and only the surface
+    contribution of f, scaled by eta_BR2; in the strong form that is
+        d_f = grad_h g + eta (2/h_d) (+-) (g*_f - g_f) lhat(+-1)      (normal component d only),
+    evaluated on f:  d_f = trace_f(grad_h g) + eta (2/h_d) (+-) (g*_f - g_f) c_+-,
+    c_+- = sum_i l_i(+-1) lhat_i(+-1) (GLL: 1/w_N, 1/w_0), with g* = 1/2 (g_L + g_R).
+    Returns, per direction d, the canonical tuple (own_plus, nbr_plus, nbr_minus, own_minus) of
+    (gx, gy) face gradients, each a pair of (ny, nx, 3, p) arrays (as ops.faces of Gx, Gy)."""
+    ops = ops or _Ops(disc)
+    eq, me = disc.eq, disc.mesh
+    b = disc.basis
+    eta = eq.eta_br2
+    cp = float(np.dot(b.l_plus, b.lhat_plus))
+    cm = float(np.dot(b.l_minus, b.lhat_minus))
+    g = physics.grad_vars(eq, _split(Wf, 2))
+    G = ad.stack(list(g), axis=2)                       # (ny, nx, 3, p, p)
+    DG = [_deriv_strong(disc, G, 0), _deriv_strong(disc, G, 1)]
+    out = []
+    for d in range(2):
+        own_p, nbr_p, nbr_m, own_m = ops.faces(G, d)
+        gstar_p = 0.5 * (own_p + nbr_p)
+        gstar_m = 0.5 * (nbr_m + own_m)
+        sc = _scale(d, me)
+        fp = []            # own plus-face gradient, components (x, y)
+        fm = []
+        for c in range(2):
+            tp = ops.trace(DG[c], d, +1)
+            tm = ops.trace(DG[c], d, -1)
+            if c == d:
+                tp = tp + (eta * sc * cp) * (gstar_p - own_p)
+                tm = tm - (eta * sc * cm) * (gstar_m - own_m)
+            fp.append(tp)
+            fm.append(tm)
+        ax = ops.elem_axis(d)
+        nbp = [_roll(x, -1, ax) for x in fm]           # neighbour across + face: its minus-face gradient
+        nbm = [_roll(x, +1, ax) for x in fp]           # neighbour across - face: its plus-face gradient
+        out.append((fp, nbp, nbm, fm))
+    return out
+
+
 def rhs1_field(disc: Disc, Wf, absolute=False):
     """R^(1)_h on a field-shaped array (values, duals or hyper-duals).
     absolute=True returns R1_abs (plain values only): every term of
@@ -219,6 +271,8 @@ def rhs1_field(disc: Disc, Wf, absolute=False):
     if eq.viscous:
         gx, gy = lifting(disc, Wf, ops)
         Gx, Gy = ad.stack(list(gx), axis=2), ad.stack(list(gy), axis=2)
+        if eq.lifting == "br2":
+            br2 = lifting_br2_faces(disc, Wf, _Ops(disc))
     total = 0.0
     for d in range(dim):
         # volume flux at the nodes
@@ -231,9 +285,14 @@ def rhs1_field(disc: Disc, Wf, absolute=False):
         wp, wnp, wnm, wm = [_split(t, va) for t in ops.faces(Wf, d)]
         fp = list(physics.numerical_flux(eq, wp, wnp, d))   # + face: L = own, R = nbr
         fm = list(physics.numerical_flux(eq, wnm, wm, d))   # - face: L = nbr, R = own
-        if eq.viscous:
+        if eq.viscous and eq.lifting == "br2":
+            faces = br2[d]                                  # (own+, nbr+, nbr-, own-), each (x, y)
+            gxp, gxnp, gxnm, gxm = [_split(t[0], 2) for t in faces]
+            gyp, gynp, gynm, gym = [_split(t[1], 2) for t in faces]
+        elif eq.viscous:
             gxp, gxnp, gxnm, gxm = [_split(t, 2) for t in ops.faces(Gx, d)]
             gyp, gynp, gynm, gym = [_split(t, 2) for t in ops.faces(Gy, d)]
+        if eq.viscous:
             fvL = physics.viscous_flux(eq, wp, gxp, gyp, d)
             fvR = physics.viscous_flux(eq, wnp, gxnp, gynp, d)
             fp = [f - 0.5 * (a + b) for f, a, b in zip(fp, fvL, fvR)]

@@ -39,6 +39,8 @@ class Equation:
     prandtl: float = 0.72
     numflux: str = "llf"       # "llf" (configs, reading R3) | "glf" (the paper's eq:Riemann)
     mach: float = 1.0          # reference Mach number eps of eq:Euler; configs: 1 (R18)
+    lifting: str = "br1"       # NS face gradients: "br1" (C5, reading R19) | "br2" (R33)
+    eta_br2: float = 2.0       # BR2 stabilisation parameter (the paper gives no value; reading R33)
 
     @property
     def nv(self):

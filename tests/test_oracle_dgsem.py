@@ -147,3 +147,75 @@ def test_lifting_constant_is_zero():
     W = const_state(d, [1.0, 0.5, 0.2, 3.0])
     gx, gy = dgsem.lifting(d, d.to_field(W))
     assert max(np.abs(g).max() for g in gx + gy) < 1e-12
+
+
+# ---- BR2 lifting (reading R33) ------------------------------------
+def _br2(N=3, nx=4, ny=3, eta=2.0, nodes="gll"):
+    return make("navier_stokes", N, nx, ny, nodes=nodes, bounds=(0, 2 * math.pi, 0, 2 * math.pi), mu=5e-2,
+                lifting="br2", eta_br2=eta)
+
+
+def test_br2_eta1_face_gradients_match_br1_traces():
+    """GLL, eta = 1: the local lifting of face f evaluated on f equals the trace of
+    the (independently computed, weak-form) BR1 lifted gradient in the normal
+    component everywhere, and in the tangential component away from the corner
+    nodes (where BR1 also carries the other direction's face term)."""
+    d = _br2(eta=1.0)
+    rng = np.random.default_rng(11)
+    W = const_state(d, [1.0, 0.3, -0.2, 2.5]) * (1 + 0.05 * rng.uniform(-1, 1, d.n))
+    Wf = d.to_field(W)
+    gx, gy = dgsem.lifting(d, Wf)
+    G = [np.stack(gx, axis=2), np.stack(gy, axis=2)]
+    ops = dgsem._Ops(d)
+    br2 = dgsem.lifting_br2_faces(d, Wf)
+    for dd in range(2):
+        br1_faces = [ops.faces(G[c], dd) for c in range(2)]        # per component: (own+, nbr+, nbr-, own-)
+        for t in range(4):
+            for c in range(2):
+                a, b = br2[dd][t][c], br1_faces[c][t]
+                if c == dd:
+                    np.testing.assert_allclose(a, b, rtol=0, atol=1e-11 * np.abs(b).max())
+                else:
+                    np.testing.assert_allclose(a[..., 1:-1], b[..., 1:-1], rtol=0, atol=1e-11 * np.abs(b).max())
+                    assert np.abs(a[..., [0, -1]] - b[..., [0, -1]]).max() > 1e-6   # corners differ
+
+
+@pytest.mark.parametrize("nodes", ["gll", "gl"])
+def test_br2_free_stream_conservation_and_r2(nodes):
+    """BR2 (eta = 2): free stream, discrete conservation (the viscous surface flux
+    stays single valued), R2 = d/dt R1 by central differences, and eta
+    enters R1 (the jump terms reach the viscous face flux)."""
+    d = _br2(nodes=nodes)
+    assert np.abs(dgsem.rhs1(d, const_state(d, [1.2, 0.3, -0.2, 2.5]))).max() < 1e-13
+    rng = np.random.default_rng(12)
+    W = const_state(d, [1.0, 0.3, -0.2, 2.5]) * (1 + 0.05 * rng.uniform(-1, 1, d.n))
+    R = dgsem.rhs1(d, W)
+    wq = np.outer(d.basis.w, d.basis.w).reshape(-1)
+    cons = (R.reshape(-1, 4, d.p * d.p) * wq).sum(axis=(0, 2))
+    assert np.abs(cons).max() <= 1e-12 * np.abs(R).max()
+    s = rng.standard_normal(d.n) * 0.1
+    h = 1e-5
+    fd = (dgsem.rhs1(d, W + h * s) - dgsem.rhs1(d, W - h * s)) / (2 * h)
+    r2 = dgsem.rhs2(d, W, s)
+    assert np.linalg.norm(r2 - fd) <= 1e-7 * np.linalg.norm(r2)
+    R4 = dgsem.rhs1(_br2(nodes=nodes, eta=4.0), W)
+    assert np.linalg.norm(R4 - R) > 1e-6 * np.linalg.norm(R)
+
+
+def test_br2_face_gradients_converge():
+    """BR2 face gradients of a smooth velocity field converge to the exact gradient
+    on the faces (the jump terms vanish with the jumps)."""
+    errs = []
+    for n in (4, 8):
+        d = make("navier_stokes", 4, n, n, bounds=(0, 2 * math.pi, 0, 2 * math.pi), mu=1e-3, lifting="br2")
+        X, Y = d.node_coords()
+        W = inputs.initial_state("C5", (X, Y))
+        br2 = dgsem.lifting_br2_faces(d, d.to_field(W))
+        ops = dgsem._Ops(d)
+        ux = np.cos(X) * np.cos(Y)                     # u = sin x cos y (C5): u_x
+        e = 0.0
+        for dd in range(2):
+            own_p = br2[dd][0][0][:, :, 0]                # x-gradient of u on the + face in direction dd
+            e = max(e, np.abs(own_p - ops.trace(ux, dd, +1)).max())
+        errs.append(e)
+    assert errs[1] < 1e-3 and errs[0] / errs[1] > 2 ** 3.5
