@@ -56,7 +56,7 @@ typedef enum {
 enum { HBPDC_ADVECTION = 0, HBPDC_EULER = 1, HBPDC_NAVIER_STOKES = 2 };
 enum { HBPDC_GLL = 0, HBPDC_GL = 1 };
 enum { HBPDC_LLF = 0, HBPDC_GLF_PAPER = 1 };
-enum { HBPDC_BR1 = 0 };
+enum { HBPDC_BR1 = 0, HBPDC_BR2 = 1 };
 enum { HBPDC_PC_NONE = 0, HBPDC_PC_BJEXT = 1, HBPDC_PC_BJEXT_H = 2 };
 enum { HBPDC_PC_PER_STEP_PER_ALPHA = 0, HBPDC_PC_PER_NEWTON = 1 };
 enum { HBPDC_JVP_AUTO = 0, HBPDC_JVP_FD = 1, HBPDC_JVP_EXACT = 2, HBPDC_JVP_LINEAR = 3 };
@@ -78,8 +78,11 @@ typedef struct {
   double xmin, xmax, ymin, ymax;   /* periodic Cartesian domain                   */
   int flux;             /* HBPDC_LLF (reading R3) | HBPDC_GLF_PAPER (eq:Riemann, P:197-201:
                            constant Lambda = diag(1/eps,1,1,1/eps), eps = 1; |a.n| for advection) */
-  int lifting;          /* HBPDC_BR1 (NS, reading R19)                             */
+  int lifting;          /* HBPDC_BR1 (NS, reading R19) | HBPDC_BR2 (reading R33;
+                           GLL, one partition)                                    */
   int q, kmax;          /* HBPC(q, k_max), q in {4, 6, 8}, k_max >= 0              */
+  double eta_br2;       /* BR2 stabilisation parameter eta (> 0; the paper gives no
+                           value, reading R33); ignored for BR1                   */
 } hbpdc_problem;
 
 typedef struct {

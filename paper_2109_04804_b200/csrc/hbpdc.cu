@@ -113,6 +113,7 @@ struct hbpdc_ctx {
   double *dnrm = nullptr, *deps = nullptr;
   double *Sb = nullptr, *gSb = nullptr;   // BJ^H_ext: sigma at the build point, R1(Wb), and its ghosts
   double *lift0 = nullptr, *lift1 = nullptr;
+  double *liftf0 = nullptr, *liftf1 = nullptr;   // BR2 per-face gradients (NULL: BR1)
   // precond
   double *S = nullptr, *Wb = nullptr, *Z = nullptr;
   double *Kst = nullptr, *KV = nullptr, *KT = nullptr, *tseed = nullptr, *y1 = nullptr, *y2 = nullptr;  // NS
@@ -285,11 +286,13 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {
     // BR1: lift the jet state(s), then (partitioned) exchange the lifted
     // gradients' face traces -- the second halo of the radius-2 stencil
-    CK(launch_lift(k, 0, c->cfg, c->geo, A, c->lift0));
+    CK(launch_lift(k, 0, c->cfg, c->geo, A, c->lift0, c->liftf0));
     A.G0 = c->lift0;
+    A.Gf0 = c->liftf0;
     if (k == OP_JVP_FD) {
-      CK(launch_lift(k, 1, c->cfg, c->geo, A, c->lift1));
+      CK(launch_lift(k, 1, c->cfg, c->geo, A, c->lift1, c->liftf1));
       A.G1 = c->lift1;
+      A.Gf1 = c->liftf1;
     }
     if (c->halo()) {
       const double* s0[1] = {c->lift0};
@@ -1511,6 +1514,11 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     const size_t lg = (size_t)c->nE * 6 * 4 * c->nodes;
     CKS(dalloc(c, &c->lift0, lg));
     CKS(dalloc(c, &c->lift1, lg));
+    if (c->pb.lifting == HBPDC_BR2) {
+      const size_t lf = (size_t)c->nE * 4 * 6 * 4 * c->P;
+      CKS(dalloc(c, &c->liftf0, lf));
+      CKS(dalloc(c, &c->liftf1, lf));
+    }
   }
   void* hp = nullptr;
   CK(cudaMallocHost(&hp, 16 * sizeof(double)));
@@ -1548,6 +1556,13 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
     return bad("Gauss-Legendre nodes with Navier-Stokes: single partition only (the BR1 lifting needs the "
                "traces of g(w), the halo carries those of w)");
   if (!(pb->mach_eps > 0.0)) return bad("mach_eps must be positive");
+  if (pb->lifting != HBPDC_BR1 && pb->lifting != HBPDC_BR2) return bad("lifting must be HBPDC_BR1 or HBPDC_BR2");
+  if (pb->lifting == HBPDC_BR2 && pb->equation == HBPDC_NAVIER_STOKES) {
+    if (!(pb->eta_br2 > 0.0)) return bad("BR2: eta_br2 must be positive");
+    if (pb->nodes != HBPDC_GLL) return bad("BR2 lifting: GLL nodes only");
+    if (c->ds.nranks > 1 || c->ds.force_halo)
+      return bad("BR2 lifting: single partition only (the halo carries node, not face, gradients)");
+  }
   if (pb->equation == HBPDC_NAVIER_STOKES && pb->mach_eps != 1.0)
     return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");
   if (pb->q != 4 && pb->q != 6 && pb->q != 8) return bad("q must be 4, 6 or 8");
@@ -1631,6 +1646,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->cfg.pp.ay = pb->a[1];
   c->cfg.pp.gamma = pb->gamma;
   c->cfg.pp.glf = pb->flux == HBPDC_GLF_PAPER ? 1 : 0;
+  c->cfg.pp.eta_br2 = pb->eta_br2;
   c->cfg.pp.ieps = 1.0 / pb->mach_eps;
   c->cfg.pp.eps2 = pb->mach_eps * pb->mach_eps;
   c->cfg.pp.ieps2 = 1.0 / c->cfg.pp.eps2;

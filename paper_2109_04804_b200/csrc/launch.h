@@ -24,11 +24,14 @@ cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A
 int op_grid(const OpCfg& c, const Geo& g);
 // Gauss-Legendre instantiations (ops_kernels_gl.cu), reached from launch_op / launch_kbuild when g.gl
 cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
-cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout);
+cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout,
+                           double* Gf);
 cudaError_t launch_kbuild_gl(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
                              double c2, double* M, int e0, int ne, const double* Sb, const double* gSb);
 // BR1 lifting of jet state `state` of operator `kind` into Gout
-cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout);
+// Gf (BR2, GLL): also write the per-face gradients [elem][face][6][JetN][P], or NULL (BR1)
+cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout,
+                        double* Gf = nullptr);
 // number of jet components of the lifted gradients of (kind, state)
 int lift_jet_components(OpKind kind, int state);
 // BJ_ext: M_i = I - a1dt K_i + c2 K_i^2 for elements [e0, e0+ne), row-major m x m each

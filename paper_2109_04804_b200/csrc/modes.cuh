@@ -31,7 +31,23 @@ struct OpArgs {
   int m;                // doubles per element
   int nE;               // local elements; e >= nE addresses a ghost element (halo)
   const double *gW, *gS, *gdW, *gdS;   // ghost copies (neighbour ranks' face traces)
+  const double *Gf0, *Gf1;   // NS BR2: per-face gradients of jet states 0 / 1, or NULL (BR1)
 };
+
+// NS BR2 face gradients: [elem][face 4][6][JetN][P] (lift_kernel), face f = 2d + plus,
+// kf the node index along the face
+template <class T>
+__device__ __forceinline__ void load_face_grads(const double* Gf, int e, int f, int kf, int P, T* gx, T* gy) {
+  constexpr int JN = JetN<T>::value;
+  const double* base = Gf + ((size_t)e * 4 + f) * 6 * JN * P + kf;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    double c[JN];
+#pragma unroll
+    for (int q = 0; q < JN; ++q) c[q] = base[(k * JN + q) * P];
+    if (k < 3) gx[k] = jmake<T>(c); else gy[k - 3] = jmake<T>(c);
+  }
+}
 
 __device__ __forceinline__ double fd_step(const OpArgs& A) { return A.d_epsw ? *A.d_epsw : A.epsw; }
 
@@ -101,6 +117,13 @@ struct OneJetMode {
     const int le = use_own ? e : nb;
     trace_load(g, use_own ? own : nnode, d, st,
                [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); }, le >= A.nE);
+    if constexpr (EQ == 2) {
+      if (A.Gf0) {                   // BR2: the face's own local-lifting gradient (reading R33)
+        const int f = 2 * d + (use_own ? (plus ? 1 : 0) : (plus ? 0 : 1));
+        const int kf = d == 0 ? own / g.P : own % g.P;
+        load_face_grads<J>(A.Gf0, le, f, kf, g.P, st.s.gx, st.s.gy);
+      }
+    }
     half_flux<EQ, J>(pp, st.s, d, raw, rs);
   }
   __device__ static void face_combine(const Args& A, const PhysParams& pp, int d, const double* rL,
@@ -338,6 +361,13 @@ template <int EQ, int NODES> struct ModeJvpFD {
         load_w<0>(A, nb, nd, s.w, true);
         ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, nb, nd, s);
       }, nb >= A.nE);
+      if constexpr (EQ == 2) {
+        if (A.Gf0) {
+          const int kf = d == 0 ? own / g.P : own % g.P;
+          load_face_grads<J1>(A.Gf0, e, 2 * d + (plus ? 1 : 0), kf, g.P, so.gx, so.gy);
+          load_face_grads<J1>(A.Gf0, nb, 2 * d + (plus ? 0 : 1), kf, g.P, sn.gx, sn.gy);
+        }
+      }
       J1 fp[NV];
       if (plus) face_flux<EQ>(pp, so, sn, d, fp);
       else face_flux<EQ>(pp, sn, so, d, fp);
@@ -352,6 +382,13 @@ template <int EQ, int NODES> struct ModeJvpFD {
         load_w<1>(A, nb, nd, s.w, true);
         ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, nb, nd, s);
       }, nb >= A.nE);
+      if constexpr (EQ == 2) {
+        if (A.Gf1) {
+          const int kf = d == 0 ? own / g.P : own % g.P;
+          load_face_grads<J2>(A.Gf1, e, 2 * d + (plus ? 1 : 0), kf, g.P, so.gx, so.gy);
+          load_face_grads<J2>(A.Gf1, nb, 2 * d + (plus ? 0 : 1), kf, g.P, sn.gx, sn.gy);
+        }
+      }
       J2 fq[NV];
       if (plus) face_flux<EQ>(pp, so, sn, d, fq);
       else face_flux<EQ>(pp, sn, so, d, fq);

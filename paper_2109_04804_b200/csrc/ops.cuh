@@ -478,7 +478,7 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g) 
 // Computed for jet state K of the mode; result [elem][6][JetN][NODES].
 template <int P, class Mode, int K, int EPB, bool GL>
 __global__ void __launch_bounds__(EPB * P * P)
-lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g, double* Gout) {
+lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g, double* Gout, double* Gf) {
   using T = typename Mode::template StateT<K>;
   constexpr int NODES = P * P, PS = P + 1, PLANE = P * PS;
   constexpr int JN = JetN<T>::value;
@@ -541,7 +541,13 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
         }
       }
     }
-  } else if (active) {
+  }
+  T gsd[2][3];                       // GLL: g* on this node's x / y face (BR2 face gradients)
+#pragma unroll
+  for (int d = 0; d < 2; ++d)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gsd[d][k] = jconst<T>(0.0);
+  if (!GL && active) {
     T w[4], gv[3];
     Mode::template load_w<K>(A, e, node, w, false);
     grad_vars(pp, w, gv);
@@ -562,12 +568,47 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           const T gs = side > 0 ? 0.5 * (gv[k] + gn[k]) : 0.5 * (gn[k] + gv[k]);
+          gsd[d][k] = gs;
           if (d == 0) sx_[k] = sx_[k] + s * gs; else sy_[k] = sy_[k] + s * gs;
         }
       }
     }
   }
   __syncthreads();
+  if constexpr (!GL) {
+    // BR2 (reading R33): on each face of this edge node, the strong-form gradient
+    // (2/h) D g (D = Dhat + M^-1 B) plus, in the normal component, eta (2/h) (+-) lhat (g* - g)
+    if (Gf && active) {
+#pragma unroll 1
+      for (int d = 0; d < 2; ++d) {
+        const int kk = d == 0 ? i : j;
+        if (kk != P - 1 && kk != 0) continue;
+        const int side = kk == P - 1 ? +1 : -1;
+        double* fo = Gf + ((size_t)e * 4 + 2 * d + (side > 0 ? 1 : 0)) * 6 * JN * P + (d == 0 ? j : i);
+        const double sd = d == 0 ? g.sx : g.sy;
+        const double lj = side > 0 ? g.lhp : -g.lhm;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int q = 0; q < JN; ++q) {
+            const double* row = sg + (k * JN + q) * PLANE;
+            const double gown = row[j * PS + i];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int ic = c == 0 ? i : j;
+              double a = 0.0;
+#pragma unroll
+              for (int l = 0; l < P; ++l) a = fma(g.Dh[ic * P + l], c == 0 ? row[j * PS + l] : row[l * PS + i], a);
+              if (ic == P - 1) a = fma(g.lhp, gown, a);
+              if (ic == 0) a = fma(-g.lhm, gown, a);
+              double v = (c == 0 ? g.sx : g.sy) * a;
+              if (c == d) v = fma(pp.eta_br2 * sd * lj, jget(gsd[d][k], q) - gown, v);
+              fo[((c * 3 + k) * JN + q) * P] = v;
+            }
+          }
+      }
+    }
+  }
   if (active) {
     double* out = Gout + (size_t)e * 6 * JN * NODES + node;
 #pragma unroll

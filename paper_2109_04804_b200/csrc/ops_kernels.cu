@@ -39,12 +39,12 @@ static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
 }
 
 template <int P, class Mode, int K>
-static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
+static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, double* G, double* Gf) {
   constexpr int NODES = P * P;
   constexpr int EPB = epb_for(NODES);
   const int grid = (g.nE + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
-  lift_kernel<P, Mode, K, EPB, kGL><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G);
+  lift_kernel<P, Mode, K, EPB, kGL><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G, Gf);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -250,16 +250,16 @@ template <int EQ, int DIM, int P> struct Disp {
       default: return cudaErrorInvalidValue;
     }
   }
-  static cudaError_t lift(OpKind k, int s, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
+  static cudaError_t lift(OpKind k, int s, const OpCfg& c, const Geo& g, const OpArgs& A, double* G, double* Gf) {
     if constexpr (EQ == 2 && DIM == 2) {
       switch (k) {
-        case OP_R1: case OP_R1ABS: return run_lift<P, ModeR1<EQ, NODES>, 0>(c, g, A, G);
-        case OP_R12: return run_lift<P, ModeR12<EQ, NODES>, 0>(c, g, A, G);
-        case OP_RESID: return run_lift<P, ModeResid<EQ, NODES>, 0>(c, g, A, G);
-        case OP_JVP_EXACT: return run_lift<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, G);
+        case OP_R1: case OP_R1ABS: return run_lift<P, ModeR1<EQ, NODES>, 0>(c, g, A, G, Gf);
+        case OP_R12: return run_lift<P, ModeR12<EQ, NODES>, 0>(c, g, A, G, Gf);
+        case OP_RESID: return run_lift<P, ModeResid<EQ, NODES>, 0>(c, g, A, G, Gf);
+        case OP_JVP_EXACT: return run_lift<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, G, Gf);
         case OP_JVP_FD:
-          return s == 0 ? run_lift<P, ModeJvpFD<EQ, NODES>, 0>(c, g, A, G)
-                        : run_lift<P, ModeJvpFD<EQ, NODES>, 1>(c, g, A, G);
+          return s == 0 ? run_lift<P, ModeJvpFD<EQ, NODES>, 0>(c, g, A, G, Gf)
+                        : run_lift<P, ModeJvpFD<EQ, NODES>, 1>(c, g, A, G, Gf);
         default: return cudaErrorInvalidValue;
       }
     }
@@ -287,8 +287,9 @@ static cudaError_t dispatch(const OpCfg& c, F&& f) {
 }
 
 #if HBPDC_OPS_GL
-cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
-  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G); });
+cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G,
+                           double* Gf) {
+  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G, Gf); });
 }
 
 cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
@@ -311,9 +312,10 @@ cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A
   return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
 }
 
-cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G) {
-  if (g.gl) return launch_lift_gl(kind, state, c, g, A, G);
-  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G); });
+cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G,
+                        double* Gf) {
+  if (g.gl) return launch_lift_gl(kind, state, c, g, A, G, Gf);
+  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G, Gf); });
 }
 
 int lift_jet_components(OpKind kind, int state) {

@@ -21,6 +21,7 @@ struct PhysParams {
   double mu, lamT, Rgas; // NS: viscosity, heat conductivity c_p mu / Pr, R = 1/gamma
   int glf;               // 1: the paper's global LF flux (Lambda = diag(1/eps,1,1,1/eps)), 0: LLF
   double ieps, eps2, ieps2;   // reference Mach number eps of eq:Euler: 1/eps, eps^2, 1/eps^2
+  double eta_br2;        // NS BR2 lifting: eta (face gradients, lift_kernel)
 };
 
 template <int EQ> struct NVars { static constexpr int value = 4; };

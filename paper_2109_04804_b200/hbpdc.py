@@ -42,7 +42,7 @@ class Problem(ctypes.Structure):
                 ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("xmin", ctypes.c_double),
                 ("xmax", ctypes.c_double), ("ymin", ctypes.c_double), ("ymax", ctypes.c_double),
                 ("flux", ctypes.c_int), ("lifting", ctypes.c_int), ("q", ctypes.c_int),
-                ("kmax", ctypes.c_int)]
+                ("kmax", ctypes.c_int), ("eta_br2", ctypes.c_double)]
 
 
 class SolverOpts(ctypes.Structure):
@@ -185,14 +185,15 @@ class Context:
                  restart=700, max_krylov=7000, precond="bjext", precond_policy="per_step_per_alpha",
                  jvp_mode="auto", batch_stages=True, gmres_sstep=1, rank=0, nranks=1, px=1, py=1, nccl_id=None, stream=None, device=0,
                  comm="auto", loopback=None, force_halo=False, flux="llf", mach=1.0, schur=False,
-                 nodes="gll"):
+                 nodes="gll", lifting="br1", eta_br2=2.0):
         import torch
         self.lib = load()
         if not torch.cuda.is_available():
             raise RuntimeError("hbpdc needs a CUDA device (no CPU fallback)")
         pb = Problem(dim=dim, equation=_EQ[equation], gamma=gamma, mach_eps=mach, mu=mu, prandtl=prandtl,
                      N=N, nodes={"gll": GLL, "gl": GL}[nodes], nx=nx, ny=ny, xmin=bounds[0], xmax=bounds[1], ymin=bounds[2],
-                     ymax=bounds[3], flux={"llf": 0, "glf": 1}[flux], lifting=0, q=q, kmax=kmax)
+                     ymax=bounds[3], flux={"llf": 0, "glf": 1}[flux], lifting={"br1": 0, "br2": 1}[lifting],
+                     q=q, kmax=kmax, eta_br2=eta_br2)
         pb.a[0], pb.a[1] = a[0], a[1]
         op = SolverOpts(newton_rtol=newton_rtol, newton_atol_dw=newton_atol_dw, newton_floor=newton_floor,
                         newton_max=newton_max, gmres_rtol=gmres_rtol, gmres_restart=restart,

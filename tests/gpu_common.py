@@ -17,7 +17,8 @@ def make_pair(kind, N, nx, ny=None, bounds=(0.0, 1.0, 0.0, 1.0), a=(1.0, 1.0), m
     """(oracle Disc, GPU Context) for the same problem."""
     from paper_2109_04804_b200 import hbpdc
     dim = 1 if ny is None else 2
-    eq = physics.Equation(kind, a=tuple(a), mu=mu, numflux=ctx_kw.get("flux", "llf"), mach=ctx_kw.get("mach", 1.0))
+    eq = physics.Equation(kind, a=tuple(a), mu=mu, numflux=ctx_kw.get("flux", "llf"), mach=ctx_kw.get("mach", 1.0),
+                          lifting=ctx_kw.get("lifting", "br1"), eta_br2=ctx_kw.get("eta_br2", 2.0))
     d = dgsem.Disc(basis.build_basis(N, ctx_kw.get("nodes", "gll")), dgsem.Mesh(dim, nx, ny or 1, *bounds), eq)
     ctx = hbpdc.Context(dim=dim, equation=kind, N=N, nx=nx, ny=ny or 1, bounds=bounds, a=a, mu=mu, q=q,
                         kmax=kmax, **ctx_kw)
