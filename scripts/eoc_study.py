@@ -14,6 +14,8 @@ EOC = log2(e(dt) / e(dt/2)), expected min(4 + k_max, q).
 Tolerances as the paper's convergence runs: GMRES 1e-5, Newton 1e-12.
 
     python scripts/eoc_study.py > profiles/<round>/eoc_study.md
+    python scripts/eoc_study.py --nodes gl --flux glf > profiles/<round>/eoc_study_gl.md
+      (the paper's own discretisation: Gauss-Legendre nodes P:176, global LF flux P:197-201)
 """
 import math
 import os
@@ -45,10 +47,13 @@ def l2_error(kind, ctx, W, t):
     return float(np.linalg.norm(W - ref) / np.linalg.norm(ref))
 
 
+NODES, FLUX = "gll", "llf"
+
+
 def run(kind, q, kmax, nsteps, N=7, ne=32):
     ctx = hbpdc.Context(dim=2, equation=kind, N=N, nx=ne, ny=ne, bounds=(-1.0, 1.0, -1.0, 1.0),
                         a=(A, A), q=q, kmax=kmax, newton_rtol=1e-12, gmres_rtol=1e-5, restart=700,
-                        max_krylov=7000, precond="bjext", gmres_sstep=1)
+                        max_krylov=7000, precond="bjext", gmres_sstep=1, nodes=NODES, flux=FLUX)
     X, Y = ctx.node_coords()
     W = torch.tensor(inputs.layout(exact(kind, X, Y, 0.0), 2), dtype=torch.float64, device="cuda")
     dt = T_END / nsteps
@@ -61,9 +66,17 @@ def run(kind, q, kmax, nsteps, N=7, ne=32):
 
 
 def main():
+    global NODES, FLUX
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nodes", default="gll", choices=["gll", "gl"])
+    ap.add_argument("--flux", default="llf", choices=["llf", "glf"])
+    args = ap.parse_args()
+    NODES, FLUX = args.nodes, args.flux
     print("# NEXT-3: temporal EOC of HBPC(q, k_max) on the GPU (`scripts/eoc_study.py`)\n")
-    print(f"T = {T_END}, 32^2 elements, N = 7 (GLL), BJ_ext, GMRES 1e-5 / Newton 1e-12; relative L2 "
-          "error at the nodes vs the exact solution; EOC = log2 of successive error ratios.\n")
+    print(f"T = {T_END}, 32^2 elements, N = 7 ({NODES.upper()} nodes, {FLUX.upper()} flux), BJ_ext, GMRES 1e-5 / "
+          "Newton 1e-12; relative L2 error at the nodes vs the exact solution; EOC = log2 of successive "
+          "error ratios.\n")
     schemes = [(4, 0), (6, 2), (6, 0), (8, 4), (8, 0)]
     steps = {4: [4, 8, 16, 32], 6: [2, 4, 8, 16], 8: [2, 4, 8]}
     for kind in ("advection", "euler"):
