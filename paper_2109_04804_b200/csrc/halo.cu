@@ -27,6 +27,7 @@ struct HaloArgs {
   size_t total;
   int gl;
   double lp[8], lm[8];
+  int facebuf;          // BR2 face-gradient buffers [elem][face 4][nv][P]: send face s, fill ghost face s^1
 };
 
 __device__ __forceinline__ int face_node(int s, int k, int P, int dim) {
@@ -69,6 +70,10 @@ __global__ void halo_pack_kernel(HaloArgs H, double* __restrict__ send) {
       case 2: e = p; break;
       default: e = (H.ny - 1) * H.nx + p; break;
     }
+    if (H.facebuf) {
+      send[flat] = H.src[f][(((size_t)e * 4 + s) * H.nv + v) * H.P + k];
+      continue;
+    }
     const double* base = H.src[f] + (size_t)e * H.m + v * H.nodes;
     if (H.gl) {
       // trace on face s: line through face node k across the element (x-sides: row k, y-sides: column k)
@@ -98,7 +103,10 @@ __global__ void halo_unpack_kernel(HaloArgs H, const double* __restrict__ recv) 
       default: gi = 2 * H.ny + H.nx + p; break;
     }
     // the neighbour across side s touches us with its face s ^ 1
-    H.dst[f][(size_t)gi * H.m + v * H.nodes + face_node(s ^ 1, k, H.P, H.dim)] = recv[flat];
+    if (H.facebuf)
+      H.dst[f][(((size_t)gi * 4 + (s ^ 1)) * H.nv + v) * H.P + k] = recv[flat];
+    else
+      H.dst[f][(size_t)gi * H.m + v * H.nodes + face_node(s ^ 1, k, H.P, H.dim)] = recv[flat];
   }
 }
 
@@ -133,9 +141,10 @@ void halo_segments(const HaloLayout& L, int nf, size_t off[4], size_t len[4], in
 }
 
 cudaError_t launch_halo_pack(const HaloLayout& L, int nf, const double* const* src, double* send,
-                             cudaStream_t st, int nvf) {
+                             cudaStream_t st, int nvf, bool facebuf) {
   if (nf < 1 || nf > HALO_MAX_FIELDS) return cudaErrorInvalidValue;
   HaloArgs H = make_args(L, nf, nvf);
+  H.facebuf = facebuf;
   for (int f = 0; f < nf; ++f) H.src[f] = src[f];
   if (H.total == 0) return cudaSuccess;
   const int grid = (int)std::min<size_t>((H.total + 255) / 256, 1184);
@@ -145,9 +154,10 @@ cudaError_t launch_halo_pack(const HaloLayout& L, int nf, const double* const* s
 }
 
 cudaError_t launch_halo_unpack(const HaloLayout& L, int nf, const double* recv, double* const* dst,
-                               cudaStream_t st, int nvf) {
+                               cudaStream_t st, int nvf, bool facebuf) {
   if (nf < 1 || nf > HALO_MAX_FIELDS) return cudaErrorInvalidValue;
   HaloArgs H = make_args(L, nf, nvf);
+  H.facebuf = facebuf;
   for (int f = 0; f < nf; ++f) H.dst[f] = dst[f];
   if (H.total == 0) return cudaSuccess;
   const int grid = (int)std::min<size_t>((H.total + 255) / 256, 1184);

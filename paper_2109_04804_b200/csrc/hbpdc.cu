@@ -139,6 +139,7 @@ struct hbpdc_ctx {
   HaloLayout hl{};
   double *gW = nullptr, *gS = nullptr, *gdW = nullptr, *gdS = nullptr, *gWb = nullptr;  // ghosts
   double *gG0 = nullptr, *gG1 = nullptr;                  // NS: ghost lifted gradients (second halo)
+  double *gGf0 = nullptr, *gGf1 = nullptr;                // NS BR2: ghost face gradients
   double *hsend = nullptr, *hrecv = nullptr;
   bool halo() const { return hl.active[0] || hl.active[2]; }
   int debug_sync = 0;              // HBPDC_DEBUG_SYNC=1: synchronise + check after every launch group
@@ -241,16 +242,17 @@ hbpdc_status allreduce(hbpdc_ctx* c, double* d, int n) {
 }
 
 // halo exchange of nf fields into their ghost copies
-hbpdc_status halo_exchange(hbpdc_ctx* c, int nf, const double* const* src, double* const* dst, int nvf = 0) {
+hbpdc_status halo_exchange(hbpdc_ctx* c, int nf, const double* const* src, double* const* dst, int nvf = 0,
+                           bool facebuf = false) {
   size_t off[4], len[4];
   halo_segments(c->hl, nf, off, len, nvf);
-  CK(launch_halo_pack(c->hl, nf, src, c->hsend, c->stream, nvf));
+  CK(launch_halo_pack(c->hl, nf, src, c->hsend, c->stream, nvf, facebuf));
   CKS(dbg_sync(c, "halo pack"));
   std::string e;
   if (c->comm->halo(c->hsend, c->hrecv, off, len, c->nbr, c->hl.active, c->stream, e))
     return fail(c, HBPDC_E_NCCL, e);
   CKS(dbg_sync(c, "halo transport"));
-  CK(launch_halo_unpack(c->hl, nf, c->hrecv, dst, c->stream, nvf));
+  CK(launch_halo_unpack(c->hl, nf, c->hrecv, dst, c->stream, nvf, facebuf));
   CKS(dbg_sync(c, "halo unpack"));
   return HBPDC_OK;
 }
@@ -299,11 +301,23 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
       double* d0[1] = {c->gG0};
       CKS(halo_exchange(c, 1, s0, d0, 6 * lift_jet_components(k, 0)));
       A.gG0 = c->gG0;
+      if (c->liftf0) {        // BR2: the neighbours' face gradients on the shared faces
+        const double* f0[1] = {c->liftf0};
+        double* g0[1] = {c->gGf0};
+        CKS(halo_exchange(c, 1, f0, g0, 6 * lift_jet_components(k, 0), true));
+        A.gGf0 = c->gGf0;
+      }
       if (k == OP_JVP_FD) {
         const double* s1[1] = {c->lift1};
         double* d1[1] = {c->gG1};
         CKS(halo_exchange(c, 1, s1, d1, 6 * lift_jet_components(k, 1)));
         A.gG1 = c->gG1;
+        if (c->liftf1) {
+          const double* f1[1] = {c->liftf1};
+          double* g1[1] = {c->gGf1};
+          CKS(halo_exchange(c, 1, f1, g1, 6 * lift_jet_components(k, 1), true));
+          A.gGf1 = c->gGf1;
+        }
       }
     }
   }
@@ -1504,6 +1518,11 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
       const size_t ngg = (size_t)(c->pb.dim == 2 ? 2 * (c->nxl + c->nyl) : 2) * 6 * 4 * c->nodes;
       CKS(dalloc(c, &c->gG0, ngg));
       CKS(dalloc(c, &c->gG1, ngg));
+      if (c->pb.lifting == HBPDC_BR2) {
+        const size_t ngf = (size_t)2 * (c->nxl + c->nyl) * 4 * 6 * 4 * c->P;
+        CKS(dalloc(c, &c->gGf0, ngf));
+        CKS(dalloc(c, &c->gGf1, ngf));
+      }
       halo_segments(c->hl, 1, off, len, 6 * 4);          // lifted gradients, hyper-dual jets
       hb = std::max(hb, off[3] + len[3]);
     }
@@ -1560,8 +1579,6 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->lifting == HBPDC_BR2 && pb->equation == HBPDC_NAVIER_STOKES) {
     if (!(pb->eta_br2 > 0.0)) return bad("BR2: eta_br2 must be positive");
     if (pb->nodes != HBPDC_GLL) return bad("BR2 lifting: GLL nodes only");
-    if (c->ds.nranks > 1 || c->ds.force_halo)
-      return bad("BR2 lifting: single partition only (the halo carries node, not face, gradients)");
   }
   if (pb->equation == HBPDC_NAVIER_STOKES && pb->mach_eps != 1.0)
     return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");

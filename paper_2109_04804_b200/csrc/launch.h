@@ -127,10 +127,11 @@ struct HaloLayout {
 // (nvf: variables per element of each field; 0 = the state's n_v)
 void halo_segments(const HaloLayout& L, int nf, size_t off[4], size_t len[4], int nvf = 0);
 // send <- boundary-node values of src[0..nf) ; dst[f] ghost elements <- recv
+// facebuf: the fields are BR2 face-gradient buffers [elem][face 4][nvf][P] (send face s, fill ghost face s^1)
 cudaError_t launch_halo_pack(const HaloLayout& L, int nf, const double* const* src, double* send, cudaStream_t st,
-                             int nvf = 0);
+                             int nvf = 0, bool facebuf = false);
 cudaError_t launch_halo_unpack(const HaloLayout& L, int nf, const double* recv, double* const* dst, cudaStream_t st,
-                               int nvf = 0);
+                               int nvf = 0, bool facebuf = false);
 // out = c / sqrt(*sum), or 0 if *sum == 0
 cudaError_t launch_fd_eps_from_sum(const double* sum, double c, double* out, cudaStream_t st);
 

@@ -32,13 +32,16 @@ struct OpArgs {
   int nE;               // local elements; e >= nE addresses a ghost element (halo)
   const double *gW, *gS, *gdW, *gdS;   // ghost copies (neighbour ranks' face traces)
   const double *Gf0, *Gf1;   // NS BR2: per-face gradients of jet states 0 / 1, or NULL (BR1)
+  const double *gGf0, *gGf1; // their ghost copies (the neighbour ranks' shared faces)
 };
 
 // NS BR2 face gradients: [elem][face 4][6][JetN][P] (lift_kernel), face f = 2d + plus,
 // kf the node index along the face
 template <class T>
-__device__ __forceinline__ void load_face_grads(const double* Gf, int e, int f, int kf, int P, T* gx, T* gy) {
+__device__ __forceinline__ void load_face_grads(const double* Gf, const double* gGf, int nE, int e, int f, int kf,
+                                                int P, T* gx, T* gy) {
   constexpr int JN = JetN<T>::value;
+  if (e >= nE) { Gf = gGf; e -= nE; }          // ghost element (halo.cu facebuf exchange)
   const double* base = Gf + ((size_t)e * 4 + f) * 6 * JN * P + kf;
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
@@ -121,7 +124,7 @@ struct OneJetMode {
       if (A.Gf0) {                   // BR2: the face's own local-lifting gradient (reading R33)
         const int f = 2 * d + (use_own ? (plus ? 1 : 0) : (plus ? 0 : 1));
         const int kf = d == 0 ? own / g.P : own % g.P;
-        load_face_grads<J>(A.Gf0, le, f, kf, g.P, st.s.gx, st.s.gy);
+        load_face_grads<J>(A.Gf0, A.gGf0, A.nE, le, f, kf, g.P, st.s.gx, st.s.gy);
       }
     }
     half_flux<EQ, J>(pp, st.s, d, raw, rs);
@@ -364,8 +367,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
       if constexpr (EQ == 2) {
         if (A.Gf0) {
           const int kf = d == 0 ? own / g.P : own % g.P;
-          load_face_grads<J1>(A.Gf0, e, 2 * d + (plus ? 1 : 0), kf, g.P, so.gx, so.gy);
-          load_face_grads<J1>(A.Gf0, nb, 2 * d + (plus ? 0 : 1), kf, g.P, sn.gx, sn.gy);
+          load_face_grads<J1>(A.Gf0, A.gGf0, A.nE, e, 2 * d + (plus ? 1 : 0), kf, g.P, so.gx, so.gy);
+          load_face_grads<J1>(A.Gf0, A.gGf0, A.nE, nb, 2 * d + (plus ? 0 : 1), kf, g.P, sn.gx, sn.gy);
         }
       }
       J1 fp[NV];
@@ -385,8 +388,8 @@ template <int EQ, int NODES> struct ModeJvpFD {
       if constexpr (EQ == 2) {
         if (A.Gf1) {
           const int kf = d == 0 ? own / g.P : own % g.P;
-          load_face_grads<J2>(A.Gf1, e, 2 * d + (plus ? 1 : 0), kf, g.P, so.gx, so.gy);
-          load_face_grads<J2>(A.Gf1, nb, 2 * d + (plus ? 0 : 1), kf, g.P, sn.gx, sn.gy);
+          load_face_grads<J2>(A.Gf1, A.gGf1, A.nE, e, 2 * d + (plus ? 1 : 0), kf, g.P, so.gx, so.gy);
+          load_face_grads<J2>(A.Gf1, A.gGf1, A.nE, nb, 2 * d + (plus ? 0 : 1), kf, g.P, sn.gx, sn.gy);
         }
       }
       J2 fq[NV];

@@ -92,9 +92,75 @@ def test_br2_end_of_run():
     assert rel(to_np(Wg), Wo) <= 1e-8
 
 
-def test_br2_rejects_gl_and_partitions():
+def test_br2_rejects_gl():
     from paper_2109_04804_b200 import hbpdc
     with pytest.raises(Exception, match="GLL"):
         hbpdc.Context(dim=2, equation="navier_stokes", N=3, nx=4, ny=4, mu=0.01, lifting="br2", nodes="gl")
-    with pytest.raises(Exception, match="single partition"):
-        hbpdc.Context(dim=2, equation="navier_stokes", N=3, nx=4, ny=4, mu=0.01, lifting="br2", force_halo=True)
+
+
+@pytest.mark.parametrize("px,py", [(2, 2), (2, 1)])
+def test_br2_loopback_operators_bitwise(px, py):
+    """BR2 across loopback ranks: the neighbour ranks' face gradients arrive by the
+    face-buffer halo and every rank's operator output equals its block of the
+    single-rank result bit for bit; one HBPC(4,0) step <= 1e-10 vs one rank."""
+    import torch
+    from paper_2109_04804_b200 import hbpdc
+    from test_gpu_partition import _block, _run_threads
+    N, nx, ny, eta = 2, 6, 6, 2.0
+    d, ctx1 = _pair(N, nx, ny, eta)
+    W = ns_ic(d, SEED + 101)
+    sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 102))
+    dW = inputs.random_field(d.n, SEED + 103, unit_norm=True)
+    ds = inputs.random_field(d.n, SEED + 104, unit_norm=True)
+    a1, a2, dt = 1 / 6, 1 / 54, 0.02
+    eps = implicit.fd_eps(dW)
+
+    def ops(ctx, blk):
+        Wg, sg, dWg, dsg = (to_gpu(blk(x)) for x in (W, sig, dW, ds))
+        torch.cuda.synchronize()
+        out = {"R1": ctx.rhs(Wg), "R2": ctx.rhs(Wg, sg),
+               "exact": ctx.jvp(a1, a2, dt, Wg, sg, dWg, dsg, mode="exact"),
+               "fd": ctx.jvp(a1, a2, dt, Wg, sg, dWg, dsg, mode="fd", eps_override=(eps, None))}
+        ctx.precond_build(a1, a2, dt, Wg)
+        out["pc"] = ctx.precond_apply(dWg, dsg)
+        torch.cuda.synchronize()
+        return {k: (np.concatenate([to_np(x) for x in v]) if isinstance(v, tuple) else to_np(v))
+                for k, v in out.items()}
+
+    ref = ops(ctx1, lambda x: x)
+    assert rel(ref["R1"], dgsem.rhs1(d, W)) <= 1e-11
+    group = hbpdc.LoopbackGroup(px * py)
+    ctxs = [hbpdc.Context(dim=2, equation="navier_stokes", N=N, nx=nx, ny=ny, bounds=(0.0, TWO_PI, 0.0, TWO_PI),
+                          a=(1.0, -0.6), mu=0.05, lifting="br2", eta_br2=eta, q=4, kmax=0, gmres_rtol=1e-10,
+                          newton_rtol=1e-10, rank=r, nranks=px * py, px=px, py=py, comm="loopback",
+                          loopback=group, stream=torch.cuda.Stream())
+            for r in range(px * py)]
+    try:
+        def blk_of(c):
+            return lambda x: _block(x, 2, nx, ny, d.m, c.ex0, c.ey0, c.nx_local, c.ny_local)
+        outs = _run_threads([lambda c=c: ops(c, blk_of(c)) for c in ctxs])
+        for c, o in zip(ctxs, outs):
+            blk = blk_of(c)
+            for key, r in ref.items():
+                rb = np.concatenate([blk(r[:d.n]), blk(r[d.n:])]) if r.size == 2 * d.n else blk(r)
+                assert np.array_equal(o[key], rb), (key, c.rank, np.abs(o[key] - rb).max())
+        # one step, partitioned vs single rank
+        _, c1 = _pair(N, nx, ny, eta, q=4, kmax=0, gmres_rtol=1e-10, newton_rtol=1e-10)
+        W0 = ns_ic(d, SEED + 105, rel_noise=1e-3)
+        W1 = to_gpu(W0)
+        c1.step(0.004, W1)
+        W1 = to_np(W1)
+
+        def run(c):
+            Wl = to_gpu(blk_of(c)(W0))
+            torch.cuda.synchronize()
+            c.step(0.004, Wl)
+            torch.cuda.synchronize()
+            return to_np(Wl)
+        outs = _run_threads([lambda c=c: run(c) for c in ctxs])
+        for c, Wl in zip(ctxs, outs):
+            assert rel(Wl, blk_of(c)(W1)) <= 1e-10, (c.rank, rel(Wl, blk_of(c)(W1)))
+    finally:
+        for c in ctxs:
+            c.close()
+        group.close()
