@@ -78,8 +78,7 @@ typedef struct {
   double xmin, xmax, ymin, ymax;   /* periodic Cartesian domain                   */
   int flux;             /* HBPDC_LLF (reading R3) | HBPDC_GLF_PAPER (eq:Riemann, P:197-201:
                            constant Lambda = diag(1/eps,1,1,1/eps), eps = 1; |a.n| for advection) */
-  int lifting;          /* HBPDC_BR1 (NS, reading R19) | HBPDC_BR2 (reading R33;
-                           GLL nodes)                                             */
+  int lifting;          /* HBPDC_BR1 (NS, reading R19) | HBPDC_BR2 (reading R33) */
   int q, kmax;          /* HBPC(q, k_max), q in {4, 6, 8}, k_max >= 0              */
   double eta_br2;       /* BR2 stabilisation parameter eta (> 0; the paper gives no
                            value, reading R33); ignored for BR1                   */

@@ -30,6 +30,8 @@ struct Basis1D {
   double lhp, lhm;                    // GLL: lhat_N(+1) = 1/w_N, lhat_0(-1) = 1/w_0
   std::vector<double> lp, lm;         // l_i(+1), l_i(-1)
   std::vector<double> lhpv, lhmv;     // lhat_i(+1), lhat_i(-1)
+  std::vector<double> D;              // D_ij = l_j'(x_i), row-major
+  std::vector<double> dlp, dlm;       // l_j'(+1), l_j'(-1)  (edge derivatives, BR2 on GL)
 };
 
 // barycentric weights, D_ij = l_j'(x_i), edge values and Dhat of a node set
@@ -58,6 +60,13 @@ static void finish_basis(Basis1D& b, const std::vector<long double>& x, const st
     b.xi[i] = (double)x[i]; b.w[i] = (double)w[i];
     b.lp[i] = (double)lp[i]; b.lm[i] = (double)lm[i];
     b.lhpv[i] = (double)(lp[i] / w[i]); b.lhmv[i] = (double)(lm[i] / w[i]);
+  }
+  b.D.resize(n * n); b.dlp.resize(n); b.dlm.resize(n);
+  for (int i = 0; i < n * n; ++i) b.D[i] = (double)D[i];
+  for (int j = 0; j < n; ++j) {                       // l_j'(+-1) = sum_i l_i(+-1) D_ij (exact for degree N)
+    long double a = 0.0L, c = 0.0L;
+    for (int i = 0; i < n; ++i) { a += lp[i] * D[i * n + j]; c += lm[i] * D[i * n + j]; }
+    b.dlp[j] = (double)a; b.dlm[j] = (double)c;
   }
   b.lhp = (double)(1.0L / w[N]);
   b.lhm = (double)(1.0L / w[0]);

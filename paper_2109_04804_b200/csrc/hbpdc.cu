@@ -22,6 +22,8 @@ struct Basis1D {
   double lhp, lhm;
   std::vector<double> lp, lm;
   std::vector<double> lhpv, lhmv;
+  std::vector<double> D;
+  std::vector<double> dlp, dlm;
 };
 Basis1D gll_basis(int N);
 Basis1D gl_basis(int N);
@@ -1578,7 +1580,6 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->lifting != HBPDC_BR1 && pb->lifting != HBPDC_BR2) return bad("lifting must be HBPDC_BR1 or HBPDC_BR2");
   if (pb->lifting == HBPDC_BR2 && pb->equation == HBPDC_NAVIER_STOKES) {
     if (!(pb->eta_br2 > 0.0)) return bad("BR2: eta_br2 must be positive");
-    if (pb->nodes != HBPDC_GLL) return bad("BR2 lifting: GLL nodes only");
   }
   if (pb->equation == HBPDC_NAVIER_STOKES && pb->mach_eps != 1.0)
     return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");
@@ -1642,6 +1643,14 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   for (int i = 0; i < c->P; ++i) { c->hl.lp[i] = c->basis.lp[i]; c->hl.lm[i] = c->basis.lm[i]; }
   c->geo.P = c->P;
   c->geo.dim = pb->dim;
+  for (int i = 0; i < c->P * c->P; ++i) c->geo.D[i] = c->basis.D[i];
+  c->geo.cp = c->geo.cm = 0.0;
+  for (int i = 0; i < c->P; ++i) {
+    c->geo.dlp[i] = c->basis.dlp[i];
+    c->geo.dlm[i] = c->basis.dlm[i];
+    c->geo.cp += c->basis.lp[i] * c->basis.lhpv[i];
+    c->geo.cm += c->basis.lm[i] * c->basis.lhmv[i];
+  }
   for (int i = 0; i < c->P; ++i) {
     c->geo.lp[i] = c->basis.lp[i];
     c->geo.lm[i] = c->basis.lm[i];

@@ -34,6 +34,9 @@ struct Geo {
   int gl, P, dim;          // gl: Gauss-Legendre nodes (no node on the element edge)
   double lp[8], lm[8];     // GL: l_i(+1), l_i(-1)  (traces)
   double lhpv[8], lhmv[8]; // GL: lhat_i(+1), lhat_i(-1)  (surface terms, eq:DGSEM_wt)
+  double D[64];            // GL BR2: strong-form D_ij = l_j'(x_i)
+  double dlp[8], dlm[8];   // GL BR2: l_j'(+1), l_j'(-1)
+  double cp, cm;           // GL BR2: sum_i l_i(+-1) lhat_i(+-1)
 };
 
 // Node set selected at compile time (the GL kernels are a separate instantiation,
@@ -538,6 +541,36 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
           const T go = jmake<T>(own[k]), gn = jmake<T>(nbr[k]);
           const T gs = side > 0 ? 0.5 * (go + gn) : 0.5 * (gn + go);
           if (d == 0) sx_[k] = sx_[k] + s * gs; else sy_[k] = sy_[k] + s * gs;
+        }
+        if (Gf && t == (side > 0 ? P - 1 : 0)) {
+          // BR2 on GL (reading R33): the face point kf of this line; normal component
+          // l'(+-1).g along d + eta s_d (+-c) (g* - g_f), tangential the trace of (2/h) D g
+          const int kf = d == 0 ? j : i;
+          const double* dl = side > 0 ? g.dlp : g.dlm;
+          const double sd = d == 0 ? g.sx : g.sy, st = d == 0 ? g.sy : g.sx;
+          const double cj = side > 0 ? g.cp : -g.cm;
+          double* fo = Gf + ((size_t)e * 4 + f) * 6 * JN * P + kf;
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < JN; ++q) {
+              const double* row = sg + (k * JN + q) * PLANE;
+              double an = 0.0, at = 0.0;
+#pragma unroll 1
+              for (int l = 0; l < P; ++l) {
+                // line node l across the face direction; tangential derivative at (l, kf)
+                const int ii = d == 0 ? l : kf, jj = d == 0 ? kf : l;
+                an = fma(dl[l], row[jj * PS + ii], an);
+                double dt = 0.0;
+                for (int m2 = 0; m2 < P; ++m2)
+                  dt = fma(g.D[kf * P + m2], d == 0 ? row[m2 * PS + ii] : row[jj * PS + m2], dt);
+                at = fma(lo[l], dt, at);
+              }
+              const double gst = side > 0 ? 0.5 * (own[k][q] + nbr[k][q]) : 0.5 * (nbr[k][q] + own[k][q]);
+              const double vn = fma(pp.eta_br2 * sd * cj, gst - own[k][q], sd * an);
+              fo[((d * 3 + k) * JN + q) * P] = vn;
+              fo[(((1 - d) * 3 + k) * JN + q) * P] = st * at;
+            }
         }
       }
     }

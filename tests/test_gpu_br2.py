@@ -17,16 +17,18 @@ pytestmark = pytest.mark.gpu
 
 TWO_PI = 2 * np.pi
 BR2_CASES = [
-    # (N, nx, ny, eta)
-    (3, 4, 4, 2.0),
-    (5, 5, 3, 4.0),
-    (2, 6, 5, 1.0),
+    # (N, nx, ny, eta, nodes)
+    (3, 4, 4, 2.0, "gll"),
+    (5, 5, 3, 4.0, "gll"),
+    (2, 6, 5, 1.0, "gll"),
+    (3, 4, 4, 2.0, "gl"),        # the paper's own NS discretisation: GL nodes + BR2
+    (4, 3, 5, 1.0, "gl"),
 ]
 
 
-def _pair(N, nx, ny, eta, **kw):
+def _pair(N, nx, ny, eta, nodes="gll", **kw):
     return make_pair("navier_stokes", N, nx, ny, bounds=(0.0, TWO_PI, 0.0, TWO_PI), a=(1.0, -0.6), mu=0.05,
-                     lifting="br2", eta_br2=eta, **kw)
+                     lifting="br2", eta_br2=eta, nodes=nodes, **kw)
 
 
 @pytest.mark.parametrize("case", BR2_CASES)
@@ -62,9 +64,10 @@ def test_br2_differs_from_br1():
     assert rel(to_np(ctx.rhs(W)), to_np(ctx1.rhs(W))) > 1e-6
 
 
-def test_br2_precond():
+@pytest.mark.parametrize("nodes", ["gll", "gl"])
+def test_br2_precond(nodes):
     """BJ_ext by the two-hop colouring with BR2 face gradients."""
-    d, ctx = _pair(2, 4, 3, 2.0)
+    d, ctx = _pair(2, 4, 3, 2.0, nodes=nodes)
     W = ns_ic(d, SEED + 97)
     a1, a2, dt = 1.0 / 6.0, 1.0 / 54.0, 0.05
     pc = implicit.BJExt(d, W, a1, a2, dt)
@@ -77,9 +80,10 @@ def test_br2_precond():
     assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11 * max(1, cond / 1e4)
 
 
-def test_br2_end_of_run():
+@pytest.mark.parametrize("nodes", ["gll", "gl"])
+def test_br2_end_of_run(nodes):
     """HBPC(4,0), BJ_ext, 2 steps on 4x4 elements, N = 3: end of run vs the oracle <= 1e-8."""
-    d, ctx = _pair(3, 4, 4, 2.0, q=4, kmax=0, gmres_rtol=1e-10, newton_rtol=1e-10)
+    d, ctx = _pair(3, 4, 4, 2.0, nodes=nodes, q=4, kmax=0, gmres_rtol=1e-10, newton_rtol=1e-10)
     W0 = ns_ic(d, SEED + 100, rel_noise=1e-3)
     dt = 0.01
     H = hbpc.HBPC(d, 4, 0, implicit.NewtonOpts(rtol=1e-10, gmres_rtol=1e-10))
@@ -90,12 +94,6 @@ def test_br2_end_of_run():
         Wo = H.step(Wo, dt, st)
         ctx.step(dt, Wg)
     assert rel(to_np(Wg), Wo) <= 1e-8
-
-
-def test_br2_rejects_gl():
-    from paper_2109_04804_b200 import hbpdc
-    with pytest.raises(Exception, match="GLL"):
-        hbpdc.Context(dim=2, equation="navier_stokes", N=3, nx=4, ny=4, mu=0.01, lifting="br2", nodes="gl")
 
 
 @pytest.mark.parametrize("px,py", [(2, 2), (2, 1)])
