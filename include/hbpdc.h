@@ -72,8 +72,7 @@ typedef struct {
   double mu;            /* dynamic viscosity (NS)                           */
   double prandtl;       /* Prandtl number (NS), e.g. 0.72                   */
   int N;                /* polynomial degree, 1..7                                 */
-  int nodes;            /* HBPDC_GLL (configs, reading R1) or HBPDC_GL (
-                           Navier-Stokes on GL: one partition only)               */
+  int nodes;            /* HBPDC_GLL (configs, reading R1) or HBPDC_GL       */
   int nx, ny;           /* global element counts (ny ignored in 1D)                */
   double xmin, xmax, ymin, ymax;   /* periodic Cartesian domain                   */
   int flux;             /* HBPDC_LLF (reading R3) | HBPDC_GLF_PAPER (eq:Riemann, P:197-201:

@@ -142,6 +142,7 @@ struct hbpdc_ctx {
   double *gW = nullptr, *gS = nullptr, *gdW = nullptr, *gdS = nullptr, *gWb = nullptr;  // ghosts
   double *gG0 = nullptr, *gG1 = nullptr;                  // NS: ghost lifted gradients (second halo)
   double *gGf0 = nullptr, *gGf1 = nullptr;                // NS BR2: ghost face gradients
+  double *tg0 = nullptr, *tg1 = nullptr, *gtg0 = nullptr, *gtg1 = nullptr;   // NS GL: g(w) face traces + ghosts
   double *hsend = nullptr, *hrecv = nullptr;
   bool halo() const { return hl.active[0] || hl.active[2]; }
   int debug_sync = 0;              // HBPDC_DEBUG_SYNC=1: synchronise + check after every launch group
@@ -290,11 +291,27 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {
     // BR1: lift the jet state(s), then (partitioned) exchange the lifted
     // gradients' face traces -- the second halo of the radius-2 stencil
-    CK(launch_lift(k, 0, c->cfg, c->geo, A, c->lift0, c->liftf0));
+    const double *gtg0 = nullptr, *gtg1 = nullptr;
+    if (c->halo() && c->geo.gl) {
+      // GL across partitions: the neighbours' face traces of g(w) for the lifting's central value
+      CK(launch_gtrace(k, 0, c->cfg, c->geo, A, c->tg0));
+      const double* t0[1] = {c->tg0};
+      double* u0[1] = {c->gtg0};
+      CKS(halo_exchange(c, 1, t0, u0, 3 * lift_jet_components(k, 0), true));
+      gtg0 = c->gtg0;
+      if (k == OP_JVP_FD) {
+        CK(launch_gtrace(k, 1, c->cfg, c->geo, A, c->tg1));
+        const double* t1[1] = {c->tg1};
+        double* u1[1] = {c->gtg1};
+        CKS(halo_exchange(c, 1, t1, u1, 3 * lift_jet_components(k, 1), true));
+        gtg1 = c->gtg1;
+      }
+    }
+    CK(launch_lift(k, 0, c->cfg, c->geo, A, c->lift0, c->liftf0, gtg0));
     A.G0 = c->lift0;
     A.Gf0 = c->liftf0;
     if (k == OP_JVP_FD) {
-      CK(launch_lift(k, 1, c->cfg, c->geo, A, c->lift1, c->liftf1));
+      CK(launch_lift(k, 1, c->cfg, c->geo, A, c->lift1, c->liftf1, gtg1));
       A.G1 = c->lift1;
       A.Gf1 = c->liftf1;
     }
@@ -1520,6 +1537,14 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
       const size_t ngg = (size_t)(c->pb.dim == 2 ? 2 * (c->nxl + c->nyl) : 2) * 6 * 4 * c->nodes;
       CKS(dalloc(c, &c->gG0, ngg));
       CKS(dalloc(c, &c->gG1, ngg));
+      if (c->pb.nodes == HBPDC_GL) {
+        const size_t lt = (size_t)c->nE * 4 * 3 * 4 * c->P;
+        const size_t gt = (size_t)2 * (c->nxl + c->nyl) * 4 * 3 * 4 * c->P;
+        CKS(dalloc(c, &c->tg0, lt));
+        CKS(dalloc(c, &c->tg1, lt));
+        CKS(dalloc(c, &c->gtg0, gt));
+        CKS(dalloc(c, &c->gtg1, gt));
+      }
       if (c->pb.lifting == HBPDC_BR2) {
         const size_t ngf = (size_t)2 * (c->nxl + c->nyl) * 4 * 6 * 4 * c->P;
         CKS(dalloc(c, &c->gGf0, ngf));
@@ -1573,9 +1598,6 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->equation != HBPDC_ADVECTION && pb->dim != 2) return bad("Euler/NS need dim = 2");
   if (pb->N < 1 || pb->N > 7) return bad("N must be in 1..7");
   if (pb->nodes != HBPDC_GLL && pb->nodes != HBPDC_GL) return bad("nodes must be HBPDC_GLL or HBPDC_GL");
-  if (pb->nodes == HBPDC_GL && pb->equation == HBPDC_NAVIER_STOKES && (c->ds.nranks > 1 || c->ds.force_halo))
-    return bad("Gauss-Legendre nodes with Navier-Stokes: single partition only (the BR1 lifting needs the "
-               "traces of g(w), the halo carries those of w)");
   if (!(pb->mach_eps > 0.0)) return bad("mach_eps must be positive");
   if (pb->lifting != HBPDC_BR1 && pb->lifting != HBPDC_BR2) return bad("lifting must be HBPDC_BR1 or HBPDC_BR2");
   if (pb->lifting == HBPDC_BR2 && pb->equation == HBPDC_NAVIER_STOKES) {

@@ -25,13 +25,16 @@ int op_grid(const OpCfg& c, const Geo& g);
 // Gauss-Legendre instantiations (ops_kernels_gl.cu), reached from launch_op / launch_kbuild when g.gl
 cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
 cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout,
-                           double* Gf);
+                           double* Gf, const double* gTg, double* Tg);
 cudaError_t launch_kbuild_gl(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
                              double c2, double* M, int e0, int ne, const double* Sb, const double* gSb);
 // BR1 lifting of jet state `state` of operator `kind` into Gout
 // Gf (BR2, GLL): also write the per-face gradients [elem][face][6][JetN][P], or NULL (BR1)
+// gTg (GL across partitions): the neighbour ranks' g(w) face traces (launch_gtrace + face-buffer halo)
 cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout,
-                        double* Gf = nullptr);
+                        double* Gf = nullptr, const double* gTg = nullptr);
+// GL: face traces of the gradient variables g(w) of jet state `state`, [elem][face][3][JetN][P]
+cudaError_t launch_gtrace(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Tg);
 // number of jet components of the lifted gradients of (kind, state)
 int lift_jet_components(OpKind kind, int state);
 // BJ_ext: M_i = I - a1dt K_i + c2 K_i^2 for elements [e0, e0+ne), row-major m x m each

@@ -481,7 +481,8 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g) 
 // Computed for jet state K of the mode; result [elem][6][JetN][NODES].
 template <int P, class Mode, int K, int EPB, bool GL>
 __global__ void __launch_bounds__(EPB * P * P)
-lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g, double* Gout, double* Gf) {
+lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g, double* Gout, double* Gf,
+            const double* gTg) {
   using T = typename Mode::template StateT<K>;
   constexpr int NODES = P * P, PS = P + 1, PLANE = P * PS;
   constexpr int JN = JetN<T>::value;
@@ -519,6 +520,7 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
         for (int k = 0; k < 3; ++k)
 #pragma unroll
           for (int q = 0; q < JN; ++q) { own[k][q] = 0.0; nbr[k][q] = 0.0; }
+        const bool ghost = nb >= g.nE;      // across a partition: the sender's g-trace (gtrace_kernel)
 #pragma unroll 1
         for (int l = 0; l < P; ++l) {
           const int ii = d == 0 ? l : i, jj = d == 0 ? j : l;
@@ -526,6 +528,7 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
           for (int k = 0; k < 3; ++k)
 #pragma unroll
             for (int q = 0; q < JN; ++q) own[k][q] = fma(lo[l], sg[(k * JN + q) * PLANE + jj * PS + ii], own[k][q]);
+          if (ghost) continue;
           T wn[4], gn[3];
           Mode::template load_w<K>(A, nb, jj * P + ii, wn, true);
           grad_vars(pp, wn, gn);
@@ -533,6 +536,13 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
           for (int k = 0; k < 3; ++k)
 #pragma unroll
             for (int q = 0; q < JN; ++q) nbr[k][q] = fma(ln[l], jget(gn[k], q), nbr[k][q]);
+        }
+        if (ghost) {
+          const double* tg = gTg + ((size_t)(nb - g.nE) * 4 + (f ^ 1)) * 3 * JN * P + (d == 0 ? j : i);
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < JN; ++q) nbr[k][q] = tg[(k * JN + q) * P];
         }
         const int t = d == 0 ? i : j;
         const double s = (d == 0 ? g.sx : g.sy) * (side > 0 ? g.lhpv[t] : -g.lhmv[t]);
@@ -659,4 +669,39 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
         out[((k + 3) * JN + q) * NODES] = g.sy * ay + jget(sy_[k], q);
       }
   }
+}
+
+// ---- GL Navier-Stokes across partitions: face traces of g(w) ----------------------
+// T[e][face f][3][JetN][P] = sum_l l_l(+-1) g(w_l) along the line through face point kf
+// (the same accumulation order as the local neighbour trace in lift_kernel), exchanged
+// by the face-buffer halo so that a rank's lift reads its neighbours' g-traces.
+template <int P, class Mode, int K>
+__global__ void gtrace_kernel(const typename Mode::Args A, const PhysParams pp, const Geo g, double* Tg) {
+  using T = typename Mode::template StateT<K>;
+  constexpr int JN = JetN<T>::value;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.nE * 4 * P) return;
+  const int kf = t % P, f = (t / P) % 4, e = t / (4 * P);
+  const int d = f >> 1;
+  const double* l = (f & 1) ? g.lp : g.lm;
+  double acc[3][JN];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int q = 0; q < JN; ++q) acc[k][q] = 0.0;
+  for (int m = 0; m < P; ++m) {
+    const int ii = d == 0 ? m : kf, jj = d == 0 ? kf : m;
+    T wn[4], gn[3];
+    Mode::template load_w<K>(A, e, jj * P + ii, wn, false);
+    grad_vars(pp, wn, gn);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int q = 0; q < JN; ++q) acc[k][q] = fma(l[m], jget(gn[k], q), acc[k][q]);
+  }
+  double* o = Tg + ((size_t)e * 4 + f) * 3 * JN * P + kf;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int q = 0; q < JN; ++q) o[(k * JN + q) * P] = acc[k][q];
 }

@@ -39,12 +39,22 @@ static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
 }
 
 template <int P, class Mode, int K>
-static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, double* G, double* Gf) {
+static cudaError_t run_gtrace(const OpCfg& c, const Geo& g, const OpArgs& A, double* Tg) {
+  const int total = g.nE * 4 * P;
+  if (total == 0) return cudaSuccess;
+  gtrace_kernel<P, Mode, K><<<(total + 127) / 128, 128, 0, c.stream>>>(A, c.pp, g, Tg);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+template <int P, class Mode, int K>
+static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, double* G, double* Gf,
+                            const double* gTg) {
   constexpr int NODES = P * P;
   constexpr int EPB = epb_for(NODES);
   const int grid = (g.nE + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
-  lift_kernel<P, Mode, K, EPB, kGL><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G, Gf);
+  lift_kernel<P, Mode, K, EPB, kGL><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G, Gf, gTg);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -250,16 +260,17 @@ template <int EQ, int DIM, int P> struct Disp {
       default: return cudaErrorInvalidValue;
     }
   }
-  static cudaError_t lift(OpKind k, int s, const OpCfg& c, const Geo& g, const OpArgs& A, double* G, double* Gf) {
+  static cudaError_t lift(OpKind k, int s, const OpCfg& c, const Geo& g, const OpArgs& A, double* G, double* Gf,
+                          const double* gTg, double* Tg) {
     if constexpr (EQ == 2 && DIM == 2) {
       switch (k) {
-        case OP_R1: case OP_R1ABS: return run_lift<P, ModeR1<EQ, NODES>, 0>(c, g, A, G, Gf);
-        case OP_R12: return run_lift<P, ModeR12<EQ, NODES>, 0>(c, g, A, G, Gf);
-        case OP_RESID: return run_lift<P, ModeResid<EQ, NODES>, 0>(c, g, A, G, Gf);
-        case OP_JVP_EXACT: return run_lift<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, G, Gf);
+        case OP_R1: case OP_R1ABS: return (Tg ? run_gtrace<P, ModeR1<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeR1<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
+        case OP_R12: return (Tg ? run_gtrace<P, ModeR12<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeR12<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
+        case OP_RESID: return (Tg ? run_gtrace<P, ModeResid<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeResid<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
+        case OP_JVP_EXACT: return (Tg ? run_gtrace<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
         case OP_JVP_FD:
-          return s == 0 ? run_lift<P, ModeJvpFD<EQ, NODES>, 0>(c, g, A, G, Gf)
-                        : run_lift<P, ModeJvpFD<EQ, NODES>, 1>(c, g, A, G, Gf);
+          return s == 0 ? (Tg ? run_gtrace<P, ModeJvpFD<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeJvpFD<EQ, NODES>, 0>(c, g, A, G, Gf, gTg))
+                        : (Tg ? run_gtrace<P, ModeJvpFD<EQ, NODES>, 1>(c, g, A, Tg) : run_lift<P, ModeJvpFD<EQ, NODES>, 1>(c, g, A, G, Gf, gTg));
         default: return cudaErrorInvalidValue;
       }
     }
@@ -288,8 +299,8 @@ static cudaError_t dispatch(const OpCfg& c, F&& f) {
 
 #if HBPDC_OPS_GL
 cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G,
-                           double* Gf) {
-  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G, Gf); });
+                           double* Gf, const double* gTg, double* Tg) {
+  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G, Gf, gTg, Tg); });
 }
 
 cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
@@ -313,9 +324,14 @@ cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A
 }
 
 cudaError_t launch_lift(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G,
-                        double* Gf) {
-  if (g.gl) return launch_lift_gl(kind, state, c, g, A, G, Gf);
-  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G, Gf); });
+                        double* Gf, const double* gTg) {
+  if (g.gl) return launch_lift_gl(kind, state, c, g, A, G, Gf, gTg, nullptr);
+  return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G, Gf, nullptr, nullptr); });
+}
+
+cudaError_t launch_gtrace(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Tg) {
+  if (!g.gl) return cudaErrorInvalidValue;
+  return launch_lift_gl(kind, state, c, g, A, nullptr, nullptr, nullptr, Tg);
 }
 
 int lift_jet_components(OpKind kind, int state) {

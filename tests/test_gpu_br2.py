@@ -96,16 +96,17 @@ def test_br2_end_of_run(nodes):
     assert rel(to_np(Wg), Wo) <= 1e-8
 
 
-@pytest.mark.parametrize("px,py", [(2, 2), (2, 1)])
-def test_br2_loopback_operators_bitwise(px, py):
+@pytest.mark.parametrize("px,py,nodes", [(2, 2, "gll"), (2, 1, "gll"), (2, 2, "gl")])
+def test_br2_loopback_operators_bitwise(px, py, nodes):
     """BR2 across loopback ranks: the neighbour ranks' face gradients arrive by the
     face-buffer halo and every rank's operator output equals its block of the
-    single-rank result bit for bit; one HBPC(4,0) step <= 1e-10 vs one rank."""
+    single-rank result bit for bit (GLL; GL: the ghost W traces are interpolated by
+    the sender, so to rounding); one HBPC(4,0) step <= 1e-10 vs one rank."""
     import torch
     from paper_2109_04804_b200 import hbpdc
     from test_gpu_partition import _block, _run_threads
     N, nx, ny, eta = 2, 6, 6, 2.0
-    d, ctx1 = _pair(N, nx, ny, eta)
+    d, ctx1 = _pair(N, nx, ny, eta, nodes=nodes)
     W = ns_ic(d, SEED + 101)
     sig = dgsem.rhs1(d, W) * (1 + 1e-2 * inputs.random_field(d.n, SEED + 102))
     dW = inputs.random_field(d.n, SEED + 103, unit_norm=True)
@@ -131,7 +132,7 @@ def test_br2_loopback_operators_bitwise(px, py):
     ctxs = [hbpdc.Context(dim=2, equation="navier_stokes", N=N, nx=nx, ny=ny, bounds=(0.0, TWO_PI, 0.0, TWO_PI),
                           a=(1.0, -0.6), mu=0.05, lifting="br2", eta_br2=eta, q=4, kmax=0, gmres_rtol=1e-10,
                           newton_rtol=1e-10, rank=r, nranks=px * py, px=px, py=py, comm="loopback",
-                          loopback=group, stream=torch.cuda.Stream())
+                          loopback=group, stream=torch.cuda.Stream(), nodes=nodes)
             for r in range(px * py)]
     try:
         def blk_of(c):
@@ -141,9 +142,12 @@ def test_br2_loopback_operators_bitwise(px, py):
             blk = blk_of(c)
             for key, r in ref.items():
                 rb = np.concatenate([blk(r[:d.n]), blk(r[d.n:])]) if r.size == 2 * d.n else blk(r)
-                assert np.array_equal(o[key], rb), (key, c.rank, np.abs(o[key] - rb).max())
+                if nodes == "gll":
+                    assert np.array_equal(o[key], rb), (key, c.rank, np.abs(o[key] - rb).max())
+                else:
+                    assert rel(o[key], rb) <= (1e-6 if key == "fd" else 1e-12), (key, c.rank, rel(o[key], rb))
         # one step, partitioned vs single rank
-        _, c1 = _pair(N, nx, ny, eta, q=4, kmax=0, gmres_rtol=1e-10, newton_rtol=1e-10)
+        _, c1 = _pair(N, nx, ny, eta, nodes=nodes, q=4, kmax=0, gmres_rtol=1e-10, newton_rtol=1e-10)
         W0 = ns_ic(d, SEED + 105, rel_noise=1e-3)
         W1 = to_gpu(W0)
         c1.step(0.004, W1)

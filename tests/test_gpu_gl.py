@@ -147,14 +147,6 @@ def test_gl_end_of_run(kind, q, kmax, sstep):
     assert rel(to_np(Wg), Wo) <= 1e-8
 
 
-def test_gl_rejects_navier_stokes_partitions():
-    """GL Navier-Stokes on several partitions is refused at init (the BR1 lifting
-    needs traces of g(w); the halo carries those of w)."""
-    from paper_2109_04804_b200 import hbpdc
-    with pytest.raises(Exception, match="single partition"):
-        hbpdc.Context(dim=2, equation="navier_stokes", N=3, nx=4, ny=4, nodes="gl", mu=0.01, force_halo=True)
-
-
 # ---- element partition (loopback ranks on one GPU; the halo carries interpolated traces) ----
 GL_PART_CASES = [
     # kind, N, nx, ny, px, py
@@ -162,6 +154,9 @@ GL_PART_CASES = [
     ("euler", 4, 6, 4, 3, 1),
     ("advection", 3, 4, 6, 1, 2),
     ("advection", 3, 8, None, 2, 1),
+    # Navier-Stokes: the lifting's central value needs the neighbours' g(w) traces (gtrace_kernel)
+    ("navier_stokes", 2, 6, 6, 2, 2),
+    ("navier_stokes", 3, 6, 4, 2, 1),
 ]
 
 
@@ -202,14 +197,15 @@ def test_gl_loopback_operators(case):
     ref = ops(ctx1, lambda x: x)
     assert rel(ref["R1"], dgsem.rhs1(d, W)) <= 1e-11
     fd_tol = None
-    if kind == "euler":
+    if kind != "advection":
         fo = np.concatenate(implicit.jvp_fd(d, a1, a2, dt, W, sig, dW, ds, eps_override=(eps, None)))
         ex = np.concatenate(implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds))
         fd_tol = max(1e-11, 4 * rel(fo, ex))
     group = hbpdc.LoopbackGroup(px * py)
     a = (1.0, 0.0) if dim == 1 else (1.0, -0.6)
+    nskw = dict(mu=NS_MU, bounds=(0.0, 2 * np.pi, 0.0, 2 * np.pi)) if kind == "navier_stokes" else {}
     ctxs = [hbpdc.Context(dim=dim, equation=kind, N=N, nx=nx, ny=ny or 1, a=a, rank=r, nranks=px * py, px=px,
-                          py=py, comm="loopback", loopback=group, stream=torch.cuda.Stream(), nodes="gl")
+                          py=py, comm="loopback", loopback=group, stream=torch.cuda.Stream(), nodes="gl", **nskw)
             for r in range(px * py)]
     try:
         def blk_of(c):
