@@ -192,6 +192,8 @@ def run_ours(args):
                   force_halo=bool(args.self_halo))
     if args.precond:
         kw["precond"] = args.precond
+    if args.nodes != "gll" or args.flux != "llf":
+        kw.update(nodes=args.nodes, flux=args.flux)      # the paper's own discretisation choices (NEXT-3)
     ctx = hbpdc.context_for(cfg, device=local, gmres_sstep=args.gmres_sstep, **kw)
     coords = inputs.tile_coords(ctx.node_coords(), cfg.bounds)
     W0 = inputs.initial_state(CONFIG, coords, noise=cfg.noise, stream=rank)
@@ -296,10 +298,12 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C3: 2D Euler isentropic vortex (beta=5, mean (1,1)) + seeded U[-1e-6,1e-6) "
-                                   "noise, [-5,5]^2 periodic, 128x128 elements, N=7 GLL, LLF, HBPC(8,4), "
+                                   f"noise, [-5,5]^2 periodic, 128x128 elements, N=7 {args.nodes.upper()}, "
+                                   f"{args.flux.upper()}, HBPC(8,4), "
                                    "BJ_ext, FD JVP, Newton/GMRES rtol 1e-10, restart 700",
                        "arnoldi": ("DCGS2" if args.gmres_sstep <= 1 else f"s-step s={args.gmres_sstep} (block CGS2)"),
                        "precond": args.precond or cfg.precond,
+                       "nodes": args.nodes, "flux": args.flux,
                        "dt": dt, "n_dof_per_gpu": n, "n_dof": n * world,
                        "parallelism": (f"element partition {px}x{py} of a {cfg.nx * px}x{cfg.ny * py} mesh "
                                        "(C3 tile per GPU), NCCL halos + all-reduces") if world > 1 else
@@ -336,6 +340,10 @@ def main():
                     help="override the config's preconditioner (default: C3's BJ_ext)")
     ap.add_argument("--gmres-sstep", type=int, default=8,
                     help="Arnoldi schedule: 1 = DCGS2, 2/4/8 = s-step blocks")
+    ap.add_argument("--nodes", default="gll", choices=["gll", "gl"],
+                    help="DGSEM nodes (C3: GLL; gl = the paper's Gauss-Legendre, NEXT-3)")
+    ap.add_argument("--flux", default="llf", choices=["llf", "glf"],
+                    help="numerical flux (C3: LLF; glf = the paper's global LF, NEXT-3)")
     ap.add_argument("--self-halo", action="store_true",
                     help="test hook: route the periodic wrap through the NCCL transport (N = 1)")
     args = ap.parse_args()
