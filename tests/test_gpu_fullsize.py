@@ -51,16 +51,29 @@ def _state(case, d_coords, cfg):
 
 @pytest.mark.parametrize("case", ["C2", "C3", "C4", "C5"])
 def test_fullsize_sampled_operators(case):
+    _sampled_operators(case)
+
+
+@pytest.mark.parametrize("case,nodes,flux,lifting", [("C3", "gl", "glf", "br1"), ("C5", "gl", "llf", "br2")])
+def test_fullsize_sampled_operators_paper_discretisation(case, nodes, flux, lifting):
+    """The same full-size sampled parity with the paper's own discretisation choices
+    (NEXT-3): Gauss-Legendre nodes, the global LF flux (C3), BR2 lifting (C5)."""
+    _sampled_operators(case, nodes=nodes, flux=flux, lifting=lifting)
+
+
+def _sampled_operators(case, nodes="gll", flux="llf", lifting="br1"):
     import torch
     cfg = configs.CONFIGS[case]
-    ctx = hbpdc.context_for(cfg, restart=min(cfg.restart, 50))     # operators only: a small Krylov basis
+    ctx = hbpdc.context_for(cfg, restart=min(cfg.restart, 50),       # operators only: a small Krylov basis
+                            nodes=nodes, flux=flux, lifting=lifting)
     r = 2 if cfg.equation == "navier_stokes" else 1
     w = 2 * r + 1
     nx, ny, m, n = cfg.nx, cfg.ny, cfg.m, cfg.n
     coords = ctx.node_coords()
     W = _state(case, coords, cfg)
-    eq = physics.Equation(cfg.equation, a=cfg.a, gamma=cfg.gamma, mu=cfg.mu, prandtl=cfg.prandtl)
-    B = basis.build_basis(cfg.N, "gll")
+    eq = physics.Equation(cfg.equation, a=cfg.a, gamma=cfg.gamma, mu=cfg.mu, prandtl=cfg.prandtl,
+                          numflux=flux, lifting=lifting)
+    B = basis.build_basis(cfg.N, nodes)
     dx = (cfg.bounds[1] - cfg.bounds[0]) / nx
     dy = (cfg.bounds[3] - cfg.bounds[2]) / ny
     dwin = dgsem.Disc(B, dgsem.Mesh(2, w, w, 0.0, w * dx, 0.0, w * dy), eq)
