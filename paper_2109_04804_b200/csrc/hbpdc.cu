@@ -1661,6 +1661,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->geo.lhm = c->basis.lhm;
   for (int i = 0; i < c->P * c->P; ++i) c->geo.Dh[i] = c->basis.Dhat[i];
   c->geo.gl = c->basis.gl;
+  c->geo.br2 = pb->equation == HBPDC_NAVIER_STOKES && pb->lifting == HBPDC_BR2;
   c->hl.gl = c->basis.gl;                // GL halos carry interpolated traces
   for (int i = 0; i < c->P; ++i) { c->hl.lp[i] = c->basis.lp[i]; c->hl.lm[i] = c->basis.lm[i]; }
   c->geo.P = c->P;

@@ -121,7 +121,7 @@ struct OneJetMode {
     trace_load(g, use_own ? own : nnode, d, st,
                [=](int nd, State& s) { load(A, g, le, slot, nd, s, !use_own); }, le >= A.nE);
     if constexpr (EQ == 2) {
-      if (A.Gf0) {                   // BR2: the face's own local-lifting gradient (reading R33)
+      if constexpr (G::BR2) {                   // BR2: the face's own local-lifting gradient (reading R33)
         const int f = 2 * d + (use_own ? (plus ? 1 : 0) : (plus ? 0 : 1));
         const int kf = d == 0 ? own / g.P : own % g.P;
         load_face_grads<J>(A.Gf0, A.gGf0, A.nE, le, f, kf, g.P, st.s.gx, st.s.gy);
@@ -365,7 +365,7 @@ template <int EQ, int NODES> struct ModeJvpFD {
         ld_state<EQ, J1, NODES>(A.G0, A.gG0, A.nE, nb, nd, s);
       }, nb >= A.nE);
       if constexpr (EQ == 2) {
-        if (A.Gf0) {
+        if constexpr (G::BR2) {
           const int kf = d == 0 ? own / g.P : own % g.P;
           load_face_grads<J1>(A.Gf0, A.gGf0, A.nE, e, 2 * d + (plus ? 1 : 0), kf, g.P, so.gx, so.gy);
           load_face_grads<J1>(A.Gf0, A.gGf0, A.nE, nb, 2 * d + (plus ? 0 : 1), kf, g.P, sn.gx, sn.gy);
@@ -386,7 +386,7 @@ template <int EQ, int NODES> struct ModeJvpFD {
         ld_state<EQ, J2, NODES>(A.G1, A.gG1, A.nE, nb, nd, s);
       }, nb >= A.nE);
       if constexpr (EQ == 2) {
-        if (A.Gf1) {
+        if constexpr (G::BR2) {
           const int kf = d == 0 ? own / g.P : own % g.P;
           load_face_grads<J2>(A.Gf1, A.gGf1, A.nE, e, 2 * d + (plus ? 1 : 0), kf, g.P, so.gx, so.gy);
           load_face_grads<J2>(A.Gf1, A.gGf1, A.nE, nb, 2 * d + (plus ? 0 : 1), kf, g.P, sn.gx, sn.gy);

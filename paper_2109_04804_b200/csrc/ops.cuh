@@ -32,6 +32,7 @@ struct Geo {
   double lhp, lhm;         // lhat_N(+1) = 1/w_N, lhat_0(-1) = 1/w_0  (GLL)
   double Dh[64];           // Dhat (P x P, row-major)
   int gl, P, dim;          // gl: Gauss-Legendre nodes (no node on the element edge)
+  int br2;                 // NS with BR2 lifting (dispatches to the BR2 instantiations)
   double lp[8], lm[8];     // GL: l_i(+1), l_i(-1)  (traces)
   double lhpv[8], lhmv[8]; // GL: lhat_i(+1), lhat_i(-1)  (surface terms, eq:DGSEM_wt)
   double D[64];            // GL BR2: strong-form D_ij = l_j'(x_i)
@@ -41,8 +42,9 @@ struct Geo {
 
 // Node set selected at compile time (the GL kernels are a separate instantiation,
 // ops_kernels_gl.cu, so the GLL hot path is compiled exactly as without GL).
-template <bool GL_> struct GeoSel : Geo {
+template <bool GL_, bool BR2_ = false> struct GeoSel : Geo {
   static constexpr bool GL = GL_;
+  static constexpr bool BR2 = BR2_;   // NS face gradients from the BR2 per-face buffers (reading R33)
 };
 
 // Face trace of a node state.  GLL: the edge node n itself.  GL: the
@@ -437,9 +439,9 @@ __host__ __device__ constexpr int epb_for(int nodes) {
 #ifndef HBPDC_MINB
 #define HBPDC_MINB 4
 #endif
-template <int EQ, int DIM, int P, class Mode, int EPB, bool GL>
+template <int EQ, int DIM, int P, class Mode, int EPB, bool GL, bool BR2>
 __global__ void __launch_bounds__(EPB * ipow(P, DIM), HBPDC_MINB)
-op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g) {
+op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL, BR2> g) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int NV = NVars<EQ>::value;
   extern __shared__ __align__(16) double sF[];     // EPB * slot_doubles (dynamic: may exceed 48 KB)

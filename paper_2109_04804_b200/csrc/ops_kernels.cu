@@ -11,10 +11,15 @@
 #ifndef HBPDC_OPS_GL
 #define HBPDC_OPS_GL 0
 #endif
+#ifndef HBPDC_OPS_BR2
+#define HBPDC_OPS_BR2 0       // 1: the Navier-Stokes operators with BR2 face gradients (ops_kernels*_br2.cu)
+#endif
 static constexpr bool kGL = HBPDC_OPS_GL;
+static constexpr bool kBR2 = HBPDC_OPS_BR2;
 using GeoK = GeoSel<kGL>;
-static GeoK geo_sel(const Geo& g) {
-  GeoK s;
+template <bool B = false>
+static GeoSel<kGL, B> geo_sel(const Geo& g) {
+  GeoSel<kGL, B> s;
   static_cast<Geo&>(s) = g;
   return s;
 }
@@ -29,11 +34,11 @@ static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
   if constexpr (smem > 48 * 1024) {
     static bool attr = false;       // once per instantiation (same value from any thread)
     if (!attr) {
-      cudaFuncSetAttribute(op_kernel<EQ, DIM, P, Mode, EPB, kGL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(op_kernel<EQ, DIM, P, Mode, EPB, kGL, kBR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
   }
-  op_kernel<EQ, DIM, P, Mode, EPB, kGL><<<grid, EPB * NODES, smem, c.stream>>>(A, c.pp, geo_sel(g));
+  op_kernel<EQ, DIM, P, Mode, EPB, kGL, kBR2><<<grid, EPB * NODES, smem, c.stream>>>(A, c.pp, geo_sel<kBR2>(g));
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -289,15 +294,25 @@ template <class F>
 static cudaError_t dispatch(const OpCfg& c, F&& f) {
 #define CASE(EQ, DIM, PP) \
   if (c.eq == EQ && c.dim == DIM && c.P == PP) return f(Disp<EQ, DIM, PP>{});
+#if !HBPDC_OPS_BR2
   HBPDC_P_LIST(CASE, 0, 1)
   HBPDC_P_LIST(CASE, 0, 2)
   HBPDC_P_LIST(CASE, 1, 2)
+#endif
   HBPDC_P_LIST(CASE, 2, 2)
 #undef CASE
   return cudaErrorInvalidValue;
 }
 
+#if HBPDC_OPS_BR2
 #if HBPDC_OPS_GL
+cudaError_t launch_op_gl_br2(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
+#else
+cudaError_t launch_op_br2(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
+#endif
+  return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
+}
+#elif HBPDC_OPS_GL
 cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* G,
                            double* Gf, const double* gTg, double* Tg) {
   return dispatch(c, [&](auto d) { return decltype(d)::lift(kind, state, c, g, A, G, Gf, gTg, Tg); });
@@ -319,6 +334,7 @@ int op_grid(const OpCfg& c, const Geo& g) {
 }
 
 cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
+  if (g.br2) return g.gl ? launch_op_gl_br2(kind, c, g, A) : launch_op_br2(kind, c, g, A);
   if (g.gl) return launch_op_gl(kind, c, g, A);
   return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
 }
@@ -416,4 +432,4 @@ cudaError_t launch_colour_gather(const double* y1, const double* y2, double* K, 
   hbpdc_count_launch();
   return cudaGetLastError();
 }
-#endif  // HBPDC_OPS_GL
+#endif  // HBPDC_OPS_BR2 / HBPDC_OPS_GL
