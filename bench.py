@@ -1,20 +1,36 @@
 """Benchmark: HBPC(q, k_max) / DGSEM time steps on B200 (arXiv 2109.04804).
 
-One bench "step" is one HBPC(8,4) time step (Alg. 1) of config C3
-(2D Euler isentropic vortex, 128x128 elements, N=7, GLL, LLF, BJ_ext, FD JVP,
-Newton-GMRES rtol 1e-10) -- every row of SURVEY 8(a): residual, FD JVP,
-BJ_ext build + apply, Arnoldi, Newton updates, stage combinations.
-Prints ONE JSON line (rank 0).
+One bench "step" is one HBPC time step (Alg. 1) of a BASELINE
+config -- every row of SURVEY 8(a): residual, FD JVP, BJ_ext build + apply,
+Arnoldi, Newton updates, stage combinations (C5 adds the NS lifting, a14).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C4|C5]
+                    [--scaling weak|strong] [--impl ours|reference]
 
---impl reference times the CPU oracle (oracle/, test infrastructure) on a
-bounded sample of the same workload, scaled to steps/s.
+* default: C3 (2D Euler isentropic vortex, 128x128 elements, N=7, GLL, LLF,
+  HBPC(8,4), BJ_ext, FD JVP, Newton/GMRES rtol 1e-10) on 1 GPU.
+* --gpus N without torchrun re-launches itself under torch.distributed.run
+  with N ranks (one process per GPU, NCCL); under torchrun WORLD_SIZE must
+  equal --gpus.
+* --scaling strong: one fixed global mesh element-partitioned px x py
+  (1x1, 2x1, 2x2, 4x2); the default for C4 and C5 (parallel
+  efficiency is strong scaling on C4).  --scaling weak: one copy of the
+  config's mesh per GPU (a (nx px) x (ny py) periodic tiling); the default
+  for C3.  `value` is the units all ranks processed / device time (max over
+  ranks): strong = global steps/s; weak = config-tile steps/s (N x global).
+* `value` is timed with the library's per-kernel profiling OFF; the kernel
+  table comes from a separate profiled pass (--profile-steps).  `e2e` replays
+  the same K steps from the same state through hbpdc_step_host (host buffer,
+  H2D + step + D2H per step).
+* --impl reference times the CPU oracle (oracle/, test infrastructure) on a
+  bounded sample of the same workload (one predictor stage solve on a small
+  periodic window of the config's mesh, same h, N, dt, tolerances), scaled to
+  steps/s; ms_per_step is the wall time of one sample.
 """
 import argparse
 import json
-import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -25,7 +41,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "HBPDC steps/s"
 UNIT = "steps/s"
-CONFIG = "C3"
+FP64_PEAK_TFLOPS = 37.0     # measured DMMA peak on this B200 pool (scripts/dmma_peak.cu)
+PARTS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
 
 
 def measured_peaks():
@@ -36,72 +53,87 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def workload_name(cfg, args):
+    eqn = {"euler": "2D Euler", "navier_stokes": "2D Navier-Stokes (BR1, Re 1000, Pr 0.72)",
+           "advection": "2D advection"}[cfg.equation]
+    ic = {"C3": "isentropic vortex (beta=5, mean (1,1)) + seeded U[-1e-6,1e-6) noise",
+          "C4": "density wave rho=1+0.2 sin(2 pi (x+y)), u=v=p=1",
+          "C5": "TGV-type vortex, Mach 0.1"}[cfg.name]
+    return (f"{cfg.name}: {eqn} {ic}, {cfg.nx}x{cfg.ny} elements, N={cfg.N} {args.nodes.upper()}, "
+            f"{args.flux.upper()}, HBPC({cfg.q},{cfg.kmax}), {(args.precond or cfg.precond).upper()}, "
+            f"FD JVP, GMRES rtol {cfg.gmres_rtol:g} / Newton {cfg.newton_rtol:g}, restart {cfg.restart}")
+
+
 # --------------------------------------------------------------------------------
 # CPU oracle sample (cpu_baseline and --impl reference)
 
-def oracle_sample():
-    """First predictor stage solve (with its BJ_ext build) of C3's first step on
-    a 4x4-element periodic window of C3's mesh centred on the vortex (same h,
-    N=7, dt, tolerances).  Returns (seconds, description, scale): steps/s of
-    the full workload ~= 1 / (seconds * scale), scale = 15 stage solves per
-    HBPC(8,4) step x (16384 / 16) elements."""
-    import numpy as np
+def stage_solves_per_step(q, kmax):
+    s = {4: 2, 6: 3, 8: 4}[q]            # stages of HBPC(q, .) (App. A)
+    return (s - 1) * (kmax + 1)
+
+
+def oracle_sample(cfg_name):
+    """First predictor stage solve (with its BJ_ext build) of the config's first
+    step on a 4x4-element periodic window of its mesh centred in the domain
+    (same h, N, equation, dt, tolerances).  Returns (seconds, cpu_seconds,
+    description, scale) with steps/s of the full workload ~= 1 / (seconds * scale),
+    scale = stage solves per step x (elements / 16)."""
+    import numpy as np  # noqa: F401
     from oracle import basis, dgsem, implicit, physics
     from paper_2109_04804_b200 import configs, inputs
-    cfg = configs.CONFIGS[CONFIG]
-    h = (cfg.bounds[1] - cfg.bounds[0]) / cfg.nx
+    cfg = configs.CONFIGS[cfg_name]
+    hx = (cfg.bounds[1] - cfg.bounds[0]) / cfg.nx
+    hy = (cfg.bounds[3] - cfg.bounds[2]) / cfg.ny
+    cx, cy = 0.5 * (cfg.bounds[0] + cfg.bounds[1]), 0.5 * (cfg.bounds[2] + cfg.bounds[3])
     nw = 4
-    half = nw * h / 2
-    d = dgsem.Disc(basis.build_basis(cfg.N, "gll"), dgsem.Mesh(2, nw, nw, -half, half, -half, half),
-                   physics.Equation("euler"))
-    W0 = inputs.initial_state(CONFIG, d.node_coords(), noise=cfg.noise)
-    # dt of the full config: element CFL 1 on the full discrete IC (reading R15)
-    full = dgsem.Disc(d.basis, dgsem.Mesh(2, cfg.nx, cfg.ny, *cfg.bounds), d.eq)
-    dt = configs.cfl_dt(cfg, inputs.initial_state(CONFIG, full.node_coords()))
-    c = 1.0 / 3.0
+    eq = physics.Equation(cfg.equation, mu=cfg.mu)
+    d = dgsem.Disc(basis.build_basis(cfg.N, "gll"),
+                   dgsem.Mesh(2, nw, nw, cx - nw * hx / 2, cx + nw * hx / 2, cy - nw * hy / 2, cy + nw * hy / 2), eq)
+    W0 = inputs.initial_state(cfg_name, d.node_coords(), noise=cfg.noise)
+    full = dgsem.Disc(d.basis, dgsem.Mesh(2, cfg.nx, cfg.ny, *cfg.bounds), eq)
+    dt = configs.cfl_dt(cfg, inputs.initial_state(cfg_name, full.node_coords()))
+    c = {4: 1.0, 6: 0.5, 8: 1.0 / 3.0}[cfg.q]          # first stage spacing of App. A
     a1, a2 = c / 2, c * c / 6
-    t0 = time.perf_counter()
-    opts = implicit.NewtonOpts(rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol)
+    t0, c0 = time.perf_counter(), time.process_time()
+    opts = implicit.NewtonOpts(rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol, restart=cfg.restart)
     R1 = dgsem.rhs1(d, W0)
     _, R2 = dgsem.rhs12(d, W0, R1)
     b = W0 + a1 * dt * R1 + a2 * dt * dt / 2 * R2
     pc = implicit.BJExt(d, W0, a1, a2, dt)
     implicit.newton_solve(d, a1, a2, dt, b, W0, opts, pc)
-    sec = time.perf_counter() - t0
-    scale = 15 * (cfg.nx * cfg.ny) / (nw * nw)
-    desc = ("oracle: first predictor stage solve (BJ_ext build + Newton-GMRES) of C3 step 1 on a 4x4-element "
-            "periodic window of C3's mesh (same h, N=7, dt, tolerances); steps/s = 1/(t x 15 stage solves x "
-            "1024 element ratio)")
-    return sec, desc, scale
-
-
-def cpu_cores():
-    try:
-        from threadpoolctl import threadpool_info
-        n = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        n = 1
-    return n
+    sec, cpu = time.perf_counter() - t0, time.process_time() - c0
+    k = stage_solves_per_step(cfg.q, cfg.kmax)
+    scale = k * (cfg.nx * cfg.ny) / (nw * nw)
+    desc = (f"oracle (numpy, fp64): first predictor stage solve (BJ_ext build + Newton-GMRES) of {cfg_name} step 1 "
+            f"on a {nw}x{nw}-element periodic window of {cfg_name}'s mesh (same h, N={cfg.N}, dt, tolerances), "
+            f"timed end to end; steps/s = 1/(t x {k} stage solves x {cfg.nx * cfg.ny // (nw * nw)} element ratio)")
+    return sec, cpu, desc, scale
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    times = []
+    from paper_2109_04804_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    times, cpus = [], []
     desc, scale = "", 1.0
     for s in range(args.warmup + args.steps):
-        sec, desc, scale = oracle_sample()
+        sec, cpu, desc, scale = oracle_sample(args.config)
         if s >= args.warmup:
             times.append(sec)
+            cpus.append(cpu)
     t = sum(times) / len(times)
+    cores = round(sum(cpus) / sum(times), 2)
     val = 1.0 / (t * scale)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * scale * 1e3,
-            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG + " (sampled)", "sample": desc},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
-                             "sample": desc},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "ms_per_step_note": "wall time of one sample step (value = 1 / (sample seconds x scale))",
+            "value_scale": scale, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg, args), "sample": desc},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                             "cores_note": "process CPU time / wall time of the samples",
+                             "host_cpus": os.cpu_count()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -156,6 +188,53 @@ class Clocks:
 # --------------------------------------------------------------------------------
 # our arm
 
+def local_initial_state(case, cfg, ctx, weak, rank):
+    """The rank's block of the config's initial state (layout L).  Strong
+    scaling: the global field's block, with the C3 noise drawn once for the
+    whole global mesh in global layout order (same numbers as on 1 GPU).
+    Weak scaling: this rank's copy of the config tile, noise stream rank."""
+    import numpy as np
+    from paper_2109_04804_b200 import inputs
+    coords = ctx.node_coords()
+    if weak:
+        coords = inputs.tile_coords(coords, cfg.bounds)
+        W = inputs.initial_state(case, coords, noise=cfg.noise, stream=rank)
+        Wc = inputs.initial_state(case, coords)
+        return W, Wc
+    Wc = inputs.initial_state(case, coords)
+    W = Wc
+    if cfg.noise:
+        rng = np.random.default_rng(inputs.MASTER_SEED + inputs.CASE_INDEX[case])
+        full = rng.uniform(-cfg.noise, cfg.noise, size=cfg.n).reshape(cfg.ny, cfg.nx, cfg.m)
+        blk = full[ctx.ey0:ctx.ey0 + ctx.ny_local, ctx.ex0:ctx.ex0 + ctx.nx_local].reshape(-1)
+        W = Wc + blk
+    return W, Wc
+
+
+def global_dt(cfg, Wc_local, use_dist):
+    """Element-CFL dt (reading R14) of the global discrete IC (before noise): the
+    rule is a max over nodes, so each rank evaluates its block and the ranks take
+    the max wave-speed sum (max all-reduce); identical on every rank."""
+    import torch
+    import torch.distributed as dist
+    from paper_2109_04804_b200 import configs
+    dt = configs.cfl_dt(cfg, Wc_local)
+    if use_dist:
+        t = torch.tensor([1.0 / dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = 1.0 / float(t.item())
+    return dt
+
+
+def relaunch_under_torchrun(args):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -165,130 +244,192 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench: --gpus {world} but only {torch.cuda.device_count()} CUDA devices")
     torch.cuda.set_device(local)
     # one dedicated stream for torch and the library (no legacy-default-stream syncs)
     torch.cuda.set_stream(torch.cuda.Stream(device=local))
-    # torchrun sets MASTER_ADDR/RANK even for one process: the distributed
-    # plumbing then runs at N = 1 too (with --self-halo it is fully exercised)
     use_dist = world > 1 or ("MASTER_ADDR" in os.environ and "RANK" in os.environ)
     if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = configs.CONFIGS[CONFIG]
-    # N > 1: ONE global problem, C3's 128x128-element tile repeated on a px x py
-    # rank grid (a (128 px) x (128 py) mesh of the periodic vortex field, same h,
-    # N, dt and tolerances), element-partitioned with one 128x128 block per GPU:
-    # face-trace halos and Krylov/norm all-reduces over NCCL.
-    # Per-GPU work is C3's: weak scaling.  DESIGN.md "Multi-GPU".
-    px, py = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}.get(world, (world, 1))
+    case = args.config
+    cfg = configs.CONFIGS[case]
+    scaling = args.scaling or ("weak" if case == "C3" else "strong")
+    weak = scaling == "weak"
+    px, py = PARTS.get(world, (world, 1))
     kw = {}
     if world > 1 or args.self_halo:
         nid = [hbpdc.nccl_unique_id() if rank == 0 else None]
         if use_dist:
             dist.broadcast_object_list(nid, src=0)
-        kw = dict(nx=cfg.nx * px, ny=cfg.ny * py,
-                  bounds=(cfg.bounds[0], cfg.bounds[0] + px * (cfg.bounds[1] - cfg.bounds[0]),
-                          cfg.bounds[2], cfg.bounds[2] + py * (cfg.bounds[3] - cfg.bounds[2])),
-                  rank=rank, nranks=world, px=px, py=py, comm="nccl", nccl_id=nid[0],
+        kw = dict(rank=rank, nranks=world, px=px, py=py, comm="nccl", nccl_id=nid[0],
                   force_halo=bool(args.self_halo))
+        if weak:
+            # one copy of the config's mesh per GPU: a (nx px) x (ny py) tiling
+            kw.update(nx=cfg.nx * px, ny=cfg.ny * py,
+                      bounds=(cfg.bounds[0], cfg.bounds[0] + px * (cfg.bounds[1] - cfg.bounds[0]),
+                              cfg.bounds[2], cfg.bounds[2] + py * (cfg.bounds[3] - cfg.bounds[2])))
     if args.precond:
         kw["precond"] = args.precond
     if args.nodes != "gll" or args.flux != "llf":
         kw.update(nodes=args.nodes, flux=args.flux)      # the paper's own discretisation choices (NEXT-3)
-    ctx = hbpdc.context_for(cfg, device=local, gmres_sstep=args.gmres_sstep, **kw)
-    coords = inputs.tile_coords(ctx.node_coords(), cfg.bounds)
-    W0 = inputs.initial_state(CONFIG, coords, noise=cfg.noise, stream=rank)
-    dt = configs.cfl_dt(cfg, inputs.initial_state(CONFIG, coords))
+    # memory plan: the lock-step corrector workspaces (NEXT-1) need (s-1) Krylov bases;
+    # C4 on few GPUs has room for one (137 GB of BJ_ext blocks on 1 GPU)
+    batch = args.batch_stages
+    if batch is None:
+        batch = not (case == "C4" and world < 4)
+    ctx = hbpdc.context_for(cfg, device=local, gmres_sstep=args.gmres_sstep, batch_stages=batch, **kw)
+    W0, Wc = local_initial_state(case, cfg, ctx, weak, rank)
+    dt = global_dt(cfg, Wc, use_dist)
     stream = ctx.stream
-    W = torch.tensor(W0, dtype=torch.float64, device=f"cuda:{local}")
+    dev = f"cuda:{local}"
+    W = torch.tensor(W0, dtype=torch.float64, device=dev)
     for _ in range(args.warmup):
         ctx.step(dt, W)
     torch.cuda.synchronize()
+    W_start = W.clone()
+    W_start_h = W_start.cpu().pin_memory()
     if use_dist:
         dist.barrier()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, profiling off -----------------------------------
     clocks = Clocks(local)
     clocks.start()
-    ctx.profile(True)
     l0 = hbpdc.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     stats = []
-    torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(args.steps):
         stats.append(ctx.step(dt, W))
     ev1.record(stream)
     torch.cuda.synchronize()
     launches = hbpdc.launch_count() - l0
-    ms = ev0.elapsed_time(ev1)
-    prof = {name: ctx.profile_read(i) for name, i in hbpdc.Context.PROFILE_IDS.items()}
-    ctx.profile(False)
     ck = clocks.stop()
-    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * args.steps / (ms_max / 1e3)
-
-    # dominant kernel + roofline (algorithmic bytes / CUDA-event time)
-    peak, peak_kind = measured_peaks()
-    dom = max(prof.items(), key=lambda kv: kv[1][1])
-    dname, (dn, dms, dbytes) = dom
-    achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
-    kernels = {k: {"launches": v[0], "ms": round(v[1], 3), "share": round(v[1] / ms, 4),
-                   "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1) if v[1] > 0 else None}
-               for k, v in prof.items()}
-    # DRAM traffic per launch: average algorithmic bytes x the DRAM/algorithmic
-    # ratio measured by ncu for this kernel (profiles/ncu_traffic.json)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp) and dn:
-        ratio = json.load(open(tp)).get(dname)
-        if isinstance(ratio, (int, float)):
-            traffic = round(dbytes / dn * ratio)
-
-    # matrix-free FD JVP throughput on the C3 state (second headline of the metric)
+    units = world if weak else 1                    # config-tile steps per global step
+    value = units * args.steps / (ms_max / 1e3)
     n = ctx.n
-    g = torch.Generator(device="cpu").manual_seed(inputs.MASTER_SEED + 200)
-    sig = ctx.rhs(W)
-    dW = torch.randn(n, generator=g, dtype=torch.float64).to(W.device)
-    dS = torch.randn(n, generator=g, dtype=torch.float64).to(W.device)
-    o1, o2 = ctx.empty(), ctx.empty()
-    for _ in range(3):
-        ctx.jvp(1.0, 1.0, dt, W, sig, dW, dS, mode="fd", out1=o1, out2=o2)
-    reps = 20
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(reps):
-        ctx.jvp(1.0, 1.0, dt, W, sig, dW, dS, mode="fd", out1=o1, out2=o2)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    jms = ev0.elapsed_time(ev1) / reps
-    jvp_rate = n / (jms / 1e3)
-    jvp_gbps = 48.0 * n / (jms / 1e3) / 1e9
+    n_global = n * world if weak or world > 1 else n
 
-    # end to end through the C-ABI with HOST buffers (H2D + step + D2H per step)
+    # ---- e2e: the same K steps from the same state, through the C-ABI with a host buffer
     e2e = None
     if not args.no_e2e:
-        Wh = torch.tensor(W0, dtype=torch.float64).pin_memory()
-        ctx.reset()
-        ctx.step_host(dt, Wh.numpy())                 # warm
-        torch.cuda.synchronize()
+        Wh = W_start_h.clone().pin_memory().numpy()
+        ctx.reset()                                   # the FSAL cache belongs to the device run
         if use_dist:
             dist.barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            ctx.step_host(dt, Wh.numpy())
-        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
+        for _ in range(args.steps):
+            ctx.step_host(dt, Wh)
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if use_dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * args.e2e_steps / float(te.item()), "unit": UNIT,
-               "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8, "steps": args.e2e_steps}
+        e2e = {"value": units * args.steps / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8, "steps": args.steps,
+               "note": "same K steps from the same start state as value, hbpdc_step_host per step"}
+
+    # ---- profiled pass (per-kernel CUDA events; not part of value) -----------------
+    peak, peak_kind = measured_peaks()
+    kernels, dom, step_roof, pstats = {}, None, None, []
+    if args.profile_steps > 0:
+        ctx.reset()
+        Wp = W_start.clone()
+        ctx.profile(True)
+        ev0.record(stream)
+        for _ in range(args.profile_steps):
+            pstats.append(ctx.step(dt, Wp))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        pms = ev0.elapsed_time(ev1)
+        prof = {name: ctx.profile_read(i) for name, i in hbpdc.Context.PROFILE_IDS.items()}
+        ctx.profile(False)
+        for k, (nl, kms, kb) in prof.items():
+            kernels[k] = {"launches": nl, "ms": round(kms, 3), "share": round(kms / pms, 4),
+                          "GBps": round(kb / (kms / 1e3) / 1e9, 1) if kms > 0 and kb > 0 else None}
+        dom = max((kv for kv in prof.items() if kv[0] != "build"), key=lambda kv: kv[1][1])
+        # step-level roofline: sum over the step's profiled calls of
+        # algorithmic bytes / BW, plus the BJ_ext build flops / FP64 peak, over the time
+        builds = sum(s["precond_builds"] for s in pstats)
+        m = ctx.m
+        build_flops = builds * ctx.n_elem * 4.0 * m ** 3      # K^2 (2 m^3) + Gauss-Jordan inverse (2 m^3)
+        ideal_ms = sum(kb for k, (nl, kms, kb) in prof.items() if k != "build") / (peak * 1e9) * 1e3 \
+            + build_flops / (FP64_PEAK_TFLOPS * 1e12) * 1e3
+        covered = sum(kms for kms in (v[1] for v in prof.values()))
+        step_roof = {"ideal_ms": round(ideal_ms, 1), "measured_ms": round(pms, 1),
+                     "frac": round(ideal_ms / pms, 4), "profiled_share": round(covered / pms, 4),
+                     "model": "sum of (algorithmic bytes / measured HBM BW) over the profiled kernels + "
+                              f"builds x elements x 4 m^3 / {FP64_PEAK_TFLOPS} TFLOP/s (K^2 + inverse), "
+                              "over the profiled steps' device time",
+                     "steps": args.profile_steps}
+
+    # ---- kernel micro-timings on the current state (C-ABI calls) ----------------------
+    g = torch.Generator(device="cpu").manual_seed(inputs.MASTER_SEED + 200)
+    sig = ctx.rhs(W)
+    dW = torch.randn(n, generator=g, dtype=torch.float64).to(dev)
+    dS = torch.randn(n, generator=g, dtype=torch.float64).to(dev)
+    o1, o2 = ctx.empty(), ctx.empty()
+    b = W.clone()
+
+    def timeit(fn, reps=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(reps):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / reps
+
+    jms = timeit(lambda: ctx.jvp(1.0, 1.0, dt, W, sig, dW, dS, mode="fd", out1=o1, out2=o2))
+    rms = timeit(lambda: ctx.residual(0.5, 1.0 / 6, dt, b, W, sig, G1=o1, G2=o2))
+    # bytes per W-DOF: JVP reads W, sigma, dW, dsigma, writes 2 blocks (48; NS +48 for the
+    # lifted gradients); residual reads W, sigma, b, writes 2 blocks (40)
+    jb = 48 + (48 if cfg.equation == "navier_stokes" else 0)
+    micro = {"jvp_fd": {"dof_applies_per_s": n_global / (jms / 1e3) if not weak else n / (jms / 1e3),
+                        "ms": jms, "bytes_per_dof": jb,
+                        "GBps_alg": round(jb * n / (jms / 1e3) / 1e9, 1),
+                        "frac_hbm": round(jb * n / (jms / 1e3) / 1e9 / peak, 4)},
+             "residual": {"ms": rms, "bytes_per_dof": 40 + (48 if cfg.equation == "navier_stokes" else 0),
+                          "GBps_alg": round((40 + (48 if cfg.equation == "navier_stokes" else 0)) * n / (rms / 1e3) / 1e9, 1)}}
+    micro["residual"]["frac_hbm"] = round(micro["residual"]["GBps_alg"] / peak, 4)
+    fp64p = os.path.join(ROOT, "profiles", "ncu_fp64.json")
+    if os.path.exists(fp64p):
+        f = json.load(open(fp64p)).get(case, {})
+        for k in ("jvp_fd", "residual"):
+            if k in f:
+                micro[k]["fp64_pipe_frac_ncu"] = f[k]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sec, desc, scale = oracle_sample()
-        cpu = {"value": 1.0 / (sec * scale), "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
-               "sample": desc, "sample_seconds": round(sec, 2)}
+        sec, cpus, desc, scale = oracle_sample(case)
+        cpu = {"value": 1.0 / (sec * scale), "unit": UNIT, "cores": round(cpus / sec, 2), "kind": "oracle",
+               "sample": desc, "sample_seconds": round(sec, 2),
+               "cores_note": "process CPU time / wall time of the sample", "host_cpus": os.cpu_count()}
+
+    roof = None
+    if dom is not None:
+        dname, (dn, dms, dbytes) = dom
+        achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp) and dn:
+            ratio = json.load(open(tp)).get(dname)
+            if isinstance(ratio, (int, float)):
+                traffic = round(dbytes / dn * ratio)
+        roof = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "launches": dn}
 
     if rank == 0:
         it = {k: sum(s[k] for s in stats) for k in ("stage_solves", "newton_its", "gmres_its",
@@ -296,25 +437,25 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C3: 2D Euler isentropic vortex (beta=5, mean (1,1)) + seeded U[-1e-6,1e-6) "
-                                   f"noise, [-5,5]^2 periodic, 128x128 elements, N=7 {args.nodes.upper()}, "
-                                   f"{args.flux.upper()}, HBPC(8,4), "
-                                   "BJ_ext, FD JVP, Newton/GMRES rtol 1e-10, restart 700",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg, args), "config": case,
                        "arnoldi": ("DCGS2" if args.gmres_sstep <= 1 else f"s-step s={args.gmres_sstep} (block CGS2)"),
-                       "precond": args.precond or cfg.precond,
-                       "nodes": args.nodes, "flux": args.flux,
-                       "dt": dt, "n_dof_per_gpu": n, "n_dof": n * world,
-                       "parallelism": (f"element partition {px}x{py} of a {cfg.nx * px}x{cfg.ny * py} mesh "
-                                       "(C3 tile per GPU), NCCL halos + all-reduces") if world > 1 else
+                       "precond": args.precond or cfg.precond, "nodes": args.nodes, "flux": args.flux,
+                       "lockstep_correctors": bool(batch),
+                       "dt": dt, "n_dof_per_gpu": n, "n_dof": n_global,
+                       "parallelism": (f"{scaling} scaling: element partition {px}x{py} of a "
+                                       f"{cfg.nx * (px if weak else 1)}x{cfg.ny * (py if weak else 1)} mesh, "
+                                       "NCCL halos + all-reduces") if world > 1 else
                                       ("1 GPU, NCCL self-halo" if args.self_halo else "1 GPU"),
-                       "l2": "working set > L2 (BJ_ext blocks 8.6 GB, Krylov basis up to 47 GB)"},
-            "roofline": {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "launches": dn},
+                       "value_unit": ("config-tile steps/s (one copy of the config mesh per GPU)" if weak and world > 1
+                                      else "global time steps/s"),
+                       "l2": "working set > L2 (BJ_ext blocks + Krylov basis, GBs): no flush needed"},
+            "global_steps_per_s": args.steps / (ms_max / 1e3),
+            "dof_steps_per_s": n_global * args.steps / (ms_max / 1e3),
+            "roofline": roof,
+            "step_roofline": step_roof,
             "kernels": kernels,
-            "jvp": {"dof_applies_per_s": jvp_rate, "ms": jms, "GBps_alg": round(jvp_gbps, 1),
-                    "frac": round(jvp_gbps / peak, 4), "bytes_per_dof": 48},
+            "micro": micro,
             "solver": it,
             "clocks": ck,
             "e2e": e2e,
@@ -333,24 +474,32 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5"])
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N > 1: weak (a config tile per GPU; C3 default) or strong (one mesh; C4/C5 default)")
+    ap.add_argument("--profile-steps", type=int, default=1,
+                    help="steps of the separate profiled pass (per-kernel table, step roofline); 0 = none")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch-stages", type=int, default=None, choices=[0, 1],
+                    help="lock-step corrector stages (default: on, except C4 below 4 GPUs: memory)")
     ap.add_argument("--precond", default=None, choices=["bjext", "bjext_h", "none"],
-                    help="override the config's preconditioner (default: C3's BJ_ext)")
+                    help="override the config's preconditioner (default: BJ_ext)")
     ap.add_argument("--gmres-sstep", type=int, default=8,
                     help="Arnoldi schedule: 1 = DCGS2, 2/4/8 = s-step blocks")
     ap.add_argument("--nodes", default="gll", choices=["gll", "gl"],
-                    help="DGSEM nodes (C3: GLL; gl = the paper's Gauss-Legendre, NEXT-3)")
+                    help="DGSEM nodes (configs: GLL; gl = the paper's Gauss-Legendre, NEXT-3)")
     ap.add_argument("--flux", default="llf", choices=["llf", "glf"],
-                    help="numerical flux (C3: LLF; glf = the paper's global LF, NEXT-3)")
+                    help="numerical flux (configs: LLF; glf = the paper's global LF, NEXT-3)")
     ap.add_argument("--self-halo", action="store_true",
                     help="test hook: route the periodic wrap through the NCCL transport (N = 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    run_ours(args)
 
 
 if __name__ == "__main__":

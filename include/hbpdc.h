@@ -75,8 +75,9 @@ typedef struct {
   int nodes;            /* HBPDC_GLL (configs, reading R1) or HBPDC_GL       */
   int nx, ny;           /* global element counts (ny ignored in 1D)                */
   double xmin, xmax, ymin, ymax;   /* periodic Cartesian domain                   */
-  int flux;             /* HBPDC_LLF (reading R3) | HBPDC_GLF_PAPER (eq:Riemann, P:197-201:
-                           constant Lambda = diag(1/eps,1,1,1/eps), eps = 1; |a.n| for advection) */
+  int flux;             /* HBPDC_LLF (reading R3) | HBPDC_GLF_PAPER (eq:Riemann, P:197-201,
+                           literally: 1/2 (F_L + F_R).n + Lambda (w_L - w_R), no 1/2 on the
+                           jump; Lambda = diag(1/eps,1,1,1/eps), |a.n|) */
   int lifting;          /* HBPDC_BR1 (NS, reading R19) | HBPDC_BR2 (reading R33) */
   int q, kmax;          /* HBPC(q, k_max), q in {4, 6, 8}, k_max >= 0              */
   double eta_br2;       /* BR2 stabilisation parameter eta (> 0; the paper gives no
@@ -210,8 +211,11 @@ HBPDC_API hbpdc_status hbpdc_precond_build(hbpdc_ctx* ctx, double alpha1, double
 HBPDC_API hbpdc_status hbpdc_precond_set(hbpdc_ctx* ctx, double alpha1, double alpha2, double dt,
                                const double* W, const double* S, int shared);
 
-/* Copy the current S blocks to a device array (n_local_elems*m*m or m*m). */
-HBPDC_API hbpdc_status hbpdc_precond_export(hbpdc_ctx* ctx, double* S_out, int* shared);
+/* Copy the current S blocks to the device array S_out of `capacity` doubles:
+ * n_local_elems*m*m doubles, or m*m when *shared = 1 (advection: one block for
+ * all elements).  S_out = NULL only reports *shared (size query).  A capacity
+ * below the block count returns HBPDC_E_ARG without writing.  Test hook. */
+HBPDC_API hbpdc_status hbpdc_precond_export(hbpdc_ctx* ctx, double* S_out, size_t capacity, int* shared);
 
 /* P^-1 X per element: (D W + E s ; F W + G s), evaluated as
  * u = S W, v = S s, top = u - c2 K v, bottom = v + K (u - a1 dt v). */
@@ -225,7 +229,10 @@ HBPDC_API hbpdc_status hbpdc_step(hbpdc_ctx* ctx, double dt, double* W, hbpdc_st
 /* Same, with W a HOST array: host->device copy, step, device->host copy. */
 HBPDC_API hbpdc_status hbpdc_step_host(hbpdc_ctx* ctx, double dt, double* W_host, hbpdc_step_stats* stats);
 
-/* Forget the FSAL cache (the next step recomputes R1/R2 of its input). */
+/* Forget the FSAL cache (the next step recomputes R1/R2 of its input).
+ * hbpdc_step reuses R1/R2 of its previous output (FSAL) only when it is
+ * called with that same device array and unchanged contents (pointer and a
+ * 64-bit fingerprint of W are checked); any other W recomputes them. */
 HBPDC_API hbpdc_status hbpdc_reset(hbpdc_ctx* ctx);
 
 /* Per-kernel timing (CUDA events on the context stream), for roofline

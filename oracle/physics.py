@@ -23,7 +23,11 @@ BASELINE configs name LLF/Rusanov, so the configs use
     lambda_f = max(|v_L.e_d| + c_L, |v_R.e_d| + c_R),
 evaluated in the canonical orientation of a face (L = the element on the
 -e_d side, normal +e_d); ties take L, sign(0) = +1.  For advection
-lambda_f = |a_d| and f* is the exact upwind flux.
+lambda_f = |a_d| and f* is the exact upwind flux.  numflux = "glf" is the
+paper's eq:Riemann literally:
+    f*(wL, wR; e_d) = 1/2 (F_d(wL) + F_d(wR)) + Lambda (wL - wR),
+Lambda = |a_d| (advection) or diag(1/eps, 1, 1, 1/eps) (Euler / NS), no 1/2
+on the jump term (0.45 for a = (0.3, 0.3), wL = 1, wR = 0).
 """
 from dataclasses import dataclass
 
@@ -101,7 +105,10 @@ def glf(eq, wL, wR, d):
     else:
         eps = eq.mach
         lam = (1.0 / eps, 1.0, 1.0, 1.0 / eps)
-    return tuple(0.5 * (fl + fr) + 0.5 * lv * (l - r)
+    # eq:Riemann: (1/2 (F_L + F_R) + lambda (w_L - w_R)) . n -- the jump term
+    # carries the full lambda, no 1/2 (S:159 gives 0.45 for its example),
+    # and is not projected on n.
+    return tuple(0.5 * (fl + fr) + lv * (l - r)
                  for fl, fr, l, r, lv in zip(FL, FR, wL, wR, lam))
 
 

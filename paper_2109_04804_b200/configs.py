@@ -85,7 +85,7 @@ def cfl_dt(cfg: Config, W):
         s = sum(abs(cfg.a[d]) / h[d] for d in range(cfg.dim))
         return cfg.cfl / s
     nd = cfg.p ** cfg.dim
-    Wv = np.asarray(W).reshape(cfg.n_elem, cfg.nv, nd)
+    Wv = np.asarray(W).reshape(-1, cfg.nv, nd)      # any block of whole elements
     rho, mx, my, E = (Wv[:, k] for k in range(4))
     u, v = mx / rho, my / rho
     p = (cfg.gamma - 1.0) * (E - 0.5 * rho * (u * u + v * v))

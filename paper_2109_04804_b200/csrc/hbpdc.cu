@@ -126,6 +126,8 @@ struct hbpdc_ctx {
   double *stw[2][4] = {}, *str1[2][4] = {}, *str2[2][4] = {};
   double *Wn = nullptr, *Wio = nullptr;
   int fsal_valid = 0;
+  const double* fsal_ptr = nullptr;      // the W the FSAL cache belongs to (the last step's output)
+  unsigned long long* dfp = nullptr;     // device fingerprints: [0] last output, [1] incoming W
   double* hpin = nullptr;      // pinned host scratch (norms)
   // profiling
   int prof_on = 0;
@@ -710,6 +712,8 @@ struct LinSys {
   bool pc;
 };
 
+constexpr double GMRES_STAGNATION = 0.9;   // reading R34, the same constant as the CPU checker
+
 struct GState {
   SysWS* w = nullptr;
   LinSys L{};
@@ -813,7 +817,11 @@ hbpdc_status g_cycle_end(hbpdc_ctx* c, GState& g) {
   use_ghosts(c, w);
   CKS(sys_matvec(c, g, w.dX, w.r));
   CK(launch_axpby(1.0, w.rhs, -1.0, w.r, n2, c->stream));
+  const double beta_start = g.beta;
   CKS(norm_host(c, w.r, n2, &g.beta));
+  // stagnation (reading R34, as the oracle): a cycle that lowered the true residual by
+  // less than 10 % has reached the FD JVP's noise level; x goes back to Newton
+  if (g.beta > GMRES_STAGNATION * beta_start && !(g.beta <= c->op.gmres_rtol * g.beta0)) g.converged = g.done = true;
   return HBPDC_OK;
 }
 
@@ -1391,6 +1399,19 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
   const int s = T.s;
   int cur = 0;
   CK(cudaMemcpyAsync(c->Wn, W, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (c->fsal_valid) {
+    // the cached R1/R2 belong to the previous step's output: reuse them only if W is that
+    // array with unchanged contents (pointer + fingerprint), else recompute
+    if (W != c->fsal_ptr) {
+      c->fsal_valid = 0;
+    } else {
+      unsigned long long fp[2];
+      CK(launch_fingerprint(W, n, c->dfp + 1, c->stream));
+      CK(cudaMemcpyAsync(fp, c->dfp, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (fp[0] != fp[1]) c->fsal_valid = 0;
+    }
+  }
   if (!c->fsal_valid) CKS(stage_ops(c, c->Wn, c->str1[cur][0], c->str2[cur][0]));
   c->pc_valid = c->pc_valid ? 1 : 0;   // a build from an earlier step is not at this W^n
   CK(cudaMemcpyAsync(c->stw[cur][0], c->Wn, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -1466,6 +1487,8 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
     CK(cudaMemcpyAsync(c->str2[0][0], c->str2[0][s - 1], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   }
   c->fsal_valid = 1;
+  c->fsal_ptr = W;
+  CK(launch_fingerprint(W, n, c->dfp, c->stream));
   if (c->pc_valid == 2) c->pc_valid = 1;
   return HBPDC_OK;
 }
@@ -1515,6 +1538,7 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
     w.hpin = (double*)hp;
   }
   CKS(dalloc(c, &c->partial, RED_BLOCKS));
+  CKS(dalloc(c, (double**)&c->dfp, 2));
   CKS(dalloc(c, &c->dnrm, 1));
   CKS(dalloc(c, &c->deps, 2));
   CKS(dalloc(c, &c->Wn, n));
@@ -1861,12 +1885,16 @@ hbpdc_status hbpdc_precond_set(hbpdc_ctx* c, double a1, double a2, double dt, co
   return HBPDC_OK;
 }
 
-hbpdc_status hbpdc_precond_export(hbpdc_ctx* c, double* S_out, int* shared) {
-  if (!c || !S_out) return HBPDC_E_ARG;
+hbpdc_status hbpdc_precond_export(hbpdc_ctx* c, double* S_out, size_t capacity, int* shared) {
+  if (!c) return HBPDC_E_ARG;
   if (!c->pc_valid) return fail(c, HBPDC_E_ARG, "no preconditioner built");
   const size_t nblk = c->s_shared ? 1 : (size_t)c->nE;
-  CK(cudaMemcpyAsync(S_out, c->S, nblk * c->m * c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   if (shared) *shared = c->s_shared;
+  if (!S_out) return HBPDC_OK;                 // query only: *shared tells the size
+  if (capacity < nblk * c->m * c->m)
+    return fail(c, HBPDC_E_ARG, "precond_export: S_out holds " + std::to_string(capacity) + " doubles, " +
+                                    std::to_string(nblk * c->m * c->m) + " needed");
+  CK(cudaMemcpyAsync(S_out, c->S, nblk * c->m * c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   return HBPDC_OK;
 }
 

@@ -116,6 +116,8 @@ cudaError_t launch_finish_norm(const double* partial, double* out, cudaStream_t 
 // out = c / sqrt(sum partial), or 0 if the sum is 0   (FD step)
 // eps_FD from np partial sums of ||dW||^2 (np <= 0: RED_BLOCKS)
 cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st, int np = 0);
+// order-independent 64-bit fingerprint of x into *out (device), FSAL cache validation
+cudaError_t launch_fingerprint(const double* x, size_t L, unsigned long long* out, cudaStream_t st);
 // HBPC quadrature: y = base + sum_j a[j] X_j + sum_j b[j] Y_j  (host coefficient arrays, <= 8 terms)
 cudaError_t launch_stage_combo(const double* base, int nx, const double* const* X, const double* a,
                                int ny, const double* const* Y, const double* b, double* y, size_t L,

@@ -1189,6 +1189,26 @@ cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, c
   return cudaGetLastError();
 }
 
+// order-independent 64-bit fingerprint of x: sum_i bits(x_i) * (2 i + 1) mod 2^64
+// (integer addition is associative: deterministic for any launch shape)
+__global__ void fingerprint_kernel(const double* __restrict__ x, size_t L, unsigned long long* out) {
+  unsigned long long h = 0ull;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride)
+    h += (unsigned long long)__double_as_longlong(x[i]) * (2ull * i + 1ull);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+
+cudaError_t launch_fingerprint(const double* x, size_t L, unsigned long long* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  fingerprint_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(x, L, out);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
 struct ComboArgs {
   const double* base;
   const double* X[8];

@@ -264,9 +264,10 @@ __device__ __forceinline__ void face_from_halves(const PhysParams& pp, const dou
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    if (EQ != 0 && pp.glf) {       // as llf_flux: constant Lambda = diag(1/eps, 1, 1, 1/eps)
-      const double lv = (v == 0 || v == NV - 1) ? pp.ieps : 1.0;
-      f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + (0.5 * lv) * (rd(rL, NV + v) - rd(rR, NV + v));
+    if (pp.glf) {       // as llf_flux: eq:Riemann with the constant Lambda, no 1/2 on the jump
+      const double lv = EQ == 0 ? (d == 0 ? fabs(pp.ax) : fabs(pp.ay))
+                                : ((v == 0 || v == NV - 1) ? pp.ieps : 1.0);
+      f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + lv * (rd(rL, NV + v) - rd(rR, NV + v));
     } else {
       f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + 0.5 * lam * (rd(rL, NV + v) - rd(rR, NV + v));
     }

@@ -7,8 +7,9 @@
 //              lam = max(|v_L.e_d| + c_L, |v_R.e_d| + c_R)  (reading R3; the paper's
 //              eq:Riemann is the global-lambda variant).  Canonical orientation:
 //              L = element on the -e_d side, normal +e_d; ties take L.
-//  GLF       : (pp.glf, HBPDC_GLF_PAPER) the paper's eq:Riemann with the constant
-//              Lambda = diag(1/eps, 1, 1, 1/eps) of P:395; advection |a_d| as LLF.
+//  GLF       : (pp.glf, HBPDC_GLF_PAPER) the paper's eq:Riemann literally:
+//              f* = 1/2 (F_d(wL) + F_d(wR)) + Lambda (wL - wR), the full Lambda on the jump
+//              (no 1/2), Lambda = diag(1/eps, 1, 1, 1/eps), advection |a_d|.
 //  eps       : reference Mach number (mach_eps): momentum flux p / eps^2, p with eps^2 in
 //              the kinetic energy, wave speed |v.n| + c / eps (Euler; NS only at eps = 1).
 //  NS        : viscous flux F^v with BR1 gradients (reading R19).
@@ -89,9 +90,11 @@ __device__ __forceinline__ void llf_flux(const PhysParams& pp, const T* wL, cons
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    if (EQ != 0 && pp.glf) {       // constant Lambda = diag(1/eps, 1, 1, 1/eps)
-      const double lv = (v == 0 || v == NV - 1) ? pp.ieps : 1.0;
-      f[v] = 0.5 * (FL[v] + FR[v]) + (0.5 * lv) * (wL[v] - wR[v]);
+    if (pp.glf) {       // eq:Riemann: full Lambda on the jump, no 1/2; Lambda = |a_d|,
+                        // diag(1/eps, 1, 1, 1/eps)
+      const double lv = EQ == 0 ? (d == 0 ? fabs(pp.ax) : fabs(pp.ay))
+                                : ((v == 0 || v == NV - 1) ? pp.ieps : 1.0);
+      f[v] = 0.5 * (FL[v] + FR[v]) + lv * (wL[v] - wR[v]);
     } else {
       f[v] = 0.5 * (FL[v] + FR[v]) + 0.5 * lam * (wL[v] - wR[v]);
     }

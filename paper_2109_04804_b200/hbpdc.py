@@ -95,7 +95,7 @@ def load():
         "hbpdc_jvp": (I, [P, D, D, D, P, P, P, P, P, P, I, P]),
         "hbpdc_precond_build": (I, [P, D, D, D, P]),
         "hbpdc_precond_set": (I, [P, D, D, D, P, P, I]),
-        "hbpdc_precond_export": (I, [P, P, ctypes.POINTER(I)]),
+        "hbpdc_precond_export": (I, [P, P, ctypes.c_size_t, ctypes.POINTER(I)]),
         "hbpdc_precond_apply": (I, [P, P, P, P, P]),
         "hbpdc_step": (I, [P, D, P, ctypes.POINTER(StepStats)]),
         "hbpdc_step_host": (I, [P, D, P, ctypes.POINTER(StepStats)]),
@@ -167,12 +167,15 @@ class HbpdcError(RuntimeError):
         self.status = status
 
 
-def _ptr(t):
+def _ptr(t, n=None):
+    """Device pointer of a contiguous float64 CUDA tensor holding at least n doubles."""
     if t is None:
         return None
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise TypeError("expected a contiguous float64 CUDA tensor")
+    if n is not None and t.numel() < n:
+        raise ValueError(f"tensor holds {t.numel()} doubles, the call needs {n}")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -252,15 +255,15 @@ class Context:
     # -- operators -------------------------------------------------------------------
     def rhs(self, W, sigma=None, out=None):
         out = self.empty() if out is None else out
-        self._check(self.lib.hbpdc_rhs(self.h, _ptr(W), _ptr(sigma), _ptr(out)))
+        self._check(self.lib.hbpdc_rhs(self.h, _ptr(W, self.n), _ptr(sigma, self.n), _ptr(out, self.n)))
         return out
 
     def residual(self, a1, a2, dt, b, W, sigma, G1=None, G2=None, norm=False):
         G1 = self.empty() if G1 is None else G1
         G2 = self.empty() if G2 is None else G2
         nrm = ctypes.c_double()
-        self._check(self.lib.hbpdc_residual(self.h, a1, a2, dt, _ptr(b), _ptr(W), _ptr(sigma), _ptr(G1),
-                                            _ptr(G2), ctypes.byref(nrm) if norm else None))
+        self._check(self.lib.hbpdc_residual(self.h, a1, a2, dt, _ptr(b, self.n), _ptr(W, self.n), _ptr(sigma, self.n), _ptr(G1, self.n),
+                                            _ptr(G2, self.n), ctypes.byref(nrm) if norm else None))
         return (G1, G2, nrm.value) if norm else (G1, G2)
 
     def jvp(self, a1, a2, dt, W, sigma, dW, dsigma, mode="auto", eps_override=None, out1=None, out2=None):
@@ -270,43 +273,49 @@ class Context:
         if eps_override is not None:
             arr = (ctypes.c_double * 2)(*[(-1.0 if e is None else e) for e in eps_override])
             eo = ctypes.cast(arr, ctypes.c_void_p)
-        self._check(self.lib.hbpdc_jvp(self.h, a1, a2, dt, _ptr(W), _ptr(sigma), _ptr(dW), _ptr(dsigma),
-                                       _ptr(out1), _ptr(out2), _JVP[mode], eo))
+        self._check(self.lib.hbpdc_jvp(self.h, a1, a2, dt, _ptr(W, self.n), _ptr(sigma, self.n), _ptr(dW, self.n), _ptr(dsigma, self.n),
+                                       _ptr(out1, self.n), _ptr(out2, self.n), _JVP[mode], eo))
         return out1, out2
 
     def precond_build(self, a1, a2, dt, W):
-        self._check(self.lib.hbpdc_precond_build(self.h, a1, a2, dt, _ptr(W)))
+        self._check(self.lib.hbpdc_precond_build(self.h, a1, a2, dt, _ptr(W, self.n)))
 
     def precond_set(self, a1, a2, dt, W, S, shared):
-        self._check(self.lib.hbpdc_precond_set(self.h, a1, a2, dt, _ptr(W), _ptr(S), int(shared)))
+        self._check(self.lib.hbpdc_precond_set(self.h, a1, a2, dt, _ptr(W, self.n),
+                                               _ptr(S, self.m * self.m * (1 if shared else self.n_elem)), int(shared)))
 
     def precond_export(self, shared_hint=None):
+        """(S blocks as a device tensor, shared flag); the size comes from the library
+        (shared_hint is accepted for compatibility and ignored)."""
         import torch
-        sh = shared_hint if shared_hint is not None else None
-        nblk = 1 if sh else self.n_elem
-        S = torch.empty(nblk * self.m * self.m, dtype=torch.float64, device=f"cuda:{self.device}")
         flag = ctypes.c_int()
-        self._check(self.lib.hbpdc_precond_export(self.h, _ptr(S), ctypes.byref(flag)))
+        self._check(self.lib.hbpdc_precond_export(self.h, None, 0, ctypes.byref(flag)))
+        nblk = 1 if flag.value else self.n_elem
+        S = torch.empty(nblk * self.m * self.m, dtype=torch.float64, device=f"cuda:{self.device}")
+        self._check(self.lib.hbpdc_precond_export(self.h, _ptr(S), S.numel(), ctypes.byref(flag)))
         return S, bool(flag.value)
 
     def precond_apply(self, inW, insig, outW=None, outsig=None):
         outW = self.empty() if outW is None else outW
         outsig = self.empty() if outsig is None else outsig
-        self._check(self.lib.hbpdc_precond_apply(self.h, _ptr(inW), _ptr(insig), _ptr(outW), _ptr(outsig)))
+        self._check(self.lib.hbpdc_precond_apply(self.h, _ptr(inW, self.n), _ptr(insig, self.n), _ptr(outW, self.n), _ptr(outsig, self.n)))
         return outW, outsig
 
     def step(self, dt, W):
         st = StepStats()
-        self._check(self.lib.hbpdc_step(self.h, dt, _ptr(W), ctypes.byref(st)))
+        self._check(self.lib.hbpdc_step(self.h, dt, _ptr(W, self.n), ctypes.byref(st)))
         return st.as_dict()
 
     def step_host(self, dt, W_host):
         """W_host: a C-contiguous float64 numpy array or pinned CPU torch tensor."""
         st = StepStats()
         if isinstance(W_host, np.ndarray):
-            assert W_host.dtype == np.float64 and W_host.flags.c_contiguous
+            if W_host.dtype != np.float64 or not W_host.flags.c_contiguous or W_host.size < self.n:
+                raise ValueError("step_host: expected a C-contiguous float64 array of n doubles")
             p = W_host.ctypes.data_as(ctypes.c_void_p)
         else:
+            if W_host.numel() < self.n:
+                raise ValueError("step_host: host tensor too small")
             p = ctypes.c_void_p(W_host.data_ptr())
         self._check(self.lib.hbpdc_step_host(self.h, dt, p, ctypes.byref(st)))
         return st.as_dict()

@@ -387,15 +387,18 @@ def test_euler_end_of_run_bjext_h(batch):
 
 # ---- NEXT-3 (part): the paper's numerical flux eq:Riemann (global LF, Lambda = I at eps = 1) ----
 
-GLF_CASES = [("euler", 3, 5, 4, (0.0, 1.0, 0.0, 1.0)),
+GLF_CASES = [("advection", 3, 16, None, (0.0, 1.0, 0.0, 1.0)),
+             ("advection", 5, 9, 7, (0.0, 1.0, 0.0, 1.0)),
+             ("euler", 3, 5, 4, (0.0, 1.0, 0.0, 1.0)),
              ("euler", 7, 3, 3, (0.0, 1.0, 0.0, 1.0)),
              ("navier_stokes", 3, 4, 4, (0.0, 2 * np.pi, 0.0, 2 * np.pi))]
 
 
 @pytest.mark.parametrize("case", GLF_CASES)
 def test_glf_operators(case):
-    """R1, R2, residual, EXACT JVP and (Euler) BJ_ext with flux = GLF_PAPER vs the
-    oracle's Equation(numflux='glf'), <= 1e-11."""
+    """R1, R2, residual, EXACT JVP and (advection, Euler) BJ_ext with flux = GLF_PAPER
+    (eq:Riemann literally: the full Lambda on the jump) vs the oracle's
+    Equation(numflux='glf'), <= 1e-11."""
     kind = case[0]
     d, ctx = _pair(*case, flux="glf")
     W = _state(d, kind, SEED + 41)
@@ -412,7 +415,7 @@ def test_glf_operators(case):
     to, bo = implicit.jvp_exact(d, a1, a2, dt, W, sig, dW, ds)
     tg, bg = ctx.jvp(a1, a2, dt, to_gpu(W), to_gpu(sig), to_gpu(dW), to_gpu(ds), mode="exact")
     assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11
-    if kind == "euler":
+    if kind != "navier_stokes":
         pc = implicit.BJExt(d, W, a1, a2, dt)
         ctx.precond_build(a1, a2, dt, to_gpu(W))
         cond = max(np.linalg.cond(M) for M in pc.M)

@@ -219,3 +219,44 @@ def test_br2_face_gradients_converge():
             e = max(e, np.abs(own_p - ops.trace(ux, dd, +1)).max())
         errs.append(e)
     assert errs[1] < 1e-3 and errs[0] / errs[1] > 2 ** 3.5
+
+
+def _exact_time_derivative(case, X, Y):
+    """w_t of an exactly translating Euler solution with mean flow (1, 1):
+    w(x, t) = w0(x - t, y - t), so w_t = -(d/dx + d/dy) w0.  The spatial
+    derivatives of the analytic IC are taken by complex step (exact to
+    rounding), independent of any flux formula."""
+    h = 1e-30
+    Wx = inputs.layout(inputs.ic_primitive(case, X + 1j * h, Y), 2).imag / h
+    Wy = inputs.layout(inputs.ic_primitive(case, X, Y + 1j * h), 2).imag / h
+    return -(Wx + Wy)
+
+
+@pytest.mark.parametrize("case,N,nxs,bounds,nodes,numflux,min_eoc", [
+    # isentropic vortex (C3 family, beta = 5, mean flow (1, 1)) on a domain wide
+    # enough that the periodic wrap of its Gaussian tail is below rounding
+    ("C3", 4, (16, 32, 64), (-10.0, 10.0, -10.0, 10.0), "gll", "llf", 3.5),
+    ("C3", 3, (16, 32, 64), (-10.0, 10.0, -10.0, 10.0), "gl", "glf", 2.5),
+    # density wave (C4 family): rho = 1 + 0.2 sin(2 pi (x + y)), u = v = p = 1
+    ("C4", 3, (4, 8, 16), (0.0, 1.0, 0.0, 1.0), "gll", "llf", 2.8),
+    ("C4", 5, (4, 8, 16), (0.0, 1.0, 0.0, 1.0), "gl", "glf", 4.5),
+])
+def test_euler_r1_converges_to_exact_translation(case, N, nxs, bounds, nodes, numflux, min_eoc):
+    """Spatial-order pin of R^(1) for the Euler equations against exact solutions
+    of the PDE (eq:Euler P:388-394, eq:DGSEM_wt P:179-201):
+    the nodal truncation error ||R1(I_h w0) - I_h w_t||, with w_t of the exactly
+    translating vortex / density wave, decays like h^N.  A wrong flux term
+    (e.g. the energy flux v E instead of v (E + p), or a momentum flux without
+    p) leaves an O(1) error that does not converge."""
+    eq = physics.Equation("euler", numflux=numflux)
+    errs = []
+    for nx in nxs:
+        d = dgsem.Disc(basis.build_basis(N, nodes), dgsem.Mesh(2, nx, nx, *bounds), eq)
+        X, Y = d.node_coords()
+        W = inputs.layout(inputs.ic_primitive(case, X, Y), 2)
+        wt = _exact_time_derivative(case, X, Y)
+        R = dgsem.rhs1(d, W)
+        errs.append(float(np.sqrt(np.mean((R - wt) ** 2)) / np.sqrt(np.mean(wt ** 2))))
+    eoc = [math.log2(a / b) for a, b in zip(errs[:-1], errs[1:])]
+    assert eoc[-1] >= min_eoc, (errs, eoc)
+    assert errs[-1] < 5e-3, errs

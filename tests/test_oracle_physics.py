@@ -133,28 +133,105 @@ def test_grad_vars_example():
     np.testing.assert_allclose([float(x) for x in out], g["wgrad"], atol=1e-15)
 
 
-def test_glf_paper_flux():
-    """The paper's eq:Riemann with Lambda = diag(1/eps,1,1,1/eps),
-    eps = 1 (R18): consistency f*(w, w) = F(w); the dissipation is exactly
-    1/2 (wL - wR) per variable; conservation under the mirror map; advection:
-    lambda = |a.n|, i.e. identical to the upwind / LLF flux."""
-    EG = physics.Equation("euler", numflux="glf")
+def test_glf_paper_flux_worked_example():
+    """S:159, the paper's eq:Riemann with lambda = |a.n|:
+    a = (0.3, 0.3), n = (1, 0), wL = 1, wR = 0 -> 1/2 (0.3 + 0) + 0.3 (1 - 0) = 0.45
+    (golden fstar_glf_paper).  LLF / upwind gives 0.30 on the same data."""
+    u = GOLD["llf_upwind"]
+    eq = physics.Equation("advection", a=tuple(u["a"]), numflux="glf")
+    f = physics.glf(eq, (np.array(u["wL"]),), (np.array(u["wR"]),), 0)[0]
+    assert float(f) == pytest.approx(u["fstar_glf_paper"], abs=1e-15)
+    assert float(physics.numerical_flux(eq, (np.array(u["wL"]),), (np.array(u["wR"]),), 0)[0]) \
+        == pytest.approx(0.45, abs=1e-15)
+    # the y-direction and a negative velocity component: lambda = |a_d|
+    eq2 = physics.Equation("advection", a=(0.3, -0.5), numflux="glf")
+    f = physics.glf(eq2, (np.array(2.0),), (np.array(1.0),), 1)[0]
+    assert float(f) == pytest.approx(0.5 * (-1.0 - 0.5) + 0.5 * (2.0 - 1.0), abs=1e-15)   # -0.25
+
+
+def test_glf_paper_flux_euler_hand_values():
+    """eq:Riemann with Lambda = diag(1/eps, 1, 1, 1/eps), values worked by
+    hand (gamma = 1.4).  wL = (1, 0, 0, 2.5) (rho = 1, v = 0, p = 1),
+    wR = (0.5, 0, 0, 1.25) (rho = 0.5, v = 0, p = 0.5), normal e_x:
+    F_x(wL) = (0, 1, 0, 0), F_x(wR) = (0, 0.5, 0, 0);
+    eps = 1:   f* = (0 + 0.5, 0.75 + 0, 0, 0 + 1.25) = (0.5, 0.75, 0, 1.25);
+    eps = 0.1 (density and energy jumps x10): momentum flux p/eps^2 = 100 p, so
+               f* = (0 + 10 * 0.5, 0.5 (100 + 50) + 0, 0, 0 + 10 * 1.25) = (5, 75, 0, 12.5)."""
+    wL = (1.0, 0.0, 0.0, 2.5)
+    wR = (0.5, 0.0, 0.0, 1.25)
+    e1 = physics.Equation("euler", numflux="glf")
+    np.testing.assert_allclose(physics.glf(e1, wL, wR, 0), (0.5, 0.75, 0.0, 1.25), rtol=0, atol=1e-15)
+    # at eps = 0.1 the same primitive states have E = p/(gamma-1) + eps^2 rho |v|^2 / 2 = same E
+    e01 = physics.Equation("euler", numflux="glf", mach=0.1)
+    np.testing.assert_allclose(physics.glf(e01, wL, wR, 0), (5.0, 75.0, 0.0, 12.5), rtol=1e-15, atol=1e-13)
+    # a momentum jump is not scaled by 1/eps: (1, 0.2, 0, 2.5) vs (1, 0, 0, 2.5) at eps = 0.1
+    wa = (1.0, 0.2, 0.0, 2.5 + 0.5 * 0.01 * 0.04)      # p = 1 exactly: E = p/0.4 + eps^2 rho u^2/2
+    wb = (1.0, 0.0, 0.0, 2.5)
+    f = physics.glf(e01, wa, wb, 0)
+    # F_x(wa) = (0.2, 0.04 + 100, 0, 0.2 (E_a + 1)), F_x(wb) = (0, 100, 0, 0)
+    Ea = wa[3]
+    expect = (0.1 + 10 * 0.0, 0.5 * (100.04 + 100.0) + 0.2, 0.0, 0.1 * (Ea + 1.0) + 10 * (Ea - 2.5))
+    np.testing.assert_allclose(f, expect, rtol=1e-14, atol=1e-14)
+    # consistency f*(w, w) = F(w) and the mirror conservation (P:197-201)
     rng = np.random.default_rng(31)
-    wL = (1.2, 0.3, -0.2, 2.6)
-    wR = (0.9, -0.1, 0.4, 2.2)
+    a, b = _rand_states(rng, 20), _rand_states(rng, 20)
     for d in (0, 1):
-        fc = physics.glf(EG, wL, wL, d)
-        F = physics.flux(EG, wL, d)
-        assert all(abs(a - b) < 1e-15 for a, b in zip(fc, F))
-        f = physics.glf(EG, wL, wR, d)
-        FL, FR = physics.flux(EG, wL, d), physics.flux(EG, wR, d)
-        for v in range(4):
-            assert f[v] == pytest.approx(0.5 * (FL[v] + FR[v]) + 0.5 * (wL[v] - wR[v]), abs=1e-15)
-    ea = physics.Equation("advection", a=(0.7, -0.4), numflux="glf")
-    el = physics.Equation("advection", a=(0.7, -0.4))
-    for d in (0, 1):
-        l, r = (rng.standard_normal(5),), (rng.standard_normal(5),)
-        np.testing.assert_allclose(physics.glf(ea, l, r, d)[0], physics.llf(el, l, r, d)[0], rtol=0, atol=1e-15)
+        for x, y in zip(physics.glf(e1, a, a, d), physics.flux(e1, a, d)):
+            np.testing.assert_allclose(x, y, rtol=1e-15, atol=1e-15)
+        fl = physics.glf(e1, a, b, d)
+        mir = lambda w: tuple(-x if k == 1 + d else x for k, x in enumerate(w))
+        fr = physics.glf(e1, mir(b), mir(a), d)
+        for k in range(4):
+            sgn = 1.0 if k == 1 + d else -1.0
+            np.testing.assert_allclose(fl[k], sgn * fr[k], rtol=1e-13, atol=1e-13)
+
+
+def test_euler_flux_moving_state_hand_values():
+    """eq:Euler at a state with non-zero velocity, worked by hand
+    (gamma = 1.4, eps = 1; every number is a binary fraction, so exact):
+    w = (2, 1, -0.5, 5): u = 0.5, v = -0.25, rho|v|^2/2 = 0.3125,
+    p = 0.4 (5 - 0.3125) = 1.875, E + p = 6.875;
+    F_x = (rho u, rho u^2 + p, rho u v, u (E + p)) = (1, 2.375, -0.25, 3.4375)
+    F_y = (rho v, rho u v, rho v^2 + p, v (E + p)) = (-0.5, -0.25, 2.0, -1.71875).
+    At eps = 0.5 (p = 0.4 (5 - 0.25 * 0.3125) = 1.96875; momentum p/eps^2 = 7.875):
+    F_x = (1, 0.5 + 7.875, -0.25, 0.5 (5 + 1.96875)) = (1, 8.375, -0.25, 3.484375)."""
+    w = (2.0, 1.0, -0.5, 5.0)
+    ap = lambda a, b: np.testing.assert_allclose(a, b, rtol=4e-16, atol=4e-16)   # gamma-1 = 0.4 rounds
+    ap(physics.pressure(EU, w), 1.875)
+    ap(physics.flux(EU, w, 0), (1.0, 2.375, -0.25, 3.4375))
+    ap(physics.flux(EU, w, 1), (-0.5, -0.25, 2.0, -1.71875))
+    e05 = physics.Equation("euler", mach=0.5)
+    ap(physics.pressure(e05, w), 1.96875)
+    ap(physics.flux(e05, w, 0), (1.0, 8.375, -0.25, 3.484375))
+
+
+def test_wave_speed_and_llf_hand_values():
+    """LLF wave speed lambda_f = max(|v_L.n| + c_L, |v_R.n| + c_R), c = sqrt(gamma p / rho)
+    (reading R3), at states chosen so that c is exact (gamma = 1.4):
+    wL: rho = 1, u = 0.5, v = -0.25, p = 1.4 -> c = sqrt(1.96) = 1.4,
+        E = 1.4/0.4 + 0.3125/2 = 3.65625; speeds: x 1.9, y 1.65.
+    wR: rho = 4, u = -1, v = 0, p = 0.7 -> c = sqrt(0.245) = 0.494974746830583...,
+        E = 1.75 + 2 = 3.75; speeds: x 1 + c, y c.
+    x face: lambda_f = 1.9 (L);  y face: lambda_f = 1.65 (L).
+    At eps = 0.5 the sound speed is c/eps (P:395 scaling): wL x speed 0.5 + 2.8 = 3.3."""
+    wL = (1.0, 0.5, -0.25, 3.65625)
+    wR = (4.0, -4.0, 0.0, 3.75)
+    assert physics.pressure(EU, wL) == pytest.approx(1.4, abs=1e-15)
+    assert physics.wave_speed(EU, wL, 0) == pytest.approx(1.9, abs=1e-15)
+    assert physics.wave_speed(EU, wL, 1) == pytest.approx(1.65, abs=1e-15)
+    assert physics.wave_speed(EU, wR, 0) == pytest.approx(1.0 + math.sqrt(0.245), abs=1e-15)
+    assert physics.wave_speed(EU, wR, 1) == pytest.approx(math.sqrt(0.245), abs=1e-15)
+    # LLF value on the x face: 1/2 (F_L + F_R) + 1/2 * 1.9 (wL - wR), by hand:
+    # F_x(wL) = (0.5, 0.25 + 1.4, -0.125, 0.5 (3.65625 + 1.4)) = (0.5, 1.65, -0.125, 2.528125)
+    # F_x(wR) = (-4, 4 + 0.7, 0, -1 (3.75 + 0.7)) = (-4, 4.7, 0, -4.45)
+    f = physics.llf(EU, wL, wR, 0)
+    FL = (0.5, 1.65, -0.125, 2.528125)
+    FR = (-4.0, 4.7, 0.0, -4.45)
+    expect = tuple(0.5 * (a + b) + 0.95 * (l - r) for a, b, l, r in zip(FL, FR, wL, wR))
+    np.testing.assert_allclose(f, expect, rtol=1e-14, atol=1e-14)
+    e05 = physics.Equation("euler", mach=0.5)
+    wL05 = (1.0, 0.5, -0.25, 1.4 / 0.4 + 0.25 * 0.3125 / 2)     # p = 1.4 at eps = 0.5
+    assert physics.wave_speed(e05, wL05, 0) == pytest.approx(0.5 + 2.8, abs=1e-14)
 
 
 def test_glf_free_stream_and_conservation():
