@@ -128,6 +128,8 @@ struct hbpdc_ctx {
   int fsal_valid = 0;
   const double* fsal_ptr = nullptr;      // the W the FSAL cache belongs to (the last step's output)
   unsigned long long* dfp = nullptr;     // device fingerprints: [0] last output, [1] incoming W
+  int* dadm = nullptr;                   // admissibility flags (launch_admissible)
+  int* hadm = nullptr;                   // pinned host copy
   double* hpin = nullptr;      // pinned host scratch (norms)
   // profiling
   int prof_on = 0;
@@ -366,6 +368,22 @@ hbpdc_status norm_host(hbpdc_ctx* c, const double* x, size_t L, double* out) {
   CK(cudaStreamSynchronize(c->stream));
   *out = c->hpin[0];
   return HBPDC_OK;
+}
+
+// Euler / NS: the state W must have rho > 0 and p > 0 everywhere; NaN / Inf
+// are reported as non-finite.  Synchronises (used at existing sync points).
+hbpdc_status check_admissible(hbpdc_ctx* c, const double* W, const char* where) {
+  if (c->pb.equation == HBPDC_ADVECTION) return HBPDC_OK;
+  const int nodes = c->m / 4;
+  CK(launch_admissible(W, c->nE, nodes, c->pb.gamma, c->pb.mach_eps * c->pb.mach_eps, c->dadm, c->stream));
+  CK(cudaMemcpyAsync(c->hadm, c->dadm, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->hadm[1] == 0) return HBPDC_OK;
+  const int t = c->hadm[0];
+  char buf[200];
+  snprintf(buf, sizeof buf, "%s: %s at local element %d node %d", where,
+           (c->hadm[1] & 1) ? "non-finite state" : "negative density or pressure", t / nodes, t % nodes);
+  return fail(c, (c->hadm[1] & 1) ? HBPDC_E_NONFINITE : HBPDC_E_NEG_PRESSURE, buf);
 }
 
 int jvp_kind(hbpdc_ctx* c, int mode) {
@@ -1312,6 +1330,11 @@ hbpdc_status newton_batch(hbpdc_ctx* c, int B, double a1, double a2, double dt, 
       }
       double gn;
       CKS(norm_host(c, w.G, n2, &gn));
+      {
+        char where[64];
+        snprintf(where, sizeof where, "Newton iterate %d", r);
+        CKS(check_admissible(c, w.X, where));
+      }
       if (!std::isfinite(gn)) return fail(c, HBPDC_E_NONFINITE, "non-finite Newton residual");
       if (g0[i] < 0) g0[i] = gn;
       if (c->trace) fprintf(stderr, "[hbpdc] newton sys %d it %d |G| %.3e |G0| %.3e floor %.3e\n", i, r, gn, g0[i], floor_[i]);
@@ -1399,6 +1422,7 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
   const int s = T.s;
   int cur = 0;
   CK(cudaMemcpyAsync(c->Wn, W, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CKS(check_admissible(c, W, "step input"));
   if (c->fsal_valid) {
     // the cached R1/R2 belong to the previous step's output: reuse them only if W is that
     // array with unchanged contents (pointer + fingerprint), else recompute
@@ -1539,6 +1563,12 @@ hbpdc_status alloc_solver(hbpdc_ctx* c) {
   }
   CKS(dalloc(c, &c->partial, RED_BLOCKS));
   CKS(dalloc(c, (double**)&c->dfp, 2));
+  CKS(dalloc(c, (double**)&c->dadm, 1));
+  {
+    void* hp = nullptr;
+    CK(cudaMallocHost(&hp, 2 * sizeof(int)));
+    c->hadm = (int*)hp;
+  }
   CKS(dalloc(c, &c->dnrm, 1));
   CKS(dalloc(c, &c->deps, 2));
   CKS(dalloc(c, &c->Wn, n));
@@ -1985,6 +2015,7 @@ void hbpdc_finalize(hbpdc_ctx* c) {
     if (w.hpin) cudaFreeHost(w.hpin);
   }
   if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->hadm) cudaFreeHost(c->hadm);
   delete c->comm;
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;

@@ -116,6 +116,9 @@ cudaError_t launch_finish_norm(const double* partial, double* out, cudaStream_t 
 // out = c / sqrt(sum partial), or 0 if the sum is 0   (FD step)
 // eps_FD from np partial sums of ||dW||^2 (np <= 0: RED_BLOCKS)
 cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st, int np = 0);
+// Euler / NS state admissibility: flag[0] = first bad node (0x7f7f7f7f if none), flag[1] = 1 non-finite | 2 rho/p <= 0
+cudaError_t launch_admissible(const double* W, int nE, int nodes, double gamma, double eps2, int* flag,
+                              cudaStream_t st);
 // order-independent 64-bit fingerprint of x into *out (device), FSAL cache validation
 cudaError_t launch_fingerprint(const double* x, size_t L, unsigned long long* out, cudaStream_t st);
 // HBPC quadrature: y = base + sum_j a[j] X_j + sum_j b[j] Y_j  (host coefficient arrays, <= 8 terms)

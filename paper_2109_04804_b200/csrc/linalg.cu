@@ -1,5 +1,6 @@
 // linalg.cu -- BJ_ext block inversion and application, GMRES/Newton vector ops.
 #include <cstdint>
+#include <cstdlib>
 #include "launch.h"
 #include "tma.cuh"
 
@@ -185,7 +186,24 @@ __global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ 
 cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, cudaStream_t st) {
   if (m > GJ_MMAX || m < 1) return cudaErrorInvalidValue;
   if (nmat <= 0) return cudaSuccess;
-  gj_kernel<<<nmat, GJ_T, 0, st>>>(Z, S, m, info);
+  // Occupancy: every resident CTA streams its whole m x m matrix through L2 on each of the
+  // m / 16 panel updates.  2 CTAs/SM x 148 SMs x 512 KB (m = 256) = 155 MB overflows the
+  // 126 MB L2 and the updates spill to DRAM (ncu r01e: 16.6x the algorithmic bytes);
+  // one CTA per SM (76 MB in flight) keeps the working set in L2.  HBPDC_GJ_OCC = 1 | 2.
+  static int occ = [] {
+    const char* e = getenv("HBPDC_GJ_OCC");
+    return e ? atoi(e) : 1;
+  }();
+  size_t smem = 0;
+  if (occ == 1 && m > 128) {
+    smem = 120 * 1024;           // reserve shared memory so that only one CTA fits per SM
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+  }
+  gj_kernel<<<nmat, GJ_T, smem, st>>>(Z, S, m, info);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -1205,6 +1223,35 @@ cudaError_t launch_fingerprint(const double* x, size_t L, unsigned long long* ou
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   fingerprint_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(x, L, out);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+// admissibility of an Euler / NS state (negative pressure is an error):
+// flag[0] = smallest inadmissible node index e * nodes + k (0x7f7f7f7f if none),
+// flag[1] |= 1 for a non-finite value, 2 for rho <= 0 or p <= 0
+__global__ void admissible_kernel(const double* __restrict__ W, int nE, int nodes, double gm1, double eps2,
+                                  int* flag) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nE * nodes; t += stride) {
+    const int e = t / nodes, k = t % nodes;
+    const double* w = W + (size_t)e * 4 * nodes + k;
+    const double rho = w[0], mx = w[nodes], my = w[2 * nodes], E = w[3 * nodes];
+    const bool fin = isfinite(rho) && isfinite(mx) && isfinite(my) && isfinite(E);
+    const double p = gm1 * (E - 0.5 * eps2 * (mx * mx + my * my) / rho);
+    if (!fin || !(rho > 0.0) || !(p > 0.0)) {
+      atomicMin(flag, t);
+      atomicOr(flag + 1, fin ? 2 : 1);
+    }
+  }
+}
+
+cudaError_t launch_admissible(const double* W, int nE, int nodes, double gamma, double eps2, int* flag,
+                              cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(flag, 0x7f, sizeof(int), st);      // 0x7f7f7f7f: no bad node
+  if (e == cudaSuccess) e = cudaMemsetAsync(flag + 1, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  admissible_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(W, nE, nodes, gamma - 1.0, eps2, flag);
   hbpdc_count_launch();
   return cudaGetLastError();
 }

@@ -292,6 +292,19 @@ template <class M> struct VolPasses<M, std::void_t<decltype(M::VOL_PASSES)>> {
   static constexpr int value = M::VOL_PASSES;
 };
 
+// ---- fp64 tensor-core contraction (mma.sync m8n8k4 f64: A row-major 8x4, B col-major 4x8;
+// lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) + {0,1}])
+#ifndef HBPDC_DMMA_CONTRACT
+#define HBPDC_DMMA_CONTRACT 1
+#endif
+template <int DIM, int P>
+constexpr bool kDmmaContract = HBPDC_DMMA_CONTRACT && DIM == 2 && P == 8;
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 // ---- the element evaluation (one slot, one node per thread) --------------------
 // Shared scratch per slot: slot_doubles<...>() = volume-flux planes
 // NCH*DIM*NV*P*(P+1) + face parts NFP*NFN*FPD.
@@ -401,30 +414,75 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       if (DIM == 2 && j == P - 1) add_face(3, i, g.lhp);
       if (DIM == 2 && j == 0) add_face(2, i, -g.lhm);
     }
-    double Dr[P], Dc[P];
+    if constexpr (!kDmmaContract<DIM, P>) {
+      double Dr[P], Dc[P];
 #pragma unroll
-    for (int l = 0; l < P; ++l) {
-      Dr[l] = g.Dh[i * P + l];
-      Dc[l] = DIM == 2 ? g.Dh[j * P + l] : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < NCH; ++c)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE + j * PS;
-        double ax = 0.0;
-#pragma unroll
-        for (int l = 0; l < P; ++l) ax = fma(Dr[l], Fx[l], ax);
-        double acc = g.sx * ax;
-        if constexpr (DIM == 2) {
-          const double* Fy = sF + ((c * DIM + 1) * NV + v) * PLANE + i;
-          double ay = 0.0;
-#pragma unroll
-          for (int l = 0; l < P; ++l) ay = fma(Dc[l], Fy[l * PS], ay);
-          acc = fma(g.sy, ay, acc);
-        }
-        out[c][v] = -(acc + sf[c][v]);
+      for (int l = 0; l < P; ++l) {
+        Dr[l] = g.Dh[i * P + l];
+        Dc[l] = DIM == 2 ? g.Dh[j * P + l] : 0.0;
       }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE + j * PS;
+          double ax = 0.0;
+#pragma unroll
+          for (int l = 0; l < P; ++l) ax = fma(Dr[l], Fx[l], ax);
+          double acc = g.sx * ax;
+          if constexpr (DIM == 2) {
+            const double* Fy = sF + ((c * DIM + 1) * NV + v) * PLANE + i;
+            double ay = 0.0;
+#pragma unroll
+            for (int l = 0; l < P; ++l) ay = fma(Dc[l], Fy[l * PS], ay);
+            acc = fma(g.sy, ay, acc);
+          }
+          out[c][v] = -(acc + sf[c][v]);
+        }
+    } else {
+      // keep the surface terms; the volume contraction follows on the tensor cores
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) out[c][v] = sf[c][v];
+    }
+  }
+  if constexpr (kDmmaContract<DIM, P>) {
+    // Volume contraction on the fp64 tensor cores (P = 8, 2D): per channel c and
+    // variable v the element's 8 x 8 node plane gives
+    //   V = sx F_x Dhat^T + sy Dhat F_y           (V_ji = sx sum_l Dhat_il Fx_jl + sy sum_m Dhat_jm Fy_mi)
+    // as four mma.sync.m8n8k4.f64 (two k-steps per direction).  The two warps of
+    // an element slot take alternate (c, v) planes; D stays in registers as
+    // fragments; the result overwrites the F_x plane (node layout) and every
+    // thread then reads its node's value back.
+    const int lane = threadIdx.x & 31, wslot = node >> 5;
+    const int r = lane >> 2, q = lane & 3;
+    if (active) {
+      double fx0 = g.sx * g.Dh[r * P + q], fx1 = g.sx * g.Dh[r * P + q + 4];   // B = sx Dhat^T: (k = l, n = i)
+      double fy0 = g.sy * g.Dh[r * P + q], fy1 = g.sy * g.Dh[r * P + q + 4];   // A = sy Dhat:   (m = j, k = m')
+#pragma unroll
+      for (int mi = wslot; mi < NCH * NV; mi += NODES / 32) {
+        const int c = mi / NV, v = mi % NV;
+        double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE;
+        const double* Fy = sF + ((c * DIM + 1) * NV + v) * PLANE;
+        double acc[2] = {0.0, 0.0};
+        dmma_8x8x4(acc, Fx[r * PS + q], fx0);
+        dmma_8x8x4(acc, Fx[r * PS + q + 4], fx1);
+        dmma_8x8x4(acc, fy0, Fy[q * PS + r]);
+        dmma_8x8x4(acc, fy1, Fy[(q + 4) * PS + r]);
+        __syncwarp();
+        Fx[r * PS + 2 * q] = acc[0];
+        Fx[r * PS + 2 * q + 1] = acc[1];
+      }
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          out[c][v] = -(sF[((c * DIM + 0) * NV + v) * PLANE + j * PS + i] + out[c][v]);
+    }
   }
 }
 

@@ -66,3 +66,38 @@ def test_precond_export_checks_capacity():
     assert "needed" in ctx.lib.hbpdc_last_error(ctx.h).decode()
     with pytest.raises(ValueError):
         ctx.rhs(ctx.empty(ctx.n - 1))                   # binding-side size check
+
+
+@pytest.mark.parametrize("kind", ["neg_pressure", "nan", "neg_density"])
+def test_inadmissible_state_is_reported(kind):
+    """SPEC S:126: a negative pressure is an error carrying the offending state;
+    NaN / Inf are reported as non-finite (fault injection into the step input)."""
+    from paper_2109_04804_b200 import hbpdc
+    d, ctx, W0, dt = _euler_ctx()
+    W = W0.copy()
+    nodes = d.m // 4
+    e, k = 5, 17
+    base = e * d.m
+    if kind == "neg_pressure":
+        W[base + 3 * nodes + k] = 0.4 * (W[base + nodes + k] ** 2 + W[base + 2 * nodes + k] ** 2) / W[base + k]
+    elif kind == "neg_density":
+        W[base + k] = -W[base + k]
+    else:
+        W[base + 2 * nodes + k] = np.nan
+    Wg = to_gpu(W)
+    with pytest.raises(hbpdc.HbpdcError) as ei:
+        ctx.step(dt, Wg)
+    assert ei.value.status == (5 if kind == "nan" else 6)
+    assert f"element {e} node {k}" in str(ei.value)
+
+
+def test_nan_in_advection_newton_residual():
+    """Advection has no admissibility test; a NaN in the state surfaces as a
+    non-finite Newton residual (HBPDC_E_NONFINITE), not as a hang or a bad result."""
+    from paper_2109_04804_b200 import hbpdc
+    d, ctx = make_pair("advection", 3, 8, 8, q=4, kmax=0)
+    W = inputs.initial_state("C2", d.node_coords())
+    W[123] = np.nan
+    with pytest.raises(hbpdc.HbpdcError) as ei:
+        ctx.step(0.01, to_gpu(W))
+    assert ei.value.status == 5
