@@ -311,11 +311,13 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
         gtg1 = c->gtg1;
       }
     }
-    CK(launch_lift(k, 0, c->cfg, c->geo, A, c->lift0, c->liftf0, gtg0));
+    Geo lg = c->geo;                 // a colour-restricted operator needs the lifting on the
+    if (lg.cmode == 1) lg.cmode = 2;   // colour's elements and their neighbours
+    CK(launch_lift(k, 0, c->cfg, lg, A, c->lift0, c->liftf0, gtg0));
     A.G0 = c->lift0;
     A.Gf0 = c->liftf0;
     if (k == OP_JVP_FD) {
-      CK(launch_lift(k, 1, c->cfg, c->geo, A, c->lift1, c->liftf1, gtg1));
+      CK(launch_lift(k, 1, c->cfg, lg, A, c->lift1, c->liftf1, gtg1));
       A.G1 = c->lift1;
       A.Gf1 = c->liftf1;
     }
@@ -531,19 +533,39 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
     const int Px = period(c->nxl), Py = period(c->nyl);
     if (Px < 3 || Py < 3)    // two seeded elements of one colour must be > 2 elements apart
       return fail(c, HBPDC_E_ARG, "Navier-Stokes BJ_ext needs local element counts with a divisor >= 3");
+    // Every launch of the loop is restricted to the colour's elements (the operator) and
+    // to those plus their 4 neighbours (the lifting, whose central face values take the
+    // seeded traces): the other elements' outputs are not needed (the gather reads the
+    // seeded elements only), so each (colour, column) costs 1 / (Px Py) of a full-mesh
+    // operator instead of one.  tseed is zero outside the seeded elements throughout.
+    CK(cudaMemsetAsync(c->tseed, 0, c->n * sizeof(double), c->stream));
+    const Geo full = c->geo;
     for (int cy = 0; cy < Py; ++cy)
-      for (int cx = 0; cx < Px; ++cx)
-        for (int col = 0; col < c->m; ++col) {
-          CK(launch_colour_seed(c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, col, c->stream));
+      for (int cx = 0; cx < Px; ++cx) {
+        c->geo.cmode = 1;
+        c->geo.cpx = Px; c->geo.cpy = Py; c->geo.ccx = cx; c->geo.ccy = cy;
+        hbpdc_status st = HBPDC_OK;
+        for (int col = 0; col < c->m && st == HBPDC_OK; ++col) {
+          cudaError_t ce = launch_colour_seed(c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, col, c->stream);
+          if (ce != cudaSuccess) { c->geo = full; CK(ce); }
           OpArgs A = base_args(c);
           A.W = c->Wb; A.S = c->tseed; A.out1 = nullptr; A.out2 = c->y1;
-          CKS(run_op(c, OP_R12, A));
-          CK(launch_colour_restrict(c->y1, c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, c->stream));
+          st = run_op(c, OP_R12, A);
+          if (st != HBPDC_OK) break;
+          ce = launch_colour_restrict(c->y1, c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, c->stream);
+          if (ce != cudaSuccess) { c->geo = full; CK(ce); }
           A.out2 = c->y2;
-          CKS(run_op(c, OP_R12, A));
-          CK(launch_colour_gather(c->y1, c->y2, c->Kst, c->S, c->nE, c->nxl, c->m, Px, Py, cx, cy, col, a1dt, c2,
-                                  c->stream));
+          st = run_op(c, OP_R12, A);
+          if (st != HBPDC_OK) break;
+          ce = launch_colour_gather(c->y1, c->y2, c->Kst, c->S, c->nE, c->nxl, c->m, Px, Py, cx, cy, col, a1dt, c2,
+                                    c->stream);
+          if (ce != cudaSuccess) { c->geo = full; CK(ce); }
         }
+        c->geo = full;
+        CKS(st);
+        // clear this colour's elements of tseed for the next colour
+        CK(launch_colour_seed(c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, -1, c->stream));
+      }
   }
   std::vector<int> hinfo(c->zchunk);
   for (int e0 = 0; e0 < nblk; e0 += c->zchunk) {

@@ -1,4 +1,5 @@
 // linalg.cu -- BJ_ext block inversion and application, GMRES/Newton vector ops.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include "launch.h"
@@ -26,8 +27,6 @@ __device__ __forceinline__ void gj_dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 constexpr int GJ_T = 256;    // threads
-constexpr int GJ_NB = 16;    // panel width
-constexpr int GJ_PS = GJ_NB + 4;   // panel row stride (== 4 mod 16: conflict-free DMMA A fragments)
 constexpr int GJ_TW = 32;    // column tile of the rank-NB update
 constexpr int GJ_APS = GJ_TW + 4;  // pivot-row tile stride (conflict-free B fragments)
 constexpr int GJ_MMAX = 256;
@@ -36,10 +35,15 @@ constexpr int GJ_MMAX = 256;
 #endif
 }
 
+// GJ_NB: panel width.  Each panel step streams the whole matrix through L2 (DRAM once the
+// in-flight matrices overflow L2), so a wider panel means proportionally fewer passes.
+template <int GJ_NB>
 __global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ Zall, double* __restrict__ Sall, int m,
                                                    int* __restrict__ info) {
-  __shared__ double Pn[GJ_MMAX * GJ_PS];    // panel, row stride GJ_PS (odd: conflict-free columns)
-  __shared__ double AP[GJ_NB * GJ_APS];
+  constexpr int GJ_PS = GJ_NB + 4;   // panel row stride (== 4 mod 16: conflict-free DMMA A fragments)
+  extern __shared__ __align__(16) double gj_dyn[];
+  double* Pn = gj_dyn;                       // panel [GJ_MMAX][GJ_PS]
+  double* AP = gj_dyn + GJ_MMAX * GJ_PS;     // pivot rows of a column tile [GJ_NB][GJ_APS]
   __shared__ int piv[GJ_MMAX];      // pivot row of column c
   __shared__ int colof[GJ_MMAX];    // column whose pivot row is r (-1: unused)
   __shared__ double redv[GJ_T / 32];
@@ -186,24 +190,27 @@ __global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ 
 cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, cudaStream_t st) {
   if (m > GJ_MMAX || m < 1) return cudaErrorInvalidValue;
   if (nmat <= 0) return cudaSuccess;
-  // Occupancy: every resident CTA streams its whole m x m matrix through L2 on each of the
-  // m / 16 panel updates.  2 CTAs/SM x 148 SMs x 512 KB (m = 256) = 155 MB overflows the
-  // 126 MB L2 and the updates spill to DRAM (ncu r01e: 16.6x the algorithmic bytes);
-  // one CTA per SM (76 MB in flight) keeps the working set in L2.  HBPDC_GJ_OCC = 1 | 2.
-  static int occ = [] {
-    const char* e = getenv("HBPDC_GJ_OCC");
-    return e ? atoi(e) : 1;
+  // Panel width: 16 (r01) or 32 (default, HBPDC_GJ_NB).  Occupancy: every resident CTA streams its
+  // whole m x m matrix through L2 on each of the m / NB panel updates; 2 CTAs/SM x 148 SMs x
+  // 512 KB (m = 256) overflow the 126 MB L2.  One CTA per SM (HBPDC_GJ_OCC=1, 76 MB in flight)
+  // was measured slower (C3 build 116 -> 141 ms, r02b): the pivot-search latency is no longer
+  // hidden.  Default 2.
+  static const int nb = [] {
+    const char* e = getenv("HBPDC_GJ_NB");
+    return e && atoi(e) == 16 ? 16 : 32;
   }();
-  size_t smem = 0;
-  if (occ == 1 && m > 128) {
-    smem = 120 * 1024;           // reserve shared memory so that only one CTA fits per SM
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
-  }
-  gj_kernel<<<nmat, GJ_T, smem, st>>>(Z, S, m, info);
+  static const int occ = [] {
+    const char* e = getenv("HBPDC_GJ_OCC");
+    return e ? atoi(e) : 2;
+  }();
+  auto go = [&](auto kern, int NB) {
+    size_t smem = (size_t)(GJ_MMAX * (NB + 4) + NB * GJ_APS) * sizeof(double);
+    if (occ == 1 && m > 128) smem = std::max<size_t>(smem, 120 * 1024);   // one CTA per SM
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<nmat, GJ_T, smem, st>>>(Z, S, m, info);
+  };
+  if (nb == 16) go(gj_kernel<16>, 16);
+  else go(gj_kernel<32>, 32);
   hbpdc_count_launch();
   return cudaGetLastError();
 }

@@ -38,7 +38,34 @@ struct Geo {
   double D[64];            // GL BR2: strong-form D_ij = l_j'(x_i)
   double dlp[8], dlm[8];   // GL BR2: l_j'(+1), l_j'(-1)
   double cp, cm;           // GL BR2: sum_i l_i(+-1) lhat_i(+-1)
+  // colour restriction (NS BJ_ext build): cmode 0 = every element; 1 = the elements of
+  // colour (ccx, ccy) of the period (cpx, cpy) colouring; 2 = those and their 4 neighbours
+  int cmode, cpx, cpy, ccx, ccy;
 };
+
+// elements a restricted launch covers (grid = ceil(count / EPB))
+__host__ __device__ inline int launch_elems(const Geo& g) {
+  if (g.cmode == 0) return g.nE;
+  const int nc = (g.nx / g.cpx) * (g.ny / g.cpy);
+  return g.cmode == 1 ? nc : 5 * nc;
+}
+
+// k-th element of a (possibly colour-restricted) launch; false past the end
+__device__ __forceinline__ bool launch_elem(const Geo& g, int k, int& e) {
+  if (g.cmode == 0) { e = k; return k < g.nE; }
+  const int nxc = g.nx / g.cpx, nc = nxc * (g.ny / g.cpy);
+  if (k >= (g.cmode == 1 ? nc : 5 * nc)) { e = 0; return false; }
+  const int s = k / nc, kk = k % nc;
+  int ex = g.ccx + g.cpx * (kk % nxc), ey = g.ccy + g.cpy * (kk / nxc);
+  // neighbours by periodic wrap inside the local grid (consistent with the global
+  // colouring: the local block sizes are multiples of the period)
+  if (s == 1) ex = ex + 1 == g.nx ? 0 : ex + 1;
+  if (s == 2) ex = ex == 0 ? g.nx - 1 : ex - 1;
+  if (s == 3) ey = ey + 1 == g.ny ? 0 : ey + 1;
+  if (s == 4) ey = ey == 0 ? g.ny - 1 : ey - 1;
+  e = ey * g.nx + ex;
+  return true;
+}
 
 // Node set selected at compile time (the GL kernels are a separate instantiation,
 // ops_kernels_gl.cu, so the GLL hot path is compiled exactly as without GL).
@@ -294,8 +321,11 @@ template <class M> struct VolPasses<M, std::void_t<decltype(M::VOL_PASSES)>> {
 
 // ---- fp64 tensor-core contraction (mma.sync m8n8k4 f64: A row-major 8x4, B col-major 4x8;
 // lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) + {0,1}])
+// Off by default: measured on C3 (r02b) the extra barrier and shared-memory round trip cost
+// more than the 128 FMAs per node they replace (FD JVP 151 -> 157 us, residual 93 -> 108 us);
+// the operators are bound by the flux arithmetic, not the contraction.
 #ifndef HBPDC_DMMA_CONTRACT
-#define HBPDC_DMMA_CONTRACT 1
+#define HBPDC_DMMA_CONTRACT 0
 #endif
 template <int DIM, int P>
 constexpr bool kDmmaContract = HBPDC_DMMA_CONTRACT && DIM == 2 && P == 8;
@@ -506,8 +536,8 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL, BR2
   extern __shared__ __align__(16) double sF[];     // EPB * slot_doubles (dynamic: may exceed 48 KB)
   constexpr int SLOT = slot_doubles<EQ, DIM, P, Mode>();
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
-  const int e = blockIdx.x * EPB + slot;
-  const bool active = e < g.nE;
+  int e;
+  const bool active = launch_elem(g, blockIdx.x * EPB + slot, e);
   double out[Mode::NCH][NV];
   typename Mode::Args Al = A;
   if constexpr (HasDevEps<typename Mode::Args>::value) {
@@ -549,8 +579,8 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
   constexpr int JN = JetN<T>::value;
   __shared__ double sG[EPB * 3 * JN * PLANE];
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
-  const int e = blockIdx.x * EPB + slot;
-  const bool active = e < g.nE;
+  int e;
+  const bool active = launch_elem(g, blockIdx.x * EPB + slot, e);
   const int i = node % P, j = node / P;
   double* sg = sG + slot * 3 * JN * PLANE;
   T sx_[3], sy_[3];

@@ -28,7 +28,7 @@ template <int EQ, int DIM, int P, class Mode>
 static cudaError_t run_op(const OpCfg& c, const Geo& g, const OpArgs& A) {
   constexpr int NODES = ipow(P, DIM);
   constexpr int EPB = epb_for(NODES);
-  const int grid = (g.nE + EPB - 1) / EPB;
+  const int grid = (launch_elems(g) + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
   constexpr size_t smem = (size_t)EPB * slot_doubles<EQ, DIM, P, Mode>() * sizeof(double);
   if constexpr (smem > 48 * 1024) {
@@ -57,7 +57,7 @@ static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, doubl
                             const double* gTg) {
   constexpr int NODES = P * P;
   constexpr int EPB = epb_for(NODES);
-  const int grid = (g.nE + EPB - 1) / EPB;
+  const int grid = (launch_elems(g) + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
   lift_kernel<P, Mode, K, EPB, kGL><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G, Gf, gTg);
   hbpdc_count_launch();
@@ -374,61 +374,71 @@ cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const 
 // elements' outputs of the linearised operator are exactly K_i e_c (the other
 // tangents are exact zeros).  Same colouring as the oracle (oracle element_jacobians).
 namespace {
-__device__ __forceinline__ bool in_colour(int e, int nx, int Px, int Py, int cx, int cy) {
-  const int ex = e % nx, ey = e / nx;
-  return ex % Px == cx && ey % Py == cy;
+// the k-th element of colour (cx, cy): ex = cx + Px (k mod nx/Px), ey = cy + Py (k div nx/Px)
+__device__ __forceinline__ int colour_elem(int k, int nx, int Px, int Py, int cx, int cy) {
+  const int nxc = nx / Px;
+  return (cy + Py * (k / nxc)) * nx + cx + Px * (k % nxc);
 }
 
-__global__ void colour_seed_kernel(double* __restrict__ t, int nE, int nx, int m, int Px, int Py, int cx, int cy,
-                                   int col) {
-  const size_t n = (size_t)nE * m;
+// t = e_col on the colour's elements (the rest of t stays zero: set once per build)
+__global__ void colour_seed_kernel(double* __restrict__ t, int nc, int nx, int m, int Px, int Py, int cx, int cy,
+                                   int col, double val) {
+  const size_t n = (size_t)nc * m;
   for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
-    const int e = (int)(k / m), r = (int)(k % m);
-    t[k] = (r == col && in_colour(e, nx, Px, Py, cx, cy)) ? 1.0 : 0.0;
+    const int e = colour_elem((int)(k / m), nx, Px, Py, cx, cy), r = (int)(k % m);
+    t[(size_t)e * m + r] = r == col ? val : 0.0;
   }
 }
 
-__global__ void colour_restrict_kernel(const double* __restrict__ y, double* __restrict__ t, int nE, int nx, int m,
+// t = y on the colour's elements
+__global__ void colour_restrict_kernel(const double* __restrict__ y, double* __restrict__ t, int nc, int nx, int m,
                                        int Px, int Py, int cx, int cy) {
-  const size_t n = (size_t)nE * m;
+  const size_t n = (size_t)nc * m;
   for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
-    const int e = (int)(k / m);
-    t[k] = in_colour(e, nx, Px, Py, cx, cy) ? y[k] : 0.0;
+    const size_t o = (size_t)colour_elem((int)(k / m), nx, Px, Py, cx, cy) * m + k % m;
+    t[o] = y[o];
   }
 }
 
-// K[e][r][col] = y1, M[e][r][col] = delta - a1dt y1 + c2 y2 for the seeded elements
+// K[e][r][col] = y1, M[e][r][col] = delta - a1dt y1 + c2 y2 for the colour's elements
 __global__ void colour_gather_kernel(const double* __restrict__ y1, const double* __restrict__ y2,
-                                     double* __restrict__ K, double* __restrict__ M, int nE, int nx, int m, int Px,
+                                     double* __restrict__ K, double* __restrict__ M, int nc, int nx, int m, int Px,
                                      int Py, int cx, int cy, int col, double a1dt, double c2) {
-  const size_t n = (size_t)nE * m;
+  const size_t n = (size_t)nc * m;
   for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
-    const int e = (int)(k / m), r = (int)(k % m);
-    if (!in_colour(e, nx, Px, Py, cx, cy)) continue;
-    const size_t o = ((size_t)e * m + r) * m + col;
-    K[o] = y1[k];
-    M[o] = fma(c2, y2[k], (r == col ? 1.0 : 0.0) - a1dt * y1[k]);
+    const int e = colour_elem((int)(k / m), nx, Px, Py, cx, cy), r = (int)(k % m);
+    const size_t i = (size_t)e * m + r;
+    const size_t o = i * m + col;
+    K[o] = y1[i];
+    M[o] = fma(c2, y2[i], (r == col ? 1.0 : 0.0) - a1dt * y1[i]);
   }
 }
+
+int colour_grid(size_t work) { return (int)std::min<size_t>(1184, (work + 255) / 256); }
 }  // namespace
 
+// seed (val = 1) or clear (val = 0: col = -1) the colour's elements of t
 cudaError_t launch_colour_seed(double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy, int col,
                                cudaStream_t st) {
-  colour_seed_kernel<<<1184, 256, 0, st>>>(t, nE, nx, m, Px, Py, cx, cy, col);
+  const int nc = nE / (Px * Py);
+  colour_seed_kernel<<<colour_grid((size_t)nc * m), 256, 0, st>>>(t, nc, nx, m, Px, Py, cx, cy, col, 1.0);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_colour_restrict(const double* y, double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy,
                                    cudaStream_t st) {
-  colour_restrict_kernel<<<1184, 256, 0, st>>>(y, t, nE, nx, m, Px, Py, cx, cy);
+  const int nc = nE / (Px * Py);
+  colour_restrict_kernel<<<colour_grid((size_t)nc * m), 256, 0, st>>>(y, t, nc, nx, m, Px, Py, cx, cy);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_colour_gather(const double* y1, const double* y2, double* K, double* M, int nE, int nx, int m,
                                  int Px, int Py, int cx, int cy, int col, double a1dt, double c2, cudaStream_t st) {
-  colour_gather_kernel<<<1184, 256, 0, st>>>(y1, y2, K, M, nE, nx, m, Px, Py, cx, cy, col, a1dt, c2);
+  const int nc = nE / (Px * Py);
+  colour_gather_kernel<<<colour_grid((size_t)nc * m), 256, 0, st>>>(y1, y2, K, M, nc, nx, m, Px, Py, cx, cy, col,
+                                                                   a1dt, c2);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
