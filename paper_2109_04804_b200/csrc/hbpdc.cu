@@ -375,7 +375,12 @@ hbpdc_status norm_host(hbpdc_ctx* c, const double* x, size_t L, double* out) {
 // Euler / NS: the state W must have rho > 0 and p > 0 everywhere; NaN / Inf
 // are reported as non-finite.  Synchronises (used at existing sync points).
 hbpdc_status check_admissible(hbpdc_ctx* c, const double* W, const char* where) {
-  if (c->pb.equation == HBPDC_ADVECTION) return HBPDC_OK;
+  if (c->pb.equation == HBPDC_ADVECTION) {       // no pressure: finiteness only
+    double nrm;
+    CKS(norm_host(c, W, c->n, &nrm));
+    if (!std::isfinite(nrm)) return fail(c, HBPDC_E_NONFINITE, std::string(where) + ": non-finite state");
+    return HBPDC_OK;
+  }
   const int nodes = c->m / 4;
   CK(launch_admissible(W, c->nE, nodes, c->pb.gamma, c->pb.mach_eps * c->pb.mach_eps, c->dadm, c->stream));
   CK(cudaMemcpyAsync(c->hadm, c->dadm, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));

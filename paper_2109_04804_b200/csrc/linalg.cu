@@ -71,8 +71,10 @@ __global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ 
     for (int k = 0; k < GJ_NB; ++k) {
       if (k >= nb) break;
       // ---- pivot search: max |row[k]| over unused rows (ties: smallest r)
+      // a NaN entry ranks as +inf so that some row is always chosen (a NaN pivot must not leave
+      // the column without a pivot row); non-finite pivots are reported as singular below
       const bool cand = r < m && !used;
-      double best = cand ? fabs(row[k]) : -1.0;
+      double best = cand ? (isnan(row[k]) ? INFINITY : fabs(row[k])) : -1.0;
       int bi = cand ? r : 0x7fffffff;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ 
 #pragma unroll
       for (int w = 1; w < GJ_T / 32; ++w)
         if (redv[w] > best || (redv[w] == best && redi[w] < bi)) { best = redv[w]; bi = redi[w]; }
-      const bool sing = !(best > 0.0);
+      const bool sing = !(best > 0.0) || !(best < INFINITY);
       if (r == bi) {                                 // the pivot row: broadcast it scaled by 1/pivot
         const double pinv = 1.0 / (sing ? 1.0 : row[k]);
 #pragma unroll

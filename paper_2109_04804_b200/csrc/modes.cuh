@@ -400,6 +400,60 @@ template <int EQ, int NODES> struct ModeJvpFD {
       }
     }
   }
+  // Staged face loads (GLL, Euler / advection): the thread of face item (part, node) prefetches
+  // the neighbour node's W, sigma and dW (part 0) or dsigma (part 1) with cp.async before the
+  // volume flux; its own edge node is L1-resident (loaded by the element's volume pass).
+#ifndef HBPDC_STAGE_FACES
+#define HBPDC_STAGE_FACES 1
+#endif
+  static constexpr int NSTAGE = (EQ != 2 && HBPDC_STAGE_FACES) ? 3 * NV : 0;
+  __device__ static void prefetch(const Args& A, int, int, int nb, int nnode, int part, double* st, int stride) {
+    const bool gh = nb >= A.nE;
+    const int eb = gh ? nb - A.nE : nb;
+    const double* f0 = gh ? A.gW : A.W;
+    const double* f1 = gh ? A.gS : A.S;
+    const double* f2 = part == 0 ? (gh ? A.gdW : A.dW) : (gh ? A.gdS : A.dS);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = IDX(eb, v, nnode);
+      cp_async8(st + (0 * NV + v) * stride, f0 + k);
+      cp_async8(st + (1 * NV + v) * stride, f1 + k);
+      cp_async8(st + (2 * NV + v) * stride, f2 + k);
+    }
+  }
+  template <class G>
+  __device__ static void face_part_staged(const Args& A, const PhysParams& pp, const G& g, int e, int own, int nb,
+                                          int nnode, bool plus, int d, int part, const double* st, int stride,
+                                          double* raw, int rs) {
+    if constexpr (EQ != 2) {
+      if (part == 0) {
+        const double ew = fd_step(A);
+        if (!(ew > 0.0)) return;
+        NodeState<EQ, J1> so, sn;
+        load_w<0>(A, e, own, so.w, false);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double Wk = st[v * stride], Sk = st[(NV + v) * stride], dk = st[(2 * NV + v) * stride];
+          sn.w[v] = J1{__dadd_rn(Wk, __dmul_rn(ew, dk)), Sk};      // as load_w<0>
+        }
+        J1 fp[NV];
+        if (plus) face_flux<EQ>(pp, so, sn, d, fp);
+        else face_flux<EQ>(pp, sn, so, d, fp);
+        for (int v = 0; v < NV; ++v) { raw[rs * (2 * v)] = fp[v].v; raw[rs * (2 * v + 1)] = fp[v].a; }
+      } else {
+        NodeState<EQ, J2> so, sn;
+        load_w<1>(A, e, own, so.w, false);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sn.w[v] = J2{st[v * stride], st[(NV + v) * stride], st[(2 * NV + v) * stride]};
+        J2 fq[NV];
+        if (plus) face_flux<EQ>(pp, so, sn, d, fq);
+        else face_flux<EQ>(pp, sn, so, d, fq);
+        for (int v = 0; v < NV; ++v) {
+          raw[rs * (3 * v)] = fq[v].v; raw[rs * (3 * v + 1)] = fq[v].a; raw[rs * (3 * v + 2)] = fq[v].b;
+        }
+      }
+    }
+  }
   __device__ static void face_combine(const Args& A, const PhysParams&, int, const double* rp, const double* rq,
                                       int rs, double (&c)[NCH][NV]) {
     const double ew = fd_step(A);

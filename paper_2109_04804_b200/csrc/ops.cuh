@@ -305,6 +305,22 @@ __device__ __forceinline__ void face_from_halves(const PhysParams& pp, const dou
   }
 }
 
+// ---- per-thread asynchronous staging (cp.async, LDGSTS) of the neighbour face data a
+// thread's face work item will read: issued before the volume flux, consumed after it,
+// so the L2 latency of the neighbour loads hides behind the flux arithmetic.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// modes that stage their neighbour face loads declare NSTAGE (doubles per thread) and
+// prefetch(A, g, e, nb, nnode, part, stage, stride) / face_part_staged(...)
+template <class M, class = void> struct Staged { static constexpr int value = 0; };
+template <class M> struct Staged<M, std::void_t<decltype(M::NSTAGE)>> { static constexpr int value = M::NSTAGE; };
+
 // modes whose epilogue also returns the node's sum of out1^2 (epilogue_ss)
 template <class M, class = void> struct NormEpilogue : std::false_type {};
 template <class M> struct NormEpilogue<M, std::void_t<decltype(M::NORM_EPILOGUE)>> : std::true_type {};
@@ -347,7 +363,8 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
 template <int EQ, int DIM, int P, class Mode>
 __host__ __device__ constexpr int slot_doubles() {
   return Mode::NCH * DIM * NVars<EQ>::value * (DIM == 2 ? P : 1) * (P + 1) +
-         Mode::NFP * 2 * DIM * (DIM == 2 ? P : 1) * Mode::FPD;
+         Mode::NFP * 2 * DIM * (DIM == 2 ? P : 1) * Mode::FPD +
+         Staged<Mode>::value * (DIM == 2 ? P * P : P);      // per-thread staging [k][node]
 }
 
 template <int EQ, int DIM, int P, class Mode, class G>
@@ -364,6 +381,30 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
   double* sRaw = sF + NCH * DIM * NV * PLANE;     // [FPD][part][face node] (conflict-free)
   const int i = node % P;
   const int j = DIM == 2 ? node / P : 0;
+  constexpr int NODES_ = DIM == 2 ? P * P : P;
+  // staged only with one face item per thread (2D: P >= 8) and GLL (GL traces are line sums)
+  constexpr int NST = (G::GL || NFP * NFN > NODES_) ? 0 : Staged<Mode>::value;
+  double* sStage = sRaw + NFP * NFN * Mode::FPD + node;   // this thread's staging column [k * NODES_]
+  auto face_item = [&](int it, int& part, int& fn, int& own, int& nb, int& nnode, int& d, bool& plus) {
+    // face f: 0 = -x, 1 = +x, 2 = -y, 3 = +y; node k along the face
+    part = it / NFN; fn = it % NFN;
+    const int f = fn / FN, k = fn % FN;
+    d = f >> 1;
+    plus = f & 1;
+    const int own_edge = plus ? P - 1 : 0, nbr_edge = plus ? 0 : P - 1;
+    own = DIM == 1 ? own_edge : (d == 0 ? k * P + own_edge : own_edge * P + k);
+    nnode = DIM == 1 ? nbr_edge : (d == 0 ? k * P + nbr_edge : nbr_edge * P + k);
+    nb = nbr_elem(g, e, d, plus ? +1 : -1);
+  };
+  if constexpr (NST > 0) {
+    if (active && node < NFP * NFN) {
+      int part, fn, own, nb, nnode, d;
+      bool plus;
+      face_item(node, part, fn, own, nb, nnode, d, plus);
+      Mode::prefetch(A, e, own, nb, nnode, part, sStage, NODES_);
+    }
+    cp_async_commit();
+  }
 
   if (active) {
     auto put = [&](const double (&cf)[DIM][NCH][NV]) {
@@ -398,17 +439,22 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
     }
   }
   constexpr int NODES = DIM == 2 ? P * P : P;
-  for (int it = node; active && it < NFP * NFN; it += NODES) {
-    // face f: 0 = -x, 1 = +x, 2 = -y, 3 = +y; node k along the face
-    const int part = it / NFN, fn = it % NFN;
-    const int f = fn / FN, k = fn % FN;
-    const int d = f >> 1;
-    const bool plus = f & 1;
-    const int own_edge = plus ? P - 1 : 0, nbr_edge = plus ? 0 : P - 1;
-    const int own = DIM == 1 ? own_edge : (d == 0 ? k * P + own_edge : own_edge * P + k);
-    const int nnode = DIM == 1 ? nbr_edge : (d == 0 ? k * P + nbr_edge : nbr_edge * P + k);
-    const int nb = nbr_elem(g, e, d, plus ? +1 : -1);
-    Mode::face_part(A, pp, g, e, own, nb, nnode, slot, plus, d, part, sRaw + part * NFN + fn, NFP * NFN);
+  if constexpr (NST > 0) {
+    if (active && node < NFP * NFN) {
+      int part, fn, own, nb, nnode, d;
+      bool plus;
+      face_item(node, part, fn, own, nb, nnode, d, plus);
+      cp_async_wait_all();
+      Mode::face_part_staged(A, pp, g, e, own, nb, nnode, plus, d, part, sStage, NODES_, sRaw + part * NFN + fn,
+                             NFP * NFN);
+    }
+  } else {
+    for (int it = node; active && it < NFP * NFN; it += NODES) {
+      int part, fn, own, nb, nnode, d;
+      bool plus;
+      face_item(it, part, fn, own, nb, nnode, d, plus);
+      Mode::face_part(A, pp, g, e, own, nb, nnode, slot, plus, d, part, sRaw + part * NFN + fn, NFP * NFN);
+    }
   }
   __syncthreads();
   if (active) {
@@ -536,8 +582,12 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL, BR2
   extern __shared__ __align__(16) double sF[];     // EPB * slot_doubles (dynamic: may exceed 48 KB)
   constexpr int SLOT = slot_doubles<EQ, DIM, P, Mode>();
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
-  int e;
-  const bool active = launch_elem(g, blockIdx.x * EPB + slot, e);
+  // colour-restricted launches exist only for the Navier-Stokes BJ_ext build; the other
+  // instantiations keep the plain element index (the runtime mapping cost R1 ~30%, r02c)
+  int e = blockIdx.x * EPB + slot;
+  bool active;
+  if constexpr (EQ == 2) active = launch_elem(g, blockIdx.x * EPB + slot, e);
+  else active = e < g.nE;
   double out[Mode::NCH][NV];
   typename Mode::Args Al = A;
   if constexpr (HasDevEps<typename Mode::Args>::value) {
