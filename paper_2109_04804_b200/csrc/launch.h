@@ -51,8 +51,9 @@ cudaError_t launch_colour_seed(double* t, int nE, int nx, int m, int Px, int Py,
                                cudaStream_t st);
 cudaError_t launch_colour_restrict(const double* y, double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy,
                                    cudaStream_t st);
-cudaError_t launch_colour_gather(const double* y1, const double* y2, double* K, double* M, int nE, int nx, int m,
-                                 int Px, int Py, int cx, int cy, int col, double a1dt, double c2, cudaStream_t st);
+cudaError_t launch_colour_gather(const double* y1, const double* y2, const double* y3, double* K, double* M, int nE,
+                                 int nx, int m, int Px, int Py, int cx, int cy, int col, double a1dt, double c2,
+                                 cudaStream_t st);
 
 // ---- linalg.cu -----------------------------------------------------------------
 // in-place Gauss-Jordan inversion with partial pivoting of `nmat` m x m

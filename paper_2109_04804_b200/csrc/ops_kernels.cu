@@ -400,17 +400,21 @@ __global__ void colour_restrict_kernel(const double* __restrict__ y, double* __r
   }
 }
 
-// K[e][r][col] = y1, M[e][r][col] = delta - a1dt y1 + c2 y2 for the colour's elements
+// K[e][r][col] = y1, M[e][r][col] = delta - a1dt y1 + c2 y2 for the colour's elements;
+// BJ^H_ext (y3 = e_c + H e_c): M = delta - a1dt y1 + c2 (y2 + y3 - delta)
 __global__ void colour_gather_kernel(const double* __restrict__ y1, const double* __restrict__ y2,
-                                     double* __restrict__ K, double* __restrict__ M, int nc, int nx, int m, int Px,
-                                     int Py, int cx, int cy, int col, double a1dt, double c2) {
+                                     const double* __restrict__ y3, double* __restrict__ K,
+                                     double* __restrict__ M, int nc, int nx, int m, int Px, int Py, int cx, int cy,
+                                     int col, double a1dt, double c2) {
   const size_t n = (size_t)nc * m;
   for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
     const int e = colour_elem((int)(k / m), nx, Px, Py, cx, cy), r = (int)(k % m);
     const size_t i = (size_t)e * m + r;
     const size_t o = i * m + col;
+    const double dl = r == col ? 1.0 : 0.0;
     K[o] = y1[i];
-    M[o] = fma(c2, y2[i], (r == col ? 1.0 : 0.0) - a1dt * y1[i]);
+    const double q = y3 ? y2[i] + (y3[i] - dl) : y2[i];
+    M[o] = fma(c2, q, dl - a1dt * y1[i]);
   }
 }
 
@@ -434,10 +438,11 @@ cudaError_t launch_colour_restrict(const double* y, double* t, int nE, int nx, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_colour_gather(const double* y1, const double* y2, double* K, double* M, int nE, int nx, int m,
-                                 int Px, int Py, int cx, int cy, int col, double a1dt, double c2, cudaStream_t st) {
+cudaError_t launch_colour_gather(const double* y1, const double* y2, const double* y3, double* K, double* M, int nE,
+                                 int nx, int m, int Px, int Py, int cx, int cy, int col, double a1dt, double c2,
+                                 cudaStream_t st) {
   const int nc = nE / (Px * Py);
-  colour_gather_kernel<<<colour_grid((size_t)nc * m), 256, 0, st>>>(y1, y2, K, M, nc, nx, m, Px, Py, cx, cy, col,
+  colour_gather_kernel<<<colour_grid((size_t)nc * m), 256, 0, st>>>(y1, y2, y3, K, M, nc, nx, m, Px, Py, cx, cy, col,
                                                                    a1dt, c2);
   hbpdc_count_launch();
   return cudaGetLastError();

@@ -96,10 +96,8 @@ def test_gl_jvp_fd(case):
                                   ("navier_stokes", 2, 4, 3)])
 def test_gl_precond(case, precond):
     """BJ_ext / BJ^H_ext on GL nodes: the element blocks see the full line traces
-    (Navier-Stokes: BJ_ext by the two-hop colouring)."""
+    (Navier-Stokes: K_i and H_i by the two-hop colouring)."""
     kind = case[0]
-    if kind == "navier_stokes" and precond == "bjext_h":
-        pytest.skip("BJ^H_ext is implemented for advection and Euler")
     d, ctx = _pair(*case, precond=precond)
     W = _state(d, kind, SEED + 70)
     a1, a2, dt = 1.0 / 6.0, 1.0 / 54.0, 0.05
