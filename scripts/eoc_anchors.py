@@ -1,0 +1,100 @@
+"""NEXT-3 / SURVEY 8(c3) T2: the paper's own convergence setups on the GPU path with
+the paper's discretisation, compared against the error levels of the paper's
+slope triangles (fig:LinAdv_convtest_HBRK4 P:706-741, fig:Euler_convtest_HBRK4
+P:772-803), within the survey's factor ~5.
+
+Setup: 32^2 elements, N = 7, T = 0.8, [-1, 1]^2, a = (0.3, 0.3),
+GMRES 1e-5 / Newton 1e-12, Gauss-Legendre nodes and the global LF flux
+eq:Riemann (Lambda = |a.n| / diag(1,1,1,1) at eps = 1).
+  * advection w = sin(pi (x + y - 0.6 t))  (P:347 sin(pi x_vec) in SPEC's sum
+    convention, reading R23);
+  * Euler rho = 1 + 0.3 sin(pi (x + y - 0.6 t)), v = a, p = 1 (eq:euler_convtest).
+Error: reading R25, e_v = sqrt(sum omega_i omega_j J (w_h - w)^2 / |Omega|) at the
+nodes, summed over the variables (the paper plots the sum of the 4 Euler columns).
+Anchors: the corner (dt, e) of each slope triangle in the paper's figure source.
+
+    python scripts/eoc_anchors.py > profiles/<round>/eoc_anchors.md
+"""
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2109_04804_b200 import hbpdc, inputs  # noqa: E402
+
+T_END, A, N, NE = 0.8, 0.3, 7, 32
+# (q, k_max, dt, anchor error) from the triangles' corners
+ANCHORS = {
+    "advection": [(4, 0, 0.4, 2.2e-4), (6, 0, 0.1, 7.2e-8), (6, 1, 0.1, 7.2e-9), (6, 2, 0.1, 5.2e-11),
+                  (8, 0, 0.1, 1.2e-8), (8, 1, 0.1, 1.2e-9), (8, 2, 0.1, 9.2e-11), (8, 4, 0.1, 4.2e-13)],
+    "euler": [(4, 0, 0.4, 1.2e-4), (6, 0, 0.1, 3.2e-8), (6, 1, 0.1, 3.2e-9), (6, 2, 0.1, 2.2e-11),
+              (8, 0, 0.1, 8.2e-9), (8, 1, 0.1, 8.2e-10), (8, 2, 0.1, 6.2e-11), (8, 4, 0.2, 1.9e-10)],
+}
+
+
+def exact(kind, X, Y, t):
+    s = np.sin(np.pi * (X + Y - 2 * A * t))
+    if kind == "advection":
+        return [s]
+    rho = 1.0 + 0.3 * s
+    return [rho, rho * A, rho * A, 1.0 / 0.4 + 0.5 * rho * 2 * A * A]
+
+
+def l2_error(kind, ctx, W, t):
+    """Reading R25: per-variable quadrature L2 error over |Omega|, summed over variables."""
+    X, Y = ctx.node_coords()
+    ref = inputs.layout(exact(kind, X, Y, t), 2)
+    xi, w = np.polynomial.legendre.leggauss(N + 1)              # GL weights (the run's nodes)
+    nv = 1 if kind == "advection" else 4
+    h = 2.0 / NE
+    wq = (np.outer(w, w) * (h / 2) ** 2).reshape(-1)           # omega_i omega_j J
+    D = (W - ref).reshape(NE * NE, nv, -1)
+    return float(sum(math.sqrt(np.sum(wq[None, :] * D[:, v] ** 2) / 4.0) for v in range(nv)))
+
+
+def run(kind, q, kmax, nsteps):
+    ctx = hbpdc.Context(dim=2, equation=kind, N=N, nx=NE, ny=NE, bounds=(-1.0, 1.0, -1.0, 1.0),
+                        a=(A, A), q=q, kmax=kmax, newton_rtol=1e-12, gmres_rtol=1e-5, restart=700,
+                        max_krylov=7000, precond="bjext", gmres_sstep=1, nodes="gl", flux="glf")
+    X, Y = ctx.node_coords()
+    W = torch.tensor(inputs.layout(exact(kind, X, Y, 0.0), 2), dtype=torch.float64, device="cuda")
+    e0 = l2_error(kind, ctx, W.cpu().numpy(), 0.0)
+    dt = T_END / nsteps
+    for _ in range(nsteps):
+        ctx.step(dt, W)
+    torch.cuda.synchronize()
+    err = l2_error(kind, ctx, W.cpu().numpy(), T_END)
+    ctx.close()
+    return err, e0
+
+
+def main():
+    print("# NEXT-3: error levels vs the paper's slope triangles (`scripts/eoc_anchors.py`)\n")
+    print(f"T = {T_END}, {NE}^2 elements, N = {N}, GL nodes, GLF flux (eq:Riemann), BJ_ext, GMRES 1e-5 / "
+          "Newton 1e-12; error = reading R25 (quadrature L2 over |Omega|, summed over variables).\n")
+    ok_all = True
+    for kind in ("advection", "euler"):
+        print(f"## {kind}\n")
+        print("| scheme | dt | error (EOC from dt/2) | paper anchor | ratio | within 5x |")
+        print("|---|---|---|---|---|---|")
+        for q, kmax, dt, anchor in ANCHORS[kind]:
+            ns = int(round(T_END / dt))
+            e, e0 = run(kind, q, kmax, ns)
+            e2, _ = run(kind, q, kmax, 2 * ns)
+            eoc = math.log2(e / e2)
+            ratio = e / anchor
+            ok = 0.2 <= ratio <= 5.0
+            ok_all &= ok
+            print(f"| HBPC({q},{kmax}) | {dt} | {e:.2e} ({eoc:.2f}) | {anchor:.1e} | {ratio:.2f} | {'yes' if ok else 'NO'} |")
+            sys.stdout.flush()
+        print(f"\n(initial projection error {e0:.1e}; the paper: ~1.1e-15 / 1.2e-15)\n")
+    print(f"all within 5x: {ok_all}")
+
+
+if __name__ == "__main__":
+    main()
