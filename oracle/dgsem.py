@@ -46,6 +46,9 @@ class Mesh:
     xmax: float = 1.0
     ymin: float = 0.0
     ymax: float = 1.0
+    nz: int = 1                # 3D (NEXT-4): elements and extent in z
+    zmin: float = 0.0
+    zmax: float = 1.0
 
     @property
     def dx(self):
@@ -56,8 +59,12 @@ class Mesh:
         return (self.ymax - self.ymin) / self.ny
 
     @property
+    def dz(self):
+        return (self.zmax - self.zmin) / self.nz
+
+    @property
     def n_elem(self):
-        return self.nx * (self.ny if self.dim == 2 else 1)
+        return self.nx * (self.ny if self.dim >= 2 else 1) * (self.nz if self.dim == 3 else 1)
 
 
 @dataclass
@@ -84,6 +91,8 @@ class Disc:
 
     def field_shape(self):
         p, nv, me = self.p, self.nv, self.mesh
+        if me.dim == 3:
+            return (me.nz, me.ny, me.nx, nv, p, p, p)      # [ez][ey][ex][var][k][j][i]
         return (me.ny, me.nx, nv, p, p) if me.dim == 2 else (me.nx, nv, p)
 
     def to_field(self, x):
@@ -100,6 +109,14 @@ class Disc:
         if me.dim == 1:
             return (xs,)                                  # (nx, p)
         ys = me.ymin + np.arange(me.ny)[:, None] * me.dy + (xi[None, :] + 1.0) * me.dy / 2
+        if me.dim == 3:
+            zs = me.zmin + np.arange(me.nz)[:, None] * me.dz + (xi[None, :] + 1.0) * me.dz / 2
+            p = self.p
+            sh = (me.nz, me.ny, me.nx, p, p, p)
+            X = np.broadcast_to(xs[None, None, :, None, None, :], sh)
+            Y = np.broadcast_to(ys[None, :, None, None, :, None], sh)
+            Z = np.broadcast_to(zs[:, None, None, :, None, None], sh)
+            return (X, Y, Z)                              # (nz, ny, nx, p(k), p(j), p(i))
         X = np.broadcast_to(xs[None, :, None, :], (me.ny, me.nx, self.p, self.p))
         Y = np.broadcast_to(ys[:, None, :, None], (me.ny, me.nx, self.p, self.p))
         return (X, Y)                                     # (ny, nx, p(j), p(i))
@@ -143,6 +160,8 @@ class _Ops:
     # traces: polynomial evaluated at the element end
     def trace(self, F, d, side):
         l = self.lp if side > 0 else self.lm
+        if self.dim == 3:                # node axis of direction d: -1 - d  ([k][j][i])
+            return _lin(lambda c: np.tensordot(c, l, axes=([c.ndim - 1 - d], [0])), F)
         if self.dim == 1:
             return _lin(lambda c: np.einsum("...i,i->...", c, l), F)
         if d == 0:
@@ -152,6 +171,11 @@ class _Ops:
     def volume(self, F, d):
         """sum_l Dhat_il F_lj (d = 0) or sum_m Dhat_jm F_im (d = 1)."""
         Dh = self.Dh
+        if self.dim == 3:                # sum_l Dhat_il F_..l.. along the node axis of d
+            def vol3(c):
+                ax = c.ndim - 1 - d
+                return np.moveaxis(np.tensordot(c, Dh, axes=([ax], [1])), -1, ax)
+            return _lin(vol3, F)
         if self.dim == 1:
             return _lin(lambda c: np.einsum("il,...l->...i", Dh, c), F)
         if d == 0:
@@ -162,6 +186,15 @@ class _Ops:
         """f+ lhat(1) - f- lhat(-1) spread onto the element nodes; f+/f- are
         canonical (normal +e_d) fluxes on the element's +/- face."""
         hp, hm = self.lhp, self.lhm
+        if self.dim == 3:                # face values spread along the node axis of d
+            def spread(h):
+                def f(c):
+                    ax = c.ndim - d          # the inserted axis sits at -1 - d of the result
+                    sh = [1] * (c.ndim + 1)
+                    sh[ax] = h.size
+                    return np.expand_dims(c, ax) * h.reshape(sh)
+                return f
+            return _lin(spread(hp), fplus) - _lin(spread(hm), fminus)
         if self.dim == 1:
             return _lin(lambda c: c[..., None] * hp, fplus) - _lin(lambda c: c[..., None] * hm, fminus)
         if d == 0:
@@ -174,6 +207,8 @@ class _Ops:
         """Array axis along which elements neighbour in direction d."""
         if self.dim == 1:
             return 0
+        if self.dim == 3:
+            return 2 - d                 # (ez, ey, ex)
         return 1 if d == 0 else 0
 
     def faces(self, F, d):
@@ -187,7 +222,7 @@ class _Ops:
 
 
 def _scale(d, me):
-    return 2.0 / (me.dx if d == 0 else me.dy)
+    return 2.0 / (me.dx if d == 0 else (me.dy if d == 1 else me.dz))
 
 
 def lifting(disc: Disc, Wf, ops=None):
@@ -266,7 +301,8 @@ def rhs1_field(disc: Disc, Wf, absolute=False):
     ab = (lambda xs: [np.abs(x) for x in xs]) if absolute else (lambda xs: xs)
     eq, me = disc.eq, disc.mesh
     dim = me.dim
-    va = 2 if dim == 2 else 1
+    va = dim                                            # variable axis: after the element axes
+    assert dim < 3 or not eq.viscous, "3D: inviscid (Euler / advection) only (NEXT-4 scope)"
     w = _split(Wf, va)
     if eq.viscous:
         gx, gy = lifting(disc, Wf, ops)

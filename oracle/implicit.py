@@ -135,14 +135,17 @@ def element_jacobians(disc: Disc, W):
     nE, m = me.n_elem, disc.m
     radius = 2 if disc.eq.viscous else 1
     Px = _period(me.nx, radius)
-    Py = _period(me.ny, radius) if me.dim == 2 else 1
+    Py = _period(me.ny, radius) if me.dim >= 2 else 1
+    Pz = _period(me.nz, radius) if me.dim == 3 else 1
     ex = np.arange(nE) % me.nx
-    ey = np.arange(nE) // me.nx
+    ey = (np.arange(nE) // me.nx) % (me.ny if me.dim >= 2 else 1)
+    ez = np.arange(nE) // (me.nx * (me.ny if me.dim >= 2 else 1))
     K = np.zeros((nE, m, m))
     W = np.asarray(W, float)
-    for cy in range(Py):
+    for cz in range(Pz):
+      for cy in range(Py):
         for cx in range(Px):
-            sel = (ex % Px == cx) & (ey % Py == cy)
+            sel = (ex % Px == cx) & (ey % Py == cy) & (ez % Pz == cz)
             for c in range(m):
                 seed = np.zeros((nE, m))
                 seed[sel, c] = 1.0
@@ -204,15 +207,18 @@ def element_hessian_blocks(disc: Disc, W, sig):
     nE, m = me.n_elem, disc.m
     radius = 2 if disc.eq.viscous else 1
     Px = _period(me.nx, radius)
-    Py = _period(me.ny, radius) if me.dim == 2 else 1
+    Py = _period(me.ny, radius) if me.dim >= 2 else 1
+    Pz = _period(me.nz, radius) if me.dim == 3 else 1
     ex = np.arange(nE) % me.nx
-    ey = np.arange(nE) // me.nx
+    ey = (np.arange(nE) // me.nx) % (me.ny if me.dim >= 2 else 1)
+    ez = np.arange(nE) // (me.nx * (me.ny if me.dim >= 2 else 1))
     H = np.zeros((nE, m, m))
     W = np.asarray(W, float)
     sig = np.asarray(sig, float)
-    for cy in range(Py):
+    for cz in range(Pz):
+      for cy in range(Py):
         for cx in range(Px):
-            sel = (ex % Px == cx) & (ey % Py == cy)
+            sel = (ex % Px == cx) & (ey % Py == cy) & (ez % Pz == cz)
             for c in range(m):
                 seed = np.zeros((nE, m))
                 seed[sel, c] = 1.0

@@ -9,6 +9,9 @@ hyper-duals.
   advection     F = a w                                   (C1/C2)
   euler         F_x = (rho u, rho u^2 + p, rho u v, u (E + p))      (eq:Euler,
                 p = (gamma-1)(E - rho |v|^2 / 2)                     P:388-394)
+                in 2D (4 variables) and 3D (5 variables: (rho, rho u, rho v,
+                rho w, E), the same system with a third momentum component --
+                the paper's 3D Taylor-Green case; NEXT-4)
                 and the reference Mach number eps of eq:Euler: momentum flux
                 rho v v + p / eps^2, p = (gamma-1)(E - eps^2 rho |v|^2 / 2)
                 (configs: eps = 1, reading R18; NS only at eps = 1)
@@ -37,7 +40,7 @@ from . import ad
 @dataclass(frozen=True)
 class Equation:
     kind: str                  # "advection" | "euler" | "navier_stokes"
-    a: tuple = (1.0, 1.0)      # advection velocity
+    a: tuple = (1.0, 1.0)      # advection velocity (3D: three components)
     gamma: float = 1.4
     mu: float = 0.0
     prandtl: float = 0.72
@@ -45,10 +48,11 @@ class Equation:
     mach: float = 1.0          # reference Mach number eps of eq:Euler; configs: 1 (R18)
     lifting: str = "br1"       # NS face gradients: "br1" (C5, reading R19) | "br2" (R33)
     eta_br2: float = 2.0       # BR2 stabilisation parameter (the paper gives no value; reading R33)
+    dim: int = 2               # space dimension of the Euler system (3: five variables, NEXT-4)
 
     @property
     def nv(self):
-        return 1 if self.kind == "advection" else 4
+        return 1 if self.kind == "advection" else (5 if self.dim == 3 else 4)
 
     @property
     def viscous(self):
@@ -56,33 +60,37 @@ class Equation:
 
 
 def pressure(eq, w):
-    """p = (gamma - 1)(E - eps^2/2 rho |v|^2)."""
-    rho, mx, my, E = w
+    """p = (gamma - 1)(E - eps^2/2 rho |v|^2); w = (rho, rho v, E)
+    with 2 (2D) or 3 (3D) momentum components."""
+    rho, E = w[0], w[-1]
     e2 = eq.mach * eq.mach
-    return (eq.gamma - 1.0) * (E - 0.5 * e2 * (mx * mx + my * my) / rho)
+    ke = w[1] * w[1]
+    for m in w[2:-1]:
+        ke = ke + m * m
+    return (eq.gamma - 1.0) * (E - 0.5 * e2 * ke / rho)
 
 
 def flux(eq, w, d):
-    """Inviscid physical flux F_d(w) in direction d (0 = x, 1 = y)."""
+    """Inviscid physical flux F_d(w) in direction d (0 = x, 1 = y, 2 = z)."""
     if eq.kind == "advection":
         return (eq.a[d] * w[0],)
-    rho, mx, my, E = w
+    rho, E = w[0], w[-1]
+    mom = w[1:-1]
     p = pressure(eq, w)
     pe = p / (eq.mach * eq.mach)             # p / eps^2 in the momentum flux (eq:Euler)
-    vn = (mx if d == 0 else my) / rho
-    return (rho * vn,
-            mx * vn + (pe if d == 0 else 0.0),
-            my * vn + (pe if d == 1 else 0.0),
-            vn * (E + p))
+    vn = mom[d] / rho
+    return ((rho * vn,)
+            + tuple(mk * vn + (pe if k == d else 0.0) for k, mk in enumerate(mom))
+            + (vn * (E + p),))
 
 
 def wave_speed(eq, w, d):
     """|v.e_d| + c (Euler/NS), |a_d| (advection)."""
     if eq.kind == "advection":
         return abs(eq.a[d]) + 0.0 * w[0]
-    rho, mx, my, E = w
+    rho = w[0]
     p = pressure(eq, w)
-    vn = (mx if d == 0 else my) / rho
+    vn = w[1 + d] / rho
     return ad.absval(vn) + ad.sqrt(eq.gamma * p / rho) / eq.mach   # eigenvalues v.n +- c / eps
 
 
@@ -104,7 +112,7 @@ def glf(eq, wL, wR, d):
         lam = (abs(eq.a[d]),)
     else:
         eps = eq.mach
-        lam = (1.0 / eps, 1.0, 1.0, 1.0 / eps)
+        lam = (1.0 / eps,) + (1.0,) * (len(wL) - 2) + (1.0 / eps,)
     # eq:Riemann: (1/2 (F_L + F_R) + lambda (w_L - w_R)) . n -- the jump term
     # carries the full lambda, no 1/2 (S:159 gives 0.45 for its example),
     # and is not projected on n.

@@ -24,9 +24,32 @@ def conserved(rho, u, v, p, gamma=GAMMA):
     return (rho, rho * u, rho * v, p / (gamma - 1.0) + 0.5 * rho * (u * u + v * v))
 
 
-def ic_primitive(case, X, Y=None, gamma=GAMMA):
-    """Analytic initial condition of a config at coordinates X (and Y).
-    Returns a tuple of variables (1 for advection, 4 conserved for Euler/NS)."""
+def conserved3(rho, u, v, w, p, gamma=GAMMA):
+    """3D: (rho, rho u, rho v, rho w, E), E = p/(gamma-1) + rho |v|^2 / 2."""
+    return (rho, rho * u, rho * v, rho * w, p / (gamma - 1.0) + 0.5 * rho * (u * u + v * v + w * w))
+
+
+def ic_primitive(case, X, Y=None, Z=None, gamma=GAMMA):
+    """Analytic initial condition of a config at coordinates X (and Y, Z).
+    Returns a tuple of variables (1 for advection, 4 conserved for Euler/NS in
+    2D, 5 in 3D).  3D cases (NEXT-4): "TGV3" = the paper's Taylor-Green data
+    (P:1088-1091 with eps = 1 and the standard divergence-free first velocity
+    component sin x cos y cos z, DESIGN.md reading R35) on [0, 2 pi]^3;
+    "DW3" = 3D density wave rho = 1 + 0.2 sin(2 pi (x + y + z)), v = (1, 1, 1),
+    p = 1 (an exact translating solution) on [0, 1]^3; "ADV3" = sin(2 pi x)
+    sin(2 pi y) sin(2 pi z)."""
+    if case == "TGV3":
+        rho = np.ones_like(X)
+        u = np.sin(X) * np.cos(Y) * np.cos(Z)
+        v = -np.cos(X) * np.sin(Y) * np.cos(Z)
+        p = rho / gamma + rho / 16.0 * (np.cos(2 * X) + np.cos(2 * Y)) * (np.cos(2 * Z) + 2.0)
+        return conserved3(rho, u, v, 0.0 * X, p, gamma)
+    if case == "DW3":
+        rho = 1.0 + 0.2 * np.sin(2 * math.pi * (X + Y + Z))
+        one = np.ones_like(X)
+        return conserved3(rho, one, one, one, one, gamma)
+    if case == "ADV3":
+        return (np.sin(2 * math.pi * X) * np.sin(2 * math.pi * Y) * np.sin(2 * math.pi * Z),)
     if case == "C1":                                       # 1D advection
         return (np.sin(2 * math.pi * X),)
     if case == "C2":                                       # 2D advection
@@ -54,13 +77,13 @@ def ic_primitive(case, X, Y=None, gamma=GAMMA):
 
 
 def layout(vars_, dim):
-    """Stack per-variable node arrays into layout L ([elem][var][j][i]).
-    2D inputs have shape (ny, nx, p, p) [j, i]; 1D inputs (nx, p)."""
-    ax = 2 if dim == 2 else 1
+    """Stack per-variable node arrays into layout L ([elem][var][(k)][j][i]).
+    3D inputs have shape (nz, ny, nx, p, p, p); 2D (ny, nx, p, p) [j, i]; 1D (nx, p)."""
+    ax = dim
     return np.ascontiguousarray(np.stack(vars_, axis=ax)).reshape(-1)
 
 
-CASE_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
+CASE_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4, "TGV3": 5, "DW3": 6, "ADV3": 7}
 
 
 def initial_state(case, coords, noise=None, gamma=GAMMA, stream=0):

@@ -12,11 +12,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # (name, file, original, mutated)
 MUTANTS = [
-    ("energy_flux_vE", "oracle/physics.py", "vn * (E + p))", "vn * E)"),
+    ("energy_flux_vE", "oracle/physics.py", "(vn * (E + p),))", "(vn * E,))"),
     ("sound_speed_no_gamma", "oracle/physics.py", "ad.sqrt(eq.gamma * p / rho)", "ad.sqrt(p / rho)"),
     ("glf_half_lambda", "oracle/physics.py", "0.5 * (fl + fr) + lv * (l - r)", "0.5 * (fl + fr) + 0.5 * lv * (l - r)"),
-    ("momentum_no_p", "oracle/physics.py", "mx * vn + (pe if d == 0 else 0.0)", "mx * vn"),
-    ("pressure_no_half", "oracle/physics.py", "(E - 0.5 * e2 *", "(E - e2 *"),
+    ("momentum_no_p", "oracle/physics.py", "mk * vn + (pe if k == d else 0.0)", "mk * vn"),
+    ("pressure_no_half", "oracle/physics.py", "(E - 0.5 * e2 * ke / rho)", "(E - e2 * ke / rho)"),
     ("llf_lambda_min", "oracle/physics.py", "lam = ad.maxval(wave_speed(eq, wL, d), wave_speed(eq, wR, d))",
      "lam = wave_speed(eq, wL, d)"),
     ("viscous_div_factor", "oracle/physics.py", "txx = mu * (2.0 * ux - (2.0 / 3.0) * div)",
