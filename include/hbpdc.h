@@ -63,7 +63,8 @@ enum { HBPDC_JVP_AUTO = 0, HBPDC_JVP_FD = 1, HBPDC_JVP_EXACT = 2, HBPDC_JVP_LINE
 
 /* The problem (P:43-47 conservation law; P:170 DGSEM degree N; P:83 HBPC(q,k_max)). */
 typedef struct {
-  int dim;              /* 1 or 2                                                  */
+  int dim;              /* 1, 2 or 3 (3: hexahedra, advection or Euler, GLL, one rank;
+                           NEXT-4, the paper's 3D case P:1080-1093, inviscid scope)   */
   int equation;         /* HBPDC_ADVECTION | HBPDC_EULER | HBPDC_NAVIER_STOKES     */
   double a[2];          /* advection velocity (advection only)                     */
   double gamma;         /* isentropic coefficient, e.g. 1.4                */
@@ -82,6 +83,9 @@ typedef struct {
   int q, kmax;          /* HBPC(q, k_max), q in {4, 6, 8}, k_max >= 0              */
   double eta_br2;       /* BR2 stabilisation parameter eta (> 0; the paper gives no
                            value, reading R33); ignored for BR1                   */
+  int nz;               /* 3D only: global element count in z (>= 1)               */
+  double zmin, zmax;    /* 3D only: periodic extent in z                          */
+  double az;            /* 3D advection only: z component of the velocity          */
 } hbpdc_problem;
 
 typedef struct {
@@ -172,6 +176,8 @@ HBPDC_API hbpdc_status hbpdc_local_shape(const hbpdc_ctx* ctx, int* n_local_elem
 /* Physical coordinates of the local nodes, layout [elem][j][i] (host arrays of
  * n_local_elems*(N+1)^dim doubles; y_host ignored in 1D).  Synchronous. */
 HBPDC_API hbpdc_status hbpdc_node_coords(const hbpdc_ctx* ctx, double* x_host, double* y_host);
+/* 3D: z coordinates of the local nodes, same order (host array of n_local_elems*(N+1)^3). */
+HBPDC_API hbpdc_status hbpdc_node_coords_z(const hbpdc_ctx* ctx, double* z_host);
 
 /* sigma == NULL: out = R^(1)_h(W) (eq:DGSEM_wt).
  * sigma != NULL: out = R^(2)_h(W, sigma) (eq:DGSEM_wtt): the time

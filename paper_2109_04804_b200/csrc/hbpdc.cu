@@ -96,7 +96,7 @@ struct hbpdc_ctx {
   hbpdc_problem pb{};
   hbpdc_solver_opts op{};
   hbpdc_dist ds{};
-  int nv = 1, P = 2, nodes = 2, m = 2, nE = 0, nxl = 0, nyl = 0, ex0 = 0, ey0 = 0;
+  int nv = 1, P = 2, nodes = 2, m = 2, nE = 0, nxl = 0, nyl = 0, nzl = 1, ex0 = 0, ey0 = 0;
   size_t n = 0;          // W-DOF on this rank
   Geo geo{};
   Geo geo_abs{};         // |Dhat|, -lhat_0(-1): R1_abs (rounding scale, reading R10b)
@@ -382,8 +382,8 @@ hbpdc_status check_admissible(hbpdc_ctx* c, const double* W, const char* where) 
     if (!std::isfinite(nrm)) return fail(c, HBPDC_E_NONFINITE, std::string(where) + ": non-finite state");
     return HBPDC_OK;
   }
-  const int nodes = c->m / 4;
-  CK(launch_admissible(W, c->nE, nodes, c->pb.gamma, c->pb.mach_eps * c->pb.mach_eps, c->dadm, c->stream));
+  const int nodes = c->nodes;
+  CK(launch_admissible(W, c->nE, nodes, c->nv, c->pb.gamma, c->pb.mach_eps * c->pb.mach_eps, c->dadm, c->stream));
   CK(cudaMemcpyAsync(c->hadm, c->dadm, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (c->hadm[1] == 0) return HBPDC_OK;
@@ -1710,9 +1710,16 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
     *out = c;   // return the context so the caller can read the message
     return HBPDC_E_ARG;
   };
-  if (pb->dim != 1 && pb->dim != 2) return bad("dim must be 1 or 2");
+  if (pb->dim < 1 || pb->dim > 3) return bad("dim must be 1, 2 or 3");
   if (pb->equation < 0 || pb->equation > 2) return bad("unknown equation");
-  if (pb->equation != HBPDC_ADVECTION && pb->dim != 2) return bad("Euler/NS need dim = 2");
+  if (pb->equation != HBPDC_ADVECTION && pb->dim == 1) return bad("Euler/NS need dim >= 2");
+  if (pb->dim == 3) {       // NEXT-4 scope: inviscid hexahedra, GLL, one rank, N <= 3 (m <= 320)
+    if (pb->equation == HBPDC_NAVIER_STOKES) return bad("3D: advection or Euler (Navier-Stokes is 2D)");
+    if (pb->nodes != HBPDC_GLL) return bad("3D: Gauss-Lobatto nodes only");
+    if (pb->N > 3) return bad("3D: N must be in 1..3");
+    if (pb->nz < 1 || pb->ny < 1 || !(pb->zmax > pb->zmin)) return bad("3D: bad z extent / element counts");
+    if (ds && (ds->nranks > 1 || ds->force_halo)) return bad("3D runs on one rank");
+  }
   if (pb->N < 1 || pb->N > 7) return bad("N must be in 1..7");
   if (pb->nodes != HBPDC_GLL && pb->nodes != HBPDC_GL) return bad("nodes must be HBPDC_GLL or HBPDC_GL");
   if (!(pb->mach_eps > 0.0)) return bad("mach_eps must be positive");
@@ -1733,12 +1740,13 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   const bool halo = c->ds.nranks > 1 || c->ds.force_halo;
 
   if (op->gmres_restart < 1 || op->krylov_max_per_newton < 1 || op->newton_max < 0) return bad("bad solver options");
-  c->nv = pb->equation == HBPDC_ADVECTION ? 1 : 4;
+  c->nv = pb->equation == HBPDC_ADVECTION ? 1 : (pb->dim == 3 ? 5 : 4);
   c->P = pb->N + 1;
-  c->nodes = pb->dim == 2 ? c->P * c->P : c->P;
+  c->nodes = pb->dim == 3 ? c->P * c->P * c->P : (pb->dim == 2 ? c->P * c->P : c->P);
   c->m = c->nv * c->nodes;
   c->nxl = pb->nx / c->ds.px;
-  c->nyl = pb->dim == 2 ? pb->ny / c->ds.py : 1;
+  c->nyl = pb->dim >= 2 ? pb->ny / c->ds.py : 1;
+  c->nzl = pb->dim == 3 ? pb->nz : 1;
   {
     const int rx = c->ds.rank % c->ds.px, ry = c->ds.rank / c->ds.px;
     c->ex0 = rx * c->nxl;
@@ -1752,7 +1760,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
     const int hy = halo && pb->dim == 2 && (c->ds.py > 1 || c->ds.force_halo);
     c->hl = HaloLayout{c->nxl, c->nyl, pb->equation == HBPDC_ADVECTION ? 1 : 4, pb->N + 1, pb->dim, {hx, hx, hy, hy}};
   }
-  c->nE = c->nxl * c->nyl;
+  c->nE = c->nxl * c->nyl * c->nzl;
   c->n = (size_t)c->nE * c->m;
   c->restart = op->gmres_restart;
   c->sstep = op->gmres_sstep > 1 ? op->gmres_sstep : 1;
@@ -1767,6 +1775,8 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   const double dy = pb->dim == 2 ? (pb->ymax - pb->ymin) / pb->ny : 1.0;
   c->geo.nx = c->nxl;
   c->geo.ny = c->nyl;
+  c->geo.nz = c->nzl;
+  c->geo.sz = pb->dim == 3 ? 2.0 / ((pb->zmax - pb->zmin) / pb->nz) : 1.0;
   c->geo.nE = c->nE;
   c->geo.hx = c->hl.active[0];
   c->geo.hy = c->hl.active[2];
@@ -1803,8 +1813,9 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
     c->geo_abs.lhpv[i] = std::fabs(c->geo.lhpv[i]);
     c->geo_abs.lhmv[i] = -std::fabs(c->geo.lhmv[i]);
   }
-  c->cfg.eq = pb->equation;
+  c->cfg.eq = (pb->equation == HBPDC_EULER && pb->dim == 3) ? 3 : pb->equation;   // EQ 3: 3D Euler (5 variables)
   c->cfg.dim = pb->dim;
+  c->cfg.pp.az = pb->dim == 3 ? pb->az : 0.0;
   c->cfg.P = c->P;
   c->cfg.pp.ax = pb->a[0];
   c->cfg.pp.ay = pb->a[1];
@@ -1898,15 +1909,29 @@ hbpdc_status hbpdc_node_coords(const hbpdc_ctx* c, double* xh, double* yh) {
   if (!c || !xh) return HBPDC_E_ARG;
   const auto& pb = c->pb;
   const double dx = (pb.xmax - pb.xmin) / pb.nx;
-  const double dy = pb.dim == 2 ? (pb.ymax - pb.ymin) / pb.ny : 0.0;
+  const double dy = pb.dim >= 2 ? (pb.ymax - pb.ymin) / pb.ny : 0.0;
   const int P = c->P;
   for (int e = 0; e < c->nE; ++e) {
-    const int ex = c->ex0 + e % c->nxl, ey = c->ey0 + e / c->nxl;
+    const int ex = c->ex0 + e % c->nxl, ey = c->ey0 + (e / c->nxl) % c->nyl;
     for (int nd = 0; nd < c->nodes; ++nd) {
-      const int i = nd % P, j = nd / P;
+      const int i = nd % P, j = (nd / P) % P;
       xh[(size_t)e * c->nodes + nd] = pb.xmin + ex * dx + (c->basis.xi[i] + 1.0) * dx / 2;
-      if (pb.dim == 2 && yh) yh[(size_t)e * c->nodes + nd] = pb.ymin + ey * dy + (c->basis.xi[j] + 1.0) * dy / 2;
+      if (pb.dim >= 2 && yh) yh[(size_t)e * c->nodes + nd] = pb.ymin + ey * dy + (c->basis.xi[j] + 1.0) * dy / 2;
     }
+  }
+  return HBPDC_OK;
+}
+
+hbpdc_status hbpdc_node_coords_z(const hbpdc_ctx* c, double* zh) {
+  if (!c || !zh) return HBPDC_E_ARG;
+  const auto& pb = c->pb;
+  if (pb.dim != 3) return fail(const_cast<hbpdc_ctx*>(c), HBPDC_E_ARG, "node_coords_z: 3D only");
+  const double dz = (pb.zmax - pb.zmin) / pb.nz;
+  const int P = c->P;
+  for (int e = 0; e < c->nE; ++e) {
+    const int ez = e / (c->nxl * c->nyl);
+    for (int nd = 0; nd < c->nodes; ++nd)
+      zh[(size_t)e * c->nodes + nd] = pb.zmin + ez * dz + (c->basis.xi[nd / (P * P)] + 1.0) * dz / 2;
   }
   return HBPDC_OK;
 }

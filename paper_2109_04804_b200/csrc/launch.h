@@ -27,6 +27,10 @@ cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs
 // Navier-Stokes operators with BR2 face gradients (ops_kernels_br2.cu, ops_kernels_gl_br2.cu), when g.br2
 cudaError_t launch_op_br2(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
 cudaError_t launch_op_gl_br2(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
+// 3D hexahedral instantiations (ops_kernels_3d.cu, NEXT-4), reached from launch_op / launch_kbuild when c.dim == 3
+cudaError_t launch_op_3d(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
+cudaError_t launch_kbuild_3d(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
+                             double c2, double* M, int e0, int ne, const double* Sb, const double* gSb);
 cudaError_t launch_lift_gl(OpKind kind, int state, const OpCfg& c, const Geo& g, const OpArgs& A, double* Gout,
                            double* Gf, const double* gTg, double* Tg);
 cudaError_t launch_kbuild_gl(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
@@ -118,7 +122,7 @@ cudaError_t launch_finish_norm(const double* partial, double* out, cudaStream_t 
 // eps_FD from np partial sums of ||dW||^2 (np <= 0: RED_BLOCKS)
 cudaError_t launch_finish_fd_eps(const double* partial, double c, double* out, cudaStream_t st, int np = 0);
 // Euler / NS state admissibility: flag[0] = first bad node (0x7f7f7f7f if none), flag[1] = 1 non-finite | 2 rho/p <= 0
-cudaError_t launch_admissible(const double* W, int nE, int nodes, double gamma, double eps2, int* flag,
+cudaError_t launch_admissible(const double* W, int nE, int nodes, int nv, double gamma, double eps2, int* flag,
                               cudaStream_t st);
 // order-independent 64-bit fingerprint of x into *out (device), FSAL cache validation
 cudaError_t launch_fingerprint(const double* x, size_t L, unsigned long long* out, cudaStream_t st);

@@ -26,10 +26,8 @@ __device__ __forceinline__ void gj_dmma(double (&d)[2], double a, double b) {
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
-constexpr int GJ_T = 256;    // threads
 constexpr int GJ_TW = 32;    // column tile of the rank-NB update
 constexpr int GJ_APS = GJ_TW + 4;  // pivot-row tile stride (conflict-free B fragments)
-constexpr int GJ_MMAX = 256;
 #ifndef GJ_MINB
 #define GJ_MINB 2
 #endif
@@ -37,9 +35,13 @@ constexpr int GJ_MMAX = 256;
 
 // GJ_NB: panel width.  Each panel step streams the whole matrix through L2 (DRAM once the
 // in-flight matrices overflow L2), so a wider panel means proportionally fewer passes.
-template <int GJ_NB>
-__global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ Zall, double* __restrict__ Sall, int m,
-                                                   int* __restrict__ info) {
+// GJ_T threads (= the largest m: thread r owns row r): 256 for the 2D configs, 384 for the
+// 3D hexahedra (m = 5 * 4^3 = 320, NEXT-4).
+template <int GJ_NB, int GJ_T>
+__global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(double* __restrict__ Zall,
+                                                                          double* __restrict__ Sall, int m,
+                                                                          int* __restrict__ info) {
+  constexpr int GJ_MMAX = GJ_T;
   constexpr int GJ_PS = GJ_NB + 4;   // panel row stride (== 4 mod 16: conflict-free DMMA A fragments)
   extern __shared__ __align__(16) double gj_dyn[];
   double* Pn = gj_dyn;                       // panel [GJ_MMAX][GJ_PS]
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(GJ_T, GJ_MINB) gj_kernel(double* __restrict__ 
 }
 
 cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, cudaStream_t st) {
-  if (m > GJ_MMAX || m < 1) return cudaErrorInvalidValue;
+  if (m > 384 || m < 1) return cudaErrorInvalidValue;
   if (nmat <= 0) return cudaSuccess;
   // Panel width: 16 (r01) or 32 (default, HBPDC_GJ_NB).  Occupancy: every resident CTA streams its
   // whole m x m matrix through L2 on each of the m / NB panel updates; 2 CTAs/SM x 148 SMs x
@@ -205,14 +207,15 @@ cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, c
     const char* e = getenv("HBPDC_GJ_OCC");
     return e ? atoi(e) : 2;
   }();
-  auto go = [&](auto kern, int NB) {
-    size_t smem = (size_t)(GJ_MMAX * (NB + 4) + NB * GJ_APS) * sizeof(double);
+  auto go = [&](auto kern, int NB, int T) {
+    size_t smem = (size_t)(T * (NB + 4) + NB * GJ_APS) * sizeof(double);
     if (occ == 1 && m > 128) smem = std::max<size_t>(smem, 120 * 1024);   // one CTA per SM
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<nmat, GJ_T, smem, st>>>(Z, S, m, info);
+    kern<<<nmat, T, smem, st>>>(Z, S, m, info);
   };
-  if (nb == 16) go(gj_kernel<16>, 16);
-  else go(gj_kernel<32>, 32);
+  if (m > 256) go(gj_kernel<32, 384>, 32, 384);
+  else if (nb == 16) go(gj_kernel<16, 256>, 16, 256);
+  else go(gj_kernel<32, 256>, 32, 256);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
@@ -638,7 +641,7 @@ static cudaError_t launch_gemvN(const double* S, const GemvRHS& io, int m, int n
     gemvN_tma_kernel<C, NR><<<grid, threads, smem, st>>>(S, io, m, nE, nst);                     \
   } break;
   switch (cpl) {
-    GT(1) GT(2) GT(3) GT(4) GT(5) GT(6) GT(7) GT(8)
+    GT(1) GT(2) GT(3) GT(4) GT(5) GT(6) GT(7) GT(8) GT(9) GT(10)     // m <= 320 (3D: 5 * 4^3)
     default: return cudaErrorInvalidValue;
   }
 #undef GT
@@ -684,7 +687,7 @@ cudaError_t launch_block_gemv2(const double* S, int shared, const double* W, con
   }
 #define G(C) case C: gemv2_kernel<C><<<nE, 256, 0, st>>>(S, shared, W, sig, U, V, m, nE); break;
   switch (cpl) {
-    G(1) G(2) G(3) G(4) G(5) G(6) G(7) G(8)
+    G(1) G(2) G(3) G(4) G(5) G(6) G(7) G(8) G(9) G(10)
     default: return cudaErrorInvalidValue;
   }
 #undef G
@@ -1239,15 +1242,21 @@ cudaError_t launch_fingerprint(const double* x, size_t L, unsigned long long* ou
 // admissibility of an Euler / NS state (negative pressure is an error):
 // flag[0] = smallest inadmissible node index e * nodes + k (0x7f7f7f7f if none),
 // flag[1] |= 1 for a non-finite value, 2 for rho <= 0 or p <= 0
-__global__ void admissible_kernel(const double* __restrict__ W, int nE, int nodes, double gm1, double eps2,
+__global__ void admissible_kernel(const double* __restrict__ W, int nE, int nodes, int nv, double gm1, double eps2,
                                   int* flag) {
   const int stride = gridDim.x * blockDim.x;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nE * nodes; t += stride) {
     const int e = t / nodes, k = t % nodes;
-    const double* w = W + (size_t)e * 4 * nodes + k;
-    const double rho = w[0], mx = w[nodes], my = w[2 * nodes], E = w[3 * nodes];
-    const bool fin = isfinite(rho) && isfinite(mx) && isfinite(my) && isfinite(E);
-    const double p = gm1 * (E - 0.5 * eps2 * (mx * mx + my * my) / rho);
+    const double* w = W + (size_t)e * nv * nodes + k;
+    const double rho = w[0], E = w[(size_t)(nv - 1) * nodes];
+    bool fin = isfinite(rho) && isfinite(E);
+    double ke = 0.0;
+    for (int v = 1; v < nv - 1; ++v) {          // 2 (2D) or 3 (3D) momentum components
+      const double mv = w[(size_t)v * nodes];
+      fin = fin && isfinite(mv);
+      ke = fma(mv, mv, ke);
+    }
+    const double p = gm1 * (E - 0.5 * eps2 * ke / rho);
     if (!fin || !(rho > 0.0) || !(p > 0.0)) {
       atomicMin(flag, t);
       atomicOr(flag + 1, fin ? 2 : 1);
@@ -1255,12 +1264,12 @@ __global__ void admissible_kernel(const double* __restrict__ W, int nE, int node
   }
 }
 
-cudaError_t launch_admissible(const double* W, int nE, int nodes, double gamma, double eps2, int* flag,
+cudaError_t launch_admissible(const double* W, int nE, int nodes, int nv, double gamma, double eps2, int* flag,
                               cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(flag, 0x7f, sizeof(int), st);      // 0x7f7f7f7f: no bad node
   if (e == cudaSuccess) e = cudaMemsetAsync(flag + 1, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  admissible_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(W, nE, nodes, gamma - 1.0, eps2, flag);
+  admissible_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(W, nE, nodes, nv, gamma - 1.0, eps2, flag);
   hbpdc_count_launch();
   return cudaGetLastError();
 }

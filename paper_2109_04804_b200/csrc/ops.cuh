@@ -29,6 +29,8 @@ struct Geo {
   int nx, ny, nE;          // local element grid
   int hx, hy;              // 1: the -x/+x (-y/+y) neighbours are ghosts (halo), not a local wrap
   double sx, sy;           // 2/dx, 2/dy
+  int nz;                  // 3D (NEXT-4): elements in z (single rank, periodic); 1 otherwise
+  double sz;               // 2/dz
   double lhp, lhm;         // lhat_N(+1) = 1/w_N, lhat_0(-1) = 1/w_0  (GLL)
   double Dh[64];           // Dhat (P x P, row-major)
   int gl, P, dim;          // gl: Gauss-Legendre nodes (no node on the element edge)
@@ -116,6 +118,13 @@ __device__ __forceinline__ void trace_load(const G& g, int n, int d, St& st, Ld 
 // nE + g, g = [-x: ey | +x: ny + ey | -y: 2ny + ex | +y: 2ny + nx + ex]
 // (1D: ny = 1), whose face traces the halo exchange filled in (comm.h).
 __device__ __forceinline__ int nbr_elem(const Geo& g, int e, int d, int side) {
+  if (g.dim == 3) {              // 3D: e = (ez ny + ey) nx + ex, periodic wrap (one rank)
+    int ex = e % g.nx, ey = (e / g.nx) % g.ny, ez = e / (g.nx * g.ny);
+    if (d == 0) ex = side > 0 ? (ex + 1 == g.nx ? 0 : ex + 1) : (ex == 0 ? g.nx - 1 : ex - 1);
+    else if (d == 1) ey = side > 0 ? (ey + 1 == g.ny ? 0 : ey + 1) : (ey == 0 ? g.ny - 1 : ey - 1);
+    else ez = side > 0 ? (ez + 1 == g.nz ? 0 : ez + 1) : (ez == 0 ? g.nz - 1 : ez - 1);
+    return (ez * g.ny + ey) * g.nx + ex;
+  }
   int ex = e % g.nx, ey = e / g.nx;
   if (d == 0) {
     if (side > 0) {
@@ -146,8 +155,12 @@ template <int EQ, int DIM, class T>
 __device__ __forceinline__ void vol_flux_all(const PhysParams& pp, const NodeState<EQ, T>& s,
                                              T (&F)[DIM][NVars<EQ>::value]) {
   if constexpr (EQ == 0) {
-    F[0][0] = pp.ax * s.w[0];
-    if constexpr (DIM == 2) F[1][0] = pp.ay * s.w[0];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) F[d][0] = adv_speed(pp, d) * s.w[0];
+  } else if constexpr (EQ == 3) {
+    const EulerPrim3<T> q = euler3_prim(pp, s.w);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) euler3_flux(s.w, q, d, F[d]);
   } else {
     const EulerPrim<T> q = euler_prim(pp, s.w);
 #pragma unroll
@@ -246,6 +259,10 @@ __device__ __forceinline__ void half_flux(const PhysParams& pp, const NodeState<
   if constexpr (EQ == 0) {
     phys_flux<EQ>(pp, s.w, d, F);
     lam = jconst<T>(0.0);
+  } else if constexpr (EQ == 3) {
+    const EulerPrim3<T> q = euler3_prim(pp, s.w);
+    euler3_flux(s.w, q, d, F);
+    lam = euler3_speed(pp, q, d);
   } else {
     const EulerPrim<T> q = euler_prim(pp, s.w);
     euler_flux(s.w, q, d, F);
@@ -285,15 +302,14 @@ __device__ __forceinline__ void face_from_halves(const PhysParams& pp, const dou
   };
   T lam;
   if constexpr (EQ == 0) {
-    lam = jconst<T>(d == 0 ? (pp.ax >= 0 ? pp.ax : -pp.ax) : (pp.ay >= 0 ? pp.ay : -pp.ay));
+    lam = jconst<T>(fabs(adv_speed(pp, d)));
   } else {
     lam = pp.glf ? jconst<T>(1.0) : jmax(rd(rL, 2 * NV), rd(rR, 2 * NV));
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if (pp.glf) {       // as llf_flux: eq:Riemann with the constant Lambda, no 1/2 on the jump
-      const double lv = EQ == 0 ? (d == 0 ? fabs(pp.ax) : fabs(pp.ay))
-                                : ((v == 0 || v == NV - 1) ? pp.ieps : 1.0);
+      const double lv = EQ == 0 ? fabs(adv_speed(pp, d)) : ((v == 0 || v == NV - 1) ? pp.ieps : 1.0);
       f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + lv * (rd(rL, NV + v) - rd(rR, NV + v));
     } else {
       f[v] = 0.5 * (rd(rL, v) + rd(rR, v)) + 0.5 * lam * (rd(rL, NV + v) - rd(rR, NV + v));
@@ -360,11 +376,18 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
 //            JVP), spread over all threads of the element -> raw parts in smem
 //   phase 3  every thread: Dhat contraction; boundary nodes combine the parts
 //            of their face(s) (Mode::face_combine) into the surface terms
+// rows of a volume plane (x-lines of P nodes, padded to P + 1) and nodes per face
+template <int DIM, int P> struct Dims {
+  static constexpr int ROWS = DIM == 1 ? 1 : (DIM == 2 ? P : P * P);
+  static constexpr int FN = ROWS;
+  static constexpr int NODES = ROWS * P;
+};
+
 template <int EQ, int DIM, int P, class Mode>
 __host__ __device__ constexpr int slot_doubles() {
-  return Mode::NCH * DIM * NVars<EQ>::value * (DIM == 2 ? P : 1) * (P + 1) +
-         Mode::NFP * 2 * DIM * (DIM == 2 ? P : 1) * Mode::FPD +
-         Staged<Mode>::value * (DIM == 2 ? P * P : P);      // per-thread staging [k][node]
+  return Mode::NCH * DIM * NVars<EQ>::value * Dims<DIM, P>::ROWS * (P + 1) +
+         Mode::NFP * 2 * DIM * Dims<DIM, P>::FN * Mode::FPD +
+         Staged<Mode>::value * Dims<DIM, P>::NODES;      // per-thread staging [k][node]
 }
 
 template <int EQ, int DIM, int P, class Mode, class G>
@@ -374,26 +397,37 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
   constexpr int NV = NVars<EQ>::value;
   constexpr int NCH = Mode::NCH;
   constexpr int NFP = Mode::NFP;
+  static_assert(DIM < 3 || !G::GL, "3D: Gauss-Lobatto nodes only");
   constexpr int PS = P + 1;                       // padded row stride (bank conflicts)
-  constexpr int PLANE = (DIM == 2 ? P : 1) * PS;  // one (ch, d, v) plane
-  constexpr int FN = DIM == 2 ? P : 1;            // nodes per face
+  constexpr int ROWS = Dims<DIM, P>::ROWS;        // x-lines per plane: 1 (1D), P (2D), P^2 (3D)
+  constexpr int PLANE = ROWS * PS;                // one (ch, d, v) plane [k][j][i], i padded
+  constexpr int FN = Dims<DIM, P>::FN;            // nodes per face
   constexpr int NFN = 2 * DIM * FN;               // face nodes per element
   double* sRaw = sF + NCH * DIM * NV * PLANE;     // [FPD][part][face node] (conflict-free)
   const int i = node % P;
-  const int j = DIM == 2 ? node / P : 0;
-  constexpr int NODES_ = DIM == 2 ? P * P : P;
+  const int j = DIM >= 2 ? (node / P) % P : 0;
+  const int kz = DIM == 3 ? node / (P * P) : 0;
+  const int row = DIM == 3 ? kz * P + j : j;      // this node's x-line
+  constexpr int NODES_ = Dims<DIM, P>::NODES;
   // staged only with one face item per thread (2D: P >= 8) and GLL (GL traces are line sums)
   constexpr int NST = (G::GL || NFP * NFN > NODES_) ? 0 : Staged<Mode>::value;
   double* sStage = sRaw + NFP * NFN * Mode::FPD + node;   // this thread's staging column [k * NODES_]
   auto face_item = [&](int it, int& part, int& fn, int& own, int& nb, int& nnode, int& d, bool& plus) {
-    // face f: 0 = -x, 1 = +x, 2 = -y, 3 = +y; node k along the face
+    // face f: 0 = -x, 1 = +x, 2 = -y, 3 = +y (3D: 4 = -z, 5 = +z); node k along the face
+    // (2D: the line index; 3D: x-faces k = kz P + j, y-faces kz P + i, z-faces j P + i)
     part = it / NFN; fn = it % NFN;
     const int f = fn / FN, k = fn % FN;
     d = f >> 1;
     plus = f & 1;
     const int own_edge = plus ? P - 1 : 0, nbr_edge = plus ? 0 : P - 1;
-    own = DIM == 1 ? own_edge : (d == 0 ? k * P + own_edge : own_edge * P + k);
-    nnode = DIM == 1 ? nbr_edge : (d == 0 ? k * P + nbr_edge : nbr_edge * P + k);
+    if constexpr (DIM == 3) {
+      const int a = k % P, b = k / P;
+      own = d == 0 ? (b * P + a) * P + own_edge : (d == 1 ? (b * P + own_edge) * P + a : (own_edge * P + b) * P + a);
+      nnode = d == 0 ? (b * P + a) * P + nbr_edge : (d == 1 ? (b * P + nbr_edge) * P + a : (nbr_edge * P + b) * P + a);
+    } else {
+      own = DIM == 1 ? own_edge : (d == 0 ? k * P + own_edge : own_edge * P + k);
+      nnode = DIM == 1 ? nbr_edge : (d == 0 ? k * P + nbr_edge : nbr_edge * P + k);
+    }
     nb = nbr_elem(g, e, d, plus ? +1 : -1);
   };
   if constexpr (NST > 0) {
@@ -413,7 +447,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i] = cf[d][c][v];
+          for (int v = 0; v < NV; ++v) sF[((c * DIM + d) * NV + v) * PLANE + row * PS + i] = cf[d][c][v];
     };
     if constexpr (VolPasses<Mode>::value == 2) {
       // two jet states evaluated one after the other, the first parked in this
@@ -427,7 +461,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) cg[d][c][v] = sF[((c * DIM + d) * NV + v) * PLANE + j * PS + i];
+          for (int v = 0; v < NV; ++v) cg[d][c][v] = sF[((c * DIM + d) * NV + v) * PLANE + row * PS + i];
       Mode::template vol_pass1<DIM>(A, pp, e, node, cg);
       put(cg);
     } else {
@@ -438,7 +472,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       put(cf);
     }
   }
-  constexpr int NODES = DIM == 2 ? P * P : P;
+  constexpr int NODES = NODES_;
   if constexpr (NST > 0) {
     if (active && node < NFP * NFN) {
       int part, fn, own, nb, nnode, d;
@@ -470,7 +504,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       const int fn = f * FN + k;
       double cf[NCH][NV];
       Mode::face_combine(A, pp, d, sRaw + fn, sRaw + NFN + fn, NFP * NFN, cf);
-      const double sc = (d == 0 ? g.sx : g.sy) * lh;
+      const double sc = (d == 0 ? g.sx : (d == 1 ? g.sy : g.sz)) * lh;
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
@@ -484,6 +518,13 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
         const int t = d == 0 ? i : j;
         add_face(plus ? 1 + 2 * d : 2 * d, d == 0 ? j : i, plus ? g.lhpv[t] : -g.lhmv[t]);
       }
+    } else if constexpr (DIM == 3) {
+      if (i == P - 1) add_face(1, kz * P + j, g.lhp);
+      if (i == 0) add_face(0, kz * P + j, -g.lhm);
+      if (j == P - 1) add_face(3, kz * P + i, g.lhp);
+      if (j == 0) add_face(2, kz * P + i, -g.lhm);
+      if (kz == P - 1) add_face(5, j * P + i, g.lhp);
+      if (kz == 0) add_face(4, j * P + i, -g.lhm);
     } else {
       if (i == P - 1) add_face(1, j, g.lhp);
       if (i == 0) add_face(0, j, -g.lhm);
@@ -491,27 +532,35 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       if (DIM == 2 && j == 0) add_face(2, i, -g.lhm);
     }
     if constexpr (!kDmmaContract<DIM, P>) {
-      double Dr[P], Dc[P];
+      double Dr[P], Dc[P], Dz[P];
 #pragma unroll
       for (int l = 0; l < P; ++l) {
         Dr[l] = g.Dh[i * P + l];
-        Dc[l] = DIM == 2 ? g.Dh[j * P + l] : 0.0;
+        Dc[l] = DIM >= 2 ? g.Dh[j * P + l] : 0.0;
+        Dz[l] = DIM == 3 ? g.Dh[kz * P + l] : 0.0;
       }
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE + j * PS;
+          const double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE + row * PS;
           double ax = 0.0;
 #pragma unroll
           for (int l = 0; l < P; ++l) ax = fma(Dr[l], Fx[l], ax);
           double acc = g.sx * ax;
-          if constexpr (DIM == 2) {
-            const double* Fy = sF + ((c * DIM + 1) * NV + v) * PLANE + i;
+          if constexpr (DIM >= 2) {
+            const double* Fy = sF + ((c * DIM + 1) * NV + v) * PLANE + kz * P * PS + i;
             double ay = 0.0;
 #pragma unroll
             for (int l = 0; l < P; ++l) ay = fma(Dc[l], Fy[l * PS], ay);
             acc = fma(g.sy, ay, acc);
+          }
+          if constexpr (DIM == 3) {
+            const double* Fz = sF + ((c * DIM + 2) * NV + v) * PLANE + j * PS + i;
+            double az = 0.0;
+#pragma unroll
+            for (int l = 0; l < P; ++l) az = fma(Dz[l], Fz[l * P * PS], az);
+            acc = fma(g.sz, az, acc);
           }
           out[c][v] = -(acc + sf[c][v]);
         }
@@ -557,7 +606,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
         for (int v = 0; v < NV; ++v)
-          out[c][v] = -(sF[((c * DIM + 0) * NV + v) * PLANE + j * PS + i] + out[c][v]);
+          out[c][v] = -(sF[((c * DIM + 0) * NV + v) * PLANE + row * PS + i] + out[c][v]);
     }
   }
 }

@@ -14,6 +14,9 @@
 #ifndef HBPDC_OPS_BR2
 #define HBPDC_OPS_BR2 0       // 1: the Navier-Stokes operators with BR2 face gradients (ops_kernels*_br2.cu)
 #endif
+#ifndef HBPDC_OPS_3D
+#define HBPDC_OPS_3D 0        // 1: the 3D hexahedral instantiations (ops_kernels_3d.cu, NEXT-4)
+#endif
 static constexpr bool kGL = HBPDC_OPS_GL;
 static constexpr bool kBR2 = HBPDC_OPS_BR2;
 using GeoK = GeoSel<kGL>;
@@ -294,17 +297,32 @@ template <class F>
 static cudaError_t dispatch(const OpCfg& c, F&& f) {
 #define CASE(EQ, DIM, PP) \
   if (c.eq == EQ && c.dim == DIM && c.P == PP) return f(Disp<EQ, DIM, PP>{});
+#if HBPDC_OPS_3D
+  // 3D hexahedra, GLL: advection (EQ 0) and Euler (EQ 3: five variables), N = 1..3
+  CASE(0, 3, 2) CASE(0, 3, 3) CASE(0, 3, 4)
+  CASE(3, 3, 2) CASE(3, 3, 3) CASE(3, 3, 4)
+#else
 #if !HBPDC_OPS_BR2
   HBPDC_P_LIST(CASE, 0, 1)
   HBPDC_P_LIST(CASE, 0, 2)
   HBPDC_P_LIST(CASE, 1, 2)
 #endif
   HBPDC_P_LIST(CASE, 2, 2)
+#endif
 #undef CASE
   return cudaErrorInvalidValue;
 }
 
-#if HBPDC_OPS_BR2
+#if HBPDC_OPS_3D
+cudaError_t launch_op_3d(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
+  return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
+}
+
+cudaError_t launch_kbuild_3d(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
+                             double c2, double* M, int e0, int ne, const double* Sb, const double* gSb) {
+  return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb); });
+}
+#elif HBPDC_OPS_BR2
 #if HBPDC_OPS_GL
 cudaError_t launch_op_gl_br2(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
 #else
@@ -334,6 +352,7 @@ int op_grid(const OpCfg& c, const Geo& g) {
 }
 
 cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A) {
+  if (c.dim == 3) return launch_op_3d(kind, c, g, A);
   if (g.br2) return g.gl ? launch_op_gl_br2(kind, c, g, A) : launch_op_br2(kind, c, g, A);
   if (g.gl) return launch_op_gl(kind, c, g, A);
   return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
@@ -362,6 +381,7 @@ int lift_jet_components(OpKind kind, int state) {
 
 cudaError_t launch_kbuild(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt, double c2,
                           double* M, int e0, int ne, const double* Sb, const double* gSb) {
+  if (c.dim == 3) return launch_kbuild_3d(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb);
   if (g.gl) return launch_kbuild_gl(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb);
   return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb); });
 }

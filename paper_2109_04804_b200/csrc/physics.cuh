@@ -17,16 +17,23 @@
 #include "jets.cuh"
 
 struct PhysParams {
-  double ax, ay;         // advection velocity
+  double ax, ay;         // advection velocity (az: 3D, below)
   double gamma;
   double mu, lamT, Rgas; // NS: viscosity, heat conductivity c_p mu / Pr, R = 1/gamma
   int glf;               // 1: the paper's global LF flux (Lambda = diag(1/eps,1,1,1/eps)), 0: LLF
   double ieps, eps2, ieps2;   // reference Mach number eps of eq:Euler: 1/eps, eps^2, 1/eps^2
   double eta_br2;        // NS BR2 lifting: eta (face gradients, lift_kernel)
+  double az;             // advection velocity, z component (3D)
 };
 
+// EQ: 0 advection, 1 Euler 2D, 2 Navier-Stokes 2D, 3 Euler 3D (NEXT-4: (rho, rho u, rho v, rho w, E))
 template <int EQ> struct NVars { static constexpr int value = 4; };
 template <> struct NVars<0> { static constexpr int value = 1; };
+template <> struct NVars<3> { static constexpr int value = 5; };
+
+__host__ __device__ inline double adv_speed(const struct PhysParams& pp, int d) {
+  return d == 0 ? pp.ax : (d == 1 ? pp.ay : pp.az);
+}
 
 // Euler primitives of a node state, computed once and shared by both flux
 // directions and the wave speed: one jet reciprocal per state.
@@ -57,11 +64,46 @@ __device__ __forceinline__ void euler_flux(const T* w, const EulerPrim<T>& q, in
   F[3] = vn * q.H;
 }
 
+// ---- 3D Euler (eq:Euler with three momentum components; the paper's 3D case P:1080-1093)
+template <class T> struct EulerPrim3 {
+  T u, v, w, p, H, rinv, pe;
+};
+
+template <class T>
+__device__ __forceinline__ EulerPrim3<T> euler3_prim(const PhysParams& pp, const T* w) {
+  EulerPrim3<T> q;
+  q.rinv = jrecip(w[0]);
+  q.u = w[1] * q.rinv;
+  q.v = w[2] * q.rinv;
+  q.w = w[3] * q.rinv;
+  q.p = (pp.gamma - 1.0) * (w[4] - (0.5 * pp.eps2) * (w[1] * q.u + w[2] * q.v + w[3] * q.w));
+  q.H = w[4] + q.p;
+  q.pe = pp.ieps2 * q.p;
+  return q;
+}
+
+template <class T>
+__device__ __forceinline__ void euler3_flux(const T* w, const EulerPrim3<T>& q, int d, T* F) {
+  const T vn = d == 0 ? q.u : (d == 1 ? q.v : q.w);
+  F[0] = w[1 + d];
+  F[1] = d == 0 ? w[1] * vn + q.pe : w[1] * vn;
+  F[2] = d == 1 ? w[2] * vn + q.pe : w[2] * vn;
+  F[3] = d == 2 ? w[3] * vn + q.pe : w[3] * vn;
+  F[4] = vn * q.H;
+}
+
+template <class T>
+__device__ __forceinline__ T euler3_speed(const PhysParams& pp, const EulerPrim3<T>& q, int d) {
+  return jabs(d == 0 ? q.u : (d == 1 ? q.v : q.w)) + pp.ieps * jsqrt(pp.gamma * q.p * q.rinv);
+}
+
 // inviscid flux in direction d
 template <int EQ, class T>
 __device__ __forceinline__ void phys_flux(const PhysParams& pp, const T* w, int d, T* F) {
   if constexpr (EQ == 0) {
-    F[0] = (d == 0 ? pp.ax : pp.ay) * w[0];
+    F[0] = adv_speed(pp, d) * w[0];
+  } else if constexpr (EQ == 3) {
+    euler3_flux(w, euler3_prim(pp, w), d, F);
   } else {
     euler_flux(w, euler_prim(pp, w), d, F);
   }
@@ -81,7 +123,12 @@ __device__ __forceinline__ void llf_flux(const PhysParams& pp, const T* wL, cons
   if constexpr (EQ == 0) {
     phys_flux<EQ>(pp, wL, d, FL);
     phys_flux<EQ>(pp, wR, d, FR);
-    lam = jconst<T>(d == 0 ? (pp.ax >= 0 ? pp.ax : -pp.ax) : (pp.ay >= 0 ? pp.ay : -pp.ay));
+    lam = jconst<T>(fabs(adv_speed(pp, d)));
+  } else if constexpr (EQ == 3) {
+    const EulerPrim3<T> qL = euler3_prim(pp, wL), qR = euler3_prim(pp, wR);
+    euler3_flux(wL, qL, d, FL);
+    euler3_flux(wR, qR, d, FR);
+    lam = pp.glf ? jconst<T>(1.0) : jmax(euler3_speed(pp, qL, d), euler3_speed(pp, qR, d));
   } else {
     const EulerPrim<T> qL = euler_prim(pp, wL), qR = euler_prim(pp, wR);
     euler_flux(wL, qL, d, FL);
@@ -92,8 +139,7 @@ __device__ __forceinline__ void llf_flux(const PhysParams& pp, const T* wL, cons
   for (int v = 0; v < NV; ++v) {
     if (pp.glf) {       // eq:Riemann: full Lambda on the jump, no 1/2; Lambda = |a_d|,
                         // diag(1/eps, 1, 1, 1/eps)
-      const double lv = EQ == 0 ? (d == 0 ? fabs(pp.ax) : fabs(pp.ay))
-                                : ((v == 0 || v == NV - 1) ? pp.ieps : 1.0);
+      const double lv = EQ == 0 ? fabs(adv_speed(pp, d)) : ((v == 0 || v == NV - 1) ? pp.ieps : 1.0);
       f[v] = 0.5 * (FL[v] + FR[v]) + lv * (wL[v] - wR[v]);
     } else {
       f[v] = 0.5 * (FL[v] + FR[v]) + 0.5 * lam * (wL[v] - wR[v]);

@@ -25,7 +25,7 @@ _JVP = {"auto": JVP_AUTO, "fd": JVP_FD, "exact": JVP_EXACT, "linear": JVP_LINEAR
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_CUDA", 3: "E_NCCL", 4: "E_OOM", 5: "E_NONFINITE",
           6: "E_NEG_PRESSURE", 7: "E_LU_SINGULAR", 8: "E_NEWTON", 9: "E_GMRES"}
 
-EXPORTS = ["hbpdc_init", "hbpdc_local_shape", "hbpdc_node_coords", "hbpdc_rhs", "hbpdc_residual",
+EXPORTS = ["hbpdc_init", "hbpdc_local_shape", "hbpdc_node_coords", "hbpdc_node_coords_z", "hbpdc_rhs", "hbpdc_residual",
            "hbpdc_jvp", "hbpdc_precond_build", "hbpdc_precond_set", "hbpdc_precond_export",
            "hbpdc_precond_apply", "hbpdc_step", "hbpdc_step_host", "hbpdc_reset", "hbpdc_profile",
            "hbpdc_profile_read", "hbpdc_launch_count", "hbpdc_last_error", "hbpdc_finalize",
@@ -42,7 +42,8 @@ class Problem(ctypes.Structure):
                 ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("xmin", ctypes.c_double),
                 ("xmax", ctypes.c_double), ("ymin", ctypes.c_double), ("ymax", ctypes.c_double),
                 ("flux", ctypes.c_int), ("lifting", ctypes.c_int), ("q", ctypes.c_int),
-                ("kmax", ctypes.c_int), ("eta_br2", ctypes.c_double)]
+                ("kmax", ctypes.c_int), ("eta_br2", ctypes.c_double), ("nz", ctypes.c_int),
+                ("zmin", ctypes.c_double), ("zmax", ctypes.c_double), ("az", ctypes.c_double)]
 
 
 class SolverOpts(ctypes.Structure):
@@ -90,6 +91,7 @@ def load():
                            ctypes.POINTER(P)]),
         "hbpdc_local_shape": (I, [P] + [ctypes.POINTER(ctypes.c_int)] * 6),
         "hbpdc_node_coords": (I, [P, P, P]),
+        "hbpdc_node_coords_z": (I, [P, P]),
         "hbpdc_rhs": (I, [P, P, P, P]),
         "hbpdc_residual": (I, [P, D, D, D, P, P, P, P, P, ctypes.POINTER(D)]),
         "hbpdc_jvp": (I, [P, D, D, D, P, P, P, P, P, P, I, P]),
@@ -188,7 +190,7 @@ class Context:
                  restart=700, max_krylov=7000, precond="bjext", precond_policy="per_step_per_alpha",
                  jvp_mode="auto", batch_stages=True, gmres_sstep=1, rank=0, nranks=1, px=1, py=1, nccl_id=None, stream=None, device=0,
                  comm="auto", loopback=None, force_halo=False, flux="llf", mach=1.0, schur=False,
-                 nodes="gll", lifting="br1", eta_br2=2.0):
+                 nodes="gll", lifting="br1", eta_br2=2.0, nz=1):
         import torch
         self.lib = load()
         if not torch.cuda.is_available():
@@ -196,7 +198,9 @@ class Context:
         pb = Problem(dim=dim, equation=_EQ[equation], gamma=gamma, mach_eps=mach, mu=mu, prandtl=prandtl,
                      N=N, nodes={"gll": GLL, "gl": GL}[nodes], nx=nx, ny=ny, xmin=bounds[0], xmax=bounds[1], ymin=bounds[2],
                      ymax=bounds[3], flux={"llf": 0, "glf": 1}[flux], lifting={"br1": 0, "br2": 1}[lifting],
-                     q=q, kmax=kmax, eta_br2=eta_br2)
+                     q=q, kmax=kmax, eta_br2=eta_br2, nz=nz,
+                     zmin=bounds[4] if len(bounds) > 4 else 0.0, zmax=bounds[5] if len(bounds) > 5 else 1.0,
+                     az=a[2] if len(a) > 2 else 0.0)
         pb.a[0], pb.a[1] = a[0], a[1]
         op = SolverOpts(newton_rtol=newton_rtol, newton_atol_dw=newton_atol_dw, newton_floor=newton_floor,
                         newton_max=newton_max, gmres_rtol=gmres_rtol, gmres_restart=restart,
@@ -228,6 +232,7 @@ class Context:
         self.n_elem, self.m, self.ex0, self.ey0, self.nx_local, self.ny_local = [v.value for v in vals]
         self.n = self.n_elem * self.m
         self.dim, self.N = dim, N
+        self.nz_local = nz if dim == 3 else 1
         self.device = device
         self.rank, self.nranks, self.px, self.py = rank, nranks, px, py
 
@@ -249,6 +254,11 @@ class Context:
         p = self.N + 1
         if self.dim == 1:
             return (x.reshape(self.nx_local, p),)
+        if self.dim == 3:
+            z = np.zeros(self.n_elem * nodes)
+            self._check(self.lib.hbpdc_node_coords_z(self.h, z.ctypes.data_as(ctypes.c_void_p)))
+            sh = (self.nz_local, self.ny_local, self.nx_local, p, p, p)
+            return (x.reshape(sh), y.reshape(sh), z.reshape(sh))
         sh = (self.ny_local, self.nx_local, p, p)
         return (x.reshape(sh), y.reshape(sh))
 
