@@ -11,3 +11,5 @@ for T in racecheck synccheck memcheck; do
   echo "sanitize $T rc=$?" | tee -a $OUT/summary.txt
   tail -3 $OUT/sanitize_$T.log
 done
+HBPDC_GJ_NB=16 timeout 300 python -m pytest tests/test_gpu_br2.py -m gpu -q -k "end_of_run and gll" > $OUT/br2_nb16.log 2>&1; echo "br2 nb16 rc=$?" | tee -a $OUT/summary.txt
+HBPDC_TRACE=1 timeout 300 python -m pytest tests/test_gpu_br2.py -m gpu -q -k "end_of_run and gll" > $OUT/br2_trace.log 2>&1; echo "br2 trace rc=$?" | tee -a $OUT/summary.txt
