@@ -551,6 +551,10 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
     // seeded elements only), so each (colour, column) costs 1 / (Px Py) of a full-mesh
     // operator instead of one.  tseed is zero outside the seeded elements throughout.
     CK(cudaMemsetAsync(c->tseed, 0, c->n * sizeof(double), c->stream));
+    // m <= 160: one operator pass per column (K e_c); K_i^2 by the element-block product on
+    // the fp64 tensor cores afterwards (K_i^2 e_c = K_i (K_i e_c) exactly: the same block),
+    // instead of a second colour pass through lifting and operator per column
+    const bool single = kk_gemm_supported(c->m) && !std::getenv("HBPDC_NS_TWOPASS");
     const Geo full = c->geo;
     for (int cy = 0; cy < Py; ++cy)
       for (int cx = 0; cx < Px; ++cx) {
@@ -573,6 +577,13 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
             st = run_op(c, OP_JVP_EXACT, H);
             if (st != HBPDC_OK) break;
           }
+          if (single) {
+            // K column only; K_i^2 comes from the element-block product below (kk_gemm)
+            ce = launch_colour_gather_k(c->y1, hess ? c->y3 : nullptr, c->Kst, c->S, c->nE, c->nxl, c->m, Px, Py,
+                                        cx, cy, col, c2, c->stream);
+            if (ce != cudaSuccess) { c->geo = full; CK(ce); }
+            continue;
+          }
           ce = launch_colour_restrict(c->y1, c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, c->stream);
           if (ce != cudaSuccess) { c->geo = full; CK(ce); }
           A.out2 = c->y2;
@@ -587,6 +598,7 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
         // clear this colour's elements of tseed for the next colour
         CK(launch_colour_seed(c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, -1, c->stream));
       }
+    if (single) CK(launch_kk_gemm(c->Kst, c->S, c->m, c->nE, a1dt, c2, c->stream));
   }
   std::vector<int> hinfo(c->zchunk);
   for (int e0 = 0; e0 < nblk; e0 += c->zchunk) {

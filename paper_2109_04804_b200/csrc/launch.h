@@ -55,6 +55,12 @@ cudaError_t launch_colour_seed(double* t, int nE, int nx, int m, int Px, int Py,
                                cudaStream_t st);
 cudaError_t launch_colour_restrict(const double* y, double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy,
                                    cudaStream_t st);
+// single-pass colour build (m <= 160): K column (and c2 H column for BJ^H_ext) per seeded element, then
+// M_i += I - a1dt K_i + c2 K_i^2 for all elements on the fp64 tensor cores (kk_gemm)
+cudaError_t launch_colour_gather_k(const double* y1, const double* y3, double* K, double* M, int nE, int nx, int m,
+                                   int Px, int Py, int cx, int cy, int col, double c2, cudaStream_t st);
+bool kk_gemm_supported(int m);
+cudaError_t launch_kk_gemm(const double* K, double* M, int m, int nE, double a1dt, double c2, cudaStream_t st);
 cudaError_t launch_colour_gather(const double* y1, const double* y2, const double* y3, double* K, double* M, int nE,
                                  int nx, int m, int Px, int Py, int cx, int cy, int col, double a1dt, double c2,
                                  cudaStream_t st);

@@ -214,6 +214,7 @@ cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, c
     kern<<<nmat, T, smem, st>>>(Z, S, m, info);
   };
   if (m > 256) go(gj_kernel<32, 384>, 32, 384);
+  else if (m <= 160 && !getenv("HBPDC_GJ_T256")) go(gj_kernel<32, 160>, 32, 160);   // C5: m = 144
   else if (nb == 16) go(gj_kernel<16, 256>, 16, 256);
   else go(gj_kernel<32, 256>, 32, 256);
   hbpdc_count_launch();

@@ -190,6 +190,7 @@ template <int EQ, int NODES> struct ModeR12 : OneJetMode<EQ, NODES, ModeR12<EQ, 
 // (eq:Newton_Residual; P:236-239 read as R4)
 template <int EQ, int NODES> struct ModeResid : OneJetMode<EQ, NODES, ModeResid<EQ, NODES>, J1, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
+  static constexpr bool NO_DMMA = true;     // FMA contraction measured faster here (r02e)
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool) {
     for (int v = 0; v < NV; ++v) w[v] = J1{FV(W, e, v, node), FV(S, e, v, node)};
@@ -403,8 +404,10 @@ template <int EQ, int NODES> struct ModeJvpFD {
   // Staged face loads (GLL, Euler / advection): the thread of face item (part, node) prefetches
   // the neighbour node's W, sigma and dW (part 0) or dsigma (part 1) with cp.async before the
   // volume flux; its own edge node is L1-resident (loaded by the element's volume pass).
+// Off by default: measured slower in the same session (r02e, C3 FD JVP 157 -> 166 us with the
+// DMMA contraction; the extra shared memory costs occupancy more than the L2 latency it hides).
 #ifndef HBPDC_STAGE_FACES
-#define HBPDC_STAGE_FACES 1
+#define HBPDC_STAGE_FACES 0
 #endif
   static constexpr int NSTAGE = (EQ != 2 && HBPDC_STAGE_FACES) ? 3 * NV : 0;
   __device__ static void prefetch(const Args& A, int, int, int nb, int nnode, int part, double* st, int stride) {

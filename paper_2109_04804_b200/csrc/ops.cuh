@@ -353,14 +353,16 @@ template <class M> struct VolPasses<M, std::void_t<decltype(M::VOL_PASSES)>> {
 
 // ---- fp64 tensor-core contraction (mma.sync m8n8k4 f64: A row-major 8x4, B col-major 4x8;
 // lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) + {0,1}])
-// Off by default: measured on C3 (r02b) the extra barrier and shared-memory round trip cost
-// more than the 128 FMAs per node they replace (FD JVP 151 -> 157 us, residual 93 -> 108 us);
-// the operators are bound by the flux arithmetic, not the contraction.
+// Per mode (measured in one session, r02e, C3): R1 57 -> 44 us, EXACT JVP 127 -> 124.9, FD JVP
+// 159 -> 157 with the tensor-core contraction; the residual alone gets slower (101.5 -> 109) and
+// opts out (NO_DMMA).  The operators stay bound by the flux arithmetic, not the contraction.
 #ifndef HBPDC_DMMA_CONTRACT
-#define HBPDC_DMMA_CONTRACT 0
+#define HBPDC_DMMA_CONTRACT 1
 #endif
-template <int DIM, int P>
-constexpr bool kDmmaContract = HBPDC_DMMA_CONTRACT && DIM == 2 && P == 8;
+template <class M, class = void> struct NoDmma : std::false_type {};
+template <class M> struct NoDmma<M, std::void_t<decltype(M::NO_DMMA)>> : std::true_type {};
+template <int DIM, int P, class Mode = void>
+constexpr bool kDmmaContract = HBPDC_DMMA_CONTRACT && DIM == 2 && P == 8 && !NoDmma<Mode>::value;
 __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d[0]), "+d"(d[1])
@@ -531,7 +533,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       if (DIM == 2 && j == P - 1) add_face(3, i, g.lhp);
       if (DIM == 2 && j == 0) add_face(2, i, -g.lhm);
     }
-    if constexpr (!kDmmaContract<DIM, P>) {
+    if constexpr (!kDmmaContract<DIM, P, Mode>) {
       double Dr[P], Dc[P], Dz[P];
 #pragma unroll
       for (int l = 0; l < P; ++l) {
@@ -572,7 +574,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
         for (int v = 0; v < NV; ++v) out[c][v] = sf[c][v];
     }
   }
-  if constexpr (kDmmaContract<DIM, P>) {
+  if constexpr (kDmmaContract<DIM, P, Mode>) {
     // Volume contraction on the fp64 tensor cores (P = 8, 2D): per channel c and
     // variable v the element's 8 x 8 node plane gives
     //   V = sx F_x Dhat^T + sy Dhat F_y           (V_ji = sx sum_l Dhat_il Fx_jl + sy sum_m Dhat_jm Fy_mi)

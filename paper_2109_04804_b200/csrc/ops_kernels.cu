@@ -439,7 +439,85 @@ __global__ void colour_gather_kernel(const double* __restrict__ y1, const double
 }
 
 int colour_grid(size_t work) { return (int)std::min<size_t>(1184, (work + 255) / 256); }
+
+// K[e][r][col] = y1 for the colour's elements; M[e][r][col] = c2 (H e_col)_r (BJ^H_ext, y3 = e_col +
+// H e_col) or 0 -- the identity, K and K^2 terms are added afterwards by kk_gemm_kernel
+__global__ void colour_gather_k_kernel(const double* __restrict__ y1, const double* __restrict__ y3,
+                                       double* __restrict__ K, double* __restrict__ M, int nc, int nx, int m,
+                                       int Px, int Py, int cx, int cy, int col, double c2) {
+  const size_t n = (size_t)nc * m;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+    const int e = colour_elem((int)(k / m), nx, Px, Py, cx, cy), r = (int)(k % m);
+    const size_t i = (size_t)e * m + r;
+    const size_t o = i * m + col;
+    K[o] = y1[i];
+    M[o] = y3 ? c2 * (y3[i] - (r == col ? 1.0 : 0.0)) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void kk_dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// M_i += I - a1dt K_i + c2 K_i K_i for every element, K_i^2 on the fp64 tensor cores:
+// one CTA per element, K_i in shared memory (rows padded to ld = mp + 4, mp = m rounded up to 8,
+// zero padding), warp w takes the 8 x 8 output tiles w, w + 8, ..., k in steps of 4 (mma.sync m8n8k4).
+constexpr int KK_T = 256;
+__global__ void __launch_bounds__(KK_T, 1) kk_gemm_kernel(const double* __restrict__ K, double* __restrict__ M,
+                                                          int m, double a1dt, double c2) {
+  extern __shared__ __align__(16) double sk[];
+  const int mp = (m + 7) & ~7, ld = mp + 4;
+  const double* Ke = K + (size_t)blockIdx.x * m * m;
+  double* Me = M + (size_t)blockIdx.x * m * m;
+  for (int t = threadIdx.x; t < mp * ld; t += KK_T) {
+    const int r = t / ld, c = t % ld;
+    sk[t] = (r < m && c < m) ? Ke[(size_t)r * m + c] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int nt = mp / 8;
+  for (int tile = wid; tile < nt * nt; tile += KK_T / 32) {
+    const int r0 = 8 * (tile / nt), c0 = 8 * (tile % nt);
+    double acc[2] = {0.0, 0.0};
+    for (int k0 = 0; k0 < mp; k0 += 4)
+      kk_dmma(acc, sk[(r0 + g) * ld + k0 + q], sk[(k0 + q) * ld + c0 + g]);
+    const int r = r0 + g;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = c0 + 2 * q + h;
+      if (r < m && c < m) {
+        const size_t o = (size_t)r * m + c;
+        Me[o] += (r == c ? 1.0 : 0.0) - a1dt * sk[r * ld + c] + c2 * acc[h];
+      }
+    }
+  }
+}
 }  // namespace
+
+cudaError_t launch_colour_gather_k(const double* y1, const double* y3, double* K, double* M, int nE, int nx, int m,
+                                   int Px, int Py, int cx, int cy, int col, double c2, cudaStream_t st) {
+  const int nc = nE / (Px * Py);
+  colour_gather_k_kernel<<<colour_grid((size_t)nc * m), 256, 0, st>>>(y1, y3, K, M, nc, nx, m, Px, Py, cx, cy, col,
+                                                                     c2);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
+bool kk_gemm_supported(int m) { return m <= 160; }
+
+cudaError_t launch_kk_gemm(const double* K, double* M, int m, int nE, double a1dt, double c2, cudaStream_t st) {
+  if (!kk_gemm_supported(m)) return cudaErrorInvalidValue;
+  if (nE <= 0) return cudaSuccess;
+  const int mp = (m + 7) & ~7;
+  const size_t smem = (size_t)mp * (mp + 4) * sizeof(double);
+  cudaFuncSetAttribute(kk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kk_gemm_kernel<<<nE, KK_T, smem, st>>>(K, M, m, a1dt, c2);
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
 
 // seed (val = 1) or clear (val = 0: col = -1) the colour's elements of t
 cudaError_t launch_colour_seed(double* t, int nE, int nx, int m, int Px, int Py, int cx, int cy, int col,
