@@ -5,6 +5,7 @@ set -u
 OUT=gpurun_out/r02g
 mkdir -p $OUT
 make -C paper_2109_04804_b200/csrc -j8 > $OUT/build.log 2>&1 || { echo build failed; tail $OUT/build.log; exit 1; }
+bash scripts/gpu_r02g2.sh
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_br2.py tests/test_gpu_gl.py tests/test_gpu_fullsize.py -m gpu -q -k "precond or bjext or c5 or ns or navier or br2 or C5" > $OUT/pytest_ns.log 2>&1; echo "pytest ns rc=$?" | tee -a $OUT/summary.txt
 tail -3 $OUT/pytest_ns.log
 for C in C3 C5; do timeout 600 python scripts/op_times.py $C 20 >> $OUT/op_times.jsonl 2>> $OUT/op_times.err; done
