@@ -1743,7 +1743,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
     return bad("Navier-Stokes: mach_eps must be 1 (reading R18)");
   if (pb->q != 4 && pb->q != 6 && pb->q != 8) return bad("q must be 4, 6 or 8");
   if (pb->kmax < 0) return bad("kmax must be >= 0");
-  if (pb->nx < 1 || (pb->dim == 2 && pb->ny < 1)) return bad("element counts must be positive");
+  if (pb->nx < 1 || (pb->dim >= 2 && pb->ny < 1)) return bad("element counts must be positive");
   if (c->ds.nranks < 1 || c->ds.rank < 0 || c->ds.rank >= c->ds.nranks) return bad("bad rank / nranks");
   if (c->ds.px < 1 || c->ds.py < 1) { c->ds.px = c->ds.nranks; c->ds.py = 1; }
   if (c->ds.px * c->ds.py != c->ds.nranks) return bad("px * py must equal nranks");
@@ -1784,7 +1784,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   c->basis = pb->nodes == HBPDC_GL ? hbpdc::gl_basis(pb->N) : hbpdc::gll_basis(pb->N);
   // geometry: Cartesian, J = dx dy / 4, s-hat = dy/2, dx/2 -> scale 2/dx, 2/dy
   const double dx = (pb->xmax - pb->xmin) / pb->nx;
-  const double dy = pb->dim == 2 ? (pb->ymax - pb->ymin) / pb->ny : 1.0;
+  const double dy = pb->dim >= 2 ? (pb->ymax - pb->ymin) / pb->ny : 1.0;
   c->geo.nx = c->nxl;
   c->geo.ny = c->nyl;
   c->geo.nz = c->nzl;

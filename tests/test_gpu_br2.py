@@ -82,10 +82,14 @@ def test_br2_precond(nodes):
 
 @pytest.mark.parametrize("nodes", ["gll", "gl"])
 def test_br2_end_of_run(nodes):
-    """HBPC(4,0), BJ_ext, 2 steps on 4x4 elements, N = 3: end of run vs the oracle <= 1e-8."""
+    """HBPC(4,0), BJ_ext, 2 steps on 4x4 elements, N = 3: end of run vs the oracle <= 1e-8.
+    dt = 0.004: at dt = 0.01 the eta = 2 stage Newton sits at the edge of its basin on this
+    coarse mesh (DESIGN.md 9: BR2 diverges there on 6x6, N = 2, in the oracle and on the GPU);
+    whether it converges then hinges on rounding-level differences of the preconditioner
+    (Gauss-Jordan panel width 16 vs 32, r02f/r02g: identical S to 1e-15, opposite outcomes)."""
     d, ctx = _pair(3, 4, 4, 2.0, nodes=nodes, q=4, kmax=0, gmres_rtol=1e-10, newton_rtol=1e-10)
     W0 = ns_ic(d, SEED + 100, rel_noise=1e-3)
-    dt = 0.01
+    dt = 0.004
     H = hbpc.HBPC(d, 4, 0, implicit.NewtonOpts(rtol=1e-10, gmres_rtol=1e-10))
     Wo = W0.copy()
     st = dict(stage_solves=0, newton_its=0, gmres_its=0, precond_builds=0)
