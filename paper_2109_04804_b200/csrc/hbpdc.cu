@@ -142,6 +142,11 @@ struct hbpdc_ctx {
   hbpdc_step_stats* st = nullptr;  // stats of the step in progress
   // element partition
   hbpdc::Comm* comm = nullptr;     // nullptr: single rank, no halo
+  // halo / compute overlap (partitioned 2D, advection / Euler): the exchange runs on cstream while
+  // the interior elements are computed on the main stream; the boundary ring follows (HBPDC_OVERLAP=0: off)
+  bool overlap = false;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   int nbr[4] = {0, 0, 0, 0};       // neighbour ranks -x, +x, -y, +y
   HaloLayout hl{};
   double *gW = nullptr, *gS = nullptr, *gdW = nullptr, *gdS = nullptr, *gWb = nullptr;  // ghosts
@@ -289,9 +294,32 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
     if (xmask & 2) { src[nf] = A.S; dst[nf++] = c->gS; }
     if (xmask & 4) { src[nf] = A.dW; dst[nf++] = c->gdW; }
     if (xmask & 8) { src[nf] = A.dS; dst[nf++] = c->gdS; }
-    if (nf) CKS(halo_exchange(c, nf, src, dst));
     A.gW = k == OP_KAPPLY ? c->gWb : c->gW;
     A.gS = c->gS; A.gdW = c->gdW; A.gdS = c->gdS;
+    if (nf && c->overlap && c->geo.cmode == 0 && c->pb.equation != HBPDC_NAVIER_STOKES) {
+      // halo / compute overlap: pack + transport + unpack on the comm stream while
+      // the interior elements (no neighbour across a halo side) run on the main stream
+      size_t off[4], len[4];
+      halo_segments(c->hl, nf, off, len, 0);
+      CK(cudaEventRecord(c->ev_ready, c->stream));
+      CK(cudaStreamWaitEvent(c->cstream, c->ev_ready, 0));
+      CK(launch_halo_pack(c->hl, nf, src, c->hsend, c->cstream, 0, false));
+      Geo gi = k == OP_R1ABS ? c->geo_abs : c->geo;
+      gi.cmode = 3;
+      CK(launch_op(k, c->cfg, gi, A));
+      std::string e;
+      if (c->comm->halo(c->hsend, c->hrecv, off, len, c->nbr, c->hl.active, c->cstream, e))
+        return fail(c, HBPDC_E_NCCL, e);
+      CK(launch_halo_unpack(c->hl, nf, c->hrecv, dst, c->cstream, 0, false));
+      CK(cudaEventRecord(c->ev_halo, c->cstream));
+      CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+      Geo gb = k == OP_R1ABS ? c->geo_abs : c->geo;
+      gb.cmode = 4;
+      CK(launch_op(k, c->cfg, gb, A));
+      CKS(dbg_sync(c, "overlapped operator"));
+      return HBPDC_OK;
+    }
+    if (nf) CKS(halo_exchange(c, nf, src, dst));
   }
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {
     // BR1: lift the jet state(s), then (partitioned) exchange the lifted
@@ -598,7 +626,7 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
         // clear this colour's elements of tseed for the next colour
         CK(launch_colour_seed(c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, -1, c->stream));
       }
-    if (single) CK(launch_kk_gemm(c->Kst, c->S, c->m, c->nE, a1dt, c2, c->stream));
+    if (single) CK(launch_kk_gemm(c->Kst, c->S, c->m, c->nE, a1dt, c2, hess ? 1 : 0, c->stream));
   }
   std::vector<int> hinfo(c->zchunk);
   for (int e0 = 0; e0 < nblk; e0 += c->zchunk) {
@@ -1864,6 +1892,16 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
       return HBPDC_E_NCCL;
     }
   }
+  if (halo && pb->dim == 2 && c->nxl >= 3 && c->nyl >= 3) {
+    const char* ov = std::getenv("HBPDC_OVERLAP");
+    c->overlap = !(ov && ov[0] == '0');
+    if (c->overlap) {
+      e = cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming);
+      if (e != cudaSuccess) { c->err = cudaGetErrorString(e); *out = c; return HBPDC_E_CUDA; }
+    }
+  }
   { const char* dbg = std::getenv("HBPDC_DEBUG_SYNC"); c->debug_sync = dbg && dbg[0] == '1'; }
   { const char* tr = std::getenv("HBPDC_TRACE"); c->trace = tr && tr[0] == '1'; }   // solver trace on stderr
   { const char* fc = std::getenv("HBPDC_FUSE_CGS"); c->fuse_cgs = !(fc && fc[0] == '0'); }
@@ -2114,6 +2152,9 @@ void hbpdc_finalize(hbpdc_ctx* c) {
   }
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->hadm) cudaFreeHost(c->hadm);
+  if (c->cstream) cudaStreamSynchronize(c->cstream), cudaStreamDestroy(c->cstream);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   delete c->comm;
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;

@@ -40,21 +40,46 @@ struct Geo {
   double D[64];            // GL BR2: strong-form D_ij = l_j'(x_i)
   double dlp[8], dlm[8];   // GL BR2: l_j'(+1), l_j'(-1)
   double cp, cm;           // GL BR2: sum_i l_i(+-1) lhat_i(+-1)
-  // colour restriction (NS BJ_ext build): cmode 0 = every element; 1 = the elements of
-  // colour (ccx, ccy) of the period (cpx, cpy) colouring; 2 = those and their 4 neighbours
+  // restricted launches: cmode 0 = every element; 1 = the elements of colour (ccx, ccy) of the
+  // period (cpx, cpy) colouring and 2 = those and their 4 neighbours (NS BJ_ext build); 3 = the
+  // interior elements of a partitioned 2D block (no neighbour across a halo side) and 4 = the
+  // boundary ring (halo / compute overlap: the interior runs while the halo is in flight)
   int cmode, cpx, cpy, ccx, ccy;
 };
 
 // elements a restricted launch covers (grid = ceil(count / EPB))
 __host__ __device__ inline int launch_elems(const Geo& g) {
   if (g.cmode == 0) return g.nE;
+  if (g.cmode >= 3) {
+    const int ni = (g.nx - 2 * g.hx) * (g.ny - 2 * g.hy);
+    return g.cmode == 3 ? ni : g.nE - ni;
+  }
   const int nc = (g.nx / g.cpx) * (g.ny / g.cpy);
   return g.cmode == 1 ? nc : 5 * nc;
 }
 
-// k-th element of a (possibly colour-restricted) launch; false past the end
+// k-th element of a (possibly restricted) launch; false past the end
 __device__ __forceinline__ bool launch_elem(const Geo& g, int k, int& e) {
   if (g.cmode == 0) { e = k; return k < g.nE; }
+  if (g.cmode >= 3) {
+    const int wi = g.nx - 2 * g.hx, hi = g.ny - 2 * g.hy, ni = wi * hi;
+    if (g.cmode == 3) {
+      if (k >= ni) { e = 0; return false; }
+      e = (g.hy + k / wi) * g.nx + g.hx + k % wi;
+      return true;
+    }
+    if (k >= g.nE - ni) { e = 0; return false; }
+    const int nrow = g.hy * g.nx;                 // first and last row (y halo sides)
+    if (k < 2 * nrow) {
+      const int r = k / g.nx;                    // 0 .. 2 hy - 1
+      e = (r < g.hy ? r : g.ny - 2 * g.hy + r) * g.nx + k % g.nx;
+      return true;
+    }
+    k -= 2 * nrow;                               // left / right columns of the middle rows
+    const int c = k % (2 * g.hx), row = g.hy + k / (2 * g.hx);
+    e = row * g.nx + (c < g.hx ? c : g.nx - 2 * g.hx + c);
+    return true;
+  }
   const int nxc = g.nx / g.cpx, nc = nxc * (g.ny / g.cpy);
   if (k >= (g.cmode == 1 ? nc : 5 * nc)) { e = 0; return false; }
   const int s = k / nc, kk = k % nc;
@@ -633,12 +658,10 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL, BR2
   extern __shared__ __align__(16) double sF[];     // EPB * slot_doubles (dynamic: may exceed 48 KB)
   constexpr int SLOT = slot_doubles<EQ, DIM, P, Mode>();
   const int slot = threadIdx.x / NODES, node = threadIdx.x % NODES;
-  // colour-restricted launches exist only for the Navier-Stokes BJ_ext build; the other
-  // instantiations keep the plain element index (the runtime mapping cost R1 ~30%, r02c)
-  int e = blockIdx.x * EPB + slot;
-  bool active;
-  if constexpr (EQ == 2) active = launch_elem(g, blockIdx.x * EPB + slot, e);
-  else active = e < g.nE;
+  // restricted launches (cmode != 0): the NS BJ_ext colour passes, the interior / boundary
+  // halves of a partitioned operator; cmode 0 is the plain element index
+  int e;
+  const bool active = launch_elem(g, blockIdx.x * EPB + slot, e);
   double out[Mode::NCH][NV];
   typename Mode::Args Al = A;
   if constexpr (HasDevEps<typename Mode::Args>::value) {

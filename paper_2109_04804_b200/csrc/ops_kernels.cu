@@ -440,18 +440,19 @@ __global__ void colour_gather_kernel(const double* __restrict__ y1, const double
 
 int colour_grid(size_t work) { return (int)std::min<size_t>(1184, (work + 255) / 256); }
 
-// K[e][r][col] = y1 for the colour's elements; M[e][r][col] = c2 (H e_col)_r (BJ^H_ext, y3 = e_col +
-// H e_col) or 0 -- the identity, K and K^2 terms are added afterwards by kk_gemm_kernel
+// Column col of K_i for the colour's elements, stored TRANSPOSED (row col of K_i^T: consecutive
+// threads write consecutive doubles; kk_gemm_kernel transposes it back in shared memory), and for
+// BJ^H_ext (y3 = e_col + H e_col) the column c2 H_i e_col of M_i in place (the identity, K and K^2
+// terms are added by kk_gemm_kernel).
 __global__ void colour_gather_k_kernel(const double* __restrict__ y1, const double* __restrict__ y3,
-                                       double* __restrict__ K, double* __restrict__ M, int nc, int nx, int m,
+                                       double* __restrict__ Kt, double* __restrict__ M, int nc, int nx, int m,
                                        int Px, int Py, int cx, int cy, int col, double c2) {
   const size_t n = (size_t)nc * m;
   for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
     const int e = colour_elem((int)(k / m), nx, Px, Py, cx, cy), r = (int)(k % m);
     const size_t i = (size_t)e * m + r;
-    const size_t o = i * m + col;
-    K[o] = y1[i];
-    M[o] = y3 ? c2 * (y3[i] - (r == col ? 1.0 : 0.0)) : 0.0;
+    Kt[((size_t)e * m + col) * m + r] = y1[i];
+    if (y3) M[i * m + col] = c2 * (y3[i] - (r == col ? 1.0 : 0.0));
   }
 }
 
@@ -461,21 +462,26 @@ __device__ __forceinline__ void kk_dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// M_i += I - a1dt K_i + c2 K_i K_i for every element, K_i^2 on the fp64 tensor cores:
-// one CTA per element, K_i in shared memory (rows padded to ld = mp + 4, mp = m rounded up to 8,
-// zero padding), warp w takes the 8 x 8 output tiles w, w + 8, ..., k in steps of 4 (mma.sync m8n8k4).
+// In place per element: K holds K_i^T from the gather (and M the c2 H_i columns for BJ^H_ext);
+// afterwards K holds K_i (row-major, the layout of the apply's GEMV) and M = [c2 H_i +] I - a1dt K_i + c2 K_i K_i
+// (P:313-314), K_i^2 on the fp64 tensor cores.  One CTA per element, K_i in shared memory (rows
+// padded to ld = mp + 4, mp = m rounded up to 8, zero padding), warp w takes the 8 x 8 output tiles
+// w, w + 8, ..., k in steps of 4 (mma.sync m8n8k4).
 constexpr int KK_T = 256;
-__global__ void __launch_bounds__(KK_T, 1) kk_gemm_kernel(const double* __restrict__ K, double* __restrict__ M,
-                                                          int m, double a1dt, double c2) {
+__global__ void __launch_bounds__(KK_T, 1) kk_gemm_kernel(double* __restrict__ K, double* __restrict__ M,
+                                                          int m, double a1dt, double c2, int hess) {
   extern __shared__ __align__(16) double sk[];
   const int mp = (m + 7) & ~7, ld = mp + 4;
-  const double* Ke = K + (size_t)blockIdx.x * m * m;
+  double* Ke = K + (size_t)blockIdx.x * m * m;
   double* Me = M + (size_t)blockIdx.x * m * m;
-  for (int t = threadIdx.x; t < mp * ld; t += KK_T) {
-    const int r = t / ld, c = t % ld;
-    sk[t] = (r < m && c < m) ? Ke[(size_t)r * m + c] : 0.0;
+  for (int t = threadIdx.x; t < mp * ld; t += KK_T) sk[t] = 0.0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < m * m; t += KK_T) {      // coalesced read of K^T, transposed store
+    const int c = t / m, r = t % m;
+    sk[r * ld + c] = Ke[t];
   }
   __syncthreads();
+  for (int t = threadIdx.x; t < m * m; t += KK_T) Ke[t] = sk[(t / m) * ld + t % m];   // K_i row-major
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int nt = mp / 8;
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(KK_T, 1) kk_gemm_kernel(const double* __restri
       const int c = c0 + 2 * q + h;
       if (r < m && c < m) {
         const size_t o = (size_t)r * m + c;
-        Me[o] += (r == c ? 1.0 : 0.0) - a1dt * sk[r * ld + c] + c2 * acc[h];
+        Me[o] = (hess ? Me[o] : 0.0) + (r == c ? 1.0 : 0.0) - a1dt * sk[r * ld + c] + c2 * acc[h];
       }
     }
   }
@@ -506,15 +512,15 @@ cudaError_t launch_colour_gather_k(const double* y1, const double* y3, double* K
   return cudaGetLastError();
 }
 
-bool kk_gemm_supported(int m) { return m <= 160; }
+bool kk_gemm_supported(int m) { return m <= 160; }   // K_i in shared memory (<= 227 KB)
 
-cudaError_t launch_kk_gemm(const double* K, double* M, int m, int nE, double a1dt, double c2, cudaStream_t st) {
+cudaError_t launch_kk_gemm(double* K, double* M, int m, int nE, double a1dt, double c2, int hess, cudaStream_t st) {
   if (!kk_gemm_supported(m)) return cudaErrorInvalidValue;
   if (nE <= 0) return cudaSuccess;
   const int mp = (m + 7) & ~7;
   const size_t smem = (size_t)mp * (mp + 4) * sizeof(double);
   cudaFuncSetAttribute(kk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kk_gemm_kernel<<<nE, KK_T, smem, st>>>(K, M, m, a1dt, c2);
+  kk_gemm_kernel<<<nE, KK_T, smem, st>>>(K, M, m, a1dt, c2, hess);
   hbpdc_count_launch();
   return cudaGetLastError();
 }

@@ -80,6 +80,11 @@ CASES = [
     ("euler", 4, 6, 4, 3, 2),
     ("advection", 3, 4, 4, 2, 2),
     ("advection", 3, 8, None, 2, 1),
+    # local blocks >= 3 x 3: the halo / compute overlap path (interior elements while the
+    # halo is in flight, then the boundary ring) -- still bitwise equal to one rank
+    ("euler", 2, 8, 6, 2, 2),
+    ("advection", 3, 9, 8, 3, 2),
+    ("euler", 7, 6, 3, 2, 1),
     # Navier-Stokes (BR1): second halo of the lifted gradients; local grids
     # keep a colouring period >= 3 for the two-hop BJ_ext blocks
     ("navier_stokes", 2, 6, 6, 2, 2),
