@@ -694,7 +694,7 @@ hbpdc_status precond_apply_multi(hbpdc_ctx* c, int B, const double* const* iw, c
   }
   if (c->op.precond != HBPDC_PC_BJEXT_H) {
     ProfScope ps(c, 0, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 + 4.0 * B * c->n * 8.0);
-    if (B == 1 || c->s_shared) {
+    if (B == 1 || c->s_shared || (c->m & 1)) {      // odd m (3D, N = 2: m = 135): 2-RHS kernel per system
       for (int i = 0; i < B; ++i)
         CK(launch_block_gemv2(c->S, c->s_shared, iw[i], is[i], c->sys[i].U, c->sys[i].V, c->m, c->nE, c->stream));
     } else {
@@ -1753,10 +1753,10 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   if (pb->dim < 1 || pb->dim > 3) return bad("dim must be 1, 2 or 3");
   if (pb->equation < 0 || pb->equation > 2) return bad("unknown equation");
   if (pb->equation != HBPDC_ADVECTION && pb->dim == 1) return bad("Euler/NS need dim >= 2");
-  if (pb->dim == 3) {       // NEXT-4 scope: inviscid hexahedra, GLL, one rank, N <= 3 (m <= 320)
+  if (pb->dim == 3) {       // NEXT-4 scope: inviscid hexahedra, GLL, one rank, N = 2, 3 (m = 135, 320)
     if (pb->equation == HBPDC_NAVIER_STOKES) return bad("3D: advection or Euler (Navier-Stokes is 2D)");
     if (pb->nodes != HBPDC_GLL) return bad("3D: Gauss-Lobatto nodes only");
-    if (pb->N > 3) return bad("3D: N must be in 1..3");
+    if (pb->N < 2 || pb->N > 3) return bad("3D: N must be 2 or 3 (m = 5 (N+1)^3 <= 320)");
     if (pb->nz < 1 || pb->ny < 1 || !(pb->zmax > pb->zmin)) return bad("3D: bad z extent / element counts");
     if (ds && (ds->nranks > 1 || ds->force_halo)) return bad("3D runs on one rank");
   }

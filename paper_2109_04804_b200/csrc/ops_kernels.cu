@@ -298,9 +298,10 @@ static cudaError_t dispatch(const OpCfg& c, F&& f) {
 #define CASE(EQ, DIM, PP) \
   if (c.eq == EQ && c.dim == DIM && c.P == PP) return f(Disp<EQ, DIM, PP>{});
 #if HBPDC_OPS_3D
-  // 3D hexahedra, GLL: advection (EQ 0) and Euler (EQ 3: five variables), N = 1..3
-  CASE(0, 3, 2) CASE(0, 3, 3) CASE(0, 3, 4)
-  CASE(3, 3, 2) CASE(3, 3, 3) CASE(3, 3, 4)
+  // 3D hexahedra, GLL: advection (EQ 0) and Euler (EQ 3: five variables), N = 2, 3
+  // (N = 1 would put 16 elements in a CTA: the jet modes' shared memory exceeds 227 KB)
+  CASE(0, 3, 3) CASE(0, 3, 4)
+  CASE(3, 3, 3) CASE(3, 3, 4)
 #else
 #if !HBPDC_OPS_BR2
   HBPDC_P_LIST(CASE, 0, 1)

@@ -31,7 +31,7 @@ def state(d, kind, seed, amp=1e-2):
     return inputs.perturbed_state(W, seed, amp) if kind == "euler" else W + inputs.random_field(d.n, seed, amp)
 
 
-CASES = [("euler", 1, (3, 2, 2)), ("euler", 2, (2, 3, 3)), ("euler", 3, (3, 2, 3)),
+CASES = [("euler", 2, (3, 2, 2)), ("euler", 2, (2, 3, 3)), ("euler", 3, (3, 2, 3)),
          ("advection", 2, (3, 3, 2)), ("advection", 3, (2, 2, 3))]
 
 
@@ -75,7 +75,7 @@ def test_operators_3d(case):
         assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= max(1e-11, 4 * delta)
 
 
-@pytest.mark.parametrize("case", [("euler", 1, (2, 3, 2)), ("euler", 2, (2, 2, 3)), ("euler", 3, (2, 2, 2)),
+@pytest.mark.parametrize("case", [("euler", 2, (2, 3, 2)), ("euler", 2, (2, 2, 3)), ("euler", 3, (2, 2, 2)),
                                   ("advection", 3, (2, 2, 2))])
 def test_bjext_3d(case):
     """BJ_ext in 3D: S_i = (I - a1 dt K_i + c2 K_i^2)^-1 (m up to 5 * 4^3 = 320: the 384-thread
@@ -97,7 +97,7 @@ def test_bjext_3d(case):
     assert rel(np.concatenate([to_np(tg), to_np(bg)]), np.concatenate([to, bo])) <= 1e-11 * max(1, cond / 1e4)
 
 
-@pytest.mark.parametrize("kind,N,n,q,kmax,sstep", [("euler", 2, (3, 3, 3), 4, 0, 1), ("euler", 3, (2, 2, 2), 4, 0, 8),
+@pytest.mark.parametrize("kind,N,n,q,kmax,sstep", [("euler", 2, (3, 3, 3), 4, 0, 1), ("euler", 3, (3, 3, 3), 4, 0, 8),
                                                   ("euler", 2, (2, 2, 3), 6, 2, 4), ("advection", 3, (2, 2, 2), 6, 2, 1)])
 def test_end_of_run_3d(kind, N, n, q, kmax, sstep):
     """The paper's 3D case in its inviscid scope: Taylor-Green initial data (P:1088-1091,
@@ -107,7 +107,7 @@ def test_end_of_run_3d(kind, N, n, q, kmax, sstep):
     X, Y, Z = d.node_coords()
     W0 = inputs.initial_state("TGV3" if kind == "euler" else "ADV3", (X, Y, Z))
     h = TWO_PI / max(n)
-    dt = 1.0 / (3 * (1.0 + 1.1) / h) if kind == "euler" else 1.0 / (2.0 / h)
+    dt = 0.5 / (3 * (1.0 + 1.1) / h) if kind == "euler" else 1.0 / (2.0 / h)      # acoustic element CFL 0.5
     H = hbpc.HBPC(d, q, kmax, implicit.NewtonOpts(rtol=1e-10, gmres_rtol=1e-10))
     Wo = W0.copy()
     for _ in range(2):
