@@ -226,6 +226,27 @@ def global_dt(cfg, Wc_local, use_dist):
     return dt
 
 
+def memory_plan(cfg, world, weak, batch, restart, sstep):
+    """Device bytes per rank of the library's resident arrays (DESIGN.md 5 / 8): BJ_ext blocks S
+    (plus the stored K_i for Navier-Stokes), the Krylov bases (restart + 1 vectors of 2n per
+    concurrently solved stage system; a restart above 64 is counted as 64: the basis grows on
+    demand and the configs' solves stay below), the Newton workspaces, the stage store (3 arrays
+    per stage, two sweeps) and the Gauss-Jordan chunk (<= 1 GiB)."""
+    n_el = cfg.n_elem if weak else cfg.n_elem // world
+    m = cfg.m
+    n = n_el * m
+    stages = {4: 2, 6: 3, 8: 4}[cfg.q]
+    systems = (stages - 1) if batch and cfg.kmax > 0 else 1
+    s_bytes = n_el * m * m * 8 * (2 if cfg.equation == "navier_stokes" else 1)
+    krylov = systems * (restart + 1) * 2 * n * 8        # grown on demand up to restart + 1 vectors
+    work = systems * (6 * 2 * n + n + 2 * n) * 8
+    store = 2 * stages * 3 * n * 8
+    total = s_bytes + krylov + work + store + min(1 << 30, m * m * 8 * n_el)
+    return {"S_GB": round(s_bytes / 1e9, 1), "krylov_GB": round(krylov / 1e9, 1),
+            "workspace_GB": round(work / 1e9, 1), "stage_store_GB": round(store / 1e9, 1),
+            "total_GB": round(total / 1e9, 1), "lockstep_systems": systems}
+
+
 def relaunch_under_torchrun(args):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -280,6 +301,11 @@ def run_ours(args):
     batch = args.batch_stages
     if batch is None:
         batch = not (case == "C4" and world < 4)
+    plan = memory_plan(cfg, world, weak, batch, cfg.restart if cfg.restart <= 64 else 64, args.gmres_sstep)
+    free_b, total_b = torch.cuda.mem_get_info(local)
+    plan["device_free_GB"] = round(free_b / 1e9, 1)
+    if plan["total_GB"] * 1e9 > free_b:
+        raise SystemExit(f"bench: memory plan {plan} exceeds the free device memory")
     ctx = hbpdc.context_for(cfg, device=local, gmres_sstep=args.gmres_sstep, batch_stages=batch, **kw)
     W0, Wc = local_initial_state(case, cfg, ctx, weak, rank)
     dt = global_dt(cfg, Wc, use_dist)
@@ -442,6 +468,7 @@ def run_ours(args):
                        "arnoldi": ("DCGS2" if args.gmres_sstep <= 1 else f"s-step s={args.gmres_sstep} (block CGS2)"),
                        "precond": args.precond or cfg.precond, "nodes": args.nodes, "flux": args.flux,
                        "lockstep_correctors": bool(batch),
+                       "memory_plan": plan,
                        "dt": dt, "n_dof_per_gpu": n, "n_dof": n_global,
                        "parallelism": (f"{scaling} scaling: element partition {px}x{py} of a "
                                        f"{cfg.nx * (px if weak else 1)}x{cfg.ny * (py if weak else 1)} mesh, "
