@@ -484,13 +484,17 @@ __global__ void __launch_bounds__(32 * (GwCons<NR>::value + 1)) gemvN_tma_kernel
 // 3 right-hand sides and is issue-bound at 6 (5.6 TB/s); here one 16-byte
 // load feeds two DMMAs of all 8 columns.
 constexpr int GD_CONS = 16;                       // consumer warps
-constexpr int GD_ROWS = 16;                       // rows per chunk
 constexpr int GD_KWMAX = 8;                       // k-steps per warp (m <= 256)
 
-template <int NR>
+// RB row blocks of 8 rows per chunk x (GD_CONS / RB) k-ranges: RB = 2 (m = 256: every k-range full)
+// or RB = 4 (m = 144: 4 k-ranges of 40 columns keep 90 % of the consumer warps busy instead of 75 %
+// with 8 k-ranges of 24 -- the chunk's makespan is the busiest warp's).
+template <int NR, int RB = 2, int KWMAX = GD_KWMAX>
 __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const double* __restrict__ S,
                                                                          const GemvRHS io, int m, int nE,
                                                                          int GW_NST, int kw) {
+  constexpr int GD_ROWS = 8 * RB;                                      // rows per chunk
+  constexpr int KR = GD_CONS / RB;                                     // k-ranges
   extern __shared__ __align__(128) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);                     // GW_NST x GD_ROWS x m
   double* rhs = ring + (size_t)GW_NST * GD_ROWS * m;                   // 2 x NR x m
@@ -533,16 +537,16 @@ __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const 
     return;
   }
   const int g = lane >> 2, t = lane & 3;
-  const int rbk = wid & 1, kr = wid >> 1;
+  const int rbk = wid % RB, kr = wid / RB;
   const int cbase = 4 * kr * kw + 2 * t;          // + 8 p + (ks & 1)
   int c = 0;
   for (int it = 0; it < nmy; ++it) {
     const int e = blockIdx.x + it * gridDim.x;
     const int rb = it & 1;
     mbar_wait(&fullR[rb], (unsigned)((it >> 1) & 1));
-    double b[GD_KWMAX];
+    double b[KWMAX];
 #pragma unroll
-    for (int ks = 0; ks < GD_KWMAX; ++ks) {
+    for (int ks = 0; ks < KWMAX; ++ks) {
       const int col = cbase + 8 * (ks >> 1) + (ks & 1);
       b[ks] = (ks < kw && g < NR && col < m) ? rhs[((size_t)rb * NR + g) * m + col] : 0.0;
     }
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const 
       const double* ar = ring + ((size_t)st * GD_ROWS + 8 * rbk + g) * m;
       double ae[2] = {0.0, 0.0}, ao[2] = {0.0, 0.0};
 #pragma unroll
-      for (int p = 0; p < GD_KWMAX / 2; ++p) {
+      for (int p = 0; p < KWMAX / 2; ++p) {
         if (2 * p < kw) {
           const int col = cbase + 8 * p;
           double2 a2 = make_double2(0.0, 0.0);
@@ -575,11 +579,11 @@ __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const 
       if (threadIdx.x < GD_ROWS * NR) {
         const int r = threadIdx.x / NR, j = threadIdx.x % NR;
         const double* rr = red + (size_t)buf * GD_CONS * 64 + (r >> 3) * 64 + (r & 7) * 8 + j;
-        double s0 = 0.0, s1 = 0.0;                  // two chains, fixed order
+        double s0 = 0.0, s1 = 0.0;                  // two chains, fixed order (warp kr RB + rb)
 #pragma unroll
-        for (int q = 0; q < GD_CONS / 2; q += 2) {
-          s0 += rr[(size_t)2 * q * 64];
-          s1 += rr[(size_t)2 * (q + 1) * 64];
+        for (int q = 0; q < KR; q += 2) {
+          s0 += rr[(size_t)RB * q * 64];
+          s1 += rr[(size_t)RB * (q + 1) * 64];
         }
         const int row = ch * GD_ROWS + r;
         if (row < m) sOut[j][(size_t)e * m + row] = s0 + s1;
@@ -588,8 +592,10 @@ __global__ void __launch_bounds__(32 * (GD_CONS + 1), 1) gemv_dmma_kernel(const 
   }
 }
 
-template <int NR>
-static cudaError_t launch_gemv_dmma(const double* S, const GemvRHS& io, int m, int nE, cudaStream_t st) {
+template <int NR, int RB = 2, int KWMAX = GD_KWMAX>
+static cudaError_t launch_gemv_dmma_rb(const double* S, const GemvRHS& io, int m, int nE, cudaStream_t st) {
+  constexpr int GD_ROWS = 8 * RB;
+  constexpr int KR = GD_CONS / RB;
   static int nsm = 0;
   if (!nsm) {
     int dev = 0, v = 0;
@@ -597,8 +603,8 @@ static cudaError_t launch_gemv_dmma(const double* S, const GemvRHS& io, int m, i
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     nsm = v;
   }
-  if (m > 4 * GD_KWMAX * (GD_CONS / 2) || (m & 1)) return cudaErrorInvalidValue;
-  int kw = ((m + 3) / 4 + GD_CONS / 2 - 1) / (GD_CONS / 2);
+  if (m > 4 * KWMAX * KR || (m & 1)) return cudaErrorInvalidValue;
+  int kw = ((m + 3) / 4 + KR - 1) / KR;
   kw += kw & 1;                                   // k-steps in pairs (16-byte loads)
   const size_t chunk = (size_t)GD_ROWS * m * sizeof(double);
   const size_t fixed = (size_t)2 * NR * m * sizeof(double) + (size_t)2 * GD_CONS * 64 * sizeof(double) +
@@ -606,13 +612,28 @@ static cudaError_t launch_gemv_dmma(const double* S, const GemvRHS& io, int m, i
   const int nst = (int)std::max<size_t>(2, std::min<size_t>(GW_NST_MAX, GW_RING_BYTES / chunk));
   const size_t smem = (size_t)nst * chunk + fixed;
   constexpr int threads = 32 * (GD_CONS + 1);
-  cudaFuncSetAttribute(gemv_dmma_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(gemv_dmma_kernel<NR, RB, KWMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_dmma_kernel<NR>, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_dmma_kernel<NR, RB, KWMAX>, threads, smem);
   const int grid = std::min(nE, nsm * std::max(occ, 1));
-  gemv_dmma_kernel<NR><<<grid, threads, smem, st>>>(S, io, m, nE, nst, kw);
+  gemv_dmma_kernel<NR, RB, KWMAX><<<grid, threads, smem, st>>>(S, io, m, nE, nst, kw);
   hbpdc_count_launch();
   return cudaGetLastError();
+}
+
+// row-block layout with the better consumer utilisation for this m (ties: RB = 2)
+inline double gemv_util(int m, int RB) {
+  const int KR = GD_CONS / RB;
+  int kw = ((m + 3) / 4 + KR - 1) / KR;
+  kw += kw & 1;
+  return (double)m / (4.0 * KR * kw);
+}
+
+template <int NR>
+static cudaError_t launch_gemv_dmma(const double* S, const GemvRHS& io, int m, int nE, cudaStream_t st) {
+  static const bool off = getenv("HBPDC_GEMV_RB2") != nullptr;
+  if (!off && gemv_util(m, 4) > gemv_util(m, 2) + 1e-12) return launch_gemv_dmma_rb<NR, 4, 16>(S, io, m, nE, st);
+  return launch_gemv_dmma_rb<NR, 2, GD_KWMAX>(S, io, m, nE, st);
 }
 
 template <int NR>
