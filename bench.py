@@ -53,13 +53,24 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+IC_CASE = {"T3": "TGV3"}          # input recipe of a bench config (inputs.ic_primitive)
+
+
+def get_config(name):
+    from paper_2109_04804_b200 import configs
+    return configs.CONFIGS[name] if name in configs.CONFIGS else configs.EXTRA[name]
+
+
 def workload_name(cfg, args):
-    eqn = {"euler": "2D Euler", "navier_stokes": "2D Navier-Stokes (BR1, Re 1000, Pr 0.72)",
+    eqn = {"euler": "3D Euler" if cfg.dim == 3 else "2D Euler",
+           "navier_stokes": "2D Navier-Stokes (BR1, Re 1000, Pr 0.72)",
            "advection": "2D advection"}[cfg.equation]
     ic = {"C3": "isentropic vortex (beta=5, mean (1,1)) + seeded U[-1e-6,1e-6) noise",
           "C4": "density wave rho=1+0.2 sin(2 pi (x+y)), u=v=p=1",
-          "C5": "TGV-type vortex, Mach 0.1"}[cfg.name]
-    return (f"{cfg.name}: {eqn} {ic}, {cfg.nx}x{cfg.ny} elements, N={cfg.N} {args.nodes.upper()}, "
+          "C5": "TGV-type vortex, Mach 0.1",
+          "T3": "Taylor-Green data (P:1088-1091, reading R35, inviscid), acoustic element CFL 1"}[cfg.name]
+    mesh = f"{cfg.nx}x{cfg.ny}x{cfg.nz}" if cfg.dim == 3 else f"{cfg.nx}x{cfg.ny}"
+    return (f"{cfg.name}: {eqn} {ic}, {mesh} elements, N={cfg.N} {args.nodes.upper()}, "
             f"{args.flux.upper()}, HBPC({cfg.q},{cfg.kmax}), {(args.precond or cfg.precond).upper()}, "
             f"FD JVP, GMRES rtol {cfg.gmres_rtol:g} / Newton {cfg.newton_rtol:g}, restart {cfg.restart}")
 
@@ -81,17 +92,31 @@ def oracle_sample(cfg_name):
     import numpy as np  # noqa: F401
     from oracle import basis, dgsem, implicit, physics
     from paper_2109_04804_b200 import configs, inputs
-    cfg = configs.CONFIGS[cfg_name]
+    cfg = get_config(cfg_name)
+    ic = IC_CASE.get(cfg_name, cfg_name)
     hx = (cfg.bounds[1] - cfg.bounds[0]) / cfg.nx
     hy = (cfg.bounds[3] - cfg.bounds[2]) / cfg.ny
     cx, cy = 0.5 * (cfg.bounds[0] + cfg.bounds[1]), 0.5 * (cfg.bounds[2] + cfg.bounds[3])
-    nw = 4
-    eq = physics.Equation(cfg.equation, mu=cfg.mu)
-    d = dgsem.Disc(basis.build_basis(cfg.N, "gll"),
-                   dgsem.Mesh(2, nw, nw, cx - nw * hx / 2, cx + nw * hx / 2, cy - nw * hy / 2, cy + nw * hy / 2), eq)
-    W0 = inputs.initial_state(cfg_name, d.node_coords(), noise=cfg.noise)
-    full = dgsem.Disc(d.basis, dgsem.Mesh(2, cfg.nx, cfg.ny, *cfg.bounds), eq)
-    dt = configs.cfl_dt(cfg, inputs.initial_state(cfg_name, full.node_coords()))
+    nw = 4 if cfg.dim == 2 else 2
+    eq = physics.Equation(cfg.equation, mu=cfg.mu, dim=cfg.dim)
+    if cfg.dim == 3:
+        cz = 0.5 * (cfg.bounds[4] + cfg.bounds[5])
+        hz = (cfg.bounds[5] - cfg.bounds[4]) / cfg.nz
+        me = dgsem.Mesh(3, nw, nw, cx - nw * hx / 2, cx + nw * hx / 2, cy - nw * hy / 2, cy + nw * hy / 2,
+                        nz=nw, zmin=cz - nw * hz / 2, zmax=cz + nw * hz / 2)
+    else:
+        me = dgsem.Mesh(2, nw, nw, cx - nw * hx / 2, cx + nw * hx / 2, cy - nw * hy / 2, cy + nw * hy / 2)
+    d = dgsem.Disc(basis.build_basis(cfg.N, "gll"), me, eq)
+    W0 = inputs.initial_state(ic, d.node_coords(), noise=cfg.noise)
+    if cfg.dt > 0:
+        dt = cfg.dt
+    else:
+        if cfg.dim == 3:
+            fm = dgsem.Mesh(3, cfg.nx, cfg.ny, *cfg.bounds[:4], nz=cfg.nz, zmin=cfg.bounds[4], zmax=cfg.bounds[5])
+        else:
+            fm = dgsem.Mesh(2, cfg.nx, cfg.ny, *cfg.bounds)
+        full = dgsem.Disc(d.basis, fm, eq)
+        dt = configs.cfl_dt(cfg, inputs.initial_state(ic, full.node_coords()))
     c = {4: 1.0, 6: 0.5, 8: 1.0 / 3.0}[cfg.q]          # first stage spacing of App. A
     a1, a2 = c / 2, c * c / 6
     t0, c0 = time.perf_counter(), time.process_time()
@@ -103,10 +128,11 @@ def oracle_sample(cfg_name):
     implicit.newton_solve(d, a1, a2, dt, b, W0, opts, pc)
     sec, cpu = time.perf_counter() - t0, time.process_time() - c0
     k = stage_solves_per_step(cfg.q, cfg.kmax)
-    scale = k * (cfg.nx * cfg.ny) / (nw * nw)
+    nwin = nw ** cfg.dim
+    scale = k * cfg.n_elem / nwin
     desc = (f"oracle (numpy, fp64): first predictor stage solve (BJ_ext build + Newton-GMRES) of {cfg_name} step 1 "
-            f"on a {nw}x{nw}-element periodic window of {cfg_name}'s mesh (same h, N={cfg.N}, dt, tolerances), "
-            f"timed end to end; steps/s = 1/(t x {k} stage solves x {cfg.nx * cfg.ny // (nw * nw)} element ratio)")
+            f"on a {'x'.join([str(nw)] * cfg.dim)}-element periodic window of {cfg_name}'s mesh (same h, N={cfg.N}, "
+            f"dt, tolerances), timed end to end; steps/s = 1/(t x {k} stage solves x {cfg.n_elem // nwin} element ratio)")
     return sec, cpu, desc, scale
 
 
@@ -114,8 +140,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2109_04804_b200 import configs
-    cfg = configs.CONFIGS[args.config]
+    cfg = get_config(args.config)
     times, cpus = [], []
     desc, scale = "", 1.0
     for s in range(args.warmup + args.steps):
@@ -276,7 +301,9 @@ def run_ours(args):
     if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     case = args.config
-    cfg = configs.CONFIGS[case]
+    cfg = get_config(case)
+    if cfg.dim == 3 and world > 1:
+        raise SystemExit("bench: the 3D configuration runs on one GPU")
     scaling = args.scaling or ("weak" if case == "C3" else "strong")
     weak = scaling == "weak"
     px, py = PARTS.get(world, (world, 1))
@@ -307,7 +334,7 @@ def run_ours(args):
     if plan["total_GB"] * 1e9 > free_b:
         raise SystemExit(f"bench: memory plan {plan} exceeds the free device memory")
     ctx = hbpdc.context_for(cfg, device=local, gmres_sstep=args.gmres_sstep, batch_stages=batch, **kw)
-    W0, Wc = local_initial_state(case, cfg, ctx, weak, rank)
+    W0, Wc = local_initial_state(IC_CASE.get(case, case), cfg, ctx, weak, rank)
     dt = global_dt(cfg, Wc, use_dist)
     stream = ctx.stream
     dev = f"cuda:{local}"
@@ -501,7 +528,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C4", "C5", "T3"],
+                    help="BASELINE config (C3 default, C4, C5) or T3: the paper's 3D case, inviscid (NEXT-4)")
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="N > 1: weak (a config tile per GPU; C3 default) or strong (one mesh; C4/C5 default)")
     ap.add_argument("--profile-steps", type=int, default=1,

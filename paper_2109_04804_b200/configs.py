@@ -36,10 +36,12 @@ class Config:
     restart: int = 700
     max_krylov: int = 7000
     precond: str = "bjext"
+    nz: int = 1                # 3D (NEXT-4): elements in z; bounds then has 6 entries
+    dt: float = 0.0            # > 0: a fixed time step (the paper's 3D case) instead of the CFL rule
 
     @property
     def nv(self):
-        return 1 if self.equation == "advection" else 4
+        return 1 if self.equation == "advection" else (5 if self.dim == 3 else 4)
 
     @property
     def p(self):
@@ -47,7 +49,7 @@ class Config:
 
     @property
     def n_elem(self):
-        return self.nx * (self.ny if self.dim == 2 else 1)
+        return self.nx * (self.ny if self.dim >= 2 else 1) * (self.nz if self.dim == 3 else 1)
 
     @property
     def m(self):
@@ -70,6 +72,14 @@ CONFIGS = {
                  (0.0, 2 * math.pi, 0.0, 2 * math.pi), 6, 2, 20, 1.0, mu=1e-3),
 }
 
+# NEXT-4 (not a BASELINE config): the paper's 3D Taylor-Green mesh and scheme (32^3
+# elements, N = 3, HBPC(4,0) on [0, 2 pi]^3) in this build's inviscid scope (3D Euler, reading R35).
+# The paper's dt = 0.25 (element CFL ~ 8) belongs to its viscous Re-800 run; the inviscid system takes
+# the configs' acoustic element-CFL-1 step (reading R14).
+EXTRA = {
+    "T3": Config("T3", 3, "euler", 3, 32, 32, (0.0, 2 * math.pi) * 3, 4, 0, 2, 1.0, nz=32),
+}
+
 
 def scaled(cfg: Config, **kw):
     """A smaller copy of a config (parity tests at oracle-friendly sizes)."""
@@ -77,18 +87,22 @@ def scaled(cfg: Config, **kw):
 
 
 def cfl_dt(cfg: Config, W):
-    """Element CFL rule on a layout-L state W (reading #14)."""
+    """Element CFL rule on a layout-L state W (reading #14); a config's fixed dt if it has one."""
+    if cfg.dt > 0.0:
+        return cfg.dt
     h = [(cfg.bounds[1] - cfg.bounds[0]) / cfg.nx]
-    if cfg.dim == 2:
+    if cfg.dim >= 2:
         h.append((cfg.bounds[3] - cfg.bounds[2]) / cfg.ny)
+    if cfg.dim == 3:
+        h.append((cfg.bounds[5] - cfg.bounds[4]) / cfg.nz)
     if cfg.equation == "advection":
         s = sum(abs(cfg.a[d]) / h[d] for d in range(cfg.dim))
         return cfg.cfl / s
     nd = cfg.p ** cfg.dim
     Wv = np.asarray(W).reshape(-1, cfg.nv, nd)      # any block of whole elements
-    rho, mx, my, E = (Wv[:, k] for k in range(4))
-    u, v = mx / rho, my / rho
-    p = (cfg.gamma - 1.0) * (E - 0.5 * rho * (u * u + v * v))
+    rho, E = Wv[:, 0], Wv[:, -1]
+    vel = [Wv[:, 1 + d] / rho for d in range(cfg.nv - 2)]
+    p = (cfg.gamma - 1.0) * (E - 0.5 * rho * sum(v * v for v in vel))
     c = np.sqrt(cfg.gamma * p / rho)
-    s = (np.abs(u) + c) / h[0] + (np.abs(v) + c) / h[1]
+    s = sum((np.abs(vel[d]) + c) / h[d] for d in range(len(vel)))
     return cfg.cfl / float(np.max(s))

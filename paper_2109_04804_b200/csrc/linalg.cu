@@ -632,6 +632,7 @@ inline double gemv_util(int m, int RB) {
 template <int NR>
 static cudaError_t launch_gemv_dmma(const double* S, const GemvRHS& io, int m, int nE, cudaStream_t st) {
   static const bool off = getenv("HBPDC_GEMV_RB2") != nullptr;
+  if (m > 256) return launch_gemv_dmma_rb<NR, 2, 10>(S, io, m, nE, st);     // 3D: m = 320, 8 k-ranges of 40
   if (!off && gemv_util(m, 4) > gemv_util(m, 2) + 1e-12) return launch_gemv_dmma_rb<NR, 4, 16>(S, io, m, nE, st);
   return launch_gemv_dmma_rb<NR, 2, GD_KWMAX>(S, io, m, nE, st);
 }
@@ -680,7 +681,7 @@ cudaError_t launch_block_gemv_multi(const double* S, int nr, const double* const
 #ifndef GEMV_USE_DMMA
 #define GEMV_USE_DMMA 1
 #endif
-  if (GEMV_USE_DMMA && m <= 4 * GD_KWMAX * (GD_CONS / 2)) {
+  if (GEMV_USE_DMMA && m <= 320) {
     switch (nr) {
       case 1: return launch_gemv_dmma<1>(S, io, m, nE, st);     // BJ^H_ext: one RHS per system
       case 2: return launch_gemv_dmma<2>(S, io, m, nE, st);

@@ -366,5 +366,7 @@ def context_for(cfg, **overrides):
               a=cfg.a, gamma=cfg.gamma, mu=cfg.mu, prandtl=cfg.prandtl, q=cfg.q, kmax=cfg.kmax,
               newton_rtol=cfg.newton_rtol, newton_atol_dw=cfg.newton_atol_dw, gmres_rtol=cfg.gmres_rtol,
               restart=cfg.restart, max_krylov=cfg.max_krylov, precond=cfg.precond)
+    if cfg.dim == 3:
+        kw["nz"] = cfg.nz
     kw.update(overrides)
     return Context(**kw)
