@@ -145,6 +145,8 @@ struct hbpdc_ctx {
   // halo / compute overlap (partitioned 2D, advection / Euler): the exchange runs on cstream while
   // the interior elements are computed on the main stream; the boundary ring follows (HBPDC_OVERLAP=0: off)
   bool overlap = false;
+  double* gltr = nullptr;          // GL FD JVP face traces (launch_gl_traces)
+  bool gl_notrace = false;         // HBPDC_GL_TRACES=0: line sums per face node (round 1)
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   int nbr[4] = {0, 0, 0, 0};       // neighbour ranks -x, +x, -y, +y
@@ -284,6 +286,12 @@ int halo_fields(OpKind k) {
 // launch an operator; exchange the halos of the fields in `xmask` first (the
 // ghosts of the other fields are assumed current); NS lifts the jet states first
 hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
+  if (k == OP_JVP_FD && c->geo.gl && c->pb.equation != HBPDC_NAVIER_STOKES && c->pb.dim == 2 && !c->gl_notrace) {
+    // Gauss-Legendre FD JVP: the elements' face traces once, read by the face work (one value per trace)
+    if (!c->gltr) CKS(dalloc(c, &c->gltr, (size_t)c->nE * 4 * 4 * c->nv * c->P));
+    CK(launch_gl_traces(c->cfg, c->geo, A, c->gltr));
+    A.Tr = c->gltr;
+  }
   if (c->halo()) {
     if (xmask < 0) xmask = halo_fields(k);
     xmask &= halo_fields(k);
@@ -1902,6 +1910,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
       if (e != cudaSuccess) { c->err = cudaGetErrorString(e); *out = c; return HBPDC_E_CUDA; }
     }
   }
+  { const char* gt = std::getenv("HBPDC_GL_TRACES"); c->gl_notrace = gt && gt[0] == '0'; }
   { const char* dbg = std::getenv("HBPDC_DEBUG_SYNC"); c->debug_sync = dbg && dbg[0] == '1'; }
   { const char* tr = std::getenv("HBPDC_TRACE"); c->trace = tr && tr[0] == '1'; }   // solver trace on stderr
   { const char* fc = std::getenv("HBPDC_FUSE_CGS"); c->fuse_cgs = !(fc && fc[0] == '0'); }

@@ -24,6 +24,8 @@ cudaError_t launch_op(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A
 int op_grid(const OpCfg& c, const Geo& g);
 // Gauss-Legendre instantiations (ops_kernels_gl.cu), reached from launch_op / launch_kbuild when g.gl
 cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
+// GL FD JVP: face traces of W, sigma, dW, dsigma (ops_kernels_gl.cu) -> OpArgs::Tr
+cudaError_t launch_gl_traces(const OpCfg& c, const Geo& g, const OpArgs& A, double* Tr);
 // Navier-Stokes operators with BR2 face gradients (ops_kernels_br2.cu, ops_kernels_gl_br2.cu), when g.br2
 cudaError_t launch_op_br2(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);
 cudaError_t launch_op_gl_br2(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs& A);

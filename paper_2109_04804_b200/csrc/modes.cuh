@@ -33,6 +33,7 @@ struct OpArgs {
   const double *gW, *gS, *gdW, *gdS;   // ghost copies (neighbour ranks' face traces)
   const double *Gf0, *Gf1;   // NS BR2: per-face gradients of jet states 0 / 1, or NULL (BR1)
   const double *gGf0, *gGf1; // their ghost copies (the neighbour ranks' shared faces)
+  const double* Tr;          // GL FD JVP: face traces [e][face 4][field W,S,dW,dS][var][P] (gl_trace_kernel), or NULL
 };
 
 // NS BR2 face gradients: [elem][face 4][6][JetN][P] (lift_kernel), face f = 2d + plus,
@@ -354,6 +355,46 @@ template <int EQ, int NODES> struct ModeJvpFD {
   __device__ static void face_part(const Args& A, const PhysParams& pp, const G& g, int e, int own, int nb,
                                    int nnode, int, bool plus, int d, int part, double* raw,
                                    int rs) {
+    if constexpr (G::GL && EQ != 2) {
+      if (A.Tr && nb < A.nE) {
+        // Gauss-Legendre: both traces from the precomputed face traces (one read per value instead
+        // of a P-node line sum per face node); p = trace(W) + eps trace(dW), as the halo's ghosts
+        const int P = g.P;
+        const int k = d == 0 ? own / P : own % P;
+        const int fo = 2 * d + (plus ? 1 : 0), fn = fo ^ 1;
+        const double* to = A.Tr + ((size_t)e * 4 + fo) * 4 * NV * P + k;
+        const double* tn = A.Tr + ((size_t)nb * 4 + fn) * 4 * NV * P + k;
+        auto fld = [&](const double* t, int f, int v) { return t[(f * NV + v) * P]; };
+        if (part == 0) {
+          const double ew = fd_step(A);
+          if (!(ew > 0.0)) return;
+          NodeState<EQ, J1> so, sn;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            so.w[v] = J1{__dadd_rn(fld(to, 0, v), __dmul_rn(ew, fld(to, 2, v))), fld(to, 1, v)};
+            sn.w[v] = J1{__dadd_rn(fld(tn, 0, v), __dmul_rn(ew, fld(tn, 2, v))), fld(tn, 1, v)};
+          }
+          J1 fp[NV];
+          if (plus) face_flux<EQ>(pp, so, sn, d, fp);
+          else face_flux<EQ>(pp, sn, so, d, fp);
+          for (int v = 0; v < NV; ++v) { raw[rs * (2 * v)] = fp[v].v; raw[rs * (2 * v + 1)] = fp[v].a; }
+        } else {
+          NodeState<EQ, J2> so, sn;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            so.w[v] = J2{fld(to, 0, v), fld(to, 1, v), fld(to, 3, v)};
+            sn.w[v] = J2{fld(tn, 0, v), fld(tn, 1, v), fld(tn, 3, v)};
+          }
+          J2 fq[NV];
+          if (plus) face_flux<EQ>(pp, so, sn, d, fq);
+          else face_flux<EQ>(pp, sn, so, d, fq);
+          for (int v = 0; v < NV; ++v) {
+            raw[rs * (3 * v)] = fq[v].v; raw[rs * (3 * v + 1)] = fq[v].a; raw[rs * (3 * v + 2)] = fq[v].b;
+          }
+        }
+        return;
+      }
+    }
     if (part == 0) {
       if (!(fd_step(A) > 0.0)) return;
       NodeState<EQ, J1> so, sn;

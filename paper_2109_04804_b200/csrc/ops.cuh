@@ -920,3 +920,31 @@ __global__ void gtrace_kernel(const typename Mode::Args A, const PhysParams pp, 
 #pragma unroll
     for (int q = 0; q < JN; ++q) o[(k * JN + q) * P] = acc[k][q];
 }
+
+// ---- GL face traces of the FD JVP inputs: Tr[e][face][field][v][k] = sum_l l_l(+-1) X(line node l),
+// fields W, sigma, dW, dsigma; one thread per (element, face, face node).  The FD JVP's GL face work then
+// reads one value per trace instead of a line sum per face node and jet state.
+template <int P, int NV>
+__global__ void gl_trace_kernel(const double* __restrict__ W, const double* __restrict__ S,
+                                const double* __restrict__ dW, const double* __restrict__ dS, const Geo g,
+                                double* __restrict__ Tr) {
+  constexpr int NODES = P * P, m = NV * NODES;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.nE * 4 * P) return;
+  const int k = t % P, f = (t / P) % 4, e = t / (4 * P);
+  const int d = f >> 1;
+  const double* l = (f & 1) ? g.lp : g.lm;
+  const double* src[4] = {W, S, dW, dS};
+  double* out = Tr + ((size_t)e * 4 + f) * 4 * NV * P + k;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double* x = src[q] + (size_t)e * m + v * NODES;
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc = fma(l[i], x[d == 0 ? k * P + i : i * P + k], acc);
+      out[(q * NV + v) * P] = acc;
+    }
+}
+

@@ -341,6 +341,20 @@ cudaError_t launch_op_gl(OpKind kind, const OpCfg& c, const Geo& g, const OpArgs
   return dispatch(c, [&](auto d) { return decltype(d)::op(kind, c, g, A); });
 }
 
+cudaError_t launch_gl_traces(const OpCfg& c, const Geo& g, const OpArgs& A, double* Tr) {
+  const int total = g.nE * 4 * c.P;
+  if (total == 0) return cudaSuccess;
+  const int grid = (total + 127) / 128;
+#define GT(PP, NVV) \
+  if (c.P == PP && (c.eq == 0 ? 1 : 4) == NVV) { gl_trace_kernel<PP, NVV><<<grid, 128, 0, c.stream>>>(A.W, A.S, A.dW, A.dS, g, Tr); }
+  if (c.dim != 2 || c.eq == 2) return cudaErrorInvalidValue;
+  GT(2, 1) GT(3, 1) GT(4, 1) GT(5, 1) GT(6, 1) GT(7, 1) GT(8, 1)
+  GT(2, 4) GT(3, 4) GT(4, 4) GT(5, 4) GT(6, 4) GT(7, 4) GT(8, 4)
+#undef GT
+  hbpdc_count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_kbuild_gl(const OpCfg& c, const Geo& g, const double* Wb, const double* gWb, double a1dt,
                              double c2, double* M, int e0, int ne, const double* Sb, const double* gSb) {
   return dispatch(c, [&](auto d) { return decltype(d)::kbuild(c, g, Wb, gWb, a1dt, c2, M, e0, ne, Sb, gSb); });

@@ -1,7 +1,7 @@
 """Operator micro-timings on a full-size config (CUDA events, median of reps):
 FD / EXACT JVP, residual, BJ_ext build, BJ_ext apply.
 
-    python scripts/op_times.py [C3|C4|C5] [reps]      -> one JSON line
+    python scripts/op_times.py [C3|C4|C5] [reps] [gl]   -> one JSON line (gl: GL nodes + the paper's GLF flux)
 """
 import json
 import os
@@ -35,7 +35,9 @@ def main():
     case = sys.argv[1] if len(sys.argv) > 1 else "C3"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     cfg = configs.CONFIGS[case]
-    ctx = hbpdc.context_for(cfg, restart=16, batch_stages=False)
+    gl = len(sys.argv) > 3 and sys.argv[3] == "gl"
+    extra = dict(nodes="gl", flux="glf") if gl else {}
+    ctx = hbpdc.context_for(cfg, restart=16, batch_stages=False, **extra)
     coords = ctx.node_coords()
     W0 = inputs.perturbed_state(inputs.initial_state(case, coords, noise=cfg.noise), inputs.MASTER_SEED + 900)
     dt = configs.cfl_dt(cfg, inputs.initial_state(case, coords))
@@ -47,7 +49,7 @@ def main():
     dS = torch.randn(n, generator=g, dtype=torch.float64).cuda()
     o1, o2 = ctx.empty(), ctx.empty()
     b = W.clone()
-    res = {"config": case, "n": n, "gj_occ": os.environ.get("HBPDC_GJ_OCC", "default")}
+    res = {"config": case, "n": n, "nodes": "gl" if gl else "gll", "gl_traces": os.environ.get("HBPDC_GL_TRACES", "1")}
     res["jvp_fd_us"] = 1e3 * timed(lambda: ctx.jvp(0.5, 1 / 6, dt, W, sig, dW, dS, mode="fd", out1=o1, out2=o2), reps)
     res["jvp_exact_us"] = 1e3 * timed(lambda: ctx.jvp(0.5, 1 / 6, dt, W, sig, dW, dS, mode="exact", out1=o1, out2=o2), reps)
     res["residual_us"] = 1e3 * timed(lambda: ctx.residual(0.5, 1 / 6, dt, b, W, sig, G1=o1, G2=o2), reps)
