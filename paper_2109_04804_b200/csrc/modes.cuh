@@ -53,6 +53,20 @@ __device__ __forceinline__ void load_face_grads(const double* Gf, const double* 
   }
 }
 
+// JVP epilogue inputs (dW, dsigma and the s-step shift vectors) of one node, prefetched
+template <int NV> struct JvpEpiPre {
+  double dw[NV], ds[NV], sw[NV], ss[NV];
+  __device__ __forceinline__ void load(const OpArgs& A, size_t k0, int stride) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const size_t k = k0 + (size_t)v * stride;
+      dw[v] = A.dW[k];
+      ds[v] = A.dS[k];
+      if (A.shw) { sw[v] = A.shw[k]; ss[v] = A.shs[k]; } else { sw[v] = 0.0; ss[v] = 0.0; }
+    }
+  }
+};
+
 __device__ __forceinline__ double fd_step(const OpArgs& A) { return A.d_epsw ? *A.d_epsw : A.epsw; }
 
 template <int EQ, class T, int NODES>
@@ -68,6 +82,10 @@ __device__ __forceinline__ void ld_state(const double* G, const double* Gg, int 
 // field F at (e, v, node) for a node-state load: elements e >= A.nE are ghosts
 // (halo copies of a neighbouring rank's face traces, same layout, comm.h)
 #define FV(F, e, v, node) ((e) < A.nE ? A.F[IDX(e, v, node)] : A.g##F[IDX((e) - A.nE, v, node)])
+// base pointer of field F at (e, node) (variable v at [v * NODES]): the own element of a node
+// state (nbr = false) is never a ghost, so its loads skip the ghost select
+#define FPTR(F, e, node, nbr) (((nbr) && (e) >= A.nE) ? A.g##F + (size_t)((e) - A.nE) * A.m + (node) \
+                                                        : A.F + (size_t)(e) * A.m + (node))
 
 // modes whose neighbour states are frozen (no tangent) declare FROZEN_NBR and load_value()
 template <class M, class = void> struct FrozenNbr : std::false_type {};
@@ -142,8 +160,9 @@ struct OneJetMode {
 template <int EQ, int NODES> struct ModeR1 : OneJetMode<EQ, NODES, ModeR1<EQ, NODES>, double, 1> {
   static constexpr int NV = NVars<EQ>::value, NCH = 1;
   template <int K>
-  __device__ static void load_w(const OpArgs& A, int e, int node, double* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = FV(W, e, v, node);
+  __device__ static void load_w(const OpArgs& A, int e, int node, double* w, bool nbr) {
+    const double* pw = FPTR(W, e, node, nbr);
+    for (int v = 0; v < NV; ++v) w[v] = pw[v * NODES];
   }
   __device__ static void comb(const OpArgs&, const double* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) c[0][v] = F[v];
@@ -158,8 +177,9 @@ template <int EQ, int NODES> struct ModeR1 : OneJetMode<EQ, NODES, ModeR1<EQ, NO
 template <int EQ, int NODES> struct ModeR1Abs : OneJetMode<EQ, NODES, ModeR1Abs<EQ, NODES>, double, 1> {
   static constexpr int NV = NVars<EQ>::value, NCH = 1;
   template <int K>
-  __device__ static void load_w(const OpArgs& A, int e, int node, double* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = FV(W, e, v, node);
+  __device__ static void load_w(const OpArgs& A, int e, int node, double* w, bool nbr) {
+    const double* pw = FPTR(W, e, node, nbr);
+    for (int v = 0; v < NV; ++v) w[v] = pw[v * NODES];
   }
   __device__ static void comb(const OpArgs&, const double* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) c[0][v] = fabs(F[v]);
@@ -173,8 +193,9 @@ template <int EQ, int NODES> struct ModeR1Abs : OneJetMode<EQ, NODES, ModeR1Abs<
 template <int EQ, int NODES> struct ModeR12 : OneJetMode<EQ, NODES, ModeR12<EQ, NODES>, J1, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
   template <int K>
-  __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = J1{FV(W, e, v, node), FV(S, e, v, node)};
+  __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool nbr) {
+    const double *pw = FPTR(W, e, node, nbr), *ps = FPTR(S, e, node, nbr);
+    for (int v = 0; v < NV; ++v) w[v] = J1{pw[v * NODES], ps[v * NODES]};
   }
   __device__ static void comb(const OpArgs&, const J1* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) { c[0][v] = F[v].v; c[1][v] = F[v].a; }
@@ -193,8 +214,9 @@ template <int EQ, int NODES> struct ModeResid : OneJetMode<EQ, NODES, ModeResid<
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
   static constexpr bool NO_DMMA = true;     // FMA contraction measured faster here (r02e)
   template <int K>
-  __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool) {
-    for (int v = 0; v < NV; ++v) w[v] = J1{FV(W, e, v, node), FV(S, e, v, node)};
+  __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool nbr) {
+    const double *pw = FPTR(W, e, node, nbr), *ps = FPTR(S, e, node, nbr);
+    for (int v = 0; v < NV; ++v) w[v] = J1{pw[v * NODES], ps[v * NODES]};
   }
   __device__ static void comb(const OpArgs& A, const J1* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
@@ -202,11 +224,15 @@ template <int EQ, int NODES> struct ModeResid : OneJetMode<EQ, NODES, ModeResid<
       c[1][v] = F[v].v;
     }
   }
-  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
+  struct EpiPre { double w[NV], b[NV], s[NV]; };
+  __device__ static void prefetch_epi(const OpArgs& A, int e, int node, EpiPre& p) {
+    for (int v = 0; v < NV; ++v) { const size_t k = IDX(e, v, node); p.w[v] = A.W[k]; p.b[v] = A.b[k]; p.s[v] = A.S[k]; }
+  }
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV], const EpiPre& p) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      A.out1[k] = (A.W[k] - A.b[k]) + o[0][v];
-      A.out2[k] = A.S[k] - o[1][v];
+      A.out1[k] = (p.w[v] - p.b[v]) + o[0][v];
+      A.out2[k] = p.s[v] - o[1][v];
     }
   }
 };
@@ -217,10 +243,10 @@ template <int EQ, int NODES> struct ModeResid : OneJetMode<EQ, NODES, ModeResid<
 template <int EQ, int NODES> struct ModeJvpExact : OneJetMode<EQ, NODES, ModeJvpExact<EQ, NODES>, HJ, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
   template <int K>
-  __device__ static void load_w(const OpArgs& A, int e, int node, HJ* w, bool) {
-    for (int v = 0; v < NV; ++v) {
-      w[v] = HJ{FV(W, e, v, node), FV(S, e, v, node), FV(dW, e, v, node), FV(dS, e, v, node)};
-    }
+  __device__ static void load_w(const OpArgs& A, int e, int node, HJ* w, bool nbr) {
+    const double *pw = FPTR(W, e, node, nbr), *ps = FPTR(S, e, node, nbr);
+    const double *pdw = FPTR(dW, e, node, nbr), *pds = FPTR(dS, e, node, nbr);
+    for (int v = 0; v < NV; ++v) w[v] = HJ{pw[v * NODES], ps[v * NODES], pdw[v * NODES], pds[v * NODES]};
   }
   __device__ static void comb(const OpArgs& A, const HJ* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) {
@@ -228,11 +254,13 @@ template <int EQ, int NODES> struct ModeJvpExact : OneJetMode<EQ, NODES, ModeJvp
       c[1][v] = F[v].b;
     }
   }
-  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
+  using EpiPre = JvpEpiPre<NV>;
+  __device__ static void prefetch_epi(const OpArgs& A, int e, int node, EpiPre& p) { p.load(A, IDX(e, 0, node), NODES); }
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV], const EpiPre& p) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      double t1 = A.dW[k] + o[0][v], t2 = A.dS[k] - o[1][v];
-      if (A.shw) { t1 = fma(-A.shift, A.shw[k], t1); t2 = fma(-A.shift, A.shs[k], t2); }
+      double t1 = p.dw[v] + o[0][v], t2 = p.ds[v] - o[1][v];
+      if (A.shw) { t1 = fma(-A.shift, p.sw[v], t1); t2 = fma(-A.shift, p.ss[v], t2); }
       A.out1[k] = t1;
       A.out2[k] = t2;
     }
@@ -251,16 +279,19 @@ template <int EQ, int NODES> struct ModeJvpFD {
   template <int K> using StateT = typename std::conditional<K == 0, J1, J2>::type;
   struct State { NodeState<EQ, J1> p; NodeState<EQ, J2> q; };
   template <int K>
-  __device__ static void load_w(const Args& A, int e, int node, StateT<K>* w, bool) {
-    for (int v = 0; v < NV; ++v) {
-      const double Wk = FV(W, e, v, node), Sk = FV(S, e, v, node);
-      if constexpr (K == 0) {
-        const double ew = fd_step(A);
-        const double wp = ew > 0.0 ? __dadd_rn(Wk, __dmul_rn(ew, FV(dW, e, v, node))) : Wk;
-        w[v] = J1{wp, Sk};
-      } else {
-        w[v] = J2{Wk, Sk, FV(dS, e, v, node)};
+  __device__ static void load_w(const Args& A, int e, int node, StateT<K>* w, bool nbr) {
+    const double *pw = FPTR(W, e, node, nbr), *ps = FPTR(S, e, node, nbr);
+    if constexpr (K == 0) {
+      const double ew = fd_step(A);
+      const double* pdw = FPTR(dW, e, node, nbr);
+      for (int v = 0; v < NV; ++v) {
+        const double Wk = pw[v * NODES];
+        const double wp = ew > 0.0 ? __dadd_rn(Wk, __dmul_rn(ew, pdw[v * NODES])) : Wk;
+        w[v] = J1{wp, ps[v * NODES]};
       }
+    } else {
+      const double* pds = FPTR(dS, e, node, nbr);
+      for (int v = 0; v < NV; ++v) w[v] = J2{pw[v * NODES], ps[v * NODES], pds[v * NODES]};
     }
   }
   __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
@@ -514,11 +545,13 @@ template <int EQ, int NODES> struct ModeJvpFD {
       }
     }
   }
-  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+  using EpiPre = JvpEpiPre<NV>;
+  __device__ static void prefetch_epi(const Args& A, int e, int node, EpiPre& p) { p.load(A, IDX(e, 0, node), NODES); }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV], const EpiPre& p) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      double t1 = A.dW[k] + o[0][v], t2 = A.dS[k] - o[1][v];
-      if (A.shw) { t1 = fma(-A.shift, A.shw[k], t1); t2 = fma(-A.shift, A.shs[k], t2); }
+      double t1 = p.dw[v] + o[0][v], t2 = p.ds[v] - o[1][v];
+      if (A.shw) { t1 = fma(-A.shift, p.sw[v], t1); t2 = fma(-A.shift, p.ss[v], t2); }
       A.out1[k] = t1;
       A.out2[k] = t2;
     }
@@ -536,10 +569,11 @@ template <int EQ, int NODES> struct ModeJvpLinear {
   __device__ static void load_w(const Args& A, int e, int node, double* w, bool) {
     for (int v = 0; v < NV; ++v) w[v] = FV(dW, e, v, node);
   }
-  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool) {
+  __device__ static void load(const Args& A, const Geo&, int e, int, int node, State& st, bool nbr) {
+    const double *pdw = FPTR(dW, e, node, nbr), *pds = FPTR(dS, e, node, nbr);
     for (int v = 0; v < NV; ++v) {
-      const double dw = FV(dW, e, v, node);
-      st.u0.w[v] = fma(A.c2, FV(dS, e, v, node), -A.a1dt * dw);
+      const double dw = pdw[v * NODES];
+      st.u0.w[v] = fma(A.c2, pds[v * NODES], -A.a1dt * dw);
       st.u1.w[v] = dw;
     }
   }
@@ -572,11 +606,13 @@ template <int EQ, int NODES> struct ModeJvpLinear {
                                       int rs, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) { c[0][v] = r0[rs * v]; c[1][v] = r1[rs * v]; }
   }
-  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV]) {
+  using EpiPre = JvpEpiPre<NV>;
+  __device__ static void prefetch_epi(const Args& A, int e, int node, EpiPre& p) { p.load(A, IDX(e, 0, node), NODES); }
+  __device__ static void epilogue(const Args& A, int e, int node, const double (&o)[NCH][NV], const EpiPre& p) {
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      double t1 = A.dW[k] + o[0][v], t2 = A.dS[k] - o[1][v];
-      if (A.shw) { t1 = fma(-A.shift, A.shw[k], t1); t2 = fma(-A.shift, A.shs[k], t2); }
+      double t1 = p.dw[v] + o[0][v], t2 = p.ds[v] - o[1][v];
+      if (A.shw) { t1 = fma(-A.shift, p.sw[v], t1); t2 = fma(-A.shift, p.ss[v], t2); }
       A.out1[k] = t1;
       A.out2[k] = t2;
     }
@@ -591,7 +627,8 @@ template <int EQ, int NODES> struct ModeKApply : OneJetMode<EQ, NODES, ModeKAppl
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
   static constexpr bool FROZEN_NBR = true;
   __device__ static void load_value(const OpArgs& A, int e, int node, double* w) {
-    for (int v = 0; v < NV; ++v) w[v] = FV(W, e, v, node);
+    const double* pw = FPTR(W, e, node, true);
+    for (int v = 0; v < NV; ++v) w[v] = pw[v * NODES];
   }
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, J2* w, bool nbr) {
@@ -607,18 +644,23 @@ template <int EQ, int NODES> struct ModeKApply : OneJetMode<EQ, NODES, ModeKAppl
   __device__ static void comb(const OpArgs&, const J2* F, double (&c)[NCH][NV]) {
     for (int v = 0; v < NV; ++v) { c[0][v] = F[v].a; c[1][v] = F[v].b; }
   }
-  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
-    (void)epilogue_ss(A, e, node, o);
-  }
+
   // epilogue that also returns this node's sum of out1^2 (op_kernel reduces it per CTA)
   static constexpr bool NORM_EPILOGUE = true;
-  __device__ static double epilogue_ss(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
+  struct EpiPre { double u[NV], vv[NV]; };
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV], const EpiPre& p) {
+    (void)epilogue_ss(A, e, node, o, p);
+  }
+  __device__ static void prefetch_epi(const OpArgs& A, int e, int node, EpiPre& p) {
+    for (int v = 0; v < NV; ++v) { const size_t k = IDX(e, v, node); p.u[v] = A.U[k]; p.vv[v] = A.V[k]; }
+  }
+  __device__ static double epilogue_ss(const OpArgs& A, int e, int node, const double (&o)[NCH][NV], const EpiPre& p) {
     double ss = 0.0;
     for (int v = 0; v < NV; ++v) {
       const size_t k = IDX(e, v, node);
-      const double t1 = fma(-A.c2, o[0][v], A.U[k]);
+      const double t1 = fma(-A.c2, o[0][v], p.u[v]);
       A.out1[k] = t1;
-      A.out2[k] = A.V[k] + o[1][v];
+      A.out2[k] = p.vv[v] + o[1][v];
       ss = fma(t1, t1, ss);
     }
     return ss;

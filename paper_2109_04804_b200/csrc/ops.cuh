@@ -371,6 +371,15 @@ template <class A, class = void> struct HasDevEps : std::false_type {};
 template <class A> struct HasDevEps<A, std::void_t<decltype(A::d_epsw)>> : std::true_type {};
 
 // modes may evaluate their volume fluxes in two passes (VOL_PASSES = 2)
+// modes whose epilogue inputs are prefetched before the element's first barrier
+// (Mode::EpiPre, prefetch_epi, epilogue(A, e, node, out, pre)): the loads overlap the
+// barrier wait, the surface terms and the contraction instead of stalling the epilogue
+template <class M, class = void> struct HasEpiPre : std::false_type {};
+template <class M> struct HasEpiPre<M, std::void_t<typename M::EpiPre>> : std::true_type {};
+struct NoEpiPre {};
+template <class M, class = void> struct EpiPreOf { using type = NoEpiPre; };
+template <class M> struct EpiPreOf<M, std::void_t<typename M::EpiPre>> { using type = typename M::EpiPre; };
+struct NoHook { __device__ void operator()() const {} };
 template <class M, class = void> struct VolPasses { static constexpr int value = 1; };
 template <class M> struct VolPasses<M, std::void_t<decltype(M::VOL_PASSES)>> {
   static constexpr int value = M::VOL_PASSES;
@@ -417,10 +426,11 @@ __host__ __device__ constexpr int slot_doubles() {
          Staged<Mode>::value * Dims<DIM, P>::NODES;      // per-thread staging [k][node]
 }
 
-template <int EQ, int DIM, int P, class Mode, class G>
+template <int EQ, int DIM, int P, class Mode, class G, class Hook = NoHook>
 __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const PhysParams& pp,
                                           const G& g, int e, int slot, int node, bool active,
-                                          double* sF, double (&out)[Mode::NCH][NVars<EQ>::value]) {
+                                          double* sF, double (&out)[Mode::NCH][NVars<EQ>::value],
+                                          Hook pre_barrier = Hook{}) {
   constexpr int NV = NVars<EQ>::value;
   constexpr int NCH = Mode::NCH;
   constexpr int NFP = Mode::NFP;
@@ -517,8 +527,9 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       Mode::face_part(A, pp, g, e, own, nb, nnode, slot, plus, d, part, sRaw + part * NFN + fn, NFP * NFN);
     }
   }
+  if (active) pre_barrier();
   __syncthreads();
-  if (active) {
+  if (active && !kDmmaContract<DIM, P, Mode>) {
     // surface terms of this node's face(s), canonical flux with the outward sign:
     // s_d (f*_+ lhat_N(1) - f*_- lhat_0(-1)), summed in the order +x, -x, +y, -y
     double sf[NCH][NV];
@@ -591,12 +602,6 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
           }
           out[c][v] = -(acc + sf[c][v]);
         }
-    } else {
-      // keep the surface terms; the volume contraction follows on the tensor cores
-#pragma unroll
-      for (int c = 0; c < NCH; ++c)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) out[c][v] = sf[c][v];
     }
   }
   if constexpr (kDmmaContract<DIM, P, Mode>) {
@@ -607,14 +612,31 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
     // an element slot take alternate (c, v) planes; D stays in registers as
     // fragments; the result overwrites the F_x plane (node layout) and every
     // thread then reads its node's value back.
+    //
+    // The surface terms are a fifth k-step (k = +x, -x, +y, -y faces):
+    //   V_ji += f*_{+x,j} sx lh+(i) - f*_{-x,j} sx lh-(i) + sy lh+(j) f*_{+y,i} - sy lh-(j) f*_{-y,i}
+    // with lh+-(i) = lhat_i(+-1) (GLL: nonzero on the edge node only).  Lane L of each warp
+    // combines the two parts of face node L (face L >> 3, node L & 7) -- warp-uniform, once per
+    // lane, instead of divergent per-boundary-node face sums -- and the fragments are
+    // gathered by shuffles.
     const int lane = threadIdx.x & 31, wslot = node >> 5;
     const int r = lane >> 2, q = lane & 3;
     if (active) {
       double fx0 = g.sx * g.Dh[r * P + q], fx1 = g.sx * g.Dh[r * P + q + 4];   // B = sx Dhat^T: (k = l, n = i)
       double fy0 = g.sy * g.Dh[r * P + q], fy1 = g.sy * g.Dh[r * P + q + 4];   // A = sy Dhat:   (m = j, k = m')
+      double lhp_r, lhm_r;
+      if constexpr (G::GL) { lhp_r = g.lhpv[r]; lhm_r = g.lhmv[r]; }
+      else { lhp_r = r == P - 1 ? g.lhp : 0.0; lhm_r = r == 0 ? g.lhm : 0.0; }
+      // constant halves of the fifth k-step: B rows k = 0, 1 (x faces), A columns k = 2, 3 (y faces)
+      const double sconst = q == 0 ? g.sx * lhp_r : (q == 1 ? -(g.sx * lhm_r) : (q == 2 ? g.sy * lhp_r : -(g.sy * lhm_r)));
+      double cfl[NCH][NV];
+      Mode::face_combine(A, pp, lane >> 4, sRaw + lane, sRaw + NFN + lane, NFP * NFN, cfl);
+      const int src = ((q ^ 1) << 3) | r;      // face slot q = +x, -x, +y, -y is face 1, 0, 3, 2
 #pragma unroll
-      for (int mi = wslot; mi < NCH * NV; mi += NODES / 32) {
+      for (int mi = 0; mi < NCH * NV; ++mi) {
+        if (mi % (NODES / 32) != wslot) continue;     // warp-uniform
         const int c = mi / NV, v = mi % NV;
+        const double fv = __shfl_sync(0xffffffffu, cfl[c][v], src);
         double* Fx = sF + ((c * DIM + 0) * NV + v) * PLANE;
         const double* Fy = sF + ((c * DIM + 1) * NV + v) * PLANE;
         double acc[2] = {0.0, 0.0};
@@ -622,6 +644,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
         dmma_8x8x4(acc, Fx[r * PS + q + 4], fx1);
         dmma_8x8x4(acc, fy0, Fy[q * PS + r]);
         dmma_8x8x4(acc, fy1, Fy[(q + 4) * PS + r]);
+        dmma_8x8x4(acc, q < 2 ? fv : sconst, q < 2 ? sconst : fv);
         __syncwarp();
         Fx[r * PS + 2 * q] = acc[0];
         Fx[r * PS + 2 * q + 1] = acc[1];
@@ -633,7 +656,7 @@ __device__ __forceinline__ void eval_slot(const typename Mode::Args& A, const Ph
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
         for (int v = 0; v < NV; ++v)
-          out[c][v] = -(sF[((c * DIM + 0) * NV + v) * PLANE + row * PS + i] + out[c][v]);
+          out[c][v] = -sF[((c * DIM + 0) * NV + v) * PLANE + row * PS + i];
     }
   }
 }
@@ -663,17 +686,25 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL, BR2
   int e;
   const bool active = launch_elem(g, blockIdx.x * EPB + slot, e);
   double out[Mode::NCH][NV];
+  using Pre = typename std::conditional<HasEpiPre<Mode>::value, typename EpiPreOf<Mode>::type, NoEpiPre>::type;
+  Pre pre;
   typename Mode::Args Al = A;
   if constexpr (HasDevEps<typename Mode::Args>::value) {
     // the FD step lives in device memory (norm computed on the device): read it once
     if (Al.d_epsw) { Al.epsw = __ldg(Al.d_epsw); Al.d_epsw = nullptr; }
     Al.iepsw = Al.epsw > 0.0 ? 1.0 / Al.epsw : 0.0;    // once per thread (was: per face and pass)
   }
-  eval_slot<EQ, DIM, P, Mode>(Al, pp, g, e, slot, node, active, sF + slot * SLOT, out);
+  auto hook = [&]() {
+    if constexpr (HasEpiPre<Mode>::value) Mode::prefetch_epi(Al, e, node, pre);
+  };
+  eval_slot<EQ, DIM, P, Mode>(Al, pp, g, e, slot, node, active, sF + slot * SLOT, out, hook);
   if constexpr (NormEpilogue<Mode>::value) {
     // per-CTA partial of sum(out1^2), fixed reduction order (warp tree, then warps in order)
     double ss = 0.0;
-    if (active) ss = Mode::epilogue_ss(Al, e, node, out);
+    if (active) {
+      if constexpr (HasEpiPre<Mode>::value) ss = Mode::epilogue_ss(Al, e, node, out, pre);
+      else ss = Mode::epilogue_ss(Al, e, node, out);
+    }
     if (Al.nrm_part) {
 #pragma unroll
       for (int o2 = 16; o2 > 0; o2 >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o2);
@@ -687,7 +718,10 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL, BR2
       }
     }
   } else {
-    if (active) Mode::epilogue(Al, e, node, out);
+    if (active) {
+      if constexpr (HasEpiPre<Mode>::value) Mode::epilogue(Al, e, node, out, pre);
+      else Mode::epilogue(Al, e, node, out);
+    }
   }
 }
 
