@@ -14,6 +14,7 @@
 // Same row layout / semantics as launch_block_dots_mma / launch_block_update_mma;
 // deterministic (fixed chunk -> CTA map, fixed accumulation order).
 #include <algorithm>
+#include <cstdlib>
 #include "launch.h"
 #include "tma.cuh"
 
@@ -557,9 +558,186 @@ __global__ void __launch_bounds__(32 * (TF_W + 1), 1) block_update_dots_tma8_ker
   part[((size_t)nq * 8 + g * 8 + 2 * t + 1) * ncol + col] = gacc[1];
 }
 
+// Chunk-resident variant (round 2): the chunk's Q tiles stay in shared memory between phase U
+// and phase D (no L2 re-stream).  Chunks of TR_E = 64 elements (512 B row copies, 4 KB tiles),
+// a 47-tile ring: a chunk holds T = nq / 8 <= 20 slots from its phase-U wait to its phase-D
+// release, and the ring holds the whole next chunk besides (measured: with 128-element chunks
+// and a 24-tile ring only part of the next chunk fits and its last tiles are issued after the
+// phase-D releases -- 3.0 TB/s), so HBM never waits on the L2 pass (ncu r02o: the L2 re-read version ran at
+// 49 % of DRAM peak, 4.0 TB/s of algorithmic bytes).  Same partial layout as above (TF_W
+// consumer warps, one partial each); only the element -> warp map (and so the rounding order)
+// differs.
+namespace {
+#ifndef TR_E_
+#define TR_E_ 64
+#endif
+constexpr int TR_E = TR_E_;
+constexpr int TR_P = TR_E + 4;
+constexpr int TR_R = (200 * 1024) / (8 * TR_P * 8);
+constexpr int TR_NB = TR_E / (8 * TF_W);
+static_assert(TR_R >= TF_MAXT, "a chunk must fit the ring");
+static_assert(TR_NB >= 1, "TR_E: at least one 8-element n-block per consumer warp");
+}
+__global__ void __launch_bounds__(32 * (TF_W + 1), 1) block_update_dots_res8_kernel(const double* __restrict__ Q, size_t ldq,
+                                                                        int nq, double* __restrict__ W, size_t ldw,
+                                                                        const double* __restrict__ C, size_t L,
+                                                                        double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nq8 = (nq + 7) / 8 * 8;
+  double* ring = reinterpret_cast<double*>(smraw);                            // TR_R x 8 x TR_P
+  double* sC = ring + (size_t)TR_R * 8 * TR_P;                                // C1 (zero padded to nq8 x 8)
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sC + (size_t)nq8 * 8);
+  unsigned long long* empty = full + TR_R;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < TR_R * 8 * TR_P; k += blockDim.x) ring[k] = 0.0;
+  for (int k = threadIdx.x; k < nq8 * 8; k += blockDim.x) sC[k] = k < nq * 8 ? C[k] : 0.0;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < TR_R; ++r) { mbar_init(&full[r], 1); mbar_init(&empty[r], TF_W); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  const int T = nq8 / 8;
+  const size_t nch = (L + TR_E - 1) / TR_E;
+  const size_t nmy = blockIdx.x < nch ? (nch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (wid == TF_W) {                                                          // ---- producer
+    size_t k = 0;
+    for (size_t ci = 0; ci < nmy; ++ci) {
+      const size_t e0 = (blockIdx.x + ci * gridDim.x) * TR_E;
+      const int ne = (int)min((size_t)TR_E, L - e0);
+      for (int tile = 0; tile < T; ++tile, ++k) {
+        const int st = (int)(k % TR_R);
+        const int nrow = min(8, nq - 8 * tile);
+        if (lane == 0) {
+          if (k >= (size_t)TR_R) mbar_wait(&empty[st], (unsigned)(((k / TR_R) - 1) & 1));
+          mbar_expect_tx(&full[st], (unsigned)(nrow * ne * sizeof(double)));
+        }
+        __syncwarp();
+        if (lane < nrow)
+          tma_load_1d(ring + ((size_t)st * 8 + lane) * TR_P, Q + (size_t)(8 * tile + lane) * ldq + e0,
+                      (unsigned)(ne * sizeof(double)), &full[st]);
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  double dacc[TF_MAXT][2], gacc[2] = {0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < TF_MAXT; ++i) { dacc[i][0] = 0.0; dacc[i][1] = 0.0; }
+  size_t k0 = 0;
+  for (size_t ci = 0; ci < nmy; ++ci, k0 += T) {
+    const size_t e0 = (blockIdx.x + ci * gridDim.x) * TR_E;
+    double wv[TR_NB][2];
+    {
+      const double* wg = W + (size_t)g * ldw;
+#pragma unroll
+      for (int nb = 0; nb < TR_NB; ++nb) {
+        const size_t e = e0 + (size_t)(wid * TR_NB + nb) * 8 + 2 * t;
+        if (e + 1 < L) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(wg + e));
+          wv[nb][0] = v.x;
+          wv[nb][1] = v.y;
+        } else {
+          wv[nb][0] = e < L ? wg[e] : 0.0;
+          wv[nb][1] = 0.0;
+        }
+      }
+    }
+    // ---- phase U: D = C1^T Q over the chunk; the tiles stay in the ring
+    double acc[TR_NB][2];
+#pragma unroll
+    for (int nb = 0; nb < TR_NB; ++nb) { acc[nb][0] = 0.0; acc[nb][1] = 0.0; }
+    for (int tile = 0; tile < T; ++tile) {
+      const size_t k = k0 + tile;
+      const int st = (int)(k % TR_R);
+      mbar_wait(&full[st], (unsigned)((k / TR_R) & 1));
+      const double* sb = ring + (size_t)st * 8 * TR_P + (size_t)(wid * TR_NB) * 8 + g;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const double a = sC[(8 * tile + 4 * kk + t) * 8 + g];
+#pragma unroll
+        for (int nb = 0; nb < TR_NB; ++nb) dmma(acc[nb], a, sb[(4 * kk + t) * TR_P + nb * 8]);
+      }
+    }
+    double (&w1)[TR_NB][2] = acc;
+#pragma unroll
+    for (int nb = 0; nb < TR_NB; ++nb) {
+      const size_t e = e0 + (size_t)(wid * TR_NB + nb) * 8 + 2 * t;
+      w1[nb][0] = e < L ? wv[nb][0] - acc[nb][0] : 0.0;          // beyond L: 0 (stale ring rows)
+      w1[nb][1] = e + 1 < L ? wv[nb][1] - acc[nb][1] : 0.0;
+      double* wg = W + (size_t)g * ldw;
+      if (e + 1 < L) {
+        *reinterpret_cast<double2*>(wg + e) = make_double2(w1[nb][0], w1[nb][1]);
+      } else if (e < L) {
+        wg[e] = w1[nb][0];
+      }
+    }
+    double bf[TR_NB][2];
+#pragma unroll
+    for (int nb = 0; nb < TR_NB; ++nb)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int src = g * 4 + 2 * kk + (t >> 1);
+        const double v0 = __shfl_sync(0xffffffffu, w1[nb][0], src);
+        const double v1 = __shfl_sync(0xffffffffu, w1[nb][1], src);
+        bf[nb][kk] = (t & 1) ? v1 : v0;
+      }
+#pragma unroll
+    for (int nb = 0; nb < TR_NB; ++nb)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) dmma(gacc, bf[nb][kk], bf[nb][kk]);
+    // ---- phase D: Q_tile^T W1 from the resident tiles, then release them
+#pragma unroll
+    for (int tile = 0; tile < TF_MAXT; ++tile) {
+      if (tile < T) {
+        const size_t k = k0 + tile;
+        const int st = (int)(k % TR_R);
+        const double* sa = ring + (size_t)st * 8 * TR_P + (size_t)g * TR_P + (size_t)(wid * TR_NB) * 8 + t;
+#pragma unroll
+        for (int nb = 0; nb < TR_NB; ++nb)
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) dmma(dacc[tile], sa[nb * 8 + 4 * kk], bf[nb][kk]);
+        fence_proxy_async_smem();      // order this lane's reads before the stage's next bulk copy
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+    }
+  }
+  const size_t col = (size_t)blockIdx.x * TF_W + wid, ncol = (size_t)gridDim.x * TF_W;
+#pragma unroll
+  for (int tile = 0; tile < TF_MAXT; ++tile) {
+    const int j = 8 * tile + g;
+    if (tile < T && j < nq) {
+      part[((size_t)j * 8 + 2 * t) * ncol + col] = dacc[tile][0];
+      part[((size_t)j * 8 + 2 * t + 1) * ncol + col] = dacc[tile][1];
+    }
+  }
+  part[((size_t)nq * 8 + g * 8 + 2 * t) * ncol + col] = gacc[0];
+  part[((size_t)nq * 8 + g * 8 + 2 * t + 1) * ncol + col] = gacc[1];
+}
+
 cudaError_t launch_block_update_dots_tma8(const double* Q, size_t ldq, int nq, double* W, size_t ldw,
                                           const double* C, size_t L, double* part, cudaStream_t st) {
   if (nq < 1 || nq > block_fused_max_nq() || (ldq & 1) || (ldw & 1)) return cudaErrorInvalidValue;
+  static const bool resident = [] {
+    const char* e = getenv("HBPDC_FUSED_L2");    // 1: the round-1 L2 re-stream kernel
+    return !(e && atoi(e) == 1);
+  }();
+  if (resident) {
+    const int nq8 = (nq + 7) / 8 * 8;
+    const size_t smem = ((size_t)TR_R * 8 * TR_P + (size_t)nq8 * 8) * sizeof(double) +
+                        2 * TR_R * sizeof(unsigned long long);
+    static size_t attr = 0;
+    if (smem > attr) {
+      if (cudaFuncSetAttribute(block_update_dots_res8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return cudaErrorInvalidValue;
+      attr = smem;
+    }
+    block_update_dots_res8_kernel<<<block_dot_blocks_tma(), 32 * (TF_W + 1), smem, st>>>(Q, ldq, nq, W, ldw, C, L, part);
+    hbpdc_count_launch();
+    return cudaGetLastError();
+  }
   const int nq8 = (nq + 7) / 8 * 8;
   const size_t smem = ((size_t)TF_R * 8 * TF_P + (size_t)nq8 * 8) * sizeof(double) +
                       2 * TF_R * sizeof(unsigned long long);
