@@ -566,7 +566,11 @@ __global__ void __launch_bounds__(32 * (TF_W + 1), 1) block_update_dots_tma8_ker
 // phase-D releases -- 3.0 TB/s), so HBM never waits on the L2 pass (ncu r02o: the L2 re-read version ran at
 // 49 % of DRAM peak, 4.0 TB/s of algorithmic bytes).  Same partial layout as above (TF_W
 // consumer warps, one partial each); only the element -> warp map (and so the rounding order)
-// differs.
+// differs.  NOT the default: the bulk copies are then 512 B / 1 KB rows and the copy issue rate,
+// not the bytes, bounds the stream (C3 bench, r02r/r02s: 1.5 TB/s with 64-element chunks,
+// 3.0 TB/s with 128, against 4.2 TB/s for the L2 re-stream kernel with 4 KB rows).  Kept behind
+// HBPDC_FUSED_RES=1 for the record; a 2D-tensor TMA box (8 rows x 64 elements per copy, swizzled)
+// would be the way to make the resident schedule pay.
 namespace {
 #ifndef TR_E_
 #define TR_E_ 64
@@ -720,8 +724,8 @@ cudaError_t launch_block_update_dots_tma8(const double* Q, size_t ldq, int nq, d
                                           const double* C, size_t L, double* part, cudaStream_t st) {
   if (nq < 1 || nq > block_fused_max_nq() || (ldq & 1) || (ldw & 1)) return cudaErrorInvalidValue;
   static const bool resident = [] {
-    const char* e = getenv("HBPDC_FUSED_L2");    // 1: the round-1 L2 re-stream kernel
-    return !(e && atoi(e) == 1);
+    const char* e = getenv("HBPDC_FUSED_RES");   // 1: the chunk-resident kernel (measured slower)
+    return e && atoi(e) == 1;
   }();
   if (resident) {
     const int nq8 = (nq + 7) / 8 * 8;
