@@ -115,6 +115,7 @@ struct hbpdc_ctx {
   double *dnrm = nullptr, *deps = nullptr;
   double *Sb = nullptr, *gSb = nullptr;   // BJ^H_ext: sigma at the build point, R1(Wb), and its ghosts
   double *lift0 = nullptr, *lift1 = nullptr;
+  double* liftB = nullptr;        // NS BJ_ext build: lifted gradients of the build state (ModeKNS)
   double *liftf0 = nullptr, *liftf1 = nullptr;   // BR2 per-face gradients (NULL: BR1)
   // precond
   double *S = nullptr, *Wb = nullptr, *Z = nullptr;
@@ -349,7 +350,8 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
       }
     }
     Geo lg = c->geo;                 // a colour-restricted operator needs the lifting on the
-    if (lg.cmode == 1) lg.cmode = 2;   // colour's elements and their neighbours
+    if (lg.cmode == 1 && k != OP_KNS) lg.cmode = 2;   // colour's elements and their neighbours
+                                     // (OP_KNS: the colour's elements only, ModeKNS)
     CK(launch_lift(k, 0, c->cfg, lg, A, c->lift0, c->liftf0, gtg0));
     A.G0 = c->lift0;
     A.Gf0 = c->liftf0;
@@ -591,6 +593,16 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
     // the fp64 tensor cores afterwards (K_i^2 e_c = K_i (K_i e_c) exactly: the same block),
     // instead of a second colour pass through lifting and operator per column
     const bool single = kk_gemm_supported(c->m) && !std::getenv("HBPDC_NS_TWOPASS");
+    // one-hop lifting (ModeKNS, GLL / BR1 / one rank): the colour pass lifts the colour's elements
+    // only; the neighbours' gradients are the build state's plus the seed's central-value term
+    const char* onehop_env = std::getenv("HBPDC_NS_ONEHOP");
+    const bool onehop = single && !c->halo() && !c->geo.gl && !c->geo.br2 && !(onehop_env && atoi(onehop_env) == 0);
+    if (onehop) {
+      if (!c->liftB) CKS(dalloc(c, &c->liftB, (size_t)c->nE * 6 * c->P * c->P));
+      OpArgs B = base_args(c);
+      B.W = c->Wb;
+      CK(launch_lift(OP_R1, 0, c->cfg, c->geo, B, c->liftB, nullptr, nullptr));
+    }
     const Geo full = c->geo;
     for (int cy = 0; cy < Py; ++cy)
       for (int cx = 0; cx < Px; ++cx) {
@@ -602,7 +614,8 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
           if (ce != cudaSuccess) { c->geo = full; CK(ce); }
           OpArgs A = base_args(c);
           A.W = c->Wb; A.S = c->tseed; A.out1 = nullptr; A.out2 = c->y1;
-          st = run_op(c, OP_R12, A);
+          A.Gb = c->liftB;
+          st = run_op(c, onehop ? OP_KNS : OP_R12, A);
           if (st != HBPDC_OK) break;
           if (hess) {
             // BJ^H_ext: H e_c = e1e2 part of R1(W_b + e1 sigma_b + e2 e_c) (reading R31), from the

@@ -10,7 +10,7 @@ struct OpArgs;
 
 // OP_R1ABS needs a Geo with |Dhat| and lhm negated (see hbpdc.cu)
 enum OpKind { OP_R1 = 0, OP_R12, OP_RESID, OP_JVP_EXACT, OP_JVP_FD, OP_JVP_LINEAR, OP_KAPPLY, OP_R1ABS, OP_KLIN,
-              OP_NKINDS };
+              OP_KNS, OP_NKINDS };
 
 struct OpCfg {
   int eq, dim, P;

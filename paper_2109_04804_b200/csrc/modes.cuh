@@ -34,6 +34,7 @@ struct OpArgs {
   const double *Gf0, *Gf1;   // NS BR2: per-face gradients of jet states 0 / 1, or NULL (BR1)
   const double *gGf0, *gGf1; // their ghost copies (the neighbour ranks' shared faces)
   const double* Tr;          // GL FD JVP: face traces [e][face 4][field W,S,dW,dS][var][P] (gl_trace_kernel), or NULL
+  const double* Gb;          // NS BJ_ext colour build (ModeKNS): lifted gradients of the build state [e][6][NODES]
 };
 
 // NS BR2 face gradients: [elem][face 4][6][JetN][P] (lift_kernel), face f = 2d + plus,
@@ -692,4 +693,57 @@ template <int EQ, int NODES> struct ModeKLin : OneJetMode<EQ, NODES, ModeKLin<EQ
 };
 
 #undef FV
+// NS BJ_ext colour build, one column of K_i for the colour's elements (GLL, BR1, one rank):
+// the tangent channel of R1(W_b + e1 t), t = the seed (zero outside the colour's elements),
+// with the lifting evaluated on the colour's elements ONLY.  The neighbour's lifted gradient
+// at the shared face is the build state's (A.Gb) plus its one seed-dependent term: the
+// neighbour's BR1 central value g* = 1/2 (g_nb + g_i) gives its normal gradient
+// component at the shared face node the tangent s_nb * 1/2 * dg_i, s_nb = (2/h) lhat of the
+// neighbour's side -- exactly what the neighbour's own lifting of the seeded state computes
+// there (its volume part and its other faces carry no tangent).  This replaces a lifting pass
+// over the colour's elements AND their four neighbours per (colour, column) (reading R19).
+template <int EQ, int NODES> struct ModeKNS : OneJetMode<EQ, NODES, ModeKNS<EQ, NODES>, J1, 1> {
+  static constexpr int NV = NVars<EQ>::value, NCH = 1;
+  using Base = OneJetMode<EQ, NODES, ModeKNS<EQ, NODES>, J1, 1>;
+  template <int K>
+  __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool nbr) {
+    const double *pw = FPTR(W, e, node, nbr), *ps = FPTR(S, e, node, nbr);
+    for (int v = 0; v < NV; ++v) w[v] = J1{pw[v * NODES], ps[v * NODES]};
+  }
+  __device__ static void comb(const OpArgs&, const J1* F, double (&c)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) c[0][v] = F[v].a;
+  }
+  __device__ static void epilogue(const OpArgs& A, int e, int node, const double (&o)[NCH][NV]) {
+    for (int v = 0; v < NV; ++v) A.out2[IDX(e, v, node)] = o[0][v];
+  }
+  template <class G>
+  __device__ static void face_part(const OpArgs& A, const PhysParams& pp, const G& g, int e, int own, int nb,
+                                   int nnode, int slot, bool plus, int d, int part, double* raw, int rs) {
+    const bool use_own = (part == 0) == plus;
+    if (use_own || EQ != 2) {
+      Base::face_part(A, pp, g, e, own, nb, nnode, slot, plus, d, part, raw, rs);
+      return;
+    }
+    if constexpr (EQ == 2) {
+      NodeState<EQ, J1> sn, so;
+      const double* pw = A.W + (size_t)nb * A.m + nnode;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sn.w[v] = J1{pw[v * NODES], 0.0};      // t = 0 off the colour
+      const double* gb = A.Gb + (size_t)nb * 6 * NODES + nnode;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { sn.gx[k] = J1{gb[k * NODES], 0.0}; sn.gy[k] = J1{gb[(k + 3) * NODES], 0.0}; }
+      load_w<0>(A, e, own, so.w, false);
+      J1 go[3];
+      grad_vars(pp, so.w, go);
+      const double snb = (d == 0 ? g.sx : g.sy) * (plus ? -g.lhm : g.lhp);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double tk = snb * (0.5 * go[k].a);
+        if (d == 0) sn.gx[k].a = tk; else sn.gy[k].a = tk;
+      }
+      half_flux<EQ, J1>(pp, sn, d, raw, rs);
+    }
+  }
+};
+
 #undef IDX

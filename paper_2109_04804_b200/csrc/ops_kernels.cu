@@ -265,6 +265,9 @@ template <int EQ, int DIM, int P> struct Disp {
       case OP_KLIN:
         if constexpr (EQ != 2) return run_op<EQ, DIM, P, ModeKLin<EQ, NODES>>(c, g, A);
         else return cudaErrorNotSupported;
+      case OP_KNS:
+        if constexpr (EQ == 2 && DIM == 2 && !kGL && !kBR2) return run_op<EQ, DIM, P, ModeKNS<EQ, NODES>>(c, g, A);
+        else return cudaErrorNotSupported;
       default: return cudaErrorInvalidValue;
     }
   }
@@ -273,7 +276,7 @@ template <int EQ, int DIM, int P> struct Disp {
     if constexpr (EQ == 2 && DIM == 2) {
       switch (k) {
         case OP_R1: case OP_R1ABS: return (Tg ? run_gtrace<P, ModeR1<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeR1<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
-        case OP_R12: return (Tg ? run_gtrace<P, ModeR12<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeR12<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
+        case OP_R12: case OP_KNS: return (Tg ? run_gtrace<P, ModeR12<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeR12<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
         case OP_RESID: return (Tg ? run_gtrace<P, ModeResid<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeResid<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
         case OP_JVP_EXACT: return (Tg ? run_gtrace<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, Tg) : run_lift<P, ModeJvpExact<EQ, NODES>, 0>(c, g, A, G, Gf, gTg));
         case OP_JVP_FD:
@@ -387,7 +390,7 @@ cudaError_t launch_gtrace(OpKind kind, int state, const OpCfg& c, const Geo& g, 
 int lift_jet_components(OpKind kind, int state) {
   switch (kind) {
     case OP_R1: case OP_R1ABS: return 1;
-    case OP_R12: case OP_RESID: return 2;
+    case OP_R12: case OP_RESID: case OP_KNS: return 2;
     case OP_JVP_EXACT: return 4;
     case OP_JVP_FD: return state == 0 ? 2 : 3;
     default: return 0;
