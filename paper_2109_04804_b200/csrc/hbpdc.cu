@@ -116,6 +116,7 @@ struct hbpdc_ctx {
   double *Sb = nullptr, *gSb = nullptr;   // BJ^H_ext: sigma at the build point, R1(Wb), and its ghosts
   double *lift0 = nullptr, *lift1 = nullptr;
   double* liftB = nullptr;        // NS BJ_ext build: lifted gradients of the build state (ModeKNS)
+  double *gGb = nullptr, *gzero = nullptr;   // their ghost copies; a zero ghost field (partitioned ModeKNS)
   double *liftf0 = nullptr, *liftf1 = nullptr;   // BR2 per-face gradients (NULL: BR1)
   // precond
   double *S = nullptr, *Wb = nullptr, *Z = nullptr;
@@ -303,8 +304,9 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
     if (xmask & 2) { src[nf] = A.S; dst[nf++] = c->gS; }
     if (xmask & 4) { src[nf] = A.dW; dst[nf++] = c->gdW; }
     if (xmask & 8) { src[nf] = A.dS; dst[nf++] = c->gdS; }
-    A.gW = k == OP_KAPPLY ? c->gWb : c->gW;
-    A.gS = c->gS; A.gdW = c->gdW; A.gdS = c->gdS;
+    A.gW = (k == OP_KAPPLY || k == OP_KNS) ? c->gWb : c->gW;
+    A.gS = k == OP_KNS ? c->gzero : c->gS;     // ModeKNS: no seed on the neighbours' ghosts
+    A.gdW = c->gdW; A.gdS = c->gdS;
     if (nf && c->overlap && c->geo.cmode == 0 && c->pb.equation != HBPDC_NAVIER_STOKES) {
       // halo / compute overlap: pack + transport + unpack on the comm stream while
       // the interior elements (no neighbour across a halo side) run on the main stream
@@ -360,7 +362,7 @@ hbpdc_status run_op(hbpdc_ctx* c, OpKind k, OpArgs A, int xmask = -1) {
       A.G1 = c->lift1;
       A.Gf1 = c->liftf1;
     }
-    if (c->halo()) {
+    if (c->halo() && k != OP_KNS) {     // ModeKNS reads the neighbours' gradients from Gb / gGb
       const double* s0[1] = {c->lift0};
       double* d0[1] = {c->gG0};
       CKS(halo_exchange(c, 1, s0, d0, 6 * lift_jet_components(k, 0)));
@@ -596,12 +598,28 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
     // one-hop lifting (ModeKNS, GLL / BR1 / one rank): the colour pass lifts the colour's elements
     // only; the neighbours' gradients are the build state's plus the seed's central-value term
     const char* onehop_env = std::getenv("HBPDC_NS_ONEHOP");
-    const bool onehop = single && !c->halo() && !c->geo.gl && !c->geo.br2 && !(onehop_env && atoi(onehop_env) == 0);
+    const bool onehop = single && !c->geo.gl && !c->geo.br2 && !(onehop_env && atoi(onehop_env) == 0);
     if (onehop) {
       if (!c->liftB) CKS(dalloc(c, &c->liftB, (size_t)c->nE * 6 * c->P * c->P));
       OpArgs B = base_args(c);
       B.W = c->Wb;
+      if (c->halo()) {
+        // the build state's ghosts (wb_halo) for the lifting's neighbour traces; its lifted
+        // gradients' ghosts for the neighbours' face gradients; a zero seed on every ghost
+        const size_t ng = (size_t)2 * (c->nxl + c->nyl) * c->m;
+        if (!c->gGb) {
+          CKS(dalloc(c, &c->gGb, (size_t)2 * (c->nxl + c->nyl) * 6 * c->P * c->P));
+          CKS(dalloc(c, &c->gzero, ng));
+          CK(cudaMemsetAsync(c->gzero, 0, ng * sizeof(double), c->stream));
+        }
+        B.gW = c->gWb;
+      }
       CK(launch_lift(OP_R1, 0, c->cfg, c->geo, B, c->liftB, nullptr, nullptr));
+      if (c->halo()) {
+        const double* s0[1] = {c->liftB};
+        double* d0[1] = {c->gGb};
+        CKS(halo_exchange(c, 1, s0, d0, 6));
+      }
     }
     const Geo full = c->geo;
     for (int cy = 0; cy < Py; ++cy)
@@ -615,6 +633,7 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
           OpArgs A = base_args(c);
           A.W = c->Wb; A.S = c->tseed; A.out1 = nullptr; A.out2 = c->y1;
           A.Gb = c->liftB;
+          A.gGb = c->gGb;
           st = run_op(c, onehop ? OP_KNS : OP_R12, A);
           if (st != HBPDC_OK) break;
           if (hess) {

@@ -35,6 +35,7 @@ struct OpArgs {
   const double *gGf0, *gGf1; // their ghost copies (the neighbour ranks' shared faces)
   const double* Tr;          // GL FD JVP: face traces [e][face 4][field W,S,dW,dS][var][P] (gl_trace_kernel), or NULL
   const double* Gb;          // NS BJ_ext colour build (ModeKNS): lifted gradients of the build state [e][6][NODES]
+  const double* gGb;         // their ghost copies (partitioned runs)
 };
 
 // NS BR2 face gradients: [elem][face 4][6][JetN][P] (lift_kernel), face f = 2d + plus,
@@ -693,7 +694,7 @@ template <int EQ, int NODES> struct ModeKLin : OneJetMode<EQ, NODES, ModeKLin<EQ
 };
 
 #undef FV
-// NS BJ_ext colour build, one column of K_i for the colour's elements (GLL, BR1, one rank):
+// NS BJ_ext colour build, one column of K_i for the colour's elements (GLL, BR1):
 // the tangent channel of R1(W_b + e1 t), t = the seed (zero outside the colour's elements),
 // with the lifting evaluated on the colour's elements ONLY.  The neighbour's lifted gradient
 // at the shared face is the build state's (A.Gb) plus its one seed-dependent term: the
@@ -726,10 +727,11 @@ template <int EQ, int NODES> struct ModeKNS : OneJetMode<EQ, NODES, ModeKNS<EQ, 
     }
     if constexpr (EQ == 2) {
       NodeState<EQ, J1> sn, so;
-      const double* pw = A.W + (size_t)nb * A.m + nnode;
+      const double* pw = FPTR(W, nb, nnode, true);
 #pragma unroll
       for (int v = 0; v < NV; ++v) sn.w[v] = J1{pw[v * NODES], 0.0};      // t = 0 off the colour
-      const double* gb = A.Gb + (size_t)nb * 6 * NODES + nnode;
+      const double* gb = nb < A.nE ? A.Gb + (size_t)nb * 6 * NODES + nnode
+                                   : A.gGb + (size_t)(nb - A.nE) * 6 * NODES + nnode;
 #pragma unroll
       for (int k = 0; k < 3; ++k) { sn.gx[k] = J1{gb[k * NODES], 0.0}; sn.gy[k] = J1{gb[(k + 3) * NODES], 0.0}; }
       load_w<0>(A, e, own, so.w, false);

@@ -728,8 +728,17 @@ op_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL, BR2
 // ---- BR1 lifting (eq:Lifting P:855, central value P:861; reading R19) -----------
 //   d^x_ij = sx ( sum_l Dh_il g_lj + g*_E,j lhat_N(1) [i=N] - g*_W,j lhat_0(-1) [i=0] )
 // Computed for jet state K of the mode; result [elem][6][JetN][NODES].
-template <int P, class Mode, int K, int EPB, bool GL>
-__global__ void __launch_bounds__(EPB * P * P)
+// CTAs per SM requested from ptxas for the lifting, by the jet width of the lifted state
+// (measured on the C5 operators, r02w: R1 lift 334 -> 286 us at 8 for plain doubles, FD JVP
+// 1650 -> 1605 us at 5 / 6 for the J1 / J2 states; the hyper-dual EXACT lift spills below 128)
+template <class Mode, int K> struct LiftMinb {
+  static constexpr int JN = JetN<typename Mode::template StateT<K>>::value;
+  static constexpr int value = JN == 1 ? 8 : (JN == 2 ? 6 : (JN == 3 ? 5 : 1));
+};
+// BR2F: the BR2 per-face gradient output (Gf) is compiled in; the BR1 instantiations drop it
+// (its unrolled face loops set the register count: J2 lift 144 -> 128 registers without it)
+template <int P, class Mode, int K, int EPB, bool GL, bool BR2F = true>
+__global__ void __launch_bounds__(EPB * P * P, (LiftMinb<Mode, K>::value))
 lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g, double* Gout, double* Gf,
             const double* gTg) {
   using T = typename Mode::template StateT<K>;
@@ -801,7 +810,7 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
           const T gs = side > 0 ? 0.5 * (go + gn) : 0.5 * (gn + go);
           if (d == 0) sx_[k] = sx_[k] + s * gs; else sy_[k] = sy_[k] + s * gs;
         }
-        if (Gf && t == (side > 0 ? P - 1 : 0)) {
+        if (BR2F && Gf && t == (side > 0 ? P - 1 : 0)) {
           // BR2 on GL (reading R33): the face point kf of this line; normal component
           // l'(+-1).g along d + eta s_d (+-c) (g* - g_f), tangential the trace of (2/h) D g
           const int kf = d == 0 ? j : i;
@@ -870,7 +879,7 @@ lift_kernel(const typename Mode::Args A, const PhysParams pp, const GeoSel<GL> g
   if constexpr (!GL) {
     // BR2 (reading R33): on each face of this edge node, the strong-form gradient
     // (2/h) D g (D = Dhat + M^-1 B) plus, in the normal component, eta (2/h) (+-) lhat (g* - g)
-    if (Gf && active) {
+    if (BR2F && Gf && active) {
 #pragma unroll 1
       for (int d = 0; d < 2; ++d) {
         const int kk = d == 0 ? i : j;

@@ -62,7 +62,10 @@ static cudaError_t run_lift(const OpCfg& c, const Geo& g, const OpArgs& A, doubl
   constexpr int EPB = epb_for(NODES);
   const int grid = (launch_elems(g) + EPB - 1) / EPB;
   if (grid == 0) return cudaSuccess;
-  lift_kernel<P, Mode, K, EPB, kGL><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G, Gf, gTg);
+  if (Gf)
+    lift_kernel<P, Mode, K, EPB, kGL, true><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G, Gf, gTg);
+  else
+    lift_kernel<P, Mode, K, EPB, kGL, false><<<grid, EPB * NODES, 0, c.stream>>>(A, c.pp, geo_sel(g), G, Gf, gTg);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
