@@ -37,10 +37,15 @@ constexpr int GJ_APS = GJ_TW + 4;  // pivot-row tile stride (conflict-free B fra
 // in-flight matrices overflow L2), so a wider panel means proportionally fewer passes.
 // GJ_T threads (= the largest m: thread r owns row r): 256 for the 2D configs, 384 for the
 // 3D hexahedra (m = 5 * 4^3 = 320, NEXT-4).
-template <int GJ_NB, int GJ_T>
+// MC: the block size as a compile-time constant (0: runtime m).  MC == GJ_T with MC a multiple
+// of GJ_NB (the 2D N = 7 blocks, m = 256) drops every bounds guard of the panel and the trailing
+// update (ncu r02o: 16 % ISETP, 10 % IMAD of the executed instructions; the DMMAs were 7 %).
+template <int GJ_NB, int GJ_T, int MC = 0>
 __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(double* __restrict__ Zall,
-                                                                          double* __restrict__ Sall, int m,
+                                                                          double* __restrict__ Sall, int m_in,
                                                                           int* __restrict__ info) {
+  constexpr bool FULL = MC == GJ_T && MC % GJ_NB == 0;
+  const int m = MC ? MC : m_in;
   constexpr int GJ_MMAX = GJ_T;
   constexpr int GJ_PS = GJ_NB + 4;   // panel row stride (== 4 mod 16: conflict-free DMMA A fragments)
   extern __shared__ __align__(16) double gj_dyn[];
@@ -63,19 +68,19 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
   const int r = tid;
   bool used = false;
   for (int c0 = 0; c0 < m; c0 += GJ_NB) {
-    const int nb = min(GJ_NB, m - c0);
+    const int nb = FULL ? GJ_NB : min(GJ_NB, m - c0);
     {
     double row[GJ_NB];
 #pragma unroll
-    for (int j = 0; j < GJ_NB; ++j) row[j] = (r < m && j < nb) ? A[(size_t)r * m + c0 + j] : 0.0;
+    for (int j = 0; j < GJ_NB; ++j) row[j] = (FULL || (r < m && j < nb)) ? A[(size_t)r * m + c0 + j] : 0.0;
     int mycol = -1;                                  // panel column this row pivoted
 #pragma unroll
     for (int k = 0; k < GJ_NB; ++k) {
-      if (k >= nb) break;
+      if (!FULL && k >= nb) break;
       // ---- pivot search: max |row[k]| over unused rows (ties: smallest r)
       // a NaN entry ranks as +inf so that some row is always chosen (a NaN pivot must not leave
       // the column without a pivot row); non-finite pivots are reported as singular below
-      const bool cand = r < m && !used;
+      const bool cand = (FULL || r < m) && !used;
       double best = cand ? (isnan(row[k]) ? INFINITY : fabs(row[k])) : -1.0;
       int bi = cand ? r : 0x7fffffff;
 #pragma unroll
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
       if (sing) singular = 1;
       const double pinv = s_pval;
       // ---- in-place GJ step on the panel columns
-      if (r < m) {
+      if (FULL || r < m) {
         if (r == bi) {
 #pragma unroll
           for (int j = 0; j < GJ_NB; ++j) row[j] = j == k ? pinv : prb[j];
@@ -117,10 +122,10 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
       }
     }
     // ---- store the panel (augmented columns E[:, P]); U = panel - I[:, P] to shared memory
-    if (r < m) {
+    if (FULL || r < m) {
 #pragma unroll
       for (int j = 0; j < GJ_NB; ++j)
-        if (j < nb) {
+        if (FULL || j < nb) {
           A[(size_t)r * m + c0 + j] = row[j];
           Pn[r * GJ_PS + j] = j == mycol ? row[j] - 1.0 : row[j];
         }
@@ -136,10 +141,10 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
       for (int idx = tid; idx < GJ_NB * GJ_TW; idx += GJ_T) {
         const int k = idx / GJ_TW, jj = idx % GJ_TW;
         const int col = t0 + jj;
-        AP[k * GJ_APS + jj] = (k < nb && col < m) ? A[(size_t)piv[c0 + k] * m + col] : 0.0;
+        AP[k * GJ_APS + jj] = (FULL || (k < nb && col < m)) ? A[(size_t)piv[c0 + k] * m + col] : 0.0;
       }
       __syncthreads();
-      if (32 * wid < m) {
+      if (FULL || 32 * wid < m) {
         double acc[4][4][2];
 #pragma unroll
         for (int rb = 0; rb < 4; ++rb) {
@@ -147,8 +152,8 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb) {
             const int col = t0 + 8 * cb + 2 * t4;
-            acc[rb][cb][0] = (r < m && col < m) ? A[(size_t)r * m + col] : 0.0;
-            acc[rb][cb][1] = (r < m && col + 1 < m) ? A[(size_t)r * m + col + 1] : 0.0;
+            acc[rb][cb][0] = (FULL || (r < m && col < m)) ? A[(size_t)r * m + col] : 0.0;
+            acc[rb][cb][1] = (FULL || (r < m && col + 1 < m)) ? A[(size_t)r * m + col + 1] : 0.0;
           }
         }
 #pragma unroll
@@ -158,7 +163,7 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
 #pragma unroll
           for (int rb = 0; rb < 4; ++rb) {
             const int r = 32 * wid + 8 * rb + g;
-            av[rb] = (r < m && kk < nb) ? Pn[r * GJ_PS + kk] : 0.0;
+            av[rb] = (FULL || (r < m && kk < nb)) ? Pn[r * GJ_PS + kk] : 0.0;
           }
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb) bv[cb] = AP[kk * GJ_APS + 8 * cb + g];
@@ -170,13 +175,13 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
 #pragma unroll
         for (int rb = 0; rb < 4; ++rb) {
           const int r = 32 * wid + 8 * rb + g;
-          if (r >= m) continue;
+          if (!FULL && r >= m) continue;
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int col = t0 + 8 * cb + 2 * t4 + h;
-              if (col < m && (col < c0 || col >= c0 + nb)) A[(size_t)r * m + col] = acc[rb][cb][h];
+              if ((FULL || col < m) && (col < c0 || col >= c0 + nb)) A[(size_t)r * m + col] = acc[rb][cb][h];
             }
         }
       }
@@ -213,9 +218,12 @@ cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, c
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<nmat, T, smem, st>>>(Z, S, m, info);
   };
-  if (m > 256) go(gj_kernel<32, 384>, 32, 384);
-  else if (m <= 160 && !getenv("HBPDC_GJ_T256")) go(gj_kernel<32, 160>, 32, 160);   // C5: m = 144
+  if (m == 320) go(gj_kernel<32, 384, 320>, 32, 384);                 // 3D N = 3 (T3)
+  else if (m > 256) go(gj_kernel<32, 384>, 32, 384);
+  else if (m == 144 && !getenv("HBPDC_GJ_T256")) go(gj_kernel<32, 160, 144>, 32, 160);   // C5: N = 5
+  else if (m <= 160 && !getenv("HBPDC_GJ_T256")) go(gj_kernel<32, 160>, 32, 160);
   else if (nb == 16) go(gj_kernel<16, 256>, 16, 256);
+  else if (m == 256) go(gj_kernel<32, 256, 256>, 32, 256);     // the 2D N = 7 blocks (C3, C4)
   else go(gj_kernel<32, 256>, 32, 256);
   hbpdc_count_launch();
   return cudaGetLastError();
