@@ -214,7 +214,8 @@ template <int EQ, int NODES> struct ModeR12 : OneJetMode<EQ, NODES, ModeR12<EQ, 
 // (eq:Newton_Residual; P:236-239 read as R4)
 template <int EQ, int NODES> struct ModeResid : OneJetMode<EQ, NODES, ModeResid<EQ, NODES>, J1, 2> {
   static constexpr int NV = NVars<EQ>::value, NCH = 2;
-  static constexpr bool NO_DMMA = true;     // FMA contraction measured faster here (r02e)
+  // (round 2: with the surface terms as the fifth DMMA k-step the tensor-core contraction is
+  // faster here too: 88 -> 78 us at C3, r02zc; it had opted out before, r02e)
   template <int K>
   __device__ static void load_w(const OpArgs& A, int e, int node, J1* w, bool nbr) {
     const double *pw = FPTR(W, e, node, nbr), *ps = FPTR(S, e, node, nbr);

@@ -388,8 +388,9 @@ template <class M> struct VolPasses<M, std::void_t<decltype(M::VOL_PASSES)>> {
 // ---- fp64 tensor-core contraction (mma.sync m8n8k4 f64: A row-major 8x4, B col-major 4x8;
 // lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) + {0,1}])
 // Per mode (measured in one session, r02e, C3): R1 57 -> 44 us, EXACT JVP 127 -> 124.9, FD JVP
-// 159 -> 157 with the tensor-core contraction; the residual alone gets slower (101.5 -> 109) and
-// opts out (NO_DMMA).  The operators stay bound by the flux arithmetic, not the contraction.
+// 159 -> 157 with the tensor-core contraction; the residual alone got slower (101.5 -> 109) and
+// opted out (NO_DMMA) until the surface terms became the fifth k-step (round 2: residual 88 -> 78 us
+// on the tensor cores).  The operators stay bound by the flux arithmetic, not the contraction.
 #ifndef HBPDC_DMMA_CONTRACT
 #define HBPDC_DMMA_CONTRACT 1
 #endif
