@@ -507,3 +507,23 @@ def test_schur_end_of_run(precond, sstep):
         its += ctx.step(dt, Wg)["gmres_its"]
     assert rel(to_np(Wg), Wo) <= 1e-8
     assert its <= 1.25 * sto["gmres_its"] + 2 * sstep + 8, (its, sto["gmres_its"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [c for c in PC_CASES if c[0] == "navier_stokes"])
+def test_ns_onehop_build_matches_colour_lifting(case, monkeypatch):
+    """The one-hop NS colour build (ModeKNS: lifting on the colour's elements only, the neighbours'
+    face gradients from the build state plus the seed's BR1 central-value term) against the
+    colour passes that lift the colour's elements and their neighbours (HBPDC_NS_ONEHOP=0):
+    the same K_i, so the same S_i up to rounding."""
+    kind = case[0]
+    d, ctx = _pair(*case)
+    W = to_gpu(_state(d, kind, SEED + 23))
+    a1, a2, dt = 1.0 / 6.0, 1.0 / 54.0, 0.05
+    monkeypatch.setenv("HBPDC_NS_ONEHOP", "0")
+    ctx.precond_build(a1, a2, dt, W)
+    S2 = to_np(ctx.precond_export()[0]).copy()
+    monkeypatch.setenv("HBPDC_NS_ONEHOP", "1")
+    ctx.precond_build(a1, a2, dt, W)
+    S1 = to_np(ctx.precond_export()[0])
+    assert rel(S1, S2) <= 1e-12, rel(S1, S2)
