@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include "../../include/hbpdc.h"
 #include "comm.h"
 #include "launch.h"
@@ -81,6 +82,7 @@ struct SysWS {
   double *X = nullptr, *G = nullptr, *dX = nullptr, *rhs = nullptr, *r = nullptr, *zb = nullptr;
   double *b = nullptr;                      // Newton right-hand side b (n)
   double *U = nullptr, *V = nullptr;        // BJ_ext GEMV outputs (n each)
+  double* ky = nullptr;                     // NS: U - a1dt V, the second K right-hand side (n)
   double *ks = nullptr, *ks2 = nullptr;     // Schur mode: K v and a discarded JVP half (n each)
   double* npart = nullptr;                  // K-apply per-CTA partials of ||out1||^2 ...
   const double* npart_of = nullptr;         // ... valid for this vector (the next FD JVP's dW)
@@ -162,6 +164,9 @@ struct hbpdc_ctx {
   int debug_sync = 0;              // HBPDC_DEBUG_SYNC=1: synchronise + check after every launch group
   int trace = 0;                   // HBPDC_TRACE=1: per stage / Newton / GMRES trace on stderr
   int fuse_cgs = 1;                // HBPDC_FUSE_CGS=0: unfused block CGS2 passes (A/B checks)
+  double sel_reorth = 1e-12;       // s = 8 block CGS: skip the second update when |C2 Rw^-1| <= this (0: never;
+                                   // HBPDC_SEL_REORTH, reading R37)
+  long long blk_count = 0, blk_skip = 0, blk_hist[6] = {0, 0, 0, 0, 0, 0};  // trace: max|C2 Rw^-1| by decade
 };
 
 namespace {
@@ -201,11 +206,21 @@ hbpdc_status dalloc(hbpdc_ctx* c, double** p, size_t n) {
 }
 
 // profiling helpers (CUDA events on the context stream)
+// NVTX ranges (header-only NVTX3: no-ops unless a tool such as ncu/nsys injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+static const char* const kProfName[8] = {"precond GEMV", "JVP", "residual", "Arnoldi dots",
+                                         "Arnoldi update", "precond K-apply", "precond build",
+                                         "Arnoldi update+dots"};
+
 struct ProfScope {
   hbpdc_ctx* c;
   int id;
   cudaEvent_t a = nullptr, b = nullptr;
-  ProfScope(hbpdc_ctx* c_, int id_, double alg_bytes = 0.0) : c(c_), id(id_) {
+  NvtxRange nv;
+  ProfScope(hbpdc_ctx* c_, int id_, double alg_bytes = 0.0) : c(c_), id(id_), nv(kProfName[id_ & 7]) {
     if (!c->prof_on) return;
     c->prof_bytes[id] += alg_bytes;
     cudaEventCreate(&a);
@@ -520,6 +535,7 @@ hbpdc_status ensure_precond_mem(hbpdc_ctx* c) {
   }
   if (c->pb.equation == HBPDC_NAVIER_STOKES) {   // explicit K_i (two-hop BR1 path) + colouring scratch
     CKS(dalloc(c, &c->Kst, nblk * mm));
+    for (auto& w : c->sys) CKS(dalloc(c, &w.ky, c->n));
     CKS(dalloc(c, &c->KV, c->n));
     CKS(dalloc(c, &c->KT, c->n));
     CKS(dalloc(c, &c->tseed, c->n));
@@ -800,16 +816,35 @@ hbpdc_status precond_apply_multi(hbpdc_ctx* c, int B, const double* const* iw, c
     }
     return HBPDC_OK;
   }
+  if (c->pb.equation == HBPDC_NAVIER_STOKES) {
+    // explicit K_i: (K V_i, K (U_i - a1dt V_i)) for all B systems in ONE 2B-RHS pass over the
+    // stored blocks (the lock-step corrector stages share it like the S pass; the DMMA GEMV sums
+    // its k-range partials in the same order for every batch width: bitwise the per-system
+    // result), K V -> ow, K (U - a1dt V) -> os, then top = U - c2 K V, bottom = V + K (U - a1dt V)
+    ProfScope ps(c, 5, (double)c->nE * c->m * c->m * 8.0 + 8.0 * B * c->n * 8.0);
+    const double* in[GEMV_MAX_RHS];
+    double* out[GEMV_MAX_RHS];
+    for (int i = 0; i < B; ++i) {
+      CK(launch_waxpby(1.0, c->sys[i].U, -a1dt, c->sys[i].V, c->sys[i].ky, c->n, c->stream));
+      in[2 * i] = c->sys[i].V; in[2 * i + 1] = c->sys[i].ky;
+      out[2 * i] = ow[i]; out[2 * i + 1] = os[i];
+    }
+    if (B == 1 || (c->m & 1)) {
+      for (int i = 0; i < B; ++i)
+        CK(launch_block_gemv2(c->Kst, 0, in[2 * i], in[2 * i + 1], out[2 * i], out[2 * i + 1], c->m, c->nE, c->stream));
+    } else {
+      CK(launch_block_gemv_multi(c->Kst, 2 * B, in, out, c->m, c->nE, c->stream));
+    }
+    for (int i = 0; i < B; ++i) {
+      CK(launch_waxpby(1.0, c->sys[i].U, -c2, ow[i], ow[i], c->n, c->stream));
+      CK(launch_waxpby(1.0, c->sys[i].V, 1.0, os[i], os[i], c->n, c->stream));
+      if (c->st) c->st->precond_applies++;
+    }
+    return HBPDC_OK;
+  }
   for (int i = 0; i < B; ++i) {
     const double *U = c->sys[i].U, *V = c->sys[i].V;
-    if (c->pb.equation == HBPDC_NAVIER_STOKES) {
-      // explicit K_i: (K V, K (U - a1dt V)) in one 2-RHS pass over the stored blocks
-      ProfScope ps(c, 5, (double)c->nE * c->m * c->m * 8.0 + 8.0 * c->n * 8.0);
-      CK(launch_waxpby(1.0, U, -a1dt, V, c->y1, c->n, c->stream));
-      CK(launch_block_gemv2(c->Kst, 0, V, c->y1, c->KV, c->KT, c->m, c->nE, c->stream));
-      CK(launch_waxpby(1.0, U, -c2, c->KV, ow[i], c->n, c->stream));
-      CK(launch_waxpby(1.0, V, 1.0, c->KT, os[i], c->n, c->stream));
-    } else {
+    {
       OpArgs A = base_args(c);
       A.W = c->Wb; A.U = U; A.V = V; A.out1 = ow[i]; A.out2 = os[i];
       A.a1dt = a1dt;
@@ -1266,6 +1301,41 @@ hbpdc_status g_block(hbpdc_ctx* c, GState& g) {
     CKS(block_dots_host(c, w, nq, W, sb, r2));
   }
   std::vector<double> C2(r2.begin(), r2.begin() + (size_t)nq * sb);
+  // Selective reorthogonalisation (reading R37; PETSc's CGS "refine if needed"): the first
+  // projection already left W1 orthogonal to Q when the second projection's coefficients,
+  // seen through the block's own orthonormalisation, X = C2 Rw0^-1 (Rw0^T Rw0 = W1^T W1),
+  // are at the level sel_reorth.  Q_new = W1 Rw0^-1 then departs from Q^T Q_new = 0 by |X|
+  // only, and the second update pass over Q is skipped (W = Q C1 + Q_new Rw0 exactly).
+  bool skip2 = false;
+  if (sb == 8 && c->fuse_cgs && (c->sel_reorth > 0.0 || c->trace)) {
+    std::vector<double> T0((size_t)sb * sb), R0, R0i;
+    for (int a = 0; a < sb * sb; ++a) T0[a] = r2[(size_t)nq * sb + a];
+    if (small_chol(T0, sb, R0)) {
+      upper_inv(R0, sb, R0i);
+      double mx = 0.0;
+      for (int j = 0; j < nq; ++j)
+        for (int b = 0; b < sb; ++b) {
+          double v = 0.0;
+          for (int a = 0; a <= b; ++a) v += C2[(size_t)j * sb + a] * R0i[(size_t)a * sb + b];
+          mx = std::max(mx, std::fabs(v));
+        }
+      ++c->blk_count;
+      const int dec = mx <= 1e-15 ? 0 : mx <= 1e-14 ? 1 : mx <= 1e-13 ? 2 : mx <= 1e-12 ? 3 : mx <= 1e-10 ? 4 : 5;
+      ++c->blk_hist[dec];
+      if (c->sel_reorth > 0.0 && mx <= c->sel_reorth) {
+        skip2 = true;
+        ++c->blk_skip;
+        Rw = R0;
+        Rwi = R0i;
+      }
+    }
+  }
+  if (skip2) {
+    std::fill(C2.begin(), C2.end(), 0.0);
+    std::vector<double> zero(sb, 0.0);
+    // W <- W Rw0^-1 with the Gram of the result (the CholQR2 reduction); q_0 with zero coefficients
+    CKS(block_update_gram_host(c, w, 1, W, zero, Rwi, r3));
+  }
   T.assign((size_t)sb * sb, 0.0);
   for (int a = 0; a < sb; ++a)
     for (int b = 0; b < sb; ++b) {
@@ -1273,8 +1343,15 @@ hbpdc_status g_block(hbpdc_ctx* c, GState& g) {
       for (int j = 0; j < nq; ++j) v -= C2[(size_t)j * sb + a] * C2[(size_t)j * sb + b];
       T[(size_t)a * sb + b] = v;
     }
-  bool ok = small_chol(T, sb, Rw);
-  if (ok) {
+  bool ok = skip2 || small_chol(T, sb, Rw);
+  if (ok && skip2) {
+    T.assign(r3.begin(), r3.begin() + (size_t)sb * sb);
+    ok = small_chol(T, sb, R3);
+    if (ok) {
+      upper_inv(R3, sb, R3i);
+      CKS(block_scale_dev(c, w, W, R3i));
+    }
+  } else if (ok) {
     upper_inv(Rw, sb, Rwi);
     // CholQR2 of the block itself: its Gram from the update pass (s = 8) or a separate pass
     const bool fused = sb == 8 && c->fuse_cgs;
@@ -1592,6 +1669,7 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
     CKS(ensure_pc_for(c, a1, a2, dt, c->Wn));
     const double* g = c->stw[cur][l - 1];
     if (c->trace) fprintf(stderr, "[hbpdc] predictor stage %d\n", l + 1);
+    NvtxRange nv("predictor stage");
     hbpdc_status stt = newton_batch(c, 1, a1, a2, dt, &g);
     if (stt != HBPDC_OK) {
       c->err = "predictor stage " + std::to_string(l + 1) + ": " + c->err;
@@ -1610,6 +1688,7 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
     CK(cudaMemcpyAsync(c->str1[nxt][0], c->str1[cur][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(c->str2[nxt][0], c->str2[cur][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     for (int l0 = 1; l0 < s; l0 += B) {
+      NvtxRange nv("corrector stages");
       const int nb = std::min(B, s - l0);
       const double* guess[GEMV_MAX_RHS / 2];
       for (int q = 0; q < nb; ++q) {
@@ -1946,6 +2025,7 @@ hbpdc_status hbpdc_init(const hbpdc_problem* pb, const hbpdc_solver_opts* op, co
   { const char* dbg = std::getenv("HBPDC_DEBUG_SYNC"); c->debug_sync = dbg && dbg[0] == '1'; }
   { const char* tr = std::getenv("HBPDC_TRACE"); c->trace = tr && tr[0] == '1'; }   // solver trace on stderr
   { const char* fc = std::getenv("HBPDC_FUSE_CGS"); c->fuse_cgs = !(fc && fc[0] == '0'); }
+  { const char* sr = std::getenv("HBPDC_SEL_REORTH"); if (sr) c->sel_reorth = std::atof(sr); }
   hbpdc_status s = alloc_solver(c);
   *out = c;
   return s;
@@ -2118,7 +2198,11 @@ hbpdc_status hbpdc_step(hbpdc_ctx* c, double dt, double* W, hbpdc_step_stats* st
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
   cudaEventRecord(t0, c->stream);
-  hbpdc_status s = step_impl(c, dt, W);
+  hbpdc_status s;
+  {
+    NvtxRange nv("hbpdc_step");
+    s = step_impl(c, dt, W);
+  }
   cudaEventRecord(t1, c->stream);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   float ms = 0.f;
@@ -2127,6 +2211,10 @@ hbpdc_status hbpdc_step(hbpdc_ctx* c, double dt, double* W, hbpdc_step_stats* st
   cudaEventDestroy(t1);
   local.wall_s = ms * 1e-3;
   c->st = nullptr;
+  if (c->trace && c->blk_count)
+    fprintf(stderr, "[hbpdc] s-step blocks %lld, second update skipped %lld; max|C2 Rw^-1| <=1e-15 %lld <=1e-14 %lld "
+            "<=1e-13 %lld <=1e-12 %lld <=1e-10 %lld larger %lld\n", c->blk_count, c->blk_skip, c->blk_hist[0],
+            c->blk_hist[1], c->blk_hist[2], c->blk_hist[3], c->blk_hist[4], c->blk_hist[5]);
   if (stats) *stats = local;
   prof_flush(c);
   if (s == HBPDC_OK && e != cudaSuccess) {

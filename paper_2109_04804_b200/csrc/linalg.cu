@@ -1198,8 +1198,19 @@ __global__ void waxpby_kernel(double a, const double* __restrict__ x, double b, 
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) y[i] = a * x[i] + b * z[i];
 }
 
+// y = a x + b y (z aliases y: same expression as waxpby_kernel, without the restrict on z / y)
+__global__ void waxpby_ip_kernel(double a, const double* __restrict__ x, double b, double* y, size_t L) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) y[i] = a * x[i] + b * y[i];
+}
+
 cudaError_t launch_waxpby(double a, const double* x, double b, const double* z, double* y, size_t L,
                           cudaStream_t st) {
+  if (z == y) {
+    waxpby_ip_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, x, b, y, L);
+    hbpdc_count_launch();
+    return cudaGetLastError();
+  }
   waxpby_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, x, b, z, y, L);
   hbpdc_count_launch();
   return cudaGetLastError();

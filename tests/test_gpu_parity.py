@@ -292,6 +292,28 @@ def test_batched_correctors_bitwise(q, kmax):
     assert out[0][1] == out[1][1]
 
 
+@pytest.mark.parametrize("q,kmax", [(6, 2), (8, 4)])
+def test_batched_correctors_bitwise_ns(q, kmax):
+    """Navier-Stokes (stored K_i): the lock-step corrector stages share ONE pass over S
+    and ONE over K for all systems (2B right-hand sides each); bit-identical to the
+    sequential order, identical iteration counts."""
+    import torch
+    cfg = configs.scaled(configs.CONFIGS["C5"], N=3, nx=6, ny=6, q=q, kmax=kmax)
+    out = []
+    for batch in (True, False):
+        d, ctx = make_pair("navier_stokes", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=q, kmax=kmax,
+                           mu=cfg.mu, gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, batch_stages=batch)
+        W0 = inputs.initial_state("C5", d.node_coords())
+        dt = configs.cfl_dt(cfg, W0)
+        Wg = to_gpu(W0)
+        st = [ctx.step(dt, Wg) for _ in range(2)]
+        torch.cuda.synchronize()
+        out.append((to_np(Wg), [(s["gmres_its"], s["newton_its"]) for s in st]))
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 @pytest.mark.parametrize("s", [2, 4, 8])
 @pytest.mark.parametrize("q,kmax", [(4, 0), (8, 4)])
 def test_sstep_gmres_end_of_run(s, q, kmax):
@@ -317,6 +339,36 @@ def test_sstep_gmres_end_of_run(s, q, kmax):
         its.append(n)
         assert rel(to_np(Wg), Wo) <= 1e-8
     assert its[0] <= 1.25 * its[1] + 2 * s, its
+
+
+@pytest.mark.parametrize("tau", ["0", "1e-6"])
+@pytest.mark.parametrize("kind", ["euler", "advection"])
+def test_sstep_selective_reorth_end_of_run(kind, tau, monkeypatch):
+    """s = 8 block CGS with the second update skipped when |C2 Rw^-1| <= tau
+    (reading R37, HBPDC_SEL_REORTH; the default 1e-12 runs in every other s = 8 test):
+    end of run vs the oracle <= 1e-8 with tau = 0 (every block reorthogonalised) and
+    tau = 1e-6 (a loose threshold: the skip branch fires on nearly every block)."""
+    import torch
+    monkeypatch.setenv("HBPDC_SEL_REORTH", tau)
+    if kind == "euler":
+        cfg = configs.scaled(configs.CONFIGS["C3"], N=3, nx=4, ny=4, steps=2, q=6, kmax=2)
+        d, ctx = make_pair("euler", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=cfg.q, kmax=cfg.kmax,
+                           gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, gmres_sstep=8)
+        W0 = inputs.initial_state("C3", d.node_coords(), noise=cfg.noise)
+        dt = configs.cfl_dt(cfg, inputs.initial_state("C3", d.node_coords()))
+        Wo, _ = _run_oracle(d, cfg.q, cfg.kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol)
+    else:
+        cfg = configs.scaled(configs.CONFIGS["C2"], nx=8, ny=8, steps=3, cfl=2.0)
+        d, ctx = make_pair("advection", cfg.N, cfg.nx, cfg.ny, a=cfg.a, q=cfg.q, kmax=cfg.kmax,
+                           gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, gmres_sstep=8)
+        W0 = inputs.initial_state("C2", d.node_coords())
+        dt = configs.cfl_dt(cfg, W0)
+        Wo, _ = _run_oracle(d, cfg.q, cfg.kmax, W0, dt, cfg.steps, rtol=cfg.newton_rtol, gmres_rtol=cfg.gmres_rtol)
+    Wg = to_gpu(W0)
+    for _ in range(cfg.steps):
+        ctx.step(dt, Wg)
+    torch.cuda.synchronize()
+    assert rel(to_np(Wg), Wo) <= 1e-8
 
 
 @pytest.mark.parametrize("s", [4, 8])
