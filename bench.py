@@ -486,7 +486,8 @@ def run_ours(args):
 
     if rank == 0:
         it = {k: sum(s[k] for s in stats) for k in ("stage_solves", "newton_its", "gmres_its",
-                                                      "precond_builds", "jvp_calls", "precond_applies")}
+                                                      "precond_builds", "jvp_calls", "precond_applies",
+                                                      "precond_k_reused")}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

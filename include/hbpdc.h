@@ -145,6 +145,7 @@ typedef struct {
 typedef struct {               /* summed over one hbpdc_step                          */
   int stage_solves, newton_its, gmres_its, precond_builds, max_krylov_j;
   int jvp_calls, precond_applies;
+  int precond_k_reused;        /* Navier-Stokes builds that reused this step's stored K_i   */
   double final_newton_rel, wall_s;
 } hbpdc_step_stats;
 

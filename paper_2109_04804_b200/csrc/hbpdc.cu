@@ -126,6 +126,7 @@ struct hbpdc_ctx {
   double *y3 = nullptr, *yz = nullptr, *yb = nullptr;   // NS BJ^H_ext build: H e_c output, zero dsigma, scratch
   int* info = nullptr;
   int s_shared = 0, pc_valid = 0, zchunk = 0;
+  int kst_step = 0;                // NS: Kst holds the K_i of this step's W^n (built by ensure_pc_for)
   double pc_a1 = 0, pc_a2 = 0, pc_dt = -1;
   // stage store: [sweep(2)][s] of w, R1, R2
   double *stw[2][4] = {}, *str1[2][4] = {}, *str2[2][4] = {};
@@ -569,7 +570,11 @@ hbpdc_status wb_halo(hbpdc_ctx* c) {
   return halo_exchange(c, 1, src, dst);
 }
 
-hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, const double* W) {
+// in_step: called by the step at W^n (ensure_pc_for).  Navier-Stokes: the stored K_i depend on the
+// build state only, not on (alpha1, alpha2), so a second build of the same step at the same W^n
+// (the correctors' alpha pair) reuses them and only redoes M_i = I - a1 dt K_i + c2 K_i^2 and
+// its inverse (bitwise the same blocks: the colour loop is deterministic); HBPDC_NS_KREUSE=0 rebuilds.
+hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, const double* W, bool in_step = false) {
   CKS(ensure_precond_mem(c));
   const bool ns = c->pb.equation == HBPDC_NAVIER_STOKES;
   ProfScope ps(c, 6, (double)(c->s_shared ? 1 : c->nE) * c->m * c->m * 8.0 * (ns ? 2.0 : 1.0) + c->n * 8.0);
@@ -606,11 +611,15 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
     // seeded traces): the other elements' outputs are not needed (the gather reads the
     // seeded elements only), so each (colour, column) costs 1 / (Px Py) of a full-mesh
     // operator instead of one.  tseed is zero outside the seeded elements throughout.
-    CK(cudaMemsetAsync(c->tseed, 0, c->n * sizeof(double), c->stream));
     // m <= 160: one operator pass per column (K e_c); K_i^2 by the element-block product on
     // the fp64 tensor cores afterwards (K_i^2 e_c = K_i (K_i e_c) exactly: the same block),
     // instead of a second colour pass through lifting and operator per column
     const bool single = kk_gemm_supported(c->m) && !std::getenv("HBPDC_NS_TWOPASS");
+    const char* kreuse_env = std::getenv("HBPDC_NS_KREUSE");
+    const bool kreuse = in_step && c->kst_step && single && !hess && !(kreuse_env && atoi(kreuse_env) == 0);
+    if (kreuse && c->st) c->st->precond_k_reused++;
+    if (!kreuse) {
+    CK(cudaMemsetAsync(c->tseed, 0, c->n * sizeof(double), c->stream));
     // one-hop lifting (ModeKNS, GLL / BR1 / one rank): the colour pass lifts the colour's elements
     // only; the neighbours' gradients are the build state's plus the seed's central-value term
     const char* onehop_env = std::getenv("HBPDC_NS_ONEHOP");
@@ -682,7 +691,9 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
         // clear this colour's elements of tseed for the next colour
         CK(launch_colour_seed(c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, -1, c->stream));
       }
+    }   // !kreuse
     if (single) CK(launch_kk_gemm(c->Kst, c->S, c->m, c->nE, a1dt, c2, hess ? 1 : 0, c->stream));
+    c->kst_step = (in_step && single && !hess) ? 1 : 0;
   }
   std::vector<int> hinfo(c->zchunk);
   for (int e0 = 0; e0 < nblk; e0 += c->zchunk) {
@@ -1626,7 +1637,7 @@ hbpdc_status ensure_pc_for(hbpdc_ctx* c, double a1, double a2, double dt, const 
   // for q = 4, 6, 8 in exact arithmetic, App. A) share one build (reading R12)
   auto same = [](double x, double y) { return std::fabs(x - y) <= 1e-12 * std::fabs(y); };
   if (c->pc_valid == 2 && same(a1, c->pc_a1) && same(a2, c->pc_a2) && c->pc_dt == dt) return HBPDC_OK;
-  CKS(precond_build_impl(c, a1, a2, dt, Wn));
+  CKS(precond_build_impl(c, a1, a2, dt, Wn, true));
   c->pc_valid = 2;   // built inside this step at W^n
   return HBPDC_OK;
 }
@@ -1658,6 +1669,7 @@ hbpdc_status step_impl(hbpdc_ctx* c, double dt, double* W) {
   }
   if (!c->fsal_valid) CKS(stage_ops(c, c->Wn, c->str1[cur][0], c->str2[cur][0]));
   c->pc_valid = c->pc_valid ? 1 : 0;   // a build from an earlier step is not at this W^n
+  c->kst_step = 0;                     // nor are its Navier-Stokes K_i
   CK(cudaMemcpyAsync(c->stw[cur][0], c->Wn, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   // ---- predictor (eq:nonlinear_predictor)
   for (int l = 1; l < s; ++l) {

@@ -394,6 +394,10 @@ constexpr int TF_R = TF_R_;        // ring stages
 #define TF_W_ 8
 #endif
 constexpr int TF_W = TF_W_;        // consumer warps
+#ifndef TF_DCH_
+#define TF_DCH_ 1
+#endif
+constexpr int TF_DCH = TF_DCH_;    // transient accumulator chains per tile in phase D
 constexpr int TF_NB = TF_E / (8 * TF_W);   // n-blocks per consumer warp
 }
 int block_fused_parts_tma() {
@@ -533,10 +537,29 @@ __global__ void __launch_bounds__(32 * (TF_W + 1), 1) block_update_dots_tma8_ker
         const int st = (int)(k % TF_R);
         mbar_wait(&full[st], (unsigned)((k / TF_R) & 1));
         const double* sa = ring + (size_t)st * 8 * TF_P + (size_t)g * TF_P + (size_t)(wid * TF_NB) * 8 + t;
+        if constexpr (TF_DCH == 1) {
 #pragma unroll
-        for (int nb = 0; nb < TF_NB; ++nb)
+          for (int nb = 0; nb < TF_NB; ++nb)
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk) dmma(dacc[tile], sa[nb * 8 + 4 * kk], bf[nb][kk]);
+            for (int kk = 0; kk < 2; ++kk) dmma(dacc[tile], sa[nb * 8 + 4 * kk], bf[nb][kk]);
+        } else {
+          // the tile's 2 TF_NB k-steps go to TF_DCH transient accumulator chains (a single
+          // chain serialises them on the DMMA latency); summed in chain order (deterministic)
+          double ch[TF_DCH][2];
+          ch[0][0] = dacc[tile][0];
+          ch[0][1] = dacc[tile][1];
+#pragma unroll
+          for (int c = 1; c < TF_DCH; ++c) { ch[c][0] = 0.0; ch[c][1] = 0.0; }
+#pragma unroll
+          for (int nb = 0; nb < TF_NB; ++nb)
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) dmma(ch[(2 * nb + kk) % TF_DCH], sa[nb * 8 + 4 * kk], bf[nb][kk]);
+          double s0 = ch[0][0], s1 = ch[0][1];
+#pragma unroll
+          for (int c = 1; c < TF_DCH; ++c) { s0 += ch[c][0]; s1 += ch[c][1]; }
+          dacc[tile][0] = s0;
+          dacc[tile][1] = s1;
+        }
         fence_proxy_async_smem();      // order this lane's reads before the stage's next bulk copy
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);

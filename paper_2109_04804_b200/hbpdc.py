@@ -66,7 +66,8 @@ class StepStats(ctypes.Structure):
     _fields_ = [("stage_solves", ctypes.c_int), ("newton_its", ctypes.c_int),
                 ("gmres_its", ctypes.c_int), ("precond_builds", ctypes.c_int),
                 ("max_krylov_j", ctypes.c_int), ("jvp_calls", ctypes.c_int),
-                ("precond_applies", ctypes.c_int), ("final_newton_rel", ctypes.c_double),
+                ("precond_applies", ctypes.c_int), ("precond_k_reused", ctypes.c_int),
+                ("final_newton_rel", ctypes.c_double),
                 ("wall_s", ctypes.c_double)]
 
     def as_dict(self):

@@ -314,6 +314,33 @@ def test_batched_correctors_bitwise_ns(q, kmax):
     assert out[0][1] == out[1][1]
 
 
+@pytest.mark.parametrize("nodes,lifting", [("gll", "br1"), ("gl", "br2")])
+def test_ns_k_reuse_bitwise(nodes, lifting, monkeypatch):
+    """Navier-Stokes: the second BJ_ext build of a step (the correctors' alpha pair, same W^n)
+    reuses the stored K_i of the first and only redoes M_i and its inverse; bit-identical
+    steps and iteration counts to rebuilding K_i (HBPDC_NS_KREUSE=0), and the reuse is
+    counted in the step stats (one per step for HBPC(6,2): two builds, one colour loop)."""
+    import torch
+    cfg = configs.scaled(configs.CONFIGS["C5"], N=3, nx=6, ny=6, q=6, kmax=2)
+    out = []
+    for reuse in ("1", "0"):
+        monkeypatch.setenv("HBPDC_NS_KREUSE", reuse)
+        d, ctx = make_pair("navier_stokes", cfg.N, cfg.nx, cfg.ny, bounds=cfg.bounds, q=cfg.q, kmax=cfg.kmax,
+                           mu=cfg.mu, gmres_rtol=cfg.gmres_rtol, newton_rtol=cfg.newton_rtol, nodes=nodes,
+                           lifting=lifting)
+        W0 = inputs.initial_state("C5", d.node_coords())
+        dt = configs.cfl_dt(cfg, W0)
+        Wg = to_gpu(W0)
+        st = [ctx.step(dt, Wg) for _ in range(2)]
+        torch.cuda.synchronize()
+        out.append((to_np(Wg), [(s["gmres_its"], s["newton_its"], s["precond_builds"]) for s in st],
+                    [s["precond_k_reused"] for s in st]))
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+    assert out[0][2] == [1, 1] and out[1][2] == [0, 0], (out[0][2], out[1][2])
+
+
 @pytest.mark.parametrize("s", [2, 4, 8])
 @pytest.mark.parametrize("q,kmax", [(4, 0), (8, 4)])
 def test_sstep_gmres_end_of_run(s, q, kmax):
