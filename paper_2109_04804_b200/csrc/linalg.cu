@@ -26,6 +26,15 @@ __device__ __forceinline__ void gj_dmma(double (&d)[2], double a, double b) {
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
+#ifndef GJ_PIPE
+#define GJ_PIPE 1
+#endif
+#ifndef GJ_ROT
+#define GJ_ROT 0
+#endif
+#ifndef GJ_ROTG
+#define GJ_ROTG 8
+#endif
 constexpr int GJ_TW = 32;    // column tile of the rank-NB update
 constexpr int GJ_APS = GJ_TW + 4;  // pivot-row tile stride (conflict-free B fragments)
 #ifndef GJ_MINB
@@ -74,14 +83,14 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
 #pragma unroll
     for (int j = 0; j < GJ_NB; ++j) row[j] = (FULL || (r < m && j < nb)) ? A[(size_t)r * m + c0 + j] : 0.0;
     int mycol = -1;                                  // panel column this row pivoted
-#pragma unroll
-    for (int k = 0; k < GJ_NB; ++k) {
-      if (!FULL && k >= nb) break;
-      // ---- pivot search: max |row[k]| over unused rows (ties: smallest r)
+    // one pivot step: ks = the register slot holding the pivot column (compile-time after
+    // unrolling), kc = the panel column it stands for
+    auto pivot_step = [&](const int ks, const int kc) {
+      // ---- pivot search: max |row[ks]| over unused rows (ties: smallest r)
       // a NaN entry ranks as +inf so that some row is always chosen (a NaN pivot must not leave
       // the column without a pivot row); non-finite pivots are reported as singular below
       const bool cand = (FULL || r < m) && !used;
-      double best = cand ? (isnan(row[k]) ? INFINITY : fabs(row[k])) : -1.0;
+      double best = cand ? (isnan(row[ks]) ? INFINITY : fabs(row[ks])) : -1.0;
       int bi = cand ? r : 0x7fffffff;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -97,14 +106,14 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
         if (redv[w] > best || (redv[w] == best && redi[w] < bi)) { best = redv[w]; bi = redi[w]; }
       const bool sing = !(best > 0.0) || !(best < INFINITY);
       if (r == bi) {                                 // the pivot row: broadcast it scaled by 1/pivot
-        const double pinv = 1.0 / (sing ? 1.0 : row[k]);
+        const double pinv = 1.0 / (sing ? 1.0 : row[ks]);
 #pragma unroll
         for (int j = 0; j < GJ_NB; ++j) prb[j] = row[j] * pinv;
         s_pval = pinv;
         used = true;
-        mycol = k;
-        colof[r] = c0 + k;
-        piv[c0 + k] = r;
+        mycol = kc;
+        colof[r] = c0 + kc;
+        piv[c0 + kc] = r;
       }
       __syncthreads();
       if (sing) singular = 1;
@@ -113,12 +122,39 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
       if (FULL || r < m) {
         if (r == bi) {
 #pragma unroll
-          for (int j = 0; j < GJ_NB; ++j) row[j] = j == k ? pinv : prb[j];
+          for (int j = 0; j < GJ_NB; ++j) row[j] = j == ks ? pinv : prb[j];
         } else {
-          const double fr = row[k];
+          const double fr = row[ks];
 #pragma unroll
-          for (int j = 0; j < GJ_NB; ++j) row[j] = j == k ? -fr * pinv : fma(-fr, prb[j], row[j]);
+          for (int j = 0; j < GJ_NB; ++j) row[j] = j == ks ? -fr * pinv : fma(-fr, prb[j], row[j]);
         }
+      }
+        };
+    constexpr bool PFULL = MC != 0 && MC % GJ_NB == 0;     // every panel has GJ_NB columns
+    if constexpr ((GJ_ROT == 2 ? PFULL : (GJ_ROT == 1 && FULL)) && GJ_NB % GJ_ROTG == 0) {
+      // The fully unrolled panel (GJ_NB pivot steps) is ~9k instructions, more than the
+      // instruction cache keeps for 16 warps at different places in it (ncu r02y: 14 % of the
+      // stall samples "no instruction").  Unroll GJ_ROTG steps only and rotate the row registers
+      // (and with them the order of the broadcast pivot row) by GJ_ROTG slots after each group:
+      // the pivot column is always in slots 0 .. GJ_ROTG-1, and after GJ_NB / GJ_ROTG rotations
+      // the columns are back in place.
+#pragma unroll 1
+      for (int kg = 0; kg < GJ_NB; kg += GJ_ROTG) {
+#pragma unroll
+        for (int kk = 0; kk < GJ_ROTG; ++kk) pivot_step(kk, kg + kk);
+        double tmp[GJ_ROTG];
+#pragma unroll
+        for (int j = 0; j < GJ_ROTG; ++j) tmp[j] = row[j];
+#pragma unroll
+        for (int j = 0; j + GJ_ROTG < GJ_NB; ++j) row[j] = row[j + GJ_ROTG];
+#pragma unroll
+        for (int j = 0; j < GJ_ROTG; ++j) row[GJ_NB - GJ_ROTG + j] = tmp[j];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < GJ_NB; ++k) {
+        if (!FULL && k >= nb) break;
+        pivot_step(k, k);
       }
     }
     // ---- store the panel (augmented columns E[:, P]); U = panel - I[:, P] to shared memory
@@ -137,6 +173,99 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
     //      4 x 4 DMMA tiles (8 x 8), k = the panel's 16 columns in 4 k-steps;
     //      A fragments (U) from the panel, B fragments (pivot rows) from AP
     const int g = lane >> 2, t4 = lane & 3;
+#if GJ_PIPE
+    // Software pipeline over the column tiles (r02zg): the tile's accumulators are loaded
+    // BEFORE the barrier that publishes its pivot rows, and the next tile's pivot rows are
+    // gathered into registers while this tile's DMMAs run (AP double-buffered), so a tile
+    // exposes one global round trip instead of two dependent ones and one barrier instead
+    // of two.  The tile made of the panel's own columns is skipped (its result was discarded).
+    constexpr int NAPL = (GJ_NB * GJ_TW + GJ_T - 1) / GJ_T;
+    constexpr bool SKIP_OWN = GJ_NB == GJ_TW;
+    auto ap_load = [&](int t0, double (&v)[NAPL]) {
+#pragma unroll
+      for (int q = 0; q < NAPL; ++q) {
+        const int idx = tid + q * GJ_T;
+        const int k = idx / GJ_TW, jj = idx % GJ_TW;
+        const int col = t0 + jj;
+        const bool in = (GJ_NB * GJ_TW) % GJ_T == 0 || idx < GJ_NB * GJ_TW;
+        v[q] = (in && (FULL || (k < nb && col < m))) ? A[(size_t)piv[c0 + k] * m + col] : 0.0;
+      }
+    };
+    auto next_tile = [&](int t0) {
+      t0 += GJ_TW;
+      if (SKIP_OWN && t0 == c0) t0 += GJ_TW;
+      return t0;
+    };
+    int t0 = (SKIP_OWN && c0 == 0) ? GJ_TW : 0;
+    double apv[NAPL];
+    if (t0 < m) ap_load(t0, apv);
+    for (int it = 0; t0 < m; t0 = next_tile(t0), ++it) {
+      double* APb = AP + (it & 1) * (GJ_NB * GJ_APS);
+      const bool mine = FULL || 32 * wid < m;
+      double acc[4][4][2];
+      if (mine) {
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+          const int r = 32 * wid + 8 * rb + g;
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            const int col = t0 + 8 * cb + 2 * t4;
+            if (FULL) {
+              const double2 v = *reinterpret_cast<const double2*>(A + (size_t)r * m + col);
+              acc[rb][cb][0] = v.x;
+              acc[rb][cb][1] = v.y;
+            } else {
+              acc[rb][cb][0] = (r < m && col < m) ? A[(size_t)r * m + col] : 0.0;
+              acc[rb][cb][1] = (r < m && col + 1 < m) ? A[(size_t)r * m + col + 1] : 0.0;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NAPL; ++q) {
+        const int idx = tid + q * GJ_T;
+        if ((GJ_NB * GJ_TW) % GJ_T == 0 || idx < GJ_NB * GJ_TW) APb[(idx / GJ_TW) * GJ_APS + idx % GJ_TW] = apv[q];
+      }
+      __syncthreads();
+      const int tn = next_tile(t0);
+      if (tn < m) ap_load(tn, apv);
+      if (mine) {
+#pragma unroll
+        for (int ks = 0; ks < GJ_NB / 4; ++ks) {
+          const int kk = 4 * ks + t4;
+          double av[4], bv[4];
+#pragma unroll
+          for (int rb = 0; rb < 4; ++rb) {
+            const int r = 32 * wid + 8 * rb + g;
+            av[rb] = (FULL || (r < m && kk < nb)) ? Pn[r * GJ_PS + kk] : 0.0;
+          }
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) bv[cb] = APb[kk * GJ_APS + 8 * cb + g];
+#pragma unroll
+          for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) gj_dmma(acc[rb][cb], av[rb], bv[cb]);
+        }
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+          const int r = 32 * wid + 8 * rb + g;
+          if (!FULL && r >= m) continue;
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            const int col = t0 + 8 * cb + 2 * t4;
+            if (FULL && SKIP_OWN) {
+              *reinterpret_cast<double2*>(A + (size_t)r * m + col) = make_double2(acc[rb][cb][0], acc[rb][cb][1]);
+            } else {
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                if ((FULL || col + h < m) && (col + h < c0 || col + h >= c0 + nb)) A[(size_t)r * m + col + h] = acc[rb][cb][h];
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();     // every tile is stored before the next panel (or the unpermute) reads A
+#else
     for (int t0 = 0; t0 < m; t0 += GJ_TW) {
       for (int idx = tid; idx < GJ_NB * GJ_TW; idx += GJ_T) {
         const int k = idx / GJ_TW, jj = idx % GJ_TW;
@@ -187,6 +316,7 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
       }
       __syncthreads();
     }
+#endif
   }
   // ---- unpermute: S[a][b] = Z[piv[a]][colof[b]]
   for (int a = wid; a < m; a += GJ_T / 32) {
@@ -213,7 +343,7 @@ cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, c
     return e ? atoi(e) : 2;
   }();
   auto go = [&](auto kern, int NB, int T) {
-    size_t smem = (size_t)(T * (NB + 4) + NB * GJ_APS) * sizeof(double);
+    size_t smem = (size_t)(T * (NB + 4) + (GJ_PIPE ? 2 : 1) * NB * GJ_APS) * sizeof(double);
     if (occ == 1 && m > 128) smem = std::max<size_t>(smem, 120 * 1024);   // one CTA per SM
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<nmat, T, smem, st>>>(Z, S, m, info);
