@@ -692,7 +692,7 @@ hbpdc_status precond_build_impl(hbpdc_ctx* c, double a1, double a2, double dt, c
         CK(launch_colour_seed(c->tseed, c->nE, c->nxl, c->m, Px, Py, cx, cy, -1, c->stream));
       }
     }   // !kreuse
-    if (single) CK(launch_kk_gemm(c->Kst, c->S, c->m, c->nE, a1dt, c2, hess ? 1 : 0, c->stream));
+    if (single) CK(launch_kk_gemm(c->Kst, c->S, c->m, c->nE, a1dt, c2, hess ? 1 : 0, kreuse ? 0 : 1, c->stream));
     c->kst_step = (in_step && single && !hess) ? 1 : 0;
   }
   std::vector<int> hinfo(c->zchunk);

@@ -62,7 +62,7 @@ cudaError_t launch_colour_restrict(const double* y, double* t, int nE, int nx, i
 cudaError_t launch_colour_gather_k(const double* y1, const double* y3, double* K, double* M, int nE, int nx, int m,
                                    int Px, int Py, int cx, int cy, int col, double c2, cudaStream_t st);
 bool kk_gemm_supported(int m);
-cudaError_t launch_kk_gemm(double* K, double* M, int m, int nE, double a1dt, double c2, int hess, cudaStream_t st);
+cudaError_t launch_kk_gemm(double* K, double* M, int m, int nE, double a1dt, double c2, int hess, int kt, cudaStream_t st);
 cudaError_t launch_colour_gather(const double* y1, const double* y2, const double* y3, double* K, double* M, int nE,
                                  int nx, int m, int Px, int Py, int cx, int cy, int col, double a1dt, double c2,
                                  cudaStream_t st);

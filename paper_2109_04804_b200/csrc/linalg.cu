@@ -30,7 +30,10 @@ __device__ __forceinline__ void gj_dmma(double (&d)[2], double a, double b) {
 #define GJ_PIPE 1
 #endif
 #ifndef GJ_ROT
-#define GJ_ROT 0
+#define GJ_ROT 1
+#endif
+#ifndef GJ_REDUX
+#define GJ_REDUX 1
 #endif
 #ifndef GJ_ROTG
 #define GJ_ROTG 8
@@ -63,6 +66,7 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
   __shared__ int piv[GJ_MMAX];      // pivot row of column c
   __shared__ int colof[GJ_MMAX];    // column whose pivot row is r (-1: unused)
   __shared__ double redv[GJ_T / 32];
+  __shared__ unsigned long long redk[GJ_T / 32];
   __shared__ int redi[GJ_T / 32];
   __shared__ double prb[GJ_NB];      // pivot row / pivot of the current column
   __shared__ double s_pval;
@@ -89,6 +93,32 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
       // ---- pivot search: max |row[ks]| over unused rows (ties: smallest r)
       // a NaN entry ranks as +inf so that some row is always chosen (a NaN pivot must not leave
       // the column without a pivot row); non-finite pivots are reported as singular below
+#if GJ_REDUX
+      // 64-bit key = bits(|x|) + 1 for a candidate row (monotone in |x| >= 0, NaN ranked as +inf),
+      // 0 otherwise; the maximum by three 32-bit warp reductions (high word, low word among the
+      // lanes that hold the high maximum, smallest row among the lanes that hold both) instead of
+      // five shuffle rounds of (value, index) pairs -- the same pivot row as before, bit for bit.
+      const bool cand = (FULL || r < m) && !used;
+      const double ax = isnan(row[ks]) ? INFINITY : fabs(row[ks]);
+      const unsigned long long key = cand ? (unsigned long long)__double_as_longlong(ax) + 1ull : 0ull;
+      auto kmax3 = [](unsigned long long kk, unsigned ri, unsigned long long& ko, unsigned& ro) {
+        const unsigned hi = (unsigned)(kk >> 32), lo = (unsigned)kk;
+        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+        ro = __reduce_min_sync(0xffffffffu, (kk != 0ull && hi == mh && lo == ml) ? ri : 0x7fffffffu);
+        ko = ((unsigned long long)mh << 32) | ml;
+      };
+      unsigned long long wk;
+      unsigned wr;
+      kmax3(key, (unsigned)r, wk, wr);
+      if (lane == 0) { redk[wid] = wk; redi[wid] = (int)wr; }
+      __syncthreads();
+      unsigned long long bk;
+      unsigned bu;
+      kmax3(lane < GJ_T / 32 ? redk[lane] : 0ull, lane < GJ_T / 32 ? (unsigned)redi[lane] : 0x7fffffffu, bk, bu);
+      const int bi = (int)bu;
+      const double best = bk ? __longlong_as_double((long long)(bk - 1ull)) : -1.0;
+#else
       const bool cand = (FULL || r < m) && !used;
       double best = cand ? (isnan(row[ks]) ? INFINITY : fabs(row[ks])) : -1.0;
       int bi = cand ? r : 0x7fffffff;
@@ -104,6 +134,7 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
 #pragma unroll
       for (int w = 1; w < GJ_T / 32; ++w)
         if (redv[w] > best || (redv[w] == best && redi[w] < bi)) { best = redv[w]; bi = redi[w]; }
+#endif
       const bool sing = !(best > 0.0) || !(best < INFINITY);
       if (r == bi) {                                 // the pivot row: broadcast it scaled by 1/pivot
         const double pinv = 1.0 / (sing ? 1.0 : row[ks]);

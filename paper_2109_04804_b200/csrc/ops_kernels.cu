@@ -490,19 +490,26 @@ __device__ __forceinline__ void kk_dmma(double (&d)[2], double a, double b) {
 // w, w + 8, ..., k in steps of 4 (mma.sync m8n8k4).
 constexpr int KK_T = 256;
 __global__ void __launch_bounds__(KK_T, 1) kk_gemm_kernel(double* __restrict__ K, double* __restrict__ M,
-                                                          int m, double a1dt, double c2, int hess) {
+                                                          int m, double a1dt, double c2, int hess, int kt) {
   extern __shared__ __align__(16) double sk[];
   const int mp = (m + 7) & ~7, ld = mp + 4;
   double* Ke = K + (size_t)blockIdx.x * m * m;
   double* Me = M + (size_t)blockIdx.x * m * m;
   for (int t = threadIdx.x; t < mp * ld; t += KK_T) sk[t] = 0.0;
   __syncthreads();
-  for (int t = threadIdx.x; t < m * m; t += KK_T) {      // coalesced read of K^T, transposed store
-    const int c = t / m, r = t % m;
-    sk[r * ld + c] = Ke[t];
+  if (kt) {
+    for (int t = threadIdx.x; t < m * m; t += KK_T) {      // coalesced read of K^T, transposed store
+      const int c = t / m, r = t % m;
+      sk[r * ld + c] = Ke[t];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < m * m; t += KK_T) Ke[t] = sk[(t / m) * ld + t % m];   // K_i row-major
+  } else {
+    // kt = 0: K already holds K_i row-major (an earlier build of this step transposed it; the
+    // second build of the step reuses it for another alpha pair) and stays as it is
+    for (int t = threadIdx.x; t < m * m; t += KK_T) sk[(t / m) * ld + t % m] = Ke[t];
+    __syncthreads();
   }
-  __syncthreads();
-  for (int t = threadIdx.x; t < m * m; t += KK_T) Ke[t] = sk[(t / m) * ld + t % m];   // K_i row-major
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int nt = mp / 8;
@@ -535,13 +542,13 @@ cudaError_t launch_colour_gather_k(const double* y1, const double* y3, double* K
 
 bool kk_gemm_supported(int m) { return m <= 160; }   // K_i in shared memory (<= 227 KB)
 
-cudaError_t launch_kk_gemm(double* K, double* M, int m, int nE, double a1dt, double c2, int hess, cudaStream_t st) {
+cudaError_t launch_kk_gemm(double* K, double* M, int m, int nE, double a1dt, double c2, int hess, int kt, cudaStream_t st) {
   if (!kk_gemm_supported(m)) return cudaErrorInvalidValue;
   if (nE <= 0) return cudaSuccess;
   const int mp = (m + 7) & ~7;
   const size_t smem = (size_t)mp * (mp + 4) * sizeof(double);
   cudaFuncSetAttribute(kk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kk_gemm_kernel<<<nE, KK_T, smem, st>>>(K, M, m, a1dt, c2, hess);
+  kk_gemm_kernel<<<nE, KK_T, smem, st>>>(K, M, m, a1dt, c2, hess, kt);
   hbpdc_count_launch();
   return cudaGetLastError();
 }
