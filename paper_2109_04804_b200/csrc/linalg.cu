@@ -379,7 +379,11 @@ cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, c
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<nmat, T, smem, st>>>(Z, S, m, info);
   };
-  if (m == 320) go(gj_kernel<32, 384, 320>, 32, 384);                 // 3D N = 3 (T3)
+#ifndef GJ_T320
+#define GJ_T320 0
+#endif
+  if (m == 320 && GJ_T320) go(gj_kernel<32, 320, 320>, 32, 320);     // 3D N = 3 (T3): 10 warps, guard-free
+  else if (m == 320) go(gj_kernel<32, 384, 320>, 32, 384);            // 3D N = 3 (T3)
   else if (m > 256) go(gj_kernel<32, 384>, 32, 384);
   else if (m == 144 && !getenv("HBPDC_GJ_T256")) go(gj_kernel<32, 160, 144>, 32, 160);   // C5: N = 5
   else if (m <= 160 && !getenv("HBPDC_GJ_T256")) go(gj_kernel<32, 160>, 32, 160);

@@ -33,4 +33,11 @@ for KS in "gemv_dmma_kernel<\(int\)6>:20" "gemv_dmma_kernel<\(int\)2>:20" "block
   ncu -i /tmp/ncu_$TAG/prof_$F.ncu-rep --page raw --csv > $OUT/ncu_raw_$F.csv 2>/dev/null
 done
 timeout 2400 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $OUT/summary.txt; tail -3 $OUT/pytest_gpu.log
+# T3 Gauss-Jordan with 320 threads (guard-free, rotated panel; build_var/libhbpdc_t320.so) vs the default 384
+for V in default t320 default t320; do
+  if [ $V = default ]; then L=paper_2109_04804_b200/libhbpdc.so; else L=build_var/libhbpdc_$V.so; fi
+  HBPDC_LIB=$PWD/$L timeout 900 python bench.py --config T3 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/bench_t3_$V.json 2> $OUT/bench_t3_$V.err; echo "bench t3 $V rc=$?"
+  python -c "import json;d=json.load(open('$OUT/bench_t3_$V.json'));print('T3 $V', d['value'], d['ms_per_step'], d['kernels']['build'])" | tee -a $OUT/summary.txt
+done
+HBPDC_LIB=$PWD/build_var/libhbpdc_t320.so timeout 900 python -m pytest tests/test_gpu_3d.py -m gpu -q > $OUT/pytest_3d_t320.log 2>&1; echo "pytest 3d t320 rc=$?" | tee -a $OUT/summary.txt; tail -2 $OUT/pytest_3d_t320.log
 du -sh $OUT
