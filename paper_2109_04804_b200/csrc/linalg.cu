@@ -380,7 +380,7 @@ cudaError_t launch_gj_invert(double* Z, double* S, int m, int nmat, int* info, c
     kern<<<nmat, T, smem, st>>>(Z, S, m, info);
   };
 #ifndef GJ_T320
-#define GJ_T320 0
+#define GJ_T320 1
 #endif
   if (m == 320 && GJ_T320) go(gj_kernel<32, 320, 320>, 32, 320);     // 3D N = 3 (T3): 10 warps, guard-free
   else if (m == 320) go(gj_kernel<32, 384, 320>, 32, 384);            // 3D N = 3 (T3)
