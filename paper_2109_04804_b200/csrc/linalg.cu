@@ -65,8 +65,11 @@ __global__ void __launch_bounds__(GJ_T, GJ_T > 256 ? 1 : GJ_MINB) gj_kernel(doub
   double* AP = gj_dyn + GJ_MMAX * GJ_PS;     // pivot rows of a column tile [GJ_NB][GJ_APS]
   __shared__ int piv[GJ_MMAX];      // pivot row of column c
   __shared__ int colof[GJ_MMAX];    // column whose pivot row is r (-1: unused)
-  __shared__ double redv[GJ_T / 32];
+#if GJ_REDUX
   __shared__ unsigned long long redk[GJ_T / 32];
+#else
+  __shared__ double redv[GJ_T / 32];
+#endif
   __shared__ int redi[GJ_T / 32];
   __shared__ double prb[GJ_NB];      // pivot row / pivot of the current column
   __shared__ double s_pval;
